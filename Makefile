@@ -1,0 +1,40 @@
+# Builds the three native artefacts in-tree (they travel to the GPU box with the gpurun snapshot):
+#   oracle/liboracle.so                           CPU oracle (test infrastructure only)
+#   paper_2203_10983_b200/inputs/libbnsgen.so      seeded input generators (setup)
+#   paper_2203_10983_b200/libbns.so                the product: C-ABI + sm_100a CUDA kernels + NCCL
+PY        ?= python
+NVCC      ?= /usr/local/cuda/bin/nvcc
+SITE      := $(shell $(PY) -c "import sysconfig; print(sysconfig.get_paths()['purelib'])")
+NCCL_DIR  := $(SITE)/nvidia/nccl
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 -Xptxas -v --expt-relaxed-constexpr
+PKG       := paper_2203_10983_b200
+CSRC      := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cpp)
+CHDR      := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/bns.h
+OBJDIR    := build
+
+all: oracle/liboracle.so $(PKG)/inputs/libbnsgen.so $(PKG)/libbns.so
+
+oracle/liboracle.so: oracle/bns_oracle.cpp
+	g++ -O2 -std=c++17 -fPIC -shared -o $@ $<
+
+$(PKG)/inputs/libbnsgen.so: $(PKG)/inputs/gen.cpp
+	g++ -O3 -std=c++17 -fPIC -shared -fopenmp -o $@ $<
+
+OBJS := $(patsubst $(PKG)/csrc/%,$(OBJDIR)/%.o,$(CSRC))
+
+$(OBJDIR)/%.cu.o: $(PKG)/csrc/%.cu $(CHDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -Iinclude -I$(NCCL_DIR)/include -dc -o $@ $< 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; false)
+
+$(OBJDIR)/%.cpp.o: $(PKG)/csrc/%.cpp $(CHDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) -O2 -std=c++17 -Xcompiler -fPIC -Iinclude -I$(NCCL_DIR)/include -c -o $@ $<
+
+$(PKG)/libbns.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib -lcuda
+
+clean:
+	rm -rf $(OBJDIR) oracle/liboracle.so $(PKG)/inputs/libbnsgen.so $(PKG)/libbns.so
+
+.PHONY: all clean

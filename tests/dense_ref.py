@@ -1,0 +1,62 @@
+"""Dense-adjacency brute force in float64 with torch autograd -- the independent pin for the oracle.
+
+It never partitions and never exchanges: it writes the sampled propagation of every inner node v as one dense
+row of an N x N matrix M (coefficients c_u/deg_G(v) for SAGE, PAPER.md:100 + :335 under readings R1-R3; or
+c_u/sqrt(d~_v d~_u) plus the self loop 1/d~_v for GCN, App. A) and lets autograd produce the
+backward.  A mistake in the oracle's partitioning, exchange, reverse exchange, accumulation order or hand-written
+backward therefore shows up as a mismatch here.
+"""
+import numpy as np
+import torch
+
+
+def dense_matrix(indptr, indices, part_of, kept, p, layer):
+    """kept[i] = set of boundary gids sampled by partition i."""
+    N = len(indptr) - 1
+    M = np.zeros((N, N))
+    deg = np.diff(indptr)
+    for v in range(N):
+        i = part_of[v]
+        for u in indices[indptr[v]:indptr[v + 1]]:
+            if part_of[u] == i:
+                c = 1.0
+            elif u in kept[i]:
+                c = 1.0 / p
+            else:
+                continue
+            if layer == 0:
+                M[v, u] += c / deg[v]
+            else:
+                M[v, u] += c / np.sqrt((deg[v] + 1.0) * (deg[u] + 1.0))
+        if layer == 1:
+            M[v, v] += 1.0 / (deg[v] + 1.0)
+    return M
+
+
+def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws):
+    M = torch.tensor(dense_matrix(indptr, indices, part_of, kept, p, layer), dtype=torch.float64)
+    H = torch.tensor(np.asarray(X, np.float64))
+    W = [torch.tensor(np.asarray(w, np.float64), requires_grad=True) for w in Ws]
+    y = torch.tensor(np.asarray(labels, np.int64))
+    L = len(W)
+    Hs, Zs = [H], []
+    for l in range(L):
+        Z = M @ Hs[-1]
+        Zs.append(Z)
+        pre = torch.cat([Z, Hs[-1]], dim=1) @ W[l] if layer == 0 else Z @ W[l]
+        Hn = torch.relu(pre) if l < L - 1 else pre
+        Hn.retain_grad()
+        Hs.append(Hn)
+    train = y >= 0
+    ntr = int(train.sum())
+    logits = Hs[-1]
+    if ntr:
+        loss = torch.nn.functional.cross_entropy(logits[train], y[train], reduction="sum") / ntr
+    else:
+        loss = logits.sum() * 0.0
+    loss.backward()
+    am = logits.detach().numpy().argmax(1)  # numpy argmax: first max = lowest index (R22)
+    acc = float(((am == y.numpy()) & train.numpy()).sum()) / ntr if ntr else 0.0
+    return dict(loss=float(loss.detach()), acc=acc, H=[h.detach().numpy() for h in Hs], Z=[z.detach().numpy() for z in Zs],
+                dH=[None] + [h.grad.numpy() if h.grad is not None else None for h in Hs[1:]],
+                dW=[w.grad.numpy() for w in W])
