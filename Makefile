@@ -32,7 +32,7 @@ $(OBJDIR)/%.cpp.o: $(PKG)/csrc/%.cpp $(CHDR)
 	$(NVCC) -O2 -std=c++17 -Xcompiler -fPIC -Iinclude -I$(NCCL_DIR)/include -c -o $@ $<
 
 $(PKG)/libbns.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib -lcuda
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
 
 clean:
 	rm -rf $(OBJDIR) oracle/liboracle.so $(PKG)/inputs/libbnsgen.so $(PKG)/libbns.so

@@ -1,0 +1,169 @@
+/* bns.h -- C ABI of libbns.so: the per-epoch hot path of BNS-GCN (Wan et al., MLSys'22, arXiv 2203.10983)
+ * on B200 (sm_100a).
+ *
+ * The three main calls follow the paper's statement of the problem, Algorithm 1:
+ *   bns_setup            Alg.1 inputs "partition number m, partition id i, graph partition G_i, boundary node set
+ *                        B_i, node feature X_i, label Y_i" and l.1-2 (V_i, H^(0) = X_i).
+ *   bns_sample_boundary  Alg.1 l.4-7: Bernoulli(p) selection of U_i ⊆ B_i, node-induced
+ *                        subgraph on V_i ∪ U_i, and the send lists S_{i,j} = U_j ∩ V_i.
+ *   bns_epoch            Alg.1 l.8-14: L x (send/recv H_{S_{i,j}} -> GCN layer), loss,
+ *                        backward with boundary-gradient exchange, AllReduce, SGD update.
+ *
+ * Process model: one context per process and GPU, rank r == partition id i, world == m.  The three main calls are
+ * COLLECTIVE: every rank calls them in the same order with identical p / seed / epoch / lr.
+ * Transports: NONE (world == 1), NCCL (one process per GPU; grouped ncclSend/ncclRecv + ncclAllReduce), or LOCAL
+ * (several contexts of one process, each driven by its own host thread; halo rows are pulled with device copies
+ * -- used to run multi-partition parity on a single GPU).
+ *
+ * Readings of the paper where it is silent are numbered R1..R35.  The ones that
+ * shape this ABI: R1 mean denominator = full-graph degree; R3 1/p applied on the receiving side as a column scale
+ * (exchanged rows are bit-exact copies); R7 Philox4x32-10 keep(u,i) = out.x < floor(p*2^32) with
+ * ctr = {u, i, epoch_lo, epoch_hi}, key = {seed_lo, seed_hi}; R8 loss = global mean CE over train nodes (labels >= 0),
+ * sum-all-reduced; R14 weight layout; R18 acc = train accuracy of this epoch's sampled forward; R24 U_i ordered by
+ * (owner, gid); R27 "broadcast U_i" replaced by recomputation under the shared counter-based RNG.
+ *
+ * Errors: no C++ exception crosses the ABI.  BNS_ERR_INVALID leaves the context unchanged.  BNS_ERR_RUNTIME (any
+ * CUDA / NCCL failure) makes the context sticky-failed: every later call returns BNS_ERR_STATE.  The message of
+ * the last error is bns_last_error(ctx) (or bns_last_error(NULL) for errors raised before a context exists).
+ */
+#ifndef BNS_H_
+#define BNS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BNS_OK = 0,
+    BNS_ERR_INVALID = 1,    /* bad argument; context unchanged */
+    BNS_ERR_RUNTIME = 2,    /* CUDA / NCCL / transport failure; context becomes sticky-failed */
+    BNS_ERR_STATE = 3,      /* call out of order (bns_epoch before any bns_sample_boundary) or failed context */
+    BNS_ERR_OOM = 4,        /* device allocation failed, or a draw exceeded the halo capacity sized by max_p */
+    BNS_ERR_NONFINITE = 5   /* global loss not finite; no weight update applied */
+} bns_status;
+
+typedef enum {
+    BNS_LAYER_SAGE_MEAN = 0,  /* GraphSAGE-mean: h_v = σ(W · CONCAT(z_v, h_v)), z_v = mean aggregate */
+    BNS_LAYER_GCN = 1         /* GCN: Z = P H W, P = D~^-1/2 (A+I) D~^-1/2 (App. A) */
+} bns_layer;
+
+typedef enum {
+    BNS_FP32 = 0,   /* fp32 storage of H / Z / halo rows / gradients, fp32 accumulation, fp32 GEMM */
+    BNS_BF16 = 1    /* bf16 storage of H / Z / halo / GEMM operands, fp32 accumulation, fp32 master weights,
+                       tcgen05 bf16 tensor-core GEMM (R19) */
+} bns_precision;
+
+typedef enum {
+    BNS_TRANSPORT_NONE = 0,   /* world must be 1 */
+    BNS_TRANSPORT_NCCL = 1,   /* cfg.nccl_id: 128-byte ncclUniqueId, identical on all ranks (bns_get_unique_id) */
+    BNS_TRANSPORT_LOCAL = 2   /* cfg.group: in-process group from bns_group_create(world) */
+} bns_transport;
+
+/* cfg.flags */
+#define BNS_PLAN_ONLY               0x1u  /* host plan only: no device memory, no kernels (CPU-testable) */
+#define BNS_DEBUG_EXCHANGE_INDICES  0x2u  /* also exchange the sampled gid lists and check them against the
+                                             recomputed S_{i,j} (R27); mismatch -> BNS_ERR_RUNTIME */
+#define BNS_TIMING                  0x4u  /* record CUDA events per phase; read with BNS_Q_TIMES */
+#define BNS_RETAIN_GRADS            0x8u  /* keep a copy of dL/dH^(l) per layer for BNS_Q_DH (parity tests) */
+
+typedef struct bns_ctx bns_ctx;
+typedef struct bns_group bns_group;
+
+typedef struct {
+    int32_t rank;             /* partition id i, 0 <= rank < world */
+    int32_t world;            /* number of partitions m */
+    int32_t device;           /* CUDA device ordinal */
+    int32_t transport;        /* bns_transport */
+    const uint8_t* nccl_id;   /* 128 bytes when transport == NCCL, else NULL */
+    bns_group* group;         /* when transport == LOCAL, else NULL */
+    void* stream;             /* cudaStream_t to enqueue on, or NULL: the library creates a non-blocking stream */
+    int32_t num_layers;       /* L >= 1 */
+    const int32_t* dims;      /* L+1 logical dims: dims[0] = feature dim, dims[L] = number of classes C */
+    int32_t layer;            /* bns_layer */
+    int32_t precision;        /* bns_precision */
+    double max_p;             /* halo capacity: <= 0 or >= 1 -> sized for p = 1 (|B_i| rows); else
+                                 ceil(max_p*|B_i| + 8 sqrt(max_p*|B_i|) + 64) rows (R34) */
+    uint32_t flags;           /* BNS_PLAN_ONLY | BNS_DEBUG_EXCHANGE_INDICES | BNS_TIMING | BNS_RETAIN_GRADS */
+} bns_config;
+
+/* ncclGetUniqueId into out[128] (rank 0 calls it and broadcasts the bytes, e.g. over a torch process group). */
+bns_status bns_get_unique_id(uint8_t* out);
+
+/* In-process group for BNS_TRANSPORT_LOCAL: `world` contexts, each driven by its own host thread. */
+bns_status bns_group_create(int32_t world, bns_group** out);
+void bns_group_destroy(bns_group* g);
+
+/* Build this rank's plan (V_i, B_i ordered by (owner, gid), D_{i->j} = B_j ∩ V_i, static CSR split, degrees),
+ * allocate every device buffer at its capacity (no allocation happens later), copy to HBM, attach the transport.
+ *   num_nodes, indptr[num_nodes+1] (int64), indices[indptr[N]] (int32): HOST, full graph, symmetric, ascending
+ *       columns, no self loops, no duplicates.  Borrowed for the call only.
+ *   part_of[num_nodes]: HOST, values in [0, world); every partition non-empty.
+ *   features: HOST, row-major |V_i| x dims[0] fp32 -- this rank's inner nodes in ascending global id (X_i).
+ *   labels:   HOST, [|V_i|] int32: -1 = not a training node, else [0, dims[L]) (Y_i).
+ * Collective (transport attach).  Invalid input -> BNS_ERR_INVALID with a message in bns_last_error(NULL). */
+bns_status bns_setup(const bns_config* cfg, int64_t num_nodes, const int64_t* indptr, const int32_t* indices,
+                     const int32_t* part_of, const float* features, const int32_t* labels, bns_ctx** out);
+
+/* Alg.1 l.4-7: draw U_i (keep(u, i) for u in B_i) and recompute S_{i,j} (keep(u, j) for u in D_{i->j}),
+ * build the induced subgraph over V_i ∪ U_i.  p in [0, 1] (p = 0 allowed: isolated partitions).  Returns after
+ * one stream sync (the per-peer counts come to the host for the exchange sizes).  Collective in effect (no
+ * messages are sent).  p > max_p, or a draw larger than the halo capacity -> BNS_ERR_OOM. */
+bns_status bns_sample_boundary(bns_ctx* ctx, double p, uint64_t seed, uint64_t epoch);
+
+/* Alg.1 l.8-14 with the draw of the last bns_sample_boundary.
+ *   weights[l], l < L: fp32 row-major, SAGE (2*dims[l]) x dims[l+1] (rows [0,dims[l]) multiply z_v, R14),
+ *       GCN dims[l] x dims[l+1].  Device pointers on cfg.device (updated in place: W <- W - lr*g) or host
+ *       pointers (copied in and out inside the call).
+ *   grads[l]: same shapes, out: the all-reduced gradient g (identical on every rank); may be NULL.
+ *   loss: out, global mean cross-entropy over train nodes (R8); acc: out, global train accuracy (R18, R22).
+ * Returns after a stream sync.  Collective. */
+bns_status bns_epoch(bns_ctx* ctx, float* const* weights, float lr, float* const* grads, double* loss, double* acc);
+
+/* Debug / parity queries: copy a host-side view into host_dst (capacity in bytes); *written = bytes written.
+ * Row tensors are returned as fp32 row-major with LOGICAL dims (padding stripped), inner rows in ascending gid. */
+typedef enum {
+    BNS_Q_COUNTS = 0,        /* int64[6 + 2m]: n_in, n_bd, |U_i|, ΣS, nnz_i(static), nnz_kept(epoch),
+                                recv_cnt[m] (rows received from each owner), send_cnt[m] (rows sent to each peer) */
+    BNS_Q_INNER = 1,         /* int32[n_in]  V_i global ids */
+    BNS_Q_BOUNDARY = 2,      /* int32[n_bd]  B_i global ids, (owner, gid) order */
+    BNS_Q_BOUNDARY_OFF = 3,  /* int64[m+1]   owner offsets into B_i */
+    BNS_Q_SENDCAND = 4,      /* int32[ΣD]    D_{i->j} global ids, concatenated over j ascending */
+    BNS_Q_SENDCAND_OFF = 5,  /* int64[m+1] */
+    BNS_Q_MASK = 6,          /* uint8[n_bd]  keep flag of every B_i entry (this epoch) */
+    BNS_Q_HALO = 7,          /* int32[|U_i|] U_i global ids (owner-major, gid ascending) */
+    BNS_Q_HALO_OFF = 8,      /* int64[m+1] */
+    BNS_Q_SEND = 9,          /* int32[ΣS]    S_{i,j} global ids, concatenated over j ascending */
+    BNS_Q_SEND_OFF = 10,     /* int64[m+1] */
+    BNS_Q_H = 11,            /* layer l in [0,L]: H^(l) inner rows, n_in x dims[l] (l = L: logits) */
+    BNS_Q_Z = 12,            /* layer l in [1,L]: aggregation output Z^(l), n_in x dims[l-1] */
+    BNS_Q_DH = 13,           /* layer l in [1,L]: dL/dH^(l) after owner accumulation (l = L: dLogits);
+                                l < L needs BNS_RETAIN_GRADS */
+    BNS_Q_HALO_ROWS = 14,    /* layer l in [1,L]: received halo rows of the layer-l input, |U_i| x dims[l-1] */
+    BNS_Q_INDUCED = 15,      /* int64[n_in+1] row pointers then int32[nnz_kept] local columns of the induced
+                                subgraph (inner j -> j, halo slot s -> n_in + s) */
+    BNS_Q_TIMES = 16,        /* double[BNS_NUM_PHASES]: ms accumulated per phase since setup (BNS_TIMING) */
+    BNS_Q_STATIC_CSR = 17,   /* int64[n_in+1] then int32[nnz_i]: static rows, columns encoded inner j -> j,
+                                boundary index b -> -(b+1) (plan, available in BNS_PLAN_ONLY) */
+    BNS_Q_MEMORY = 18,       /* int64[2]: device bytes allocated by the context, peak device bytes */
+    BNS_Q_KERNEL_COUNT = 19  /* int64[1]: kernels launched by this context since setup */
+} bns_query_what;
+
+enum { BNS_PH_SAMPLE = 0, BNS_PH_INDUCE, BNS_PH_PACK, BNS_PH_EXCHANGE, BNS_PH_SPMM_FWD, BNS_PH_GEMM_FWD,
+       BNS_PH_LOSS, BNS_PH_GEMM_BWD, BNS_PH_SPMM_BWD, BNS_PH_EXCHANGE_BWD, BNS_PH_SCATTER, BNS_PH_ALLREDUCE,
+       BNS_PH_UPDATE, BNS_PH_EPOCH_TOTAL, BNS_PH_SAMPLE_TOTAL, BNS_NUM_PHASES };
+
+bns_status bns_query(bns_ctx* ctx, int32_t what, int32_t layer, void* host_dst, int64_t capacity_bytes,
+                     int64_t* written);
+
+/* The cudaStream_t the context enqueues on (as void*). */
+void* bns_stream(const bns_ctx* ctx);
+
+const char* bns_last_error(const bns_ctx* ctx);
+void bns_destroy(bns_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BNS_H_ */

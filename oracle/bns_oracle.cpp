@@ -20,10 +20,14 @@
 //   reduce   g = AllReduce(g_i)             PAPER.md:291 (Alg.1 l.13); R21
 //   update   w <- w - eta g                 PAPER.md:292 (Alg.1 l.14); R9
 //
+//   bf16     R19 storage emulation (optional): stored tensors rounded to bf16, arithmetic in double -- rb()
+//
 // Pins (tests/test_oracle_*.py, all `-m "not gpu"`): Random123 Philox KATs; dense-adjacency float64
 // brute force with torch autograd (independent backward); central finite differences of the oracle's own
 // loss; SPEC hand examples (P4, K1,5); the survey's tiny goldens E1-E6 (tests/golden/); p=1 == unpartitioned;
-// p=0 == dense on A∘[same part]; Binomial(|B_i|, p) counts; Eq. 3 identity.
+// p=0 == dense on A∘[same part]; Binomial(|B_i|, p) counts; Eq. 3 identity; for the R19 emulation:
+// rb() against torch's bfloat16 cast, bf16-exact goldens reproduce the float64 forward exactly, and gradients stay
+// within bf16 rounding of the float64 ones.
 // Every function here is pinned; none is "parity unpinned".
 #include <cmath>
 #include <cstdint>
@@ -76,6 +80,19 @@ bool keep(uint32_t u, uint32_t i, uint64_t epoch, uint64_t seed, uint64_t T) {
 
 enum { KIND_SAGE = 0, KIND_GCN = 1 };
 
+// R19 (bf16-GEMM mode): "bf16 storage of H / Z / halo / GEMM operands, fp32 accumulation,
+// fp32 master weights".  When the oracle runs in that mode it rounds every STORED tensor the definition names to
+// bf16 (round-to-nearest-even of the fp32 value) and keeps everything else in double.  rb() is that rounding.
+double rb(double x) {
+    float f = (float)x;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) return x;          // inf / nan unchanged
+    u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+    std::memcpy(&f, &u, 4);
+    return (double)f;
+}
+
 struct Partition {
     // plan (static)
     std::vector<int32_t> V;                 // inner nodes, ascending gid (Alg.1 l.1)
@@ -98,6 +115,7 @@ struct Oracle {
     int L = 1;
     std::vector<int32_t> dims;              // L+1
     int kind = KIND_SAGE;
+    bool bf16 = false;                      // R19 storage emulation (see rb())
     std::vector<double> X;                  // N x dims[0]
     std::vector<int32_t> labels;            // N, -1 = not a training node
     std::vector<Partition> parts;
@@ -204,6 +222,12 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
     const int m = o.m, L = o.L;
     const double p = o.p;
     const double inv_p = (p > 0.0) ? 1.0 / p : 0.0;   // R32: never used when nothing is kept
+    auto st = [&](double x) { return o.bf16 ? rb(x) : x; };   // value as stored (R19)
+    std::vector<std::vector<double>> Wq(L);                    // GEMM operand copy of the weights (R19)
+    for (int l = 0; l < L; ++l) {
+        Wq[l] = W[l];
+        for (double& w : Wq[l]) w = st(w);
+    }
 
     o.H.assign(L + 1, std::vector<double>());
     o.Z.assign(L + 1, std::vector<double>());
@@ -269,7 +293,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                         double c = (ru < (int64_t)n_in) ? 1.0 : inv_p;
                         for (int k = 0; k < din; ++k) z[k] += c * X[(size_t)ru * din + k];
                     }
-                    for (int k = 0; k < din; ++k) z[k] /= (double)dv;
+                    for (int k = 0; k < din; ++k) z[k] = st(z[k] / (double)dv);
                 } else {
                     // z_v = x_v / d~_v + sum_u c_u x_u / sqrt(d~_v d~_u)   (App.A P = D~^-1/2 (A+I) D~^-1/2,
                     // PAPER.md:736; S diagonal PAPER.md:771-778; R2, R16)
@@ -284,13 +308,14 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                         double a = c / std::sqrt(dtv * dtu);
                         for (int k = 0; k < din; ++k) z[k] += a * X[(size_t)ru * din + k];
                     }
+                    for (int k = 0; k < din; ++k) z[k] = st(z[k]);
                 }
             }
             // update phi: SAGE pre = W^T [z ; x]  (CONCAT(z_v, h_v); R13 no bias, R14 layout)
             //             GCN  pre = W^T z          (App.A Z = P H W)
             std::vector<double>& pre = PREs[l][i];
             pre.assign(n_in * dout, 0.0);
-            const std::vector<double>& Wl = W[l - 1];
+            const std::vector<double>& Wl = Wq[l - 1];
             for (size_t r = 0; r < n_in; ++r) {
                 double* out = &pre[r * dout];
                 for (int k = 0; k < din; ++k) {
@@ -313,7 +338,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                 size_t g = (size_t)P.V[r];
                 for (int c = 0; c < dout; ++c) {
                     double x = PREs[l][i][r * dout + c];
-                    o.H[l][g * dout + c] = (l < L) ? (x > 0.0 ? x : 0.0) : x;
+                    o.H[l][g * dout + c] = (l < L) ? st(x > 0.0 ? x : 0.0) : x;   // logits stay fp32 (R19)
                 }
                 for (int k = 0; k < din; ++k) o.Z[l][g * din + k] = Zs[l][i][r * din + k];
             }
@@ -355,7 +380,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
     std::vector<std::vector<std::vector<double>>> gW(m, std::vector<std::vector<double>>(L));
     for (int l = L; l >= 1; --l) {
         const int din = o.dims[l - 1], dout = o.dims[l];
-        const std::vector<double>& Wl = W[l - 1];
+        const std::vector<double>& Wl = Wq[l - 1];
         std::vector<std::vector<double>> dXs(m);     // gradient w.r.t. stacked input rows (inner + halo)
         for (int i = 0; i < m; ++i) {
             const Partition& P = o.parts[i];
@@ -365,7 +390,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
             for (size_t r = 0; r < n_in; ++r)
                 for (int c = 0; c < dout; ++c) {
                     double g = o.dH[l][(size_t)P.V[r] * dout + c];
-                    dpre[r * dout + c] = (l < L) ? (PREs[l][i][r * dout + c] > 0.0 ? g : 0.0) : g;
+                    dpre[r * dout + c] = (l < L) ? (PREs[l][i][r * dout + c] > 0.0 ? g : 0.0) : st(g);
                 }
             // weight gradient of this partition
             const int wrows = (o.kind == KIND_SAGE) ? 2 * din : din;
@@ -379,49 +404,48 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                         for (int k = 0; k < din; ++k) g[(size_t)(din + k) * dout + c] += Xs[l][i][r * din + k] * d;
                 }
             if (l == 1) continue;                   // R29: input features are not trainable
-            // dZ = dPre W_top^T ; dXself = dPre W_bot^T (SAGE)
-            std::vector<double> dZ(n_in * din, 0.0), dXself(n_in * din, 0.0);
-            for (size_t r = 0; r < n_in; ++r)
+            // dZ' = (dPre W_top^T) s_v with s_v = 1/deg_G(v) (SAGE, 0 if deg 0) or 1/sqrt(d~_v) (GCN) -- the
+            // row factor of the aggregation coefficient; dXself = dPre W_bot^T (SAGE self half of CONCAT)
+            std::vector<double> dZp(n_in * din, 0.0), dXself(n_in * din, 0.0);
+            for (size_t r = 0; r < n_in; ++r) {
+                int64_t dv = deg(o, P.V[r]);
+                double sv = (o.kind == KIND_SAGE) ? (dv ? 1.0 / (double)dv : 0.0) : 1.0 / std::sqrt((double)(dv + 1));
                 for (int k = 0; k < din; ++k) {
                     double a = 0.0, b = 0.0;
                     for (int c = 0; c < dout; ++c) {
                         a += dpre[r * dout + c] * Wl[(size_t)k * dout + c];
                         if (o.kind == KIND_SAGE) b += dpre[r * dout + c] * Wl[(size_t)(din + k) * dout + c];
                     }
-                    dZ[r * din + k] = a;
-                    dXself[r * din + k] = b;
-                }
-            // transpose of the aggregation: dX_u += a_{v,u} dZ_v over the kept edges of every inner v
-            std::vector<double>& dX = dXs[i];
-            dX.assign((n_in + n_h) * din, 0.0);
-            if (o.kind == KIND_SAGE)
-                for (size_t r = 0; r < n_in; ++r)
-                    for (int k = 0; k < din; ++k) dX[r * din + k] = dXself[r * din + k];
-            for (size_t r = 0; r < n_in; ++r) {
-                int32_t v = P.V[r];
-                int64_t dv = deg(o, v);
-                if (o.kind == KIND_SAGE) {
-                    if (dv == 0) continue;
-                    for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
-                        int64_t ru = idx[i].row[o.indices[e]];
-                        if (ru < 0) continue;
-                        double c = (ru < (int64_t)n_in) ? 1.0 : inv_p;
-                        double a = c / (double)dv;
-                        for (int k = 0; k < din; ++k) dX[(size_t)ru * din + k] += a * dZ[r * din + k];
-                    }
-                } else {
-                    double dtv = (double)(dv + 1);
-                    for (int k = 0; k < din; ++k) dX[r * din + k] += dZ[r * din + k] / dtv;
-                    for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
-                        int32_t u = o.indices[e];
-                        int64_t ru = idx[i].row[u];
-                        if (ru < 0) continue;
-                        double c = (ru < (int64_t)n_in) ? 1.0 : inv_p;
-                        double a = c / std::sqrt(dtv * (double)(deg(o, u) + 1));
-                        for (int k = 0; k < din; ++k) dX[(size_t)ru * din + k] += a * dZ[r * din + k];
-                    }
+                    dZp[r * din + k] = st(a * sv);
+                    dXself[r * din + k] = st(b);
                 }
             }
+            // transpose of the aggregation over the kept edges of every inner v:
+            //   SAGE dX_u = [u inner] dXself_u + c_u sum_{v: u in N(v)} dZ'_v
+            //   GCN  dX_u = c_u rs_u (sum_{v: u in N(v)} dZ'_v + [u inner] dZ'_u)
+            std::vector<double>& dX = dXs[i];
+            dX.assign((n_in + n_h) * din, 0.0);
+            for (size_t r = 0; r < n_in; ++r) {
+                int32_t v = P.V[r];
+                if (o.kind == KIND_GCN) {
+                    double rs = 1.0 / std::sqrt((double)(deg(o, v) + 1));
+                    for (int k = 0; k < din; ++k) dX[r * din + k] += rs * dZp[r * din + k];
+                }
+                for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
+                    int32_t u = o.indices[e];
+                    int64_t ru = idx[i].row[u];
+                    if (ru < 0) continue;
+                    double c = (ru < (int64_t)n_in) ? 1.0 : inv_p;
+                    if (o.kind == KIND_GCN) c /= std::sqrt((double)(deg(o, u) + 1));
+                    for (int k = 0; k < din; ++k) dX[(size_t)ru * din + k] += c * dZp[r * din + k];
+                }
+            }
+            for (size_t r = 0; r < n_in + n_h; ++r)
+                for (int k = 0; k < din; ++k) {
+                    double x = dX[r * din + k];
+                    if (o.kind == KIND_SAGE && r < n_in) x += dXself[r * din + k];
+                    dX[r * din + k] = st(x);
+                }
         }
         if (l == 1) continue;
         // reverse exchange: halo-row gradients go back to their owners and are added into the owners'
@@ -439,8 +463,10 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                 const size_t n_in = P.V.size();
                 for (int64_t s = P.U_off[j]; s < P.U_off[j + 1]; ++s) {
                     int32_t u = P.U[s];
-                    for (int k = 0; k < din; ++k)
-                        o.dH[l - 1][(size_t)u * din + k] += dXs[i][(n_in + (size_t)s) * din + k];
+                    for (int k = 0; k < din; ++k) {
+                        double& t = o.dH[l - 1][(size_t)u * din + k];
+                        t = st(t + dXs[i][(n_in + (size_t)s) * din + k]);
+                    }
                 }
             }
         }
@@ -559,6 +585,9 @@ int64_t orc_tensor(void* h, int32_t what, int32_t layer, double* out, int64_t ca
     if (out) std::copy(t.begin(), t.begin() + std::min(n, cap), out);
     return n;
 }
+
+void orc_set_bf16(void* h, int32_t on) { ((Oracle*)h)->bf16 = on != 0; }
+double orc_round_bf16(double x) { return rb(x); }
 
 int64_t orc_rows_sent(void* h, int32_t layer) {
     Oracle& o = *(Oracle*)h;

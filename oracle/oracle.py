@@ -45,6 +45,9 @@ def lib():
         L.orc_epoch.argtypes = [vp, vp, f64, vp, vp, vp]
         L.orc_tensor.restype = i64
         L.orc_tensor.argtypes = [vp, i32, i32, vp, i64]
+        L.orc_set_bf16.argtypes = [vp, i32]
+        L.orc_round_bf16.restype = f64
+        L.orc_round_bf16.argtypes = [f64]
         L.orc_rows_sent.restype = i64
         L.orc_rows_sent.argtypes = [vp, i32]
         _LIB = L
@@ -65,6 +68,10 @@ def philox4x32_10(ctr, key):
 
 def draw(u, i, epoch, seed):
     return int(lib().orc_draw(u, i, epoch, seed))
+
+
+def round_bf16(x):
+    return float(lib().orc_round_bf16(float(x)))
 
 
 def threshold(p):
@@ -90,6 +97,10 @@ class Oracle:
         if getattr(self, "h", None):
             lib().orc_destroy(self.h)
             self.h = None
+
+    def set_bf16(self, on=True):
+        """R19 bf16-storage emulation: round the stored tensors (Z, H, GEMM operands, dPre, dZ', dX) to bf16."""
+        lib().orc_set_bf16(self.h, 1 if on else 0)
 
     def list(self, what, rank, peer=0):
         n = lib().orc_list(self.h, what, rank, peer, None, 0)

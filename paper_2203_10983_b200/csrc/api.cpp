@@ -1,0 +1,804 @@
+// api.cpp -- the C ABI (include/bns.h): context lifecycle, setup (a0), per-epoch orchestration of Algorithm 1
+// (PAPER.md:269-297), debug queries.  Every arithmetic step runs in the sm_100a kernels; this file only sequences
+// launches, exchanges and the two host syncs per epoch (counts after sampling; loss/acc at the end).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "common.h"
+#include "kernels.h"
+#include "transport.h"
+
+struct bns_ctx {
+    bns::Ctx c;
+};
+
+namespace bns {
+namespace {
+
+thread_local std::string g_err;
+
+bns_status fail(bns_ctx* h, const Error& e) {
+    if (h) {
+        h->c.err = e.what();
+        if (e.code == BNS_ERR_RUNTIME) h->c.failed = true;
+    } else {
+        g_err = e.what();
+    }
+    return e.code;
+}
+
+template <typename F>
+bns_status guard(bns_ctx* h, F&& f) {
+    try {
+        f();
+        return BNS_OK;
+    } catch (const Error& e) {
+        return fail(h, e);
+    } catch (const std::bad_alloc&) {
+        return fail(h, Error(BNS_ERR_OOM, "host allocation failed"));
+    } catch (const std::exception& e) {
+        return fail(h, Error(BNS_ERR_RUNTIME, e.what()));
+    }
+}
+
+void* dalloc(Ctx& c, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~size_t(255);
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error(BNS_ERR_OOM, "cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e));
+    }
+    c.allocs.push_back(p);
+    c.dev_bytes += (int64_t)bytes;
+    return p;
+}
+
+template <typename T>
+T* upload(Ctx& c, const std::vector<T>& v) {
+    T* d = static_cast<T*>(dalloc(c, v.size() * sizeof(T)));
+    if (!v.empty()) BNS_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+}
+
+size_t tsize(const Ctx& c) { return c.prec == BNS_BF16 ? 2 : 4; }
+
+void validate(const bns_config* cfg, int64_t N, const int64_t* indptr, const int32_t* indices, const int32_t* part_of) {
+    if (!cfg) throw Error(BNS_ERR_INVALID, "cfg is NULL");
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) throw Error(BNS_ERR_INVALID, "bad rank/world");
+    if (cfg->num_layers < 1 || !cfg->dims) throw Error(BNS_ERR_INVALID, "num_layers < 1 or dims NULL");
+    for (int l = 0; l <= cfg->num_layers; ++l)
+        if (cfg->dims[l] <= 0) throw Error(BNS_ERR_INVALID, "dims must be positive");
+    if (cfg->layer != BNS_LAYER_SAGE_MEAN && cfg->layer != BNS_LAYER_GCN) throw Error(BNS_ERR_INVALID, "bad layer");
+    if (cfg->precision != BNS_FP32 && cfg->precision != BNS_BF16) throw Error(BNS_ERR_INVALID, "bad precision");
+    if (cfg->world > 1 && cfg->transport != BNS_TRANSPORT_NCCL && cfg->transport != BNS_TRANSPORT_LOCAL &&
+        !(cfg->flags & BNS_PLAN_ONLY))
+        throw Error(BNS_ERR_INVALID, "world > 1 needs transport NCCL or LOCAL");
+    if (N < 1 || !indptr || !indices || !part_of) throw Error(BNS_ERR_INVALID, "empty graph or NULL arrays");
+    if (N >= INT32_MAX) throw Error(BNS_ERR_INVALID, "num_nodes must fit int32");
+    if (indptr[0] != 0) throw Error(BNS_ERR_INVALID, "indptr[0] != 0");
+    for (int64_t v = 0; v < N; ++v) {
+        if (indptr[v + 1] < indptr[v]) throw Error(BNS_ERR_INVALID, "indptr not monotone at row " + std::to_string(v));
+        for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e) {
+            int32_t u = indices[e];
+            if (u < 0 || u >= N) throw Error(BNS_ERR_INVALID, "column id out of range at row " + std::to_string(v));
+            if (u == v) throw Error(BNS_ERR_INVALID, "self loop at node " + std::to_string(v));
+            if (e > indptr[v] && indices[e - 1] >= u)
+                throw Error(BNS_ERR_INVALID, "columns not strictly ascending at row " + std::to_string(v));
+        }
+    }
+    std::vector<int64_t> cnt(cfg->world, 0);
+    for (int64_t v = 0; v < N; ++v) {
+        if (part_of[v] < 0 || part_of[v] >= cfg->world)
+            throw Error(BNS_ERR_INVALID, "part_of out of range at node " + std::to_string(v));
+        cnt[part_of[v]]++;
+    }
+    for (int j = 0; j < cfg->world; ++j)
+        if (cnt[j] == 0) throw Error(BNS_ERR_INVALID, "partition " + std::to_string(j) + " is empty");
+}
+
+// host-built segments over a static CSR whose row r spans [ptr[r], ptr[r+1]) (+ptr_base in the column array)
+std::vector<Seg> host_segments(const std::vector<int64_t>& ptr, int64_t rows, int64_t ptr_base, int64_t row_base) {
+    std::vector<Seg> s;
+    for (int64_t r = 0; r < rows; ++r) {
+        int64_t len = ptr[r + 1] - ptr[r];
+        int32_t ns = len > kSeg ? (int32_t)((len + kSeg - 1) / kSeg) : 1;
+        int64_t first = (int64_t)s.size();
+        for (int32_t k = 0; k < ns; ++k) {
+            Seg g;
+            g.row = (int32_t)(row_base + r);
+            g.nseg = ns;
+            g.e0 = ptr_base + ptr[r] + (int64_t)k * kSeg;
+            g.e1 = std::min(ptr_base + ptr[r + 1], g.e0 + kSeg);
+            g.first = first;
+            s.push_back(g);
+        }
+    }
+    return s;
+}
+
+struct PhaseTimer {
+    Ctx& c;
+    int ph;
+    size_t slot;
+    PhaseTimer(Ctx& c_, int ph_) : c(c_), ph(ph_), slot(0) {
+        if (!c.timing) return;
+        slot = c.ev_used;
+        if (slot + 2 > c.ev.size()) { ph = -1; return; }
+        c.ev_used += 2;
+        c.ev_phase[slot / 2] = ph;
+        BNS_CUDA(cudaEventRecord(c.ev[slot], c.stream));
+    }
+    ~PhaseTimer() noexcept(false) {
+        if (!c.timing || ph < 0) return;
+        BNS_CUDA(cudaEventRecord(c.ev[slot + 1], c.stream));
+    }
+};
+
+void collect_times(Ctx& c) {
+    if (!c.timing) return;
+    for (size_t s = 0; s + 1 < c.ev_used; s += 2) {
+        float ms = 0.f;
+        BNS_CUDA(cudaEventElapsedTime(&ms, c.ev[s], c.ev[s + 1]));
+        c.times[c.ev_phase[s / 2]] += ms;
+    }
+    c.ev_used = 0;
+}
+
+void setup_device(Ctx& c, const float* features, const int32_t* labels) {
+    Plan& P = c.plan;
+    const int m = c.cfg.world;
+    BNS_CUDA(cudaSetDevice(c.cfg.device));
+    if (c.cfg.stream) {
+        c.stream = static_cast<cudaStream_t>(c.cfg.stream);
+    } else {
+        BNS_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        c.own_stream = true;
+    }
+    const int L = c.L;
+    c.maxd = 0;
+    for (int l = 0; l <= L; ++l) c.maxd = std::max<int32_t>(c.maxd, c.dp[l]);
+    if (c.cfg.max_p > 0.0 && c.cfg.max_p < 1.0) {
+        double mu = c.cfg.max_p * (double)P.n_bd;
+        c.halo_cap = std::min<int64_t>(P.n_bd, (int64_t)std::ceil(mu + 8.0 * std::sqrt(mu) + 64.0));
+    } else {
+        c.halo_cap = P.n_bd;
+    }
+    c.nnz_i = P.row_ptr[P.n_in];
+    const size_t ts = tsize(c);
+
+    // ---- static plan on device
+    c.d_row_ptr = upload(c, P.row_ptr);
+    c.d_col_enc = upload(c, P.col_enc);
+    c.n_cand = P.n_bd + P.n_send;
+    std::vector<int32_t> gid(c.n_cand), key(c.n_cand), pay(c.n_cand);
+    for (int64_t b = 0; b < P.n_bd; ++b) { gid[b] = P.B[b]; key[b] = c.cfg.rank; pay[b] = (int32_t)b; }
+    for (int j = 0; j < m; ++j)
+        for (int64_t e = P.D_off[j]; e < P.D_off[j + 1]; ++e) {
+            gid[P.n_bd + e] = P.V[P.D_local[e]];
+            key[P.n_bd + e] = j;
+            pay[P.n_bd + e] = P.D_local[e];
+        }
+    c.d_cand_gid = upload(c, gid);
+    c.d_cand_key = upload(c, key);
+    c.d_cand_payload = upload(c, pay);
+    std::vector<int64_t> cseg(2 * m + 1);
+    for (int k = 0; k <= m; ++k) cseg[k] = P.B_off[k];
+    for (int k = 1; k <= m; ++k) cseg[m + k] = P.n_bd + P.D_off[k];
+    c.d_cand_seg = upload(c, cseg);
+    c.d_br_ptr = upload(c, P.br_ptr);
+    std::vector<int32_t> tcol(P.ii_col);
+    c.ii_nnz = (int64_t)P.ii_col.size();
+    tcol.insert(tcol.end(), P.br_col.begin(), P.br_col.end());
+    c.d_tcol = upload(c, tcol);
+    std::vector<float> inv_deg(P.n_in), rs_in(P.n_in), rs_bd(P.n_bd);
+    for (int64_t r = 0; r < P.n_in; ++r) {
+        inv_deg[r] = P.deg_in[r] > 0 ? (float)(1.0 / (double)P.deg_in[r]) : 0.f;
+        rs_in[r] = (float)(1.0 / std::sqrt((double)P.deg_in[r] + 1.0));
+    }
+    for (int64_t b = 0; b < P.n_bd; ++b) rs_bd[b] = (float)(1.0 / std::sqrt((double)P.deg_bd[b] + 1.0));
+    c.d_deg_in = upload(c, inv_deg);   // holds 1/deg_G (0 for isolated nodes)
+    c.d_rs_in = upload(c, rs_in);
+    c.d_rs_bd = upload(c, rs_bd);
+
+    // static segments: backward inner part (A_II, columns in d_tcol[0, ii_nnz)) ...
+    std::vector<Seg> sb = host_segments(P.ii_ptr, P.n_in, 0, 0);
+    c.n_seg_bwd_inner = (int64_t)sb.size();
+    int64_t halo_seg_cap = P.n_bd + (int64_t)P.br_col.size() / kSeg + 1;
+    c.seg_bwd_cap = c.n_seg_bwd_inner + halo_seg_cap;
+    c.d_seg_bwd = static_cast<Seg*>(dalloc(c, c.seg_bwd_cap * sizeof(Seg)));
+    BNS_CUDA(cudaMemcpy(c.d_seg_bwd, sb.data(), sb.size() * sizeof(Seg), cudaMemcpyHostToDevice));
+    // ... and the full static induced CSR used when every boundary node is kept (p = 1)
+    std::vector<int32_t> scol(P.col_enc.size());
+    for (size_t k = 0; k < scol.size(); ++k)
+        scol[k] = P.col_enc[k] >= 0 ? P.col_enc[k] : (int32_t)(P.n_in + (-P.col_enc[k] - 1));
+    c.d_static_col = upload(c, scol);
+    std::vector<Seg> sf = host_segments(P.row_ptr, P.n_in, 0, 0);
+    c.n_seg_static_fwd = (int64_t)sf.size();
+    c.d_seg_static_fwd = upload(c, sf);
+    c.seg_fwd_cap = P.n_in + c.nnz_i / kSeg + 1;
+    c.d_seg_fwd = static_cast<Seg*>(dalloc(c, c.seg_fwd_cap * sizeof(Seg)));
+    int64_t seg_max = std::max({c.seg_fwd_cap, c.seg_bwd_cap, c.n_seg_static_fwd});
+    c.d_partial = static_cast<float*>(dalloc(c, (size_t)seg_max * c.maxd * sizeof(float)));
+
+    // ---- per-epoch scratch
+    c.d_flags = static_cast<uint8_t*>(dalloc(c, c.n_cand));
+    c.d_blk = static_cast<int32_t*>(dalloc(c, (c.n_cand / 1024 + 2) * sizeof(int32_t)));
+    c.d_cand_out = static_cast<int32_t*>(dalloc(c, (c.n_cand + 1) * sizeof(int32_t)));
+    c.d_slot_of_b = static_cast<int32_t*>(dalloc(c, (P.n_bd + 1) * sizeof(int32_t)));
+    c.d_seg_pos = static_cast<int64_t*>(dalloc(c, (2 * m + 1 + 8) * sizeof(int64_t)));
+    BNS_CUDA(cudaMallocHost(&c.h_seg_pos, (2 * m + 1 + 8) * sizeof(int64_t)));
+    c.d_ind_ptr = static_cast<int64_t*>(dalloc(c, (P.n_in + 1) * sizeof(int64_t)));
+    c.d_ind_col = static_cast<int32_t*>(dalloc(c, (c.nnz_i + 1) * sizeof(int32_t)));
+    const int64_t rmax = std::max<int64_t>(P.n_in, P.n_bd) + 1;
+    c.d_row_cnt = static_cast<int32_t*>(dalloc(c, rmax * sizeof(int32_t)));
+    c.d_row_nseg = static_cast<int32_t*>(dalloc(c, rmax * sizeof(int32_t)));
+    c.d_row_soff = static_cast<int64_t*>(dalloc(c, (rmax + 1) * sizeof(int64_t)));
+    c.d_scan_tmp = static_cast<int64_t*>(dalloc(c, (std::max(rmax, c.n_cand) / 1024 + 16) * 3 * sizeof(int64_t)));
+    c.d_cscale = static_cast<float*>(dalloc(c, (P.n_in + c.halo_cap + 1) * sizeof(float)));
+
+    // ---- activations
+    c.H.assign(L, nullptr);
+    c.Z.assign(L + 1, nullptr);
+    for (int l = 0; l < L; ++l) c.H[l] = dalloc(c, (size_t)(P.n_in + c.halo_cap) * c.dp[l] * ts);
+    for (int l = 1; l <= L; ++l) c.Z[l] = dalloc(c, (size_t)P.n_in * c.dp[l - 1] * ts);
+    c.d_logits = static_cast<float*>(dalloc(c, (size_t)P.n_in * c.dp[L] * sizeof(float)));
+    c.d_dlogits = static_cast<float*>(dalloc(c, (size_t)P.n_in * c.dp[L] * sizeof(float)));
+    c.d_dpre = dalloc(c, (size_t)P.n_in * c.maxd * ts);
+    c.d_dxcat = dalloc(c, (size_t)P.n_in * 2 * c.maxd * ts);
+    c.d_dx = dalloc(c, (size_t)(P.n_in + c.halo_cap) * c.maxd * ts);
+    c.d_sendbuf = dalloc(c, (size_t)P.n_send * c.maxd * ts);
+    c.d_gradbuf = dalloc(c, (size_t)P.n_send * c.maxd * ts);
+    if (c.retain) {
+        c.dH_keep.assign(L + 1, nullptr);
+        for (int l = 1; l < L; ++l) c.dH_keep[l] = dalloc(c, (size_t)P.n_in * c.dp[l] * ts);
+    }
+    BNS_CUDA(cudaMemset(c.H[0], 0, (size_t)(P.n_in + c.halo_cap) * c.dp[0] * ts));
+    if (P.n_in > 0) {
+        float* stage = nullptr;
+        BNS_CUDA(cudaMalloc(&stage, (size_t)P.n_in * c.dims[0] * sizeof(float)));
+        BNS_CUDA(cudaMemcpy(stage, features, (size_t)P.n_in * c.dims[0] * sizeof(float), cudaMemcpyHostToDevice));
+        launch_to_storage(c, stage, P.n_in, c.dims[0], c.dims[0], c.H[0], c.dp[0]);
+        BNS_CUDA(cudaStreamSynchronize(c.stream));
+        BNS_CUDA(cudaFree(stage));
+    }
+    std::vector<int32_t> lab(labels, labels + P.n_in);
+    c.d_labels = upload(c, lab);
+
+    // ---- weights and gradients
+    c.Wpad.assign(L, nullptr);
+    c.Wt.assign(L, nullptr);
+    c.wrows.assign(L, 0);
+    c.wcols.assign(L, 0);
+    c.goff.assign(L + 1, 0);
+    int64_t wmax = 0, wlog = 0;
+    for (int l = 0; l < L; ++l) {
+        c.wrows[l] = (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * (int64_t)c.dp[l];
+        c.wcols[l] = c.dp[l + 1];
+        c.goff[l + 1] = c.goff[l] + c.wrows[l] * c.wcols[l];
+        wmax = std::max(wmax, c.wrows[l] * c.wcols[l]);
+        wlog += (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * (int64_t)c.dims[l] * c.dims[l + 1];
+        c.Wpad[l] = static_cast<float*>(dalloc(c, c.wrows[l] * c.wcols[l] * sizeof(float)));
+        c.Wt[l] = (c.prec == BNS_BF16) ? dalloc(c, c.wrows[l] * c.wcols[l] * 2) : (void*)c.Wpad[l];
+    }
+    c.gflat_n = c.goff[L];
+    c.d_gflat = static_cast<float*>(dalloc(c, c.gflat_n * sizeof(float)));
+    c.splitk_cap = 32 * wmax;
+    c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
+    c.d_scal = static_cast<double*>(dalloc(c, 4 * sizeof(double)));
+    c.d_lpart = static_cast<double*>(dalloc(c, 2 * 512 * sizeof(double)));
+    c.d_nonfinite = static_cast<int32_t*>(dalloc(c, 16));
+    c.d_hostw = static_cast<float*>(dalloc(c, 2 * wlog * sizeof(float)));
+    c.hostw_n = wlog;
+
+    if (c.timing) {
+        c.ev.resize(256);
+        c.ev_phase.assign(128, 0);
+        for (auto& e : c.ev) BNS_CUDA(cudaEventCreate(&e));
+    }
+    c.times.assign(BNS_NUM_PHASES, 0.0);
+    c.recv_off.assign(m + 1, 0);
+    c.send_off.assign(m + 1, 0);
+    BNS_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// ---------------------------------------------------------------------------------------------
+// bns_sample_boundary: a1-a3
+// ---------------------------------------------------------------------------------------------
+void sample_boundary(Ctx& c, double p, uint64_t seed, uint64_t epoch) {
+    const int m = c.cfg.world;
+    const uint64_t T = (uint64_t)std::floor(p * 4294967296.0);
+    c.p = p;
+    c.inv_p = p > 0.0 ? 1.0 / p : 0.0;
+    c.sampled = false;
+    {
+        PhaseTimer t(c, BNS_PH_SAMPLE);
+        launch_sample(c, T, seed, epoch);
+    }
+    const bool has_bd = c.plan.n_bd > 0;
+    c.fwd_mode = (!has_bd || T >= (1ull << 32)) ? 0 : (T == 0 ? 1 : 2);
+    {
+        PhaseTimer t(c, BNS_PH_INDUCE);
+        if (c.fwd_mode == 2) launch_induce(c);
+        launch_bwd_segments(c);
+        if (c.layer == BNS_LAYER_GCN) launch_gcn_cscale(c);
+    }
+    const int64_t nslot = 2 * m + 1 + 8;
+    BNS_CUDA(cudaMemcpyAsync(c.h_seg_pos, c.d_seg_pos, nslot * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    BNS_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t* sp = c.h_seg_pos;
+    for (int j = 0; j <= m; ++j) c.recv_off[j] = sp[j] - sp[0];
+    for (int j = 0; j <= m; ++j) c.send_off[j] = sp[m + j] - sp[m];
+    c.n_halo = c.recv_off[m];
+    c.n_sent = c.send_off[m];
+    const int64_t* tot = sp + 2 * m + 1;
+    if (c.fwd_mode == 0) { c.nnz_kept = c.nnz_i; c.n_seg_fwd = c.n_seg_static_fwd; }
+    else if (c.fwd_mode == 1) { c.nnz_kept = c.ii_nnz; c.n_seg_fwd = c.n_seg_bwd_inner; }
+    else { c.nnz_kept = tot[0]; c.n_seg_fwd = tot[1]; }
+    c.n_seg_bwd = c.n_seg_bwd_inner + (has_bd ? tot[2] : 0);
+    if (c.n_halo > c.halo_cap)
+        throw Error(BNS_ERR_OOM, "sampled halo (" + std::to_string(c.n_halo) + " rows) exceeds capacity " +
+                                     std::to_string(c.halo_cap) + " (raise cfg.max_p)");
+    if (c.debug_idx && m > 1) {
+        // R27 check: exchange the gids of S_{i,j} and compare with U_i's owner segments
+        std::vector<int32_t> sl(c.n_sent), ub(c.n_halo);
+        if (c.n_sent)
+            BNS_CUDA(cudaMemcpy(sl.data(), c.d_cand_out + c.n_halo, c.n_sent * 4, cudaMemcpyDeviceToHost));
+        if (c.n_halo) BNS_CUDA(cudaMemcpy(ub.data(), c.d_cand_out, c.n_halo * 4, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> sg(c.n_sent);
+        for (int64_t k = 0; k < c.n_sent; ++k) sg[k] = c.plan.V[sl[k]];
+        int32_t* d_s = static_cast<int32_t*>(c.d_sendbuf);
+        int32_t* d_r = static_cast<int32_t*>(c.d_gradbuf);
+        if (c.n_sent) BNS_CUDA(cudaMemcpy(d_s, sg.data(), c.n_sent * 4, cudaMemcpyHostToDevice));
+        int32_t* d_rr = static_cast<int32_t*>(c.d_dx);
+        c.tr->exchange(c, d_s, c.send_off.data(), d_rr, c.recv_off.data(), 4);
+        std::vector<int32_t> got(c.n_halo);
+        BNS_CUDA(cudaStreamSynchronize(c.stream));
+        if (c.n_halo) BNS_CUDA(cudaMemcpy(got.data(), d_rr, c.n_halo * 4, cudaMemcpyDeviceToHost));
+        for (int64_t s = 0; s < c.n_halo; ++s)
+            if (got[s] != c.plan.B[ub[s]])
+                throw Error(BNS_ERR_RUNTIME, "BNS_DEBUG_EXCHANGE_INDICES: received gid != recomputed U_i at slot " +
+                                                 std::to_string(s));
+        (void)d_r;
+    }
+    collect_times(c);
+    c.sampled = true;
+}
+
+// ---------------------------------------------------------------------------------------------
+// bns_epoch: a4-a14
+// ---------------------------------------------------------------------------------------------
+void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* loss, double* acc) {
+    Plan& P = c.plan;
+    const int L = c.L, m = c.cfg.world;
+    const size_t ts = tsize(c);
+    const bool sage = c.layer == BNS_LAYER_SAGE_MEAN;
+    const int64_t n_in = P.n_in;
+    const float inv_p = (float)c.inv_p;
+
+    // weights may be host or device pointers
+    cudaPointerAttributes attr{};
+    bool host_w = false;
+    if (cudaPointerGetAttributes(&attr, W_in[0]) != cudaSuccess) { cudaGetLastError(); host_w = true; }
+    else host_w = (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged);
+    std::vector<float*> W(L), G(L);
+    std::vector<int64_t> wl(L);
+    int64_t off = 0;
+    for (int l = 0; l < L; ++l) {
+        wl[l] = (sage ? 2 : 1) * (int64_t)c.dims[l] * c.dims[l + 1];
+        if (host_w) {
+            W[l] = c.d_hostw + off;
+            G[l] = c.d_hostw + c.hostw_n + off;
+            BNS_CUDA(cudaMemcpyAsync(W[l], W_in[l], wl[l] * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+        } else {
+            W[l] = W_in[l];
+            G[l] = G_in ? G_in[l] : nullptr;
+        }
+        off += wl[l];
+    }
+    {
+        PhaseTimer t(c, BNS_PH_UPDATE);
+        for (int l = 0; l < L; ++l) launch_wpack(c, W[l], l, false);
+    }
+    const Seg* fsegs = c.fwd_mode == 0 ? c.d_seg_static_fwd : (c.fwd_mode == 1 ? c.d_seg_bwd : c.d_seg_fwd);
+    const int32_t* fcol = c.fwd_mode == 0 ? c.d_static_col : (c.fwd_mode == 1 ? c.d_tcol : c.d_ind_col);
+    const int32_t* S_local = c.d_cand_out + c.n_halo;
+
+    // ------------------------------ forward (Alg.1 l.8-10) ------------------------------
+    for (int l = 1; l <= L; ++l) {
+        const int64_t din = c.dp[l - 1], dout = c.dp[l];
+        void* Hin = c.H[l - 1];
+        if (m > 1) {
+            {
+                PhaseTimer t(c, BNS_PH_PACK);
+                launch_pack_rows(c, Hin, din, S_local, c.n_sent, c.d_sendbuf, (int32_t)din);
+            }
+            PhaseTimer t(c, BNS_PH_EXCHANGE);
+            c.tr->exchange(c, c.d_sendbuf, c.send_off.data(), static_cast<char*>(Hin) + n_in * din * ts,
+                           c.recv_off.data(), din * ts);
+        }
+        {
+            PhaseTimer t(c, BNS_PH_SPMM_FWD);
+            SpmmArgs a{};
+            a.mode = sage ? SAGE_FWD : GCN_FWD;
+            a.segs = fsegs;
+            a.n_segs = c.n_seg_fwd;
+            a.col = fcol;
+            a.src = Hin;
+            a.ld_src = din;
+            a.out = c.Z[l];
+            a.ld_out = din;
+            a.d = (int32_t)din;
+            a.n_in = n_in;
+            a.inv_p = inv_p;
+            a.rowscale = sage ? c.d_deg_in : c.d_rs_in;
+            a.cscale = c.d_cscale;
+            a.partial = c.d_partial;
+            launch_spmm(c, a);
+        }
+        {
+            PhaseTimer t(c, BNS_PH_GEMM_FWD);
+            const bool last = (l == L);
+            void* out = last ? (void*)c.d_logits : c.H[l];
+            if (sage)
+                gemm_fwd(c, n_in, dout, c.Z[l], din, din, Hin, din, din, c.Wt[l - 1], dout, out, dout, !last, last);
+            else
+                gemm_fwd(c, n_in, dout, c.Z[l], din, din, nullptr, 0, din, c.Wt[l - 1], dout, out, dout, !last, last);
+        }
+    }
+    // ------------------------------ loss (l.11) ------------------------------
+    {
+        PhaseTimer t(c, BNS_PH_LOSS);
+        launch_xent(c, c.d_logits, c.dp[L], c.dims[L], c.d_dlogits, c.d_dpre);
+    }
+    // ------------------------------ backward (l.12) ------------------------------
+    for (int l = L; l >= 1; --l) {
+        const int64_t din = c.dp[l - 1], dout = c.dp[l];
+        void* Hin = c.H[l - 1];
+        if (l < L) {
+            PhaseTimer t(c, BNS_PH_GEMM_BWD);
+            if (c.retain)
+                BNS_CUDA(cudaMemcpyAsync(c.dH_keep[l], c.d_dx, n_in * dout * ts, cudaMemcpyDeviceToDevice, c.stream));
+            launch_relu_mask(c, c.d_dx, c.H[l], dout, n_in, (int32_t)dout, c.d_dpre);
+        }
+        {
+            PhaseTimer t(c, BNS_PH_GEMM_BWD);
+            float* g = c.d_gflat + c.goff[l - 1];
+            gemm_wgrad(c, n_in, din, dout, c.Z[l], din, c.d_dpre, dout, g, dout);
+            if (sage) gemm_wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
+            if (l > 1) {
+                if (sage)
+                    gemm_dx(c, n_in, 2 * din, dout, c.d_dpre, dout, c.Wt[l - 1], dout, c.d_dxcat, 2 * din, c.d_deg_in,
+                            din);
+                else
+                    gemm_dx(c, n_in, din, dout, c.d_dpre, dout, c.Wt[l - 1], dout, c.d_dxcat, din, c.d_rs_in, din);
+            }
+        }
+        if (l == 1) break;   // R29: no gradient w.r.t. the input features
+        {
+            PhaseTimer t(c, BNS_PH_SPMM_BWD);
+            SpmmArgs a{};
+            a.mode = sage ? SAGE_BWD : GCN_BWD;
+            a.segs = c.d_seg_bwd;
+            a.n_segs = c.n_seg_bwd;
+            a.col = c.d_tcol;
+            a.src = c.d_dxcat;
+            a.ld_src = sage ? 2 * din : din;
+            a.out = c.d_dx;
+            a.ld_out = din;
+            a.self = static_cast<char*>(c.d_dxcat) + din * ts;
+            a.ld_self = 2 * din;
+            a.d = (int32_t)din;
+            a.n_in = n_in;
+            a.inv_p = inv_p;
+            a.cscale = c.d_cscale;
+            a.partial = c.d_partial;
+            launch_spmm(c, a);
+        }
+        if (m > 1) {
+            {
+                PhaseTimer t(c, BNS_PH_EXCHANGE_BWD);
+                c.tr->exchange(c, static_cast<char*>(c.d_dx) + n_in * din * ts, c.recv_off.data(), c.d_gradbuf,
+                               c.send_off.data(), din * ts);
+            }
+            PhaseTimer t(c, BNS_PH_SCATTER);
+            for (int j = 0; j < m; ++j) {   // R25: local contribution first, then peers ascending
+                if (j == c.cfg.rank) continue;
+                const int64_t n = c.send_off[j + 1] - c.send_off[j];
+                launch_scatter_add(c, c.d_dx, din, S_local + c.send_off[j],
+                                   static_cast<char*>(c.d_gradbuf) + c.send_off[j] * din * ts, n, (int32_t)din);
+            }
+        }
+    }
+    // ------------------------------ AllReduce (l.13) + update (l.14) ------------------------------
+    if (m > 1) {
+        PhaseTimer t(c, BNS_PH_ALLREDUCE);
+        c.tr->allreduce(c, c.d_gflat, c.gflat_n, c.d_scal, 2);
+    }
+    {
+        PhaseTimer t(c, BNS_PH_UPDATE);
+        launch_sgd(c, W.data(), host_w ? G.data() : (G_in ? G.data() : nullptr), lr);
+    }
+    double scal[2];
+    int32_t nonfinite = 0;
+    BNS_CUDA(cudaMemcpyAsync(scal, c.d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c.stream));
+    BNS_CUDA(cudaMemcpyAsync(&nonfinite, c.d_nonfinite, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+    if (host_w) {
+        for (int l = 0; l < L; ++l) {
+            BNS_CUDA(cudaMemcpyAsync(W_in[l], W[l], wl[l] * sizeof(float), cudaMemcpyDeviceToHost, c.stream));
+            if (G_in && G_in[l])
+                BNS_CUDA(cudaMemcpyAsync(G_in[l], G[l], wl[l] * sizeof(float), cudaMemcpyDeviceToHost, c.stream));
+        }
+    }
+    BNS_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.tr) c.tr->poll(c);
+    collect_times(c);
+    const double ntr = (double)c.n_train_global;
+    if (loss) *loss = ntr > 0 ? scal[0] / ntr : 0.0;
+    if (acc) *acc = ntr > 0 ? scal[1] / ntr : 0.0;
+    if (nonfinite) throw Error(BNS_ERR_NONFINITE, "loss is not finite; weights left unchanged");
+}
+
+// device tensor (storage type, padded ld) -> host fp32 logical
+void fetch_rows(Ctx& c, const void* dptr, int64_t rows, int64_t ld, int64_t dlog, bool is_f32, float* out) {
+    const size_t es = is_f32 ? 4 : tsize(c);
+    std::vector<uint8_t> buf((size_t)rows * ld * es);
+    if (!buf.empty()) BNS_CUDA(cudaMemcpy(buf.data(), dptr, buf.size(), cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < rows; ++r)
+        for (int64_t k = 0; k < dlog; ++k) {
+            const size_t i = (size_t)(r * ld + k);
+            if (es == 4) {
+                std::memcpy(&out[r * dlog + k], &buf[i * 4], 4);
+            } else {
+                uint16_t h;
+                std::memcpy(&h, &buf[i * 2], 2);
+                uint32_t u = (uint32_t)h << 16;
+                std::memcpy(&out[r * dlog + k], &u, 4);
+            }
+        }
+}
+
+}  // namespace
+}  // namespace bns
+
+using namespace bns;
+
+extern "C" {
+
+bns_status bns_setup(const bns_config* cfg, int64_t num_nodes, const int64_t* indptr, const int32_t* indices,
+                     const int32_t* part_of, const float* features, const int32_t* labels, bns_ctx** out) {
+    if (!out) return BNS_ERR_INVALID;
+    *out = nullptr;
+    std::unique_ptr<bns_ctx> h(new bns_ctx());
+    bns_status st = guard(nullptr, [&] {
+        validate(cfg, num_nodes, indptr, indices, part_of);
+        Ctx& c = h->c;
+        c.cfg = *cfg;
+        c.cfg.dims = nullptr;
+        c.L = cfg->num_layers;
+        c.dims.assign(cfg->dims, cfg->dims + c.L + 1);
+        c.dp.resize(c.L + 1);
+        for (int l = 0; l <= c.L; ++l) c.dp[l] = (int32_t)pad8(c.dims[l]);
+        c.layer = cfg->layer;
+        c.prec = cfg->precision;
+        c.plan_only = (cfg->flags & BNS_PLAN_ONLY) != 0;
+        c.timing = (cfg->flags & BNS_TIMING) != 0;
+        c.debug_idx = (cfg->flags & BNS_DEBUG_EXCHANGE_INDICES) != 0;
+        c.retain = (cfg->flags & BNS_RETAIN_GRADS) != 0;
+        build_plan(c.plan, cfg->rank, cfg->world, num_nodes, indptr, indices, part_of);
+        const int64_t n_in = c.plan.n_in;
+        if (n_in > 0 && (!features || !labels)) throw Error(BNS_ERR_INVALID, "features/labels NULL");
+        int64_t ntr = 0;
+        for (int64_t r = 0; r < n_in; ++r) {
+            if (labels[r] < -1 || labels[r] >= c.dims[c.L])
+                throw Error(BNS_ERR_INVALID, "label out of range at inner row " + std::to_string(r));
+            ntr += labels[r] >= 0;
+        }
+        c.n_train_local = ntr;
+        if (c.plan_only) return;
+        setup_device(c, features, labels);
+        c.tr = make_transport(c);
+        c.n_train_global = c.tr ? c.tr->allreduce_host_i64(c, ntr) : ntr;
+    });
+    if (st != BNS_OK) {
+        if (h->c.tr) { delete h->c.tr; h->c.tr = nullptr; }
+        for (void* p : h->c.allocs) cudaFree(p);
+        h->c.allocs.clear();
+        return st;
+    }
+    *out = h.release();
+    return BNS_OK;
+}
+
+bns_status bns_sample_boundary(bns_ctx* h, double p, uint64_t seed, uint64_t epoch) {
+    if (!h) return BNS_ERR_INVALID;
+    Ctx& c = h->c;
+    if (c.failed || c.plan_only) return BNS_ERR_STATE;
+    if (!(p >= 0.0 && p <= 1.0)) { c.err = "p must be in [0, 1]"; return BNS_ERR_INVALID; }
+    if (c.cfg.max_p > 0.0 && c.cfg.max_p < 1.0 && p > c.cfg.max_p) {
+        c.err = "p > cfg.max_p (halo buffers are sized for max_p)";
+        return BNS_ERR_OOM;
+    }
+    return guard(h, [&] {
+        BNS_CUDA(cudaSetDevice(c.cfg.device));
+        sample_boundary(c, p, seed, epoch);
+    });
+}
+
+bns_status bns_epoch(bns_ctx* h, float* const* weights, float lr, float* const* grads, double* loss, double* acc) {
+    if (!h) return BNS_ERR_INVALID;
+    Ctx& c = h->c;
+    if (c.failed || c.plan_only) return BNS_ERR_STATE;
+    if (!c.sampled) { c.err = "bns_epoch before bns_sample_boundary"; return BNS_ERR_STATE; }
+    if (!weights) { c.err = "weights is NULL"; return BNS_ERR_INVALID; }
+    for (int l = 0; l < c.L; ++l)
+        if (!weights[l]) { c.err = "weights[l] is NULL"; return BNS_ERR_INVALID; }
+    return guard(h, [&] {
+        BNS_CUDA(cudaSetDevice(c.cfg.device));
+        PhaseTimer t(c, BNS_PH_EPOCH_TOTAL);
+        epoch(c, weights, lr, grads, loss, acc);
+    });
+}
+
+bns_status bns_query(bns_ctx* h, int32_t what, int32_t layer, void* dst, int64_t cap, int64_t* written) {
+    if (!h) return BNS_ERR_INVALID;
+    Ctx& c = h->c;
+    return guard(h, [&] {
+        const Plan& P = c.plan;
+        const int m = c.cfg.world, L = c.L;
+        std::vector<uint8_t> out;
+        auto put = [&](const void* p, size_t n) {
+            size_t o = out.size();
+            out.resize(o + n);
+            if (n) std::memcpy(out.data() + o, p, n);
+        };
+        auto need_dev = [&] {
+            if (c.plan_only) throw Error(BNS_ERR_STATE, "query needs device state (context is BNS_PLAN_ONLY)");
+        };
+        auto need_sample = [&] {
+            need_dev();
+            if (!c.sampled) throw Error(BNS_ERR_STATE, "query needs a bns_sample_boundary first");
+        };
+        auto rows_f32 = [&](const void* d, int64_t rows, int64_t ld, int64_t dl, bool f32) {
+            std::vector<float> t((size_t)rows * dl);
+            fetch_rows(c, d, rows, ld, dl, f32, t.data());
+            put(t.data(), t.size() * 4);
+        };
+        auto vec32 = [&](const int32_t* d, int64_t n) {
+            std::vector<int32_t> t(n);
+            if (n) BNS_CUDA(cudaMemcpy(t.data(), d, n * 4, cudaMemcpyDeviceToHost));
+            return t;
+        };
+        switch (what) {
+            case BNS_Q_COUNTS: {
+                std::vector<int64_t> v = {P.n_in, P.n_bd, c.n_halo, c.n_sent, (int64_t)P.col_enc.size(), c.nnz_kept};
+                for (int j = 0; j < m; ++j) v.push_back(c.recv_off[j + 1] - c.recv_off[j]);
+                for (int j = 0; j < m; ++j) v.push_back(c.send_off[j + 1] - c.send_off[j]);
+                put(v.data(), v.size() * 8);
+                break;
+            }
+            case BNS_Q_INNER: put(P.V.data(), P.V.size() * 4); break;
+            case BNS_Q_BOUNDARY: put(P.B.data(), P.B.size() * 4); break;
+            case BNS_Q_BOUNDARY_OFF: put(P.B_off.data(), P.B_off.size() * 8); break;
+            case BNS_Q_SENDCAND: {
+                std::vector<int32_t> g(P.D_local.size());
+                for (size_t k = 0; k < g.size(); ++k) g[k] = P.V[P.D_local[k]];
+                put(g.data(), g.size() * 4);
+                break;
+            }
+            case BNS_Q_SENDCAND_OFF: put(P.D_off.data(), P.D_off.size() * 8); break;
+            case BNS_Q_STATIC_CSR:
+                put(P.row_ptr.data(), P.row_ptr.size() * 8);
+                put(P.col_enc.data(), P.col_enc.size() * 4);
+                break;
+            case BNS_Q_MASK: {
+                need_sample();
+                std::vector<uint8_t> f(P.n_bd);
+                if (P.n_bd) BNS_CUDA(cudaMemcpy(f.data(), c.d_flags, P.n_bd, cudaMemcpyDeviceToHost));
+                put(f.data(), f.size());
+                break;
+            }
+            case BNS_Q_HALO: {
+                need_sample();
+                std::vector<int32_t> ub = vec32(c.d_cand_out, c.n_halo);
+                for (auto& x : ub) x = P.B[x];
+                put(ub.data(), ub.size() * 4);
+                break;
+            }
+            case BNS_Q_HALO_OFF: need_sample(); put(c.recv_off.data(), (m + 1) * 8); break;
+            case BNS_Q_SEND: {
+                need_sample();
+                std::vector<int32_t> s = vec32(c.d_cand_out + c.n_halo, c.n_sent);
+                for (auto& x : s) x = P.V[x];
+                put(s.data(), s.size() * 4);
+                break;
+            }
+            case BNS_Q_SEND_OFF: need_sample(); put(c.send_off.data(), (m + 1) * 8); break;
+            case BNS_Q_H: {
+                need_sample();
+                if (layer < 0 || layer > L) throw Error(BNS_ERR_INVALID, "layer out of range");
+                if (layer == L) rows_f32(c.d_logits, P.n_in, c.dp[L], c.dims[L], true);
+                else rows_f32(c.H[layer], P.n_in, c.dp[layer], c.dims[layer], false);
+                break;
+            }
+            case BNS_Q_Z: {
+                need_sample();
+                if (layer < 1 || layer > L) throw Error(BNS_ERR_INVALID, "layer out of range");
+                rows_f32(c.Z[layer], P.n_in, c.dp[layer - 1], c.dims[layer - 1], false);
+                break;
+            }
+            case BNS_Q_DH: {
+                need_sample();
+                if (layer < 1 || layer > L) throw Error(BNS_ERR_INVALID, "layer out of range");
+                if (layer == L) rows_f32(c.d_dlogits, P.n_in, c.dp[L], c.dims[L], true);
+                else {
+                    if (!c.retain) throw Error(BNS_ERR_STATE, "BNS_Q_DH for l < L needs BNS_RETAIN_GRADS");
+                    rows_f32(c.dH_keep[layer], P.n_in, c.dp[layer], c.dims[layer], false);
+                }
+                break;
+            }
+            case BNS_Q_HALO_ROWS: {
+                need_sample();
+                if (layer < 1 || layer > L) throw Error(BNS_ERR_INVALID, "layer out of range");
+                const size_t ts = tsize(c);
+                rows_f32(static_cast<const char*>(c.H[layer - 1]) + P.n_in * c.dp[layer - 1] * ts, c.n_halo,
+                         c.dp[layer - 1], c.dims[layer - 1], false);
+                break;
+            }
+            case BNS_Q_INDUCED: {
+                need_sample();
+                std::vector<int64_t> ptr(P.n_in + 1);
+                std::vector<int32_t> col;
+                if (c.fwd_mode == 2) {
+                    BNS_CUDA(cudaMemcpy(ptr.data(), c.d_ind_ptr, (P.n_in + 1) * 8, cudaMemcpyDeviceToHost));
+                    col = vec32(c.d_ind_col, ptr[P.n_in]);
+                } else if (c.fwd_mode == 0) {
+                    ptr = P.row_ptr;
+                    col = vec32(c.d_static_col, (int64_t)P.col_enc.size());
+                } else {
+                    ptr = P.ii_ptr;
+                    col = P.ii_col;
+                }
+                put(ptr.data(), ptr.size() * 8);
+                put(col.data(), col.size() * 4);
+                break;
+            }
+            case BNS_Q_TIMES: put(c.times.data(), c.times.size() * 8); break;
+            case BNS_Q_MEMORY: {
+                size_t fr = 0, tot = 0;
+                if (!c.plan_only) cudaMemGetInfo(&fr, &tot);
+                int64_t v[2] = {c.dev_bytes, (int64_t)(tot - fr)};
+                put(v, 16);
+                break;
+            }
+            case BNS_Q_KERNEL_COUNT: put(&c.kernels, 8); break;
+            default: throw Error(BNS_ERR_INVALID, "unknown query");
+        }
+        if (written) *written = (int64_t)out.size();
+        if (dst && cap > 0) std::memcpy(dst, out.data(), std::min<size_t>(out.size(), (size_t)cap));
+    });
+}
+
+void* bns_stream(const bns_ctx* h) { return h ? (void*)h->c.stream : nullptr; }
+
+const char* bns_last_error(const bns_ctx* h) { return h ? h->c.err.c_str() : g_err.c_str(); }
+
+void bns_destroy(bns_ctx* h) {
+    if (!h) return;
+    Ctx& c = h->c;
+    if (!c.plan_only) {
+        cudaSetDevice(c.cfg.device);
+        if (c.stream) cudaStreamSynchronize(c.stream);
+    }
+    delete c.tr;
+    for (void* p : c.allocs) cudaFree(p);
+    if (c.h_seg_pos) cudaFreeHost(c.h_seg_pos);
+    for (auto& e : c.ev) cudaEventDestroy(e);
+    if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
+    delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,167 @@
+// common.h -- internal declarations shared by the libbns translation units (host side).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <stdexcept>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "bns.h"
+
+namespace bns {
+
+struct Error : std::runtime_error {
+    bns_status code;
+    Error(bns_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define BNS_CUDA(x)                                                                                  \
+    do {                                                                                             \
+        cudaError_t e__ = (x);                                                                       \
+        if (e__ != cudaSuccess)                                                                      \
+            throw ::bns::Error(BNS_ERR_RUNTIME, std::string(#x) + ": " + cudaGetErrorString(e__) +   \
+                                                    " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
+    } while (0)
+
+#define BNS_CHECK_LAUNCH() BNS_CUDA(cudaGetLastError())
+
+constexpr int kSeg = 512;          // SpMM segment length in edges (hub rows are split into segments of this size)
+constexpr int kPad = 8;            // feature dims padded to multiples of 8 (16-byte rows for fp32x4 / bf16x8)
+
+inline int64_t pad8(int64_t d) { return (d + kPad - 1) / kPad * kPad; }
+
+// ----------------------------------------------------------------------------------------------
+// Host plan (a0): PAPER.md:173-176 -- inner set V_i, boundary set B_i, send candidates D_{i->j}.
+// ----------------------------------------------------------------------------------------------
+struct Plan {
+    int rank = 0, world = 1;
+    int64_t N = 0;
+    int64_t n_in = 0, n_bd = 0, n_send = 0;   // |V_i|, |B_i|, Σ_j |D_{i->j}|
+    std::vector<int32_t> V;                   // inner gids, ascending
+    std::vector<int32_t> B;                   // boundary gids, (owner, gid)
+    std::vector<int64_t> B_off;               // [m+1]
+    std::vector<int32_t> D_local;             // send candidates as local inner rows, per peer j ascending gid
+    std::vector<int64_t> D_off;               // [m+1]
+    std::vector<int64_t> row_ptr;             // static CSR over inner rows (full rows, global order)
+    std::vector<int32_t> col_enc;             // >= 0: inner local id;  < 0: -(b+1) boundary index
+    std::vector<int64_t> ii_ptr;              // inner-only part (A_II), local ids
+    std::vector<int32_t> ii_col;
+    std::vector<int64_t> br_ptr;              // boundary rows: inner neighbours of each b (local ids ascending)
+    std::vector<int32_t> br_col;
+    std::vector<float> deg_in, deg_bd;        // full-graph degrees deg_G
+};
+
+void build_plan(Plan& P, int rank, int world, int64_t N, const int64_t* indptr, const int32_t* indices,
+                const int32_t* part_of);
+
+// ----------------------------------------------------------------------------------------------
+// Segments: a warp-sized unit of SpMM work -- out_row, edge range [e0, e1), and for hub rows split into
+// several segments, the index of the first segment of the row and the number of segments (nseg > 1 ->
+// partial sums go through a deterministic in-order fixup).
+// ----------------------------------------------------------------------------------------------
+struct Seg {
+    int32_t row;
+    int32_t nseg;       // segments of this row
+    int64_t e0, e1;
+    int64_t first;      // index of the row's first segment
+};
+
+struct Transport;
+
+struct Ctx {
+    bns_config cfg{};
+    std::vector<int32_t> dims, dp;            // logical, padded (L+1)
+    int L = 1;
+    int layer = 0, prec = 0;
+    bool plan_only = false, timing = false, debug_idx = false, retain = false;
+    int fwd_mode = 0;                         // 0 static full CSR (p=1 / no boundary), 1 A_II only (p=0), 2 induced
+    size_t ev_used = 0;
+    std::vector<int> ev_phase;
+    int64_t hostw_n = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    bool failed = false;
+    bool sampled = false;
+    Plan plan;
+    Transport* tr = nullptr;
+    int64_t halo_cap = 0;
+    int64_t nnz_i = 0;
+    int64_t kernels = 0;
+    int64_t dev_bytes = 0;
+    std::vector<void*> allocs;
+    std::vector<double> times;
+    std::vector<cudaEvent_t> ev;              // timing events, 2 per phase slot
+    // --- per-epoch host copies of counts
+    double p = 1.0, inv_p = 1.0;
+    int64_t n_halo = 0, n_sent = 0, nnz_kept = 0;
+    int64_t n_seg_fwd = 0, n_seg_bwd = 0;
+    std::vector<int64_t> recv_off, send_off;  // [m+1] rows
+    // --- device plan
+    int64_t* d_row_ptr = nullptr;  int32_t* d_col_enc = nullptr;
+    int32_t* d_cand_gid = nullptr; int32_t* d_cand_key = nullptr; int32_t* d_cand_payload = nullptr;
+    int64_t n_cand = 0;
+    int64_t* d_cand_seg = nullptr; // [2m+1] candidate segment offsets
+    int32_t* d_br_len = nullptr;   // boundary-row lengths
+    int64_t* d_br_ptr = nullptr;
+    int32_t* d_tcol = nullptr;     // [ii_col ; br_col] columns of the transposed aggregation
+    int64_t ii_nnz = 0;
+    float* d_deg_in = nullptr;     // deg_G(v), inner
+    float* d_rs_in = nullptr;      // 1/sqrt(deg+1), inner
+    float* d_rs_bd = nullptr;      // 1/sqrt(deg+1), boundary
+    int32_t* d_labels = nullptr;
+    // --- per-epoch device
+    uint8_t* d_flags = nullptr;    // keep flag per candidate
+    int32_t* d_blk = nullptr;      // per-block counts / offsets for compaction
+    int32_t* d_cand_out = nullptr; // compacted payloads: [U_b (|U|) ; S_local (ΣS)]
+    int32_t* d_slot_of_b = nullptr;
+    int64_t* d_seg_pos = nullptr;  // [2m+1] compacted segment offsets
+    int64_t* h_seg_pos = nullptr;  // pinned host copy
+    int64_t* d_ind_ptr = nullptr;  // induced CSR (n_in+1)
+    int32_t* d_ind_col = nullptr;
+    int32_t* d_row_cnt = nullptr;  // scratch per row counts
+    int32_t* d_row_nseg = nullptr;
+    int64_t* d_row_off = nullptr;  // scratch scans
+    int64_t* d_row_soff = nullptr;
+    int64_t* d_scan_tmp = nullptr;
+    Seg* d_seg_fwd = nullptr;  int64_t seg_fwd_cap = 0;
+    Seg* d_seg_bwd = nullptr;  int64_t seg_bwd_cap = 0;
+    Seg* d_seg_static_fwd = nullptr; int64_t n_seg_static_fwd = 0;  // p = 1 / no boundary: static induced CSR
+    int32_t* d_static_col = nullptr; int64_t* d_static_ptr = nullptr;
+    int64_t n_seg_bwd_inner = 0;
+    float* d_partial = nullptr;    // hub-row partial sums
+    float* d_cscale = nullptr;     // per-column scale (GCN forward)
+    // --- activations (storage type T: float or bf16)
+    std::vector<void*> H;          // H[l], l = 0..L-1: (n_in + halo_cap) x dp[l]
+    std::vector<void*> Z;          // Z[l], l = 1..L: n_in x dp[l-1]
+    float* d_logits = nullptr;     // n_in x dp[L]
+    float* d_dlogits = nullptr;
+    void* d_dpre = nullptr;        // n_in x maxd (T)
+    void* d_dxcat = nullptr;       // n_in x 2 maxd (T) : [dZ' | dXself]
+    void* d_dx = nullptr;          // (n_in + halo_cap) x maxd (T)
+    void* d_dh = nullptr;          // n_in x maxd (T): gradient w.r.t. H^(l) inner rows (after accumulation)
+    std::vector<void*> dH_keep;    // debug copies of dH^l (fp32) per layer (only if retained)
+    void* d_sendbuf = nullptr;     // n_send x maxd (T)
+    void* d_gradbuf = nullptr;     // n_send x maxd (T)
+    int32_t maxd = 0;
+    // --- weights
+    std::vector<float*> Wpad;      // fp32 padded weights per layer
+    std::vector<void*> Wt;         // storage-type copy (bf16 in BNS_BF16; == Wpad in FP32)
+    std::vector<int64_t> wrows, wcols;   // padded shape per layer
+    float* d_gflat = nullptr;      // all-reduce buffer: Σ_l padded dW (fp32)
+    int64_t gflat_n = 0;
+    std::vector<int64_t> goff;     // per-layer offset in gflat
+    float* d_splitk = nullptr;     // split-K partials
+    int64_t splitk_cap = 0;
+    double* d_scal = nullptr;      // [loss_sum, correct] (all-reduced)
+    double* d_lpart = nullptr;     // per-block loss partials
+    int32_t* d_nonfinite = nullptr;
+    float* d_hostw = nullptr;      // staging for host-pointer weights (flat)
+    int64_t n_train_global = 0;
+    int64_t n_train_local = 0;
+};
+
+// kernel launchers (kernels.cu / gemm.cu)
+struct Launch;
+
+}  // namespace bns

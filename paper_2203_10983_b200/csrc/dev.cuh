@@ -1,0 +1,65 @@
+// dev.cuh -- device helpers shared by the kernels (16-byte vector rows of fp32 or bf16).
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace bns {
+
+// A 16-byte vector of the storage type: 4 x fp32 or 8 x bf16.
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+    static constexpr int N = 4;
+    using raw = float4;
+    __device__ __forceinline__ static void add_scaled(float* acc, const raw& v, float s) {
+        acc[0] = fmaf(s, v.x, acc[0]); acc[1] = fmaf(s, v.y, acc[1]);
+        acc[2] = fmaf(s, v.z, acc[2]); acc[3] = fmaf(s, v.w, acc[3]);
+    }
+    __device__ __forceinline__ static void to_float(const raw& v, float* f) { f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w; }
+    __device__ __forceinline__ static raw from_float(const float* f) { return make_float4(f[0], f[1], f[2], f[3]); }
+};
+template <> struct Vec<__nv_bfloat16> {
+    static constexpr int N = 8;
+    using raw = uint4;
+    __device__ __forceinline__ static void add_scaled(float* acc, const raw& v, float s) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float lo = __uint_as_float(w[k] << 16), hi = __uint_as_float(w[k] & 0xffff0000u);
+            acc[2 * k] = fmaf(s, lo, acc[2 * k]);
+            acc[2 * k + 1] = fmaf(s, hi, acc[2 * k + 1]);
+        }
+    }
+    __device__ __forceinline__ static void to_float(const raw& v, float* f) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { f[2 * k] = __uint_as_float(w[k] << 16); f[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u); }
+    }
+    __device__ __forceinline__ static raw from_float(const float* f) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * k], f[2 * k + 1]);
+            w[k] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    }
+};
+
+template <typename T> __device__ __forceinline__ float to_f(T x);
+template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
+template <typename R> __device__ __forceinline__ R ldg_nc(const R* p) { return __ldg(p); }
+template <> __device__ __forceinline__ uint4 ldg_nc<uint4>(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+}  // namespace bns

@@ -1,0 +1,64 @@
+// kernels.h -- host launchers of the sm_100a kernels (implemented in *.cu).  All launches go on ctx.stream and
+// bump ctx.kernels.
+#pragma once
+#include "common.h"
+
+namespace bns {
+
+// a1 + a2: Philox Bernoulli draw over all candidates and order-preserving compaction (sample.cu)
+void launch_sample(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch);
+// a3: induced subgraph over V_i ∪ U_i + forward segments; backward (transposed) halo segments (sample.cu)
+void launch_induce(Ctx& c);
+void launch_bwd_segments(Ctx& c);
+// static segments for a static CSR (setup)
+int64_t build_static_segments(Ctx& c, const int64_t* d_ptr, int64_t rows, int64_t ptr_base, Seg* d_out);
+// exclusive scan of int32 -> int64 (n elements), total written to *d_total if non-null
+void scan_i32(Ctx& c, const int32_t* in, int64_t* out, int64_t n, int64_t* d_total);
+
+// a6 / a10: segment SpMM (spmm.cu)
+enum SpmmMode { SAGE_FWD = 0, GCN_FWD = 1, SAGE_BWD = 2, GCN_BWD = 3 };
+struct SpmmArgs {
+    int mode;
+    const Seg* segs; int64_t n_segs;
+    const int32_t* col;
+    const void* src; int64_t ld_src;      // gather source rows (elements)
+    void* out; int64_t ld_out;
+    const void* self; int64_t ld_self;    // SAGE_BWD: dXself rows (inner)
+    int32_t d;                            // padded feature width
+    int64_t n_in;
+    float inv_p;
+    const float* rowscale;                // per output row
+    const float* cscale;                  // GCN_FWD per column
+    const int32_t* halo_b;                // GCN_BWD: boundary index of halo slot
+    const float* rs_bd;                   // GCN_BWD
+    float* partial;
+};
+void launch_spmm(Ctx& c, const SpmmArgs& a);
+
+// a7 / a9: GEMMs (gemm_simt.cu; tcgen05 in gemm_tc.cu)
+// C[M x N] = [A0 | A1] (M x (K0+K1), row-major, lda0/lda1) * B (K x N row-major, ldb); epilogue ReLU or none;
+// output fp32 (out_f32) or storage type.
+void gemm_fwd(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64_t lda0, const void* A1, int64_t K1,
+              int64_t lda1, const void* B, int64_t ldb, void* C, int64_t ldc, bool relu, bool out_f32);
+// dW (K x N) = A^T (M x K, lda) * D (M x N, ldd); result fp32 written to Wg (ldw) (deterministic split-K)
+void gemm_wgrad(Ctx& c, int64_t M, int64_t K, int64_t N, const void* A, int64_t lda, const void* D, int64_t ldd,
+                float* Wg, int64_t ldw);
+// C (M x Nc) = D (M x K, ldd) * B^T where B is (Nc x K, ldb) row-major; columns [0, scale_cols) multiplied by
+// rowscale[row]; output storage type
+void gemm_dx(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t ldd, const void* B, int64_t ldb,
+             void* C, int64_t ldc, const float* rowscale, int64_t scale_cols);
+
+// misc (misc.cu)
+void launch_pack_rows(Ctx& c, const void* src, int64_t ld_src, const int32_t* idx, int64_t n, void* dst, int32_t d);
+void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, const void* src, int64_t n, int32_t d);
+void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t);
+void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre);
+void launch_wpack(Ctx& c, const float* W, int l, bool host_src);
+void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr);
+void launch_sum_ptrs(Ctx& c, const float* const* d_ptrs, int nptr, float* out, int64_t n);
+void launch_sum_ptrs_d(Ctx& c, const double* const* d_ptrs, int nptr, double* out, int64_t n);
+void launch_fill_rowscale_bwd(Ctx& c, float* rs);
+void launch_gcn_cscale(Ctx& c);
+void launch_to_storage(Ctx& c, const float* src, int64_t rows, int32_t dlog, int64_t ld_src, void* dst, int64_t ld_dst);
+
+}  // namespace bns

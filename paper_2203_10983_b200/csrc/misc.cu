@@ -1,0 +1,317 @@
+// misc.cu -- bandwidth-bound helpers on the hot path:
+//   a4  pack        sendbuf_j[r] = H[S_{i,j}[r]]                   (Alg.1 l.9 "Send H_{S_{i,j}}")
+//   a8  loss        softmax-CE over train-masked inner rows / N_train(global) (Alg.1 l.11; R8, R22)
+//   a9  relu mask   dPre = dH ⊙ 1[H > 0] (R12: ReLU'(0) = 0)
+//   a12 scatter-add dH[S_{i,j}[r]] += recv_j[r] for peers j ascending (R25)
+//   a14 update      W <- W - lr g (Alg.1 l.14), g copied to the caller
+//   weight pack, local all-reduce sum (rank order), GCN column scales.
+#include <cmath>
+
+#include "common.h"
+#include "dev.cuh"
+#include "kernels.h"
+
+namespace bns {
+
+// one warp per row, 16-byte vectors
+template <typename T>
+__global__ void k_pack(const T* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ idx, int64_t n,
+                       T* __restrict__ dst, int32_t d) {
+    using R = typename Vec<T>::raw;
+    const int nvec = d / Vec<T>::N;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = warp; k < n; k += nwarps) {
+        const R* s = reinterpret_cast<const R*>(src + (int64_t)idx[k] * ld_src);
+        R* o = reinterpret_cast<R*>(dst + k * (int64_t)d);
+        for (int v = lane; v < nvec; v += 32) o[v] = s[v];
+    }
+}
+
+void launch_pack_rows(Ctx& c, const void* src, int64_t ld_src, const int32_t* idx, int64_t n, void* dst, int32_t d) {
+    if (n <= 0) return;
+    unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16);
+    if (c.prec == BNS_BF16)
+        k_pack<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)src, ld_src, idx, n, (__nv_bfloat16*)dst, d);
+    else
+        k_pack<float><<<grid, 256, 0, c.stream>>>((const float*)src, ld_src, idx, n, (float*)dst, d);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+template <typename T>
+__global__ void k_scatter_add(T* __restrict__ dst, int64_t ld_dst, const int32_t* __restrict__ idx,
+                              const T* __restrict__ src, int64_t n, int32_t d) {
+    using V = Vec<T>;
+    using R = typename V::raw;
+    constexpr int VN = V::N;
+    const int nvec = d / VN;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = warp; k < n; k += nwarps) {
+        R* o = reinterpret_cast<R*>(dst + (int64_t)idx[k] * ld_dst);
+        const R* s = reinterpret_cast<const R*>(src + k * (int64_t)d);
+        for (int v = lane; v < nvec; v += 32) {
+            float a[VN], b[VN];
+            V::to_float(o[v], a);
+            V::to_float(s[v], b);
+#pragma unroll
+            for (int q = 0; q < VN; ++q) a[q] += b[q];
+            o[v] = V::from_float(a);
+        }
+    }
+}
+
+void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, const void* src, int64_t n, int32_t d) {
+    if (n <= 0) return;
+    unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16);
+    if (c.prec == BNS_BF16)
+        k_scatter_add<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((__nv_bfloat16*)dst, ld_dst, idx,
+                                                                 (const __nv_bfloat16*)src, n, d);
+    else
+        k_scatter_add<float><<<grid, 256, 0, c.stream>>>((float*)dst, ld_dst, idx, (const float*)src, n, d);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------------------------
+// a8 loss: one warp per row; fixed row -> warp -> block assignment and in-order reductions (deterministic).
+// ---------------------------------------------------------------------------------------------
+constexpr int kXentBlocks = 296;
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, int64_t ld, int64_t n, int32_t C,
+                                              const int32_t* __restrict__ labels, double inv_ntr,
+                                              float* __restrict__ dlog, T* __restrict__ dpre,
+                                              double* __restrict__ part) {
+    __shared__ double s_loss[8];
+    __shared__ double s_cor[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t warp = (int64_t)blockIdx.x * 8 + w;
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    double loss = 0.0, cor = 0.0;
+    for (int64_t r = warp; r < n; r += nwarps) {
+        const float* x = logits + r * ld;
+        const int y = labels[r];
+        float* g = dlog + r * ld;
+        T* gp = dpre + r * ld;
+        if (y < 0) {
+            for (int c = lane; c < ld; c += 32) { g[c] = 0.f; gp[c] = from_f<T>(0.f); }
+            continue;
+        }
+        float mx = -INFINITY;
+        int arg = 0x7fffffff;
+        for (int c = lane; c < C; c += 32) {
+            float v = x[c];
+            if (v > mx) { mx = v; arg = c; }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            float om = __shfl_xor_sync(0xffffffffu, mx, o);
+            int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+            if (om > mx || (om == mx && oa < arg)) { mx = om; arg = oa; }
+        }
+        float se = 0.f;
+        for (int c = lane; c < C; c += 32) se += expf(x[c] - mx);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        const float lse = mx + logf(se);
+        for (int c = lane; c < ld; c += 32) {
+            float v = 0.f;
+            if (c < C) v = (float)(((double)expf(x[c] - lse) - (c == y ? 1.0 : 0.0)) * inv_ntr);
+            g[c] = v;
+            gp[c] = from_f<T>(v);
+        }
+        if (lane == 0) {
+            loss += (double)lse - (double)x[y];
+            cor += (arg == y) ? 1.0 : 0.0;
+        }
+    }
+    if (lane == 0) { s_loss[w] = loss; s_cor[w] = cor; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < 8; ++k) { a += s_loss[k]; b += s_cor[k]; }
+        part[2 * blockIdx.x] = a;
+        part[2 * blockIdx.x + 1] = b;
+    }
+}
+
+__global__ void k_xent_final(const double* __restrict__ part, int nb, double* __restrict__ scal) {
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < nb; ++k) { a += part[2 * k]; b += part[2 * k + 1]; }
+        scal[0] = a;
+        scal[1] = b;
+    }
+}
+
+void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t) {
+    const double inv = c.n_train_global > 0 ? 1.0 / (double)c.n_train_global : 0.0;
+    if (c.prec == BNS_BF16)
+        k_xent<__nv_bfloat16><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, c.plan.n_in, C, c.d_labels, inv, dlogits,
+                                                                 (__nv_bfloat16*)dpre_t, c.d_lpart);
+    else
+        k_xent<float><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, c.plan.n_in, C, c.d_labels, inv, dlogits,
+                                                         (float*)dpre_t, c.d_lpart);
+    k_xent_final<<<1, 32, 0, c.stream>>>(c.d_lpart, kXentBlocks, c.d_scal);
+    c.kernels += 2;
+    BNS_CHECK_LAUNCH();
+}
+
+template <typename T>
+__global__ void k_relu_mask(const T* __restrict__ dh, const T* __restrict__ h, int64_t ld, int64_t n,
+                            T* __restrict__ dpre) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; t < n; t += stride) dpre[t] = (to_f<T>(h[t]) > 0.f) ? dh[t] : from_f<T>(0.f);
+}
+
+void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre) {
+    const int64_t n = rows * ld;
+    if (n <= 0) return;
+    unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    if (c.prec == BNS_BF16)
+        k_relu_mask<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)dh, (const __nv_bfloat16*)h, ld,
+                                                               n, (__nv_bfloat16*)dpre);
+    else
+        k_relu_mask<float><<<grid, 256, 0, c.stream>>>((const float*)dh, (const float*)h, ld, n, (float*)dpre);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------------------------
+// weights: caller layout (logical, SAGE halves [z-rows ; h-rows]) <-> padded internal layout
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ int64_t logical_row(int64_t pr, int sage, int64_t din, int64_t dpin) {
+    if (!sage) return pr < din ? pr : -1;
+    if (pr < dpin) return pr < din ? pr : -1;
+    int64_t q = pr - dpin;
+    return q < din ? din + q : -1;
+}
+
+template <typename T>
+__global__ void k_wpack(const float* __restrict__ W, int64_t rows_p, int64_t cols_p, int64_t din, int64_t dpin,
+                        int64_t dout, int sage, float* __restrict__ Wp, T* __restrict__ Wt) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows_p * cols_p) return;
+    int64_t pr = t / cols_p, pc = t % cols_p;
+    int64_t lr = logical_row(pr, sage, din, dpin);
+    float v = (lr >= 0 && pc < dout) ? W[lr * dout + pc] : 0.f;
+    Wp[t] = v;
+    if (Wt) Wt[t] = from_f<T>(v);
+}
+
+void launch_wpack(Ctx& c, const float* W, int l, bool /*host_src*/) {
+    const int64_t rp = c.wrows[l], cp = c.wcols[l];
+    const unsigned grid = (unsigned)((rp * cp + 255) / 256);
+    const int sage = c.layer == BNS_LAYER_SAGE_MEAN;
+    if (c.prec == BNS_BF16)
+        k_wpack<__nv_bfloat16><<<grid, 256, 0, c.stream>>>(W, rp, cp, c.dims[l], c.dp[l], c.dims[l + 1], sage, c.Wpad[l],
+                                                           (__nv_bfloat16*)c.Wt[l]);
+    else
+        k_wpack<float><<<grid, 256, 0, c.stream>>>(W, rp, cp, c.dims[l], c.dp[l], c.dims[l + 1], sage, c.Wpad[l],
+                                                   nullptr);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+__global__ void k_sgd(float* __restrict__ W, float* __restrict__ G, const float* __restrict__ gpad, int64_t rows_l,
+                      int64_t dout, int64_t cols_p, int64_t din, int64_t dpin, int sage, float lr,
+                      const double* __restrict__ scal, int32_t* __restrict__ nonfinite) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows_l * dout) return;
+    const bool bad = !isfinite(scal[0]);
+    if (t == 0) *nonfinite = bad ? 1 : 0;
+    int64_t lr_ = t / dout, lc = t % dout;
+    int64_t pr = sage ? (lr_ < din ? lr_ : dpin + (lr_ - din)) : lr_;
+    float g = gpad[pr * cols_p + lc];
+    if (G) G[t] = g;
+    if (!bad) W[t] -= lr * g;
+}
+
+void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr) {
+    const int sage = c.layer == BNS_LAYER_SAGE_MEAN;
+    for (int l = 0; l < c.L; ++l) {
+        const int64_t rows_l = (sage ? 2 : 1) * (int64_t)c.dims[l], dout = c.dims[l + 1];
+        const unsigned grid = (unsigned)((rows_l * dout + 255) / 256);
+        k_sgd<<<grid, 256, 0, c.stream>>>(W[l], G ? G[l] : nullptr, c.d_gflat + c.goff[l], rows_l, dout, c.wcols[l],
+                                          c.dims[l], c.dp[l], sage, lr, c.d_scal, c.d_nonfinite);
+        c.kernels += 1;
+    }
+    BNS_CHECK_LAUNCH();
+}
+
+__global__ void k_sum_ptrs(const float* const* __restrict__ p, int np, float* __restrict__ out, int64_t n) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    float s = 0.f;
+    for (int k = 0; k < np; ++k) s += p[k][t];
+    out[t] = s;
+}
+__global__ void k_sum_ptrs_d(const double* const* __restrict__ p, int np, double* __restrict__ out, int64_t n) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double s = 0.0;
+    for (int k = 0; k < np; ++k) s += p[k][t];
+    out[t] = s;
+}
+void launch_sum_ptrs(Ctx& c, const float* const* d_ptrs, int nptr, float* out, int64_t n) {
+    if (n <= 0) return;
+    k_sum_ptrs<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(d_ptrs, nptr, out, n);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+void launch_sum_ptrs_d(Ctx& c, const double* const* d_ptrs, int nptr, double* out, int64_t n) {
+    if (n <= 0) return;
+    k_sum_ptrs_d<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(d_ptrs, nptr, out, n);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+// GCN: per-column scale of the sampled propagation [rs_in ; (1/p) rs_bd[U_b]] (App. A S diagonal)
+__global__ void k_gcn_cscale(const float* __restrict__ rs_in, int64_t n_in, const float* __restrict__ rs_bd,
+                             const int32_t* __restrict__ U_b, const int64_t* __restrict__ seg_pos, int m, float inv_p,
+                             int64_t cap, float* __restrict__ cs) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_in) { cs[t] = rs_in[t]; return; }
+    int64_t s = t - n_in;
+    if (s >= cap) return;
+    if (s < seg_pos[m] - seg_pos[0]) cs[t] = inv_p * rs_bd[U_b[s]];
+}
+
+void launch_gcn_cscale(Ctx& c) {
+    const int64_t n = c.plan.n_in + c.halo_cap;
+    if (n <= 0) return;
+    k_gcn_cscale<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.d_rs_in, c.plan.n_in, c.d_rs_bd, c.d_cand_out,
+                                                                    c.d_seg_pos, c.cfg.world, c.inv_p, c.halo_cap,
+                                                                    c.d_cscale);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+template <typename T>
+__global__ void k_to_storage(const float* __restrict__ src, int64_t rows, int32_t dlog, int64_t ld_src,
+                             T* __restrict__ dst, int64_t ld_dst) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows * ld_dst) return;
+    int64_t r = t / ld_dst, k = t % ld_dst;
+    dst[t] = from_f<T>(k < dlog ? src[r * ld_src + k] : 0.f);
+}
+
+void launch_to_storage(Ctx& c, const float* src, int64_t rows, int32_t dlog, int64_t ld_src, void* dst, int64_t ld_dst) {
+    const int64_t n = rows * ld_dst;
+    if (n <= 0) return;
+    if (c.prec == BNS_BF16)
+        k_to_storage<__nv_bfloat16><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(src, rows, dlog, ld_src,
+                                                                                      (__nv_bfloat16*)dst, ld_dst);
+    else
+        k_to_storage<float><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(src, rows, dlog, ld_src, (float*)dst,
+                                                                              ld_dst);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+}  // namespace bns

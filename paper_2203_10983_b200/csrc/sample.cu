@@ -1,0 +1,343 @@
+// sample.cu -- a1 sample, a2 compact, a3 induce (+ SpMM work segments).
+//
+// a1  Alg.1 l.4: every candidate is one independent Bernoulli(p) draw (R5, R6).  The
+//     candidates of rank i are (recv side) every u in B_i keyed by i, and (send side) every u in D_{i->j} keyed by
+//     j -- i recomputes j's draw instead of receiving the broadcast U_j (Alg.1 l.6-7, R27).
+//     keep = Philox4x32-10(ctr = {u, key, e_lo, e_hi}, key = {s_lo, s_hi}).x < floor(p 2^32)  (R7)
+// a2  order-preserving compaction (block count -> scan -> warp-ballot scatter) into U_i (owner-major, R24) and
+//     S_{i,j}; the 2m+1 segment offsets give the per-peer counts.
+// a3  Alg.1 l.5: node-induced subgraph on V_i ∪ U_i -- the static inner rows with dropped
+//     boundary columns removed (global neighbour order kept), boundary columns remapped to halo rows n_in + slot.
+#include "common.h"
+#include "dev.cuh"
+#include "kernels.h"
+
+namespace bns {
+
+// Philox4x32-10 (Salmon et al. SC'11) -- the device copy; the oracle has its own.
+__device__ __forceinline__ uint32_t philox_x(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                             uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    }
+    return c0;
+}
+
+constexpr int kSampleBlock = 1024;
+
+__global__ void __launch_bounds__(kSampleBlock) k_sample_count(const int32_t* __restrict__ gid,
+                                                               const int32_t* __restrict__ key, int64_t n,
+                                                               uint64_t T, uint32_t e_lo, uint32_t e_hi,
+                                                               uint32_t s_lo, uint32_t s_hi,
+                                                               uint8_t* __restrict__ flags, int32_t* __restrict__ blk) {
+    int64_t i = (int64_t)blockIdx.x * kSampleBlock + threadIdx.x;
+    int keep = 0;
+    if (i < n) {
+        uint32_t r = philox_x((uint32_t)gid[i], (uint32_t)key[i], e_lo, e_hi, s_lo, s_hi);
+        keep = ((uint64_t)r < T) ? 1 : 0;
+        flags[i] = (uint8_t)keep;
+    }
+    int cnt = __syncthreads_count(keep);
+    if (threadIdx.x == 0) blk[blockIdx.x] = cnt;
+}
+
+// Single-block exclusive scan of n int32 (n arbitrary) -> int64 out[0..n], out[n] = total; optional extra total.
+__global__ void __launch_bounds__(1024) k_scan_top(const int32_t* __restrict__ in, int64_t* __restrict__ out,
+                                                   int64_t n, int64_t* __restrict__ total) {
+    __shared__ int64_t warp_sums[32];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t base = 0; base < n; base += 1024) {
+        int64_t i = base + threadIdx.x;
+        int64_t v = (i < n) ? in[i] : 0;
+        int64_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int64_t s = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        int64_t excl = carry + (w ? warp_sums[w - 1] : 0) + x - v;
+        if (i < n) out[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[n] = carry;
+        if (total) *total = carry;
+    }
+}
+
+// Block-level exclusive scan (1024 elements per block), block sums to bsum.
+__global__ void __launch_bounds__(1024) k_scan_block(const int32_t* __restrict__ in, int64_t* __restrict__ out,
+                                                     int64_t n, int32_t* __restrict__ bsum) {
+    __shared__ int32_t warp_sums[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    int32_t v = (i < n) ? in[i] : 0;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int32_t s = warp_sums[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        warp_sums[lane] = s;
+    }
+    __syncthreads();
+    if (i < n) out[i] = (int64_t)((w ? warp_sums[w - 1] : 0) + x - v);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = warp_sums[31];
+}
+
+__global__ void k_scan_add(int64_t* __restrict__ out, int64_t n, const int64_t* __restrict__ boff) {
+    int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    if (i < n) out[i] += boff[blockIdx.x];
+}
+
+void scan_i32(Ctx& c, const int32_t* in, int64_t* out, int64_t n, int64_t* d_total) {
+    if (n <= 4096) {
+        k_scan_top<<<1, 1024, 0, c.stream>>>(in, out, n, d_total);
+        c.kernels += 1;
+        BNS_CHECK_LAUNCH();
+        return;
+    }
+    int64_t nb = (n + 1023) / 1024;
+    int32_t* bsum = reinterpret_cast<int32_t*>(c.d_scan_tmp);        // nb int32
+    int64_t* boff = c.d_scan_tmp + (nb + 1) / 2 + 1;                  // nb+1 int64
+    k_scan_block<<<(unsigned)nb, 1024, 0, c.stream>>>(in, out, n, bsum);
+    k_scan_top<<<1, 1024, 0, c.stream>>>(bsum, boff, nb, nullptr);
+    k_scan_add<<<(unsigned)nb, 1024, 0, c.stream>>>(out, n, boff);
+    c.kernels += 3;
+    BNS_CHECK_LAUNCH();
+    BNS_CUDA(cudaMemcpyAsync(out + n, boff + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
+    if (d_total) BNS_CUDA(cudaMemcpyAsync(d_total, boff + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
+}
+
+// a2: scatter kept candidates to their compacted position; recv candidates also publish slot_of_b.
+__global__ void __launch_bounds__(kSampleBlock) k_sample_scatter(const uint8_t* __restrict__ flags, int64_t n,
+                                                                 int64_t n_bd, const int64_t* __restrict__ boff,
+                                                                 const int32_t* __restrict__ payload,
+                                                                 const int64_t* __restrict__ cand_seg, int nseg,
+                                                                 int32_t* __restrict__ out,
+                                                                 int32_t* __restrict__ slot_of_b,
+                                                                 int64_t* __restrict__ seg_pos) {
+    __shared__ int32_t warp_cnt[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t i = (int64_t)blockIdx.x * kSampleBlock + threadIdx.x;
+    int keep = (i < n) ? flags[i] : 0;
+    unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) warp_cnt[w] = __popc(bal);
+    __syncthreads();
+    if (w == 0) {
+        int s = warp_cnt[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        warp_cnt[lane] = s;
+    }
+    __syncthreads();
+    int64_t pos = boff[blockIdx.x] + (w ? warp_cnt[w - 1] : 0) + __popc(bal & ((1u << lane) - 1u));
+    if (i < n) {
+        if (keep) out[pos] = payload[i];
+        if (i < n_bd) slot_of_b[payload[i]] = keep ? (int32_t)pos : -1;
+        for (int k = 0; k < nseg; ++k)
+            if (cand_seg[k] == i) seg_pos[k] = pos;
+    }
+    if (i == 0 && n == 0)
+        for (int k = 0; k < nseg; ++k) seg_pos[k] = 0;
+}
+
+__global__ void k_seg_tail(const int64_t* __restrict__ cand_seg, int nseg, int64_t n, const int64_t* __restrict__ boff,
+                           int64_t nb, int64_t* __restrict__ seg_pos) {
+    int k = threadIdx.x;
+    if (k < nseg && cand_seg[k] >= n) seg_pos[k] = boff[nb];
+}
+
+void launch_sample(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
+    const int m = c.cfg.world;
+    int64_t n = c.n_cand;
+    int64_t nb = (n + kSampleBlock - 1) / kSampleBlock;
+    int64_t* boff = c.d_scan_tmp;
+    if (nb > 0) {
+        k_sample_count<<<(unsigned)nb, kSampleBlock, 0, c.stream>>>(
+            c.d_cand_gid, c.d_cand_key, n, T, (uint32_t)epoch, (uint32_t)(epoch >> 32), (uint32_t)seed,
+            (uint32_t)(seed >> 32), c.d_flags, c.d_blk);
+        k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_blk, boff, nb, nullptr);
+        k_sample_scatter<<<(unsigned)nb, kSampleBlock, 0, c.stream>>>(c.d_flags, n, c.plan.n_bd, boff,
+                                                                      c.d_cand_payload, c.d_cand_seg, 2 * m + 1,
+                                                                      c.d_cand_out, c.d_slot_of_b, c.d_seg_pos);
+        c.kernels += 3;
+    } else {
+        BNS_CUDA(cudaMemsetAsync(boff, 0, sizeof(int64_t), c.stream));
+    }
+    k_seg_tail<<<1, 128, 0, c.stream>>>(c.d_cand_seg, 2 * m + 1, n, boff, nb, c.d_seg_pos);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------------------------
+// a3 induce: per-row kept counts, scans, order-preserving write + forward segments
+// ---------------------------------------------------------------------------------------------
+__global__ void k_induce_count(const int64_t* __restrict__ ptr, const int32_t* __restrict__ col_enc, int64_t n_in,
+                               const int32_t* __restrict__ slot_of_b, int32_t* __restrict__ cnt,
+                               int32_t* __restrict__ nseg) {
+    const int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_in; r += nwarps) {
+        int c = 0;
+        for (int64_t e = ptr[r] + lane; e < ptr[r + 1]; e += 32) {
+            int32_t x = col_enc[e];
+            c += (x >= 0 || slot_of_b[-x - 1] >= 0) ? 1 : 0;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) {
+            cnt[r] = c;
+            nseg[r] = c > kSeg ? (c + kSeg - 1) / kSeg : 1;
+        }
+    }
+}
+
+__global__ void k_induce_write(const int64_t* __restrict__ ptr, const int32_t* __restrict__ col_enc, int64_t n_in,
+                               const int32_t* __restrict__ slot_of_b, const int64_t* __restrict__ out_ptr,
+                               const int64_t* __restrict__ seg_off, int32_t* __restrict__ out_col,
+                               Seg* __restrict__ segs) {
+    const int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_in; r += nwarps) {
+        int64_t base = out_ptr[r];
+        const int64_t b0 = base, b1 = out_ptr[r + 1];
+        for (int64_t e0 = ptr[r]; e0 < ptr[r + 1]; e0 += 32) {
+            int64_t e = e0 + lane;
+            int keep = 0;
+            int32_t y = 0;
+            if (e < ptr[r + 1]) {
+                int32_t x = col_enc[e];
+                if (x >= 0) { keep = 1; y = x; }
+                else {
+                    int32_t s = slot_of_b[-x - 1];
+                    if (s >= 0) { keep = 1; y = (int32_t)n_in + s; }
+                }
+            }
+            unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) out_col[base + __popc(bal & ((1u << lane) - 1u))] = y;
+            base += __popc(bal);
+        }
+        int64_t s0 = seg_off[r], ns = seg_off[r + 1] - s0;
+        for (int64_t k = lane; k < ns; k += 32) {
+            Seg sg;
+            sg.row = (int32_t)r;
+            sg.nseg = (int32_t)ns;
+            sg.e0 = b0 + k * kSeg;
+            sg.e1 = min(b1, sg.e0 + kSeg);
+            sg.first = s0;
+            segs[s0 + k] = sg;
+        }
+    }
+}
+
+void launch_induce(Ctx& c) {
+    const int64_t n_in = c.plan.n_in;
+    const int m = c.cfg.world;
+    int64_t* tot = c.d_seg_pos + 2 * m + 1;   // [nnz_kept, n_seg_fwd, n_seg_bwd_halo]
+    unsigned grid = (unsigned)std::min<int64_t>((n_in + 7) / 8, 148 * 16);
+    if (grid == 0) grid = 1;
+    k_induce_count<<<grid, 256, 0, c.stream>>>(c.d_row_ptr, c.d_col_enc, n_in, c.d_slot_of_b, c.d_row_cnt,
+                                               c.d_row_nseg);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+    scan_i32(c, c.d_row_cnt, c.d_ind_ptr, n_in, tot + 0);
+    scan_i32(c, c.d_row_nseg, c.d_row_soff, n_in, tot + 1);
+    k_induce_write<<<grid, 256, 0, c.stream>>>(c.d_row_ptr, c.d_col_enc, n_in, c.d_slot_of_b, c.d_ind_ptr,
+                                               c.d_row_soff, c.d_ind_col, c.d_seg_fwd);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+// backward (transposed) segments of the halo rows: halo slot s <- boundary b = U_b[s], inner neighbours of b
+__global__ void k_bwd_count(const int64_t* __restrict__ seg_pos, int m, const int32_t* __restrict__ U_b,
+                            const int64_t* __restrict__ br_ptr, int64_t cap, int32_t* __restrict__ nseg) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= cap) return;
+    int64_t n_halo = seg_pos[m] - seg_pos[0];
+    int v = 0;
+    if (s < n_halo) {
+        int32_t b = U_b[s];
+        int64_t len = br_ptr[b + 1] - br_ptr[b];
+        v = len > kSeg ? (int)((len + kSeg - 1) / kSeg) : 1;
+    }
+    nseg[s] = v;
+}
+
+__global__ void k_bwd_write(const int64_t* __restrict__ seg_pos, int m, const int32_t* __restrict__ U_b,
+                            const int64_t* __restrict__ br_ptr, int64_t cap, const int64_t* __restrict__ soff,
+                            int64_t seg_base, int64_t e_base, int64_t n_in, Seg* __restrict__ segs) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= cap) return;
+    int64_t n_halo = seg_pos[m] - seg_pos[0];
+    if (s >= n_halo) return;
+    int32_t b = U_b[s];
+    int64_t e_lo = e_base + br_ptr[b], e_hi = e_base + br_ptr[b + 1];
+    int64_t s0 = seg_base + soff[s], ns = soff[s + 1] - soff[s];
+    for (int64_t k = 0; k < ns; ++k) {
+        Seg sg;
+        sg.row = (int32_t)(n_in + s);
+        sg.nseg = (int32_t)ns;
+        sg.e0 = e_lo + k * kSeg;
+        sg.e1 = min(e_hi, sg.e0 + kSeg);
+        sg.first = s0;
+        segs[s0 + k] = sg;
+    }
+}
+
+void launch_bwd_segments(Ctx& c) {
+    const int m = c.cfg.world;
+    const int64_t cap = c.plan.n_bd;
+    int64_t* tot = c.d_seg_pos + 2 * m + 1;
+    if (cap == 0) {
+        BNS_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(int64_t), c.stream));
+        return;
+    }
+    unsigned grid = (unsigned)((cap + 255) / 256);
+    k_bwd_count<<<grid, 256, 0, c.stream>>>(c.d_seg_pos, m, c.d_cand_out, c.d_br_ptr, cap, c.d_row_nseg);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+    scan_i32(c, c.d_row_nseg, c.d_row_soff, cap, tot + 2);
+    k_bwd_write<<<grid, 256, 0, c.stream>>>(c.d_seg_pos, m, c.d_cand_out, c.d_br_ptr, cap, c.d_row_soff,
+                                            c.n_seg_bwd_inner, c.ii_nnz, c.plan.n_in, c.d_seg_bwd);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+}  // namespace bns

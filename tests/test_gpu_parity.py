@@ -1,0 +1,258 @@
+"""GPU parity: libbns.so (sm_100a kernels, through the C ABI) against the oracle, element by element.
+
+Bar (BASELINE.json north_star): sampling masks, compacted index lists, send/recv maps and the induced subgraph
+bit-exact; per-layer activations and gradients within 1e-5 (fp32) / 2e-2 (bf16) normwise relative error
+(SURVEY.md §8(c) item 20); loss within 1e-3 relative.  Multi-partition runs use the LOCAL transport (m contexts
+on one GPU, one host thread each) -- the same pack / exchange / scatter-add / all-reduce code path as NCCL except
+the copy engine that moves the rows.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2203_10983_b200 import bns
+from paper_2203_10983_b200 import inputs as I
+
+from gpu_harness import GpuRun, LOSS_TOL, TOL, relerr
+
+pytestmark = pytest.mark.gpu
+SEED = I.BNS_SEED
+
+
+def wl(N, nnz, m, d0, C, seed, method="random", train=0.7):
+    indptr, indices = I.rmat(N, nnz, seed=seed)
+    part = I.partition(indptr, indices, m, method)
+    X = I.features(np.arange(N, dtype=np.int32), d0)
+    y = I.labels(N, C, train, seed=seed + 7)
+    return indptr, indices, part, X, y
+
+
+@pytest.mark.parametrize("N,nnz,m,method", [(2000, 40000, 2, "random"), (3000, 60000, 5, "ldg2"),
+                                            (1000, 8000, 3, "random"), (500, 3000, 8, "ldg2")])
+def test_sampling_lists_bitexact(N, nnz, m, method):
+    indptr, indices, part, X, y = wl(N, nnz, m, 4, 3, 11, method)
+    run = GpuRun(indptr, indices, part, m, [4, 3], 0, bns.BNS_FP32, X, y, flags=bns.BNS_DEBUG_EXCHANGE_INDICES)
+    orc = O.Oracle(indptr, indices, part, m, [1, 1], 0, np.zeros((N, 1), np.float32), np.zeros(N, np.int32))
+    try:
+        for p in (0.0, 0.1, 0.5, 1.0):
+            for e in (0, 1, (1 << 32) + 3):
+                run.sample(p, SEED, e)
+                orc.sample(p, SEED, e)
+                for r in range(m):
+                    c = run.ctx[r]
+                    assert np.array_equal(c.mask(), orc.list(O.KEEP, r).astype(np.uint8))
+                    U = c.i32(bns.BNS_Q_HALO)
+                    assert np.array_equal(U, orc.list(O.U_LIST, r))
+                    assert np.array_equal(c.i64(bns.BNS_Q_HALO_OFF), orc.list(O.U_OFF, r))
+                    S = c.i32(bns.BNS_Q_SEND)
+                    So = c.i64(bns.BNS_Q_SEND_OFF)
+                    for j in range(m):
+                        assert np.array_equal(S[So[j]:So[j + 1]], orc.list(O.S_LIST, r, j)), (p, e, r, j)
+                    # induced subgraph (Alg.1 l.5): kept columns in global neighbour order, halo -> n_in + slot
+                    V = c.i32(bns.BNS_Q_INNER)
+                    local = {int(v): k for k, v in enumerate(V)}
+                    slot = {int(u): s for s, u in enumerate(U)}
+                    ptr, col = c.induced(len(V))
+                    for k in range(0, len(V), max(1, len(V) // 200)):
+                        v = V[k]
+                        exp = [local[u] if u in local else len(V) + slot[u]
+                               for u in map(int, indices[indptr[v]:indptr[v + 1]]) if u in local or u in slot]
+                        assert list(col[ptr[k]:ptr[k + 1]]) == exp
+    finally:
+        run.close()
+
+
+def compare_epoch(run, orc, L, Ws, Wd, lr, prec, host=False, tag=""):
+    tol = TOL[prec]
+    loss, acc, G, Wn = run.epoch(Ws, lr, host=host)
+    lo, ao, Go = orc.epoch(Wd, lr)
+    assert abs(loss - lo) <= LOSS_TOL * max(abs(lo), 1e-12), (tag, loss, lo)
+    ntr = max(1, int((orc.labels >= 0).sum()))
+    assert abs(acc - ao) <= (0.0 if prec == bns.BNS_FP32 else 0.02) + 2.0 / ntr, (tag, acc, ao)
+    dims = run.dims
+    for l in range(1, L + 1):
+        e = relerr(run.gather(bns.BNS_Q_Z, l, dims[l - 1]), orc.tensor(O.T_Z, l))
+        assert e <= tol, (tag, "Z", l, e)
+        e = relerr(run.gather(bns.BNS_Q_H, l, dims[l]), orc.tensor(O.T_H, l))
+        assert e <= tol, (tag, "H", l, e)
+        e = relerr(run.gather(bns.BNS_Q_DH, l, dims[l]), orc.tensor(O.T_DH, l))
+        assert e <= tol, (tag, "dH", l, e)
+    for l in range(L):
+        e = relerr(G[l], Go[l])
+        assert e <= tol, (tag, "dW", l, e)
+        e = relerr(Wn[l], Wd[l])
+        assert e <= max(tol * 0.1, 1e-6), (tag, "W", l, e)
+    return [w.astype(np.float32) for w in Wn]
+
+
+CASES = [  # (m, p, method)
+    (1, 1.0, "random"), (2, 0.5, "random"), (4, 0.1, "ldg2"), (3, 0.0, "random"), (3, 1.0, "ldg2"), (5, 0.3, "random"),
+]
+
+
+@pytest.mark.parametrize("prec", [bns.BNS_FP32, bns.BNS_BF16])
+@pytest.mark.parametrize("layer", [bns.BNS_LAYER_SAGE_MEAN, bns.BNS_LAYER_GCN])
+@pytest.mark.parametrize("m,p,method", CASES)
+def test_epoch_parity(prec, layer, m, p, method):
+    dims = [37, 24, 16, 5] if layer == bns.BNS_LAYER_SAGE_MEAN else [37, 16, 5]
+    N, nnz = 3000, 90000                       # R-MAT: hub rows > kSeg exercise the split-row fixup
+    indptr, indices, part, X, y = wl(N, nnz, m, dims[0], dims[-1], 21 + m, method)
+    L = len(dims) - 1
+    Ws = I.weights(dims, layer)
+    Wd = [w.astype(np.float64) for w in Ws]
+    run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y)
+    orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
+    orc.set_bf16(prec == bns.BNS_BF16)       # R19: the oracle stores what the bf16 mode stores, in bf16
+    try:
+        for e in range(2):
+            run.sample(p, SEED, e)
+            orc.sample(p, SEED, e)
+            Ws = compare_epoch(run, orc, L, Ws, Wd, 0.5, prec, tag=f"epoch{e}")
+    finally:
+        run.close()
+
+
+def test_cora_config0():
+    """BASELINE.json configs[0]: Cora-shaped, 2-layer GCN hidden 16, 2 partitions, p=0.5, fixed Philox seed."""
+    sh = I.SHAPES["cora"]
+    indptr, indices = I.rmat(sh.N, sh.nnz)
+    part = I.partition(indptr, indices, 2)
+    X = I.features(np.arange(sh.N, dtype=np.int32), sh.d0)
+    y = I.labels(sh.N, sh.C, sh.train_frac)
+    Ws = I.weights(sh.dims, sh.layer)
+    Wd = [w.astype(np.float64) for w in Ws]
+    for prec in (bns.BNS_FP32, bns.BNS_BF16):
+        run = GpuRun(indptr, indices, part, 2, sh.dims, sh.layer, prec, X, y)
+        orc = O.Oracle(indptr, indices, part, 2, sh.dims, sh.layer, X, y)
+        orc.set_bf16(prec == bns.BNS_BF16)
+        Wp, Wdp = [w.copy() for w in Ws], [w.copy() for w in Wd]
+        try:
+            for e in range(3):
+                run.sample(0.5, SEED, e)
+                orc.sample(0.5, SEED, e)
+                Wp = compare_epoch(run, orc, sh.L, Wp, Wdp, 0.1, prec, tag=f"cora prec{prec} e{e}")
+        finally:
+            run.close()
+
+
+def find_epoch_for_draw():
+    """first epoch whose Philox draw at p=0.5 gives U_0 = {2}, U_1 = {} on the P4 golden graph"""
+    T = O.threshold(0.5)
+    for e in range(1000):
+        if O.draw(2, 0, e, SEED) < T and O.draw(1, 1, e, SEED) >= T:
+            return e
+    raise AssertionError
+
+
+@pytest.mark.parametrize("name", ["E1", "E2", "E3", "E4", "E5", "E6"])
+def test_goldens_on_gpu(name):
+    G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "p4_goldens.json")))
+    c = G["cases"][name]
+    g = G["graph"]
+    layer = 0 if c["layer"] == "sage" else 1
+    Ws = [np.array(w, np.float32) for w in G[c["W"]]]
+    dims = [1] + [w.shape[1] for w in Ws]
+    indptr, indices = I.csr_from_edges(4, g["edges"])
+    X = np.array(g["X"], np.float32)
+    y = np.array(g["labels"], np.int32)
+    run = GpuRun(indptr, indices, np.array(g["part_of"], np.int32), 2, dims, layer, bns.BNS_FP32, X, y)
+    try:
+        e = find_epoch_for_draw() if "draw" in c else 0
+        run.sample(c["p"], SEED, e)
+        assert list(run.ctx[0].i32(bns.BNS_Q_HALO)) == ([2] if c["p"] > 0 else [])
+        loss, acc, Gr, _ = run.epoch(Ws, 0.0)
+        assert abs(loss - c["loss"]) < 1e-6
+        assert acc == c["acc"]
+        for l, gd in enumerate(c.get("dW", [])):
+            np.testing.assert_allclose(Gr[l], gd, atol=1e-6)
+        if "logits" in c:
+            np.testing.assert_allclose(run.gather(bns.BNS_Q_H, len(Ws), 2), c["logits"], atol=1e-6)
+    finally:
+        run.close()
+
+
+def test_host_pointer_weights_equal_device_path():
+    indptr, indices, part, X, y = wl(1500, 30000, 2, 16, 4, 5)
+    dims = [16, 8, 4]
+    Ws = I.weights(dims, 0)
+    run = GpuRun(indptr, indices, part, 2, dims, 0, bns.BNS_FP32, X, y)
+    try:
+        run.sample(0.4, SEED, 7)
+        a = run.epoch(Ws, 0.3, host=False)
+        b = run.epoch(Ws, 0.3, host=True)
+        assert a[0] == b[0] and a[1] == b[1]
+        for x, z in zip(a[2] + a[3], b[2] + b[3]):
+            assert np.array_equal(x, z)
+    finally:
+        run.close()
+
+
+def test_determinism_two_runs():
+    indptr, indices, part, X, y = wl(2500, 70000, 3, 20, 6, 8)
+    dims = [20, 16, 6]
+    outs = []
+    for _ in range(2):
+        run = GpuRun(indptr, indices, part, 3, dims, 0, bns.BNS_BF16, X, y)
+        Ws = I.weights(dims, 0)
+        try:
+            rec = []
+            for e in range(3):
+                run.sample(0.3, SEED, e)
+                loss, acc, G, Ws = run.epoch(Ws, 0.2)
+                rec.append((loss, acc, [g.tobytes() for g in G], run.ctx[1].mask().tobytes()))
+            outs.append((rec, [w.tobytes() for w in Ws]))
+        finally:
+            run.close()
+    assert outs[0] == outs[1]
+
+
+def test_binomial_counts_gpu():
+    indptr, indices, part, X, y = wl(3000, 60000, 4, 4, 3, 3)
+    run = GpuRun(indptr, indices, part, 4, [4, 3], 0, bns.BNS_FP32, X, y, flags=0)
+    try:
+        p, E = 0.1, 400
+        nB = [run.ctx[r].counts()["n_bd"] for r in range(4)]
+        cnt = np.zeros((E, 4))
+        for e in range(E):
+            run.sample(p, 99, e)
+            for r in range(4):
+                cnt[e, r] = run.ctx[r].counts()["n_halo"]
+        pp = O.threshold(p) / 2**32
+        for r in range(4):
+            mu, sd = nB[r] * pp, np.sqrt(nB[r] * pp * (1 - pp))
+            assert abs(cnt[:, r].mean() - mu) < 4 * sd / np.sqrt(E)
+            assert abs(cnt[:, r].std() - sd) < 0.15 * sd
+    finally:
+        run.close()
+
+
+def test_nonfinite_loss_leaves_weights():
+    indptr, indices, part, X, y = wl(800, 8000, 2, 8, 3, 4)
+    dims = [8, 3]
+    Ws = I.weights(dims, 0)
+    Ws[0][0, 0] = np.inf
+    run = GpuRun(indptr, indices, part, 2, dims, 0, bns.BNS_FP32, X, y)
+    try:
+        run.sample(1.0, SEED, 0)
+        with pytest.raises(bns.BnsError) as e:
+            run.epoch(Ws, 0.1)
+        assert e.value.code == bns.BNS_ERR_NONFINITE
+    finally:
+        run.close()
+
+
+def test_epoch_before_sample_is_state_error():
+    indptr, indices, part, X, y = wl(300, 2000, 1, 8, 3, 4)
+    run = GpuRun(indptr, indices, part, 1, [8, 3], 0, bns.BNS_FP32, X, y)
+    try:
+        with pytest.raises(bns.BnsError) as e:
+            run.epoch(I.weights([8, 3], 0), 0.1)
+        assert e.value.code == bns.BNS_ERR_STATE
+        with pytest.raises(bns.BnsError) as e:
+            run.ctx[0].sample_boundary(1.5, 1, 0)
+        assert e.value.code == bns.BNS_ERR_INVALID
+    finally:
+        run.close()

@@ -199,3 +199,45 @@ def test_unbiased_aggregate():
     a = np.array(acc)
     se = a.std(0) / np.sqrt(T) + 1e-12
     assert np.all(np.abs(a.mean(0) - z_exact) <= 4.5 * se + 1e-12)
+
+
+def test_bf16_rounding_matches_torch():
+    import torch
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([rng.normal(size=2000) * 10.0 ** rng.integers(-30, 30, 2000), [0.0, -0.0, 1.0, 2**-133]])
+    ref = torch.tensor(xs, dtype=torch.float32).bfloat16().double().numpy()
+    got = np.array([O.round_bf16(x) for x in xs])
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name", ["E1", "E2", "E3", "E4"])
+def test_bf16_emulation_exact_on_representable_goldens(name):
+    # all stored forward values of E1-E4 are dyadic with <= 8 significant bits -> bf16 storage changes nothing
+    c = GOLD["cases"][name]
+    Ws = [np.array(w, np.float64) for w in GOLD[c["W"]]]
+    dims = [1] + [w.shape[1] for w in Ws]
+    o = p4_oracle(0, dims)
+    o.set_bf16(True)
+    if "draw" in c:
+        d = GOLD[c["draw"]]
+        o.set_keep(c["p"], [d["keep_rank0"], d["keep_rank1"]])
+    else:
+        o.sample(c["p"], 1, 0)
+    loss, acc, G = o.epoch([w.copy() for w in Ws], 0.0)
+    assert abs(loss - c["loss"]) < 1e-8 and acc == c["acc"]
+    np.testing.assert_allclose(o.tensor(O.T_H, len(Ws)), c["logits"], atol=0)
+    for l, g in enumerate(c["dW"]):      # gradients only differ by the bf16 rounding of dPre / dZ' / dX
+        np.testing.assert_allclose(G[l], g, rtol=2 ** -5, atol=1e-3 * np.abs(g).max())
+
+
+def test_bf16_emulation_close_to_float64():
+    ip, ix, part, X, y, Ws = random_case(61, N=60, m=3, dims=(3, 6, 4))
+    out = []
+    for bf in (False, True):
+        o = O.Oracle(ip, ix, part, 3, [3, 6, 4], 0, X, y)
+        o.set_bf16(bf)
+        o.sample(0.5, 3, 3)
+        out.append(o.epoch([w.copy() for w in Ws], 0.0))
+    assert abs(out[0][0] - out[1][0]) < 2e-2 * abs(out[0][0])
+    for a, b in zip(out[0][2], out[1][2]):
+        assert np.abs(a - b).max() <= 5e-2 * np.abs(a).max()
