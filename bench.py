@@ -1,0 +1,444 @@
+"""bench.py -- BNS-GCN epoch throughput on B200 (BASELINE.json metric).
+
+One step = one epoch of the hot path = bns_sample_boundary (Alg.1 l.4-7) + bns_epoch (l.8-14), on the
+Reddit-shaped synthetic R-MAT graph (BASELINE.json configs[1]), 4-layer GraphSAGE-mean (hidden 256), p = 0.1,
+m = number of GPUs = number of partitions (one process per GPU, NCCL over NVLink for N > 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--prec bf16|fp32] [--p 0.1]
+
+Timing: per-step CUDA events on the library's stream with an L2 flush between steps (outside the events), W
+untimed warm-up steps, K timed steps bracketed by barrier + synchronize; the max over ranks of the summed step
+times gives ms_per_step; value = K / that time (epochs/s of the whole job).  Rank 0 prints one JSON line.
+--impl reference times the oracle (oracle/, single-threaded float64 C++) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "epochs/s Reddit-shaped GraphSAGE p=0.1 at 1/2/4/8 B200; SpMM HBM GB/s"
+UNIT = "epochs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="reddit")
+    ap.add_argument("--p", type=float, default=0.1)
+    ap.add_argument("--prec", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--partition", default="ldg2", choices=["ldg2", "random"])
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-scale", type=float, default=64.0, help="oracle sample = workload scaled down by this")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------------------------------------------
+# workload (setup, never timed)
+# ------------------------------------------------------------------------------------------------
+def load_workload(shape, m, method, rank, world, dist):
+    from paper_2203_10983_b200 import inputs as I
+    shm = os.path.join("/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir(),
+                       f"bns_{shape.name}_{shape.N}_{shape.nnz}_{m}_{method}_{os.getpid() if world == 1 else os.environ.get('MASTER_PORT', '0')}")
+    if world == 1:
+        indptr, indices = I.rmat(shape.N, shape.nnz)
+        part = I.partition(indptr, indices, m, method)
+        return indptr, indices, part
+    if rank == 0:
+        indptr, indices = I.rmat(shape.N, shape.nnz)
+        part = I.partition(indptr, indices, m, method)
+        np.save(shm + "_ip.npy", indptr)
+        np.save(shm + "_ix.npy", indices)
+        np.save(shm + "_pt.npy", part)
+    dist.barrier()
+    if rank != 0:
+        indptr = np.load(shm + "_ip.npy")
+        indices = np.load(shm + "_ix.npy")
+        part = np.load(shm + "_pt.npy")
+    dist.barrier()
+    if rank == 0:
+        for s in ("_ip.npy", "_ix.npy", "_pt.npy"):
+            try:
+                os.remove(shm + s)
+            except OSError:
+                pass
+    return indptr, indices, part
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ------------------------------------------------------------------------------------------------
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 3:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx.append(float(parts[1]))
+                    bits = int(parts[2], 16)
+                except ValueError:
+                    continue
+                for b, n in REASONS.items():
+                    if bits & b and n != "gpu_idle":
+                        reasons.add(n)
+        finally:
+            try:
+                os.remove(self.path)
+            except OSError:
+                pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+# algorithmic bytes / flops
+# ------------------------------------------------------------------------------------------------
+def spmm_bytes(dp, L, n_in, n_halo, kept, s):
+    fwd = sum(kept * (dp[l] * s + 4) + (n_in + 1) * 4 + n_in * dp[l] * s for l in range(L))
+    bwd = sum(kept * (dp[l] * s + 4) + (n_in + n_halo + 1) * 4 + (n_in + n_halo) * dp[l] * s for l in range(1, L))
+    return fwd, bwd
+
+
+def gemm_flops(dp, L, n_in, sage):
+    f = 0
+    for l in range(L):
+        K = (2 if sage else 1) * dp[l]
+        f += 2 * n_in * K * dp[l + 1]          # forward
+        f += 2 * n_in * K * dp[l + 1]          # dW
+        if l > 0:
+            f += 2 * n_in * K * dp[l + 1]      # dX
+    return f
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def latest_traffic():
+    """dram bytes per SpMM launch from the newest committed ncu --set full summary (profiles/*spmm*.json)."""
+    d = os.path.join(ROOT, "profiles")
+    best = None
+    if os.path.isdir(d):
+        for f in sorted(os.listdir(d)):
+            if f.endswith(".json") and "spmm" in f:
+                best = os.path.join(d, f)
+    if not best:
+        return None
+    try:
+        return json.load(open(best)).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline: the oracle as it stands, single-threaded, on a scaled-down sample of the same workload
+# ------------------------------------------------------------------------------------------------
+def cpu_baseline(shape, scale, steps=1):
+    from oracle import oracle as O
+    from paper_2203_10983_b200 import inputs as I
+    sm = shape.scaled(scale)
+    indptr, indices = I.rmat(sm.N, sm.nnz)
+    X = I.features(np.arange(sm.N, dtype=np.int32), sm.d0)
+    y = I.labels(sm.N, sm.C, sm.train_frac)
+    part = np.zeros(sm.N, np.int32)
+    orc = O.Oracle(indptr, indices, part, 1, sm.dims, sm.layer, X, y)
+    W = [w.astype(np.float64) for w in I.weights(sm.dims, sm.layer)]
+    ts = []
+    for e in range(steps):
+        orc.sample(shape.p, I.BNS_SEED, e)
+        t0 = time.perf_counter()
+        orc.epoch(W, 0.01)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    actual_scale = shape.nnz / float(indptr[-1])
+    value = 1.0 / (t * actual_scale)
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": (f"oracle (single-thread float64 C++) full epoch on a {shape.name}-shaped R-MAT scaled 1/{scale:g} "
+                       f"(N={sm.N}, nnz={int(indptr[-1])}, same dims), m=1; {t:.2f} s/epoch x {actual_scale:.1f} "
+                       f"(nnz ratio; oracle work is linear in nnz at fixed dims) -> epochs/s of the full workload")}
+
+
+# ------------------------------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            return
+    from paper_2203_10983_b200 import inputs as I
+    shape = I.SHAPES[args.config]
+    shape.p = args.p
+    scale = max(args.cpu_scale, 256.0)
+    for _ in range(args.warmup):
+        cpu_baseline(shape, scale * 4)
+    t0 = time.perf_counter()
+    vals = [cpu_baseline(shape, scale) for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    v = float(np.mean([x["value"] for x in vals]))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (R-MAT, Philox features/labels)",
+            "config": {"workload": f"{shape.name}-shaped R-MAT GraphSAGE {shape.L}x{shape.hidden}, p={shape.p}",
+                       "note": "oracle timed on host cores; each step is a bounded sample scaled to the full workload"},
+            "cpu_baseline": {**vals[0], "value": v}, "wall_s": wall,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2203_10983_b200 import bns
+    from paper_2203_10983_b200 import inputs as I
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or world == 1, "launch with torchrun --nproc-per-node N for --gpus N"
+    if args.gpus > 1 and world == 1:
+        raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    shape = I.SHAPES[args.config]
+    shape.p = args.p
+    m = world
+    prec = bns.BNS_BF16 if args.prec == "bf16" else bns.BNS_FP32
+    t_setup = time.perf_counter()
+    indptr, indices, part = load_workload(shape, m, args.partition, rank, world, dist)
+    inner = np.nonzero(part == rank)[0].astype(np.int32)
+    X = I.features(inner, shape.d0)
+    y_all = I.labels(shape.N, shape.C, shape.train_frac)
+    y = np.ascontiguousarray(y_all[inner])
+    nccl_id = None
+    if world > 1:
+        obj = [bns.bns_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = bns.Context(rank=rank, world=world, dims=shape.dims, layer=shape.layer, precision=prec, indptr=indptr,
+                      indices=indices, part_of=part, features=X, labels=y, device=local, nccl_id=nccl_id,
+                      max_p=0.0, flags=bns.BNS_TIMING)
+    del X
+    t_setup = time.perf_counter() - t_setup
+    Ws = I.weights(shape.dims, shape.layer)
+    Wt = [torch.tensor(w, device="cuda") for w in Ws]
+    Gt = [torch.zeros_like(w) for w in Wt]
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = torch.empty(int(2 * l2) // 4 + 1024, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(e, W, G):
+        ctx.sample_boundary(args.p, I.BNS_SEED, e)
+        return ctx.epoch(W, args.lr, G)
+
+    for e in range(args.warmup):
+        flush.fill_(float(e))
+        step(e, Wt, Gt)
+    barrier()
+    t0_times = ctx.times()
+    k0 = ctx.kernel_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    losses = []
+    with ClockSampler(local) as clk:
+        barrier()
+        wall0 = time.perf_counter()
+        for k in range(args.steps):
+            flush.fill_(float(k))                       # evict L2 between timed steps (outside the events)
+            torch.cuda.synchronize()
+            ev[k][0].record(stream)
+            loss, acc = step(args.warmup + k, Wt, Gt)
+            ev[k][1].record(stream)
+            losses.append(loss)
+        barrier()
+        wall = time.perf_counter() - wall0
+    clocks = clk.summary()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    launches = ctx.kernel_count() - k0
+    t1_times = ctx.times()
+    ph = {k: (t1_times[k] - t0_times[k]) / args.steps for k in t1_times}
+    cnt = ctx.counts()
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_max = float(t.item())
+    else:
+        total_max = total_ms
+    ms_per_step = total_max / args.steps
+    value = 1000.0 / ms_per_step
+
+    # ---- e2e: same steps through the C ABI with pinned HOST weights (H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        Wh = [torch.from_numpy(w.copy()).pin_memory() for w in Ws]
+        Gh = [torch.zeros_like(w).pin_memory() for w in Wh]
+        for e in range(2):
+            step(10_000 + e, Wh, Gh)
+        barrier()
+        e_ms = 0.0
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step(20_000 + k, Wh, Gh)
+            b.record(stream)
+            b.synchronize()
+            e_ms += a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        wbytes = sum(w.numel() * 4 for w in Wh)
+        e2e = {"value": 1000.0 * args.steps / e_ms, "unit": UNIT, "h2d_bytes_per_step": wbytes,
+               "d2h_bytes_per_step": 2 * wbytes + 16,
+               "note": "weights in pinned host memory: H2D of W, D2H of updated W + grads + loss/acc every step"}
+
+    # ---- per-rank partition stats (Table tab:partition style)
+    stats = np.array([cnt["n_in"], cnt["n_bd"], cnt["n_halo"], cnt["nnz"], cnt["nnz_kept"]], np.float64)
+    if world > 1:
+        t = torch.tensor(stats, device="cuda")
+        allst = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allst, t)
+        allst = [a.cpu().numpy() for a in allst]
+    else:
+        allst = [stats]
+
+    if rank == 0:
+        peaks = measured_peaks()
+        s = 2 if prec == bns.BNS_BF16 else 4
+        dp = [((d + 7) // 8) * 8 for d in shape.dims]
+        fwd_b, bwd_b = spmm_bytes(dp, shape.L, cnt["n_in"], cnt["n_halo"], cnt["nnz_kept"], s)
+        spmm_ms = ph["spmm_fwd"] + ph["spmm_bwd"]
+        hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        achieved = (fwd_b + bwd_b) / (spmm_ms * 1e-3) / 1e9 if spmm_ms > 0 else None
+        ws_bytes = (cnt["n_in"] + cnt["n_halo"]) * max(dp[1:-1] or dp) * s
+        gf = gemm_flops(dp, shape.L, cnt["n_in"], shape.layer == 0)
+        gemm_ms = ph["gemm_fwd"] + ph["gemm_bwd"]
+        bf16_peak = peaks.get("bf16_tflops_sustained", 1391.8)
+        # fp32 mode runs the GEMMs on the CUDA cores: peak = 148 SMs x 128 FMA lanes x 2 flop x max SM clock
+        peak_dtype = bf16_peak if prec == bns.BNS_BF16 else 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16" if prec == bns.BNS_BF16 else "f32",
+            "data": "synthetic: R-MAT graph (Graph500 a,b,c=.57,.19,.19), Philox features/labels, Glorot weights",
+            "config": {"workload": f"{shape.name}-shaped R-MAT N={shape.N} nnz={int(indptr[-1])}, GraphSAGE-mean "
+                                   f"{shape.L} layers hidden {shape.hidden}, d0={shape.d0}, C={shape.C}, p={args.p}, "
+                                   f"m={world} partitions ({args.partition})",
+                       "global_batch": "full graph", "parallelism": f"partition-parallel m={world}",
+                       "l2": "flushed between timed steps (2x L2 write, outside the events)",
+                       "step": "bns_sample_boundary + bns_epoch (SGD update included)"},
+            "roofline": {"bound": "hbm", "kernel": "segment SpMM (a6 fwd + a10 bwd, incl. split-row fixup)",
+                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (achieved / hbm_peak) if achieved else None, "traffic": latest_traffic(),
+                         "algorithmic_bytes_per_step": fwd_b + bwd_b, "spmm_ms_per_step": spmm_ms,
+                         "spmm_share_of_step": spmm_ms / ms_per_step,
+                         "gather_working_set_bytes": ws_bytes, "l2_bytes": l2,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peaks else "fallback 6.65 TB/s"},
+            "roofline_gemm": {"bound": "tensor" if prec == bns.BNS_BF16 else "alu", "achieved": gf / (gemm_ms * 1e-3) / 1e12
+                              if gemm_ms > 0 else None, "unit": "TFLOP/s", "flops_per_step": gf, "gemm_ms_per_step": gemm_ms,
+                              "peak": peak_dtype},
+            "phases_ms": ph,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": e2e,
+            "partition_stats": {"n_in": [int(a[0]) for a in allst], "n_bd": [int(a[1]) for a in allst],
+                                "n_halo": [int(a[2]) for a in allst], "nnz": [int(a[3]) for a in allst],
+                                "nnz_kept": [int(a[4]) for a in allst]},
+            "loss_last": losses[-1], "setup_s": t_setup, "wall_s_timed": wall,
+            "step_ms": step_ms,
+            "memory_bytes": ctx.memory()[0],
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(shape, args.cpu_scale)
+        else:
+            line["cpu_baseline"] = None
+        print(json.dumps(line), flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                json.dump(line, f, indent=1)
+    ctx.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -3,6 +3,7 @@
 // launches, exchanges and the two host syncs per epoch (counts after sampling; loss/acc at the end).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -274,6 +275,12 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.wrows.assign(L, 0);
     c.wcols.assign(L, 0);
     c.goff.assign(L + 1, 0);
+    c.WT.assign(L, nullptr);
+    c.wkw.assign(L, 0);
+    {
+        const char* no_tc = std::getenv("BNS_NO_TC");
+        c.use_tc = (c.prec == BNS_BF16) && !(no_tc && no_tc[0] == '1');
+    }
     int64_t wmax = 0, wlog = 0;
     for (int l = 0; l < L; ++l) {
         c.wrows[l] = (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * (int64_t)c.dp[l];
@@ -283,6 +290,8 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
         wlog += (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * (int64_t)c.dims[l] * c.dims[l + 1];
         c.Wpad[l] = static_cast<float*>(dalloc(c, c.wrows[l] * c.wcols[l] * sizeof(float)));
         c.Wt[l] = (c.prec == BNS_BF16) ? dalloc(c, c.wrows[l] * c.wcols[l] * 2) : (void*)c.Wpad[l];
+        c.wkw[l] = (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * ((int64_t)(c.dp[l] + 63) / 64 * 64);
+        if (c.use_tc) c.WT[l] = dalloc(c, c.wcols[l] * c.wkw[l] * 2);
     }
     c.gflat_n = c.goff[L];
     c.d_gflat = static_cast<float*>(dalloc(c, c.gflat_n * sizeof(float)));
@@ -443,7 +452,10 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             PhaseTimer t(c, BNS_PH_GEMM_FWD);
             const bool last = (l == L);
             void* out = last ? (void*)c.d_logits : c.H[l];
-            if (sage)
+            if (c.use_tc)
+                gemm_fwd_tc(c, n_in, dout, c.Z[l], din, din, sage ? Hin : nullptr, sage ? din : 0, din, c.WT[l - 1],
+                            c.wkw[l - 1], out, dout, !last, last);
+            else if (sage)
                 gemm_fwd(c, n_in, dout, c.Z[l], din, din, Hin, din, din, c.Wt[l - 1], dout, out, dout, !last, last);
             else
                 gemm_fwd(c, n_in, dout, c.Z[l], din, din, nullptr, 0, din, c.Wt[l - 1], dout, out, dout, !last, last);
@@ -467,14 +479,15 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         {
             PhaseTimer t(c, BNS_PH_GEMM_BWD);
             float* g = c.d_gflat + c.goff[l - 1];
-            gemm_wgrad(c, n_in, din, dout, c.Z[l], din, c.d_dpre, dout, g, dout);
-            if (sage) gemm_wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
+            auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
+            auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
+            wgrad(c, n_in, din, dout, c.Z[l], din, c.d_dpre, dout, g, dout);
+            if (sage) wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
             if (l > 1) {
                 if (sage)
-                    gemm_dx(c, n_in, 2 * din, dout, c.d_dpre, dout, c.Wt[l - 1], dout, c.d_dxcat, 2 * din, c.d_deg_in,
-                            din);
+                    dxg(c, n_in, 2 * din, dout, c.d_dpre, dout, c.Wt[l - 1], dout, c.d_dxcat, 2 * din, c.d_deg_in, din);
                 else
-                    gemm_dx(c, n_in, din, dout, c.d_dpre, dout, c.Wt[l - 1], dout, c.d_dxcat, din, c.d_rs_in, din);
+                    dxg(c, n_in, din, dout, c.d_dpre, dout, c.Wt[l - 1], dout, c.d_dxcat, din, c.d_rs_in, din);
             }
         }
         if (l == 1) break;   // R29: no gradient w.r.t. the input features

@@ -148,6 +148,9 @@ struct Ctx {
     std::vector<float*> Wpad;      // fp32 padded weights per layer
     std::vector<void*> Wt;         // storage-type copy (bf16 in BNS_BF16; == Wpad in FP32)
     std::vector<int64_t> wrows, wcols;   // padded shape per layer
+    std::vector<void*> WT;         // bf16 W^T [wcols][wkw] for the tcgen05 forward (K-major B operand)
+    std::vector<int64_t> wkw;      // K of W^T: each concat half padded to a multiple of 64
+    bool use_tc = false;           // tcgen05 GEMMs (BNS_BF16)
     float* d_gflat = nullptr;      // all-reduce buffer: Σ_l padded dW (fp32)
     int64_t gflat_n = 0;
     std::vector<int64_t> goff;     // per-layer offset in gflat

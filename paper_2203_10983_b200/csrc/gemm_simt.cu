@@ -103,6 +103,13 @@ __global__ void k_splitk_reduce(const float* __restrict__ part, int S, int64_t M
     out[i * ldo + j] = s;
 }
 
+void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw) {
+    const int64_t tot = K * N;
+    k_splitk_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, c.stream>>>(c.d_splitk, S, K, N, N, Wg, ldw);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
 template <typename T>
 static void fwd_t(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64_t lda0, const void* A1, int64_t K1,
                   int64_t lda1, const void* B, int64_t ldb, void* C, int64_t ldc, bool relu, bool out_f32) {

@@ -1,0 +1,348 @@
+// gemm_tc.cu -- a7 / a9 dense update on the 5th-generation tensor cores (tcgen05, BNS_BF16 mode).
+//
+// The update φ(z_v, h_v) = σ(W · CONCAT(z_v, h_v)) is the only true contraction on the path:
+//   fwd  Pre[n_in x d_out] = [Z | H] · W              A K-major (two tensor maps, concat along K), B = W^T K-major
+//   dW   dW[d_in x d_out]  = Z^T · dPre (and H^T ·)   A and B MN-major (the node dimension is the reduction),
+//                                                     split-K over nodes, fp32 partials reduced in fixed order
+//   dX   [dZ'|dXself]      = dPre · W^T               A K-major, B = W K-major; epilogue x 1/deg_G (or rs) on dZ'
+//
+// One CTA = one 128 x BN output tile (BN <= 256), 4 warps: warp 0 lane 0 issues TMA (SWIZZLE_128B boxes of 64
+// bf16 = 128 B) into a 4-stage mbarrier ring, warp 1 lane 0 issues tcgen05.mma.cta_group::1.kind::f16
+// (M=128, N=BN, K=16, fp32 accumulator in TMEM) and releases stages with tcgen05.commit; after the last k-block
+// all 4 warps drain TMEM with tcgen05.ld.32x32b and apply the epilogue (ReLU / cast / row scale).  K tails and
+// partial M / N tiles are handled by TMA's zero fill and masked stores.
+#include <cuda.h>
+
+#include "common.h"
+#include "dev.cuh"
+#include "kernels.h"
+
+namespace bns {
+
+constexpr int TC_BM = 128, TC_BK = 64, TC_STAGES = 4;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;             // 16 KB
+constexpr int TC_B_BYTES = 256 * TC_BK * 2;               // 32 KB (max BN)
+constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
+constexpr int TC_SMEM = TC_STAGES * TC_STAGE_BYTES + 1024 + 256;
+
+enum TcEpi { EPI_BF16 = 0, EPI_F32 = 1, EPI_BF16_ROWSCALE = 2 };
+
+struct TcArgs {
+    int64_t M, N;
+    int BN;                 // MMA N (multiple of 16; multiple of 64 when B is MN-major)
+    int nk0, nk;            // k-blocks from map A0, total k-blocks
+    int kb_per_split;       // k-blocks per blockIdx.z (split-K), 0 = all
+    int epi;
+    int relu;
+    void* out;
+    int64_t ldc;
+    int64_t split_stride;   // elements between split-K partial slices
+    const float* rowscale;
+    int64_t scale_cols;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t a = smem_u32(b);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);   // version 1, SWIZZLE_128B
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(128, 1)
+k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+          const __grid_constant__ CUtensorMap mapB, const TcArgs args) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
+    uint64_t* empty = full + TC_STAGES;
+    uint64_t* accum = empty + TC_STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t m0 = (int64_t)blockIdx.x * TC_BM;
+    const int64_t n0 = (int64_t)blockIdx.y * args.BN;
+    int kb0 = 0, kb1 = args.nk;
+    if (args.kb_per_split > 0) {
+        kb0 = blockIdx.z * args.kb_per_split;
+        kb1 = min(args.nk, kb0 + args.kb_per_split);
+    }
+    const int nk = max(0, kb1 - kb0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(accum, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA1) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    const uint32_t b_bytes = (uint32_t)args.BN * TC_BK * 2;
+    if (warp == 0 && lane == 0 && nk > 0) {
+        // ---------------- TMA producer ----------------
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % TC_STAGES;
+            const uint32_t ph = (uint32_t)(i / TC_STAGES) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            uint8_t* sa = smem + s * TC_STAGE_BYTES;
+            uint8_t* sb = sa + TC_A_BYTES;
+            mbar_expect_tx(&full[s], TC_A_BYTES + b_bytes);
+            const int kb = kb0 + i;
+            if (!A_MN) {
+                // A K-major: box {64 (k), 128 (m)}; concat along K: blocks [0, nk0) from A0, the rest from A1
+                if (kb < args.nk0) tma_load_2d(&mapA0, &full[s], sa, kb * TC_BK, (int)m0);
+                else tma_load_2d(&mapA1, &full[s], sa, (kb - args.nk0) * TC_BK, (int)m0);
+            } else {
+                // A MN-major (A^T stored row-major as [k][m]): two boxes {64 (m), 64 (k)}
+                tma_load_2d(&mapA0, &full[s], sa, (int)m0, kb * TC_BK);
+                tma_load_2d(&mapA0, &full[s], sa + 8192, (int)m0 + 64, kb * TC_BK);
+            }
+            if (!B_MN) {
+                tma_load_2d(&mapB, &full[s], sb, kb * TC_BK, (int)n0);        // box {64 (k), BN (n)}
+            } else {
+                for (int j = 0; j < args.BN / 64; ++j)                         // boxes {64 (n), 64 (k)}
+                    tma_load_2d(&mapB, &full[s], sb + j * 8192, (int)n0 + 64 * j, kb * TC_BK);
+            }
+        }
+    } else if (warp == 1 && lane == 0 && nk > 0) {
+        // ---------------- MMA issuer ----------------
+        // instruction descriptor: D fp32, A/B bf16, A/B major, N >> 3, M >> 4
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                               ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(args.BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % TC_STAGES;
+            const uint32_t ph = (uint32_t)(i / TC_STAGES) & 1u;
+            mbar_wait(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sa = smem_u32(smem + s * TC_STAGE_BYTES);
+            const uint32_t sb = sa + TC_A_BYTES;
+#pragma unroll
+            for (int k = 0; k < TC_BK / 16; ++k) {
+                // K-major SW128: +32 B per 16-element k step inside the 128 B row; LBO unused (16), SBO = 8 rows
+                // MN-major SW128: +16 rows (2048 B) per k step; LBO = MN-atom stride (8 KB), SBO = 8 k-rows (1 KB)
+                const uint64_t ad = A_MN ? umma_desc(sa + k * 2048, 8192, 1024) : umma_desc(sa + k * 32, 16, 1024);
+                const uint64_t bd = B_MN ? umma_desc(sb + k * 2048, 8192, 1024) : umma_desc(sb + k * 32, 16, 1024);
+                umma_bf16(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+            }
+            umma_commit(&empty[s]);
+        }
+        umma_commit(accum);
+    }
+    __syncwarp();
+
+    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    if (nk > 0) {
+        mbar_wait(accum, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    const int64_t row = m0 + warp * 32 + lane;
+    const int ncols = (args.N - n0 < args.BN) ? (int)(args.N - n0) : args.BN;
+    for (int c0 = 0; c0 < args.BN; c0 += 16) {
+        uint32_t r[16];
+        if (nk > 0) {
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) r[q] = 0u;
+        }
+        if (row >= args.M || c0 >= ncols) continue;
+        float v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
+        const int64_t col = n0 + c0;
+        if (args.epi == EPI_F32) {
+            float* o = static_cast<float*>(args.out) + (int64_t)blockIdx.z * args.split_stride + row * args.ldc + col;
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                if (c0 + 4 * h < ncols) {
+                    float4 w = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+                    if (args.relu) { w.x = fmaxf(w.x, 0.f); w.y = fmaxf(w.y, 0.f); w.z = fmaxf(w.z, 0.f); w.w = fmaxf(w.w, 0.f); }
+                    *reinterpret_cast<float4*>(o + 4 * h) = w;
+                }
+        } else {
+            if (args.epi == EPI_BF16_ROWSCALE) {
+                const float rs = args.rowscale[row];
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    if (col + q < args.scale_cols) v[q] *= rs;
+            }
+            if (args.relu)
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = fmaxf(v[q], 0.f);
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(args.out) + row * args.ldc + col;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (c0 + 8 * h < ncols)
+                    *reinterpret_cast<uint4*>(o + 8 * h) = Vec<__nv_bfloat16>::from_float(v + 8 * h);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// ------------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        BNS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw Error(BNS_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 2-D bf16 row-major tensor [outer][inner] with row pitch ld (elements); box {64, box_outer}, SWIZZLE_128B
+static CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+    cuuint32_t box[2] = {64u, (cuuint32_t)box_outer};
+    cuuint32_t es[2] = {1u, 1u};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(BNS_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+template <bool A_MN, bool B_MN>
+static void launch_tc(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const TcArgs& args,
+                      dim3 grid) {
+    static bool configured = false;
+    if (!configured) {
+        BNS_CUDA(cudaFuncSetAttribute(k_gemm_tc<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+        configured = true;
+    }
+    k_gemm_tc<A_MN, B_MN><<<grid, 128, TC_SMEM, c.stream>>>(a0, a1, b, args);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// fwd: C[M x N] = [A0 | A1] · W, B = W^T stored [N][Kw] (Kw = 64-padded per concat half)
+void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64_t lda0, const void* A1, int64_t K1,
+                 int64_t lda1, const void* WT, int64_t Kw, void* C, int64_t ldc, bool relu, bool out_f32) {
+    if (M <= 0 || N <= 0) return;
+    TcArgs a{};
+    a.M = M;
+    a.N = N;
+    a.BN = (int)std::min<int64_t>(256, cdiv(N, 16) * 16);
+    a.nk0 = (int)cdiv(K0, 64);
+    a.nk = a.nk0 + (int)cdiv(K1, 64);
+    a.epi = out_f32 ? EPI_F32 : EPI_BF16;
+    a.relu = relu ? 1 : 0;
+    a.out = C;
+    a.ldc = ldc;
+    CUtensorMap m0 = make_map(A0, K0, M, lda0, TC_BM);
+    CUtensorMap m1 = A1 ? make_map(A1, K1, M, lda1, TC_BM) : m0;
+    CUtensorMap mb = make_map(WT, Kw, N, Kw, a.BN);
+    launch_tc<false, false>(c, m0, m1, mb, a, dim3((unsigned)cdiv(M, TC_BM), (unsigned)cdiv(N, a.BN), 1));
+}
+
+// dW partials: out[z][K x N] = A^T · D over k-block range z; A is [M_nodes][K] row-major, D is [M_nodes][N]
+void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int64_t lda, const void* D, int64_t ldd,
+                   float* Wg, int64_t ldw) {
+    if (K <= 0 || N <= 0) return;
+    TcArgs a{};
+    a.M = K;
+    a.N = N;
+    a.BN = (int)std::min<int64_t>(256, cdiv(N, 64) * 64);
+    a.nk = (int)cdiv(Mn, 64);
+    a.nk0 = a.nk;
+    const int64_t tiles = cdiv(K, TC_BM) * cdiv(N, a.BN);
+    int64_t S = std::max<int64_t>(1, std::min<int64_t>(cdiv(296, tiles), std::max(1, a.nk / 8)));
+    while (S > 1 && S * K * N > c.splitk_cap) --S;
+    a.kb_per_split = (int)cdiv(a.nk, S);
+    S = cdiv(a.nk, a.kb_per_split);
+    a.epi = EPI_F32;
+    a.out = c.d_splitk;
+    a.ldc = N;
+    a.split_stride = K * N;
+    CUtensorMap ma = make_map(A, K, Mn, lda, 64);
+    CUtensorMap mb = make_map(D, N, Mn, ldd, 64);
+    launch_tc<true, true>(c, ma, ma, mb, a, dim3((unsigned)cdiv(K, TC_BM), (unsigned)cdiv(N, a.BN), (unsigned)S));
+    splitk_reduce(c, (int)S, K, N, Wg, ldw);
+}
+
+// dX: C[M x Nc] = D[M x K] · B^T with B = W [Nc][K] row-major; columns < scale_cols scaled by rowscale[row]
+void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t ldd, const void* B, int64_t ldb,
+                void* C, int64_t ldc, const float* rowscale, int64_t scale_cols) {
+    if (M <= 0 || Nc <= 0) return;
+    TcArgs a{};
+    a.M = M;
+    a.N = Nc;
+    a.BN = (int)std::min<int64_t>(256, cdiv(Nc, 16) * 16);
+    a.nk = (int)cdiv(K, 64);
+    a.nk0 = a.nk;
+    a.epi = EPI_BF16_ROWSCALE;
+    a.out = C;
+    a.ldc = ldc;
+    a.rowscale = rowscale;
+    a.scale_cols = scale_cols;
+    CUtensorMap ma = make_map(D, K, M, ldd, TC_BM);
+    CUtensorMap mb = make_map(B, K, Nc, ldb, a.BN);
+    launch_tc<false, false>(c, ma, ma, mb, a, dim3((unsigned)cdiv(M, TC_BM), (unsigned)cdiv(Nc, a.BN), 1));
+}
+
+}  // namespace bns

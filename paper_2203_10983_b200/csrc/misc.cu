@@ -204,6 +204,17 @@ __global__ void k_wpack(const float* __restrict__ W, int64_t rows_p, int64_t col
     if (Wt) Wt[t] = from_f<T>(v);
 }
 
+// W^T for the tcgen05 forward: WT[n][kw], kw = half * K64 + j  <->  padded row half * dpin + j (0 if j >= dpin)
+__global__ void k_wpack_t(const float* __restrict__ Wp, int64_t cols_p, int64_t dpin, int64_t K64, int64_t Kw,
+                          __nv_bfloat16* __restrict__ WT) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cols_p * Kw) return;
+    int64_t n = t / Kw, kw = t % Kw;
+    int64_t half = kw / K64, j = kw % K64;
+    float v = (j < dpin) ? Wp[(half * dpin + j) * cols_p + n] : 0.f;
+    WT[t] = __float2bfloat16_rn(v);
+}
+
 void launch_wpack(Ctx& c, const float* W, int l, bool /*host_src*/) {
     const int64_t rp = c.wrows[l], cp = c.wcols[l];
     const unsigned grid = (unsigned)((rp * cp + 255) / 256);
@@ -215,6 +226,13 @@ void launch_wpack(Ctx& c, const float* W, int l, bool /*host_src*/) {
         k_wpack<float><<<grid, 256, 0, c.stream>>>(W, rp, cp, c.dims[l], c.dp[l], c.dims[l + 1], sage, c.Wpad[l],
                                                    nullptr);
     c.kernels += 1;
+    if (c.use_tc) {
+        const int64_t K64 = (c.dp[l] + 63) / 64 * 64;
+        const int64_t n = cp * c.wkw[l];
+        k_wpack_t<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.Wpad[l], cp, c.dp[l], K64, c.wkw[l],
+                                                                     (__nv_bfloat16*)c.WT[l]);
+        c.kernels += 1;
+    }
     BNS_CHECK_LAUNCH();
 }
 
