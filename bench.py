@@ -166,6 +166,14 @@ def gemm_flops(dp, L, n_in, sage):
     return f
 
 
+def max_over_ranks(x: float, dist, device) -> float:
+    """max of a per-rank scalar over all ranks (device time is taken as the slowest rank's)."""
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -184,7 +192,9 @@ def latest_traffic():
     if not best:
         return None
     try:
-        return json.load(open(best)).get("dram_bytes_per_launch")
+        d = json.load(open(best))
+        return {"dram_bytes_per_step": d.get("spmm_dram_bytes_per_step"), "source": os.path.relpath(best, ROOT),
+                "note": d.get("note")}
     except (OSError, ValueError):
         return None
 
@@ -326,12 +336,7 @@ def run_ours(args):
     t1_times = ctx.times()
     ph = {k: (t1_times[k] - t0_times[k]) / args.steps for k in t1_times}
     cnt = ctx.counts()
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_max = float(t.item())
-    else:
-        total_max = total_ms
+    total_max = max_over_ranks(total_ms, dist, "cuda") if world > 1 else total_ms
     ms_per_step = total_max / args.steps
     value = 1000.0 / ms_per_step
 
@@ -354,9 +359,7 @@ def run_ours(args):
             b.synchronize()
             e_ms += a.elapsed_time(b)
         if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+            e_ms = max_over_ranks(e_ms, dist, "cuda")
         wbytes = sum(w.numel() * 4 for w in Wh)
         e2e = {"value": 1000.0 * args.steps / e_ms, "unit": UNIT, "h2d_bytes_per_step": wbytes,
                "d2h_bytes_per_step": 2 * wbytes + 16,
@@ -403,6 +406,9 @@ def run_ours(args):
                          "algorithmic_bytes_per_step": fwd_b + bwd_b, "spmm_ms_per_step": spmm_ms,
                          "spmm_share_of_step": spmm_ms / ms_per_step,
                          "gather_working_set_bytes": ws_bytes, "l2_bytes": l2,
+                         "regime": ("L2-resident gathers (working set of the hidden layers fits the 126 MB L2): "
+                                    "algorithmic GB/s above the HBM copy peak is served from L2, see traffic")
+                         if ws_bytes <= l2 else "DRAM-resident gathers",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peaks else "fallback 6.65 TB/s"},
             "roofline_gemm": {"bound": "tensor" if prec == bns.BNS_BF16 else "alu", "achieved": gf / (gemm_ms * 1e-3) / 1e12
                               if gemm_ms > 0 else None, "unit": "TFLOP/s", "flops_per_step": gf, "gemm_ms_per_step": gemm_ms,

@@ -323,6 +323,7 @@ void sample_boundary(Ctx& c, double p, uint64_t seed, uint64_t epoch) {
     c.p = p;
     c.inv_p = p > 0.0 ? 1.0 / p : 0.0;
     c.sampled = false;
+    std::unique_ptr<PhaseTimer> total(new PhaseTimer(c, BNS_PH_SAMPLE_TOTAL));
     {
         PhaseTimer t(c, BNS_PH_SAMPLE);
         launch_sample(c, T, seed, epoch);
@@ -335,6 +336,7 @@ void sample_boundary(Ctx& c, double p, uint64_t seed, uint64_t epoch) {
         launch_bwd_segments(c);
         if (c.layer == BNS_LAYER_GCN) launch_gcn_cscale(c);
     }
+    total.reset();
     const int64_t nslot = 2 * m + 1 + 8;
     BNS_CUDA(cudaMemcpyAsync(c.h_seg_pos, c.d_seg_pos, nslot * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
     BNS_CUDA(cudaStreamSynchronize(c.stream));
@@ -388,6 +390,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     const int64_t n_in = P.n_in;
     const float inv_p = (float)c.inv_p;
 
+    std::unique_ptr<PhaseTimer> total(new PhaseTimer(c, BNS_PH_EPOCH_TOTAL));
     // weights may be host or device pointers
     cudaPointerAttributes attr{};
     bool host_w = false;
@@ -535,6 +538,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         PhaseTimer t(c, BNS_PH_UPDATE);
         launch_sgd(c, W.data(), host_w ? G.data() : (G_in ? G.data() : nullptr), lr);
     }
+    total.reset();
     double scal[2];
     int32_t nonfinite = 0;
     BNS_CUDA(cudaMemcpyAsync(scal, c.d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c.stream));
@@ -651,7 +655,6 @@ bns_status bns_epoch(bns_ctx* h, float* const* weights, float lr, float* const* 
         if (!weights[l]) { c.err = "weights[l] is NULL"; return BNS_ERR_INVALID; }
     return guard(h, [&] {
         BNS_CUDA(cudaSetDevice(c.cfg.device));
-        PhaseTimer t(c, BNS_PH_EPOCH_TOTAL);
         epoch(c, weights, lr, grads, loss, acc);
     });
 }

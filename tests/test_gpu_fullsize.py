@@ -1,0 +1,107 @@
+"""Full-size parity (BASELINE.json configs[1], Reddit-shaped: 232,965 nodes, 114.6 M arcs, 602 features, SAGE 4x256):
+
+* m = 1 in bench.py's launch configuration (bf16, tcgen05 GEMMs): sampled rows of Z^1 and H^1 recomputed one by one
+  in float64 from raw neighbours (PAPER.md:100 / R1), and a finite loss;
+* m = 8, p = 0.1 on one GPU (LOCAL transport): keep masks, U_i and S_{i,j} bit-exact against the oracle's plan +
+  sample at full size, and sampled rows of Z^1 recomputed from the oracle's U_i (1/p on kept halo columns, R3).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2203_10983_b200 import bns
+from paper_2203_10983_b200 import inputs as I
+
+from gpu_harness import GpuRun, parallel
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+SEED = I.BNS_SEED
+
+
+@pytest.fixture(scope="module")
+def reddit():
+    sh = I.SHAPES["reddit"]
+    indptr, indices = I.rmat(sh.N, sh.nnz)
+    y = I.labels(sh.N, sh.C, sh.train_frac)
+    return sh, indptr, indices, y
+
+
+def z_rows(indptr, indices, X_of, rows, kept_of=None, inv_p=1.0, part=None):
+    """z_v = (1/deg_G v) Σ_{u ∈ N(v), kept} c_u x_u in float64 for the listed gids"""
+    out = []
+    for v in rows:
+        nb = indices[indptr[v]:indptr[v + 1]]
+        if len(nb) == 0:
+            out.append(np.zeros(X_of(np.array([v])).shape[1]))
+            continue
+        if kept_of is None:
+            use, c = nb, np.ones(len(nb))
+        else:
+            inner = part[nb] == part[v]
+            keep = inner | np.isin(nb, kept_of)
+            use = nb[keep]
+            c = np.where(inner[keep], 1.0, inv_p)
+        out.append((X_of(use).astype(np.float64) * c[:, None]).sum(0) / len(nb))
+    return np.array(out)
+
+
+def test_reddit_m1_bench_config(reddit):
+    sh, indptr, indices, y = reddit
+    part = np.zeros(sh.N, np.int32)
+    X = I.features(np.arange(sh.N, dtype=np.int32), sh.d0)
+    run = GpuRun(indptr, indices, part, 1, sh.dims, sh.layer, bns.BNS_BF16, X, y, flags=0)
+    try:
+        Ws = I.weights(sh.dims, sh.layer)
+        run.sample(0.1, SEED, 0)
+        loss, acc, G, _ = run.epoch(Ws, 0.0)
+        assert np.isfinite(loss) and 0.5 * np.log(sh.C) < loss < 3 * np.log(sh.C)
+        rng = np.random.default_rng(0)
+        rows = np.sort(rng.choice(sh.N, 400, replace=False))
+        deg = np.diff(indptr)
+        rows = np.union1d(rows, np.argsort(-deg)[:8])          # include the biggest hubs (split rows)
+        Z = run.ctx[0].rows(bns.BNS_Q_Z, 1, sh.d0)
+        zr = z_rows(indptr, indices, lambda g: X[g], rows)
+        err = np.abs(Z[rows] - zr).max() / np.abs(zr).max()
+        assert err < 2e-2, err
+        H1 = run.ctx[0].rows(bns.BNS_Q_H, 1, sh.hidden)
+        W0 = Ws[0].astype(np.float64)
+        pre = np.concatenate([zr, X[rows].astype(np.float64)], 1) @ W0
+        h = np.maximum(pre, 0)
+        err = np.abs(H1[rows] - h).max() / np.abs(h).max()
+        assert err < 2e-2, err
+    finally:
+        run.close()
+
+
+def test_reddit_m8_sampling_bitexact_and_rows(reddit):
+    sh, indptr, indices, y = reddit
+    m, p = 8, 0.1
+    part = I.partition(indptr, indices, m, "ldg2")
+    dims = [sh.d0, 16, 8]
+    X = I.features(np.arange(sh.N, dtype=np.int32), sh.d0)
+    run = GpuRun(indptr, indices, part, m, dims, sh.layer, bns.BNS_BF16, X, y, flags=0, max_p=0.2)
+    orc = O.Oracle(indptr, indices, part, m, [1, 1], 0, np.zeros((sh.N, 1), np.float32), np.zeros(sh.N, np.int32))
+    try:
+        for e in (0, 1):
+            run.sample(p, SEED, e)
+            orc.sample(p, SEED, e)
+            for r in range(m):
+                c = run.ctx[r]
+                assert np.array_equal(c.mask(), orc.list(O.KEEP, r).astype(np.uint8))
+                assert np.array_equal(c.i32(bns.BNS_Q_HALO), orc.list(O.U_LIST, r))
+                S, So = c.i32(bns.BNS_Q_SEND), c.i64(bns.BNS_Q_SEND_OFF)
+                for j in range(m):
+                    assert np.array_equal(S[So[j]:So[j + 1]], orc.list(O.S_LIST, r, j))
+        Ws = I.weights(dims, sh.layer)
+        run.epoch(Ws, 0.0)
+        rng = np.random.default_rng(1)
+        for r in (0, 5):
+            V = run.inner[r]
+            Z = run.ctx[r].rows(bns.BNS_Q_Z, 1, sh.d0)
+            k = np.sort(rng.choice(len(V), 200, replace=False))
+            U = orc.list(O.U_LIST, r)
+            zr = z_rows(indptr, indices, lambda g: X[g], V[k], kept_of=U, inv_p=1.0 / p, part=part)
+            err = np.abs(Z[k] - zr).max() / np.abs(zr).max()
+            assert err < 2e-2, (r, err)
+    finally:
+        run.close()
