@@ -46,6 +46,79 @@ template <> struct Vec<__nv_bfloat16> {
     }
 };
 
+// Packed fp32x2 accumulate (sm_100 FFMA2 / FADD2): acc[0..1] += s * (x, y)  /  acc[0..1] += (x, y)
+__device__ __forceinline__ void ffma2(float* acc, float x, float y, float s) {
+    uint64_t c, a, b;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(c) : "f"(acc[0]), "f"(acc[1]));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(x), "f"(y));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(s));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[0]), "=f"(acc[1]) : "l"(c));
+}
+__device__ __forceinline__ void fadd2(float* acc, float x, float y) {
+    uint64_t c, a;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(c) : "f"(acc[0]), "f"(acc[1]));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(x), "f"(y));
+    asm("add.rn.f32x2 %0, %1, %0;" : "+l"(c) : "l"(a));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[0]), "=f"(acc[1]) : "l"(c));
+}
+// Packed-pair accumulators kept as 64-bit registers (no repacking inside the edge loop).
+__device__ __forceinline__ uint64_t pk2(float x, float y) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& x, float& y) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(r));
+}
+__device__ __forceinline__ void ffma2p(uint64_t& acc, uint64_t a, uint64_t s2) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(s2));
+}
+__device__ __forceinline__ void fadd2p(uint64_t& acc, uint64_t a) {
+    asm("add.rn.f32x2 %0, %1, %0;" : "+l"(acc) : "l"(a));
+}
+// acc2 (VN/2 pairs) += s * v (SCALED) or += v
+template <typename T, bool SCALED> __device__ __forceinline__ void acc_vec2(uint64_t* acc2, const typename Vec<T>::raw& v, uint64_t s2);
+template <> __device__ __forceinline__ void acc_vec2<float, true>(uint64_t* a, const float4& v, uint64_t s2) {
+    ffma2p(a[0], pk2(v.x, v.y), s2);
+    ffma2p(a[1], pk2(v.z, v.w), s2);
+}
+template <> __device__ __forceinline__ void acc_vec2<float, false>(uint64_t* a, const float4& v, uint64_t) {
+    fadd2p(a[0], pk2(v.x, v.y));
+    fadd2p(a[1], pk2(v.z, v.w));
+}
+template <> __device__ __forceinline__ void acc_vec2<__nv_bfloat16, true>(uint64_t* a, const uint4& v, uint64_t s2) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ffma2p(a[k], pk2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xffff0000u)), s2);
+}
+template <> __device__ __forceinline__ void acc_vec2<__nv_bfloat16, false>(uint64_t* a, const uint4& v, uint64_t) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) fadd2p(a[k], pk2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xffff0000u)));
+}
+
+// acc (VN floats) += s * v, or += v when SCALED is false
+template <typename T, bool SCALED> __device__ __forceinline__ void acc_vec(float* acc, const typename Vec<T>::raw& v, float s);
+template <> __device__ __forceinline__ void acc_vec<float, true>(float* acc, const float4& v, float s) {
+    ffma2(acc, v.x, v.y, s);
+    ffma2(acc + 2, v.z, v.w, s);
+}
+template <> __device__ __forceinline__ void acc_vec<float, false>(float* acc, const float4& v, float) {
+    fadd2(acc, v.x, v.y);
+    fadd2(acc + 2, v.z, v.w);
+}
+template <> __device__ __forceinline__ void acc_vec<__nv_bfloat16, true>(float* acc, const uint4& v, float s) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ffma2(acc + 2 * k, __uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xffff0000u), s);
+}
+template <> __device__ __forceinline__ void acc_vec<__nv_bfloat16, false>(float* acc, const uint4& v, float) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) fadd2(acc + 2 * k, __uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xffff0000u));
+}
+
 template <typename T> __device__ __forceinline__ float to_f(T x);
 template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
 template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }

@@ -68,60 +68,88 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
     *reinterpret_cast<typename V::raw*>(static_cast<T*>(a.out) + row * a.ld_out + vi * VN) = V::from_float(acc);
 }
 
-template <typename T, int LPR, int VPL>
+// SC: per-edge column scale -- 0 none (backward modes, and the forward when every column has c_u = 1),
+//     1 c_u = 1/p for halo columns (col >= n_in, SAGE forward), 2 c_u from cscale[] (GCN forward).
+template <typename T, int LPR, int VPL, int SC>
 __global__ void __launch_bounds__(256) k_spmm(const SpmmArgs a) {
     using V = Vec<T>;
     using R = typename V::raw;
     constexpr int VN = V::N;
     constexpr int G = 32 / LPR;                              // edge groups per warp
-    constexpr int U0 = (VPL <= 1) ? 4 : (VPL <= 2) ? 2 : 1;
+    constexpr int U0 = (VPL <= 1) ? 8 : (VPL <= 2) ? 4 : (VPL <= 4) ? 2 : 1;
     constexpr int U = (G * U0 > 32) ? (32 / G) : U0;         // edges in flight per group
     static_assert(32 % (G * U) == 0, "bad unroll");
     const int lane = threadIdx.x & 31, g = lane / LPR, l = lane % LPR;
     const int nvec = a.d / VN;
-    const T* __restrict__ src = static_cast<const T*>(a.src);
+    const char* __restrict__ base = reinterpret_cast<const char*>(static_cast<const R*>(a.src) + l);
+    const uint32_t rvb = (uint32_t)(a.ld_src * sizeof(T));   // row pitch in bytes (32-bit multiply per edge)
+    // lanes past the row end re-load the last vector (same address as a live lane: no extra sectors) and
+    // accumulate into registers that are never stored -- no branches in the edge loop
+    int voff[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) voff[v] = min(l + v * LPR, nvec - 1) - l;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t sid = warp; sid < a.n_segs; sid += nwarps) {
         const Seg s = a.segs[sid];
-        float acc[VPL][VN];
+        uint64_t acc2[VPL][VN / 2];
 #pragma unroll
         for (int v = 0; v < VPL; ++v)
 #pragma unroll
-            for (int k = 0; k < VN; ++k) acc[v][k] = 0.f;
+            for (int k = 0; k < VN / 2; ++k) acc2[v][k] = 0ull;
         for (int64_t eb = s.e0; eb < s.e1; eb += 32) {
             const int cnt = (s.e1 - eb < 32) ? (int)(s.e1 - eb) : 32;
             int32_t ci = 0;
             float sc = 1.f;
             if (lane < cnt) {
                 ci = a.col[eb + lane];
-                if (a.mode == SAGE_FWD) sc = (ci >= a.n_in) ? a.inv_p : 1.f;
-                else if (a.mode == GCN_FWD) sc = a.cscale[ci];
+                if (SC == 1) sc = (ci >= a.n_in) ? a.inv_p : 1.f;
+                if (SC == 2) sc = a.cscale[ci];
             }
-            for (int j0 = 0; j0 < cnt; j0 += G * U) {
-                R r[U][VPL];
-                float sj[U];
+            if (cnt == 32) {
+                // full chunk: no bounds checks on the edges
+#pragma unroll 1
+                for (int j0 = 0; j0 < 32; j0 += G * U) {
+                    R r[U][VPL];
+                    uint64_t sj[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int j = j0 + u * G + g;
-                    const int32_t cj = __shfl_sync(0xffffffffu, ci, j);
-                    sj[u] = __shfl_sync(0xffffffffu, sc, j);
-                    const bool ok = j < cnt;
-                    const R* rowp = reinterpret_cast<const R*>(src + (int64_t)cj * a.ld_src);
+                    for (int u = 0; u < U; ++u) {
+                        const int j = j0 + u * G + g;
+                        const uint32_t cj = (uint32_t)__shfl_sync(0xffffffffu, ci, j);
+                        if (SC) {
+                            const float t = __shfl_sync(0xffffffffu, sc, j);
+                            sj[u] = pk2(t, t);
+                        }
+                        const R* rowp = reinterpret_cast<const R*>(base + (uint64_t)cj * rvb);
 #pragma unroll
-                    for (int v = 0; v < VPL; ++v) {
-                        const int vi = l + v * LPR;
-                        if (ok && vi < nvec) r[u][v] = ldg_nc(rowp + vi);
-                        else r[u][v] = R{};
+                        for (int v = 0; v < VPL; ++v)
+                            r[u][v] = ldg_nc(rowp + voff[v]);
                     }
-                    if (!ok) sj[u] = 0.f;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int v = 0; v < VPL; ++v)
+                            acc_vec2<T, SC != 0>(acc2[v], r[u][v], SC ? sj[u] : 0ull);
                 }
+            } else {
+                for (int j0 = 0; j0 < cnt; j0 += G) {
+                    const int j = j0 + g;
+                    const uint32_t cj = (uint32_t)__shfl_sync(0xffffffffu, ci, j & 31);
+                    const float t = SC ? __shfl_sync(0xffffffffu, sc, j & 31) : 1.f;
+                    if (j < cnt) {
+                        const R* rowp = reinterpret_cast<const R*>(base + (uint64_t)cj * rvb);
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-#pragma unroll
-                    for (int v = 0; v < VPL; ++v) V::add_scaled(acc[v], r[u][v], sj[u]);
+                        for (int v = 0; v < VPL; ++v)
+                            acc_vec2<T, SC != 0>(acc2[v], ldg_nc(rowp + voff[v]), pk2(t, t));
+                    }
+                }
             }
         }
+        float acc[VPL][VN];
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+#pragma unroll
+            for (int k = 0; k < VN / 2; ++k) upk2(acc2[v][k], acc[v][2 * k], acc[v][2 * k + 1]);
         if (G > 1) {
 #pragma unroll
             for (int o = LPR; o < 32; o <<= 1)
@@ -179,7 +207,13 @@ __global__ void __launch_bounds__(256) k_spmm_fixup(const SpmmArgs a) {
 
 template <typename T, int LPR, int VPL>
 static void go(Ctx& c, const SpmmArgs& a, unsigned grid) {
-    k_spmm<T, LPR, VPL><<<grid, 256, 0, c.stream>>>(a);
+    // per-edge column scale needed?  SAGE forward only when halo columns carry 1/p != 1
+    int sc = 0;
+    if (a.mode == GCN_FWD) sc = 2;
+    else if (a.mode == SAGE_FWD && a.inv_p != 1.f) sc = 1;
+    if (sc == 0) k_spmm<T, LPR, VPL, 0><<<grid, 256, 0, c.stream>>>(a);
+    else if (sc == 1) k_spmm<T, LPR, VPL, 1><<<grid, 256, 0, c.stream>>>(a);
+    else k_spmm<T, LPR, VPL, 2><<<grid, 256, 0, c.stream>>>(a);
 }
 
 template <typename T>

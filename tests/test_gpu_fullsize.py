@@ -78,6 +78,7 @@ def test_reddit_m8_sampling_bitexact_and_rows(reddit):
     m, p = 8, 0.1
     part = I.partition(indptr, indices, m, "ldg2")
     dims = [sh.d0, 16, 8]
+    y = I.labels(sh.N, dims[-1], sh.train_frac)
     X = I.features(np.arange(sh.N, dtype=np.int32), sh.d0)
     run = GpuRun(indptr, indices, part, m, dims, sh.layer, bns.BNS_BF16, X, y, flags=0, max_p=0.2)
     orc = O.Oracle(indptr, indices, part, m, [1, 1], 0, np.zeros((sh.N, 1), np.float32), np.zeros(sh.N, np.int32))
