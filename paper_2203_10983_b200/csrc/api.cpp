@@ -388,7 +388,8 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     const size_t ts = tsize(c);
     const bool sage = c.layer == BNS_LAYER_SAGE_MEAN;
     const int64_t n_in = P.n_in;
-    const float inv_p = (float)c.inv_p;
+    // c_u = 1/p only exists on halo columns; with no halo every column scale is 1 (the kernels then skip it)
+    const float inv_p = (c.n_halo > 0) ? (float)c.inv_p : 1.f;
 
     std::unique_ptr<PhaseTimer> total(new PhaseTimer(c, BNS_PH_EPOCH_TOTAL));
     // weights may be host or device pointers

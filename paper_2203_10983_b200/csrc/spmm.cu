@@ -71,7 +71,7 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
 // SC: per-edge column scale -- 0 none (backward modes, and the forward when every column has c_u = 1),
 //     1 c_u = 1/p for halo columns (col >= n_in, SAGE forward), 2 c_u from cscale[] (GCN forward).
 template <typename T, int LPR, int VPL, int SC>
-__global__ void __launch_bounds__(256) k_spmm(const SpmmArgs a) {
+__global__ void __launch_bounds__(256, (VPL <= 1) ? 4 : (VPL <= 2) ? 3 : 2) k_spmm(const SpmmArgs a) {
     using V = Vec<T>;
     using R = typename V::raw;
     constexpr int VN = V::N;
@@ -246,16 +246,31 @@ static void dispatch(Ctx& c, const SpmmArgs& a, unsigned grid) {
 #undef BNS_SPMM_CASE
 }
 
-void launch_spmm(Ctx& c, const SpmmArgs& a) {
-    if (a.n_segs <= 0) return;
-    unsigned grid = (unsigned)std::min<int64_t>((a.n_segs + 7) / 8, 148 * 32);
-    if (c.prec == BNS_BF16) dispatch<__nv_bfloat16>(c, a, grid);
-    else dispatch<float>(c, a, grid);
-    BNS_CHECK_LAUNCH();
-    if (c.prec == BNS_BF16) k_spmm_fixup<__nv_bfloat16><<<grid, 256, 0, c.stream>>>(a);
-    else k_spmm_fixup<float><<<grid, 256, 0, c.stream>>>(a);
-    c.kernels += 2;
-    BNS_CHECK_LAUNCH();
+// Feature-dimension tiling: when the gathered rows (n_in + |U| rows x d) exceed an L2 budget, the aggregation is
+// run as several passes over column tiles of 512 bytes per row, each with an L2-resident working set (the column
+// indices are re-read per pass: 4 B per edge against 512 B of row data).
+constexpr int64_t kL2Budget = 96ll << 20;
+
+void launch_spmm(Ctx& c, const SpmmArgs& a0) {
+    if (a0.n_segs <= 0) return;
+    const int64_t ts = c.prec == BNS_BF16 ? 2 : 4;
+    const int64_t rows = c.plan.n_in + c.n_halo;
+    const int64_t tile = (rows * a0.d * ts > kL2Budget) ? std::min<int64_t>(a0.d, 512 / ts) : a0.d;
+    unsigned grid = (unsigned)std::min<int64_t>((a0.n_segs + 7) / 8, 148 * 32);
+    for (int64_t c0 = 0; c0 < a0.d; c0 += tile) {
+        SpmmArgs a = a0;
+        a.d = (int32_t)std::min<int64_t>(tile, a0.d - c0);
+        a.src = static_cast<const char*>(a0.src) + c0 * ts;
+        a.out = static_cast<char*>(a0.out) + c0 * ts;
+        if (a0.self) a.self = static_cast<const char*>(a0.self) + c0 * ts;
+        if (c.prec == BNS_BF16) dispatch<__nv_bfloat16>(c, a, grid);
+        else dispatch<float>(c, a, grid);
+        BNS_CHECK_LAUNCH();
+        if (c.prec == BNS_BF16) k_spmm_fixup<__nv_bfloat16><<<grid, 256, 0, c.stream>>>(a);
+        else k_spmm_fixup<float><<<grid, 256, 0, c.stream>>>(a);
+        c.kernels += 2;
+        BNS_CHECK_LAUNCH();
+    }
 }
 
 }  // namespace bns
