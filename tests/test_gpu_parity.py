@@ -256,3 +256,22 @@ def test_epoch_before_sample_is_state_error():
         assert e.value.code == bns.BNS_ERR_INVALID
     finally:
         run.close()
+
+
+def test_nccl_transport_world1_matches_none():
+    """The NCCL transport (communicator init, grouped send/recv skipping self, ncclAllReduce of the gradient and
+    loss scalars) at world = 1 gives the same bits as no transport (a 1-GPU box cannot host 2 NCCL ranks)."""
+    indptr, indices, part, X, y = wl(2000, 40000, 1, 24, 5, 12)
+    dims = [24, 16, 5]
+    outs = []
+    for transport in (bns.BNS_TRANSPORT_NONE, bns.BNS_TRANSPORT_NCCL):
+        nid = bns.bns_get_unique_id() if transport == bns.BNS_TRANSPORT_NCCL else None
+        c = bns.Context(rank=0, world=1, dims=dims, layer=0, precision=bns.BNS_BF16, indptr=indptr, indices=indices,
+                        part_of=part, features=X, labels=y, transport=transport, nccl_id=nid)
+        Ws = [w.copy() for w in I.weights(dims, 0)]
+        G = [np.zeros_like(w) for w in Ws]
+        c.sample_boundary(0.3, SEED, 1)
+        loss, acc = c.epoch(Ws, 0.1, G)
+        outs.append((loss, acc, [w.tobytes() for w in Ws], [g.tobytes() for g in G]))
+        c.close()
+    assert outs[0] == outs[1]
