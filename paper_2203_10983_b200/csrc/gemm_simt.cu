@@ -93,19 +93,24 @@ __global__ void __launch_bounds__(256) k_gemm(int64_t M, int64_t N, int64_t K, c
     }
 }
 
+// fixed-order sum of the split-K partial slices (deterministic), 4 columns per thread (N is a multiple of 8)
 __global__ void k_splitk_reduce(const float* __restrict__ part, int S, int64_t M, int64_t N, int64_t ldp,
                                 float* __restrict__ out, int64_t ldo) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= M * N) return;
-    int64_t i = t / N, j = t % N;
-    float s = 0.f;
-    for (int z = 0; z < S; ++z) s += part[(int64_t)z * M * ldp + i * ldp + j];
-    out[i * ldo + j] = s;
+    const int64_t n4 = N / 4;
+    if (t >= M * n4) return;
+    int64_t i = t / n4, j = (t % n4) * 4;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int z = 0; z < S; ++z) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(part + (int64_t)z * M * ldp + i * ldp + j));
+        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    *reinterpret_cast<float4*>(out + i * ldo + j) = s;
 }
 
 void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw) {
     const int64_t tot = K * N;
-    k_splitk_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, c.stream>>>(c.d_splitk, S, K, N, N, Wg, ldw);
+    k_splitk_reduce<<<(unsigned)((tot / 4 + 255) / 256), 256, 0, c.stream>>>(c.d_splitk, S, K, N, N, Wg, ldw);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -146,7 +151,7 @@ static void wgrad_t(Ctx& c, int64_t M, int64_t K, int64_t N, const void* A, int6
     k_gemm<T, float, 1><<<grid, 256, 0, c.stream>>>(K, N, M, (const T*)A, 0, lda, nullptr, 0, (const T*)D, ldd,
                                                     c.d_splitk, N, false, nullptr, 0, chunk);
     int64_t tot = K * N;
-    k_splitk_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, c.stream>>>(c.d_splitk, (int)S, K, N, N, Wg, ldw);
+    k_splitk_reduce<<<(unsigned)((tot / 4 + 255) / 256), 256, 0, c.stream>>>(c.d_splitk, (int)S, K, N, N, Wg, ldw);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
 }

@@ -84,152 +84,188 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// Persistent, warp-specialized: grid = min(#tiles, #SMs); tile t = (m-tile, n-tile, split) visited in
+// blockIdx-strided order.  warp 0 lane 0: TMA producer over a 4-stage smem ring; warp 1 lane 0: MMA issuer into
+// one of two TMEM accumulators (2 x 256 columns), so the epilogue of tile i overlaps the MMAs of tile i+1;
+// warps 2-5: epilogue (warp w drains TMEM lanes 32*(w%4) .. +31).
+constexpr int TC_THREADS = 192;
+
 template <bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
           const __grid_constant__ CUtensorMap mapB, const TcArgs args) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
     uint64_t* empty = full + TC_STAGES;
-    uint64_t* accum = empty + TC_STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+    uint64_t* tfull = empty + TC_STAGES;      // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;             // [2] accumulator drained (4 epilogue warps arrive)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t m0 = (int64_t)blockIdx.x * TC_BM;
-    const int64_t n0 = (int64_t)blockIdx.y * args.BN;
-    int kb0 = 0, kb1 = args.nk;
-    if (args.kb_per_split > 0) {
-        kb0 = blockIdx.z * args.kb_per_split;
-        kb1 = min(args.nk, kb0 + args.kb_per_split);
-    }
-    const int nk = max(0, kb1 - kb0);
+    const int64_t tiles_m = (args.M + TC_BM - 1) / TC_BM;
+    const int64_t tiles_n = (args.N + args.BN - 1) / args.BN;
+    const int splits = args.kb_per_split > 0 ? (args.nk + args.kb_per_split - 1) / args.kb_per_split : 1;
+    const int64_t tiles = tiles_m * tiles_n * splits;
+    auto decode = [&](int64_t t, int64_t& m0, int64_t& n0, int& z, int& kb0, int& nk) {
+        z = (int)(t / (tiles_m * tiles_n));
+        const int64_t r = t % (tiles_m * tiles_n);
+        m0 = (r % tiles_m) * TC_BM;
+        n0 = (r / tiles_m) * args.BN;
+        kb0 = args.kb_per_split > 0 ? z * args.kb_per_split : 0;
+        const int kb1 = args.kb_per_split > 0 ? min(args.nk, kb0 + args.kb_per_split) : args.nk;
+        nk = kb1 - kb0;    // >= 1 by construction of the split count
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        mbar_init(accum, 1);
+        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA1) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-
     const uint32_t b_bytes = (uint32_t)args.BN * TC_BK * 2;
-    if (warp == 0 && lane == 0 && nk > 0) {
-        // ---------------- TMA producer ----------------
-        for (int i = 0; i < nk; ++i) {
-            const int s = i % TC_STAGES;
-            const uint32_t ph = (uint32_t)(i / TC_STAGES) & 1u;
-            mbar_wait(&empty[s], ph ^ 1u);
-            uint8_t* sa = smem + s * TC_STAGE_BYTES;
-            uint8_t* sb = sa + TC_A_BYTES;
-            mbar_expect_tx(&full[s], TC_A_BYTES + b_bytes);
-            const int kb = kb0 + i;
-            if (!A_MN) {
-                // A K-major: box {64 (k), 128 (m)}; concat along K: blocks [0, nk0) from A0, the rest from A1
-                if (kb < args.nk0) tma_load_2d(&mapA0, &full[s], sa, kb * TC_BK, (int)m0);
-                else tma_load_2d(&mapA1, &full[s], sa, (kb - args.nk0) * TC_BK, (int)m0);
-            } else {
-                // A MN-major (A^T stored row-major as [k][m]): two boxes {64 (m), 64 (k)}
-                tma_load_2d(&mapA0, &full[s], sa, (int)m0, kb * TC_BK);
-                tma_load_2d(&mapA0, &full[s], sa + 8192, (int)m0 + 64, kb * TC_BK);
-            }
-            if (!B_MN) {
-                tma_load_2d(&mapB, &full[s], sb, kb * TC_BK, (int)n0);        // box {64 (k), BN (n)}
-            } else {
-                for (int j = 0; j < args.BN / 64; ++j)                         // boxes {64 (n), 64 (k)}
-                    tma_load_2d(&mapB, &full[s], sb + j * 8192, (int)n0 + 64 * j, kb * TC_BK);
-            }
-        }
-    } else if (warp == 1 && lane == 0 && nk > 0) {
-        // ---------------- MMA issuer ----------------
-        // instruction descriptor: D fp32, A/B bf16, A/B major, N >> 3, M >> 4
-        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
-                               ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(args.BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
-        for (int i = 0; i < nk; ++i) {
-            const int s = i % TC_STAGES;
-            const uint32_t ph = (uint32_t)(i / TC_STAGES) & 1u;
-            mbar_wait(&full[s], ph);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t sa = smem_u32(smem + s * TC_STAGE_BYTES);
-            const uint32_t sb = sa + TC_A_BYTES;
-#pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k) {
-                // K-major SW128: +32 B per 16-element k step inside the 128 B row; LBO unused (16), SBO = 8 rows
-                // MN-major SW128: +16 rows (2048 B) per k step; LBO = MN-atom stride (8 KB), SBO = 8 k-rows (1 KB)
-                const uint64_t ad = A_MN ? umma_desc(sa + k * 2048, 8192, 1024) : umma_desc(sa + k * 32, 16, 1024);
-                const uint64_t bd = B_MN ? umma_desc(sb + k * 2048, 8192, 1024) : umma_desc(sb + k * 32, 16, 1024);
-                umma_bf16(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
-            }
-            umma_commit(&empty[s]);
-        }
-        umma_commit(accum);
-    }
-    __syncwarp();
 
-    // ---------------- epilogue: TMEM -> registers -> global ----------------
-    if (nk > 0) {
-        mbar_wait(accum, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-    const int64_t row = m0 + warp * 32 + lane;
-    const int ncols = (args.N - n0 < args.BN) ? (int)(args.N - n0) : args.BN;
-    for (int c0 = 0; c0 < args.BN; c0 += 16) {
-        uint32_t r[16];
-        if (nk > 0) {
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        } else {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) r[q] = 0u;
-        }
-        if (row >= args.M || c0 >= ncols) continue;
-        float v[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
-        const int64_t col = n0 + c0;
-        if (args.epi == EPI_F32) {
-            float* o = static_cast<float*>(args.out) + (int64_t)blockIdx.z * args.split_stride + row * args.ldc + col;
-#pragma unroll
-            for (int h = 0; h < 4; ++h)
-                if (c0 + 4 * h < ncols) {
-                    float4 w = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
-                    if (args.relu) { w.x = fmaxf(w.x, 0.f); w.y = fmaxf(w.y, 0.f); w.z = fmaxf(w.z, 0.f); w.w = fmaxf(w.w, 0.f); }
-                    *reinterpret_cast<float4*>(o + 4 * h) = w;
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int64_t m0, n0;
+                int z, kb0, nk;
+                decode(t, m0, n0, z, kb0, nk);
+                for (int i = 0; i < nk; ++i) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    uint8_t* sa = smem + s * TC_STAGE_BYTES;
+                    uint8_t* sb = sa + TC_A_BYTES;
+                    mbar_expect_tx(&full[s], TC_A_BYTES + b_bytes);
+                    const int kb = kb0 + i;
+                    if (!A_MN) {
+                        // A K-major: box {64 (k), 128 (m)}; concat along K: blocks [0, nk0) from A0, the rest from A1
+                        if (kb < args.nk0) tma_load_2d(&mapA0, &full[s], sa, kb * TC_BK, (int)m0);
+                        else tma_load_2d(&mapA1, &full[s], sa, (kb - args.nk0) * TC_BK, (int)m0);
+                    } else {
+                        // A MN-major (A^T stored row-major as [k][m]): two boxes {64 (m), 64 (k)}
+                        tma_load_2d(&mapA0, &full[s], sa, (int)m0, kb * TC_BK);
+                        tma_load_2d(&mapA0, &full[s], sa + 8192, (int)m0 + 64, kb * TC_BK);
+                    }
+                    if (!B_MN) {
+                        tma_load_2d(&mapB, &full[s], sb, kb * TC_BK, (int)n0);        // box {64 (k), BN (n)}
+                    } else {
+                        for (int j = 0; j < args.BN / 64; ++j)                         // boxes {64 (n), 64 (k)}
+                            tma_load_2d(&mapB, &full[s], sb + j * 8192, (int)n0 + 64 * j, kb * TC_BK);
+                    }
+                    if (++s == TC_STAGES) { s = 0; ph ^= 1u; }
                 }
-        } else {
-            if (args.epi == EPI_BF16_ROWSCALE) {
-                const float rs = args.rowscale[row];
-#pragma unroll
-                for (int q = 0; q < 16; ++q)
-                    if (col + q < args.scale_cols) v[q] *= rs;
             }
-            if (args.relu)
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer ----------------
+            // instruction descriptor: D fp32, A/B bf16, A/B major, N >> 3, M >> 4
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                                   ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(args.BN >> 3) << 17) |
+                                   ((uint32_t)(TC_BM >> 4) << 24);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+                int64_t m0, n0;
+                int z, kb0, nk;
+                decode(t, m0, n0, z, kb0, nk);
+                const int b = it & 1;
+                mbar_wait(&tempty[b], (((uint32_t)it >> 1) & 1u) ^ 1u);   // accumulator b drained by the epilogue
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + (uint32_t)(b * 256);
+                for (int i = 0; i < nk; ++i) {
+                    mbar_wait(&full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t sa = smem_u32(smem + s * TC_STAGE_BYTES);
+                    const uint32_t sb = sa + TC_A_BYTES;
 #pragma unroll
-                for (int q = 0; q < 16; ++q) v[q] = fmaxf(v[q], 0.f);
-            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(args.out) + row * args.ldc + col;
+                    for (int k = 0; k < TC_BK / 16; ++k) {
+                        // K-major SW128: +32 B per 16-element k step inside the 128 B row; SBO = 8 rows (1 KB)
+                        // MN-major SW128: +16 rows (2 KB) per k step; LBO = MN-atom stride (8 KB), SBO = 8 k-rows
+                        const uint64_t ad = A_MN ? umma_desc(sa + k * 2048, 8192, 1024) : umma_desc(sa + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? umma_desc(sb + k * 2048, 8192, 1024) : umma_desc(sb + k * 32, 16, 1024);
+                        umma_bf16(d, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);     // stage free once these MMAs have read it
+                    if (++s == TC_STAGES) { s = 0; ph ^= 1u; }
+                }
+                umma_commit(&tfull[b]);         // accumulator b complete
+            }
+        }
+    } else {
+        // ---------------- epilogue: TMEM -> registers -> global (warps 2..5) ----------------
+        const int q = warp & 3;                 // TMEM lane quarter this warp may access
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            int64_t m0, n0;
+            int z, kb0, nk;
+            decode(t, m0, n0, z, kb0, nk);
+            const int b = it & 1;
+            mbar_wait(&tfull[b], ((uint32_t)it >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t row = m0 + q * 32 + lane;
+            const int ncols = (args.N - n0 < args.BN) ? (int)(args.N - n0) : args.BN;
+            const float rs = (args.epi == EPI_BF16_ROWSCALE && row < args.M) ? args.rowscale[row] : 1.f;
+            for (int c0 = 0; c0 < ncols; c0 += 16) {
+                uint32_t r[16];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 256 + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (row >= args.M) continue;
+                float v[16];
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-                if (c0 + 8 * h < ncols)
-                    *reinterpret_cast<uint4*>(o + 8 * h) = Vec<__nv_bfloat16>::from_float(v + 8 * h);
+                for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+                const int64_t col = n0 + c0;
+                if (args.epi == EPI_F32) {
+                    float* o = static_cast<float*>(args.out) + (int64_t)z * args.split_stride + row * args.ldc + col;
+#pragma unroll
+                    for (int h = 0; h < 4; ++h)
+                        if (c0 + 4 * h < ncols) {
+                            float4 w = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+                            if (args.relu) { w.x = fmaxf(w.x, 0.f); w.y = fmaxf(w.y, 0.f); w.z = fmaxf(w.z, 0.f); w.w = fmaxf(w.w, 0.f); }
+                            *reinterpret_cast<float4*>(o + 4 * h) = w;
+                        }
+                } else {
+                    if (args.epi == EPI_BF16_ROWSCALE)
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            if (col + k < args.scale_cols) v[k] *= rs;
+                    if (args.relu)
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) v[k] = fmaxf(v[k], 0.f);
+                    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(args.out) + row * args.ldc + col;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (c0 + 8 * h < ncols) *reinterpret_cast<uint4*>(o + 8 * h) = Vec<__nv_bfloat16>::from_float(v + 8 * h);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -273,12 +309,22 @@ static void launch_tc(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, cons
         BNS_CUDA(cudaFuncSetAttribute(k_gemm_tc<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
         configured = true;
     }
-    k_gemm_tc<A_MN, B_MN><<<grid, 128, TC_SMEM, c.stream>>>(a0, a1, b, args);
+    k_gemm_tc<A_MN, B_MN><<<grid, TC_THREADS, TC_SMEM, c.stream>>>(a0, a1, b, args);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static dim3 persistent_grid(int64_t tiles) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        BNS_CUDA(cudaGetDevice(&dev));
+        BNS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
+}
 
 // fwd: C[M x N] = [A0 | A1] · W, B = W^T stored [N][Kw] (Kw = 64-padded per concat half)
 void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64_t lda0, const void* A1, int64_t K1,
@@ -297,7 +343,7 @@ void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64
     CUtensorMap m0 = make_map(A0, K0, M, lda0, TC_BM);
     CUtensorMap m1 = A1 ? make_map(A1, K1, M, lda1, TC_BM) : m0;
     CUtensorMap mb = make_map(WT, Kw, N, Kw, a.BN);
-    launch_tc<false, false>(c, m0, m1, mb, a, dim3((unsigned)cdiv(M, TC_BM), (unsigned)cdiv(N, a.BN), 1));
+    launch_tc<false, false>(c, m0, m1, mb, a, persistent_grid(cdiv(M, TC_BM) * cdiv(N, a.BN)));
 }
 
 // dW partials: out[z][K x N] = A^T · D over k-block range z; A is [M_nodes][K] row-major, D is [M_nodes][N]
@@ -321,7 +367,7 @@ void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int6
     a.split_stride = K * N;
     CUtensorMap ma = make_map(A, K, Mn, lda, 64);
     CUtensorMap mb = make_map(D, N, Mn, ldd, 64);
-    launch_tc<true, true>(c, ma, ma, mb, a, dim3((unsigned)cdiv(K, TC_BM), (unsigned)cdiv(N, a.BN), (unsigned)S));
+    launch_tc<true, true>(c, ma, ma, mb, a, persistent_grid(cdiv(K, TC_BM) * cdiv(N, a.BN) * S));
     splitk_reduce(c, (int)S, K, N, Wg, ldw);
 }
 
@@ -342,7 +388,7 @@ void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t
     a.scale_cols = scale_cols;
     CUtensorMap ma = make_map(D, K, M, ldd, TC_BM);
     CUtensorMap mb = make_map(B, K, Nc, ldb, a.BN);
-    launch_tc<false, false>(c, ma, ma, mb, a, dim3((unsigned)cdiv(M, TC_BM), (unsigned)cdiv(Nc, a.BN), 1));
+    launch_tc<false, false>(c, ma, ma, mb, a, persistent_grid(cdiv(M, TC_BM) * cdiv(Nc, a.BN)));
 }
 
 }  // namespace bns

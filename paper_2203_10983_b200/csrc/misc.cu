@@ -161,18 +161,32 @@ void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlog
     BNS_CHECK_LAUNCH();
 }
 
+// 16-byte vectors: dpre = dh where h > 0 else 0 (bit select on the storage words; R12 ReLU'(0) = 0)
 template <typename T>
 __global__ void k_relu_mask(const T* __restrict__ dh, const T* __restrict__ h, int64_t ld, int64_t n,
                             T* __restrict__ dpre) {
+    using R = typename Vec<T>::raw;
+    constexpr int VN = Vec<T>::N;
+    const int64_t nv = n / VN;
+    const R* dv = reinterpret_cast<const R*>(dh);
+    const R* hv = reinterpret_cast<const R*>(h);
+    R* ov = reinterpret_cast<R*>(dpre);
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (; t < n; t += stride) dpre[t] = (to_f<T>(h[t]) > 0.f) ? dh[t] : from_f<T>(0.f);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; t < nv; t += stride) {
+        float a[VN], b[VN];
+        Vec<T>::to_float(dv[t], a);
+        Vec<T>::to_float(hv[t], b);
+#pragma unroll
+        for (int k = 0; k < VN; ++k) a[k] = (b[k] > 0.f) ? a[k] : 0.f;
+        ov[t] = Vec<T>::from_float(a);
+    }
 }
 
 void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre) {
-    const int64_t n = rows * ld;
+    const int64_t n = rows * ld;   // ld is a multiple of 8: whole 16-byte vectors
     if (n <= 0) return;
-    unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    unsigned grid = (unsigned)std::min<int64_t>((n / 4 + 255) / 256, 148 * 16);
     if (c.prec == BNS_BF16)
         k_relu_mask<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)dh, (const __nv_bfloat16*)h, ld,
                                                                n, (__nv_bfloat16*)dpre);

@@ -13,6 +13,8 @@
 // are in flight per lane.  fp32 accumulation for both storage types.  Hub rows (deg > kSeg) are split into several
 // segments whose fp32 partials are summed in segment order by k_spmm_fixup -- deterministic, and the split
 // depends only on the row length.
+#include <cstdlib>
+
 #include "common.h"
 #include "dev.cuh"
 #include "kernels.h"
@@ -132,16 +134,28 @@ __global__ void __launch_bounds__(256, (VPL <= 1) ? 4 : (VPL <= 2) ? 3 : 2) k_sp
                             acc_vec2<T, SC != 0>(acc2[v], r[u][v], SC ? sj[u] : 0ull);
                 }
             } else {
-                for (int j0 = 0; j0 < cnt; j0 += G) {
-                    const int j = j0 + g;
-                    const uint32_t cj = (uint32_t)__shfl_sync(0xffffffffu, ci, j & 31);
-                    const float t = SC ? __shfl_sync(0xffffffffu, sc, j & 31) : 1.f;
-                    if (j < cnt) {
+                // tail chunk: same U-deep batches; slots past the row end re-load the chunk's first row (a live
+                // address, cached) with scale 0, so there is no branch and U loads stay in flight
+                const int32_t c_first = __shfl_sync(0xffffffffu, ci, 0);
+                if (lane >= cnt) ci = c_first;
+                for (int j0 = 0; j0 < cnt; j0 += G * U) {
+                    R r[U][VPL];
+                    uint64_t sj[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int j = j0 + u * G + g;
+                        const uint32_t cj = (uint32_t)__shfl_sync(0xffffffffu, ci, j & 31);
+                        const float t = SC ? __shfl_sync(0xffffffffu, sc, j & 31) : 1.f;
+                        const float tt = (j < cnt) ? t : 0.f;
+                        sj[u] = pk2(tt, tt);
                         const R* rowp = reinterpret_cast<const R*>(base + (uint64_t)cj * rvb);
 #pragma unroll
-                        for (int v = 0; v < VPL; ++v)
-                            acc_vec2<T, SC != 0>(acc2[v], ldg_nc(rowp + voff[v]), pk2(t, t));
+                        for (int v = 0; v < VPL; ++v) r[u][v] = ldg_nc(rowp + voff[v]);
                     }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int v = 0; v < VPL; ++v) acc_vec2<T, true>(acc2[v], r[u][v], sj[u]);
                 }
             }
         }
@@ -255,7 +269,16 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
     if (a0.n_segs <= 0) return;
     const int64_t ts = c.prec == BNS_BF16 ? 2 : 4;
     const int64_t rows = c.plan.n_in + c.n_halo;
-    const int64_t tile = (rows * a0.d * ts > kL2Budget) ? std::min<int64_t>(a0.d, 512 / ts) : a0.d;
+    int64_t tile = a0.d;
+    if (rows * a0.d * ts > kL2Budget) {
+        static const int mode = [] { const char* e = std::getenv("BNS_SPMM_TILE"); return e ? std::atoi(e) : 0; }();
+        if (mode == 0) {
+            tile = std::min<int64_t>(a0.d, 512 / ts);                      // 512-byte tiles
+        } else {
+            const int64_t nt = (rows * a0.d * ts + kL2Budget - 1) / kL2Budget;   // balanced tiles
+            tile = ((a0.d + nt - 1) / nt + 7) / 8 * 8;
+        }
+    }
     unsigned grid = (unsigned)std::min<int64_t>((a0.n_segs + 7) / 8, 148 * 32);
     for (int64_t c0 = 0; c0 < a0.d; c0 += tile) {
         SpmmArgs a = a0;
