@@ -58,7 +58,9 @@ typedef enum {
 typedef enum {
     BNS_TRANSPORT_NONE = 0,   /* world must be 1 */
     BNS_TRANSPORT_NCCL = 1,   /* cfg.nccl_id: 128-byte ncclUniqueId, identical on all ranks (bns_get_unique_id) */
-    BNS_TRANSPORT_LOCAL = 2   /* cfg.group: in-process group from bns_group_create(world) */
+    BNS_TRANSPORT_LOCAL = 2,  /* cfg.group: in-process group from bns_group_create(world) */
+    BNS_TRANSPORT_NULL_EMULATE = 3  /* BENCHMARKING ONLY: run one rank of an m-rank job alone on one GPU; the
+                                       exchanges and the all-reduce are no-ops, so outputs are not the method's */
 } bns_transport;
 
 /* cfg.flags */

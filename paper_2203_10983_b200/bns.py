@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libbns.so")
 BNS_OK, BNS_ERR_INVALID, BNS_ERR_RUNTIME, BNS_ERR_STATE, BNS_ERR_OOM, BNS_ERR_NONFINITE = range(6)
 BNS_LAYER_SAGE_MEAN, BNS_LAYER_GCN = 0, 1
 BNS_FP32, BNS_BF16 = 0, 1
-BNS_TRANSPORT_NONE, BNS_TRANSPORT_NCCL, BNS_TRANSPORT_LOCAL = 0, 1, 2
+BNS_TRANSPORT_NONE, BNS_TRANSPORT_NCCL, BNS_TRANSPORT_LOCAL, BNS_TRANSPORT_NULL_EMULATE = 0, 1, 2, 3
 BNS_PLAN_ONLY, BNS_DEBUG_EXCHANGE_INDICES, BNS_TIMING, BNS_RETAIN_GRADS = 0x1, 0x2, 0x4, 0x8
 (BNS_Q_COUNTS, BNS_Q_INNER, BNS_Q_BOUNDARY, BNS_Q_BOUNDARY_OFF, BNS_Q_SENDCAND, BNS_Q_SENDCAND_OFF, BNS_Q_MASK,
  BNS_Q_HALO, BNS_Q_HALO_OFF, BNS_Q_SEND, BNS_Q_SEND_OFF, BNS_Q_H, BNS_Q_Z, BNS_Q_DH, BNS_Q_HALO_ROWS, BNS_Q_INDUCED,

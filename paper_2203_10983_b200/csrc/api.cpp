@@ -76,7 +76,7 @@ void validate(const bns_config* cfg, int64_t N, const int64_t* indptr, const int
     if (cfg->layer != BNS_LAYER_SAGE_MEAN && cfg->layer != BNS_LAYER_GCN) throw Error(BNS_ERR_INVALID, "bad layer");
     if (cfg->precision != BNS_FP32 && cfg->precision != BNS_BF16) throw Error(BNS_ERR_INVALID, "bad precision");
     if (cfg->world > 1 && cfg->transport != BNS_TRANSPORT_NCCL && cfg->transport != BNS_TRANSPORT_LOCAL &&
-        !(cfg->flags & BNS_PLAN_ONLY))
+        cfg->transport != BNS_TRANSPORT_NULL_EMULATE && !(cfg->flags & BNS_PLAN_ONLY))
         throw Error(BNS_ERR_INVALID, "world > 1 needs transport NCCL or LOCAL");
     if (N < 1 || !indptr || !indices || !part_of) throw Error(BNS_ERR_INVALID, "empty graph or NULL arrays");
     if (N >= INT32_MAX) throw Error(BNS_ERR_INVALID, "num_nodes must fit int32");
@@ -234,6 +234,12 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     BNS_CUDA(cudaMallocHost(&c.h_seg_pos, (2 * m + 1 + 8) * sizeof(int64_t)));
     c.d_ind_ptr = static_cast<int64_t*>(dalloc(c, (P.n_in + 1) * sizeof(int64_t)));
     c.d_ind_col = static_cast<int32_t*>(dalloc(c, (c.nnz_i + 1) * sizeof(int32_t)));
+    {
+        const int64_t nb = (c.nnz_i + 1023) / 1024;
+        c.d_ebits = static_cast<uint32_t*>(dalloc(c, (nb * 32 + 32) * sizeof(uint32_t)));
+        c.d_eblk = static_cast<int32_t*>(dalloc(c, (nb + 1) * sizeof(int32_t)));
+        c.d_eboff = static_cast<int64_t*>(dalloc(c, (nb + 2) * sizeof(int64_t)));
+    }
     const int64_t rmax = std::max<int64_t>(P.n_in, P.n_bd) + 1;
     c.d_row_cnt = static_cast<int32_t*>(dalloc(c, rmax * sizeof(int32_t)));
     c.d_row_nseg = static_cast<int32_t*>(dalloc(c, rmax * sizeof(int32_t)));

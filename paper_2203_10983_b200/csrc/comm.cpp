@@ -206,10 +206,21 @@ struct LocalTransport : Transport {
     void poll(Ctx&) override {}
 };
 
+// Timing emulation of one rank of an m-rank job on a single GPU: every call is a no-op (no rows move, no sum is
+// taken), so the rank runs exactly its own kernels with its own sampled sizes.  Results are NOT the method's.
+struct NullTransport : Transport {
+    void exchange(Ctx&, const void*, const int64_t*, void*, const int64_t*, size_t) override {}
+    void allreduce(Ctx&, float*, int64_t, double*, int64_t) override {}
+    int64_t allreduce_host_i64(Ctx&, int64_t v) override { return v; }
+    void poll(Ctx&) override {}
+};
+
 }  // namespace
 
 Transport* make_transport(Ctx& c) {
     switch (c.cfg.transport) {
+        case BNS_TRANSPORT_NULL_EMULATE:
+            return new NullTransport();
         case BNS_TRANSPORT_NCCL:
             if (!c.cfg.nccl_id) throw Error(BNS_ERR_INVALID, "transport NCCL needs cfg.nccl_id");
             return new NcclTransport(c, c.cfg.nccl_id);

@@ -117,6 +117,9 @@ struct Ctx {
     int32_t* d_slot_of_b = nullptr;
     int64_t* d_seg_pos = nullptr;  // [2m+1] compacted segment offsets
     int64_t* h_seg_pos = nullptr;  // pinned host copy
+    uint32_t* d_ebits = nullptr;   // induce: keep bit per static edge
+    int32_t* d_eblk = nullptr;     // induce: kept edges per 1024-edge block
+    int64_t* d_eboff = nullptr;    // induce: scanned block offsets
     int64_t* d_ind_ptr = nullptr;  // induced CSR (n_in+1)
     int32_t* d_ind_col = nullptr;
     int32_t* d_row_cnt = nullptr;  // scratch per row counts

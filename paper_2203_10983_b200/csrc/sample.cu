@@ -205,82 +205,115 @@ void launch_sample(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// a3 induce: per-row kept counts, scans, order-preserving write + forward segments
+// a3 induce, edge-parallel (balanced over nnz, so hub rows cost no more than their edges):
+//   K1 keep bit of every static edge (ballot words) + per-1024-edge counts, K2 scan of the counts,
+//   K3 order-preserving scatter of the kept (remapped) columns, K4 row pointers from the bit prefix + segment
+//   counts per row, scan, K5 segment list.
 // ---------------------------------------------------------------------------------------------
-__global__ void k_induce_count(const int64_t* __restrict__ ptr, const int32_t* __restrict__ col_enc, int64_t n_in,
-                               const int32_t* __restrict__ slot_of_b, int32_t* __restrict__ cnt,
-                               int32_t* __restrict__ nseg) {
-    const int lane = threadIdx.x & 31;
-    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < n_in; r += nwarps) {
-        int c = 0;
-        for (int64_t e = ptr[r] + lane; e < ptr[r + 1]; e += 32) {
-            int32_t x = col_enc[e];
-            c += (x >= 0 || slot_of_b[-x - 1] >= 0) ? 1 : 0;
-        }
+__device__ __forceinline__ bool edge_kept(int32_t x, const int32_t* __restrict__ slot_of_b) {
+    return x >= 0 || slot_of_b[-x - 1] >= 0;
+}
+
+__global__ void __launch_bounds__(1024) k_induce_flags(const int32_t* __restrict__ col_enc, int64_t nnz,
+                                                       const int32_t* __restrict__ slot_of_b,
+                                                       uint32_t* __restrict__ bits, int32_t* __restrict__ blk) {
+    const int64_t e = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    const int keep = (e < nnz) ? (edge_kept(col_enc[e], slot_of_b) ? 1 : 0) : 0;
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    if ((threadIdx.x & 31) == 0) bits[e >> 5] = b;
+    const int cnt = __syncthreads_count(keep);
+    if (threadIdx.x == 0) blk[blockIdx.x] = cnt;
+}
+
+__global__ void __launch_bounds__(1024) k_induce_scatter(const int32_t* __restrict__ col_enc, int64_t nnz,
+                                                         const int32_t* __restrict__ slot_of_b,
+                                                         const uint32_t* __restrict__ bits,
+                                                         const int64_t* __restrict__ boff, int64_t n_in,
+                                                         int32_t* __restrict__ out_col) {
+    __shared__ int32_t wsum[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t e = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    const uint32_t word = (e < nnz) ? bits[e >> 5] : 0u;
+    if (lane == 0) wsum[w] = __popc(word);
+    __syncthreads();
+    if (w == 0) {
+        int s = wsum[lane];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) {
-            cnt[r] = c;
-            nseg[r] = c > kSeg ? (c + kSeg - 1) / kSeg : 1;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
         }
+        wsum[lane] = s;
+    }
+    __syncthreads();
+    if (e < nnz && ((word >> lane) & 1u)) {
+        const int64_t pos = boff[blockIdx.x] + (w ? wsum[w - 1] : 0) + __popc(word & ((1u << lane) - 1u));
+        const int32_t x = col_enc[e];
+        out_col[pos] = x >= 0 ? x : (int32_t)n_in + slot_of_b[-x - 1];
     }
 }
 
-__global__ void k_induce_write(const int64_t* __restrict__ ptr, const int32_t* __restrict__ col_enc, int64_t n_in,
-                               const int32_t* __restrict__ slot_of_b, const int64_t* __restrict__ out_ptr,
-                               const int64_t* __restrict__ seg_off, int32_t* __restrict__ out_col,
-                               Seg* __restrict__ segs) {
-    const int lane = threadIdx.x & 31;
-    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < n_in; r += nwarps) {
-        int64_t base = out_ptr[r];
-        const int64_t b0 = base, b1 = out_ptr[r + 1];
-        for (int64_t e0 = ptr[r]; e0 < ptr[r + 1]; e0 += 32) {
-            int64_t e = e0 + lane;
-            int keep = 0;
-            int32_t y = 0;
-            if (e < ptr[r + 1]) {
-                int32_t x = col_enc[e];
-                if (x >= 0) { keep = 1; y = x; }
-                else {
-                    int32_t s = slot_of_b[-x - 1];
-                    if (s >= 0) { keep = 1; y = (int32_t)n_in + s; }
-                }
-            }
-            unsigned bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) out_col[base + __popc(bal & ((1u << lane) - 1u))] = y;
-            base += __popc(bal);
-        }
-        int64_t s0 = seg_off[r], ns = seg_off[r + 1] - s0;
-        for (int64_t k = lane; k < ns; k += 32) {
-            Seg sg;
-            sg.row = (int32_t)r;
-            sg.nseg = (int32_t)ns;
-            sg.e0 = b0 + k * kSeg;
-            sg.e1 = min(b1, sg.e0 + kSeg);
-            sg.first = s0;
-            segs[s0 + k] = sg;
-        }
+// number of kept edges before static edge position e
+__device__ __forceinline__ int64_t kept_before(int64_t e, const uint32_t* __restrict__ bits,
+                                               const int64_t* __restrict__ boff) {
+    const int64_t b = e >> 10;
+    int64_t s = boff[b];
+    for (int64_t w = b << 5; w < (e >> 5); ++w) s += __popc(bits[w]);
+    if (e & 31) s += __popc(bits[e >> 5] & ((1u << (e & 31)) - 1u));
+    return s;
+}
+
+__global__ void k_induce_rows(const int64_t* __restrict__ ptr, int64_t n_in, const uint32_t* __restrict__ bits,
+                              const int64_t* __restrict__ boff, int64_t* __restrict__ out_ptr,
+                              int32_t* __restrict__ nseg) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > n_in) return;
+    const int64_t a = kept_before(ptr[r], bits, boff);
+    out_ptr[r] = a;
+    if (r == n_in) return;
+    const int64_t cnt = kept_before(ptr[r + 1], bits, boff) - a;
+    nseg[r] = cnt > kSeg ? (int32_t)((cnt + kSeg - 1) / kSeg) : 1;
+}
+
+__global__ void k_induce_segs(const int64_t* __restrict__ out_ptr, int64_t n_in, const int64_t* __restrict__ seg_off,
+                              Seg* __restrict__ segs) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_in) return;
+    const int64_t b0 = out_ptr[r], b1 = out_ptr[r + 1];
+    const int64_t s0 = seg_off[r], ns = seg_off[r + 1] - s0;
+    for (int64_t k = 0; k < ns; ++k) {
+        Seg sg;
+        sg.row = (int32_t)r;
+        sg.nseg = (int32_t)ns;
+        sg.e0 = b0 + k * kSeg;
+        sg.e1 = min(b1, sg.e0 + kSeg);
+        sg.first = s0;
+        segs[s0 + k] = sg;
     }
 }
 
 void launch_induce(Ctx& c) {
     const int64_t n_in = c.plan.n_in;
+    const int64_t nnz = c.nnz_i;
     const int m = c.cfg.world;
     int64_t* tot = c.d_seg_pos + 2 * m + 1;   // [nnz_kept, n_seg_fwd, n_seg_bwd_halo]
-    unsigned grid = (unsigned)std::min<int64_t>((n_in + 7) / 8, 148 * 16);
-    if (grid == 0) grid = 1;
-    k_induce_count<<<grid, 256, 0, c.stream>>>(c.d_row_ptr, c.d_col_enc, n_in, c.d_slot_of_b, c.d_row_cnt,
-                                               c.d_row_nseg);
+    const int64_t nb = (nnz + 1023) / 1024;
+    if (nb > 0) {
+        k_induce_flags<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eblk);
+        k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_eblk, c.d_eboff, nb, tot + 0);
+        k_induce_scatter<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff,
+                                                              n_in, c.d_ind_col);
+        c.kernels += 3;
+    } else {
+        BNS_CUDA(cudaMemsetAsync(c.d_eboff, 0, sizeof(int64_t), c.stream));
+        BNS_CUDA(cudaMemsetAsync(tot, 0, sizeof(int64_t), c.stream));
+    }
+    k_induce_rows<<<(unsigned)((n_in + 1 + 255) / 256), 256, 0, c.stream>>>(c.d_row_ptr, n_in, c.d_ebits, c.d_eboff,
+                                                                          c.d_ind_ptr, c.d_row_nseg);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
-    scan_i32(c, c.d_row_cnt, c.d_ind_ptr, n_in, tot + 0);
     scan_i32(c, c.d_row_nseg, c.d_row_soff, n_in, tot + 1);
-    k_induce_write<<<grid, 256, 0, c.stream>>>(c.d_row_ptr, c.d_col_enc, n_in, c.d_slot_of_b, c.d_ind_ptr,
-                                               c.d_row_soff, c.d_ind_col, c.d_seg_fwd);
+    k_induce_segs<<<(unsigned)((n_in + 255) / 256), 256, 0, c.stream>>>(c.d_ind_ptr, n_in, c.d_row_soff, c.d_seg_fwd);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }

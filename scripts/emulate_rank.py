@@ -1,0 +1,90 @@
+"""Single-GPU timing emulation of one rank of an m-partition BNS-GCN job (BNS_TRANSPORT_NULL_EMULATE).
+
+The rank runs exactly its own kernels with its own sampled sizes; the exchanges and the all-reduce are no-ops
+(their cost is estimated separately from the bytes each would move at the measured 770 GB/s NVLink peer
+bandwidth, B200_PROFILING.md).  Output: one JSON line per (p, rank).  This is NOT an 8-GPU measurement; it
+exposes per-rank kernel behaviour at the paper's scale (small partitions, launch/latency sensitivity).
+
+    python scripts/emulate_rank.py --m 8 --p 0.1 0.01 --ranks all
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="reddit")
+    ap.add_argument("--m", type=int, default=8)
+    ap.add_argument("--p", type=float, nargs="+", default=[0.1])
+    ap.add_argument("--ranks", default="0")
+    ap.add_argument("--prec", default="bf16")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--partition", default="ldg2")
+    args = ap.parse_args()
+    import torch
+    from paper_2203_10983_b200 import bns
+    from paper_2203_10983_b200 import inputs as I
+    sh = I.SHAPES[args.config]
+    indptr, indices = I.rmat(sh.N, sh.nnz)
+    part = I.partition(indptr, indices, args.m, args.partition)
+    y_all = I.labels(sh.N, sh.C, sh.train_frac)
+    ranks = list(range(args.m)) if args.ranks == "all" else [int(r) for r in args.ranks.split(",")]
+    prec = bns.BNS_BF16 if args.prec == "bf16" else bns.BNS_FP32
+    s = 2 if prec == bns.BNS_BF16 else 4
+    dp = [((d + 7) // 8) * 8 for d in sh.dims]
+    for r in ranks:
+        inner = np.nonzero(part == r)[0].astype(np.int32)
+        ctx = bns.Context(rank=r, world=args.m, dims=sh.dims, layer=sh.layer, precision=prec, indptr=indptr,
+                          indices=indices, part_of=part, features=I.features(inner, sh.d0),
+                          labels=np.ascontiguousarray(y_all[inner]), transport=bns.BNS_TRANSPORT_NULL_EMULATE,
+                          flags=bns.BNS_TIMING)
+        W = [torch.tensor(w, device="cuda") for w in I.weights(sh.dims, sh.layer)]
+        G = [torch.zeros_like(w) for w in W]
+        stream = torch.cuda.ExternalStream(ctx.stream())
+        for p in args.p:
+            for e in range(args.warmup):
+                ctx.sample_boundary(p, I.BNS_SEED, e)
+                ctx.epoch(W, 0.0, G)
+            torch.cuda.synchronize()
+            t0 = ctx.times()
+            k0 = ctx.kernel_count()
+            ms = []
+            wall0 = time.perf_counter()
+            for k in range(args.steps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                ctx.sample_boundary(p, I.BNS_SEED, 100 + k)
+                ctx.epoch(W, 0.0, G)
+                b.record(stream)
+                b.synchronize()
+                ms.append(a.elapsed_time(b))
+            wall = (time.perf_counter() - wall0) / args.steps * 1e3
+            t1 = ctx.times()
+            cnt = ctx.counts()
+            ph = {k: round((t1[k] - t0[k]) / args.steps, 4) for k in t1 if t1[k] - t0[k] > 0}
+            # bytes this rank moves per epoch: forward halo rows (recv) and sent rows, backward the reverse
+            fwd = sum((cnt["n_halo"] + cnt["n_sent"]) * dp[l] * s for l in range(sh.L)) / 2
+            bwd = sum((cnt["n_halo"] + cnt["n_sent"]) * dp[l] * s for l in range(1, sh.L)) / 2
+            wbytes = sum(w.numel() * 4 for w in W)
+            comm_ms = (fwd + bwd) / 770e9 * 1e3 + 2 * wbytes / 725e9 * 1e3
+            rec = {"config": sh.name, "m": args.m, "rank": r, "p": p, "prec": args.prec,
+                   "device_ms_per_epoch": float(np.median(ms)), "wall_ms_per_epoch": wall,
+                   "est_nvlink_ms": comm_ms, "kernels_per_epoch": (ctx.kernel_count() - k0) / args.steps,
+                   "n_in": cnt["n_in"], "n_bd": cnt["n_bd"], "n_halo": cnt["n_halo"], "n_sent": cnt["n_sent"],
+                   "nnz_kept": cnt["nnz_kept"], "phases_ms": ph,
+                   "note": "single-GPU emulation: exchanges/all-reduce are no-ops; NOT an m-GPU measurement"}
+            print(json.dumps(rec), flush=True)
+        ctx.close()
+
+
+if __name__ == "__main__":
+    main()
