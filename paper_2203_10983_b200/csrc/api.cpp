@@ -224,6 +224,23 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.d_seg_fwd = static_cast<Seg*>(dalloc(c, c.seg_fwd_cap * sizeof(Seg)));
     int64_t seg_max = std::max({c.seg_fwd_cap, c.seg_bwd_cap, c.n_seg_static_fwd});
     c.d_partial = static_cast<float*>(dalloc(c, (size_t)seg_max * c.maxd * sizeof(float)));
+    // split (hub) row lists: first segment of every row with more than one segment
+    auto split_list = [](const std::vector<Seg>& s) {
+        std::vector<int64_t> l;
+        for (size_t k = 0; k < s.size(); ++k)
+            if (s[k].nseg > 1 && (int64_t)k == s[k].first) l.push_back((int64_t)k);
+        return l;
+    };
+    {
+        std::vector<int64_t> lf = split_list(sf), lb = split_list(sb);
+        c.n_split_sf = (int64_t)lf.size();
+        c.d_split_sf = upload(c, lf);
+        c.n_split_bwd_inner = (int64_t)lb.size();
+        c.d_split_bwd = static_cast<int64_t*>(dalloc(c, (lb.size() + P.n_bd + 1) * sizeof(int64_t)));
+        if (!lb.empty())
+            BNS_CUDA(cudaMemcpy(c.d_split_bwd, lb.data(), lb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        c.d_split_fwd = static_cast<int64_t*>(dalloc(c, (P.n_in + 1) * sizeof(int64_t)));
+    }
 
     // ---- per-epoch scratch
     c.d_flags = static_cast<uint8_t*>(dalloc(c, c.n_cand));
@@ -352,10 +369,11 @@ void sample_boundary(Ctx& c, double p, uint64_t seed, uint64_t epoch) {
     c.n_halo = c.recv_off[m];
     c.n_sent = c.send_off[m];
     const int64_t* tot = sp + 2 * m + 1;
-    if (c.fwd_mode == 0) { c.nnz_kept = c.nnz_i; c.n_seg_fwd = c.n_seg_static_fwd; }
-    else if (c.fwd_mode == 1) { c.nnz_kept = c.ii_nnz; c.n_seg_fwd = c.n_seg_bwd_inner; }
-    else { c.nnz_kept = tot[0]; c.n_seg_fwd = tot[1]; }
+    if (c.fwd_mode == 0) { c.nnz_kept = c.nnz_i; c.n_seg_fwd = c.n_seg_static_fwd; c.n_split_fwd = c.n_split_sf; }
+    else if (c.fwd_mode == 1) { c.nnz_kept = c.ii_nnz; c.n_seg_fwd = c.n_seg_bwd_inner; c.n_split_fwd = c.n_split_bwd_inner; }
+    else { c.nnz_kept = tot[0]; c.n_seg_fwd = tot[1]; c.n_split_fwd = tot[4]; }
     c.n_seg_bwd = c.n_seg_bwd_inner + (has_bd ? tot[2] : 0);
+    c.n_split_bwd = c.n_split_bwd_inner + (has_bd ? tot[3] : 0);
     if (c.n_halo > c.halo_cap)
         throw Error(BNS_ERR_OOM, "sampled halo (" + std::to_string(c.n_halo) + " rows) exceeds capacity " +
                                      std::to_string(c.halo_cap) + " (raise cfg.max_p)");
@@ -420,7 +438,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     }
     {
         PhaseTimer t(c, BNS_PH_UPDATE);
-        for (int l = 0; l < L; ++l) launch_wpack(c, W[l], l, false);
+        launch_wpack_all(c, W.data());
     }
     const Seg* fsegs = c.fwd_mode == 0 ? c.d_seg_static_fwd : (c.fwd_mode == 1 ? c.d_seg_bwd : c.d_seg_fwd);
     const int32_t* fcol = c.fwd_mode == 0 ? c.d_static_col : (c.fwd_mode == 1 ? c.d_tcol : c.d_ind_col);
@@ -456,6 +474,8 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             a.rowscale = sage ? c.d_deg_in : c.d_rs_in;
             a.cscale = c.d_cscale;
             a.partial = c.d_partial;
+            a.split = c.fwd_mode == 0 ? c.d_split_sf : (c.fwd_mode == 1 ? c.d_split_bwd : c.d_split_fwd);
+            a.n_split = c.n_split_fwd;
             launch_spmm(c, a);
         }
         {
@@ -519,6 +539,8 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             a.inv_p = inv_p;
             a.cscale = c.d_cscale;
             a.partial = c.d_partial;
+            a.split = c.d_split_bwd;
+            a.n_split = c.n_split_bwd;
             launch_spmm(c, a);
         }
         if (m > 1) {

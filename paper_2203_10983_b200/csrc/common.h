@@ -133,6 +133,10 @@ struct Ctx {
     int32_t* d_static_col = nullptr; int64_t* d_static_ptr = nullptr;
     int64_t n_seg_bwd_inner = 0;
     float* d_partial = nullptr;    // hub-row partial sums
+    int64_t* d_split_sf = nullptr;  int64_t n_split_sf = 0;      // split rows of the static forward segments
+    int64_t* d_split_bwd = nullptr; int64_t n_split_bwd_inner = 0; // [static inner part ; per-epoch halo part]
+    int64_t* d_split_fwd = nullptr;                                  // per-epoch induced forward segments
+    int64_t n_split_fwd = 0, n_split_bwd = 0;                        // this epoch's list lengths
     float* d_cscale = nullptr;     // per-column scale (GCN forward)
     // --- activations (storage type T: float or bf16)
     std::vector<void*> H;          // H[l], l = 0..L-1: (n_in + halo_cap) x dp[l]

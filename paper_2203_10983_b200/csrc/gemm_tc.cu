@@ -357,7 +357,8 @@ void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int6
     a.nk = (int)cdiv(Mn, 64);
     a.nk0 = a.nk;
     const int64_t tiles = cdiv(K, TC_BM) * cdiv(N, a.BN);
-    int64_t S = std::max<int64_t>(1, std::min<int64_t>(cdiv(296, tiles), std::max(1, a.nk / 8)));
+    // ~one CTA per SM, but at least 32 k-blocks (2048 nodes) per split so the partial slices stay small
+    int64_t S = std::max<int64_t>(1, std::min<int64_t>(cdiv(148, tiles), std::max(1, a.nk / 32)));
     while (S > 1 && S * K * N > c.splitk_cap) --S;
     a.kb_per_split = (int)cdiv(a.nk, S);
     S = cdiv(a.nk, a.kb_per_split);

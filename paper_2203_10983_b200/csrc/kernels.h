@@ -32,6 +32,7 @@ struct SpmmArgs {
     const int32_t* halo_b;                // GCN_BWD: boundary index of halo slot
     const float* rs_bd;                   // GCN_BWD
     float* partial;
+    const int64_t* split; int64_t n_split;  // first-segment index of every split (hub) row -> in-order fixup
 };
 void launch_spmm(Ctx& c, const SpmmArgs& a);
 
@@ -63,7 +64,7 @@ void launch_pack_rows(Ctx& c, const void* src, int64_t ld_src, const int32_t* id
 void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, const void* src, int64_t n, int32_t d);
 void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t);
 void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre);
-void launch_wpack(Ctx& c, const float* W, int l, bool host_src);
+void launch_wpack_all(Ctx& c, float* const* W);
 void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr);
 void launch_sum_ptrs(Ctx& c, const float* const* d_ptrs, int nptr, float* out, int64_t n);
 void launch_sum_ptrs_d(Ctx& c, const double* const* d_ptrs, int nptr, double* out, int64_t n);

@@ -139,13 +139,17 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
     }
 }
 
+// one warp: lane-strided partial sums then a fixed butterfly (deterministic)
 __global__ void k_xent_final(const double* __restrict__ part, int nb, double* __restrict__ scal) {
-    if (threadIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (int k = 0; k < nb; ++k) { a += part[2 * k]; b += part[2 * k + 1]; }
-        scal[0] = a;
-        scal[1] = b;
+    const int lane = threadIdx.x & 31;
+    double a = 0.0, b = 0.0;
+    for (int k = lane; k < nb; k += 32) { a += part[2 * k]; b += part[2 * k + 1]; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
     }
+    if (lane == 0) { scal[0] = a; scal[1] = b; }
 }
 
 void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t) {
@@ -206,73 +210,104 @@ __device__ __forceinline__ int64_t logical_row(int64_t pr, int sage, int64_t din
     return q < din ? din + q : -1;
 }
 
+// all layers in one launch: blockIdx.y = layer (blockIdx.y >= L: the W^T copy of layer y - L)
+constexpr int kMaxLayers = 16;
+struct WDesc {
+    const float* W[kMaxLayers];
+    float* G[kMaxLayers];
+    float* Wp[kMaxLayers];
+    void* Wt[kMaxLayers];
+    void* WT[kMaxLayers];
+    const float* gpad[kMaxLayers];
+    int64_t rows_p[kMaxLayers], cols_p[kMaxLayers], din[kMaxLayers], dpin[kMaxLayers], dout[kMaxLayers];
+    int64_t K64[kMaxLayers], Kw[kMaxLayers];
+    int L, sage, tc;
+};
+
 template <typename T>
-__global__ void k_wpack(const float* __restrict__ W, int64_t rows_p, int64_t cols_p, int64_t din, int64_t dpin,
-                        int64_t dout, int sage, float* __restrict__ Wp, T* __restrict__ Wt) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= rows_p * cols_p) return;
-    int64_t pr = t / cols_p, pc = t % cols_p;
-    int64_t lr = logical_row(pr, sage, din, dpin);
-    float v = (lr >= 0 && pc < dout) ? W[lr * dout + pc] : 0.f;
-    Wp[t] = v;
-    if (Wt) Wt[t] = from_f<T>(v);
-}
-
-// W^T for the tcgen05 forward: WT[n][kw], kw = half * K64 + j  <->  padded row half * dpin + j (0 if j >= dpin)
-__global__ void k_wpack_t(const float* __restrict__ Wp, int64_t cols_p, int64_t dpin, int64_t K64, int64_t Kw,
-                          __nv_bfloat16* __restrict__ WT) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= cols_p * Kw) return;
-    int64_t n = t / Kw, kw = t % Kw;
-    int64_t half = kw / K64, j = kw % K64;
-    float v = (j < dpin) ? Wp[(half * dpin + j) * cols_p + n] : 0.f;
-    WT[t] = __float2bfloat16_rn(v);
-}
-
-void launch_wpack(Ctx& c, const float* W, int l, bool /*host_src*/) {
-    const int64_t rp = c.wrows[l], cp = c.wcols[l];
-    const unsigned grid = (unsigned)((rp * cp + 255) / 256);
-    const int sage = c.layer == BNS_LAYER_SAGE_MEAN;
-    if (c.prec == BNS_BF16)
-        k_wpack<__nv_bfloat16><<<grid, 256, 0, c.stream>>>(W, rp, cp, c.dims[l], c.dp[l], c.dims[l + 1], sage, c.Wpad[l],
-                                                           (__nv_bfloat16*)c.Wt[l]);
-    else
-        k_wpack<float><<<grid, 256, 0, c.stream>>>(W, rp, cp, c.dims[l], c.dp[l], c.dims[l + 1], sage, c.Wpad[l],
-                                                   nullptr);
-    c.kernels += 1;
-    if (c.use_tc) {
-        const int64_t K64 = (c.dp[l] + 63) / 64 * 64;
-        const int64_t n = cp * c.wkw[l];
-        k_wpack_t<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.Wpad[l], cp, c.dp[l], K64, c.wkw[l],
-                                                                     (__nv_bfloat16*)c.WT[l]);
-        c.kernels += 1;
+__global__ void k_wpack_all(const WDesc d) {
+    const int y = blockIdx.y;
+    const int l = y % d.L;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t cp = d.cols_p[l];
+    if (y < d.L) {
+        if (t >= d.rows_p[l] * cp) return;
+        const int64_t pr = t / cp, pc = t % cp;
+        const int64_t lr = logical_row(pr, d.sage, d.din[l], d.dpin[l]);
+        const float v = (lr >= 0 && pc < d.dout[l]) ? d.W[l][lr * d.dout[l] + pc] : 0.f;
+        d.Wp[l][t] = v;
+        if (d.Wt[l] != (void*)d.Wp[l]) static_cast<T*>(d.Wt[l])[t] = from_f<T>(v);
+    } else {
+        // W^T for the tcgen05 forward: WT[n][kw], kw = half * K64 + j <-> padded row half * dpin + j
+        if (t >= cp * d.Kw[l]) return;
+        const int64_t n = t / d.Kw[l], kw = t % d.Kw[l];
+        const int64_t half = kw / d.K64[l], j = kw % d.K64[l];
+        float v = 0.f;
+        if (j < d.dpin[l]) {
+            const int64_t lr = logical_row(half * d.dpin[l] + j, d.sage, d.din[l], d.dpin[l]);
+            if (lr >= 0 && n < d.dout[l]) v = d.W[l][lr * d.dout[l] + n];
+        }
+        static_cast<__nv_bfloat16*>(d.WT[l])[t] = __float2bfloat16_rn(v);
     }
+}
+
+static WDesc make_desc(Ctx& c, float* const* W, float* const* G) {
+    if (c.L > kMaxLayers) throw Error(BNS_ERR_INVALID, "too many layers");
+    WDesc d{};
+    d.L = c.L;
+    d.sage = c.layer == BNS_LAYER_SAGE_MEAN;
+    d.tc = c.use_tc ? 1 : 0;
+    for (int l = 0; l < c.L; ++l) {
+        d.W[l] = W[l];
+        d.G[l] = G ? G[l] : nullptr;
+        d.Wp[l] = c.Wpad[l];
+        d.Wt[l] = c.Wt[l];
+        d.WT[l] = c.use_tc ? c.WT[l] : nullptr;
+        d.gpad[l] = c.d_gflat + c.goff[l];
+        d.rows_p[l] = c.wrows[l];
+        d.cols_p[l] = c.wcols[l];
+        d.din[l] = c.dims[l];
+        d.dpin[l] = c.dp[l];
+        d.dout[l] = c.dims[l + 1];
+        d.K64[l] = (c.dp[l] + 63) / 64 * 64;
+        d.Kw[l] = c.wkw[l];
+    }
+    return d;
+}
+
+void launch_wpack_all(Ctx& c, float* const* W) {
+    const WDesc d = make_desc(c, W, nullptr);
+    int64_t mx = 0;
+    for (int l = 0; l < c.L; ++l)
+        mx = std::max<int64_t>(std::max<int64_t>(mx, d.rows_p[l] * d.cols_p[l]), d.tc ? d.cols_p[l] * d.Kw[l] : 0);
+    const dim3 grid((unsigned)((mx + 255) / 256), (unsigned)(c.L * (d.tc ? 2 : 1)));
+    if (c.prec == BNS_BF16) k_wpack_all<__nv_bfloat16><<<grid, 256, 0, c.stream>>>(d);
+    else k_wpack_all<float><<<grid, 256, 0, c.stream>>>(d);
+    c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 
-__global__ void k_sgd(float* __restrict__ W, float* __restrict__ G, const float* __restrict__ gpad, int64_t rows_l,
-                      int64_t dout, int64_t cols_p, int64_t din, int64_t dpin, int sage, float lr,
-                      const double* __restrict__ scal, int32_t* __restrict__ nonfinite) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// a14 W <- W - lr g for every layer (g copied to the caller); skipped when the all-reduced loss is not finite
+__global__ void k_sgd_all(const WDesc d, float lr, const double* __restrict__ scal, int32_t* __restrict__ nonfinite) {
+    const int l = blockIdx.y;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t rows_l = (d.sage ? 2 : 1) * d.din[l], dout = d.dout[l];
     if (t >= rows_l * dout) return;
     const bool bad = !isfinite(scal[0]);
-    if (t == 0) *nonfinite = bad ? 1 : 0;
-    int64_t lr_ = t / dout, lc = t % dout;
-    int64_t pr = sage ? (lr_ < din ? lr_ : dpin + (lr_ - din)) : lr_;
-    float g = gpad[pr * cols_p + lc];
-    if (G) G[t] = g;
-    if (!bad) W[t] -= lr * g;
+    if (t == 0 && l == 0) *nonfinite = bad ? 1 : 0;
+    const int64_t lr_ = t / dout, lc = t % dout;
+    const int64_t pr = d.sage ? (lr_ < d.din[l] ? lr_ : d.dpin[l] + (lr_ - d.din[l])) : lr_;
+    const float g = d.gpad[l][pr * d.cols_p[l] + lc];
+    if (d.G[l]) d.G[l][t] = g;
+    if (!bad) const_cast<float*>(d.W[l])[t] -= lr * g;
 }
 
 void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr) {
-    const int sage = c.layer == BNS_LAYER_SAGE_MEAN;
-    for (int l = 0; l < c.L; ++l) {
-        const int64_t rows_l = (sage ? 2 : 1) * (int64_t)c.dims[l], dout = c.dims[l + 1];
-        const unsigned grid = (unsigned)((rows_l * dout + 255) / 256);
-        k_sgd<<<grid, 256, 0, c.stream>>>(W[l], G ? G[l] : nullptr, c.d_gflat + c.goff[l], rows_l, dout, c.wcols[l],
-                                          c.dims[l], c.dp[l], sage, lr, c.d_scal, c.d_nonfinite);
-        c.kernels += 1;
-    }
+    const WDesc d = make_desc(c, W, G);
+    int64_t mx = 0;
+    for (int l = 0; l < c.L; ++l) mx = std::max(mx, (d.sage ? 2 : 1) * d.din[l] * d.dout[l]);
+    k_sgd_all<<<dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, c.stream>>>(d, lr, c.d_scal, c.d_nonfinite);
+    c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 

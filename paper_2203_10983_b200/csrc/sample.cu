@@ -275,12 +275,19 @@ __global__ void k_induce_rows(const int64_t* __restrict__ ptr, int64_t n_in, con
     nseg[r] = cnt > kSeg ? (int32_t)((cnt + kSeg - 1) / kSeg) : 1;
 }
 
+// rows split into several segments are appended (first segment index) to a split list for the SpMM fixup;
+// list order is irrelevant (each row's partials are summed in segment order)
+__device__ __forceinline__ void push_split(int64_t* list, int64_t* count, int64_t s0) {
+    list[atomicAdd(reinterpret_cast<unsigned long long*>(count), 1ull)] = s0;
+}
+
 __global__ void k_induce_segs(const int64_t* __restrict__ out_ptr, int64_t n_in, const int64_t* __restrict__ seg_off,
-                              Seg* __restrict__ segs) {
+                              Seg* __restrict__ segs, int64_t* __restrict__ split, int64_t* __restrict__ n_split) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_in) return;
     const int64_t b0 = out_ptr[r], b1 = out_ptr[r + 1];
     const int64_t s0 = seg_off[r], ns = seg_off[r + 1] - s0;
+    if (ns > 1) push_split(split, n_split, s0);
     for (int64_t k = 0; k < ns; ++k) {
         Seg sg;
         sg.row = (int32_t)r;
@@ -313,7 +320,9 @@ void launch_induce(Ctx& c) {
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
     scan_i32(c, c.d_row_nseg, c.d_row_soff, n_in, tot + 1);
-    k_induce_segs<<<(unsigned)((n_in + 255) / 256), 256, 0, c.stream>>>(c.d_ind_ptr, n_in, c.d_row_soff, c.d_seg_fwd);
+    BNS_CUDA(cudaMemsetAsync(tot + 4, 0, sizeof(int64_t), c.stream));
+    k_induce_segs<<<(unsigned)((n_in + 255) / 256), 256, 0, c.stream>>>(c.d_ind_ptr, n_in, c.d_row_soff, c.d_seg_fwd,
+                                                                       c.d_split_fwd, tot + 4);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -335,7 +344,8 @@ __global__ void k_bwd_count(const int64_t* __restrict__ seg_pos, int m, const in
 
 __global__ void k_bwd_write(const int64_t* __restrict__ seg_pos, int m, const int32_t* __restrict__ U_b,
                             const int64_t* __restrict__ br_ptr, int64_t cap, const int64_t* __restrict__ soff,
-                            int64_t seg_base, int64_t e_base, int64_t n_in, Seg* __restrict__ segs) {
+                            int64_t seg_base, int64_t e_base, int64_t n_in, Seg* __restrict__ segs,
+                            int64_t* __restrict__ split, int64_t* __restrict__ n_split) {
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= cap) return;
     int64_t n_halo = seg_pos[m] - seg_pos[0];
@@ -343,6 +353,7 @@ __global__ void k_bwd_write(const int64_t* __restrict__ seg_pos, int m, const in
     int32_t b = U_b[s];
     int64_t e_lo = e_base + br_ptr[b], e_hi = e_base + br_ptr[b + 1];
     int64_t s0 = seg_base + soff[s], ns = soff[s + 1] - soff[s];
+    if (ns > 1) push_split(split, n_split, s0);
     for (int64_t k = 0; k < ns; ++k) {
         Seg sg;
         sg.row = (int32_t)(n_in + s);
@@ -358,6 +369,7 @@ void launch_bwd_segments(Ctx& c) {
     const int m = c.cfg.world;
     const int64_t cap = c.plan.n_bd;
     int64_t* tot = c.d_seg_pos + 2 * m + 1;
+    BNS_CUDA(cudaMemsetAsync(tot + 3, 0, sizeof(int64_t), c.stream));
     if (cap == 0) {
         BNS_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(int64_t), c.stream));
         return;
@@ -368,7 +380,8 @@ void launch_bwd_segments(Ctx& c) {
     BNS_CHECK_LAUNCH();
     scan_i32(c, c.d_row_nseg, c.d_row_soff, cap, tot + 2);
     k_bwd_write<<<grid, 256, 0, c.stream>>>(c.d_seg_pos, m, c.d_cand_out, c.d_br_ptr, cap, c.d_row_soff,
-                                            c.n_seg_bwd_inner, c.ii_nnz, c.plan.n_in, c.d_seg_bwd);
+                                            c.n_seg_bwd_inner, c.ii_nnz, c.plan.n_in, c.d_seg_bwd,
+                                            c.d_split_bwd + c.n_split_bwd_inner, tot + 3);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }

@@ -73,7 +73,8 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
 // SC: per-edge column scale -- 0 none (backward modes, and the forward when every column has c_u = 1),
 //     1 c_u = 1/p for halo columns (col >= n_in, SAGE forward), 2 c_u from cscale[] (GCN forward).
 template <typename T, int LPR, int VPL, int SC>
-__global__ void __launch_bounds__(256, (VPL <= 1) ? 4 : (VPL <= 2) ? 3 : 2) k_spmm(const SpmmArgs a) {
+__global__ void __launch_bounds__(256, (VPL <= 1 && SC == 0) ? 4 : (VPL <= 2) ? 3 : (VPL <= 6) ? 2 : 1)
+k_spmm(const SpmmArgs a) {
     using V = Vec<T>;
     using R = typename V::raw;
     constexpr int VN = V::N;
@@ -134,28 +135,17 @@ __global__ void __launch_bounds__(256, (VPL <= 1) ? 4 : (VPL <= 2) ? 3 : 2) k_sp
                             acc_vec2<T, SC != 0>(acc2[v], r[u][v], SC ? sj[u] : 0ull);
                 }
             } else {
-                // tail chunk: same U-deep batches; slots past the row end re-load the chunk's first row (a live
-                // address, cached) with scale 0, so there is no branch and U loads stay in flight
-                const int32_t c_first = __shfl_sync(0xffffffffu, ci, 0);
-                if (lane >= cnt) ci = c_first;
-                for (int j0 = 0; j0 < cnt; j0 += G * U) {
-                    R r[U][VPL];
-                    uint64_t sj[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int j = j0 + u * G + g;
-                        const uint32_t cj = (uint32_t)__shfl_sync(0xffffffffu, ci, j & 31);
-                        const float t = SC ? __shfl_sync(0xffffffffu, sc, j & 31) : 1.f;
-                        const float tt = (j < cnt) ? t : 0.f;
-                        sj[u] = pk2(tt, tt);
+                // tail chunk (< 32 edges): one edge per lane group per step
+                for (int j0 = 0; j0 < cnt; j0 += G) {
+                    const int j = j0 + g;
+                    const uint32_t cj = (uint32_t)__shfl_sync(0xffffffffu, ci, j & 31);
+                    const float t = SC ? __shfl_sync(0xffffffffu, sc, j & 31) : 1.f;
+                    if (j < cnt) {
                         const R* rowp = reinterpret_cast<const R*>(base + (uint64_t)cj * rvb);
 #pragma unroll
-                        for (int v = 0; v < VPL; ++v) r[u][v] = ldg_nc(rowp + voff[v]);
+                        for (int v = 0; v < VPL; ++v)
+                            acc_vec2<T, SC != 0>(acc2[v], ldg_nc(rowp + voff[v]), pk2(t, t));
                     }
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-#pragma unroll
-                        for (int v = 0; v < VPL; ++v) acc_vec2<T, true>(acc2[v], r[u][v], sj[u]);
                 }
             }
         }
@@ -202,9 +192,9 @@ __global__ void __launch_bounds__(256) k_spmm_fixup(const SpmmArgs a) {
     const int nvec = a.d / VN;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t sid = warp; sid < a.n_segs; sid += nwarps) {
+    for (int64_t q0 = warp; q0 < a.n_split; q0 += nwarps) {
+        const int64_t sid = a.split[q0];
         const Seg s = a.segs[sid];
-        if (s.nseg <= 1 || sid != s.first) continue;
         for (int vi = lane; vi < nvec; vi += 32) {
             float acc[VN];
 #pragma unroll
@@ -288,11 +278,15 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
         if (a0.self) a.self = static_cast<const char*>(a0.self) + c0 * ts;
         if (c.prec == BNS_BF16) dispatch<__nv_bfloat16>(c, a, grid);
         else dispatch<float>(c, a, grid);
+        c.kernels += 1;
         BNS_CHECK_LAUNCH();
-        if (c.prec == BNS_BF16) k_spmm_fixup<__nv_bfloat16><<<grid, 256, 0, c.stream>>>(a);
-        else k_spmm_fixup<float><<<grid, 256, 0, c.stream>>>(a);
-        c.kernels += 2;
-        BNS_CHECK_LAUNCH();
+        if (a.n_split > 0) {   // only the split (hub) rows, listed by their first segment
+            const unsigned fg = (unsigned)std::min<int64_t>((a.n_split + 7) / 8, 148 * 8);
+            if (c.prec == BNS_BF16) k_spmm_fixup<__nv_bfloat16><<<fg, 256, 0, c.stream>>>(a);
+            else k_spmm_fixup<float><<<fg, 256, 0, c.stream>>>(a);
+            c.kernels += 1;
+            BNS_CHECK_LAUNCH();
+        }
     }
 }
 
