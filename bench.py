@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--config", default="reddit")
     ap.add_argument("--p", type=float, default=0.1)
     ap.add_argument("--prec", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--partition", default="ldg2", choices=["ldg2", "random"])
+    # random: on R-MAT (no community structure) it balances kept edges best (max/mean 1.03 vs 1.17 for ldg2 at
+    # m=8, p=0.1) -- the slowest rank sets the epoch time; see DESIGN.md §4
+    ap.add_argument("--partition", default="random", choices=["ldg2", "random"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-scale", type=float, default=64.0, help="oracle sample = workload scaled down by this")
