@@ -14,7 +14,7 @@ from typing import Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbns.so")
+LIB_PATH = os.environ.get("BNS_LIB") or os.path.join(_HERE, "libbns.so")   # BNS_LIB: A/B builds only
 
 BNS_OK, BNS_ERR_INVALID, BNS_ERR_RUNTIME, BNS_ERR_STATE, BNS_ERR_OOM, BNS_ERR_NONFINITE = range(6)
 BNS_LAYER_SAGE_MEAN, BNS_LAYER_GCN = 0, 1

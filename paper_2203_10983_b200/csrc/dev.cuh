@@ -127,9 +127,18 @@ template <> __device__ __forceinline__ float from_f<float>(float x) { return x; 
 template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 
 template <typename R> __device__ __forceinline__ R ldg_nc(const R* p) { return __ldg(p); }
+#if defined(BNS_LDG_NA)
+#define BNS_LDG_HINT ".L1::no_allocate"
+#elif defined(BNS_LDG_EL)
+#define BNS_LDG_HINT ".L1::evict_last"
+#elif defined(BNS_LDG_EF)
+#define BNS_LDG_HINT ".L1::evict_first"
+#else
+#define BNS_LDG_HINT ""
+#endif
 template <> __device__ __forceinline__ uint4 ldg_nc<uint4>(const uint4* p) {
     uint4 r;
-    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    asm("ld.global.nc" BNS_LDG_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     return r;
 }
 

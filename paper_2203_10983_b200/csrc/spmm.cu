@@ -72,14 +72,20 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
 
 // SC: per-edge column scale -- 0 none (backward modes, and the forward when every column has c_u = 1),
 //     1 c_u = 1/p for halo columns (col >= n_in, SAGE forward), 2 c_u from cscale[] (GCN forward).
+#ifndef BNS_SPMM_U1
+#define BNS_SPMM_U1 8       // edges in flight per lane group for 1-vector rows
+#endif
+#ifndef BNS_SPMM_MINB1
+#define BNS_SPMM_MINB1 4    // resident 256-thread blocks per SM for 1-vector rows
+#endif
 template <typename T, int LPR, int VPL, int SC>
-__global__ void __launch_bounds__(256, (VPL <= 1 && SC == 0) ? 4 : (VPL <= 2) ? 3 : (VPL <= 6) ? 2 : 1)
+__global__ void __launch_bounds__(256, (VPL <= 1 && SC == 0) ? BNS_SPMM_MINB1 : (VPL <= 2) ? 3 : (VPL <= 6) ? 2 : 1)
 k_spmm(const SpmmArgs a) {
     using V = Vec<T>;
     using R = typename V::raw;
     constexpr int VN = V::N;
     constexpr int G = 32 / LPR;                              // edge groups per warp
-    constexpr int U0 = (VPL <= 1) ? 8 : (VPL <= 2) ? 4 : (VPL <= 4) ? 2 : 1;
+    constexpr int U0 = (VPL <= 1) ? BNS_SPMM_U1 : (VPL <= 2) ? 4 : (VPL <= 4) ? 2 : 1;
     constexpr int U = (G * U0 > 32) ? (32 / G) : U0;         // edges in flight per group
     static_assert(32 % (G * U) == 0, "bad unroll");
     const int lane = threadIdx.x & 31, g = lane / LPR, l = lane % LPR;
