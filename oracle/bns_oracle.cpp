@@ -127,7 +127,27 @@ struct Oracle {
     std::vector<std::vector<double>> dH;    // dH[l], l=0..L : N x dims[l]  (dH[0] is not computed)
     std::vector<std::vector<double>> G;     // all-reduced weight gradients, per layer
     std::vector<int64_t> rows_sent_fwd;     // per layer, total rows exchanged (Eq. 3 accounting)
+    // f2: the paper's training recipe, Adam + dropout
+    int optimizer = 0;                      // 0 SGD (Alg.1 l.14), 1 Adam
+    double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+    int64_t adam_t = 0;
+    std::vector<std::vector<double>> adam_m, adam_v;
+    double drop = 0.0;                      // dropout rate r on every layer's input (R38)
+    uint64_t drop_seed = 0;
+    uint64_t epoch_id = 0;                  // epoch of the last draw (keys the dropout masks)
 };
+
+// R38 dropout mask: keep(u, c, l, e) = Philox4x32-10(ctr = {u, c >> 2, l, e_lo}, key = {s_lo ^ 0xD809, s_hi})
+// .word[c & 3] >= floor(r 2^32); a kept value is scaled by 1/(1-r).  Keyed by the global node id, so every copy
+// of a row (owner and halo) gets the same mask.
+double drop_factor(const Oracle& o, int32_t u, int c, int l) {
+    if (o.drop <= 0.0) return 1.0;
+    uint32_t ctr[4] = {(uint32_t)u, (uint32_t)(c >> 2), (uint32_t)l, (uint32_t)(o.epoch_id & 0xffffffffu)};
+    uint32_t key[2] = {(uint32_t)(o.drop_seed & 0xffffffffu) ^ 0xD809u, (uint32_t)(o.drop_seed >> 32)};
+    uint32_t out[4];
+    philox4x32_10(ctr, key, out);
+    return ((uint64_t)out[c & 3] >= threshold_of(o.drop)) ? 1.0 / (1.0 - o.drop) : 0.0;
+}
 
 int64_t deg(const Oracle& o, int32_t v) { return o.indptr[v + 1] - o.indptr[v]; }
 
@@ -276,6 +296,12 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                 for (size_t k = 0; k < buf.size(); ++k) X[(size_t)(n_in + P.U_off[j]) * din + k] = buf[k];
                 o.rows_sent_fwd[l] += (int64_t)rows;
             }
+            // R38 dropout on the layer input (inner and halo rows alike, mask keyed by global id), stored (R19)
+            if (o.drop > 0.0)
+                for (size_t r = 0; r < n_in + n_h; ++r) {
+                    const int32_t u = (r < n_in) ? P.V[r] : P.U[r - n_in];
+                    for (int k = 0; k < din; ++k) X[r * din + k] = st(X[r * din + k] * drop_factor(o, u, k, l));
+                }
             // l.10: GCN^(l)(H_i, [H; H_U], w)
             std::vector<double>& Zl = Zs[l][i];
             Zl.assign(n_in * din, 0.0);
@@ -444,7 +470,12 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                 for (int k = 0; k < din; ++k) {
                     double x = dX[r * din + k];
                     if (o.kind == KIND_SAGE && r < n_in) x += dXself[r * din + k];
-                    dX[r * din + k] = st(x);
+                    x = st(x);
+                    if (o.drop > 0.0) {   // R38: through the dropout of this layer's input
+                        const int32_t u = (r < n_in) ? P.V[r] : P.U[r - n_in];
+                        x = st(x * drop_factor(o, u, k, l));
+                    }
+                    dX[r * din + k] = x;
                 }
         }
         if (l == 1) continue;
@@ -474,11 +505,29 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
 
     // ---------------- AllReduce (l.13, sum in rank order, R21) and SGD update (l.14) ----------------
     o.G.assign(L, std::vector<double>());
+    if (o.optimizer == 1) {
+        ++o.adam_t;
+        if ((int)o.adam_m.size() != L) { o.adam_m.assign(L, {}); o.adam_v.assign(L, {}); }
+    }
     for (int l = 0; l < L; ++l) {
         o.G[l].assign(W[l].size(), 0.0);
         for (int i = 0; i < m; ++i)
             for (size_t k = 0; k < W[l].size(); ++k) o.G[l][k] += gW[i][l][k];
-        for (size_t k = 0; k < W[l].size(); ++k) W[l][k] -= lr * o.G[l][k];
+        if (o.optimizer == 0) {
+            for (size_t k = 0; k < W[l].size(); ++k) W[l][k] -= lr * o.G[l][k];
+        } else {
+            // Adam (Kingma & Ba; bias-corrected), the paper's optimizer, f2
+            std::vector<double>& mm = o.adam_m[l];
+            std::vector<double>& vv = o.adam_v[l];
+            if (mm.size() != W[l].size()) { mm.assign(W[l].size(), 0.0); vv.assign(W[l].size(), 0.0); }
+            const double c1 = 1.0 - std::pow(o.beta1, (double)o.adam_t), c2 = 1.0 - std::pow(o.beta2, (double)o.adam_t);
+            for (size_t k = 0; k < W[l].size(); ++k) {
+                const double g = o.G[l][k];
+                mm[k] = o.beta1 * mm[k] + (1.0 - o.beta1) * g;
+                vv[k] = o.beta2 * vv[k] + (1.0 - o.beta2) * g * g;
+                W[l][k] -= lr * (mm[k] / c1) / (std::sqrt(vv[k] / c2) + o.eps);
+            }
+        }
     }
     return 0;
 }
@@ -540,8 +589,28 @@ int32_t orc_sample(void* h, double p, uint64_t seed, uint64_t epoch) {
     if (!(p >= 0.0 && p <= 1.0)) return 1;
     sample(o, p, seed, epoch);
     finish_sample(o);
+    o.epoch_id = epoch;
     return 0;
 }
+
+// f2: optimizer (0 SGD, 1 Adam) and dropout rate / seed.  Resets the Adam state.
+int32_t orc_set_training(void* h, int32_t optimizer, double beta1, double beta2, double eps, double drop,
+                         uint64_t drop_seed) {
+    Oracle& o = *(Oracle*)h;
+    if (optimizer < 0 || optimizer > 1 || !(drop >= 0.0 && drop < 1.0)) return 1;
+    o.optimizer = optimizer;
+    o.beta1 = beta1;
+    o.beta2 = beta2;
+    o.eps = eps;
+    o.drop = drop;
+    o.drop_seed = drop_seed;
+    o.adam_t = 0;
+    o.adam_m.clear();
+    o.adam_v.clear();
+    return 0;
+}
+
+double orc_drop_factor(void* h, int32_t u, int32_t c, int32_t l) { return drop_factor(*(Oracle*)h, u, c, l); }
 
 // Explicit draw (for the hand-computed goldens): keep flags for B_rank in B order.
 int32_t orc_set_keep(void* h, double p, int32_t rank, const int32_t* flags) {

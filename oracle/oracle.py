@@ -48,6 +48,10 @@ def lib():
         L.orc_set_bf16.argtypes = [vp, i32]
         L.orc_round_bf16.restype = f64
         L.orc_round_bf16.argtypes = [f64]
+        L.orc_set_training.restype = i32
+        L.orc_set_training.argtypes = [vp, i32, f64, f64, f64, f64, u64]
+        L.orc_drop_factor.restype = f64
+        L.orc_drop_factor.argtypes = [vp, i32, i32, i32]
         L.orc_rows_sent.restype = i64
         L.orc_rows_sent.argtypes = [vp, i32]
         _LIB = L
@@ -101,6 +105,14 @@ class Oracle:
     def set_bf16(self, on=True):
         """R19 bf16-storage emulation: round the stored tensors (Z, H, GEMM operands, dPre, dZ', dX) to bf16."""
         lib().orc_set_bf16(self.h, 1 if on else 0)
+
+    def set_training(self, optimizer=0, beta1=0.9, beta2=0.999, eps=1e-8, dropout=0.0, dropout_seed=0):
+        """f2: optimizer 0 = SGD (Alg.1 l.14), 1 = Adam; dropout rate on every layer input (R38)."""
+        rc = lib().orc_set_training(self.h, optimizer, beta1, beta2, eps, dropout, dropout_seed)
+        assert rc == 0, rc
+
+    def drop_factor(self, gid, col, layer):
+        return float(lib().orc_drop_factor(self.h, gid, col, layer))
 
     def list(self, what, rank, peer=0):
         n = lib().orc_list(self.h, what, rank, peer, None, 0)

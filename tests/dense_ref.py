@@ -33,7 +33,8 @@ def dense_matrix(indptr, indices, part_of, kept, p, layer):
     return M
 
 
-def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws):
+def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws, masks=None):
+    """masks[l]: optional N x d_l elementwise factors on the input of layer l+1 (dropout, R38)."""
     M = torch.tensor(dense_matrix(indptr, indices, part_of, kept, p, layer), dtype=torch.float64)
     H = torch.tensor(np.asarray(X, np.float64))
     W = [torch.tensor(np.asarray(w, np.float64), requires_grad=True) for w in Ws]
@@ -41,9 +42,10 @@ def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws):
     L = len(W)
     Hs, Zs = [H], []
     for l in range(L):
-        Z = M @ Hs[-1]
+        Xin = Hs[-1] if masks is None else Hs[-1] * torch.tensor(masks[l], dtype=torch.float64)
+        Z = M @ Xin
         Zs.append(Z)
-        pre = torch.cat([Z, Hs[-1]], dim=1) @ W[l] if layer == 0 else Z @ W[l]
+        pre = torch.cat([Z, Xin], dim=1) @ W[l] if layer == 0 else Z @ W[l]
         Hn = torch.relu(pre) if l < L - 1 else pre
         Hn.retain_grad()
         Hs.append(Hn)

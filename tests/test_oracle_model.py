@@ -241,3 +241,86 @@ def test_bf16_emulation_close_to_float64():
     assert abs(out[0][0] - out[1][0]) < 2e-2 * abs(out[0][0])
     for a, b in zip(out[0][2], out[1][2]):
         assert np.abs(a - b).max() <= 5e-2 * np.abs(a).max()
+
+
+# ---------------- f2: Adam and dropout (readings R38, R39) ----------------
+def test_adam_matches_torch_optim():
+    import torch
+    ip, ix, part, X, y, Ws = random_case(71, N=30, m=3, dims=(3, 5, 4))
+    o = O.Oracle(ip, ix, part, 3, [3, 5, 4], 0, X, y)
+    o.set_training(optimizer=1, beta1=0.8, beta2=0.95, eps=1e-6)
+    g_orc = O.Oracle(ip, ix, part, 3, [3, 5, 4], 0, X, y)       # SGD at lr=0: plain gradient at given weights
+    o.sample(0.5, 3, 1)
+    g_orc.sample(0.5, 3, 1)
+    Wo = [w.copy() for w in Ws]
+    Wt = [torch.tensor(w.copy(), requires_grad=False) for w in Ws]
+    opt = torch.optim.Adam(Wt, lr=0.05, betas=(0.8, 0.95), eps=1e-6)
+    for _ in range(4):
+        o.epoch(Wo, 0.05)
+        _, _, G = g_orc.epoch([w.numpy().copy() for w in Wt], 0.0)
+        for w, g in zip(Wt, G):
+            w.grad = torch.tensor(g)
+        opt.step()
+        for a, b in zip(Wo, Wt):
+            np.testing.assert_allclose(a, b.numpy(), rtol=0, atol=1e-12)
+
+
+def test_dropout_mask_definition_and_rate():
+    ip, ix, part, X, y, Ws = random_case(72, N=40, m=2, dims=(8, 4))
+    o = O.Oracle(ip, ix, part, 2, [8, 4], 0, X, y)
+    r, seed = 0.3, 0xABCDEF0123
+    o.set_training(dropout=r, dropout_seed=seed)
+    o.sample(1.0, 1, 5)
+    T = O.threshold(r)
+    kept = 0
+    for u in range(40):
+        for c in range(8):
+            for l in (1, 2):
+                out = O.philox4x32_10([u, c >> 2, l, 5], [(seed & 0xFFFFFFFF) ^ 0xD809, seed >> 32])
+                f = o.drop_factor(u, c, l)
+                assert f == ((1.0 / (1.0 - r)) if out[c & 3] >= T else 0.0)
+                kept += f > 0
+    n = 40 * 8 * 2
+    assert abs(kept / n - (1 - r)) < 4 * np.sqrt(r * (1 - r) / n)
+
+
+@pytest.mark.parametrize("layer", [0, 1])
+def test_dropout_dense_bruteforce(layer):
+    ip, ix, part, X, y, Ws = random_case(73, N=24, m=3, layer=layer, dims=(3, 5, 4, 3))
+    dims = [3, 5, 4, 3]
+    o = O.Oracle(ip, ix, part, 3, dims, layer, X, y)
+    o.set_training(dropout=0.4, dropout_seed=77)
+    o.sample(0.5, 9, 4)
+    kept = [set(int(u) for u in o.list(O.U_LIST, r)) for r in range(3)]
+    masks = [np.array([[o.drop_factor(u, c, l + 1) for c in range(dims[l])] for u in range(24)]) for l in range(3)]
+    ref = forward_backward(ip, ix, part, kept, 0.5, layer, X, y, Ws, masks=masks)
+    loss, acc, G = o.epoch([w.copy() for w in Ws], 0.0)
+    assert abs(loss - ref["loss"]) <= 1e-12 * max(1.0, abs(ref["loss"]))
+    for l in range(1, 3):
+        np.testing.assert_allclose(o.tensor(O.T_DH, l), ref["dH"][l], rtol=1e-10, atol=1e-13)
+    for g, r in zip(G, ref["dW"]):
+        np.testing.assert_allclose(g, r, rtol=1e-10, atol=1e-13)
+
+
+def test_dropout_zero_is_identity_and_unbiased():
+    ip, ix, part, X, y, Ws = random_case(74, N=30, m=2, dims=(3, 4))
+    base = O.Oracle(ip, ix, part, 2, [3, 4], 0, X, y)
+    base.sample(0.5, 1, 1)
+    l0, _, g0 = base.epoch([w.copy() for w in Ws], 0.0)
+    o = O.Oracle(ip, ix, part, 2, [3, 4], 0, X, y)
+    o.set_training(dropout=0.0, dropout_seed=5)
+    o.sample(0.5, 1, 1)
+    l1, _, g1 = o.epoch([w.copy() for w in Ws], 0.0)
+    assert l0 == l1 and all(np.array_equal(a, b) for a, b in zip(g0, g1))
+    # E over epochs of the dropped-out aggregate equals the aggregate without dropout (p = 1 sampling)
+    o.set_training(dropout=0.5, dropout_seed=6)
+    base.sample(1.0, 0, 0)
+    base.epoch([w.copy() for w in Ws], 0.0)
+    z = base.tensor(O.T_Z, 1)
+    acc = []
+    for e in range(1500):
+        o.sample(1.0, 0, e)
+        o.epoch([w.copy() for w in Ws], 0.0)
+        acc.append(o.tensor(O.T_Z, 1))
+    a = np.array(acc)
+    assert np.all(np.abs(a.mean(0) - z) <= 4.5 * a.std(0) / np.sqrt(len(acc)) + 1e-12)
