@@ -123,6 +123,20 @@ bns_status bns_sample_boundary(bns_ctx* ctx, double p, uint64_t seed, uint64_t e
  * Returns after a stream sync.  Collective. */
 bns_status bns_epoch(bns_ctx* ctx, float* const* weights, float lr, float* const* grads, double* loss, double* acc);
 
+/* the paper's training recipe ("a GraphSAGE model with an Adam optimizer",
+ * per-dataset dropout).  Defaults after bns_setup: SGD (Alg.1 l.14), no dropout.
+ *   optimizer: BNS_OPT_SGD or BNS_OPT_ADAM (bias-corrected Adam; beta1, beta2, eps as usual).  The Adam moments live
+ *       on the device (fp32, allocated here -- not in the hot path) and advance on every bns_epoch call (R39);
+ *       calling this function resets them.
+ *   dropout: rate r in [0, 1) applied to the input of every layer, inner and halo rows alike (R38):
+ *       keep(u, c, l, e) = Philox4x32-10(ctr = {u, c >> 2, l, epoch_lo}, key = {seed_lo ^ 0xD809, seed_hi})
+ *       .word[c & 3] >= floor(r 2^32), kept values scaled by 1/(1-r); u = global node id, l = layer (1-based),
+ *       epoch = the epoch of the last bns_sample_boundary.  Keyed by the global id, so every copy of a row agrees.
+ * Not collective; every rank must pass the same values.  Invalid values -> BNS_ERR_INVALID. */
+typedef enum { BNS_OPT_SGD = 0, BNS_OPT_ADAM = 1 } bns_optimizer;
+bns_status bns_set_training(bns_ctx* ctx, int32_t optimizer, double beta1, double beta2, double eps, double dropout,
+                            uint64_t dropout_seed);
+
 /* Debug / parity queries: copy a host-side view into host_dst (capacity in bytes); *written = bytes written.
  * Row tensors are returned as fp32 row-major with LOGICAL dims (padding stripped), inner rows in ascending gid. */
 typedef enum {

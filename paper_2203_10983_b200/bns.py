@@ -28,7 +28,8 @@ PHASES = ["sample", "induce", "pack", "exchange", "spmm_fwd", "gemm_fwd", "loss"
           "exchange_bwd", "scatter", "allreduce", "update", "epoch_total", "sample_total"]
 
 EXPORTS = ["bns_get_unique_id", "bns_group_create", "bns_group_destroy", "bns_setup", "bns_sample_boundary",
-           "bns_epoch", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
+           "bns_epoch", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
+BNS_OPT_SGD, BNS_OPT_ADAM = 0, 1
 
 
 class BnsError(RuntimeError):
@@ -62,6 +63,7 @@ def lib():
         L.bns_setup.argtypes = [ctypes.POINTER(bns_config), i64, vp, vp, vp, vp, vp, ctypes.POINTER(vp)]
         L.bns_sample_boundary.argtypes = [vp, f64, u64, u64]
         L.bns_epoch.argtypes = [vp, vp, f32, vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]
+        L.bns_set_training.argtypes = [vp, i32, f64, f64, f64, f64, u64]
         L.bns_query.argtypes = [vp, i32, i32, vp, i64, ctypes.POINTER(i64)]
         L.bns_stream.restype = vp
         L.bns_stream.argtypes = [vp]
@@ -69,7 +71,7 @@ def lib():
         L.bns_last_error.argtypes = [vp]
         L.bns_destroy.argtypes = [vp]
         for f in ("bns_get_unique_id", "bns_group_create", "bns_setup", "bns_sample_boundary", "bns_epoch",
-                  "bns_query"):
+                  "bns_set_training", "bns_query"):
             getattr(L, f).restype = ctypes.c_int
         L.bns_group_destroy.restype = None
         L.bns_destroy.restype = None
@@ -133,6 +135,11 @@ def bns_epoch(ctx, weights: Sequence, lr: float, grads: Sequence | None = None):
     return loss.value, acc.value
 
 
+def bns_set_training(ctx, optimizer: int = BNS_OPT_SGD, beta1: float = 0.9, beta2: float = 0.999,
+                     eps: float = 1e-8, dropout: float = 0.0, dropout_seed: int = 0):
+    _check(lib().bns_set_training(ctx, optimizer, beta1, beta2, eps, dropout, int(dropout_seed) & (2**64 - 1)), ctx)
+
+
 def bns_query(ctx, what: int, layer: int = 0) -> bytes:
     n = ctypes.c_int64()
     _check(lib().bns_query(ctx, what, layer, None, 0, ctypes.byref(n)), ctx)
@@ -190,6 +197,9 @@ class Context:
             import torch
             torch.cuda.current_stream().synchronize()
         return bns_epoch(self.h, weights, lr, grads)
+
+    def set_training(self, optimizer=BNS_OPT_SGD, beta1=0.9, beta2=0.999, eps=1e-8, dropout=0.0, dropout_seed=0):
+        bns_set_training(self.h, optimizer, beta1, beta2, eps, dropout, dropout_seed)
 
     def query(self, what, layer=0):
         return bns_query(self.h, what, layer)

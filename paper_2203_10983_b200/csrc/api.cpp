@@ -400,6 +400,7 @@ void sample_boundary(Ctx& c, double p, uint64_t seed, uint64_t epoch) {
         (void)d_r;
     }
     collect_times(c);
+    c.epoch_id = epoch;
     c.sampled = true;
 }
 
@@ -443,6 +444,8 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     const Seg* fsegs = c.fwd_mode == 0 ? c.d_seg_static_fwd : (c.fwd_mode == 1 ? c.d_seg_bwd : c.d_seg_fwd);
     const int32_t* fcol = c.fwd_mode == 0 ? c.d_static_col : (c.fwd_mode == 1 ? c.d_tcol : c.d_ind_col);
     const int32_t* S_local = c.d_cand_out + c.n_halo;
+    const bool dropout = c.drop > 0.0;
+    if (dropout) launch_halo_gid(c);
 
     // ------------------------------ forward (Alg.1 l.8-10) ------------------------------
     for (int l = 1; l <= L; ++l) {
@@ -456,6 +459,11 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             PhaseTimer t(c, BNS_PH_EXCHANGE);
             c.tr->exchange(c, c.d_sendbuf, c.send_off.data(), static_cast<char*>(Hin) + n_in * din * ts,
                            c.recv_off.data(), din * ts);
+        }
+        if (dropout) {   // f2 / R38: the layer input as seen by the aggregation and the CONCAT self term
+            PhaseTimer t(c, BNS_PH_UPDATE);
+            launch_dropout(c, Hin, c.Xd[l - 1], n_in + c.n_halo, din, l);
+            Hin = c.Xd[l - 1];
         }
         {
             PhaseTimer t(c, BNS_PH_SPMM_FWD);
@@ -499,7 +507,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     // ------------------------------ backward (l.12) ------------------------------
     for (int l = L; l >= 1; --l) {
         const int64_t din = c.dp[l - 1], dout = c.dp[l];
-        void* Hin = c.H[l - 1];
+        void* Hin = dropout ? c.Xd[l - 1] : c.H[l - 1];
         if (l < L) {
             PhaseTimer t(c, BNS_PH_GEMM_BWD);
             if (c.retain)
@@ -543,6 +551,10 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             a.n_split = c.n_split_bwd;
             launch_spmm(c, a);
         }
+        if (dropout) {   // R38: gradient w.r.t. the dropped-out input -> w.r.t. the layer input (all stacked rows)
+            PhaseTimer t(c, BNS_PH_UPDATE);
+            launch_dropout(c, c.d_dx, c.d_dx, n_in + c.n_halo, din, l);
+        }
         if (m > 1) {
             {
                 PhaseTimer t(c, BNS_PH_EXCHANGE_BWD);
@@ -565,7 +577,13 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     }
     {
         PhaseTimer t(c, BNS_PH_UPDATE);
-        launch_sgd(c, W.data(), host_w ? G.data() : (G_in ? G.data() : nullptr), lr);
+        float* const* Gp = host_w ? G.data() : (G_in ? G.data() : nullptr);
+        if (c.optimizer == BNS_OPT_ADAM) {
+            ++c.adam_t;   // R39: one Adam step per bns_epoch call
+            launch_adam(c, W.data(), Gp, lr);
+        } else {
+            launch_sgd(c, W.data(), Gp, lr);
+        }
     }
     total.reset();
     double scal[2];
@@ -685,6 +703,45 @@ bns_status bns_epoch(bns_ctx* h, float* const* weights, float lr, float* const* 
     return guard(h, [&] {
         BNS_CUDA(cudaSetDevice(c.cfg.device));
         epoch(c, weights, lr, grads, loss, acc);
+    });
+}
+
+bns_status bns_set_training(bns_ctx* h, int32_t optimizer, double beta1, double beta2, double eps, double dropout,
+                            uint64_t dropout_seed) {
+    if (!h) return BNS_ERR_INVALID;
+    Ctx& c = h->c;
+    if (c.failed || c.plan_only) return BNS_ERR_STATE;
+    if ((optimizer != BNS_OPT_SGD && optimizer != BNS_OPT_ADAM) || !(dropout >= 0.0 && dropout < 1.0) ||
+        !(beta1 >= 0.0 && beta1 < 1.0) || !(beta2 >= 0.0 && beta2 < 1.0) || !(eps > 0.0)) {
+        c.err = "bns_set_training: invalid optimizer / betas / eps / dropout";
+        return BNS_ERR_INVALID;
+    }
+    return guard(h, [&] {
+        BNS_CUDA(cudaSetDevice(c.cfg.device));
+        BNS_CUDA(cudaStreamSynchronize(c.stream));
+        c.optimizer = optimizer;
+        c.beta1 = beta1;
+        c.beta2 = beta2;
+        c.eps = eps;
+        c.adam_t = 0;
+        if (optimizer == BNS_OPT_ADAM) {
+            if (!c.d_adam_m) {
+                c.d_adam_m = static_cast<float*>(dalloc(c, c.hostw_n * sizeof(float)));
+                c.d_adam_v = static_cast<float*>(dalloc(c, c.hostw_n * sizeof(float)));
+            }
+            BNS_CUDA(cudaMemset(c.d_adam_m, 0, c.hostw_n * sizeof(float)));
+            BNS_CUDA(cudaMemset(c.d_adam_v, 0, c.hostw_n * sizeof(float)));
+        }
+        c.drop = dropout;
+        c.drop_seed = dropout_seed;
+        if (dropout > 0.0 && c.Xd.empty()) {
+            const size_t ts = tsize(c);
+            c.Xd.assign(c.L, nullptr);
+            for (int l = 0; l < c.L; ++l)
+                c.Xd[l] = dalloc(c, (size_t)(c.plan.n_in + c.halo_cap) * c.dp[l] * ts);
+            c.d_rowgid = static_cast<int32_t*>(dalloc(c, (c.plan.n_in + c.halo_cap + 1) * sizeof(int32_t)));
+            BNS_CUDA(cudaMemcpy(c.d_rowgid, c.plan.V.data(), c.plan.n_in * sizeof(int32_t), cudaMemcpyHostToDevice));
+        }
     });
 }
 

@@ -158,6 +158,16 @@ struct Ctx {
     std::vector<void*> WT;         // bf16 W^T [wcols][wkw] for the tcgen05 forward (K-major B operand)
     std::vector<int64_t> wkw;      // K of W^T: each concat half padded to a multiple of 64
     bool use_tc = false;           // tcgen05 GEMMs (BNS_BF16)
+    // --- f2: Adam + dropout
+    int optimizer = 0;
+    double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+    int64_t adam_t = 0;
+    float* d_adam_m = nullptr;     // logical-size moments, all layers flat (hostw_n)
+    float* d_adam_v = nullptr;
+    double drop = 0.0;
+    uint64_t drop_seed = 0, epoch_id = 0;
+    std::vector<void*> Xd;         // dropped-out layer inputs [inner ; halo] (storage type), per layer
+    int32_t* d_rowgid = nullptr;   // global id of every stacked row [V_i ; U_i]
     float* d_gflat = nullptr;      // all-reduce buffer: Σ_l padded dW (fp32)
     int64_t gflat_n = 0;
     std::vector<int64_t> goff;     // per-layer offset in gflat

@@ -66,6 +66,9 @@ void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlog
 void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre);
 void launch_wpack_all(Ctx& c, float* const* W);
 void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr);
+void launch_adam(Ctx& c, float* const* W, float* const* G, float lr);
+void launch_dropout(Ctx& c, const void* src, void* dst, int64_t rows, int64_t ld, int layer);
+void launch_halo_gid(Ctx& c);
 void launch_sum_ptrs(Ctx& c, const float* const* d_ptrs, int nptr, float* out, int64_t n);
 void launch_sum_ptrs_d(Ctx& c, const double* const* d_ptrs, int nptr, double* out, int64_t n);
 void launch_fill_rowscale_bwd(Ctx& c, float* rs);

@@ -382,3 +382,118 @@ void launch_to_storage(Ctx& c, const float* src, int64_t rows, int32_t dlog, int
 }
 
 }  // namespace bns
+
+namespace bns {
+
+// ---------------------------------------------------------------------------------------------
+// f2 dropout (R38): dst[r][c] = src[r][c] * (keep ? 1/(1-r) : 0), one Philox call per 4 columns, keyed by the
+// row's global id, the column quad, the layer and the epoch.  Used on the layer input (forward) and, in place, on
+// the gradient w.r.t. it (backward).
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void k_dropout(const T* __restrict__ src, T* __restrict__ dst, int64_t rows, int64_t ld,
+                          const int32_t* __restrict__ gid, uint32_t layer, uint32_t e_lo, uint32_t k0, uint32_t k1,
+                          uint64_t thr, float scale) {
+    const int64_t nq = (ld + 3) / 4;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows * nq) return;
+    const int64_t r = t / nq, q = t % nq;
+    const uint4 w = philox4((uint32_t)gid[r], (uint32_t)q, layer, e_lo, k0, k1);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t c = q * 4 + k;
+        if (c >= ld) break;
+        const float f = ((uint64_t)ws[k] >= thr) ? scale : 0.f;
+        dst[r * ld + c] = from_f<T>(to_f<T>(src[r * ld + c]) * f);
+    }
+}
+
+void launch_dropout(Ctx& c, const void* src, void* dst, int64_t rows, int64_t ld, int layer) {
+    if (rows <= 0 || c.drop <= 0.0) return;
+    const uint64_t thr = (uint64_t)std::floor(c.drop * 4294967296.0);
+    const float scale = (float)(1.0 / (1.0 - c.drop));
+    const uint32_t k0 = (uint32_t)(c.drop_seed & 0xffffffffu) ^ 0xD809u, k1 = (uint32_t)(c.drop_seed >> 32);
+    const int64_t n = rows * ((ld + 3) / 4);
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    if (c.prec == BNS_BF16)
+        k_dropout<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, rows, ld,
+                                                             c.d_rowgid, (uint32_t)layer, (uint32_t)c.epoch_id, k0, k1,
+                                                             thr, scale);
+    else
+        k_dropout<float><<<grid, 256, 0, c.stream>>>((const float*)src, (float*)dst, rows, ld, c.d_rowgid,
+                                                     (uint32_t)layer, (uint32_t)c.epoch_id, k0, k1, thr, scale);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+// global ids of the halo rows of this epoch: rowgid[n_in + s] = gid of boundary node U_b[s]
+__global__ void k_halo_gid(const int32_t* __restrict__ cand_gid, const int32_t* __restrict__ U_b, int64_t n_halo,
+                           int64_t n_in, int32_t* __restrict__ rowgid) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n_halo) rowgid[n_in + s] = cand_gid[U_b[s]];
+}
+
+void launch_halo_gid(Ctx& c) {
+    if (c.n_halo <= 0) return;
+    k_halo_gid<<<(unsigned)((c.n_halo + 255) / 256), 256, 0, c.stream>>>(c.d_cand_gid, c.d_cand_out, c.n_halo,
+                                                                         c.plan.n_in, c.d_rowgid);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+// f2 Adam (bias-corrected; Kingma & Ba) over every layer in one launch, moments in fp32 at the logical layout;
+// skipped (moments untouched) when the all-reduced loss is not finite
+struct AdamArgs {
+    float* m;
+    float* v;
+    int64_t moff[kMaxLayers];
+    float lr, b1, b2, eps, c1, c2;
+};
+
+__global__ void k_adam_all(const WDesc d, const AdamArgs a, const double* __restrict__ scal,
+                           int32_t* __restrict__ nonfinite) {
+    const int l = blockIdx.y;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t rows_l = (d.sage ? 2 : 1) * d.din[l], dout = d.dout[l];
+    if (t >= rows_l * dout) return;
+    const bool bad = !isfinite(scal[0]);
+    if (t == 0 && l == 0) *nonfinite = bad ? 1 : 0;
+    const int64_t lr_ = t / dout, lc = t % dout;
+    const int64_t pr = d.sage ? (lr_ < d.din[l] ? lr_ : d.dpin[l] + (lr_ - d.din[l])) : lr_;
+    const float g = d.gpad[l][pr * d.cols_p[l] + lc];
+    if (d.G[l]) d.G[l][t] = g;
+    if (bad) return;
+    float* mm = a.m + a.moff[l] + t;
+    float* vv = a.v + a.moff[l] + t;
+    const float m1 = a.b1 * *mm + (1.f - a.b1) * g;
+    const float v1 = a.b2 * *vv + (1.f - a.b2) * g * g;
+    *mm = m1;
+    *vv = v1;
+    const_cast<float*>(d.W[l])[t] -= a.lr * (m1 / a.c1) / (sqrtf(v1 / a.c2) + a.eps);
+}
+
+void launch_adam(Ctx& c, float* const* W, float* const* G, float lr) {
+    const WDesc d = make_desc(c, W, G);
+    AdamArgs a{};
+    a.m = c.d_adam_m;
+    a.v = c.d_adam_v;
+    int64_t off = 0, mx = 0;
+    for (int l = 0; l < c.L; ++l) {
+        a.moff[l] = off;
+        const int64_t n = (d.sage ? 2 : 1) * d.din[l] * d.dout[l];
+        off += n;
+        mx = std::max(mx, n);
+    }
+    a.lr = lr;
+    a.b1 = (float)c.beta1;
+    a.b2 = (float)c.beta2;
+    a.eps = (float)c.eps;
+    a.c1 = (float)(1.0 - std::pow(c.beta1, (double)c.adam_t));
+    a.c2 = (float)(1.0 - std::pow(c.beta2, (double)c.adam_t));
+    k_adam_all<<<dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, c.stream>>>(d, a, c.d_scal, c.d_nonfinite);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+}  // namespace bns

@@ -275,3 +275,63 @@ def test_nccl_transport_world1_matches_none():
         outs.append((loss, acc, [w.tobytes() for w in Ws], [g.tobytes() for g in G]))
         c.close()
     assert outs[0] == outs[1]
+
+
+# ---------------- f2: Adam + dropout, the paper's recipe ----------------
+@pytest.mark.parametrize("prec", [bns.BNS_FP32, bns.BNS_BF16])
+@pytest.mark.parametrize("layer", [bns.BNS_LAYER_SAGE_MEAN, bns.BNS_LAYER_GCN])
+@pytest.mark.parametrize("m,p,drop", [(1, 1.0, 0.5), (3, 0.5, 0.3)])
+def test_adam_dropout_parity(prec, layer, m, p, drop):
+    dims = [37, 24, 16, 5] if layer == bns.BNS_LAYER_SAGE_MEAN else [37, 16, 5]
+    indptr, indices, part, X, y = wl(3000, 90000, m, dims[0], dims[-1], 31 + m)
+    L = len(dims) - 1
+    Ws = I.weights(dims, layer)
+    Wd = [w.astype(np.float64) for w in Ws]
+    lr, seed = 0.01, 0xD0D0
+    run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y)
+    for c in run.ctx:
+        c.set_training(bns.BNS_OPT_ADAM, 0.9, 0.999, 1e-8, drop, seed)
+    orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
+    orc.set_bf16(prec == bns.BNS_BF16)
+    orc.set_training(optimizer=1, beta1=0.9, beta2=0.999, eps=1e-8, dropout=drop, dropout_seed=seed)
+    tol = TOL[prec]
+    # Adam normalises each step to ~lr, so a gradient entry within its rounding error of zero can take a step of
+    # either sign: weights are compared on the scale of the steps (all within 2 lr per step, and almost all
+    # entries within 0.1 lr).  In bf16 those weight differences then move the next forward beyond the bf16
+    # tolerance, so bf16 is compared over one epoch and fp32 over three.
+    try:
+        for e in range(3 if prec == bns.BNS_FP32 else 1):
+            run.sample(p, SEED, e)
+            orc.sample(p, SEED, e)
+            loss, acc, G, Wn = run.epoch(Ws, lr)
+            lo, ao, Go = orc.epoch(Wd, lr)
+            assert abs(loss - lo) <= LOSS_TOL * abs(lo), (e, loss, lo)
+            for l in range(1, L + 1):
+                assert relerr(run.gather(bns.BNS_Q_Z, l, dims[l - 1]), orc.tensor(O.T_Z, l)) <= tol, ("Z", e, l)
+                assert relerr(run.gather(bns.BNS_Q_DH, l, dims[l]), orc.tensor(O.T_DH, l)) <= tol, ("dH", e, l)
+            for l in range(L):
+                assert relerr(G[l], Go[l]) <= tol, ("dW", e, l)
+                dw = np.abs(Wn[l] - Wd[l])
+                assert dw.max() <= 2.01 * lr * (e + 1), ("W", e, l, dw.max())
+                assert np.mean(dw > 0.1 * lr) < 0.01, ("W", e, l, np.mean(dw > 0.1 * lr))
+            Ws = [w.astype(np.float32) for w in Wn]
+    finally:
+        run.close()
+
+
+def test_dropout_masks_change_per_epoch_and_zero_rate_is_identity():
+    indptr, indices, part, X, y = wl(1500, 30000, 2, 16, 4, 13)
+    dims = [16, 8, 4]
+    outs = []
+    for drop in (0.0, 0.0, 0.4):
+        run = GpuRun(indptr, indices, part, 2, dims, 0, bns.BNS_FP32, X, y)
+        if drop or len(outs) == 1:
+            for c in run.ctx:
+                c.set_training(bns.BNS_OPT_SGD, 0.9, 0.999, 1e-8, drop, 3)
+        try:
+            run.sample(0.5, SEED, 1)
+            outs.append(run.epoch(I.weights(dims, 0), 0.1)[:3])
+        finally:
+            run.close()
+    assert outs[0][0] == outs[1][0] and all(np.array_equal(a, b) for a, b in zip(outs[0][2], outs[1][2]))
+    assert outs[2][0] != outs[0][0]
