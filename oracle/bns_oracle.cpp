@@ -135,7 +135,45 @@ struct Oracle {
     double drop = 0.0;                      // dropout rate r on every layer's input (R38)
     uint64_t drop_seed = 0;
     uint64_t epoch_id = 0;                  // epoch of the last draw (keys the dropout masks)
+    // f3: edge samplers BES / DropEdge (Table tab:bes)
+    int sampler = 0;                        // 0 BNS (node), 1 BES, 2 DropEdge
+    double q = 1.0;                         // arc keep probability of the edge samplers
+    uint64_t sample_seed = 0;
 };
+
+enum { SAMPLER_BNS = 0, SAMPLER_BES = 1, SAMPLER_DROPEDGE = 2 };
+
+// R40 arc draw of the edge samplers: the arc (v <- u) -- target v aggregates source u -- is kept iff
+// Philox4x32-10(ctr = {v, u, e_lo, e_hi}, key = {s_lo ^ 0xED6E, s_hi}).x < floor(q 2^32).  Each direction of an
+// undirected edge is its own arc (it feeds a different node's aggregation); keyed by global ids only, so the
+// draw does not depend on the partitioning.
+bool arc_keep(const Oracle& o, int32_t v, int32_t u) {
+    uint32_t ctr[4] = {(uint32_t)v, (uint32_t)u, (uint32_t)(o.epoch_id & 0xffffffffu), (uint32_t)(o.epoch_id >> 32)};
+    uint32_t key[2] = {(uint32_t)(o.sample_seed & 0xffffffffu) ^ 0xED6Eu, (uint32_t)(o.sample_seed >> 32)};
+    uint32_t out[4];
+    philox4x32_10(ctr, key, out);
+    return (uint64_t)out[0] < threshold_of(o.q);
+}
+
+// Arc (v <- u) of partition i's sampled aggregation, v in V_i: is it in the sampled graph, and with which
+// column scale c (R3, R41)?
+//   BNS      (Alg.1 l.4-5):      u inner -> 1;  u in U_i -> 1/p;  other boundary u -> dropped
+//   BES:     u inner -> 1;  u boundary -> own Bernoulli(q) arc draw, kept -> 1/q
+//   DropEdge:     every arc -> own Bernoulli(q) draw, kept -> 1/q
+// u_row = stacked row of u in partition i (-1 if absent), n_in = |V_i|.
+bool arc_in(const Oracle& o, int32_t v, int32_t u, int64_t u_row, int64_t n_in, double* c) {
+    const bool inner = u_row >= 0 && u_row < n_in;
+    if (o.sampler == SAMPLER_BNS) {
+        if (u_row < 0) return false;
+        *c = inner ? 1.0 : (o.p > 0.0 ? 1.0 / o.p : 0.0);
+        return true;
+    }
+    const double inv_q = o.q > 0.0 ? 1.0 / o.q : 0.0;
+    if (o.sampler == SAMPLER_BES && inner) { *c = 1.0; return true; }
+    if (!arc_keep(o, v, u)) return false;
+    *c = inv_q;
+    return true;
+}
 
 // R38 dropout mask: keep(u, c, l, e) = Philox4x32-10(ctr = {u, c >> 2, l, e_lo}, key = {s_lo ^ 0xD809, s_hi})
 // .word[c & 3] >= floor(r 2^32); a kept value is scaled by 1/(1-r).  Keyed by the global node id, so every copy
@@ -193,11 +231,34 @@ void build_plan(Oracle& o) {
 void sample(Oracle& o, double p, uint64_t seed, uint64_t epoch) {
     uint64_t T = threshold_of(p);
     o.p = p;
+    o.sampler = SAMPLER_BNS;
     for (int i = 0; i < o.m; ++i) {
         Partition& P = o.parts[i];
         P.keep_B.assign(P.B.size(), 0);
         for (size_t k = 0; k < P.B.size(); ++k)
             P.keep_B[k] = keep((uint32_t)P.B[k], (uint32_t)i, epoch, seed, T) ? 1 : 0;
+    }
+}
+
+// f3 edge samplers: a boundary node u in B_i is communicated to i iff at least
+// one of its arcs into V_i survives (u's owner recomputes the same arc draws, R27) -- so U_i is B_i filtered by
+// "some kept arc", in B order, and S_{i,j} = U_j ∩ V_i exactly as for BNS.
+void sample_edges(Oracle& o, int sampler, double q, uint64_t seed, uint64_t epoch) {
+    o.sampler = sampler;
+    o.q = q;
+    o.p = q;
+    o.sample_seed = seed;
+    o.epoch_id = epoch;
+    for (int i = 0; i < o.m; ++i) {
+        Partition& P = o.parts[i];
+        std::vector<uint8_t> hit(o.N, 0);
+        for (int32_t v : P.V)
+            for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
+                const int32_t u = o.indices[e];
+                if (o.part_of[u] != i && arc_keep(o, v, u)) hit[u] = 1;
+            }
+        P.keep_B.assign(P.B.size(), 0);
+        for (size_t k = 0; k < P.B.size(); ++k) P.keep_B[k] = hit[P.B[k]];
     }
 }
 
@@ -240,8 +301,6 @@ struct LocalIndex {
 int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* loss_out, double* acc_out) {
     if (!o.sampled) return 3;
     const int m = o.m, L = o.L;
-    const double p = o.p;
-    const double inv_p = (p > 0.0) ? 1.0 / p : 0.0;   // R32: never used when nothing is kept
     auto st = [&](double x) { return o.bf16 ? rb(x) : x; };   // value as stored (R19)
     std::vector<std::vector<double>> Wq(L);                    // GEMM operand copy of the weights (R19)
     for (int l = 0; l < L; ++l) {
@@ -315,8 +374,8 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                     for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
                         int32_t u = o.indices[e];
                         int64_t ru = idx[i].row[u];
-                        if (ru < 0) continue;                   // dropped boundary neighbour contributes 0
-                        double c = (ru < (int64_t)n_in) ? 1.0 : inv_p;
+                        double c;
+                        if (!arc_in(o, v, u, ru, (int64_t)n_in, &c)) continue;   // dropped: contributes 0
                         for (int k = 0; k < din; ++k) z[k] += c * X[(size_t)ru * din + k];
                     }
                     for (int k = 0; k < din; ++k) z[k] = st(z[k] / (double)dv);
@@ -328,8 +387,8 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                     for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
                         int32_t u = o.indices[e];
                         int64_t ru = idx[i].row[u];
-                        if (ru < 0) continue;
-                        double c = (ru < (int64_t)n_in) ? 1.0 : inv_p;
+                        double c;
+                        if (!arc_in(o, v, u, ru, (int64_t)n_in, &c)) continue;
                         double dtu = (double)(deg(o, u) + 1);
                         double a = c / std::sqrt(dtv * dtu);
                         for (int k = 0; k < din; ++k) z[k] += a * X[(size_t)ru * din + k];
@@ -460,8 +519,8 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                 for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
                     int32_t u = o.indices[e];
                     int64_t ru = idx[i].row[u];
-                    if (ru < 0) continue;
-                    double c = (ru < (int64_t)n_in) ? 1.0 : inv_p;
+                    double c;
+                    if (!arc_in(o, v, u, ru, (int64_t)n_in, &c)) continue;
                     if (o.kind == KIND_GCN) c /= std::sqrt((double)(deg(o, u) + 1));
                     for (int k = 0; k < din; ++k) dX[(size_t)ru * din + k] += c * dZp[r * din + k];
                 }
@@ -577,6 +636,23 @@ int64_t orc_list(void* h, int32_t what, int32_t rank, int32_t peer, int64_t* out
         case 5: v.assign(P.U_off.begin(), P.U_off.end()); break;
         case 6: v.assign(P.S[peer].begin(), P.S[peer].end()); break;
         case 7: v.assign(P.keep_B.begin(), P.keep_B.end()); break;
+        case 8:     // induced (sampled) forward CSR of partition rank: row pointers over V_i
+        case 9: {   // ... and the gids of the kept arcs, rows in V_i order, neighbours in global order
+            if (!o.sampled) return -1;
+            std::vector<int64_t> row(o.N, -1);
+            for (size_t r = 0; r < P.V.size(); ++r) row[P.V[r]] = (int64_t)r;
+            for (size_t s = 0; s < P.U.size(); ++s) row[P.U[s]] = (int64_t)(P.V.size() + s);
+            std::vector<int64_t> ptr(1, 0), col;
+            for (int32_t x : P.V) {
+                for (int64_t e = o.indptr[x]; e < o.indptr[x + 1]; ++e) {
+                    double c;
+                    if (arc_in(o, x, o.indices[e], row[o.indices[e]], (int64_t)P.V.size(), &c)) col.push_back(o.indices[e]);
+                }
+                ptr.push_back((int64_t)col.size());
+            }
+            if (what == 8) v = ptr; else v = col;
+            break;
+        }
         default: return -1;
     }
     int64_t n = (int64_t)v.size();
@@ -612,10 +688,23 @@ int32_t orc_set_training(void* h, int32_t optimizer, double beta1, double beta2,
 
 double orc_drop_factor(void* h, int32_t u, int32_t c, int32_t l) { return drop_factor(*(Oracle*)h, u, c, l); }
 
+// f3: edge samplers (1 BES, 2 DropEdge) with arc keep probability q; then S_{i,j} as for BNS.
+int32_t orc_sample_edges(void* h, int32_t sampler, double q, uint64_t seed, uint64_t epoch) {
+    Oracle& o = *(Oracle*)h;
+    if (!(q >= 0.0 && q <= 1.0) || (sampler != SAMPLER_BES && sampler != SAMPLER_DROPEDGE)) return 1;
+    sample_edges(o, sampler, q, seed, epoch);
+    finish_sample(o);
+    return 0;
+}
+
+// R40 arc draw (v <- u) under the last orc_sample_edges' q / seed / epoch
+int32_t orc_arc_keep(void* h, int32_t v, int32_t u) { return arc_keep(*(Oracle*)h, v, u) ? 1 : 0; }
+
 // Explicit draw (for the hand-computed goldens): keep flags for B_rank in B order.
 int32_t orc_set_keep(void* h, double p, int32_t rank, const int32_t* flags) {
     Oracle& o = *(Oracle*)h;
     o.p = p;
+    o.sampler = SAMPLER_BNS;
     Partition& P = o.parts[rank];
     P.keep_B.assign(P.B.size(), 0);
     for (size_t k = 0; k < P.B.size(); ++k) P.keep_B[k] = flags[k] ? 1 : 0;

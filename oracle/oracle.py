@@ -14,7 +14,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
-V_LIST, B_LIST, B_OFF, D_LIST, U_LIST, U_OFF, S_LIST, KEEP = range(8)
+V_LIST, B_LIST, B_OFF, D_LIST, U_LIST, U_OFF, S_LIST, KEEP, INDUCED_PTR, INDUCED_COL = range(10)
+SAMPLER_BES, SAMPLER_DROPEDGE = 1, 2
 T_H, T_Z, T_DH = 0, 1, 2
 
 
@@ -52,6 +53,10 @@ def lib():
         L.orc_set_training.argtypes = [vp, i32, f64, f64, f64, f64, u64]
         L.orc_drop_factor.restype = f64
         L.orc_drop_factor.argtypes = [vp, i32, i32, i32]
+        L.orc_sample_edges.restype = i32
+        L.orc_sample_edges.argtypes = [vp, i32, f64, u64, u64]
+        L.orc_arc_keep.restype = i32
+        L.orc_arc_keep.argtypes = [vp, i32, i32]
         L.orc_rows_sent.restype = i64
         L.orc_rows_sent.argtypes = [vp, i32]
         _LIB = L
@@ -123,6 +128,14 @@ class Oracle:
     def sample(self, p, seed, epoch):
         rc = lib().orc_sample(self.h, p, seed, epoch)
         assert rc == 0, rc
+
+    def sample_edges(self, sampler, q, seed, epoch):
+        """f3: BES (sampler 1) or DropEdge (2) with arc keep probability q (R40, R41)."""
+        rc = lib().orc_sample_edges(self.h, sampler, q, seed, epoch)
+        assert rc == 0, rc
+
+    def arc_keep(self, v, u):
+        return bool(lib().orc_arc_keep(self.h, v, u))
 
     def set_keep(self, p, per_rank_flags):
         for r, f in enumerate(per_rank_flags):

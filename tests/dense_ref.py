@@ -10,15 +10,20 @@ import numpy as np
 import torch
 
 
-def dense_matrix(indptr, indices, part_of, kept, p, layer):
-    """kept[i] = set of boundary gids sampled by partition i."""
+def dense_matrix(indptr, indices, part_of, kept, p, layer, arcs=None):
+    """kept[i] = set of boundary gids sampled by partition i.  arcs (edge samplers, f3): dict (v, u) -> column
+    scale of every arc in the sampled graph; arcs absent from it are dropped (kept/p are then ignored)."""
     N = len(indptr) - 1
     M = np.zeros((N, N))
     deg = np.diff(indptr)
     for v in range(N):
         i = part_of[v]
         for u in indices[indptr[v]:indptr[v + 1]]:
-            if part_of[u] == i:
+            if arcs is not None:
+                c = arcs.get((v, int(u)))
+                if c is None:
+                    continue
+            elif part_of[u] == i:
                 c = 1.0
             elif u in kept[i]:
                 c = 1.0 / p
@@ -33,9 +38,9 @@ def dense_matrix(indptr, indices, part_of, kept, p, layer):
     return M
 
 
-def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws, masks=None):
+def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws, masks=None, arcs=None):
     """masks[l]: optional N x d_l elementwise factors on the input of layer l+1 (dropout, R38)."""
-    M = torch.tensor(dense_matrix(indptr, indices, part_of, kept, p, layer), dtype=torch.float64)
+    M = torch.tensor(dense_matrix(indptr, indices, part_of, kept, p, layer, arcs), dtype=torch.float64)
     H = torch.tensor(np.asarray(X, np.float64))
     W = [torch.tensor(np.asarray(w, np.float64), requires_grad=True) for w in Ws]
     y = torch.tensor(np.asarray(labels, np.int64))
