@@ -44,6 +44,13 @@ def parse():
     # m=8, p=0.1) -- the slowest rank sets the epoch time; see DESIGN.md §4
     ap.add_argument("--partition", default="random", choices=["ldg2", "random"])
     ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--adam", action="store_true", help="Adam instead of SGD (the paper's optimizer, §8(f) f2)")
+    ap.add_argument("--dropout", type=float, default=0.0, help="dropout rate (paper: 0.5 on Reddit, §8(f) f2)")
+    ap.add_argument("--sampler", default="bns", choices=["bns", "bes", "dropedge"],
+                    help="f3: BES / DropEdge edge sampling instead of BNS (PAPER.md:676-688, Table tab:bes)")
+    ap.add_argument("--q", type=float, default=None,
+                    help="edge keep probability; default matched to BNS p (P:681): BES q = p, "
+                         "DropEdge q = 1 - (1-p) cross/nnz")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-scale", type=float, default=64.0, help="oracle sample = workload scaled down by this")
     ap.add_argument("--no-e2e", action="store_true")
@@ -293,6 +300,8 @@ def run_ours(args):
     ctx = bns.Context(rank=rank, world=world, dims=shape.dims, layer=shape.layer, precision=prec, indptr=indptr,
                       indices=indices, part_of=part, features=X, labels=y, device=local, nccl_id=nccl_id,
                       max_p=0.0, flags=bns.BNS_TIMING)
+    if args.adam or args.dropout > 0:
+        ctx.set_training(bns.BNS_OPT_ADAM if args.adam else bns.BNS_OPT_SGD, 0.9, 0.999, 1e-8, args.dropout, 0xD0)
     del X
     t_setup = time.perf_counter() - t_setup
     Ws = I.weights(shape.dims, shape.layer)
@@ -307,8 +316,20 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    sampler = {"bns": bns.BNS_SAMPLER_BNS, "bes": bns.BNS_SAMPLER_BES, "dropedge": bns.BNS_SAMPLER_DROPEDGE}[args.sampler]
+    q = args.q
+    if sampler != bns.BNS_SAMPLER_BNS and q is None:
+        # P:681 "all methods drop the same number of edges with BNS-GCN (p=0.1) over the full graph"
+        src = np.repeat(np.arange(len(indptr) - 1, dtype=np.int32), np.diff(indptr))
+        cross = int(np.count_nonzero(part[src] != part[indices]))
+        q = args.p if sampler == bns.BNS_SAMPLER_BES else 1.0 - (1.0 - args.p) * cross / max(1, len(indices))
+        del src
+
     def step(e, W, G):
-        ctx.sample_boundary(args.p, I.BNS_SEED, e)
+        if sampler == bns.BNS_SAMPLER_BNS:
+            ctx.sample_boundary(args.p, I.BNS_SEED, e)
+        else:
+            ctx.sample_edges(sampler, q, I.BNS_SEED, e)
         return ctx.epoch(W, args.lr, G)
 
     for e in range(args.warmup):
@@ -401,7 +422,11 @@ def run_ours(args):
                                    f"m={world} partitions ({args.partition})",
                        "global_batch": "full graph", "parallelism": f"partition-parallel m={world}",
                        "l2": "flushed between timed steps (2x L2 write, outside the events)",
-                       "step": "bns_sample_boundary + bns_epoch (SGD update included)"},
+                       "step": "%s + bns_epoch (%s update included%s)" % (
+                           "bns_sample_boundary" if sampler == bns.BNS_SAMPLER_BNS else
+                           f"bns_sample_edges({args.sampler}, q={q:.4f})",
+                           "Adam" if args.adam else "SGD",
+                           f", dropout {args.dropout}" if args.dropout > 0 else "")},
             "roofline": {"bound": "hbm", "kernel": "segment SpMM (a6 fwd + a10 bwd, incl. split-row fixup)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": (achieved / hbm_peak) if achieved else None, "traffic": latest_traffic(),
@@ -422,6 +447,7 @@ def run_ours(args):
             "partition_stats": {"n_in": [int(a[0]) for a in allst], "n_bd": [int(a[1]) for a in allst],
                                 "n_halo": [int(a[2]) for a in allst], "nnz": [int(a[3]) for a in allst],
                                 "nnz_kept": [int(a[4]) for a in allst]},
+            "rows_exchanged_per_layer": int(sum(a[2] for a in allst)),
             "loss_last": losses[-1], "setup_s": t_setup, "wall_s_timed": wall,
             "step_ms": step_ms,
             "memory_bytes": ctx.memory()[0],

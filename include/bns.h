@@ -114,7 +114,21 @@ bns_status bns_setup(const bns_config* cfg, int64_t num_nodes, const int64_t* in
  * messages are sent).  p > max_p, or a draw larger than the halo capacity -> BNS_ERR_OOM. */
 bns_status bns_sample_boundary(bns_ctx* ctx, double p, uint64_t seed, uint64_t epoch);
 
-/* Alg.1 l.8-14 with the draw of the last bns_sample_boundary.
+/* the edge-sampling baselines of PAPER.md:676-688 (Table tab:bes), on the same exchange
+ * machinery; a replacement for bns_sample_boundary before bns_epoch.
+ *   sampler BNS_SAMPLER_BES: every cross-partition arc (v <- u), v in V_i, u in B_i, kept with probability q;
+ *       intra-partition arcs always kept.  BNS_SAMPLER_DROPEDGE: every arc of the graph kept with probability q.
+ *   Arc draw (R40): keep(v <- u) = Philox4x32-10(ctr = {v, u, e_lo, e_hi}, key = {seed_lo ^ 0xED6E, seed_hi}).x
+ *       < floor(q 2^32), global ids; each direction of an edge is its own arc.
+ *   U_i = the u in B_i with at least one kept arc into V_i (B order); the owner recomputes the same draws for S_{i,j}
+ *   (R27).  Kept arcs carry the column scale 1/q (R41: unbiased; BES intra arcs 1; GCN self loops 1, never
+ *   dropped); the SAGE denominator stays deg_G(v).
+ *   q in [0, 1].  The first call allocates the per-arc buffers (two int32 per static arc).  A halo larger than
+ *   the capacity (cfg.max_p) -> BNS_ERR_OOM.  Same sync / collective behaviour as bns_sample_boundary. */
+typedef enum { BNS_SAMPLER_BNS = 0, BNS_SAMPLER_BES = 1, BNS_SAMPLER_DROPEDGE = 2 } bns_sampler;
+bns_status bns_sample_edges(bns_ctx* ctx, int32_t sampler, double q, uint64_t seed, uint64_t epoch);
+
+/* Alg.1 l.8-14 with the draw of the last bns_sample_boundary (or bns_sample_edges).
  *   weights[l], l < L: fp32 row-major, SAGE (2*dims[l]) x dims[l+1] (rows [0,dims[l]) multiply z_v, R14),
  *       GCN dims[l] x dims[l+1].  Device pointers on cfg.device (updated in place: W <- W - lr*g) or host
  *       pointers (copied in and out inside the call).
@@ -163,7 +177,9 @@ typedef enum {
     BNS_Q_STATIC_CSR = 17,   /* int64[n_in+1] then int32[nnz_i]: static rows, columns encoded inner j -> j,
                                 boundary index b -> -(b+1) (plan, available in BNS_PLAN_ONLY) */
     BNS_Q_MEMORY = 18,       /* int64[2]: device bytes allocated by the context, peak device bytes */
-    BNS_Q_KERNEL_COUNT = 19  /* int64[1]: kernels launched by this context since setup */
+    BNS_Q_KERNEL_COUNT = 19, /* int64[1]: kernels launched by this context since setup */
+    BNS_Q_INDUCED_T = 20     /* edge samplers: int64[n_in+n_bd+1] row pointers then int32[nnz] local inner columns
+                                of the sampled TRANSPOSED aggregation (rows: inner u, then boundary index b) */
 } bns_query_what;
 
 enum { BNS_PH_SAMPLE = 0, BNS_PH_INDUCE, BNS_PH_PACK, BNS_PH_EXCHANGE, BNS_PH_SPMM_FWD, BNS_PH_GEMM_FWD,

@@ -23,12 +23,13 @@ BNS_TRANSPORT_NONE, BNS_TRANSPORT_NCCL, BNS_TRANSPORT_LOCAL, BNS_TRANSPORT_NULL_
 BNS_PLAN_ONLY, BNS_DEBUG_EXCHANGE_INDICES, BNS_TIMING, BNS_RETAIN_GRADS = 0x1, 0x2, 0x4, 0x8
 (BNS_Q_COUNTS, BNS_Q_INNER, BNS_Q_BOUNDARY, BNS_Q_BOUNDARY_OFF, BNS_Q_SENDCAND, BNS_Q_SENDCAND_OFF, BNS_Q_MASK,
  BNS_Q_HALO, BNS_Q_HALO_OFF, BNS_Q_SEND, BNS_Q_SEND_OFF, BNS_Q_H, BNS_Q_Z, BNS_Q_DH, BNS_Q_HALO_ROWS, BNS_Q_INDUCED,
- BNS_Q_TIMES, BNS_Q_STATIC_CSR, BNS_Q_MEMORY, BNS_Q_KERNEL_COUNT) = range(20)
+ BNS_Q_TIMES, BNS_Q_STATIC_CSR, BNS_Q_MEMORY, BNS_Q_KERNEL_COUNT, BNS_Q_INDUCED_T) = range(21)
+BNS_SAMPLER_BNS, BNS_SAMPLER_BES, BNS_SAMPLER_DROPEDGE = 0, 1, 2
 PHASES = ["sample", "induce", "pack", "exchange", "spmm_fwd", "gemm_fwd", "loss", "gemm_bwd", "spmm_bwd",
           "exchange_bwd", "scatter", "allreduce", "update", "epoch_total", "sample_total"]
 
 EXPORTS = ["bns_get_unique_id", "bns_group_create", "bns_group_destroy", "bns_setup", "bns_sample_boundary",
-           "bns_epoch", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
+           "bns_sample_edges", "bns_epoch", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
 BNS_OPT_SGD, BNS_OPT_ADAM = 0, 1
 
 
@@ -62,6 +63,7 @@ def lib():
         L.bns_group_destroy.argtypes = [vp]
         L.bns_setup.argtypes = [ctypes.POINTER(bns_config), i64, vp, vp, vp, vp, vp, ctypes.POINTER(vp)]
         L.bns_sample_boundary.argtypes = [vp, f64, u64, u64]
+        L.bns_sample_edges.argtypes = [vp, i32, f64, u64, u64]
         L.bns_epoch.argtypes = [vp, vp, f32, vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]
         L.bns_set_training.argtypes = [vp, i32, f64, f64, f64, f64, u64]
         L.bns_query.argtypes = [vp, i32, i32, vp, i64, ctypes.POINTER(i64)]
@@ -70,7 +72,7 @@ def lib():
         L.bns_last_error.restype = ctypes.c_char_p
         L.bns_last_error.argtypes = [vp]
         L.bns_destroy.argtypes = [vp]
-        for f in ("bns_get_unique_id", "bns_group_create", "bns_setup", "bns_sample_boundary", "bns_epoch",
+        for f in ("bns_get_unique_id", "bns_group_create", "bns_setup", "bns_sample_boundary", "bns_sample_edges", "bns_epoch",
                   "bns_set_training", "bns_query"):
             getattr(L, f).restype = ctypes.c_int
         L.bns_group_destroy.restype = None
@@ -122,6 +124,10 @@ def bns_setup(cfg: bns_config, indptr, indices, part_of, features, labels):
 
 def bns_sample_boundary(ctx, p: float, seed: int, epoch: int):
     _check(lib().bns_sample_boundary(ctx, float(p), int(seed) & (2**64 - 1), int(epoch) & (2**64 - 1)), ctx)
+
+
+def bns_sample_edges(ctx, sampler: int, q: float, seed: int, epoch: int):
+    _check(lib().bns_sample_edges(ctx, int(sampler), float(q), int(seed) & (2**64 - 1), int(epoch) & (2**64 - 1)), ctx)
 
 
 def bns_epoch(ctx, weights: Sequence, lr: float, grads: Sequence | None = None):
@@ -192,6 +198,9 @@ class Context:
     def sample_boundary(self, p, seed, epoch):
         bns_sample_boundary(self.h, p, seed, epoch)
 
+    def sample_edges(self, sampler, q, seed, epoch):
+        bns_sample_edges(self.h, sampler, q, seed, epoch)
+
     def epoch(self, weights, lr, grads=None):
         if weights and hasattr(weights[0], "is_cuda") and weights[0].is_cuda:
             import torch
@@ -228,6 +237,13 @@ class Context:
         b = self.query(BNS_Q_INDUCED)
         ptr = np.frombuffer(b[: 8 * (n_in + 1)], np.int64).copy()
         col = np.frombuffer(b[8 * (n_in + 1):], np.int32).copy()
+        return ptr, col
+
+    def induced_t(self, n_rows):
+        """Edge samplers: sampled transposed CSR over rows [inner u ; boundary index b] (n_rows = n_in + n_bd)."""
+        b = self.query(BNS_Q_INDUCED_T)
+        ptr = np.frombuffer(b[: 8 * (n_rows + 1)], np.int64).copy()
+        col = np.frombuffer(b[8 * (n_rows + 1):], np.int32).copy()
         return ptr, col
 
     def static_csr(self, n_in):

@@ -337,26 +337,65 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     BNS_CUDA(cudaStreamSynchronize(c.stream));
 }
 
+// f3: the edge samplers' static per-arc arrays, built by the first bns_sample_edges (not on the BNS path)
+void edge_init(Ctx& c) {
+    if (c.edge_ready) return;
+    const Plan& P = c.plan;
+    const int64_t n_rows = P.n_in + P.n_bd;
+    c.d_vgid = upload(c, P.V);
+    std::vector<int32_t> erow(c.nnz_i);
+    for (int64_t r = 0; r < P.n_in; ++r)
+        for (int64_t e = P.row_ptr[r]; e < P.row_ptr[r + 1]; ++e) erow[e] = (int32_t)r;
+    c.d_erow = upload(c, erow);
+    c.tnnz = c.ii_nnz + (int64_t)P.br_col.size();
+    if (c.tnnz != c.nnz_i) throw Error(BNS_ERR_RUNTIME, "transposed arc count != static arc count");
+    std::vector<int64_t> tptr(n_rows + 1);
+    for (int64_t r = 0; r <= P.n_in; ++r) tptr[r] = P.ii_ptr[r];
+    for (int64_t b = 1; b <= P.n_bd; ++b) tptr[P.n_in + b] = c.ii_nnz + P.br_ptr[b];
+    std::vector<int32_t> terow(c.tnnz);
+    for (int64_t r = 0; r < n_rows; ++r)
+        for (int64_t e = tptr[r]; e < tptr[r + 1]; ++e) terow[e] = (int32_t)r;
+    c.d_tptr = upload(c, tptr);
+    c.d_terow = upload(c, terow);
+    c.d_ind_tcol = static_cast<int32_t*>(dalloc(c, (c.tnnz + 1) * sizeof(int32_t)));
+    c.d_ind_tptr = static_cast<int64_t*>(dalloc(c, (n_rows + 1) * sizeof(int64_t)));
+    c.d_trow_nseg = static_cast<int32_t*>(dalloc(c, (n_rows + 1) * sizeof(int32_t)));
+    c.d_trow_soff = static_cast<int64_t*>(dalloc(c, (n_rows + 2) * sizeof(int64_t)));
+    c.d_eseg_bwd = static_cast<Seg*>(dalloc(c, c.seg_bwd_cap * sizeof(Seg)));
+    c.d_esplit_bwd = static_cast<int64_t*>(dalloc(c, (c.n_split_bwd_inner + P.n_bd + 1) * sizeof(int64_t)));
+    c.edge_ready = true;
+}
+
 // ---------------------------------------------------------------------------------------------
-// bns_sample_boundary: a1-a3
+// bns_sample_boundary / bns_sample_edges: a1-a3
 // ---------------------------------------------------------------------------------------------
-void sample_boundary(Ctx& c, double p, uint64_t seed, uint64_t epoch) {
+void sample_boundary(Ctx& c, int sampler, double p, uint64_t seed, uint64_t epoch) {
     const int m = c.cfg.world;
     const uint64_t T = (uint64_t)std::floor(p * 4294967296.0);
+    const bool edges = sampler != BNS_SAMPLER_BNS;
+    c.sampler = sampler;
     c.p = p;
-    c.inv_p = p > 0.0 ? 1.0 / p : 0.0;
+    if (sampler == BNS_SAMPLER_DROPEDGE) {   // R41: 1/q on every arc -> neighbour-sum scale, no column scale
+        c.inv_p = 1.0;
+        c.nscale = p > 0.0 ? (float)(1.0 / p) : 0.f;
+    } else {                                 // BNS 1/p, BES 1/q: column scale of the halo columns (R3, R41)
+        c.inv_p = p > 0.0 ? 1.0 / p : 0.0;
+        c.nscale = 1.f;
+    }
     c.sampled = false;
     std::unique_ptr<PhaseTimer> total(new PhaseTimer(c, BNS_PH_SAMPLE_TOTAL));
     {
         PhaseTimer t(c, BNS_PH_SAMPLE);
-        launch_sample(c, T, seed, epoch);
+        if (edges) launch_sample_edges(c, T, seed, epoch);
+        else launch_sample(c, T, seed, epoch);
     }
     const bool has_bd = c.plan.n_bd > 0;
-    c.fwd_mode = (!has_bd || T >= (1ull << 32)) ? 0 : (T == 0 ? 1 : 2);
+    c.fwd_mode = edges ? 2 : (!has_bd || T >= (1ull << 32)) ? 0 : (T == 0 ? 1 : 2);
     {
         PhaseTimer t(c, BNS_PH_INDUCE);
-        if (c.fwd_mode == 2) launch_induce(c);
-        launch_bwd_segments(c);
+        if (c.fwd_mode == 2) launch_induce(c, T, seed, epoch);
+        if (edges) launch_induce_bwd_edges(c, T, seed, epoch);
+        else launch_bwd_segments(c);
         if (c.layer == BNS_LAYER_GCN) launch_gcn_cscale(c);
     }
     total.reset();
@@ -372,8 +411,13 @@ void sample_boundary(Ctx& c, double p, uint64_t seed, uint64_t epoch) {
     if (c.fwd_mode == 0) { c.nnz_kept = c.nnz_i; c.n_seg_fwd = c.n_seg_static_fwd; c.n_split_fwd = c.n_split_sf; }
     else if (c.fwd_mode == 1) { c.nnz_kept = c.ii_nnz; c.n_seg_fwd = c.n_seg_bwd_inner; c.n_split_fwd = c.n_split_bwd_inner; }
     else { c.nnz_kept = tot[0]; c.n_seg_fwd = tot[1]; c.n_split_fwd = tot[4]; }
-    c.n_seg_bwd = c.n_seg_bwd_inner + (has_bd ? tot[2] : 0);
-    c.n_split_bwd = c.n_split_bwd_inner + (has_bd ? tot[3] : 0);
+    if (edges) {
+        c.n_seg_bwd = tot[6];
+        c.n_split_bwd = tot[7];
+    } else {
+        c.n_seg_bwd = c.n_seg_bwd_inner + (has_bd ? tot[2] : 0);
+        c.n_split_bwd = c.n_split_bwd_inner + (has_bd ? tot[3] : 0);
+    }
     if (c.n_halo > c.halo_cap)
         throw Error(BNS_ERR_OOM, "sampled halo (" + std::to_string(c.n_halo) + " rows) exceeds capacity " +
                                      std::to_string(c.halo_cap) + " (raise cfg.max_p)");
@@ -479,6 +523,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             a.d = (int32_t)din;
             a.n_in = n_in;
             a.inv_p = inv_p;
+            a.nscale = c.nscale;
             a.rowscale = sage ? c.d_deg_in : c.d_rs_in;
             a.cscale = c.d_cscale;
             a.partial = c.d_partial;
@@ -532,10 +577,11 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         {
             PhaseTimer t(c, BNS_PH_SPMM_BWD);
             SpmmArgs a{};
+            const bool eb = c.sampler != BNS_SAMPLER_BNS;   // f3: the sampled transposed CSR of this epoch
             a.mode = sage ? SAGE_BWD : GCN_BWD;
-            a.segs = c.d_seg_bwd;
+            a.segs = eb ? c.d_eseg_bwd : c.d_seg_bwd;
             a.n_segs = c.n_seg_bwd;
-            a.col = c.d_tcol;
+            a.col = eb ? c.d_ind_tcol : c.d_tcol;
             a.src = c.d_dxcat;
             a.ld_src = sage ? 2 * din : din;
             a.out = c.d_dx;
@@ -545,9 +591,10 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             a.d = (int32_t)din;
             a.n_in = n_in;
             a.inv_p = inv_p;
+            a.nscale = c.nscale;
             a.cscale = c.d_cscale;
             a.partial = c.d_partial;
-            a.split = c.d_split_bwd;
+            a.split = eb ? c.d_esplit_bwd : c.d_split_bwd;
             a.n_split = c.n_split_bwd;
             launch_spmm(c, a);
         }
@@ -688,7 +735,20 @@ bns_status bns_sample_boundary(bns_ctx* h, double p, uint64_t seed, uint64_t epo
     }
     return guard(h, [&] {
         BNS_CUDA(cudaSetDevice(c.cfg.device));
-        sample_boundary(c, p, seed, epoch);
+        sample_boundary(c, BNS_SAMPLER_BNS, p, seed, epoch);
+    });
+}
+
+bns_status bns_sample_edges(bns_ctx* h, int32_t sampler, double q, uint64_t seed, uint64_t epoch) {
+    if (!h) return BNS_ERR_INVALID;
+    Ctx& c = h->c;
+    if (c.failed || c.plan_only) return BNS_ERR_STATE;
+    if (sampler != BNS_SAMPLER_BES && sampler != BNS_SAMPLER_DROPEDGE) { c.err = "bad sampler"; return BNS_ERR_INVALID; }
+    if (!(q >= 0.0 && q <= 1.0)) { c.err = "q must be in [0, 1]"; return BNS_ERR_INVALID; }
+    return guard(h, [&] {
+        BNS_CUDA(cudaSetDevice(c.cfg.device));
+        edge_init(c);
+        sample_boundary(c, sampler, q, seed, epoch);
     });
 }
 
@@ -877,6 +937,17 @@ bns_status bns_query(bns_ctx* h, int32_t what, int32_t layer, void* dst, int64_t
                 break;
             }
             case BNS_Q_KERNEL_COUNT: put(&c.kernels, 8); break;
+            case BNS_Q_INDUCED_T: {
+                need_sample();
+                if (c.sampler == BNS_SAMPLER_BNS) throw Error(BNS_ERR_STATE, "BNS_Q_INDUCED_T needs bns_sample_edges");
+                const int64_t n_rows = P.n_in + P.n_bd;
+                std::vector<int64_t> ptr(n_rows + 1);
+                BNS_CUDA(cudaMemcpy(ptr.data(), c.d_ind_tptr, (n_rows + 1) * 8, cudaMemcpyDeviceToHost));
+                std::vector<int32_t> col = vec32(c.d_ind_tcol, ptr[n_rows]);
+                put(ptr.data(), ptr.size() * 8);
+                put(col.data(), col.size() * 4);
+                break;
+            }
             default: throw Error(BNS_ERR_INVALID, "unknown query");
         }
         if (written) *written = (int64_t)out.size();

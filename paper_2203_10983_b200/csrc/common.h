@@ -176,6 +176,18 @@ struct Ctx {
     double* d_scal = nullptr;      // [loss_sum, correct] (all-reduced)
     double* d_lpart = nullptr;     // per-block loss partials
     int32_t* d_nonfinite = nullptr;
+    // --- f3: edge samplers (BES / DropEdge); allocated by the first bns_sample_edges
+    int sampler = 0;               // BNS_SAMPLER_* of the last draw
+    float nscale = 1.f;            // neighbour-sum scale (DropEdge: 1/q on every arc; else 1)
+    bool edge_ready = false;
+    int32_t* d_vgid = nullptr;     // inner gids
+    int32_t* d_erow = nullptr;     // row of every static forward arc
+    int64_t* d_tptr = nullptr;     // transposed rows [A_II rows ; boundary rows], n_in + n_bd + 1
+    int32_t* d_terow = nullptr;    // row of every transposed arc
+    int64_t tnnz = 0;
+    int32_t* d_ind_tcol = nullptr; int64_t* d_ind_tptr = nullptr;
+    int32_t* d_trow_nseg = nullptr; int64_t* d_trow_soff = nullptr;
+    Seg* d_eseg_bwd = nullptr; int64_t* d_esplit_bwd = nullptr;
     float* d_hostw = nullptr;      // staging for host-pointer weights (flat)
     int64_t n_train_global = 0;
     int64_t n_train_local = 0;

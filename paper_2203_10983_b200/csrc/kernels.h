@@ -8,8 +8,12 @@ namespace bns {
 // a1 + a2: Philox Bernoulli draw over all candidates and order-preserving compaction (sample.cu)
 void launch_sample(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch);
 // a3: induced subgraph over V_i ∪ U_i + forward segments; backward (transposed) halo segments (sample.cu)
-void launch_induce(Ctx& c);
+void launch_induce(Ctx& c, uint64_t T = 0, uint64_t seed = 0, uint64_t epoch = 0);   // T, seed, epoch: edge samplers
 void launch_bwd_segments(Ctx& c);
+// f3 edge samplers: candidate flags from the arc draws (replaces the node draw of launch_sample), and the sampled
+// transposed CSR + backward segments (replaces launch_bwd_segments)
+void launch_sample_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch);
+void launch_induce_bwd_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch);
 // static segments for a static CSR (setup)
 int64_t build_static_segments(Ctx& c, const int64_t* d_ptr, int64_t rows, int64_t ptr_base, Seg* d_out);
 // exclusive scan of int32 -> int64 (n elements), total written to *d_total if non-null
@@ -27,6 +31,7 @@ struct SpmmArgs {
     int32_t d;                            // padded feature width
     int64_t n_in;
     float inv_p;
+    float nscale = 1.f;                   // neighbour-sum scale before the epilogue terms (DropEdge 1/q; else 1)
     const float* rowscale;                // per output row
     const float* cscale;                  // GCN_FWD per column
     const int32_t* halo_b;                // GCN_BWD: boundary index of halo slot

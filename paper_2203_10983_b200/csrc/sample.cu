@@ -299,14 +299,19 @@ __global__ void k_induce_segs(const int64_t* __restrict__ out_ptr, int64_t n_in,
     }
 }
 
-void launch_induce(Ctx& c) {
+void launch_induce_flags_edge(Ctx& c, int64_t nb, uint64_t T, uint64_t seed, uint64_t epoch);
+
+void launch_induce(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     const int64_t n_in = c.plan.n_in;
     const int64_t nnz = c.nnz_i;
     const int m = c.cfg.world;
     int64_t* tot = c.d_seg_pos + 2 * m + 1;   // [nnz_kept, n_seg_fwd, n_seg_bwd_halo]
     const int64_t nb = (nnz + 1023) / 1024;
     if (nb > 0) {
-        k_induce_flags<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eblk);
+        if (c.sampler == BNS_SAMPLER_BNS)
+            k_induce_flags<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eblk);
+        else
+            launch_induce_flags_edge(c, nb, T, seed, epoch);
         k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_eblk, c.d_eboff, nb, tot + 0);
         k_induce_scatter<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff,
                                                               n_in, c.d_ind_col);
@@ -384,6 +389,197 @@ void launch_bwd_segments(Ctx& c) {
                                             c.d_split_bwd + c.n_split_bwd_inner, tot + 3);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------------------------
+// f3 edge samplers: BES keeps each cross-partition arc with probability q, DropEdge every arc.
+// R40 arc draw: keep(v <- u) = Philox4x32-10(ctr = {v, u, e_lo, e_hi}, key = {s_lo ^ 0xED6E, s_hi}).x < T(q).
+// ---------------------------------------------------------------------------------------------
+struct ArcKey {
+    uint64_t T;
+    uint32_t e_lo, e_hi, k0, k1;
+    __device__ __forceinline__ bool keep(int32_t v, int32_t u) const {
+        return (uint64_t)philox_x((uint32_t)v, (uint32_t)u, e_lo, e_hi, k0, k1) < T;
+    }
+};
+
+inline ArcKey arc_key(uint64_t T, uint64_t seed, uint64_t epoch) {
+    return ArcKey{T, (uint32_t)epoch, (uint32_t)(epoch >> 32), (uint32_t)seed ^ 0xED6Eu, (uint32_t)(seed >> 32)};
+}
+
+// a1 for the edge samplers: receive candidate b in B_i is communicated iff one of its arcs into V_i survives;
+// send candidate (u, peer j) iff one of u's arcs into V_j survives (j's draw recomputed, R27).  Same flags/block
+// count contract as k_sample_count, so the a2 compaction is shared.
+__global__ void __launch_bounds__(kSampleBlock) k_edge_cand(int64_t n_bd, int64_t n, const int32_t* __restrict__ gid,
+                                                            const int32_t* __restrict__ key,
+                                                            const int32_t* __restrict__ payload,
+                                                            const int32_t* __restrict__ vgid,
+                                                            const int64_t* __restrict__ br_ptr,
+                                                            const int32_t* __restrict__ br_col,
+                                                            const int64_t* __restrict__ row_ptr,
+                                                            const int32_t* __restrict__ col_enc,
+                                                            const int64_t* __restrict__ b_off, ArcKey ak,
+                                                            uint8_t* __restrict__ flags, int32_t* __restrict__ blk) {
+    const int64_t i = (int64_t)blockIdx.x * kSampleBlock + threadIdx.x;
+    int keep = 0;
+    if (i < n) {
+        if (i < n_bd) {
+            const int32_t ug = gid[i];
+            for (int64_t e = br_ptr[i]; e < br_ptr[i + 1] && !keep; ++e) keep = ak.keep(vgid[br_col[e]], ug);
+        } else {
+            const int32_t u = payload[i], j = key[i], ug = gid[i];
+            const int64_t lo = b_off[j], hi = b_off[j + 1];
+            for (int64_t e = row_ptr[u]; e < row_ptr[u + 1] && !keep; ++e) {
+                const int32_t x = col_enc[e];
+                if (x < 0 && -x - 1 >= lo && -x - 1 < hi) keep = ak.keep(gid[-x - 1], ug);
+            }
+        }
+        flags[i] = (uint8_t)keep;
+    }
+    const int cnt = __syncthreads_count(keep);
+    if (threadIdx.x == 0) blk[blockIdx.x] = cnt;
+}
+
+void launch_sample_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
+    const int m = c.cfg.world;
+    const int64_t n = c.n_cand;
+    const int64_t nb = (n + kSampleBlock - 1) / kSampleBlock;
+    int64_t* boff = c.d_scan_tmp;
+    if (nb > 0) {
+        k_edge_cand<<<(unsigned)nb, kSampleBlock, 0, c.stream>>>(
+            c.plan.n_bd, n, c.d_cand_gid, c.d_cand_key, c.d_cand_payload, c.d_vgid, c.d_br_ptr, c.d_tcol + c.ii_nnz,
+            c.d_row_ptr, c.d_col_enc, c.d_cand_seg, arc_key(T, seed, epoch), c.d_flags, c.d_blk);
+        k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_blk, boff, nb, nullptr);
+        k_sample_scatter<<<(unsigned)nb, kSampleBlock, 0, c.stream>>>(c.d_flags, n, c.plan.n_bd, boff,
+                                                                      c.d_cand_payload, c.d_cand_seg, 2 * m + 1,
+                                                                      c.d_cand_out, c.d_slot_of_b, c.d_seg_pos);
+        c.kernels += 3;
+    } else {
+        BNS_CUDA(cudaMemsetAsync(boff, 0, sizeof(int64_t), c.stream));
+    }
+    k_seg_tail<<<1, 128, 0, c.stream>>>(c.d_cand_seg, 2 * m + 1, n, boff, nb, c.d_seg_pos);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+// a3 for the edge samplers, forward: arc (v <- x) of the static CSR kept by its draw (DropEdge: every arc; BES:
+// boundary columns only).  A kept boundary arc implies its column's node is in U_i, so the remap is defined.
+__global__ void __launch_bounds__(1024) k_induce_flags_edge(const int32_t* __restrict__ col_enc,
+                                                            const int32_t* __restrict__ erow, int64_t nnz,
+                                                            const int32_t* __restrict__ vgid,
+                                                            const int32_t* __restrict__ bgid, int dropedge, ArcKey ak,
+                                                            uint32_t* __restrict__ bits, int32_t* __restrict__ blk) {
+    const int64_t e = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    int keep = 0;
+    if (e < nnz) {
+        const int32_t x = col_enc[e];
+        if (x >= 0) keep = dropedge ? ak.keep(vgid[erow[e]], vgid[x]) : 1;
+        else keep = ak.keep(vgid[erow[e]], bgid[-x - 1]);
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    if ((threadIdx.x & 31) == 0) bits[e >> 5] = b;
+    const int cnt = __syncthreads_count(keep);
+    if (threadIdx.x == 0) blk[blockIdx.x] = cnt;
+}
+
+void launch_induce_flags_edge(Ctx& c, int64_t nb, uint64_t T, uint64_t seed, uint64_t epoch) {
+    k_induce_flags_edge<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_col_enc, c.d_erow, c.nnz_i, c.d_vgid, c.d_cand_gid,
+                                                             c.sampler == BNS_SAMPLER_DROPEDGE,
+                                                             arc_key(T, seed, epoch), c.d_ebits, c.d_eblk);
+}
+
+// backward: the transposed arcs (row u <- column v means v aggregates u) -- inner rows u (A_II^T), then boundary
+// rows b (the arcs v <- b of every inner v); the same draw keep(v <- u) decides both directions of use
+__global__ void __launch_bounds__(1024) k_tinduce_flags(const int32_t* __restrict__ tcol,
+                                                        const int32_t* __restrict__ terow, int64_t nnz, int64_t n_in,
+                                                        const int32_t* __restrict__ vgid,
+                                                        const int32_t* __restrict__ bgid, int dropedge, ArcKey ak,
+                                                        uint32_t* __restrict__ bits, int32_t* __restrict__ blk) {
+    const int64_t e = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    int keep = 0;
+    if (e < nnz) {
+        const int32_t r = terow[e], v = tcol[e];
+        if (r < n_in) keep = dropedge ? ak.keep(vgid[v], vgid[r]) : 1;
+        else keep = ak.keep(vgid[v], bgid[r - n_in]);
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    if ((threadIdx.x & 31) == 0) bits[e >> 5] = b;
+    const int cnt = __syncthreads_count(keep);
+    if (threadIdx.x == 0) blk[blockIdx.x] = cnt;
+}
+
+// output row of transposed row r: inner r -> r; boundary b -> halo row n_in + slot (or none if b is not in U_i)
+__device__ __forceinline__ int64_t trow_out(int64_t r, int64_t n_in, const int32_t* __restrict__ slot_of_b) {
+    if (r < n_in) return r;
+    const int32_t s = slot_of_b[r - n_in];
+    return s < 0 ? -1 : n_in + s;
+}
+
+__global__ void k_tinduce_rows(const int64_t* __restrict__ ptr, int64_t n_rows, int64_t n_in,
+                               const int32_t* __restrict__ slot_of_b, const uint32_t* __restrict__ bits,
+                               const int64_t* __restrict__ boff, int64_t* __restrict__ out_ptr,
+                               int32_t* __restrict__ nseg) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > n_rows) return;
+    const int64_t a = kept_before(ptr[r], bits, boff);
+    out_ptr[r] = a;
+    if (r == n_rows) return;
+    const int64_t cnt = kept_before(ptr[r + 1], bits, boff) - a;
+    nseg[r] = trow_out(r, n_in, slot_of_b) < 0 ? 0 : (cnt > kSeg ? (int32_t)((cnt + kSeg - 1) / kSeg) : 1);
+}
+
+__global__ void k_tinduce_segs(const int64_t* __restrict__ out_ptr, int64_t n_rows, int64_t n_in,
+                               const int32_t* __restrict__ slot_of_b, const int64_t* __restrict__ seg_off,
+                               Seg* __restrict__ segs, int64_t* __restrict__ split, int64_t* __restrict__ n_split) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rows) return;
+    const int64_t s0 = seg_off[r], ns = seg_off[r + 1] - s0;
+    if (ns == 0) return;
+    const int64_t b0 = out_ptr[r], b1 = out_ptr[r + 1];
+    if (ns > 1) push_split(split, n_split, s0);
+    const int32_t row = (int32_t)trow_out(r, n_in, slot_of_b);
+    for (int64_t k = 0; k < ns; ++k) {
+        Seg sg;
+        sg.row = row;
+        sg.nseg = (int32_t)ns;
+        sg.e0 = b0 + k * kSeg;
+        sg.e1 = min(b1, sg.e0 + kSeg);
+        sg.first = s0;
+        segs[s0 + k] = sg;
+    }
+}
+
+void launch_induce_bwd_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
+    const int64_t n_in = c.plan.n_in, n_rows = n_in + c.plan.n_bd;
+    const int m = c.cfg.world;
+    int64_t* tot = c.d_seg_pos + 2 * m + 1;   // [5] kept transposed arcs, [6] segments, [7] split rows
+    const int64_t nnz = c.tnnz;
+    const int64_t nb = (nnz + 1023) / 1024;
+    if (nb > 0) {
+        k_tinduce_flags<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_tcol, c.d_terow, nnz, n_in, c.d_vgid, c.d_cand_gid,
+                                                             c.sampler == BNS_SAMPLER_DROPEDGE,
+                                                             arc_key(T, seed, epoch), c.d_ebits, c.d_eblk);
+        k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_eblk, c.d_eboff, nb, tot + 5);
+        // every transposed column is an inner id (>= 0): the scatter's remap is the identity
+        k_induce_scatter<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_tcol, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff,
+                                                              n_in, c.d_ind_tcol);
+        c.kernels += 3;
+    } else {
+        BNS_CUDA(cudaMemsetAsync(c.d_eboff, 0, sizeof(int64_t), c.stream));
+        BNS_CUDA(cudaMemsetAsync(tot + 5, 0, sizeof(int64_t), c.stream));
+    }
+    k_tinduce_rows<<<(unsigned)((n_rows + 1 + 255) / 256), 256, 0, c.stream>>>(
+        c.d_tptr, n_rows, n_in, c.d_slot_of_b, c.d_ebits, c.d_eboff, c.d_ind_tptr, c.d_trow_nseg);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+    scan_i32(c, c.d_trow_nseg, c.d_trow_soff, n_rows, tot + 6);
+    BNS_CUDA(cudaMemsetAsync(tot + 7, 0, sizeof(int64_t), c.stream));
+    if (n_rows > 0) {
+        k_tinduce_segs<<<(unsigned)((n_rows + 255) / 256), 256, 0, c.stream>>>(
+            c.d_ind_tptr, n_rows, n_in, c.d_slot_of_b, c.d_trow_soff, c.d_eseg_bwd, c.d_esplit_bwd, tot + 7);
+        c.kernels += 1;
+        BNS_CHECK_LAUNCH();
+    }
 }
 
 }  // namespace bns

@@ -6,6 +6,8 @@
 // Backward (transpose of the same sampled operator):
 //   SAGE:  dX_u = c_u Σ_{v ∈ N(u) ∩ V_i} dZ'_v + [u inner] dXself_u     (dZ'_v = dZ_v / deg_G(v), GEMM epilogue)
 //   GCN:   dX_u = c_u rs_u (Σ_{v ∈ N(u) ∩ V_i} dZ'_v + [u inner] dZ'_u)   (dZ'_v = rs_v dZ_v)
+// Edge samplers (f3, R41): the CSR holds only the sampled arcs; BES carries 1/q as c_u of halo columns (like 1/p),
+// DropEdge 1/q on every arc as nscale, applied to the neighbour sum before the self terms.
 //
 // Work unit = one warp per segment (<= kSeg edges of one output row, edges in CSR order).  Each lane owns VPL
 // 16-byte vectors of the row (LPR lanes per row; with narrow rows the warp's 32/LPR lane groups take alternate
@@ -26,6 +28,10 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
     using V = Vec<T>;
     constexpr int VN = V::N;
     float rs;
+    if (a.nscale != 1.f) {   // f3 DropEdge: 1/q on every sampled arc (R41), before the self terms
+#pragma unroll
+        for (int k = 0; k < VN; ++k) acc[k] *= a.nscale;
+    }
     switch (a.mode) {
         case SAGE_FWD:
             rs = a.rowscale[row];

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--partition", default="ldg2")
+    ap.add_argument("--samplers", nargs="+", default=["bns"], choices=["bns", "bes", "dropedge"],
+                    help="f3 Table tab:bes analogue: edge samplers at matched dropped-edge counts (P:681)")
     args = ap.parse_args()
     import torch
     from paper_2203_10983_b200 import bns
@@ -41,6 +43,10 @@ def main():
     prec = bns.BNS_BF16 if args.prec == "bf16" else bns.BNS_FP32
     s = 2 if prec == bns.BNS_BF16 else 4
     dp = [((d + 7) // 8) * 8 for d in sh.dims]
+    src = np.repeat(np.arange(sh.N, dtype=np.int32), np.diff(indptr))
+    cross_frac = float(np.count_nonzero(part[src] != part[indices])) / max(1, len(indices))
+    del src
+    SAMP = {"bns": bns.BNS_SAMPLER_BNS, "bes": bns.BNS_SAMPLER_BES, "dropedge": bns.BNS_SAMPLER_DROPEDGE}
     for r in ranks:
         inner = np.nonzero(part == r)[0].astype(np.int32)
         ctx = bns.Context(rank=r, world=args.m, dims=sh.dims, layer=sh.layer, precision=prec, indptr=indptr,
@@ -50,9 +56,18 @@ def main():
         W = [torch.tensor(w, device="cuda") for w in I.weights(sh.dims, sh.layer)]
         G = [torch.zeros_like(w) for w in W]
         stream = torch.cuda.ExternalStream(ctx.stream())
-        for p in args.p:
+        for p, sname in [(p, sn) for p in args.p for sn in args.samplers]:
+            smp = SAMP[sname]
+            q = p if smp != bns.BNS_SAMPLER_DROPEDGE else 1.0 - (1.0 - p) * cross_frac
+
+            def draw(e):
+                if smp == bns.BNS_SAMPLER_BNS:
+                    ctx.sample_boundary(p, I.BNS_SEED, e)
+                else:
+                    ctx.sample_edges(smp, q, I.BNS_SEED, e)
+
             for e in range(args.warmup):
-                ctx.sample_boundary(p, I.BNS_SEED, e)
+                draw(e)
                 ctx.epoch(W, 0.0, G)
             torch.cuda.synchronize()
             t0 = ctx.times()
@@ -62,7 +77,7 @@ def main():
             for k in range(args.steps):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                ctx.sample_boundary(p, I.BNS_SEED, 100 + k)
+                draw(100 + k)
                 ctx.epoch(W, 0.0, G)
                 b.record(stream)
                 b.synchronize()
@@ -76,7 +91,7 @@ def main():
             bwd = sum((cnt["n_halo"] + cnt["n_sent"]) * dp[l] * s for l in range(1, sh.L)) / 2
             wbytes = sum(w.numel() * 4 for w in W)
             comm_ms = (fwd + bwd) / 770e9 * 1e3 + 2 * wbytes / 725e9 * 1e3
-            rec = {"config": sh.name, "m": args.m, "rank": r, "p": p, "prec": args.prec,
+            rec = {"config": sh.name, "m": args.m, "rank": r, "p": p, "sampler": sname, "q": q, "prec": args.prec,
                    "device_ms_per_epoch": float(np.median(ms)), "wall_ms_per_epoch": wall,
                    "est_nvlink_ms": comm_ms, "kernels_per_epoch": (ctx.kernel_count() - k0) / args.steps,
                    "n_in": cnt["n_in"], "n_bd": cnt["n_bd"], "n_halo": cnt["n_halo"], "n_sent": cnt["n_sent"],
