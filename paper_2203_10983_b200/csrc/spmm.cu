@@ -276,6 +276,9 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
         static const int mode = [] { const char* e = std::getenv("BNS_SPMM_TILE"); return e ? std::atoi(e) : 0; }();
         if (mode == 0) {
             tile = std::min<int64_t>(a0.d, 512 / ts);                      // 512-byte tiles
+        } else if (mode == 2 || mode == 3) {                               // balanced tiles of <= / >= 512 bytes
+            const int64_t nt = mode == 2 ? (a0.d * ts + 511) / 512 : std::max<int64_t>(1, a0.d * ts / 512);
+            tile = ((a0.d + nt - 1) / nt + 7) / 8 * 8;
         } else {
             const int64_t nt = (rows * a0.d * ts + kL2Budget - 1) / kL2Budget;   // balanced tiles
             tile = ((a0.d + nt - 1) / nt + 7) / 8 * 8;
