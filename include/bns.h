@@ -69,6 +69,11 @@ typedef enum {
                                              recomputed S_{i,j} (R27); mismatch -> BNS_ERR_RUNTIME */
 #define BNS_TIMING                  0x4u  /* record CUDA events per phase; read with BNS_Q_TIMES */
 #define BNS_RETAIN_GRADS            0x8u  /* keep a copy of dL/dH^(l) per layer for BNS_Q_DH (parity tests) */
+/* GraphSAGE layers whose (8-padded) output is narrower than their input are evaluated transform-first by default
+ * (R42): [Y | S] = H [W_top | W_bot] on every stacked row, then z'_v = (1/deg_G(v)) Σ_u c_u Y_u + S_v -- the same
+ * layer by linearity, with the neighbour gather at the narrow width (Reddit: 608 -> 256, 256 -> 41).  Z^(l) is then
+ * not materialised (BNS_Q_Z fails with BNS_ERR_STATE on those layers).  This flag keeps aggregate-first everywhere. */
+#define BNS_NO_TRANSFORM_FIRST      0x10u
 
 typedef struct bns_ctx bns_ctx;
 typedef struct bns_group bns_group;
@@ -87,7 +92,8 @@ typedef struct {
     int32_t precision;        /* bns_precision */
     double max_p;             /* halo capacity: <= 0 or >= 1 -> sized for p = 1 (|B_i| rows); else
                                  ceil(max_p*|B_i| + 8 sqrt(max_p*|B_i|) + 64) rows (R34) */
-    uint32_t flags;           /* BNS_PLAN_ONLY | BNS_DEBUG_EXCHANGE_INDICES | BNS_TIMING | BNS_RETAIN_GRADS */
+    uint32_t flags;           /* BNS_PLAN_ONLY | BNS_DEBUG_EXCHANGE_INDICES | BNS_TIMING | BNS_RETAIN_GRADS |
+                                 BNS_NO_TRANSFORM_FIRST */
 } bns_config;
 
 /* ncclGetUniqueId into out[128] (rank 0 calls it and broadcasts the bytes, e.g. over a torch process group). */
@@ -178,8 +184,9 @@ typedef enum {
                                 boundary index b -> -(b+1) (plan, available in BNS_PLAN_ONLY) */
     BNS_Q_MEMORY = 18,       /* int64[2]: device bytes allocated by the context, peak device bytes */
     BNS_Q_KERNEL_COUNT = 19, /* int64[1]: kernels launched by this context since setup */
-    BNS_Q_INDUCED_T = 20     /* edge samplers: int64[n_in+n_bd+1] row pointers then int32[nnz] local inner columns
+    BNS_Q_INDUCED_T = 20,    /* edge samplers: int64[n_in+n_bd+1] row pointers then int32[nnz] local inner columns
                                 of the sampled TRANSPOSED aggregation (rows: inner u, then boundary index b) */
+    BNS_Q_TF_LAYERS = 21     /* int32[1]: bit l-1 set <=> layer l runs transform-first (R42) */
 } bns_query_what;
 
 enum { BNS_PH_SAMPLE = 0, BNS_PH_INDUCE, BNS_PH_PACK, BNS_PH_EXCHANGE, BNS_PH_SPMM_FWD, BNS_PH_GEMM_FWD,

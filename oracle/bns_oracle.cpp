@@ -137,6 +137,7 @@ struct Oracle {
     uint64_t epoch_id = 0;                  // epoch of the last draw (keys the dropout masks)
     // f3: edge samplers BES / DropEdge (Table tab:bes)
     int sampler = 0;                        // 0 BNS (node), 1 BES, 2 DropEdge
+    uint32_t tf_mask = 0;                   // R42: layers (bit l-1) whose bf16 emulation follows the transform-first order
     double q = 1.0;                         // arc keep probability of the edge samplers
     uint64_t sample_seed = 0;
 };
@@ -401,7 +402,40 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
             std::vector<double>& pre = PREs[l][i];
             pre.assign(n_in * dout, 0.0);
             const std::vector<double>& Wl = Wq[l - 1];
-            for (size_t r = 0; r < n_in; ++r) {
+            const bool tf = o.bf16 && o.kind == KIND_SAGE && ((o.tf_mask >> (l - 1)) & 1u);
+            if (tf) {
+                // R42 (bf16 emulation only): the same layer evaluated as [Y | S] = X [W_top | W_bot] (stored), then
+                // pre_v = (1/deg_G(v)) Σ_u c_u Y_u + S_v -- equal to W^T [z ; x] by linearity, rounded where the
+                // transform-first kernel stores
+                std::vector<double> Y((n_in + n_h) * dout, 0.0);
+                for (size_t r = 0; r < n_in + n_h; ++r)
+                    for (int c = 0; c < dout; ++c) {
+                        double y = 0.0;
+                        for (int k = 0; k < din; ++k) y += X[r * din + k] * Wl[(size_t)k * dout + c];
+                        Y[r * dout + c] = st(y);
+                    }
+                for (size_t r = 0; r < n_in; ++r) {
+                    int32_t v = P.V[r];
+                    int64_t dv = deg(o, v);
+                    double* out = &pre[r * dout];
+                    if (dv > 0) {
+                        for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
+                            int32_t u = o.indices[e];
+                            int64_t ru = idx[i].row[u];
+                            double c;
+                            if (!arc_in(o, v, u, ru, (int64_t)n_in, &c)) continue;
+                            for (int k = 0; k < dout; ++k) out[k] += c * Y[(size_t)ru * dout + k];
+                        }
+                        for (int k = 0; k < dout; ++k) out[k] /= (double)dv;
+                    }
+                    for (int c = 0; c < dout; ++c) {
+                        double sv = 0.0;
+                        for (int k = 0; k < din; ++k) sv += X[r * din + k] * Wl[(size_t)(din + k) * dout + c];
+                        out[c] += st(sv);
+                    }
+                }
+            }
+            for (size_t r = 0; r < n_in && !tf; ++r) {
                 double* out = &pre[r * dout];
                 for (int k = 0; k < din; ++k) {
                     double zk = Zl[r * din + k];
@@ -481,6 +515,53 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
             const int wrows = (o.kind == KIND_SAGE) ? 2 * din : din;
             std::vector<double>& g = gW[i][l - 1];
             g.assign((size_t)wrows * dout, 0.0);
+            const bool tf = o.bf16 && o.kind == KIND_SAGE && ((o.tf_mask >> (l - 1)) & 1u);
+            if (tf) {
+                // R42 emulation: dY_u = c_u Σ_{v: u in N(v)} dPre_v / deg_G(v) on every stacked row (stored);
+                // dW_top = X^T dY, dW_bot = X_inner^T dPre; dX = dY W_top^T + [inner] dPre W_bot^T (stored)
+                std::vector<double> dY((n_in + n_h) * dout, 0.0);
+                for (size_t r = 0; r < n_in; ++r) {
+                    int32_t v = P.V[r];
+                    int64_t dv = deg(o, v);
+                    if (dv == 0) continue;
+                    for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
+                        int32_t u = o.indices[e];
+                        int64_t ru = idx[i].row[u];
+                        double c;
+                        if (!arc_in(o, v, u, ru, (int64_t)n_in, &c)) continue;
+                        for (int k = 0; k < dout; ++k) dY[(size_t)ru * dout + k] += c * dpre[r * dout + k] / (double)dv;
+                    }
+                }
+                for (double& x : dY) x = st(x);
+                for (size_t r = 0; r < n_in + n_h; ++r)
+                    for (int c = 0; c < dout; ++c) {
+                        const double d = dY[r * dout + c];
+                        for (int k = 0; k < din; ++k) g[(size_t)k * dout + c] += Xs[l][i][r * din + k] * d;
+                    }
+                for (size_t r = 0; r < n_in; ++r)
+                    for (int c = 0; c < dout; ++c) {
+                        const double d = dpre[r * dout + c];
+                        for (int k = 0; k < din; ++k) g[(size_t)(din + k) * dout + c] += Xs[l][i][r * din + k] * d;
+                    }
+                if (l == 1) continue;
+                std::vector<double>& dX = dXs[i];
+                dX.assign((n_in + n_h) * din, 0.0);
+                for (size_t r = 0; r < n_in + n_h; ++r)
+                    for (int k = 0; k < din; ++k) {
+                        double x = 0.0;
+                        for (int c = 0; c < dout; ++c) {
+                            x += dY[r * dout + c] * Wl[(size_t)k * dout + c];
+                            if (r < n_in) x += dpre[r * dout + c] * Wl[(size_t)(din + k) * dout + c];
+                        }
+                        x = st(x);
+                        if (o.drop > 0.0) {
+                            const int32_t u = (r < n_in) ? P.V[r] : P.U[r - n_in];
+                            x = st(x * drop_factor(o, u, k, l));
+                        }
+                        dX[r * din + k] = x;
+                    }
+                continue;
+            }
             for (size_t r = 0; r < n_in; ++r)
                 for (int c = 0; c < dout; ++c) {
                     double d = dpre[r * dout + c];
@@ -699,6 +780,10 @@ int32_t orc_sample_edges(void* h, int32_t sampler, double q, uint64_t seed, uint
 
 // R40 arc draw (v <- u) under the last orc_sample_edges' q / seed / epoch
 int32_t orc_arc_keep(void* h, int32_t v, int32_t u) { return arc_keep(*(Oracle*)h, v, u) ? 1 : 0; }
+
+// R42: layers (bit l-1) whose bf16-storage emulation follows the transform-first evaluation order (no effect in
+// double mode, where both orders are the same arithmetic)
+void orc_set_transform_first(void* h, uint32_t mask) { ((Oracle*)h)->tf_mask = mask; }
 
 // Explicit draw (for the hand-computed goldens): keep flags for B_rank in B order.
 int32_t orc_set_keep(void* h, double p, int32_t rank, const int32_t* flags) {

@@ -57,6 +57,7 @@ def lib():
         L.orc_sample_edges.argtypes = [vp, i32, f64, u64, u64]
         L.orc_arc_keep.restype = i32
         L.orc_arc_keep.argtypes = [vp, i32, i32]
+        L.orc_set_transform_first.argtypes = [vp, u32]
         L.orc_rows_sent.restype = i64
         L.orc_rows_sent.argtypes = [vp, i32]
         _LIB = L
@@ -110,6 +111,10 @@ class Oracle:
     def set_bf16(self, on=True):
         """R19 bf16-storage emulation: round the stored tensors (Z, H, GEMM operands, dPre, dZ', dX) to bf16."""
         lib().orc_set_bf16(self.h, 1 if on else 0)
+
+    def set_transform_first(self, mask):
+        """R42: bf16 emulation of the transform-first order on layers in mask (bit l-1); no effect in double."""
+        lib().orc_set_transform_first(self.h, int(mask))
 
     def set_training(self, optimizer=0, beta1=0.9, beta2=0.999, eps=1e-8, dropout=0.0, dropout_seed=0):
         """f2: optimizer 0 = SGD (Alg.1 l.14), 1 = Adam; dropout rate on every layer input (R38)."""

@@ -20,10 +20,10 @@ BNS_OK, BNS_ERR_INVALID, BNS_ERR_RUNTIME, BNS_ERR_STATE, BNS_ERR_OOM, BNS_ERR_NO
 BNS_LAYER_SAGE_MEAN, BNS_LAYER_GCN = 0, 1
 BNS_FP32, BNS_BF16 = 0, 1
 BNS_TRANSPORT_NONE, BNS_TRANSPORT_NCCL, BNS_TRANSPORT_LOCAL, BNS_TRANSPORT_NULL_EMULATE = 0, 1, 2, 3
-BNS_PLAN_ONLY, BNS_DEBUG_EXCHANGE_INDICES, BNS_TIMING, BNS_RETAIN_GRADS = 0x1, 0x2, 0x4, 0x8
+BNS_PLAN_ONLY, BNS_DEBUG_EXCHANGE_INDICES, BNS_TIMING, BNS_RETAIN_GRADS, BNS_NO_TRANSFORM_FIRST = 0x1, 0x2, 0x4, 0x8, 0x10
 (BNS_Q_COUNTS, BNS_Q_INNER, BNS_Q_BOUNDARY, BNS_Q_BOUNDARY_OFF, BNS_Q_SENDCAND, BNS_Q_SENDCAND_OFF, BNS_Q_MASK,
  BNS_Q_HALO, BNS_Q_HALO_OFF, BNS_Q_SEND, BNS_Q_SEND_OFF, BNS_Q_H, BNS_Q_Z, BNS_Q_DH, BNS_Q_HALO_ROWS, BNS_Q_INDUCED,
- BNS_Q_TIMES, BNS_Q_STATIC_CSR, BNS_Q_MEMORY, BNS_Q_KERNEL_COUNT, BNS_Q_INDUCED_T) = range(21)
+ BNS_Q_TIMES, BNS_Q_STATIC_CSR, BNS_Q_MEMORY, BNS_Q_KERNEL_COUNT, BNS_Q_INDUCED_T, BNS_Q_TF_LAYERS) = range(22)
 BNS_SAMPLER_BNS, BNS_SAMPLER_BES, BNS_SAMPLER_DROPEDGE = 0, 1, 2
 PHASES = ["sample", "induce", "pack", "exchange", "spmm_fwd", "gemm_fwd", "loss", "gemm_bwd", "spmm_bwd",
           "exchange_bwd", "scatter", "allreduce", "update", "epoch_total", "sample_total"]
@@ -255,6 +255,10 @@ class Context:
     def times(self):
         t = np.frombuffer(self.query(BNS_Q_TIMES), np.float64)
         return dict(zip(PHASES, t.tolist()))
+
+    def tf_layers(self):
+        """bit l-1 set <=> layer l runs transform-first (R42)"""
+        return int(np.frombuffer(self.query(BNS_Q_TF_LAYERS), np.int32)[0])
 
     def kernel_count(self):
         return int(np.frombuffer(self.query(BNS_Q_KERNEL_COUNT), np.int64)[0])

@@ -316,6 +316,20 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
         c.wkw[l] = (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * ((int64_t)(c.dp[l] + 63) / 64 * 64);
         if (c.use_tc) c.WT[l] = dalloc(c, c.wcols[l] * c.wkw[l] * 2);
     }
+    // R42: transform-first SAGE layers (narrower padded output than input), unless BNS_NO_TRANSFORM_FIRST
+    c.tf_mask = 0;
+    c.Wcat.assign(L, nullptr);
+    c.WTtf.assign(L, nullptr);
+    int64_t tfw = 0;
+    if (c.layer == BNS_LAYER_SAGE_MEAN && !(c.cfg.flags & BNS_NO_TRANSFORM_FIRST))
+        for (int l = 0; l < L; ++l)
+            if (c.dp[l + 1] < c.dp[l]) {
+                c.tf_mask |= 1u << l;
+                tfw = std::max<int64_t>(tfw, 2 * (int64_t)c.dp[l + 1]);
+                c.Wcat[l] = dalloc(c, (size_t)c.dp[l] * 2 * c.dp[l + 1] * ts);
+                if (c.use_tc) c.WTtf[l] = dalloc(c, (size_t)2 * c.dp[l + 1] * ((c.dp[l] + 63) / 64 * 64) * 2);
+            }
+    if (c.tf_mask) c.d_tfy = dalloc(c, (size_t)(P.n_in + c.halo_cap) * tfw * ts);
     c.gflat_n = c.goff[L];
     c.d_gflat = static_cast<float*>(dalloc(c, c.gflat_n * sizeof(float)));
     c.splitk_cap = 32 * wmax;
@@ -484,6 +498,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     {
         PhaseTimer t(c, BNS_PH_UPDATE);
         launch_wpack_all(c, W.data());
+        if (c.tf_mask) launch_wpack_tf(c);
     }
     const Seg* fsegs = c.fwd_mode == 0 ? c.d_seg_static_fwd : (c.fwd_mode == 1 ? c.d_seg_bwd : c.d_seg_fwd);
     const int32_t* fcol = c.fwd_mode == 0 ? c.d_static_col : (c.fwd_mode == 1 ? c.d_tcol : c.d_ind_col);
@@ -508,6 +523,45 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             PhaseTimer t(c, BNS_PH_UPDATE);
             launch_dropout(c, Hin, c.Xd[l - 1], n_in + c.n_halo, din, l);
             Hin = c.Xd[l - 1];
+        }
+        if ((c.tf_mask >> (l - 1)) & 1u) {
+            // R42 transform-first: [Y | S] = Hin [W_top | W_bot] on every stacked row, then
+            // pre_v = (1/deg_G(v)) Σ_u c_u Y_u + S_v with ReLU (hidden) or fp32 logits (last) in the SpMM epilogue
+            const bool last = (l == L);
+            const int64_t rows = n_in + c.n_halo;
+            {
+                PhaseTimer t(c, BNS_PH_GEMM_FWD);
+                if (c.use_tc)
+                    gemm_fwd_tc(c, rows, 2 * dout, Hin, din, din, nullptr, 0, din, c.WTtf[l - 1], (din + 63) / 64 * 64,
+                                c.d_tfy, 2 * dout, false, false);
+                else
+                    gemm_fwd(c, rows, 2 * dout, Hin, din, din, nullptr, 0, din, c.Wcat[l - 1], 2 * dout, c.d_tfy,
+                             2 * dout, false, false);
+            }
+            PhaseTimer t(c, BNS_PH_SPMM_FWD);
+            SpmmArgs a{};
+            a.mode = SAGE_FWD_TF;
+            a.segs = fsegs;
+            a.n_segs = c.n_seg_fwd;
+            a.col = fcol;
+            a.src = c.d_tfy;
+            a.ld_src = 2 * dout;
+            a.self = static_cast<char*>(c.d_tfy) + dout * ts;
+            a.ld_self = 2 * dout;
+            a.out = last ? (void*)c.d_logits : c.H[l];
+            a.ld_out = dout;
+            a.d = (int32_t)dout;
+            a.n_in = n_in;
+            a.inv_p = inv_p;
+            a.nscale = c.nscale;
+            a.rowscale = c.d_deg_in;
+            a.partial = c.d_partial;
+            a.split = c.fwd_mode == 0 ? c.d_split_sf : (c.fwd_mode == 1 ? c.d_split_bwd : c.d_split_fwd);
+            a.n_split = c.n_split_fwd;
+            a.relu = last ? 0 : 1;
+            a.out_f32 = last ? 1 : 0;
+            launch_spmm(c, a);
+            continue;
         }
         {
             PhaseTimer t(c, BNS_PH_SPMM_FWD);
@@ -559,6 +613,52 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
                 BNS_CUDA(cudaMemcpyAsync(c.dH_keep[l], c.d_dx, n_in * dout * ts, cudaMemcpyDeviceToDevice, c.stream));
             launch_relu_mask(c, c.d_dx, c.H[l], dout, n_in, (int32_t)dout, c.d_dpre);
         }
+        if ((c.tf_mask >> (l - 1)) & 1u) {
+            // R42 transform-first backward: dY_u = c_u Σ_v dPre_v / deg_G(v) over every stacked row (SpMM^T at the
+            // narrow width), dW_top = Hin^T dY, dW_bot = Hin_inner^T dPre, dX = [dY | dPre] [W_top | W_bot]^T
+            const bool eb = c.sampler != BNS_SAMPLER_BNS;
+            const int64_t rows = n_in + c.n_halo;
+            {
+                PhaseTimer t(c, BNS_PH_SPMM_BWD);
+                SpmmArgs a{};
+                a.mode = SAGE_BWD;
+                a.segs = eb ? c.d_eseg_bwd : c.d_seg_bwd;
+                a.n_segs = c.n_seg_bwd;
+                a.col = eb ? c.d_ind_tcol : c.d_tcol;
+                a.src = c.d_dpre;
+                a.ld_src = dout;
+                a.out = c.d_tfy;
+                a.ld_out = 2 * dout;
+                a.self = nullptr;
+                a.d = (int32_t)dout;
+                a.n_in = n_in;
+                a.inv_p = inv_p;
+                a.nscale = c.nscale;
+                a.sc = 2;
+                a.cscale = c.d_deg_in;   // gathered row v scaled by 1/deg_G(v)
+                a.partial = c.d_partial;
+                a.split = eb ? c.d_esplit_bwd : c.d_split_bwd;
+                a.n_split = c.n_split_bwd;
+                launch_spmm(c, a);
+            }
+            {
+                PhaseTimer t(c, BNS_PH_GEMM_BWD);
+                float* g = c.d_gflat + c.goff[l - 1];
+                auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
+                auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
+                wgrad(c, rows, din, dout, Hin, din, c.d_tfy, 2 * dout, g, dout);
+                wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
+                if (l > 1) {
+                    BNS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(c.d_tfy) + dout * ts, 2 * dout * ts, c.d_dpre,
+                                               dout * ts, dout * ts, n_in, cudaMemcpyDeviceToDevice, c.stream));
+                    dxg(c, n_in, din, 2 * dout, c.d_tfy, 2 * dout, c.Wcat[l - 1], 2 * dout, c.d_dx, din, nullptr, 0);
+                    if (c.n_halo > 0)
+                        dxg(c, c.n_halo, din, dout, static_cast<char*>(c.d_tfy) + n_in * 2 * dout * ts, 2 * dout,
+                            c.Wcat[l - 1], 2 * dout, static_cast<char*>(c.d_dx) + n_in * din * ts, din, nullptr, 0);
+                }
+            }
+            if (l == 1) break;   // R29
+        } else {
         {
             PhaseTimer t(c, BNS_PH_GEMM_BWD);
             float* g = c.d_gflat + c.goff[l - 1];
@@ -597,6 +697,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             a.split = eb ? c.d_esplit_bwd : c.d_split_bwd;
             a.n_split = c.n_split_bwd;
             launch_spmm(c, a);
+        }
         }
         if (dropout) {   // R38: gradient w.r.t. the dropped-out input -> w.r.t. the layer input (all stacked rows)
             PhaseTimer t(c, BNS_PH_UPDATE);
@@ -889,6 +990,8 @@ bns_status bns_query(bns_ctx* h, int32_t what, int32_t layer, void* dst, int64_t
             case BNS_Q_Z: {
                 need_sample();
                 if (layer < 1 || layer > L) throw Error(BNS_ERR_INVALID, "layer out of range");
+                if ((c.tf_mask >> (layer - 1)) & 1u)
+                    throw Error(BNS_ERR_STATE, "layer runs transform-first (R42): Z is not materialised");
                 rows_f32(c.Z[layer], P.n_in, c.dp[layer - 1], c.dims[layer - 1], false);
                 break;
             }
@@ -937,6 +1040,11 @@ bns_status bns_query(bns_ctx* h, int32_t what, int32_t layer, void* dst, int64_t
                 break;
             }
             case BNS_Q_KERNEL_COUNT: put(&c.kernels, 8); break;
+            case BNS_Q_TF_LAYERS: {
+                const int32_t v = (int32_t)c.tf_mask;
+                put(&v, 4);
+                break;
+            }
             case BNS_Q_INDUCED_T: {
                 need_sample();
                 if (c.sampler == BNS_SAMPLER_BNS) throw Error(BNS_ERR_STATE, "BNS_Q_INDUCED_T needs bns_sample_edges");

@@ -156,6 +156,11 @@ struct Ctx {
     std::vector<void*> Wt;         // storage-type copy (bf16 in BNS_BF16; == Wpad in FP32)
     std::vector<int64_t> wrows, wcols;   // padded shape per layer
     std::vector<void*> WT;         // bf16 W^T [wcols][wkw] for the tcgen05 forward (K-major B operand)
+    // --- R42 transform-first SAGE layers (bit l-1 of tf_mask <=> layer l)
+    uint32_t tf_mask = 0;
+    void* d_tfy = nullptr;         // (n_in + halo_cap) x 2 dout: forward [Y | S], backward [dY | dPre]
+    std::vector<void*> Wcat;       // storage type [W_top | W_bot]: dpin x 2 dpout (SIMT forward B, dX B operand)
+    std::vector<void*> WTtf;       // bf16 [W_top | W_bot]^T: 2 dpout x K64 (tcgen05 forward B operand)
     std::vector<int64_t> wkw;      // K of W^T: each concat half padded to a multiple of 64
     bool use_tc = false;           // tcgen05 GEMMs (BNS_BF16)
     // --- f2: Adam + dropout

@@ -382,7 +382,7 @@ void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t
     a.BN = (int)std::min<int64_t>(256, cdiv(Nc, 16) * 16);
     a.nk = (int)cdiv(K, 64);
     a.nk0 = a.nk;
-    a.epi = EPI_BF16_ROWSCALE;
+    a.epi = rowscale ? EPI_BF16_ROWSCALE : EPI_BF16;
     a.out = C;
     a.ldc = ldc;
     a.rowscale = rowscale;

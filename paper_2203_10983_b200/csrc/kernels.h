@@ -20,14 +20,14 @@ int64_t build_static_segments(Ctx& c, const int64_t* d_ptr, int64_t rows, int64_
 void scan_i32(Ctx& c, const int32_t* in, int64_t* out, int64_t n, int64_t* d_total);
 
 // a6 / a10: segment SpMM (spmm.cu)
-enum SpmmMode { SAGE_FWD = 0, GCN_FWD = 1, SAGE_BWD = 2, GCN_BWD = 3 };
+enum SpmmMode { SAGE_FWD = 0, GCN_FWD = 1, SAGE_BWD = 2, GCN_BWD = 3, SAGE_FWD_TF = 4 };
 struct SpmmArgs {
     int mode;
     const Seg* segs; int64_t n_segs;
     const int32_t* col;
     const void* src; int64_t ld_src;      // gather source rows (elements)
     void* out; int64_t ld_out;
-    const void* self; int64_t ld_self;    // SAGE_BWD: dXself rows (inner)
+    const void* self; int64_t ld_self;    // SAGE_BWD: dXself rows (inner; null = none); SAGE_FWD_TF: S rows (inner)
     int32_t d;                            // padded feature width
     int64_t n_in;
     float inv_p;
@@ -38,6 +38,9 @@ struct SpmmArgs {
     const float* rs_bd;                   // GCN_BWD
     float* partial;
     const int64_t* split; int64_t n_split;  // first-segment index of every split (hub) row -> in-order fixup
+    int sc = -1;                          // per-edge column scale override (-1: by mode; 2: cscale[col])
+    int relu = 0;                         // SAGE_FWD_TF: ReLU in the epilogue
+    int out_f32 = 0;                      // SAGE_FWD_TF: fp32 output (logits) instead of the storage type
 };
 void launch_spmm(Ctx& c, const SpmmArgs& a);
 
@@ -70,6 +73,7 @@ void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, c
 void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t);
 void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre);
 void launch_wpack_all(Ctx& c, float* const* W);
+void launch_wpack_tf(Ctx& c);
 void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr);
 void launch_adam(Ctx& c, float* const* W, float* const* G, float lr);
 void launch_dropout(Ctx& c, const void* src, void* dst, int64_t rows, int64_t ld, int layer);

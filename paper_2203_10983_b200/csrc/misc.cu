@@ -287,6 +287,43 @@ void launch_wpack_all(Ctx& c, float* const* W) {
     BNS_CHECK_LAUNCH();
 }
 
+// R42: [W_top | W_bot] (dpin x 2 dpout, storage type) and its bf16 transpose (2 dpout x K64) for a transform-first
+// layer, from the padded fp32 weights Wp (2 dpin x dpout) packed just before on the same stream
+template <typename T>
+__global__ void k_wpack_tf(const float* __restrict__ Wp, int64_t dpin, int64_t dpout, int64_t K64, T* __restrict__ Wcat,
+                           __nv_bfloat16* __restrict__ WTtf) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n2 = 2 * dpout;
+    if (t < dpin * n2) {
+        const int64_t k = t / n2, c = t % n2;
+        const float v = c < dpout ? Wp[k * dpout + c] : Wp[(dpin + k) * dpout + (c - dpout)];
+        Wcat[t] = from_f<T>(v);
+    }
+    if (WTtf && t < n2 * K64) {
+        const int64_t n = t / K64, k = t % K64;
+        float v = 0.f;
+        if (k < dpin) v = n < dpout ? Wp[k * dpout + n] : Wp[(dpin + k) * dpout + (n - dpout)];
+        WTtf[t] = __float2bfloat16_rn(v);
+    }
+}
+
+void launch_wpack_tf(Ctx& c) {
+    for (int l = 0; l < c.L; ++l) {
+        if (!((c.tf_mask >> l) & 1u)) continue;
+        const int64_t dpin = c.dp[l], dpout = c.dp[l + 1], K64 = (dpin + 63) / 64 * 64;
+        const int64_t n = std::max(dpin * 2 * dpout, 2 * dpout * K64);
+        __nv_bfloat16* wt = c.use_tc ? static_cast<__nv_bfloat16*>(c.WTtf[l]) : nullptr;
+        if (c.prec == BNS_BF16)
+            k_wpack_tf<__nv_bfloat16><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
+                c.Wpad[l], dpin, dpout, K64, static_cast<__nv_bfloat16*>(c.Wcat[l]), wt);
+        else
+            k_wpack_tf<float><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
+                c.Wpad[l], dpin, dpout, K64, static_cast<float*>(c.Wcat[l]), wt);
+        c.kernels += 1;
+        BNS_CHECK_LAUNCH();
+    }
+}
+
 // a14 W <- W - lr g for every layer (g copied to the caller); skipped when the all-reduced loss is not finite
 __global__ void k_sgd_all(const WDesc d, float lr, const double* __restrict__ scal, int32_t* __restrict__ nonfinite) {
     const int l = blockIdx.y;

@@ -47,8 +47,26 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
             for (int k = 0; k < VN; ++k) acc[k] = (acc[k] + cs * f[k]) * rs;
             break;
         }
+        case SAGE_FWD_TF: {   // R42: pre_v = (1/deg_G(v)) Σ_u c_u Y_u + S_v, ReLU on hidden layers
+            float f[VN];
+            V::to_float(*reinterpret_cast<const typename V::raw*>(static_cast<const T*>(a.self) + row * a.ld_self + vi * VN), f);
+            rs = a.rowscale[row];
+#pragma unroll
+            for (int k = 0; k < VN; ++k) {
+                acc[k] = acc[k] * rs + f[k];
+                if (a.relu) acc[k] = fmaxf(acc[k], 0.f);
+            }
+            if (a.out_f32) {
+                float* o = static_cast<float*>(a.out) + row * a.ld_out + vi * VN;
+#pragma unroll
+                for (int k = 0; k < VN; k += 4) *reinterpret_cast<float4*>(o + k) = make_float4(acc[k], acc[k + 1], acc[k + 2], acc[k + 3]);
+                return;
+            }
+            break;
+        }
         case SAGE_BWD: {
             if (row < a.n_in) {
+                if (!a.self) break;   // R42 backward: dY has no self term
                 float f[VN];
                 V::to_float(*reinterpret_cast<const typename V::raw*>(static_cast<const T*>(a.self) + row * a.ld_self + vi * VN), f);
 #pragma unroll
@@ -225,8 +243,9 @@ template <typename T, int LPR, int VPL>
 static void go(Ctx& c, const SpmmArgs& a, unsigned grid) {
     // per-edge column scale needed?  SAGE forward only when halo columns carry 1/p != 1
     int sc = 0;
-    if (a.mode == GCN_FWD) sc = 2;
-    else if (a.mode == SAGE_FWD && a.inv_p != 1.f) sc = 1;
+    if (a.sc >= 0) sc = a.sc;
+    else if (a.mode == GCN_FWD) sc = 2;
+    else if ((a.mode == SAGE_FWD || a.mode == SAGE_FWD_TF) && a.inv_p != 1.f) sc = 1;
     if (sc == 0) k_spmm<T, LPR, VPL, 0><<<grid, 256, 0, c.stream>>>(a);
     else if (sc == 1) k_spmm<T, LPR, VPL, 1><<<grid, 256, 0, c.stream>>>(a);
     else k_spmm<T, LPR, VPL, 2><<<grid, 256, 0, c.stream>>>(a);
@@ -289,7 +308,7 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
         SpmmArgs a = a0;
         a.d = (int32_t)std::min<int64_t>(tile, a0.d - c0);
         a.src = static_cast<const char*>(a0.src) + c0 * ts;
-        a.out = static_cast<char*>(a0.out) + c0 * ts;
+        a.out = static_cast<char*>(a0.out) + c0 * (a0.out_f32 ? 4 : ts);
         if (a0.self) a.self = static_cast<const char*>(a0.self) + c0 * ts;
         if (c.prec == BNS_BF16) dispatch<__nv_bfloat16>(c, a, grid);
         else dispatch<float>(c, a, grid);

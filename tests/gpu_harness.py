@@ -57,6 +57,8 @@ class GpuRun:
 
         self.ctx = parallel(m, mk)
         self.inner = [self.ctx[r].i32(bns.BNS_Q_INNER) for r in range(m)]
+        self.tf = 0 if flags & bns.BNS_NO_TRANSFORM_FIRST else tf_rule(self.dims, layer)
+        assert all(c.tf_layers() == self.tf for c in self.ctx), "transform-first layers differ from R42's rule"
 
     def close(self):
         for c in self.ctx:
@@ -97,6 +99,12 @@ class GpuRun:
             rows = self.ctx[r].rows(what, layer, d)
             g[self.inner[r]] = rows
         return g
+
+
+def tf_rule(dims, layer):
+    """R42: a GraphSAGE layer runs transform-first iff its 8-padded output is narrower than its input."""
+    pad = [(d + 7) // 8 * 8 for d in dims]
+    return sum(1 << l for l in range(len(dims) - 1) if layer == bns.BNS_LAYER_SAGE_MEAN and pad[l + 1] < pad[l])
 
 
 def oracle_for(indptr, indices, part, m, dims, layer, X, y):

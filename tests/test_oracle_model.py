@@ -324,3 +324,30 @@ def test_dropout_zero_is_identity_and_unbiased():
         acc.append(o.tensor(O.T_Z, 1))
     a = np.array(acc)
     assert np.all(np.abs(a.mean(0) - z) <= 4.5 * a.std(0) / np.sqrt(len(acc)) + 1e-12)
+
+
+# ---------------- R42: transform-first evaluation order (bf16 emulation only) ----------------
+@pytest.mark.parametrize("drop", [0.0, 0.3])
+def test_transform_first_is_noop_in_double_and_close_in_bf16(drop):
+    """In double the transform-first order is the same arithmetic (mask must not change a bit); in bf16 it only
+    moves the rounding points, so loss / grads stay within bf16 rounding of the double result, and they do move."""
+    dims = [9, 6, 5, 3]
+    ip, ix, part, X, y, Ws = random_case(73, N=60, m=3, dims=tuple(dims))
+    res = {}
+    for bf in (False, True):
+        for tf in (0, 0b111):
+            o = O.Oracle(ip, ix, part, 3, dims, 0, X, y)
+            o.set_bf16(bf)
+            o.set_transform_first(tf)
+            o.set_training(0, dropout=drop, dropout_seed=9)
+            o.sample(0.5, 3, 3)
+            loss, acc, G = o.epoch([w.copy() for w in Ws], 0.0)
+            res[(bf, tf)] = (loss, G, [o.tensor(O.T_H, l) for l in range(1, 4)],
+                             [o.tensor(O.T_DH, l) for l in range(1, 3)])
+    a, b = res[(False, 0)], res[(False, 0b111)]
+    assert a[0] == b[0] and all(np.array_equal(x, z) for x, z in zip(a[1] + a[2] + a[3], b[1] + b[2] + b[3]))
+    d, t = res[(False, 0)], res[(True, 0b111)]
+    assert abs(d[0] - t[0]) < 2e-2 * abs(d[0])
+    for x, z in zip(d[1] + d[2], t[1] + t[2]):
+        assert np.abs(x - z).max() <= 5e-2 * np.abs(x).max()
+    assert not all(np.array_equal(x, z) for x, z in zip(res[(True, 0)][1], t[1]))
