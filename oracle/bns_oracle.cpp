@@ -517,7 +517,8 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
             g.assign((size_t)wrows * dout, 0.0);
             const bool tf = o.bf16 && o.kind == KIND_SAGE && ((o.tf_mask >> (l - 1)) & 1u);
             if (tf) {
-                // R42 emulation: dY_u = c_u Σ_{v: u in N(v)} dPre_v / deg_G(v) on every stacked row (stored);
+                // R42 emulation: dY_u = c_u Σ_{v: u in N(v)} [dPre_v / deg_G(v)] on every stacked row, the bracket
+                // and dY stored;
                 // dW_top = X^T dY, dW_bot = X_inner^T dPre; dX = dY W_top^T + [inner] dPre W_bot^T (stored)
                 std::vector<double> dY((n_in + n_h) * dout, 0.0);
                 for (size_t r = 0; r < n_in; ++r) {
@@ -529,7 +530,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                         int64_t ru = idx[i].row[u];
                         double c;
                         if (!arc_in(o, v, u, ru, (int64_t)n_in, &c)) continue;
-                        for (int k = 0; k < dout; ++k) dY[(size_t)ru * dout + k] += c * dpre[r * dout + k] / (double)dv;
+                        for (int k = 0; k < dout; ++k) dY[(size_t)ru * dout + k] += c * st(dpre[r * dout + k] / (double)dv);
                     }
                 }
                 for (double& x : dY) x = st(x);

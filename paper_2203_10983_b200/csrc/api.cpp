@@ -601,7 +601,9 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     // ------------------------------ loss (l.11) ------------------------------
     {
         PhaseTimer t(c, BNS_PH_LOSS);
-        launch_xent(c, c.d_logits, c.dp[L], c.dims[L], c.d_dlogits, c.d_dpre);
+        const bool tfL = (c.tf_mask >> (L - 1)) & 1u;
+        launch_xent(c, c.d_logits, c.dp[L], c.dims[L], c.d_dlogits, c.d_dpre, tfL ? c.d_deg_in : nullptr,
+                    tfL ? c.d_dxcat : nullptr);
     }
     // ------------------------------ backward (l.12) ------------------------------
     for (int l = L; l >= 1; --l) {
@@ -611,7 +613,9 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             PhaseTimer t(c, BNS_PH_GEMM_BWD);
             if (c.retain)
                 BNS_CUDA(cudaMemcpyAsync(c.dH_keep[l], c.d_dx, n_in * dout * ts, cudaMemcpyDeviceToDevice, c.stream));
-            launch_relu_mask(c, c.d_dx, c.H[l], dout, n_in, (int32_t)dout, c.d_dpre);
+            const bool tfl = (c.tf_mask >> (l - 1)) & 1u;   // R42: + dPre / deg_G into d_dxcat (unused there)
+            launch_relu_mask(c, c.d_dx, c.H[l], dout, n_in, (int32_t)dout, c.d_dpre, tfl ? c.d_deg_in : nullptr,
+                             tfl ? c.d_dxcat : nullptr);
         }
         if ((c.tf_mask >> (l - 1)) & 1u) {
             // R42 transform-first backward: dY_u = c_u Σ_v dPre_v / deg_G(v) over every stacked row (SpMM^T at the
@@ -625,7 +629,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
                 a.segs = eb ? c.d_eseg_bwd : c.d_seg_bwd;
                 a.n_segs = c.n_seg_bwd;
                 a.col = eb ? c.d_ind_tcol : c.d_tcol;
-                a.src = c.d_dpre;
+                a.src = c.d_dxcat;       // dPre_v / deg_G(v), written by k_xent / k_relu_mask
                 a.ld_src = dout;
                 a.out = c.d_tfy;
                 a.ld_out = 2 * dout;
@@ -634,8 +638,6 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
                 a.n_in = n_in;
                 a.inv_p = inv_p;
                 a.nscale = c.nscale;
-                a.sc = 2;
-                a.cscale = c.d_deg_in;   // gathered row v scaled by 1/deg_G(v)
                 a.partial = c.d_partial;
                 a.split = eb ? c.d_esplit_bwd : c.d_split_bwd;
                 a.n_split = c.n_split_bwd;

@@ -70,8 +70,11 @@ void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t
 // misc (misc.cu)
 void launch_pack_rows(Ctx& c, const void* src, int64_t ld_src, const int32_t* idx, int64_t n, void* dst, int32_t d);
 void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, const void* src, int64_t n, int32_t d);
-void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t);
-void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre);
+// rs / dps (optional, R42): also write dps = dPre * rs[row] (the transform-first SpMM^T source)
+void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t,
+                 const float* rs = nullptr, void* dps = nullptr);
+void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre,
+                      const float* rs = nullptr, void* dps = nullptr);
 void launch_wpack_all(Ctx& c, float* const* W);
 void launch_wpack_tf(Ctx& c);
 void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr);

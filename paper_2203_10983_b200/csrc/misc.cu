@@ -85,7 +85,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, int64_t ld, int64_t n, int32_t C,
                                               const int32_t* __restrict__ labels, double inv_ntr,
                                               float* __restrict__ dlog, T* __restrict__ dpre,
-                                              double* __restrict__ part) {
+                                              double* __restrict__ part, const float* __restrict__ rs,
+                                              T* __restrict__ dps) {
     __shared__ double s_loss[8];
     __shared__ double s_cor[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -98,7 +99,11 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
         float* g = dlog + r * ld;
         T* gp = dpre + r * ld;
         if (y < 0) {
-            for (int c = lane; c < ld; c += 32) { g[c] = 0.f; gp[c] = from_f<T>(0.f); }
+            for (int c = lane; c < ld; c += 32) {
+                g[c] = 0.f;
+                gp[c] = from_f<T>(0.f);
+                if (dps) dps[r * ld + c] = from_f<T>(0.f);
+            }
             continue;
         }
         float mx = -INFINITY;
@@ -122,7 +127,9 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
             float v = 0.f;
             if (c < C) v = (float)(((double)expf(x[c] - lse) - (c == y ? 1.0 : 0.0)) * inv_ntr);
             g[c] = v;
-            gp[c] = from_f<T>(v);
+            const T q = from_f<T>(v);
+            gp[c] = q;
+            if (dps) dps[r * ld + c] = from_f<T>(to_f(q) * rs[r]);   // R42: dPre / deg_G(v), from the stored dPre
         }
         if (lane == 0) {
             loss += (double)lse - (double)x[y];
@@ -152,14 +159,16 @@ __global__ void k_xent_final(const double* __restrict__ part, int nb, double* __
     if (lane == 0) { scal[0] = a; scal[1] = b; }
 }
 
-void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t) {
+void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
+                 void* dps) {
     const double inv = c.n_train_global > 0 ? 1.0 / (double)c.n_train_global : 0.0;
     if (c.prec == BNS_BF16)
         k_xent<__nv_bfloat16><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, c.plan.n_in, C, c.d_labels, inv, dlogits,
-                                                                 (__nv_bfloat16*)dpre_t, c.d_lpart);
+                                                                 (__nv_bfloat16*)dpre_t, c.d_lpart, rs,
+                                                                 (__nv_bfloat16*)dps);
     else
         k_xent<float><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, c.plan.n_in, C, c.d_labels, inv, dlogits,
-                                                         (float*)dpre_t, c.d_lpart);
+                                                         (float*)dpre_t, c.d_lpart, rs, (float*)dps);
     k_xent_final<<<1, 32, 0, c.stream>>>(c.d_lpart, kXentBlocks, c.d_scal);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
@@ -168,7 +177,7 @@ void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlog
 // 16-byte vectors: dpre = dh where h > 0 else 0 (bit select on the storage words; R12 ReLU'(0) = 0)
 template <typename T>
 __global__ void k_relu_mask(const T* __restrict__ dh, const T* __restrict__ h, int64_t ld, int64_t n,
-                            T* __restrict__ dpre) {
+                            T* __restrict__ dpre, const float* __restrict__ rs, T* __restrict__ dps) {
     using R = typename Vec<T>::raw;
     constexpr int VN = Vec<T>::N;
     const int64_t nv = n / VN;
@@ -184,18 +193,26 @@ __global__ void k_relu_mask(const T* __restrict__ dh, const T* __restrict__ h, i
 #pragma unroll
         for (int k = 0; k < VN; ++k) a[k] = (b[k] > 0.f) ? a[k] : 0.f;
         ov[t] = Vec<T>::from_float(a);
+        if (dps) {   // R42: dPre / deg_G(v) for the transform-first SpMM^T (a is exact in T: masked copies of dh)
+            const float f = rs[t * VN / ld];
+#pragma unroll
+            for (int k = 0; k < VN; ++k) a[k] *= f;
+            reinterpret_cast<R*>(dps)[t] = Vec<T>::from_float(a);
+        }
     }
 }
 
-void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre) {
+void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre,
+                      const float* rs, void* dps) {
     const int64_t n = rows * ld;   // ld is a multiple of 8: whole 16-byte vectors
     if (n <= 0) return;
     unsigned grid = (unsigned)std::min<int64_t>((n / 4 + 255) / 256, 148 * 16);
     if (c.prec == BNS_BF16)
         k_relu_mask<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)dh, (const __nv_bfloat16*)h, ld,
-                                                               n, (__nv_bfloat16*)dpre);
+                                                               n, (__nv_bfloat16*)dpre, rs, (__nv_bfloat16*)dps);
     else
-        k_relu_mask<float><<<grid, 256, 0, c.stream>>>((const float*)dh, (const float*)h, ld, n, (float*)dpre);
+        k_relu_mask<float><<<grid, 256, 0, c.stream>>>((const float*)dh, (const float*)h, ld, n, (float*)dpre, rs,
+                                                       (float*)dps);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
