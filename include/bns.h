@@ -87,7 +87,7 @@ typedef struct {
     bns_group* group;         /* when transport == LOCAL, else NULL */
     void* stream;             /* cudaStream_t to enqueue on, or NULL: the library creates a non-blocking stream */
     int32_t num_layers;       /* L >= 1 */
-    const int32_t* dims;      /* L+1 logical dims: dims[0] = feature dim, dims[L] = number of classes C */
+    const int32_t* dims;      /* L+1 logical dims: dims[0] = feature dim, dims[L] = number of classes C (<= 256) */
     int32_t layer;            /* bns_layer */
     int32_t precision;        /* bns_precision */
     double max_p;             /* halo capacity: <= 0 or >= 1 -> sized for p = 1 (|B_i| rows); else

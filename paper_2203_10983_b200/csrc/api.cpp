@@ -73,6 +73,7 @@ void validate(const bns_config* cfg, int64_t N, const int64_t* indptr, const int
     if (cfg->num_layers < 1 || !cfg->dims) throw Error(BNS_ERR_INVALID, "num_layers < 1 or dims NULL");
     for (int l = 0; l <= cfg->num_layers; ++l)
         if (cfg->dims[l] <= 0) throw Error(BNS_ERR_INVALID, "dims must be positive");
+    if (cfg->dims[cfg->num_layers] > 256) throw Error(BNS_ERR_INVALID, "at most 256 classes (dims[L])");
     if (cfg->layer != BNS_LAYER_SAGE_MEAN && cfg->layer != BNS_LAYER_GCN) throw Error(BNS_ERR_INVALID, "bad layer");
     if (cfg->precision != BNS_FP32 && cfg->precision != BNS_BF16) throw Error(BNS_ERR_INVALID, "bad precision");
     if (cfg->world > 1 && cfg->transport != BNS_TRANSPORT_NCCL && cfg->transport != BNS_TRANSPORT_LOCAL &&
@@ -335,7 +336,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.splitk_cap = 32 * wmax;
     c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
     c.d_scal = static_cast<double*>(dalloc(c, 4 * sizeof(double)));
-    c.d_lpart = static_cast<double*>(dalloc(c, 2 * 512 * sizeof(double)));
+    c.d_lpart = static_cast<double*>(dalloc(c, 2 * 2048 * sizeof(double)));   // k_xent block partials
     c.d_nonfinite = static_cast<int32_t*>(dalloc(c, 16));
     c.d_hostw = static_cast<float*>(dalloc(c, 2 * wlog * sizeof(float)));
     c.hostw_n = wlog;

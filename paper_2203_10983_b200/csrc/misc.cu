@@ -79,9 +79,10 @@ void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, c
 // ---------------------------------------------------------------------------------------------
 // a8 loss: one warp per row; fixed row -> warp -> block assignment and in-order reductions (deterministic).
 // ---------------------------------------------------------------------------------------------
-constexpr int kXentBlocks = 296;
+constexpr int kXentBlocks = 1184;   // 148 SMs x 8: enough warps to hide the per-row latency
 
-template <typename T>
+// NPL = logits per lane held in registers (C <= 32 NPL); the row is read once
+template <typename T, int NPL>
 __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, int64_t ld, int64_t n, int32_t C,
                                               const int32_t* __restrict__ labels, double inv_ntr,
                                               float* __restrict__ dlog, T* __restrict__ dpre,
@@ -106,12 +107,17 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
             }
             continue;
         }
+        float xv[NPL];
+#pragma unroll
+        for (int k = 0; k < NPL; ++k) {
+            const int c = lane + 32 * k;
+            xv[k] = c < C ? x[c] : -INFINITY;
+        }
         float mx = -INFINITY;
         int arg = 0x7fffffff;
-        for (int c = lane; c < C; c += 32) {
-            float v = x[c];
-            if (v > mx) { mx = v; arg = c; }
-        }
+#pragma unroll
+        for (int k = 0; k < NPL; ++k)
+            if (xv[k] > mx) { mx = xv[k]; arg = lane + 32 * k; }   // ascending c per lane: first max kept (R22)
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             float om = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -119,17 +125,23 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
             if (om > mx || (om == mx && oa < arg)) { mx = om; arg = oa; }
         }
         float se = 0.f;
-        for (int c = lane; c < C; c += 32) se += expf(x[c] - mx);
+#pragma unroll
+        for (int k = 0; k < NPL; ++k)
+            if (lane + 32 * k < C) se += expf(xv[k] - mx);
 #pragma unroll
         for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
         const float lse = mx + logf(se);
-        for (int c = lane; c < ld; c += 32) {
+        const float rsr = dps ? rs[r] : 0.f;
+#pragma unroll
+        for (int k = 0; k < NPL; ++k) {
+            const int c = lane + 32 * k;
+            if (c >= ld) break;
             float v = 0.f;
-            if (c < C) v = (float)(((double)expf(x[c] - lse) - (c == y ? 1.0 : 0.0)) * inv_ntr);
+            if (c < C) v = (float)(((double)expf(xv[k] - lse) - (c == y ? 1.0 : 0.0)) * inv_ntr);
             g[c] = v;
             const T q = from_f<T>(v);
             gp[c] = q;
-            if (dps) dps[r * ld + c] = from_f<T>(to_f(q) * rs[r]);   // R42: dPre / deg_G(v), from the stored dPre
+            if (dps) dps[r * ld + c] = from_f<T>(to_f(q) * rsr);   // R42: dPre / deg_G(v), from the stored dPre
         }
         if (lane == 0) {
             loss += (double)lse - (double)x[y];
@@ -162,13 +174,20 @@ __global__ void k_xent_final(const double* __restrict__ part, int nb, double* __
 void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
                  void* dps) {
     const double inv = c.n_train_global > 0 ? 1.0 / (double)c.n_train_global : 0.0;
-    if (c.prec == BNS_BF16)
-        k_xent<__nv_bfloat16><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, c.plan.n_in, C, c.d_labels, inv, dlogits,
-                                                                 (__nv_bfloat16*)dpre_t, c.d_lpart, rs,
-                                                                 (__nv_bfloat16*)dps);
-    else
-        k_xent<float><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, c.plan.n_in, C, c.d_labels, inv, dlogits,
-                                                         (float*)dpre_t, c.d_lpart, rs, (float*)dps);
+    const int64_t n = c.plan.n_in;
+    const int npl = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : ld <= 256 ? 8 : 0;
+    if (npl == 0) throw Error(BNS_ERR_INVALID, "more than 256 classes are not supported by k_xent");
+#define BNS_XENT(T, NPL)                                                                                          \
+    k_xent<T, NPL><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, n, C, c.d_labels, inv, dlogits, (T*)dpre_t,   \
+                                                      c.d_lpart, rs, (T*)dps)
+    if (c.prec == BNS_BF16) {
+        if (npl == 1) BNS_XENT(__nv_bfloat16, 1); else if (npl == 2) BNS_XENT(__nv_bfloat16, 2);
+        else if (npl == 4) BNS_XENT(__nv_bfloat16, 4); else BNS_XENT(__nv_bfloat16, 8);
+    } else {
+        if (npl == 1) BNS_XENT(float, 1); else if (npl == 2) BNS_XENT(float, 2);
+        else if (npl == 4) BNS_XENT(float, 4); else BNS_XENT(float, 8);
+    }
+#undef BNS_XENT
     k_xent_final<<<1, 32, 0, c.stream>>>(c.d_lpart, kXentBlocks, c.d_scal);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();

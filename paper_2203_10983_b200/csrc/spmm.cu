@@ -229,11 +229,35 @@ __global__ void __launch_bounds__(256) k_spmm_fixup(const SpmmArgs a) {
             float acc[VN];
 #pragma unroll
             for (int k = 0; k < VN; ++k) acc[k] = 0.f;
-            for (int q = 0; q < s.nseg; ++q) {
-                const float* pp = a.partial + (sid + q) * (int64_t)a.d + vi * VN;
+            const float* pp = a.partial + sid * (int64_t)a.d + vi * VN;
+            int q = 0;
+            // 4 segments' partials in flight (16-byte loads), still added in segment order
+            for (; q + 4 <= s.nseg; q += 4) {
+                float4 t[4][VN / 4];
 #pragma unroll
-                for (int k = 0; k < VN; ++k) acc[k] += pp[k];
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int k = 0; k < VN / 4; ++k)
+                        t[j][k] = *reinterpret_cast<const float4*>(pp + (int64_t)(q + j) * a.d + 4 * k);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int k = 0; k < VN / 4; ++k) {
+                        acc[4 * k] += t[j][k].x;
+                        acc[4 * k + 1] += t[j][k].y;
+                        acc[4 * k + 2] += t[j][k].z;
+                        acc[4 * k + 3] += t[j][k].w;
+                    }
             }
+            for (; q < s.nseg; ++q)
+#pragma unroll
+                for (int k = 0; k < VN / 4; ++k) {
+                    const float4 t = *reinterpret_cast<const float4*>(pp + (int64_t)q * a.d + 4 * k);
+                    acc[4 * k] += t.x;
+                    acc[4 * k + 1] += t.y;
+                    acc[4 * k + 2] += t.z;
+                    acc[4 * k + 3] += t.w;
+                }
             epilogue_store<T>(a, s.row, vi, acc);
         }
     }
