@@ -158,9 +158,17 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 # algorithmic bytes / flops
 # ------------------------------------------------------------------------------------------------
-def spmm_bytes(dp, L, n_in, n_halo, kept, s):
-    fwd = sum(kept * (dp[l] * s + 4) + (n_in + 1) * 4 + n_in * dp[l] * s for l in range(L))
-    bwd = sum(kept * (dp[l] * s + 4) + (n_in + n_halo + 1) * 4 + (n_in + n_halo) * dp[l] * s for l in range(1, L))
+def spmm_bytes(dp, L, n_in, n_halo, kept, s, tf=0):
+    """Row-gather model per step.  Layer l (0-based) gathers at its input width dp[l], or at its
+    output width dp[l+1] when it runs transform-first (R42, bit l of tf) -- then it also reads S (n_in x width) in
+    the forward and has a backward gather even at l = 0 (dY for dW_top)."""
+    fwd = bwd = 0
+    for l in range(L):
+        t = (tf >> l) & 1
+        w = dp[l + 1] if t else dp[l]
+        fwd += kept * (w * s + 4) + (n_in + 1) * 4 + n_in * w * s * (2 if t else 1)
+        if l > 0 or t:
+            bwd += kept * (w * s + 4) + (n_in + n_halo + 1) * 4 + (n_in + n_halo) * w * s
     return fwd, bwd
 
 
@@ -402,7 +410,7 @@ def run_ours(args):
         peaks = measured_peaks()
         s = 2 if prec == bns.BNS_BF16 else 4
         dp = [((d + 7) // 8) * 8 for d in shape.dims]
-        fwd_b, bwd_b = spmm_bytes(dp, shape.L, cnt["n_in"], cnt["n_halo"], cnt["nnz_kept"], s)
+        fwd_b, bwd_b = spmm_bytes(dp, shape.L, cnt["n_in"], cnt["n_halo"], cnt["nnz_kept"], s, ctx.tf_layers())
         spmm_ms = ph["spmm_fwd"] + ph["spmm_bwd"]
         hbm_peak = peaks.get("hbm_gbs", 6650.0)
         achieved = (fwd_b + bwd_b) / (spmm_ms * 1e-3) / 1e9 if spmm_ms > 0 else None
@@ -421,6 +429,7 @@ def run_ours(args):
                                    f"{shape.L} layers hidden {shape.hidden}, d0={shape.d0}, C={shape.C}, p={args.p}, "
                                    f"m={world} partitions ({args.partition})",
                        "global_batch": "full graph", "parallelism": f"partition-parallel m={world}",
+                       "transform_first_layers": [l + 1 for l in range(shape.L) if (ctx.tf_layers() >> l) & 1],
                        "l2": "flushed between timed steps (2x L2 write, outside the events)",
                        "step": "%s + bns_epoch (%s update included%s)" % (
                            "bns_sample_boundary" if sampler == bns.BNS_SAMPLER_BNS else

@@ -76,7 +76,7 @@ def full(src, dst, regex=None):
     dram = [x.get("dram__bytes_read.sum", 0) * (1e6 if x.get("dram__bytes_read.sum.unit") == "Mbyte" else 1e9 if x.get("dram__bytes_read.sum.unit") == "Gbyte" else 1e3 if x.get("dram__bytes_read.sum.unit") == "Kbyte" else 1)
             + x.get("dram__bytes_write.sum", 0) * (1e6 if x.get("dram__bytes_write.sum.unit") == "Mbyte" else 1e9 if x.get("dram__bytes_write.sum.unit") == "Gbyte" else 1e3 if x.get("dram__bytes_write.sum.unit") == "Kbyte" else 1)
             for x in res]
-    summary = {"source": src, "launches": res,
+    summary = {"source": src, "launches": res, "dram_bytes_sum": sum(dram) if dram else None,
                "dram_bytes_per_launch": (sum(dram) / len(dram)) if dram else None}
     json.dump(summary, open(dst, "w"), indent=1)
     print(json.dumps(summary, indent=1)[:4000])
