@@ -264,6 +264,10 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.d_row_soff = static_cast<int64_t*>(dalloc(c, (rmax + 1) * sizeof(int64_t)));
     c.d_scan_tmp = static_cast<int64_t*>(dalloc(c, (std::max(rmax, c.n_cand) / 1024 + 16) * 3 * sizeof(int64_t)));
     c.d_cscale = static_cast<float*>(dalloc(c, (P.n_in + c.halo_cap + 1) * sizeof(float)));
+    if (m > 1 && m <= 32) {
+        c.d_scat_mask = static_cast<uint32_t*>(dalloc(c, (P.n_in + 1) * sizeof(uint32_t)));
+        c.d_scat_pos = static_cast<int32_t*>(dalloc(c, (size_t)(P.n_in + 1) * m * sizeof(int32_t)));
+    }
 
     // ---- activations
     c.H.assign(L, nullptr);
@@ -436,6 +440,7 @@ void sample_boundary(Ctx& c, int sampler, double p, uint64_t seed, uint64_t epoc
     if (c.n_halo > c.halo_cap)
         throw Error(BNS_ERR_OOM, "sampled halo (" + std::to_string(c.n_halo) + " rows) exceeds capacity " +
                                      std::to_string(c.halo_cap) + " (raise cfg.max_p)");
+    if (c.d_scat_mask) launch_scatter_prep(c, c.n_sent);
     if (c.debug_idx && m > 1) {
         // R27 check: exchange the gids of S_{i,j} and compare with U_i's owner segments
         std::vector<int32_t> sl(c.n_sent), ub(c.n_halo);
@@ -713,11 +718,15 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
                                c.send_off.data(), din * ts);
             }
             PhaseTimer t(c, BNS_PH_SCATTER);
-            for (int j = 0; j < m; ++j) {   // R25: local contribution first, then peers ascending
-                if (j == c.cfg.rank) continue;
-                const int64_t n = c.send_off[j + 1] - c.send_off[j];
-                launch_scatter_add(c, c.d_dx, din, S_local + c.send_off[j],
-                                   static_cast<char*>(c.d_gradbuf) + c.send_off[j] * din * ts, n, (int32_t)din);
+            if (c.d_scat_mask) {            // R25: local contribution first, then peers ascending, one launch
+                launch_scatter_rows(c, c.d_dx, din, c.d_gradbuf, (int32_t)din);
+            } else {
+                for (int j = 0; j < m; ++j) {
+                    if (j == c.cfg.rank) continue;
+                    const int64_t n = c.send_off[j + 1] - c.send_off[j];
+                    launch_scatter_add(c, c.d_dx, din, S_local + c.send_off[j],
+                                       static_cast<char*>(c.d_gradbuf) + c.send_off[j] * din * ts, n, (int32_t)din);
+                }
             }
         }
     }

@@ -138,6 +138,8 @@ struct Ctx {
     int64_t* d_split_fwd = nullptr;                                  // per-epoch induced forward segments
     int64_t n_split_fwd = 0, n_split_bwd = 0;                        // this epoch's list lengths
     float* d_cscale = nullptr;     // per-column scale (GCN forward)
+    uint32_t* d_scat_mask = nullptr; // a12 merged scatter: peers holding each owner row (bit j), world <= 32
+    int32_t* d_scat_pos = nullptr;   // ... and the row's position in the returned buffer, n_in x world
     // --- activations (storage type T: float or bf16)
     std::vector<void*> H;          // H[l], l = 0..L-1: (n_in + halo_cap) x dp[l]
     std::vector<void*> Z;          // Z[l], l = 1..L: n_in x dp[l-1]

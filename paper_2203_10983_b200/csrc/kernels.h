@@ -70,6 +70,9 @@ void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t
 // misc (misc.cu)
 void launch_pack_rows(Ctx& c, const void* src, int64_t ld_src, const int32_t* idx, int64_t n, void* dst, int32_t d);
 void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, const void* src, int64_t n, int32_t d);
+// a12 merged over peers (world <= 32): prep once per draw, then one launch per layer
+void launch_scatter_prep(Ctx& c, int64_t n_sent);
+void launch_scatter_rows(Ctx& c, void* dst, int64_t ld, const void* src, int32_t d);
 // rs / dps (optional, R42): also write dps = dPre * rs[row] (the transform-first SpMM^T source)
 void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t,
                  const float* rs = nullptr, void* dps = nullptr);

@@ -76,6 +76,80 @@ void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, c
     BNS_CHECK_LAUNCH();
 }
 
+// a12 with every peer in one launch.  k_scatter_prep (once per draw) marks, for each owner row r, the peers j holding
+// it (bit j of mask[r]) and the row's position in the returned buffer (pos[r m + j]); k_scatter_rows then adds the
+// peers' rows in ascending j, rounding to the storage type after every add -- the same values as one launch per
+// peer in ascending order (R25, R19).
+__global__ void k_scatter_prep(const int32_t* __restrict__ S_local, int64_t n_sent, const int64_t* __restrict__ seg_pos,
+                               int m, uint32_t* __restrict__ mask, int32_t* __restrict__ pos) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_sent) return;
+    const int64_t base = seg_pos[m];
+    int j = 0;
+    while (j < m - 1 && seg_pos[m + j + 1] - base <= k) ++j;
+    const int32_t r = S_local[k];
+    atomicOr(&mask[r], 1u << j);
+    pos[(int64_t)r * m + j] = (int32_t)k;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_scatter_rows(T* __restrict__ dst, int64_t ld, const T* __restrict__ src,
+                                                      int32_t d, const uint32_t* __restrict__ mask,
+                                                      const int32_t* __restrict__ pos, int m, int64_t n_rows) {
+    using V = Vec<T>;
+    using R = typename V::raw;
+    constexpr int VN = V::N;
+    const int nvec = d / VN;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nwarps) {
+        const uint32_t mk = mask[r];
+        if (!mk) continue;
+        R* o = reinterpret_cast<R*>(dst + r * ld);
+        for (int v = lane; v < nvec; v += 32) {
+            float a[VN], b[VN];
+            V::to_float(o[v], a);
+            uint32_t mm = mk;
+            while (mm) {
+                const int j = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const int64_t k = pos[r * m + j];
+                V::to_float(reinterpret_cast<const R*>(src + k * (int64_t)d)[v], b);
+#pragma unroll
+                for (int q = 0; q < VN; ++q) a[q] += b[q];
+                V::to_float(V::from_float(a), a);   // stored after every peer, as the per-peer sequence
+            }
+            o[v] = V::from_float(a);
+        }
+    }
+}
+
+void launch_scatter_prep(Ctx& c, int64_t n_sent) {
+    const int m = c.cfg.world;
+    BNS_CUDA(cudaMemsetAsync(c.d_scat_mask, 0, (c.plan.n_in + 1) * sizeof(uint32_t), c.stream));
+    if (n_sent <= 0) return;
+    k_scatter_prep<<<(unsigned)((n_sent + 255) / 256), 256, 0, c.stream>>>(c.d_cand_out + c.n_halo, n_sent,
+                                                                           c.d_seg_pos, m, c.d_scat_mask,
+                                                                           c.d_scat_pos);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+void launch_scatter_rows(Ctx& c, void* dst, int64_t ld, const void* src, int32_t d) {
+    const int64_t n = c.plan.n_in;
+    if (n <= 0 || c.n_sent <= 0) return;
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16);
+    if (c.prec == BNS_BF16)
+        k_scatter_rows<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((__nv_bfloat16*)dst, ld, (const __nv_bfloat16*)src,
+                                                                  d, c.d_scat_mask, c.d_scat_pos, c.cfg.world, n);
+    else
+        k_scatter_rows<float><<<grid, 256, 0, c.stream>>>((float*)dst, ld, (const float*)src, d, c.d_scat_mask,
+                                                          c.d_scat_pos, c.cfg.world, n);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
 // ---------------------------------------------------------------------------------------------
 // a8 loss: one warp per row; fixed row -> warp -> block assignment and in-order reductions (deterministic).
 // ---------------------------------------------------------------------------------------------

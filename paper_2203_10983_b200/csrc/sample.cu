@@ -206,7 +206,7 @@ void launch_sample(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
 
 // ---------------------------------------------------------------------------------------------
 // a3 induce, edge-parallel (balanced over nnz, so hub rows cost no more than their edges):
-//   K1 keep bit of every static edge (ballot words) + per-1024-edge counts, K2 scan of the counts,
+//   K1 keep bit of every static edge (one 32-edge word per thread) + per-1024-edge counts, K2 scan of the counts,
 //   K3 order-preserving scatter of the kept (remapped) columns, K4 row pointers from the bit prefix + segment
 //   counts per row, scan, K5 segment list.
 // ---------------------------------------------------------------------------------------------
@@ -214,42 +214,62 @@ __device__ __forceinline__ bool edge_kept(int32_t x, const int32_t* __restrict__
     return x >= 0 || slot_of_b[-x - 1] >= 0;
 }
 
-__global__ void __launch_bounds__(1024) k_induce_flags(const int32_t* __restrict__ col_enc, int64_t nnz,
-                                                       const int32_t* __restrict__ slot_of_b,
-                                                       uint32_t* __restrict__ bits, int32_t* __restrict__ blk) {
-    const int64_t e = (int64_t)blockIdx.x * 1024 + threadIdx.x;
-    const int keep = (e < nnz) ? (edge_kept(col_enc[e], slot_of_b) ? 1 : 0) : 0;
-    const unsigned b = __ballot_sync(0xffffffffu, keep);
-    if ((threadIdx.x & 31) == 0) bits[e >> 5] = b;
-    const int cnt = __syncthreads_count(keep);
-    if (threadIdx.x == 0) blk[blockIdx.x] = cnt;
+// Word-per-thread versions (same bits / per-1024-edge count layout): thread t owns edges [32t, 32t + 32) and builds
+// their keep word from eight 16-byte column loads; a warp covers one 1024-edge block, so the block counts and the
+// in-block prefix are warp shuffles (no shared memory, no block barrier).
+__global__ void __launch_bounds__(256) k_induce_flags_w(const int32_t* __restrict__ col_enc, int64_t nnz,
+                                                        const int32_t* __restrict__ slot_of_b,
+                                                        uint32_t* __restrict__ bits, int32_t* __restrict__ blk) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nw = (nnz + 31) >> 5;
+    uint32_t word = 0;
+    if (w < nw) {
+        const int64_t e0 = w << 5;
+        if (e0 + 32 <= nnz) {
+            const int4* p = reinterpret_cast<const int4*>(col_enc + e0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int4 v = __ldg(p + q);
+                word |= (uint32_t)edge_kept(v.x, slot_of_b) << (4 * q);
+                word |= (uint32_t)edge_kept(v.y, slot_of_b) << (4 * q + 1);
+                word |= (uint32_t)edge_kept(v.z, slot_of_b) << (4 * q + 2);
+                word |= (uint32_t)edge_kept(v.w, slot_of_b) << (4 * q + 3);
+            }
+        } else {
+            for (int j = 0; j < (int)(nnz - e0); ++j) word |= (uint32_t)edge_kept(col_enc[e0 + j], slot_of_b) << j;
+        }
+        bits[w] = word;
+    }
+    int cnt = __popc(word);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && (w >> 5) < ((nnz + 1023) >> 10)) blk[w >> 5] = cnt;
 }
 
-__global__ void __launch_bounds__(1024) k_induce_scatter(const int32_t* __restrict__ col_enc, int64_t nnz,
-                                                         const int32_t* __restrict__ slot_of_b,
-                                                         const uint32_t* __restrict__ bits,
-                                                         const int64_t* __restrict__ boff, int64_t n_in,
-                                                         int32_t* __restrict__ out_col) {
-    __shared__ int32_t wsum[32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t e = (int64_t)blockIdx.x * 1024 + threadIdx.x;
-    const uint32_t word = (e < nnz) ? bits[e >> 5] : 0u;
-    if (lane == 0) wsum[w] = __popc(word);
-    __syncthreads();
-    if (w == 0) {
-        int s = wsum[lane];
+__global__ void __launch_bounds__(256) k_induce_scatter_w(const int32_t* __restrict__ col, int64_t nnz,
+                                                          const int32_t* __restrict__ slot_of_b,
+                                                          const uint32_t* __restrict__ bits,
+                                                          const int64_t* __restrict__ boff, int64_t n_in,
+                                                          int32_t* __restrict__ out_col) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nw = (nnz + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t word = w < nw ? bits[w] : 0u;
+    const int c = __popc(word);
+    int x = c;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, s, o);
-            if (lane >= o) s += y;
-        }
-        wsum[lane] = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
     }
-    __syncthreads();
-    if (e < nnz && ((word >> lane) & 1u)) {
-        const int64_t pos = boff[blockIdx.x] + (w ? wsum[w - 1] : 0) + __popc(word & ((1u << lane) - 1u));
-        const int32_t x = col_enc[e];
-        out_col[pos] = x >= 0 ? x : (int32_t)n_in + slot_of_b[-x - 1];
+    if (word == 0) return;
+    int64_t pos = boff[w >> 5] + (x - c);
+    uint32_t m = word;
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const int32_t v = col[(w << 5) + j];
+        out_col[pos++] = v >= 0 ? v : (int32_t)n_in + slot_of_b[-v - 1];
     }
 }
 
@@ -308,13 +328,14 @@ void launch_induce(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     int64_t* tot = c.d_seg_pos + 2 * m + 1;   // [nnz_kept, n_seg_fwd, n_seg_bwd_halo]
     const int64_t nb = (nnz + 1023) / 1024;
     if (nb > 0) {
+        const unsigned wb = (unsigned)((((nnz + 31) >> 5) + 255) / 256);
         if (c.sampler == BNS_SAMPLER_BNS)
-            k_induce_flags<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eblk);
+            k_induce_flags_w<<<wb, 256, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eblk);
         else
             launch_induce_flags_edge(c, nb, T, seed, epoch);
         k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_eblk, c.d_eboff, nb, tot + 0);
-        k_induce_scatter<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff,
-                                                              n_in, c.d_ind_col);
+        k_induce_scatter_w<<<wb, 256, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff, n_in,
+                                                     c.d_ind_col);
         c.kernels += 3;
     } else {
         BNS_CUDA(cudaMemsetAsync(c.d_eboff, 0, sizeof(int64_t), c.stream));
@@ -561,8 +582,8 @@ void launch_induce_bwd_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) 
                                                              arc_key(T, seed, epoch), c.d_ebits, c.d_eblk);
         k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_eblk, c.d_eboff, nb, tot + 5);
         // every transposed column is an inner id (>= 0): the scatter's remap is the identity
-        k_induce_scatter<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_tcol, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff,
-                                                              n_in, c.d_ind_tcol);
+        k_induce_scatter_w<<<(unsigned)((((nnz + 31) >> 5) + 255) / 256), 256, 0, c.stream>>>(
+            c.d_tcol, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff, n_in, c.d_ind_tcol);
         c.kernels += 3;
     } else {
         BNS_CUDA(cudaMemsetAsync(c.d_eboff, 0, sizeof(int64_t), c.stream));
