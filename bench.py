@@ -307,7 +307,7 @@ def run_ours(args):
         nccl_id = obj[0]
     ctx = bns.Context(rank=rank, world=world, dims=shape.dims, layer=shape.layer, precision=prec, indptr=indptr,
                       indices=indices, part_of=part, features=X, labels=y, device=local, nccl_id=nccl_id,
-                      max_p=0.0, flags=bns.BNS_TIMING)
+                      max_p=0.0, flags=bns.BNS_TIMING | (bns.BNS_CACHE_INPUT_HALO if world > 1 else 0))
     if args.adam or args.dropout > 0:
         ctx.set_training(bns.BNS_OPT_ADAM if args.adam else bns.BNS_OPT_SGD, 0.9, 0.999, 1e-8, args.dropout, 0xD0)
     del X

@@ -74,6 +74,11 @@ typedef enum {
  * layer by linearity, with the neighbour gather at the narrow width (Reddit: 608 -> 256, 256 -> 41).  Z^(l) is then
  * not materialised (BNS_Q_Z fails with BNS_ERR_STATE on those layers).  This flag keeps aggregate-first everywhere. */
 #define BNS_NO_TRANSFORM_FIRST      0x10u
+/* the input features never change, so with this flag bns_setup exchanges every boundary node's
+ * X^(0) row once (collective, the p = 1 lists) into a per-rank cache of |B_i| rows, and each epoch's layer-1 halo is
+ * gathered locally from it (U_i ⊆ B_i) instead of being packed and exchanged: identical values, no layer-1 message
+ * (R43).  Costs |B_i| x dims[0] stored elements of HBM. */
+#define BNS_CACHE_INPUT_HALO        0x20u
 
 typedef struct bns_ctx bns_ctx;
 typedef struct bns_group bns_group;
@@ -93,7 +98,7 @@ typedef struct {
     double max_p;             /* halo capacity: <= 0 or >= 1 -> sized for p = 1 (|B_i| rows); else
                                  ceil(max_p*|B_i| + 8 sqrt(max_p*|B_i|) + 64) rows (R34) */
     uint32_t flags;           /* BNS_PLAN_ONLY | BNS_DEBUG_EXCHANGE_INDICES | BNS_TIMING | BNS_RETAIN_GRADS |
-                                 BNS_NO_TRANSFORM_FIRST */
+                                 BNS_NO_TRANSFORM_FIRST | BNS_CACHE_INPUT_HALO */
 } bns_config;
 
 /* ncclGetUniqueId into out[128] (rank 0 calls it and broadcasts the bytes, e.g. over a torch process group). */

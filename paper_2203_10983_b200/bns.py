@@ -21,6 +21,7 @@ BNS_LAYER_SAGE_MEAN, BNS_LAYER_GCN = 0, 1
 BNS_FP32, BNS_BF16 = 0, 1
 BNS_TRANSPORT_NONE, BNS_TRANSPORT_NCCL, BNS_TRANSPORT_LOCAL, BNS_TRANSPORT_NULL_EMULATE = 0, 1, 2, 3
 BNS_PLAN_ONLY, BNS_DEBUG_EXCHANGE_INDICES, BNS_TIMING, BNS_RETAIN_GRADS, BNS_NO_TRANSFORM_FIRST = 0x1, 0x2, 0x4, 0x8, 0x10
+BNS_CACHE_INPUT_HALO = 0x20
 (BNS_Q_COUNTS, BNS_Q_INNER, BNS_Q_BOUNDARY, BNS_Q_BOUNDARY_OFF, BNS_Q_SENDCAND, BNS_Q_SENDCAND_OFF, BNS_Q_MASK,
  BNS_Q_HALO, BNS_Q_HALO_OFF, BNS_Q_SEND, BNS_Q_SEND_OFF, BNS_Q_H, BNS_Q_Z, BNS_Q_DH, BNS_Q_HALO_ROWS, BNS_Q_INDUCED,
  BNS_Q_TIMES, BNS_Q_STATIC_CSR, BNS_Q_MEMORY, BNS_Q_KERNEL_COUNT, BNS_Q_INDUCED_T, BNS_Q_TF_LAYERS) = range(22)

@@ -385,6 +385,18 @@ void edge_init(Ctx& c) {
     c.edge_ready = true;
 }
 
+// f1 / R43: one p = 1 exchange of the input rows (every send candidate D_{i->j} to j, received in B_i order) into
+// the per-rank boundary-feature cache; layer 1 then gathers its halo rows from it every epoch
+void fill_x0_cache(Ctx& c) {
+    const Plan& P = c.plan;
+    const size_t ts = tsize(c);
+    const int64_t d0 = c.dp[0];
+    c.d_x0cache = dalloc(c, (size_t)(P.n_bd + 1) * d0 * ts);
+    launch_pack_rows(c, c.H[0], d0, c.d_cand_payload + P.n_bd, P.n_send, c.d_sendbuf, (int32_t)d0);
+    c.tr->exchange(c, c.d_sendbuf, P.D_off.data(), c.d_x0cache, P.B_off.data(), d0 * ts);
+    BNS_CUDA(cudaStreamSynchronize(c.stream));
+}
+
 // ---------------------------------------------------------------------------------------------
 // bns_sample_boundary / bns_sample_edges: a1-a3
 // ---------------------------------------------------------------------------------------------
@@ -516,7 +528,11 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     for (int l = 1; l <= L; ++l) {
         const int64_t din = c.dp[l - 1], dout = c.dp[l];
         void* Hin = c.H[l - 1];
-        if (m > 1) {
+        if (m > 1 && l == 1 && c.d_x0cache) {   // R43: layer-1 halo rows from the boundary-feature cache
+            PhaseTimer t(c, BNS_PH_PACK);
+            launch_pack_rows(c, c.d_x0cache, din, c.d_cand_out, c.n_halo, static_cast<char*>(Hin) + n_in * din * ts,
+                             (int32_t)din);
+        } else if (m > 1) {
             {
                 PhaseTimer t(c, BNS_PH_PACK);
                 launch_pack_rows(c, Hin, din, S_local, c.n_sent, c.d_sendbuf, (int32_t)din);
@@ -826,6 +842,7 @@ bns_status bns_setup(const bns_config* cfg, int64_t num_nodes, const int64_t* in
         setup_device(c, features, labels);
         c.tr = make_transport(c);
         c.n_train_global = c.tr ? c.tr->allreduce_host_i64(c, ntr) : ntr;
+        if ((cfg->flags & BNS_CACHE_INPUT_HALO) && c.tr && c.cfg.world > 1) fill_x0_cache(c);
     });
     if (st != BNS_OK) {
         if (h->c.tr) { delete h->c.tr; h->c.tr = nullptr; }

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--partition", default="ldg2")
+    ap.add_argument("--cache-x0", action="store_true", help="BNS_CACHE_INPUT_HALO (f1, R43): no layer-1 exchange")
     ap.add_argument("--samplers", nargs="+", default=["bns"], choices=["bns", "bes", "dropedge"],
                     help="f3 Table tab:bes analogue: edge samplers at matched dropped-edge counts (P:681)")
     args = ap.parse_args()
@@ -52,7 +53,7 @@ def main():
         ctx = bns.Context(rank=r, world=args.m, dims=sh.dims, layer=sh.layer, precision=prec, indptr=indptr,
                           indices=indices, part_of=part, features=I.features(inner, sh.d0),
                           labels=np.ascontiguousarray(y_all[inner]), transport=bns.BNS_TRANSPORT_NULL_EMULATE,
-                          flags=bns.BNS_TIMING)
+                          flags=bns.BNS_TIMING | (bns.BNS_CACHE_INPUT_HALO if args.cache_x0 else 0))
         W = [torch.tensor(w, device="cuda") for w in I.weights(sh.dims, sh.layer)]
         G = [torch.zeros_like(w) for w in W]
         stream = torch.cuda.ExternalStream(ctx.stream())
@@ -87,11 +88,12 @@ def main():
             cnt = ctx.counts()
             ph = {k: round((t1[k] - t0[k]) / args.steps, 4) for k in t1 if t1[k] - t0[k] > 0}
             # bytes this rank moves per epoch: forward halo rows (recv) and sent rows, backward the reverse
-            fwd = sum((cnt["n_halo"] + cnt["n_sent"]) * dp[l] * s for l in range(sh.L)) / 2
+            fwd = sum((cnt["n_halo"] + cnt["n_sent"]) * dp[l] * s for l in range(1 if args.cache_x0 else 0, sh.L)) / 2
             bwd = sum((cnt["n_halo"] + cnt["n_sent"]) * dp[l] * s for l in range(1, sh.L)) / 2
             wbytes = sum(w.numel() * 4 for w in W)
             comm_ms = (fwd + bwd) / 770e9 * 1e3 + 2 * wbytes / 725e9 * 1e3
             rec = {"config": sh.name, "m": args.m, "rank": r, "p": p, "sampler": sname, "q": q, "prec": args.prec,
+                   "cache_x0": bool(args.cache_x0),
                    "device_ms_per_epoch": float(np.median(ms)), "wall_ms_per_epoch": wall,
                    "est_nvlink_ms": comm_ms, "kernels_per_epoch": (ctx.kernel_count() - k0) / args.steps,
                    "n_in": cnt["n_in"], "n_bd": cnt["n_bd"], "n_halo": cnt["n_halo"], "n_sent": cnt["n_sent"],

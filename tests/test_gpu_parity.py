@@ -16,7 +16,7 @@ from oracle import oracle as O
 from paper_2203_10983_b200 import bns
 from paper_2203_10983_b200 import inputs as I
 
-from gpu_harness import GpuRun, LOSS_TOL, TOL, relerr
+from gpu_harness import GpuRun, LOSS_TOL, TOL, parallel, relerr
 
 pytestmark = pytest.mark.gpu
 SEED = I.BNS_SEED
@@ -377,3 +377,38 @@ def test_dropout_masks_change_per_epoch_and_zero_rate_is_identity():
             run.close()
     assert outs[0][0] == outs[1][0] and all(np.array_equal(a, b) for a, b in zip(outs[0][2], outs[1][2]))
     assert outs[2][0] != outs[0][0]
+
+
+# ---------------- f1 / R43: boundary-feature (X^(0)) cache ----------------
+@pytest.mark.parametrize("prec", [bns.BNS_FP32, bns.BNS_BF16])
+@pytest.mark.parametrize("layer", [bns.BNS_LAYER_SAGE_MEAN, bns.BNS_LAYER_GCN])
+def test_input_halo_cache_is_bit_identical(prec, layer):
+    """BNS_CACHE_INPUT_HALO replaces the layer-1 pack + exchange by a local gather from rows exchanged once at setup:
+    every output must be bitwise the same as the literal per-epoch exchange (R28), across BNS and edge draws."""
+    m = 3
+    dims = [37, 24, 16, 5] if layer == bns.BNS_LAYER_SAGE_MEAN else [37, 16, 5]
+    indptr, indices, part, X, y = wl(2500, 60000, m, dims[0], dims[-1], 17)
+    Ws = I.weights(dims, layer)
+    outs = []
+    for flags in (bns.BNS_RETAIN_GRADS, bns.BNS_RETAIN_GRADS | bns.BNS_CACHE_INPUT_HALO):
+        run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y, flags=flags)
+        W = [w.copy() for w in Ws]
+        rec = []
+        try:
+            for e in range(3):
+                if e == 2:
+                    parallel(m, lambda r: run.ctx[r].sample_edges(bns.BNS_SAMPLER_BES, 0.3, SEED, 2))
+                else:
+                    run.sample(0.3 if e == 0 else 1.0, SEED, e)
+                loss, acc, G, W = run.epoch(W, 0.3)
+                W = [w.astype(np.float32) for w in W]
+                rec.append((loss, acc, [g.copy() for g in G],
+                            [run.gather(bns.BNS_Q_H, l, dims[l]) for l in range(1, len(dims))],
+                            [run.gather(bns.BNS_Q_DH, l, dims[l]) for l in range(1, len(dims))]))
+        finally:
+            run.close()
+        outs.append(rec)
+    for a, b in zip(outs[0], outs[1]):
+        assert a[0] == b[0] and a[1] == b[1]
+        for x, z in zip(a[2] + a[3] + a[4], b[2] + b[3] + b[4]):
+            assert np.array_equal(x, z)
