@@ -138,6 +138,9 @@ struct Oracle {
     // f3: edge samplers BES / DropEdge (Table tab:bes)
     int sampler = 0;                        // 0 BNS (node), 1 BES, 2 DropEdge
     uint32_t tf_mask = 0;                   // R42: layers (bit l-1) whose bf16 emulation follows the transform-first order
+    // f4: multi-label targets (Yelp): sigmoid BCE over the train rows' C logits, F1-micro (R44)
+    bool multilabel = false;
+    std::vector<uint8_t> targets;           // N x C in {0, 1}
     double q = 1.0;                         // arc keep probability of the edge samplers
     uint64_t sample_seed = 0;
 };
@@ -470,7 +473,33 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
     for (int64_t v = 0; v < o.N; ++v) if (o.labels[v] >= 0) ++n_train;
     double loss = 0.0, correct = 0.0;
     o.dH[L].assign((size_t)o.N * C, 0.0);
-    for (int i = 0; i < m; ++i) {                 // f_i summed per partition, then across (rank order)
+    if (o.multilabel) {
+        // R44: loss = (1/(N_train C)) Σ_{v train} Σ_c [softplus(x_vc) - y_vc x_vc] (= BCE(σ(x), y), mean over the
+        // train rows x classes); dLogits = (σ(x) - y)/(N_train C); "accuracy" = F1-micro of x > 0 over the train rows
+        double tp = 0.0, fp = 0.0, fn = 0.0;
+        const double inv = n_train > 0 ? 1.0 / ((double)n_train * C) : 0.0;
+        for (int i = 0; i < m; ++i) {
+            double f_i = 0.0;
+            for (int32_t v : o.parts[i].V) {
+                if (o.labels[v] < 0) continue;
+                const double* x = &o.H[L][(size_t)v * C];
+                double* g = &o.dH[L][(size_t)v * C];
+                for (int c = 0; c < C; ++c) {
+                    const double y = o.targets[(size_t)v * C + c] ? 1.0 : 0.0;
+                    f_i += std::max(x[c], 0.0) - x[c] * y + std::log1p(std::exp(-std::fabs(x[c])));
+                    g[c] = (1.0 / (1.0 + std::exp(-x[c])) - y) * inv;
+                    const bool pred = x[c] > 0.0;
+                    if (pred && y > 0.0) tp += 1.0;
+                    if (pred && y == 0.0) fp += 1.0;
+                    if (!pred && y > 0.0) fn += 1.0;
+                }
+            }
+            loss += f_i;
+        }
+        *loss_out = loss * inv;
+        *acc_out = (2.0 * tp + fp + fn) > 0.0 ? 2.0 * tp / (2.0 * tp + fp + fn) : 0.0;
+    }
+    for (int i = 0; i < m && !o.multilabel; ++i) {   // f_i summed per partition, then across (rank order)
         double f_i = 0.0, c_i = 0.0;
         for (int32_t v : o.parts[i].V) {
             int32_t y = o.labels[v];
@@ -491,9 +520,11 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
         loss += f_i;
         correct += c_i;
     }
-    if (n_train > 0) { loss /= (double)n_train; correct /= (double)n_train; }
-    *loss_out = loss;
-    *acc_out = correct;
+    if (!o.multilabel) {
+        if (n_train > 0) { loss /= (double)n_train; correct /= (double)n_train; }
+        *loss_out = loss;
+        *acc_out = correct;
+    }
 
     // ---------------- backward (Alg.1 l.12) ----------------
     std::vector<std::vector<std::vector<double>>> gW(m, std::vector<std::vector<double>>(L));
@@ -785,6 +816,14 @@ int32_t orc_arc_keep(void* h, int32_t v, int32_t u) { return arc_keep(*(Oracle*)
 // R42: layers (bit l-1) whose bf16-storage emulation follows the transform-first evaluation order (no effect in
 // double mode, where both orders are the same arithmetic)
 void orc_set_transform_first(void* h, uint32_t mask) { ((Oracle*)h)->tf_mask = mask; }
+
+// f4 / R44: multi-label targets, N x C (global ids) in {0, 1}; switches the loss to sigmoid BCE and acc to F1-micro
+void orc_set_multilabel(void* h, const uint8_t* targets) {
+    Oracle& o = *(Oracle*)h;
+    const int C = o.dims[o.L];
+    o.multilabel = targets != nullptr;
+    o.targets.assign(targets ? targets : (const uint8_t*)nullptr, targets ? targets + (size_t)o.N * C : nullptr);
+}
 
 // Explicit draw (for the hand-computed goldens): keep flags for B_rank in B order.
 int32_t orc_set_keep(void* h, double p, int32_t rank, const int32_t* flags) {

@@ -58,6 +58,7 @@ def lib():
         L.orc_arc_keep.restype = i32
         L.orc_arc_keep.argtypes = [vp, i32, i32]
         L.orc_set_transform_first.argtypes = [vp, u32]
+        L.orc_set_multilabel.argtypes = [vp, vp]
         L.orc_rows_sent.restype = i64
         L.orc_rows_sent.argtypes = [vp, i32]
         _LIB = L
@@ -115,6 +116,15 @@ class Oracle:
     def set_transform_first(self, mask):
         """R42: bf16 emulation of the transform-first order on layers in mask (bit l-1); no effect in double."""
         lib().orc_set_transform_first(self.h, int(mask))
+
+    def set_multilabel(self, targets):
+        """f4 / R44: N x C multi-hot targets (global ids); loss -> sigmoid BCE, acc -> F1-micro.  None: back to CE."""
+        if targets is None:
+            lib().orc_set_multilabel(self.h, None)
+            return
+        self._targets = np.ascontiguousarray(targets, np.uint8)
+        assert self._targets.shape == (self.N, int(self.dims[-1]))
+        lib().orc_set_multilabel(self.h, _p(self._targets))
 
     def set_training(self, optimizer=0, beta1=0.9, beta2=0.999, eps=1e-8, dropout=0.0, dropout_seed=0):
         """f2: optimizer 0 = SGD (Alg.1 l.14), 1 = Adam; dropout rate on every layer input (R38)."""

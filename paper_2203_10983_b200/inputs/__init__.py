@@ -89,6 +89,14 @@ def labels(N: int, C: int, train_frac: float, seed: int = SEED_LABEL) -> np.ndar
     return out
 
 
+def multilabels(N: int, C: int, density: float = 0.1, seed: int = 0x5E1B) -> np.ndarray:
+    """f4 (Yelp-style multi-label task): N x C multi-hot uint8 targets, each entry an independent
+    Bernoulli(density) from a seeded Philox stream (row v depends only on the seed, so every rank slices the same
+    global matrix).  The density is an assumption (the paper gives none)."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    return (rng.random((N, C), dtype=np.float32) < density).astype(np.uint8)
+
+
 def weights(dims, layer_kind: int, seed: int = SEED_WEIGHT) -> list[np.ndarray]:
     """Glorot-uniform fp32 weights; SAGE W^l is (2 d_{l-1}) x d_l (rows [0,d) multiply z), GCN d_{l-1} x d_l."""
     out = []

@@ -38,7 +38,7 @@ def dense_matrix(indptr, indices, part_of, kept, p, layer, arcs=None):
     return M
 
 
-def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws, masks=None, arcs=None):
+def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws, masks=None, arcs=None, targets=None):
     """masks[l]: optional N x d_l elementwise factors on the input of layer l+1 (dropout, R38)."""
     M = torch.tensor(dense_matrix(indptr, indices, part_of, kept, p, layer, arcs), dtype=torch.float64)
     H = torch.tensor(np.asarray(X, np.float64))
@@ -57,13 +57,22 @@ def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws, ma
     train = y >= 0
     ntr = int(train.sum())
     logits = Hs[-1]
-    if ntr:
-        loss = torch.nn.functional.cross_entropy(logits[train], y[train], reduction="sum") / ntr
+    if targets is not None:   # f4: multi-label, torch's BCE-with-logits (mean) and sklearn's F1-micro (independent)
+        T = torch.tensor(np.asarray(targets, np.float64))
+        loss = (torch.nn.functional.binary_cross_entropy_with_logits(logits[train], T[train], reduction="mean")
+                if ntr else logits.sum() * 0.0)
+        loss.backward()
+        from sklearn.metrics import f1_score
+        pred = (logits.detach().numpy()[train.numpy()] > 0).astype(int)
+        acc = float(f1_score(np.asarray(targets)[train.numpy()], pred, average="micro", zero_division=0)) if ntr else 0.0
     else:
-        loss = logits.sum() * 0.0
-    loss.backward()
-    am = logits.detach().numpy().argmax(1)  # numpy argmax: first max = lowest index (R22)
-    acc = float(((am == y.numpy()) & train.numpy()).sum()) / ntr if ntr else 0.0
+        if ntr:
+            loss = torch.nn.functional.cross_entropy(logits[train], y[train], reduction="sum") / ntr
+        else:
+            loss = logits.sum() * 0.0
+        loss.backward()
+        am = logits.detach().numpy().argmax(1)  # numpy argmax: first max = lowest index (R22)
+        acc = float(((am == y.numpy()) & train.numpy()).sum()) / ntr if ntr else 0.0
     return dict(loss=float(loss.detach()), acc=acc, H=[h.detach().numpy() for h in Hs], Z=[z.detach().numpy() for z in Zs],
                 dH=[None] + [h.grad.numpy() if h.grad is not None else None for h in Hs[1:]],
                 dW=[w.grad.numpy() for w in W])

@@ -351,3 +351,40 @@ def test_transform_first_is_noop_in_double_and_close_in_bf16(drop):
     for x, z in zip(d[1] + d[2], t[1] + t[2]):
         assert np.abs(x - z).max() <= 5e-2 * np.abs(x).max()
     assert not all(np.array_equal(x, z) for x, z in zip(res[(True, 0)][1], t[1]))
+
+
+# ---------------- f4: multi-label sigmoid BCE + F1-micro (Yelp; reading R44) ----------------
+@pytest.mark.parametrize("layer", [0, 1])
+@pytest.mark.parametrize("seed,m,p", [(81, 3, 0.5), (82, 1, 1.0), (83, 4, 0.2)])
+def test_multilabel_bce_dense_bruteforce(layer, seed, m, p):
+    dims = [3, 5, 6]
+    ip, ix, part, X, y, Ws = random_case(seed, m=m, layer=layer, dims=tuple(dims))
+    T = I.multilabels(len(ip) - 1, dims[-1], 0.3, seed=seed)
+    o = O.Oracle(ip, ix, part, m, dims, layer, X, y)
+    o.set_multilabel(T)
+    o.sample(p, 77, seed)
+    kept = [set(int(u) for u in o.list(O.U_LIST, r)) for r in range(m)]
+    ref = forward_backward(ip, ix, part, kept, p, layer, X, y, Ws, targets=T)
+    loss, acc, G = o.epoch([w.copy() for w in Ws], 0.0)
+    assert abs(loss - ref["loss"]) <= 1e-12 * max(1.0, abs(ref["loss"]))
+    assert abs(acc - ref["acc"]) <= 1e-12
+    np.testing.assert_allclose(o.tensor(O.T_DH, 2), ref["dH"][2], rtol=1e-10, atol=1e-15)
+    for g, r in zip(G, ref["dW"]):
+        np.testing.assert_allclose(g, r, rtol=1e-10, atol=1e-15)
+
+
+def test_multilabel_closed_forms():
+    """zero logits: loss = ln 2 exactly, no positive prediction -> F1 = 0; CE mode restored by set_multilabel(None)"""
+    dims = [3, 4, 5]
+    ip, ix, part, X, y, Ws = random_case(84, m=2, dims=tuple(dims))
+    T = I.multilabels(len(ip) - 1, dims[-1], 0.5, seed=3)
+    o = O.Oracle(ip, ix, part, 2, dims, 0, X, y)
+    o.set_multilabel(T)
+    o.sample(0.5, 1, 1)
+    Wz = [w.copy() for w in Ws]
+    Wz[-1][...] = 0.0
+    loss, acc, G = o.epoch(Wz, 0.0)
+    assert abs(loss - math.log(2.0)) < 1e-15 and acc == 0.0
+    o.set_multilabel(None)
+    loss, acc, G = o.epoch([w.copy() for w in Wz], 0.0)
+    assert abs(loss - math.log(dims[-1])) < 1e-12
