@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--q", type=float, default=None,
                     help="edge keep probability; default matched to BNS p (P:681): BES q = p, "
                          "DropEdge q = 1 - (1-p) cross/nnz")
+    ap.add_argument("--multilabel", action="store_true",
+                    help="f4: sigmoid BCE + F1-micro on seeded multi-hot targets (the Yelp task, PAPER.md:384)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-scale", type=float, default=64.0, help="oracle sample = workload scaled down by this")
     ap.add_argument("--no-e2e", action="store_true")
@@ -308,6 +310,8 @@ def run_ours(args):
     ctx = bns.Context(rank=rank, world=world, dims=shape.dims, layer=shape.layer, precision=prec, indptr=indptr,
                       indices=indices, part_of=part, features=X, labels=y, device=local, nccl_id=nccl_id,
                       max_p=0.0, flags=bns.BNS_TIMING | (bns.BNS_CACHE_INPUT_HALO if world > 1 else 0))
+    if args.multilabel:
+        ctx.set_multilabel(I.multilabels(shape.N, shape.C, 0.1)[inner])
     if args.adam or args.dropout > 0:
         ctx.set_training(bns.BNS_OPT_ADAM if args.adam else bns.BNS_OPT_SGD, 0.9, 0.999, 1e-8, args.dropout, 0xD0)
     del X
@@ -435,7 +439,8 @@ def run_ours(args):
                            "bns_sample_boundary" if sampler == bns.BNS_SAMPLER_BNS else
                            f"bns_sample_edges({args.sampler}, q={q:.4f})",
                            "Adam" if args.adam else "SGD",
-                           f", dropout {args.dropout}" if args.dropout > 0 else "")},
+                           (f", dropout {args.dropout}" if args.dropout > 0 else "") +
+                           (", multi-label sigmoid BCE loss" if args.multilabel else ""))},
             "roofline": {"bound": "hbm", "kernel": "segment SpMM (a6 fwd + a10 bwd, incl. split-row fixup)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": (achieved / hbm_peak) if achieved else None, "traffic": latest_traffic(),

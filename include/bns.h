@@ -162,6 +162,14 @@ typedef enum { BNS_OPT_SGD = 0, BNS_OPT_ADAM = 1 } bns_optimizer;
 bns_status bns_set_training(bns_ctx* ctx, int32_t optimizer, double beta1, double beta2, double eps, double dropout,
                             uint64_t dropout_seed);
 
+/* the multi-label task of the Yelp experiments: targets = HOST uint8
+ * |V_i| x dims[L] in {0, 1} (this rank's inner rows, ascending global id; copied), the train rows are those with
+ * labels >= 0 as given to bns_setup.  Then bns_epoch's loss is the mean over train rows x classes of
+ * BCE(σ(x), y) = softplus(x) - y x, dLogits = (σ(x) - y) / (N_train C), and acc is F1-micro of x > 0 over the train
+ * rows (R44; all-reduced TP / FP / FN).  NULL restores the single-label cross entropy.  Not collective; every rank
+ * must choose the same mode.  A value other than 0 / 1 -> BNS_ERR_INVALID. */
+bns_status bns_set_multilabel(bns_ctx* ctx, const uint8_t* targets);
+
 /* Debug / parity queries: copy a host-side view into host_dst (capacity in bytes); *written = bytes written.
  * Row tensors are returned as fp32 row-major with LOGICAL dims (padding stripped), inner rows in ascending gid. */
 typedef enum {

@@ -30,7 +30,7 @@ PHASES = ["sample", "induce", "pack", "exchange", "spmm_fwd", "gemm_fwd", "loss"
           "exchange_bwd", "scatter", "allreduce", "update", "epoch_total", "sample_total"]
 
 EXPORTS = ["bns_get_unique_id", "bns_group_create", "bns_group_destroy", "bns_setup", "bns_sample_boundary",
-           "bns_sample_edges", "bns_epoch", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
+           "bns_sample_edges", "bns_set_multilabel", "bns_epoch", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
 BNS_OPT_SGD, BNS_OPT_ADAM = 0, 1
 
 
@@ -65,6 +65,7 @@ def lib():
         L.bns_setup.argtypes = [ctypes.POINTER(bns_config), i64, vp, vp, vp, vp, vp, ctypes.POINTER(vp)]
         L.bns_sample_boundary.argtypes = [vp, f64, u64, u64]
         L.bns_sample_edges.argtypes = [vp, i32, f64, u64, u64]
+        L.bns_set_multilabel.argtypes = [vp, vp]
         L.bns_epoch.argtypes = [vp, vp, f32, vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]
         L.bns_set_training.argtypes = [vp, i32, f64, f64, f64, f64, u64]
         L.bns_query.argtypes = [vp, i32, i32, vp, i64, ctypes.POINTER(i64)]
@@ -73,7 +74,8 @@ def lib():
         L.bns_last_error.restype = ctypes.c_char_p
         L.bns_last_error.argtypes = [vp]
         L.bns_destroy.argtypes = [vp]
-        for f in ("bns_get_unique_id", "bns_group_create", "bns_setup", "bns_sample_boundary", "bns_sample_edges", "bns_epoch",
+        for f in ("bns_get_unique_id", "bns_group_create", "bns_setup", "bns_sample_boundary", "bns_sample_edges",
+                  "bns_set_multilabel", "bns_epoch",
                   "bns_set_training", "bns_query"):
             getattr(L, f).restype = ctypes.c_int
         L.bns_group_destroy.restype = None
@@ -129,6 +131,15 @@ def bns_sample_boundary(ctx, p: float, seed: int, epoch: int):
 
 def bns_sample_edges(ctx, sampler: int, q: float, seed: int, epoch: int):
     _check(lib().bns_sample_edges(ctx, int(sampler), float(q), int(seed) & (2**64 - 1), int(epoch) & (2**64 - 1)), ctx)
+
+
+def bns_set_multilabel(ctx, targets):
+    """f4: |V_i| x C multi-hot uint8 targets (None: back to single-label cross entropy)."""
+    if targets is None:
+        _check(lib().bns_set_multilabel(ctx, None), ctx)
+        return
+    t = np.ascontiguousarray(targets, np.uint8)
+    _check(lib().bns_set_multilabel(ctx, t.ctypes.data_as(ctypes.c_void_p)), ctx)
 
 
 def bns_epoch(ctx, weights: Sequence, lr: float, grads: Sequence | None = None):
@@ -198,6 +209,9 @@ class Context:
 
     def sample_boundary(self, p, seed, epoch):
         bns_sample_boundary(self.h, p, seed, epoch)
+
+    def set_multilabel(self, targets):
+        bns_set_multilabel(self.h, targets)
 
     def sample_edges(self, sampler, q, seed, epoch):
         bns_sample_edges(self.h, sampler, q, seed, epoch)

@@ -340,7 +340,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.splitk_cap = 32 * wmax;
     c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
     c.d_scal = static_cast<double*>(dalloc(c, 4 * sizeof(double)));
-    c.d_lpart = static_cast<double*>(dalloc(c, 2 * 2048 * sizeof(double)));   // k_xent block partials
+    c.d_lpart = static_cast<double*>(dalloc(c, 4 * 2048 * sizeof(double)));   // k_xent / k_bce block partials
     c.d_nonfinite = static_cast<int32_t*>(dalloc(c, 16));
     c.d_hostw = static_cast<float*>(dalloc(c, 2 * wlog * sizeof(float)));
     c.hostw_n = wlog;
@@ -624,8 +624,12 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     {
         PhaseTimer t(c, BNS_PH_LOSS);
         const bool tfL = (c.tf_mask >> (L - 1)) & 1u;
-        launch_xent(c, c.d_logits, c.dp[L], c.dims[L], c.d_dlogits, c.d_dpre, tfL ? c.d_deg_in : nullptr,
-                    tfL ? c.d_dxcat : nullptr);
+        if (c.multilabel)
+            launch_bce(c, c.d_logits, c.dp[L], c.dims[L], c.d_dlogits, c.d_dpre, tfL ? c.d_deg_in : nullptr,
+                       tfL ? c.d_dxcat : nullptr);
+        else
+            launch_xent(c, c.d_logits, c.dp[L], c.dims[L], c.d_dlogits, c.d_dpre, tfL ? c.d_deg_in : nullptr,
+                        tfL ? c.d_dxcat : nullptr);
     }
     // ------------------------------ backward (l.12) ------------------------------
     for (int l = L; l >= 1; --l) {
@@ -749,7 +753,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     // ------------------------------ AllReduce (l.13) + update (l.14) ------------------------------
     if (m > 1) {
         PhaseTimer t(c, BNS_PH_ALLREDUCE);
-        c.tr->allreduce(c, c.d_gflat, c.gflat_n, c.d_scal, 2);
+        c.tr->allreduce(c, c.d_gflat, c.gflat_n, c.d_scal, c.multilabel ? 4 : 2);
     }
     {
         PhaseTimer t(c, BNS_PH_UPDATE);
@@ -762,7 +766,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         }
     }
     total.reset();
-    double scal[2];
+    double scal[4] = {0.0, 0.0, 0.0, 0.0};
     int32_t nonfinite = 0;
     BNS_CUDA(cudaMemcpyAsync(scal, c.d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c.stream));
     BNS_CUDA(cudaMemcpyAsync(&nonfinite, c.d_nonfinite, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
@@ -777,8 +781,14 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     if (c.tr) c.tr->poll(c);
     collect_times(c);
     const double ntr = (double)c.n_train_global;
-    if (loss) *loss = ntr > 0 ? scal[0] / ntr : 0.0;
-    if (acc) *acc = ntr > 0 ? scal[1] / ntr : 0.0;
+    if (c.multilabel) {   // R44: mean BCE over train rows x classes; F1-micro = 2TP / (2TP + FP + FN)
+        if (loss) *loss = ntr > 0 ? scal[0] / (ntr * c.dims[L]) : 0.0;
+        const double den = 2.0 * scal[1] + scal[2] + scal[3];
+        if (acc) *acc = den > 0 ? 2.0 * scal[1] / den : 0.0;
+    } else {
+        if (loss) *loss = ntr > 0 ? scal[0] / ntr : 0.0;
+        if (acc) *acc = ntr > 0 ? scal[1] / ntr : 0.0;
+    }
     if (nonfinite) throw Error(BNS_ERR_NONFINITE, "loss is not finite; weights left unchanged");
 }
 
@@ -932,6 +942,23 @@ bns_status bns_set_training(bns_ctx* h, int32_t optimizer, double beta1, double 
             c.d_rowgid = static_cast<int32_t*>(dalloc(c, (c.plan.n_in + c.halo_cap + 1) * sizeof(int32_t)));
             BNS_CUDA(cudaMemcpy(c.d_rowgid, c.plan.V.data(), c.plan.n_in * sizeof(int32_t), cudaMemcpyHostToDevice));
         }
+    });
+}
+
+bns_status bns_set_multilabel(bns_ctx* h, const uint8_t* targets) {
+    if (!h) return BNS_ERR_INVALID;
+    Ctx& c = h->c;
+    if (c.failed || c.plan_only) return BNS_ERR_STATE;
+    return guard(h, [&] {
+        BNS_CUDA(cudaSetDevice(c.cfg.device));
+        BNS_CUDA(cudaStreamSynchronize(c.stream));
+        if (!targets) { c.multilabel = false; return; }
+        const int64_t n = c.plan.n_in * (int64_t)c.dims[c.L];
+        for (int64_t k = 0; k < n; ++k)
+            if (targets[k] > 1) throw Error(BNS_ERR_INVALID, "targets must be 0 or 1");
+        if (!c.d_targets) c.d_targets = static_cast<uint8_t*>(dalloc(c, (size_t)n + 16));
+        if (n) BNS_CUDA(cudaMemcpy(c.d_targets, targets, (size_t)n, cudaMemcpyHostToDevice));
+        c.multilabel = true;
     });
 }
 

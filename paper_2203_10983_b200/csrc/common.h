@@ -138,6 +138,8 @@ struct Ctx {
     int64_t* d_split_fwd = nullptr;                                  // per-epoch induced forward segments
     int64_t n_split_fwd = 0, n_split_bwd = 0;                        // this epoch's list lengths
     float* d_cscale = nullptr;     // per-column scale (GCN forward)
+    bool multilabel = false;         // f4 / R44: sigmoid BCE + F1-micro (bns_set_multilabel)
+    uint8_t* d_targets = nullptr;    // n_in x C multi-hot targets
     void* d_x0cache = nullptr;       // f1 / R43: X^(0) rows of every boundary node, B_i order (BNS_CACHE_INPUT_HALO)
     uint32_t* d_scat_mask = nullptr; // a12 merged scatter: peers holding each owner row (bit j), world <= 32
     int32_t* d_scat_pos = nullptr;   // ... and the row's position in the returned buffer, n_in x world

@@ -76,6 +76,8 @@ void launch_scatter_rows(Ctx& c, void* dst, int64_t ld, const void* src, int32_t
 // rs / dps (optional, R42): also write dps = dPre * rs[row] (the transform-first SpMM^T source)
 void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t,
                  const float* rs = nullptr, void* dps = nullptr);
+void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
+                void* dps);
 void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre,
                       const float* rs = nullptr, void* dps = nullptr);
 void launch_wpack_all(Ctx& c, float* const* W);

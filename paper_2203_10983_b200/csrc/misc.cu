@@ -232,17 +232,97 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
     }
 }
 
-// one warp: lane-strided partial sums then a fixed butterfly (deterministic)
-__global__ void k_xent_final(const double* __restrict__ part, int nb, double* __restrict__ scal) {
-    const int lane = threadIdx.x & 31;
-    double a = 0.0, b = 0.0;
-    for (int k = lane; k < nb; k += 32) { a += part[2 * k]; b += part[2 * k + 1]; }
+// f4 / R44 multi-label: per train row and class, softplus(x) - y x (= BCE(σ(x), y)); dLogits = (σ(x) - y) / (N_train C);
+// TP / FP / FN of x > 0 for F1-micro.  Block partials [loss, tp, fp, fn], fixed order as k_xent.
+template <typename T, int NPL>
+__global__ void __launch_bounds__(256) k_bce(const float* __restrict__ logits, int64_t ld, int64_t n, int32_t C,
+                                             const int32_t* __restrict__ labels, const uint8_t* __restrict__ tgt,
+                                             double inv, float* __restrict__ dlog, T* __restrict__ dpre,
+                                             double* __restrict__ part, const float* __restrict__ rs,
+                                             T* __restrict__ dps) {
+    __shared__ double s_v[4][8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t warp = (int64_t)blockIdx.x * 8 + w;
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    double loss = 0.0, tp = 0.0, fp = 0.0, fn = 0.0;
+    for (int64_t r = warp; r < n; r += nwarps) {
+        const bool train = labels[r] >= 0;
+        const float rsr = dps ? rs[r] : 0.f;
+        float lsum = 0.f;
+        int ntp = 0, nfp = 0, nfn = 0;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
+        for (int k = 0; k < NPL; ++k) {
+            const int c = lane + 32 * k;
+            if (c >= ld) break;
+            float v = 0.f;
+            if (train && c < C) {
+                const float x = logits[r * ld + c];
+                const float y = tgt[r * C + c] ? 1.f : 0.f;
+                lsum += fmaxf(x, 0.f) - x * y + log1pf(expf(-fabsf(x)));
+                v = (float)((1.0 / (1.0 + exp(-(double)x)) - (double)y) * inv);
+                const bool pred = x > 0.f;
+                ntp += (pred && y > 0.f);
+                nfp += (pred && y == 0.f);
+                nfn += (!pred && y > 0.f);
+            }
+            dlog[r * ld + c] = v;
+            const T q = from_f<T>(v);
+            dpre[r * ld + c] = q;
+            if (dps) dps[r * ld + c] = from_f<T>(to_f(q) * rsr);
+        }
+        if (!train) continue;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+            ntp += __shfl_xor_sync(0xffffffffu, ntp, o);
+            nfp += __shfl_xor_sync(0xffffffffu, nfp, o);
+            nfn += __shfl_xor_sync(0xffffffffu, nfn, o);
+        }
+        loss += (double)lsum;
+        tp += ntp;
+        fp += nfp;
+        fn += nfn;
     }
-    if (lane == 0) { scal[0] = a; scal[1] = b; }
+    if (lane == 0) { s_v[0][w] = loss; s_v[1][w] = tp; s_v[2][w] = fp; s_v[3][w] = fn; }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double a = 0.0;
+        for (int k = 0; k < 8; ++k) a += s_v[threadIdx.x][k];
+        part[4 * blockIdx.x + threadIdx.x] = a;
+    }
+}
+
+// one warp: lane-strided partial sums of nv interleaved values, then a fixed butterfly (deterministic)
+__global__ void k_xent_final(const double* __restrict__ part, int nb, int nv, double* __restrict__ scal) {
+    const int lane = threadIdx.x & 31;
+    for (int q = 0; q < nv; ++q) {
+        double a = 0.0;
+        for (int k = lane; k < nb; k += 32) a += part[nv * k + q];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) scal[q] = a;
+    }
+}
+
+void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
+                void* dps) {
+    const double inv = c.n_train_global > 0 ? 1.0 / ((double)c.n_train_global * C) : 0.0;
+    const int64_t n = c.plan.n_in;
+    const int npl = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
+#define BNS_BCE(T, NPL)                                                                                              \
+    k_bce<T, NPL><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, n, C, c.d_labels, c.d_targets, inv, dlogits,        \
+                                                     (T*)dpre_t, c.d_lpart, rs, (T*)dps)
+    if (c.prec == BNS_BF16) {
+        if (npl == 1) BNS_BCE(__nv_bfloat16, 1); else if (npl == 2) BNS_BCE(__nv_bfloat16, 2);
+        else if (npl == 4) BNS_BCE(__nv_bfloat16, 4); else BNS_BCE(__nv_bfloat16, 8);
+    } else {
+        if (npl == 1) BNS_BCE(float, 1); else if (npl == 2) BNS_BCE(float, 2);
+        else if (npl == 4) BNS_BCE(float, 4); else BNS_BCE(float, 8);
+    }
+#undef BNS_BCE
+    k_xent_final<<<1, 32, 0, c.stream>>>(c.d_lpart, kXentBlocks, 4, c.d_scal);
+    c.kernels += 2;
+    BNS_CHECK_LAUNCH();
 }
 
 void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
@@ -262,7 +342,7 @@ void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlog
         else if (npl == 4) BNS_XENT(float, 4); else BNS_XENT(float, 8);
     }
 #undef BNS_XENT
-    k_xent_final<<<1, 32, 0, c.stream>>>(c.d_lpart, kXentBlocks, c.d_scal);
+    k_xent_final<<<1, 32, 0, c.stream>>>(c.d_lpart, kXentBlocks, 2, c.d_scal);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
 }

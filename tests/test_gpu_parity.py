@@ -412,3 +412,51 @@ def test_input_halo_cache_is_bit_identical(prec, layer):
         assert a[0] == b[0] and a[1] == b[1]
         for x, z in zip(a[2] + a[3] + a[4], b[2] + b[3] + b[4]):
             assert np.array_equal(x, z)
+
+
+# ---------------- f4: multi-label sigmoid BCE + F1-micro (Yelp; R44) ----------------
+@pytest.mark.parametrize("prec", [bns.BNS_FP32, bns.BNS_BF16])
+@pytest.mark.parametrize("layer", [bns.BNS_LAYER_SAGE_MEAN, bns.BNS_LAYER_GCN])
+@pytest.mark.parametrize("m,p", [(1, 1.0), (3, 0.3)])
+def test_multilabel_parity(prec, layer, m, p):
+    dims = [37, 24, 16, 12] if layer == bns.BNS_LAYER_SAGE_MEAN else [37, 16, 12]
+    indptr, indices, part, X, y = wl(3000, 90000, m, dims[0], dims[-1], 51 + m)
+    N, L = len(indptr) - 1, len(dims) - 1
+    T = I.multilabels(N, dims[-1], 0.2, seed=7)
+    Ws = I.weights(dims, layer)
+    Wd = [w.astype(np.float64) for w in Ws]
+    run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y)
+    for r, c in enumerate(run.ctx):
+        c.set_multilabel(T[run.inner[r]])
+    orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
+    orc.set_bf16(prec == bns.BNS_BF16)
+    orc.set_multilabel(T)
+    tol = TOL[prec]
+    try:
+        for e in range(2 if prec == bns.BNS_FP32 else 1):
+            run.sample(p, SEED, e)
+            orc.sample(p, SEED, e)
+            orc.set_transform_first(run.tf)
+            loss, f1, G, Wn = run.epoch(Ws, 0.5)
+            lo, fo, Go = orc.epoch(Wd, 0.5)
+            assert abs(loss - lo) <= LOSS_TOL * abs(lo), (e, loss, lo)
+            assert abs(f1 - fo) <= (1e-3 if prec == bns.BNS_FP32 else 2e-2), (e, f1, fo)
+            F = relu_flip_floor(run, orc, L, prec, f"bce{e}")
+            assert relerr(run.gather(bns.BNS_Q_DH, L, dims[L]), orc.tensor(O.T_DH, L)) <= tol
+            for l in range(L):
+                if l + 1 > F:
+                    assert relerr(G[l], Go[l]) <= tol, ("dW", e, l)
+            Ws = [w.astype(np.float32) for w in Wn]
+    finally:
+        run.close()
+
+
+def test_multilabel_rejects_non_binary_targets():
+    indptr, indices, part, X, y = wl(300, 2000, 1, 4, 3, 3)
+    run = GpuRun(indptr, indices, part, 1, [4, 3], 0, bns.BNS_FP32, X, y)
+    try:
+        with pytest.raises(bns.BnsError) as ei:
+            run.ctx[0].set_multilabel(np.full((len(indptr) - 1, 3), 2, np.uint8))
+        assert ei.value.code == bns.BNS_ERR_INVALID
+    finally:
+        run.close()
