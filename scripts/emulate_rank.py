@@ -92,7 +92,12 @@ def main():
             bwd = sum((cnt["n_halo"] + cnt["n_sent"]) * dp[l] * s for l in range(1, sh.L)) / 2
             wbytes = sum(w.numel() * 4 for w in W)
             comm_ms = (fwd + bwd) / 770e9 * 1e3 + 2 * wbytes / 725e9 * 1e3
+            # a4 pack reads + writes |S| rows per layer, a12 scatter reads 2 and writes 1 row per returned row
+            pack_b = sum(2 * cnt["n_sent"] * dp[l] * s for l in range(1 if args.cache_x0 else 0, sh.L))
+            scat_b = sum(3 * cnt["n_sent"] * dp[l] * s for l in range(1, sh.L))
+            gbs = lambda b, ph: round(b / (ph * 1e-3) / 1e9, 1) if ph and ph > 0 else None
             rec = {"config": sh.name, "m": args.m, "rank": r, "p": p, "sampler": sname, "q": q, "prec": args.prec,
+                   "pack_gbs": gbs(pack_b, ph.get("pack")), "scatter_gbs": gbs(scat_b, ph.get("scatter")),
                    "cache_x0": bool(args.cache_x0),
                    "device_ms_per_epoch": float(np.median(ms)), "wall_ms_per_epoch": wall,
                    "est_nvlink_ms": comm_ms, "kernels_per_epoch": (ctx.kernel_count() - k0) / args.steps,
