@@ -78,7 +78,7 @@ bool keep(uint32_t u, uint32_t i, uint64_t epoch, uint64_t seed, uint64_t T) {
     return (uint64_t)draw(u, i, epoch, seed) < T;
 }
 
-enum { KIND_SAGE = 0, KIND_GCN = 1 };
+enum { KIND_SAGE = 0, KIND_GCN = 1, KIND_GAT = 2 };
 
 // R19 (bf16-GEMM mode): "bf16 storage of H / Z / halo / GEMM operands, fp32 accumulation,
 // fp32 master weights".  When the oracle runs in that mode it rounds every STORED tensor the definition names to
@@ -298,6 +298,144 @@ struct LocalIndex {
 };
 
 // ---------------------------------------------------------------------------------------------
+// f4 / R45: GAT layer (Velickovic et al.; the paper's Table tab:gat ablation), one head, on the
+// sampled graph of partition i: Y = X W on every stacked row, el = Y a_l, er = Y a_r,
+//   e_vu = LeakyReLU_0.2(el_v + er_u) over u in N'(v) = {kept neighbours} ∪ {v},
+//   alpha_vu = softmax_u(e_vu),  pre_v = Σ_u alpha_vu Y_u.
+// Dropped boundary neighbours simply leave N'(v) (the softmax renormalises; no 1/p).  Weights: (din + 2) x dout
+// rows [W ; a_l ; a_r].  Y and dY are stored tensors in the bf16 emulation (R19); a_l, a_r stay fp32 / double.
+// ---------------------------------------------------------------------------------------------
+struct GatEdges {
+    std::vector<int64_t> ptr;   // per inner row r: [ptr[r], ptr[r+1]) into col / s
+    std::vector<int64_t> col;   // stacked row of u (self last)
+    std::vector<double> s;      // el_v + er_u
+};
+
+template <typename ST>
+void gat_setup(const Oracle& o, int i, const std::vector<int64_t>& row, const std::vector<double>& X, int din,
+               int dout, const std::vector<double>& Wq, const std::vector<double>& W, ST st, std::vector<double>& Y,
+               std::vector<double>& el, std::vector<double>& er, GatEdges& E) {
+    const Partition& P = o.parts[i];
+    const size_t n_in = P.V.size(), n_h = P.U.size(), n = n_in + n_h;
+    Y.assign(n * dout, 0.0);
+    el.assign(n, 0.0);
+    er.assign(n, 0.0);
+    for (size_t r = 0; r < n; ++r) {
+        for (int c = 0; c < dout; ++c) {
+            double y = 0.0;
+            for (int k = 0; k < din; ++k) y += X[r * din + k] * Wq[(size_t)k * dout + c];
+            Y[r * dout + c] = st(y);
+        }
+        for (int c = 0; c < dout; ++c) {
+            el[r] += Y[r * dout + c] * W[(size_t)din * dout + c];
+            er[r] += Y[r * dout + c] * W[(size_t)(din + 1) * dout + c];
+        }
+    }
+    E.ptr.assign(1, 0);
+    E.col.clear();
+    E.s.clear();
+    for (size_t r = 0; r < n_in; ++r) {
+        const int32_t v = P.V[r];
+        for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
+            const int32_t u = o.indices[e];
+            double c;
+            if (!arc_in(o, v, u, row[u], (int64_t)n_in, &c)) continue;
+            E.col.push_back(row[u]);
+            E.s.push_back(el[r] + er[row[u]]);
+        }
+        E.col.push_back((int64_t)r);   // self loop
+        E.s.push_back(el[r] + er[r]);
+        E.ptr.push_back((int64_t)E.col.size());
+    }
+}
+
+double leaky(double x) { return x > 0.0 ? x : 0.2 * x; }
+
+void gat_alpha(const GatEdges& E, size_t r, std::vector<double>& a) {
+    double mx = -INFINITY;
+    for (int64_t e = E.ptr[r]; e < E.ptr[r + 1]; ++e) mx = std::max(mx, leaky(E.s[e]));
+    double den = 0.0;
+    for (int64_t e = E.ptr[r]; e < E.ptr[r + 1]; ++e) den += std::exp(leaky(E.s[e]) - mx);
+    a.clear();
+    for (int64_t e = E.ptr[r]; e < E.ptr[r + 1]; ++e) a.push_back(std::exp(leaky(E.s[e]) - mx) / den);
+}
+
+template <typename ST>
+void gat_forward(const Oracle& o, int i, const std::vector<int64_t>& row, const std::vector<double>& X, int din,
+                 int dout, const std::vector<double>& Wq, const std::vector<double>& W, ST st, std::vector<double>& pre) {
+    std::vector<double> Y, el, er, a;
+    GatEdges E;
+    gat_setup(o, i, row, X, din, dout, Wq, W, st, Y, el, er, E);
+    const size_t n_in = o.parts[i].V.size();
+    pre.assign(n_in * dout, 0.0);
+    for (size_t r = 0; r < n_in; ++r) {
+        gat_alpha(E, r, a);
+        for (int64_t e = E.ptr[r]; e < E.ptr[r + 1]; ++e)
+            for (int c = 0; c < dout; ++c) pre[r * dout + c] += a[e - E.ptr[r]] * Y[(size_t)E.col[e] * dout + c];
+    }
+}
+
+// backward: c_v = g_v . pre_v; per edge dalpha = g_v . Y_u, ds = alpha (dalpha - c_v) LeakyReLU'(s);
+// dY_u += alpha g_v; del_v += ds; der_u += ds; then dY_v += del_v a_l, dY_u += der_u a_r (stored);
+// dW = X^T dY, da_l = Σ_v del_v Y_v, da_r = Σ_u der_u Y_u; dX = dY W^T (stored, then the layer's dropout)
+template <typename ST>
+void gat_backward(const Oracle& o, int i, const std::vector<int64_t>& row, const std::vector<double>& X, int din,
+                  int dout, const std::vector<double>& Wq, const std::vector<double>& W, ST st,
+                  const std::vector<double>& dpre, std::vector<double>& g, std::vector<double>* dX, int l) {
+    std::vector<double> Y, el, er, a;
+    GatEdges E;
+    gat_setup(o, i, row, X, din, dout, Wq, W, st, Y, el, er, E);
+    const Partition& P = o.parts[i];
+    const size_t n_in = P.V.size(), n = n_in + P.U.size();
+    std::vector<double> dY(n * dout, 0.0), del(n, 0.0), der(n, 0.0);
+    for (size_t r = 0; r < n_in; ++r) {
+        gat_alpha(E, r, a);
+        const double* gv = &dpre[r * dout];
+        std::vector<double> outv(dout, 0.0);
+        for (int64_t e = E.ptr[r]; e < E.ptr[r + 1]; ++e)
+            for (int c = 0; c < dout; ++c) outv[c] += a[e - E.ptr[r]] * Y[(size_t)E.col[e] * dout + c];
+        double cv = 0.0;
+        for (int c = 0; c < dout; ++c) cv += gv[c] * outv[c];
+        for (int64_t e = E.ptr[r]; e < E.ptr[r + 1]; ++e) {
+            const size_t u = (size_t)E.col[e];
+            const double al = a[e - E.ptr[r]];
+            double da = 0.0;
+            for (int c = 0; c < dout; ++c) da += gv[c] * Y[u * dout + c];
+            const double ds = al * (da - cv) * (E.s[e] > 0.0 ? 1.0 : 0.2);
+            del[r] += ds;
+            der[u] += ds;
+            for (int c = 0; c < dout; ++c) dY[u * dout + c] += al * gv[c];
+        }
+    }
+    for (size_t r = 0; r < n; ++r)
+        for (int c = 0; c < dout; ++c) {
+            double x = dY[r * dout + c] + der[r] * W[(size_t)(din + 1) * dout + c];
+            if (r < n_in) x += del[r] * W[(size_t)din * dout + c];
+            dY[r * dout + c] = st(x);
+        }
+    for (size_t r = 0; r < n; ++r)
+        for (int c = 0; c < dout; ++c) {
+            const double d = dY[r * dout + c];
+            for (int k = 0; k < din; ++k) g[(size_t)k * dout + c] += X[r * din + k] * d;
+            if (r < n_in) g[(size_t)din * dout + c] += del[r] * Y[r * dout + c];
+            g[(size_t)(din + 1) * dout + c] += der[r] * Y[r * dout + c];
+        }
+    if (!dX) return;
+    dX->assign(n * din, 0.0);
+    for (size_t r = 0; r < n; ++r)
+        for (int k = 0; k < din; ++k) {
+            double x = 0.0;
+            for (int c = 0; c < dout; ++c) x += dY[r * dout + c] * Wq[(size_t)k * dout + c];
+            x = st(x);
+            if (o.drop > 0.0) {
+                const int32_t u = (r < n_in) ? P.V[r] : P.U[r - n_in];
+                x = st(x * drop_factor(o, u, k, l));
+            }
+            (*dX)[r * din + k] = x;
+        }
+}
+
+// ---------------------------------------------------------------------------------------------
 // One epoch of Algorithm 1 for all partitions (l.8-14).
 // W[l] (l=0..L-1) is row-major: SAGE (2*d_in) x d_out with rows [0,d_in) multiplying z (R14);
 // GCN d_in x d_out.
@@ -365,6 +503,11 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                     const int32_t u = (r < n_in) ? P.V[r] : P.U[r - n_in];
                     for (int k = 0; k < din; ++k) X[r * din + k] = st(X[r * din + k] * drop_factor(o, u, k, l));
                 }
+            if (o.kind == KIND_GAT) {   // f4 / R45: the attention layer on the same sampled graph
+                gat_forward(o, i, idx[i].row, X, din, dout, Wq[l - 1], W[l - 1], st, PREs[l][i]);
+                Zs[l][i].assign(n_in * din, 0.0);   // GAT has no separate aggregation tensor Z
+                continue;
+            }
             // l.10: GCN^(l)(H_i, [H; H_U], w)
             std::vector<double>& Zl = Zs[l][i];
             Zl.assign(n_in * din, 0.0);
@@ -543,9 +686,15 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                     dpre[r * dout + c] = (l < L) ? (PREs[l][i][r * dout + c] > 0.0 ? g : 0.0) : st(g);
                 }
             // weight gradient of this partition
-            const int wrows = (o.kind == KIND_SAGE) ? 2 * din : din;
+            const int wrows = (o.kind == KIND_SAGE) ? 2 * din : (o.kind == KIND_GAT) ? din + 2 : din;
             std::vector<double>& g = gW[i][l - 1];
             g.assign((size_t)wrows * dout, 0.0);
+            if (o.kind == KIND_GAT) {
+                std::vector<double>& dX = dXs[i];
+                gat_backward(o, i, idx[i].row, Xs[l][i], din, dout, Wq[l - 1], W[l - 1], st, dpre, g,
+                             l > 1 ? &dX : nullptr, l);
+                continue;
+            }
             const bool tf = o.bf16 && o.kind == KIND_SAGE && ((o.tf_mask >> (l - 1)) & 1u);
             if (tf) {
                 // R42 emulation: dY_u = c_u Σ_{v: u in N(v)} [dPre_v / deg_G(v)] on every stacked row, the bracket
@@ -845,7 +994,7 @@ int32_t orc_epoch(void* h, double* const* W, double lr, double* const* G, double
     std::vector<std::vector<double>> Wv(o.L);
     for (int l = 0; l < o.L; ++l) {
         int din = o.dims[l], dout = o.dims[l + 1];
-        size_t rows = (o.kind == KIND_SAGE) ? 2 * (size_t)din : (size_t)din;
+        size_t rows = (o.kind == KIND_SAGE) ? 2 * (size_t)din : (o.kind == KIND_GAT) ? (size_t)din + 2 : (size_t)din;
         Wv[l].assign(W[l], W[l] + rows * dout);
     }
     int rc = epoch(o, Wv, lr, loss, acc);

@@ -76,3 +76,41 @@ def forward_backward(indptr, indices, part_of, kept, p, layer, X, labels, Ws, ma
     return dict(loss=float(loss.detach()), acc=acc, H=[h.detach().numpy() for h in Hs], Z=[z.detach().numpy() for z in Zs],
                 dH=[None] + [h.grad.numpy() if h.grad is not None else None for h in Hs[1:]],
                 dW=[w.grad.numpy() for w in W])
+
+
+def gat_forward_backward(indptr, indices, part_of, kept, X, labels, Ws):
+    """f4 / R45 brute force: dense masked GAT (one head, self loops, LeakyReLU 0.2, softmax over the sampled
+    neighbourhood), W^l = [W ; a_l ; a_r] ((d_in + 2) x d_out), torch autograd for the backward."""
+    N = len(indptr) - 1
+    mask = np.zeros((N, N), bool)
+    for v in range(N):
+        i = part_of[v]
+        mask[v, v] = True
+        for u in indices[indptr[v]:indptr[v + 1]]:
+            if part_of[u] == i or u in kept[i]:
+                mask[v, u] = True
+    Mk = torch.tensor(mask)
+    H = torch.tensor(np.asarray(X, np.float64))
+    W = [torch.tensor(np.asarray(w, np.float64), requires_grad=True) for w in Ws]
+    y = torch.tensor(np.asarray(labels, np.int64))
+    Hs = [H]
+    for l in range(len(W)):
+        din = Hs[-1].shape[1]
+        Y = Hs[-1] @ W[l][:din]
+        el = Y @ W[l][din]
+        er = Y @ W[l][din + 1]
+        E = torch.nn.functional.leaky_relu(el[:, None] + er[None, :], 0.2)
+        E = E.masked_fill(~Mk, float("-inf"))
+        A = torch.softmax(E, dim=1)
+        pre = A @ Y
+        Hn = torch.relu(pre) if l < len(W) - 1 else pre
+        Hn.retain_grad()
+        Hs.append(Hn)
+    train = y >= 0
+    ntr = int(train.sum())
+    logits = Hs[-1]
+    loss = torch.nn.functional.cross_entropy(logits[train], y[train], reduction="sum") / ntr
+    loss.backward()
+    return dict(loss=float(loss.detach()), H=[h.detach().numpy() for h in Hs],
+                dH=[None] + [h.grad.numpy() if h.grad is not None else None for h in Hs[1:]],
+                dW=[w.grad.numpy() for w in W])

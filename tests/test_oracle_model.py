@@ -388,3 +388,40 @@ def test_multilabel_closed_forms():
     o.set_multilabel(None)
     loss, acc, G = o.epoch([w.copy() for w in Wz], 0.0)
     assert abs(loss - math.log(dims[-1])) < 1e-12
+
+
+# ---------------- f4: GAT layer (Table tab:gat; reading R45) ----------------
+@pytest.mark.parametrize("seed,m,p", [(91, 3, 0.5), (92, 1, 1.0), (93, 4, 0.0), (94, 2, 0.3)])
+def test_gat_dense_bruteforce(seed, m, p):
+    from dense_ref import gat_forward_backward
+    dims = [3, 5, 4, 3]
+    ip, ix, part, X, y, _ = random_case(seed, m=m, layer=1, dims=tuple(dims))
+    rng = np.random.default_rng(seed)
+    Ws = [rng.uniform(-1, 1, (dims[l] + 2, dims[l + 1])) for l in range(3)]
+    o = O.Oracle(ip, ix, part, m, dims, 2, X, y)
+    o.sample(p, 77, seed)
+    kept = [set(int(u) for u in o.list(O.U_LIST, r)) for r in range(m)]
+    ref = gat_forward_backward(ip, ix, part, kept, X, y, Ws)
+    loss, acc, G = o.epoch([w.copy() for w in Ws], 0.0)
+    assert abs(loss - ref["loss"]) <= 1e-12 * max(1.0, abs(ref["loss"]))
+    for l in range(1, 4):
+        np.testing.assert_allclose(o.tensor(O.T_H, l), ref["H"][l], rtol=1e-11, atol=1e-12)
+    for l in range(1, 3):
+        np.testing.assert_allclose(o.tensor(O.T_DH, l), ref["dH"][l], rtol=1e-9, atol=1e-13)
+    for g, r in zip(G, ref["dW"]):
+        np.testing.assert_allclose(g, r, rtol=1e-9, atol=1e-13)
+
+
+def test_gat_single_neighbour_closed_form():
+    """a node whose only sampled neighbour is itself gets alpha_vv = 1: pre_v = x_v W (p = 0, isolated partitions)"""
+    dims = [3, 2]
+    ip, ix, part, X, y, _ = random_case(95, m=3, layer=1, dims=tuple(dims))
+    W = [np.random.default_rng(1).uniform(-1, 1, (5, 2))]
+    o = O.Oracle(ip, ix, part, 3, dims, 2, X, y)
+    o.sample(0.0, 1, 1)
+    o.epoch([W[0].copy()], 0.0)
+    H1 = o.tensor(O.T_H, 1)
+    alone = [v for v in range(len(ip) - 1) if np.all(part[ix[ip[v]:ip[v + 1]]] != part[v])]
+    assert len(alone) >= 3
+    for v in alone:
+        np.testing.assert_allclose(H1[v], X[v].astype(np.float64) @ W[0][:3], rtol=1e-12, atol=1e-14)
