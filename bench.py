@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--q", type=float, default=None,
                     help="edge keep probability; default matched to BNS p (P:681): BES q = p, "
                          "DropEdge q = 1 - (1-p) cross/nnz")
+    ap.add_argument("--model", default="sage", choices=["sage", "gat"],
+                    help="gat: the paper's 2-layer GAT ablation (f4, Table tab:gat, PAPER.md:691-709; R45)")
     ap.add_argument("--multilabel", action="store_true",
                     help="f4: sigmoid BCE + F1-micro on seeded multi-hot targets (the Yelp task, PAPER.md:384)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -294,6 +296,9 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     shape = I.SHAPES[args.config]
     shape.p = args.p
+    if args.model == "gat":
+        import dataclasses
+        shape = dataclasses.replace(shape, layer=I.LAYER_GAT, L=2)
     m = world
     prec = bns.BNS_BF16 if args.prec == "bf16" else bns.BNS_FP32
     t_setup = time.perf_counter()
@@ -414,7 +419,12 @@ def run_ours(args):
         peaks = measured_peaks()
         s = 2 if prec == bns.BNS_BF16 else 4
         dp = [((d + 7) // 8) * 8 for d in shape.dims]
-        fwd_b, bwd_b = spmm_bytes(dp, shape.L, cnt["n_in"], cnt["n_halo"], cnt["nnz_kept"], s, ctx.tf_layers())
+        if shape.layer == I.LAYER_GAT:
+            # one gather of Y at d_out per layer forward; three in the backward (edge ds forward / transposed, dY)
+            fwd_b = sum(cnt["nnz_kept"] * (dp[l + 1] * s + 4) + cnt["n_in"] * dp[l + 1] * s for l in range(shape.L))
+            bwd_b = 3 * fwd_b
+        else:
+            fwd_b, bwd_b = spmm_bytes(dp, shape.L, cnt["n_in"], cnt["n_halo"], cnt["nnz_kept"], s, ctx.tf_layers())
         spmm_ms = ph["spmm_fwd"] + ph["spmm_bwd"]
         hbm_peak = peaks.get("hbm_gbs", 6650.0)
         achieved = (fwd_b + bwd_b) / (spmm_ms * 1e-3) / 1e9 if spmm_ms > 0 else None
@@ -429,7 +439,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16" if prec == bns.BNS_BF16 else "f32",
             "data": "synthetic: R-MAT graph (Graph500 a,b,c=.57,.19,.19), Philox features/labels, Glorot weights",
-            "config": {"workload": f"{shape.name}-shaped R-MAT N={shape.N} nnz={int(indptr[-1])}, GraphSAGE-mean "
+            "config": {"workload": f"{shape.name}-shaped R-MAT N={shape.N} nnz={int(indptr[-1])}, "
+                                   f"{'GAT (1 head)' if shape.layer == I.LAYER_GAT else 'GraphSAGE-mean'} "
                                    f"{shape.L} layers hidden {shape.hidden}, d0={shape.d0}, C={shape.C}, p={args.p}, "
                                    f"m={world} partitions ({args.partition})",
                        "global_batch": "full graph", "parallelism": f"partition-parallel m={world}",

@@ -46,7 +46,10 @@ typedef enum {
 
 typedef enum {
     BNS_LAYER_SAGE_MEAN = 0,  /* GraphSAGE-mean: h_v = σ(W · CONCAT(z_v, h_v)), z_v = mean aggregate */
-    BNS_LAYER_GCN = 1         /* GCN: Z = P H W, P = D~^-1/2 (A+I) D~^-1/2 (App. A) */
+    BNS_LAYER_GCN = 1,        /* GCN: Z = P H W, P = D~^-1/2 (A+I) D~^-1/2 (App. A) */
+    BNS_LAYER_GAT = 2         /* f4 / R45: one-head GAT (Table tab:gat): Y = H W, e_vu =
+                                 LeakyReLU_0.2(Y_v a_l + Y_u a_r), alpha = softmax over the sampled neighbours and v
+                                 itself, h'_v = σ(Σ_u alpha_vu Y_u); weights (d_in + 2) x d_out rows [W ; a_l ; a_r] */
 } bns_layer;
 
 typedef enum {
@@ -141,7 +144,8 @@ bns_status bns_sample_edges(bns_ctx* ctx, int32_t sampler, double q, uint64_t se
 
 /* Alg.1 l.8-14 with the draw of the last bns_sample_boundary (or bns_sample_edges).
  *   weights[l], l < L: fp32 row-major, SAGE (2*dims[l]) x dims[l+1] (rows [0,dims[l]) multiply z_v, R14),
- *       GCN dims[l] x dims[l+1].  Device pointers on cfg.device (updated in place: W <- W - lr*g) or host
+ *       GCN dims[l] x dims[l+1], GAT (dims[l] + 2) x dims[l+1] ([W ; a_l ; a_r]).  Device pointers on cfg.device
+ *       (updated in place: W <- W - lr*g) or host
  *       pointers (copied in and out inside the call).
  *   grads[l]: same shapes, out: the all-reduced gradient g (identical on every rank); may be NULL.
  *   loss: out, global mean cross-entropy over train nodes (R8); acc: out, global train accuracy (R18, R22).

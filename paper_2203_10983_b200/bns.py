@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BNS_LIB") or os.path.join(_HERE, "libbns.so")   # BNS_LIB: A/B builds only
 
 BNS_OK, BNS_ERR_INVALID, BNS_ERR_RUNTIME, BNS_ERR_STATE, BNS_ERR_OOM, BNS_ERR_NONFINITE = range(6)
-BNS_LAYER_SAGE_MEAN, BNS_LAYER_GCN = 0, 1
+BNS_LAYER_SAGE_MEAN, BNS_LAYER_GCN, BNS_LAYER_GAT = 0, 1, 2
 BNS_FP32, BNS_BF16 = 0, 1
 BNS_TRANSPORT_NONE, BNS_TRANSPORT_NCCL, BNS_TRANSPORT_LOCAL, BNS_TRANSPORT_NULL_EMULATE = 0, 1, 2, 3
 BNS_PLAN_ONLY, BNS_DEBUG_EXCHANGE_INDICES, BNS_TIMING, BNS_RETAIN_GRADS, BNS_NO_TRANSFORM_FIRST = 0x1, 0x2, 0x4, 0x8, 0x10

@@ -67,6 +67,12 @@ T* upload(Ctx& c, const std::vector<T>& v) {
 
 size_t tsize(const Ctx& c) { return c.prec == BNS_BF16 ? 2 : 4; }
 
+// logical rows of layer l's weight at the ABI: SAGE 2 d_in, GCN d_in, GAT d_in + 2 ([W ; a_l ; a_r])
+int64_t wlogical_rows(const Ctx& c, int l) {
+    return c.layer == BNS_LAYER_SAGE_MEAN ? 2 * (int64_t)c.dims[l]
+           : c.layer == BNS_LAYER_GAT ? (int64_t)c.dims[l] + 2 : (int64_t)c.dims[l];
+}
+
 void validate(const bns_config* cfg, int64_t N, const int64_t* indptr, const int32_t* indices, const int32_t* part_of) {
     if (!cfg) throw Error(BNS_ERR_INVALID, "cfg is NULL");
     if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) throw Error(BNS_ERR_INVALID, "bad rank/world");
@@ -74,7 +80,8 @@ void validate(const bns_config* cfg, int64_t N, const int64_t* indptr, const int
     for (int l = 0; l <= cfg->num_layers; ++l)
         if (cfg->dims[l] <= 0) throw Error(BNS_ERR_INVALID, "dims must be positive");
     if (cfg->dims[cfg->num_layers] > 256) throw Error(BNS_ERR_INVALID, "at most 256 classes (dims[L])");
-    if (cfg->layer != BNS_LAYER_SAGE_MEAN && cfg->layer != BNS_LAYER_GCN) throw Error(BNS_ERR_INVALID, "bad layer");
+    if (cfg->layer != BNS_LAYER_SAGE_MEAN && cfg->layer != BNS_LAYER_GCN && cfg->layer != BNS_LAYER_GAT)
+        throw Error(BNS_ERR_INVALID, "bad layer");
     if (cfg->precision != BNS_FP32 && cfg->precision != BNS_BF16) throw Error(BNS_ERR_INVALID, "bad precision");
     if (cfg->world > 1 && cfg->transport != BNS_TRANSPORT_NCCL && cfg->transport != BNS_TRANSPORT_LOCAL &&
         cfg->transport != BNS_TRANSPORT_NULL_EMULATE && !(cfg->flags & BNS_PLAN_ONLY))
@@ -311,11 +318,13 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     }
     int64_t wmax = 0, wlog = 0;
     for (int l = 0; l < L; ++l) {
-        c.wrows[l] = (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * (int64_t)c.dp[l];
+        // padded rows: SAGE [z-half ; h-half] 2 dp; GCN dp; GAT [W (dp) ; a_l ; a_r ; 6 zero rows]
+        c.wrows[l] = c.layer == BNS_LAYER_SAGE_MEAN ? 2 * (int64_t)c.dp[l]
+                     : c.layer == BNS_LAYER_GAT ? (int64_t)c.dp[l] + 8 : (int64_t)c.dp[l];
         c.wcols[l] = c.dp[l + 1];
         c.goff[l + 1] = c.goff[l] + c.wrows[l] * c.wcols[l];
         wmax = std::max(wmax, c.wrows[l] * c.wcols[l]);
-        wlog += (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * (int64_t)c.dims[l] * c.dims[l + 1];
+        wlog += wlogical_rows(c, l) * c.dims[l + 1];
         c.Wpad[l] = static_cast<float*>(dalloc(c, c.wrows[l] * c.wcols[l] * sizeof(float)));
         c.Wt[l] = (c.prec == BNS_BF16) ? dalloc(c, c.wrows[l] * c.wcols[l] * 2) : (void*)c.Wpad[l];
         c.wkw[l] = (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * ((int64_t)(c.dp[l] + 63) / 64 * 64);
@@ -334,7 +343,13 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
                 c.Wcat[l] = dalloc(c, (size_t)c.dp[l] * 2 * c.dp[l + 1] * ts);
                 if (c.use_tc) c.WTtf[l] = dalloc(c, (size_t)2 * c.dp[l + 1] * ((c.dp[l] + 63) / 64 * 64) * 2);
             }
-    if (c.tf_mask) c.d_tfy = dalloc(c, (size_t)(P.n_in + c.halo_cap) * tfw * ts);
+    if (c.layer == BNS_LAYER_GAT) {   // f4 / R45: Y buffer, per-layer attention scalars, dY
+        for (int l = 0; l < L; ++l) tfw = std::max<int64_t>(tfw, c.dp[l + 1]);
+        const int64_t R = P.n_in + c.halo_cap;
+        c.d_gat = static_cast<float*>(dalloc(c, (size_t)(2 * L * R + 2 * L * P.n_in + 3 * P.n_in + R + 16) * sizeof(float)));
+        c.d_gat_dy = dalloc(c, (size_t)R * c.maxd * ts);
+    }
+    if (c.tf_mask || c.layer == BNS_LAYER_GAT) c.d_tfy = dalloc(c, (size_t)(P.n_in + c.halo_cap) * tfw * ts);
     c.gflat_n = c.goff[L];
     c.d_gflat = static_cast<float*>(dalloc(c, c.gflat_n * sizeof(float)));
     c.splitk_cap = 32 * wmax;
@@ -502,7 +517,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     std::vector<int64_t> wl(L);
     int64_t off = 0;
     for (int l = 0; l < L; ++l) {
-        wl[l] = (sage ? 2 : 1) * (int64_t)c.dims[l] * c.dims[l + 1];
+        wl[l] = wlogical_rows(c, l) * c.dims[l + 1];
         if (host_w) {
             W[l] = c.d_hostw + off;
             G[l] = c.d_hostw + c.hostw_n + off;
@@ -520,6 +535,16 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     }
     const Seg* fsegs = c.fwd_mode == 0 ? c.d_seg_static_fwd : (c.fwd_mode == 1 ? c.d_seg_bwd : c.d_seg_fwd);
     const int32_t* fcol = c.fwd_mode == 0 ? c.d_static_col : (c.fwd_mode == 1 ? c.d_tcol : c.d_ind_col);
+    const int64_t* fsplit = c.fwd_mode == 0 ? c.d_split_sf : (c.fwd_mode == 1 ? c.d_split_bwd : c.d_split_fwd);
+    const bool ebw = c.sampler != BNS_SAMPLER_BNS;
+    const Seg* bsegs = ebw ? c.d_eseg_bwd : c.d_seg_bwd;
+    const int32_t* bcol = ebw ? c.d_ind_tcol : c.d_tcol;
+    const int64_t* bsplit = ebw ? c.d_esplit_bwd : c.d_split_bwd;
+    // f4 / R45 GAT scalars of layer l (1-based): el, er over the stacked rows, softmax max / 1/Σ over inner rows
+    const int64_t gR = n_in + c.halo_cap;
+    auto gat_el = [&](int l) { return c.d_gat + (int64_t)(l - 1) * 2 * gR; };
+    auto gat_m = [&](int l) { return c.d_gat + (int64_t)2 * L * gR + (int64_t)(l - 1) * 2 * n_in; };
+    float* gat_tail = c.d_gat ? c.d_gat + (int64_t)2 * L * gR + (int64_t)2 * L * n_in : nullptr;   // c, selfds, del, der
     const int32_t* S_local = c.d_cand_out + c.n_halo;
     const bool dropout = c.drop > 0.0;
     if (dropout) launch_halo_gid(c);
@@ -545,6 +570,55 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             PhaseTimer t(c, BNS_PH_UPDATE);
             launch_dropout(c, Hin, c.Xd[l - 1], n_in + c.n_halo, din, l);
             Hin = c.Xd[l - 1];
+        }
+        if (c.layer == BNS_LAYER_GAT) {
+            // f4 / R45: Y = Hin W on every stacked row (tcgen05), el / er, softmax statistics, then
+            // pre_v = Σ_u alpha_vu Y_u + alpha_vv Y_v with ReLU (hidden) or fp32 logits (last) in the SpMM epilogue
+            const bool last = (l == L);
+            const int64_t rows = n_in + c.n_halo;
+            float* el = gat_el(l);
+            float* er = el + gR;
+            float* gm = gat_m(l);
+            float* ginv = gm + n_in;
+            const float* al = c.Wpad[l - 1] + din * dout;
+            {
+                PhaseTimer t(c, BNS_PH_GEMM_FWD);
+                if (c.use_tc)
+                    gemm_fwd_tc(c, rows, dout, Hin, din, din, nullptr, 0, din, c.WT[l - 1], c.wkw[l - 1], c.d_tfy,
+                                dout, false, false);
+                else
+                    gemm_fwd(c, rows, dout, Hin, din, din, nullptr, 0, din, c.Wt[l - 1], dout, c.d_tfy, dout, false,
+                             false);
+            }
+            PhaseTimer t(c, BNS_PH_SPMM_FWD);
+            launch_gat_scores(c, c.d_tfy, dout, rows, (int32_t)dout, al, al + dout, el, er);
+            launch_gat_stats(c, fsegs, c.n_seg_fwd, fcol, fsplit, c.n_split_fwd, el, er, gm, ginv);
+            SpmmArgs a{};
+            a.mode = GAT_FWD;
+            a.segs = fsegs;
+            a.n_segs = c.n_seg_fwd;
+            a.col = fcol;
+            a.src = c.d_tfy;
+            a.ld_src = dout;
+            a.self = c.d_tfy;
+            a.ld_self = dout;
+            a.out = last ? (void*)c.d_logits : c.H[l];
+            a.ld_out = dout;
+            a.d = (int32_t)dout;
+            a.n_in = n_in;
+            a.inv_p = 1.f;
+            a.sc = 3;
+            a.gat_el = el;
+            a.gat_er = er;
+            a.gat_m = gm;
+            a.gat_inv = ginv;
+            a.partial = c.d_partial;
+            a.split = fsplit;
+            a.n_split = c.n_split_fwd;
+            a.relu = last ? 0 : 1;
+            a.out_f32 = last ? 1 : 0;
+            launch_spmm(c, a);
+            continue;
         }
         if ((c.tf_mask >> (l - 1)) & 1u) {
             // R42 transform-first: [Y | S] = Hin [W_top | W_bot] on every stacked row, then
@@ -643,7 +717,75 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             launch_relu_mask(c, c.d_dx, c.H[l], dout, n_in, (int32_t)dout, c.d_dpre, tfl ? c.d_deg_in : nullptr,
                              tfl ? c.d_dxcat : nullptr);
         }
-        if ((c.tf_mask >> (l - 1)) & 1u) {
+        if (c.layer == BNS_LAYER_GAT) {
+            // f4 / R45 backward (g = dPre): c_v = g_v . pre_v, del_v / der_u = Σ ds over the forward / transposed
+            // segments, dY by the weighted SpMM^T, dW = Hin^T dY, da_l = Σ del Y, da_r = Σ der Y, dX = dY W^T
+            const bool last = (l == L);
+            const int64_t rows = n_in + c.n_halo;
+            float* el = gat_el(l);
+            float* er = el + gR;
+            float* gm = gat_m(l);
+            float* ginv = gm + n_in;
+            float* cdot = gat_tail;
+            float* selfds = cdot + n_in;
+            float* del = selfds + n_in;
+            float* der = del + n_in;
+            const float* al = c.Wpad[l - 1] + din * dout;
+            float* g = c.d_gflat + c.goff[l - 1];
+            {
+                PhaseTimer t(c, BNS_PH_GEMM_BWD);   // Y again (same GEMM, same values)
+                if (c.use_tc)
+                    gemm_fwd_tc(c, rows, dout, Hin, din, din, nullptr, 0, din, c.WT[l - 1], c.wkw[l - 1], c.d_tfy,
+                                dout, false, false);
+                else
+                    gemm_fwd(c, rows, dout, Hin, din, din, nullptr, 0, din, c.Wt[l - 1], dout, c.d_tfy, dout, false,
+                             false);
+            }
+            {
+                PhaseTimer t(c, BNS_PH_SPMM_BWD);
+                launch_gat_rowdots(c, c.d_dpre, last ? (const void*)c.d_logits : c.H[l], last, c.d_tfy, dout,
+                                   (int32_t)dout, el, er, gm, ginv, cdot, selfds);
+                launch_gat_edge_ds(c, 0, fsegs, c.n_seg_fwd, fcol, fsplit, c.n_split_fwd, c.d_dpre, c.d_tfy, dout,
+                                   (int32_t)dout, el, er, gm, ginv, cdot, selfds, del);
+                launch_gat_edge_ds(c, 1, bsegs, c.n_seg_bwd, bcol, bsplit, c.n_split_bwd, c.d_dpre, c.d_tfy, dout,
+                                   (int32_t)dout, el, er, gm, ginv, cdot, selfds, der);
+                SpmmArgs a{};
+                a.mode = GAT_BWD;
+                a.segs = bsegs;
+                a.n_segs = c.n_seg_bwd;
+                a.col = bcol;
+                a.src = c.d_dpre;
+                a.ld_src = dout;
+                a.out = c.d_gat_dy;
+                a.ld_out = dout;
+                a.d = (int32_t)dout;
+                a.n_in = n_in;
+                a.inv_p = 1.f;
+                a.sc = 4;
+                a.gat_el = el;
+                a.gat_er = er;
+                a.gat_m = gm;
+                a.gat_inv = ginv;
+                a.gat_al = al;
+                a.gat_ar = al + dout;
+                a.gat_del = del;
+                a.gat_der = der;
+                a.partial = c.d_partial;
+                a.split = bsplit;
+                a.n_split = c.n_split_bwd;
+                launch_spmm(c, a);
+            }
+            {
+                PhaseTimer t(c, BNS_PH_GEMM_BWD);
+                auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
+                auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
+                wgrad(c, rows, din, dout, Hin, din, c.d_gat_dy, dout, g, dout);
+                launch_gat_da(c, c.d_tfy, dout, (int32_t)dout, del, n_in, g + din * dout);
+                launch_gat_da(c, c.d_tfy, dout, (int32_t)dout, der, rows, g + (din + 1) * dout);
+                if (l > 1) dxg(c, rows, din, dout, c.d_gat_dy, dout, c.Wt[l - 1], dout, c.d_dx, din, nullptr, 0);
+            }
+            if (l == 1) break;   // R29
+        } else if ((c.tf_mask >> (l - 1)) & 1u) {
             // R42 transform-first backward: dY_u = c_u Σ_v dPre_v / deg_G(v) over every stacked row (SpMM^T at the
             // narrow width), dW_top = Hin^T dY, dW_bot = Hin_inner^T dPre, dX = [dY | dPre] [W_top | W_bot]^T
             const bool eb = c.sampler != BNS_SAMPLER_BNS;
@@ -1046,8 +1188,8 @@ bns_status bns_query(bns_ctx* h, int32_t what, int32_t layer, void* dst, int64_t
             case BNS_Q_Z: {
                 need_sample();
                 if (layer < 1 || layer > L) throw Error(BNS_ERR_INVALID, "layer out of range");
-                if ((c.tf_mask >> (layer - 1)) & 1u)
-                    throw Error(BNS_ERR_STATE, "layer runs transform-first (R42): Z is not materialised");
+                if (((c.tf_mask >> (layer - 1)) & 1u) || c.layer == BNS_LAYER_GAT)
+                    throw Error(BNS_ERR_STATE, "layer runs transform-first (R42) or is GAT: Z is not materialised");
                 rows_f32(c.Z[layer], P.n_in, c.dp[layer - 1], c.dims[layer - 1], false);
                 break;
             }

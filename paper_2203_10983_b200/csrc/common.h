@@ -138,6 +138,9 @@ struct Ctx {
     int64_t* d_split_fwd = nullptr;                                  // per-epoch induced forward segments
     int64_t n_split_fwd = 0, n_split_bwd = 0;                        // this epoch's list lengths
     float* d_cscale = nullptr;     // per-column scale (GCN forward)
+    float* d_gat = nullptr;          // f4 / R45 GAT scalars: per layer el, er (stacked rows) and softmax max / 1/Σ
+                                     // (inner rows), then c, selfds, del (inner), der (stacked)
+    void* d_gat_dy = nullptr;        // GAT dY, (n_in + halo_cap) x maxd storage
     bool multilabel = false;         // f4 / R44: sigmoid BCE + F1-micro (bns_set_multilabel)
     uint8_t* d_targets = nullptr;    // n_in x C multi-hot targets
     void* d_x0cache = nullptr;       // f1 / R43: X^(0) rows of every boundary node, B_i order (BNS_CACHE_INPUT_HALO)

@@ -20,7 +20,7 @@ int64_t build_static_segments(Ctx& c, const int64_t* d_ptr, int64_t rows, int64_
 void scan_i32(Ctx& c, const int32_t* in, int64_t* out, int64_t n, int64_t* d_total);
 
 // a6 / a10: segment SpMM (spmm.cu)
-enum SpmmMode { SAGE_FWD = 0, GCN_FWD = 1, SAGE_BWD = 2, GCN_BWD = 3, SAGE_FWD_TF = 4 };
+enum SpmmMode { SAGE_FWD = 0, GCN_FWD = 1, SAGE_BWD = 2, GCN_BWD = 3, SAGE_FWD_TF = 4, GAT_FWD = 5, GAT_BWD = 6 };
 struct SpmmArgs {
     int mode;
     const Seg* segs; int64_t n_segs;
@@ -40,9 +40,26 @@ struct SpmmArgs {
     const int64_t* split; int64_t n_split;  // first-segment index of every split (hub) row -> in-order fixup
     int sc = -1;                          // per-edge column scale override (-1: by mode; 2: cscale[col])
     int relu = 0;                         // SAGE_FWD_TF: ReLU in the epilogue
-    int out_f32 = 0;                      // SAGE_FWD_TF: fp32 output (logits) instead of the storage type
+    int out_f32 = 0;                      // SAGE_FWD_TF / GAT_FWD: fp32 output (logits) instead of the storage type
+    // f4 / R45 GAT: per-node attention scores and softmax statistics (fp32), attention vectors a_l / a_r (dout),
+    // del / der (backward)
+    const float *gat_el = nullptr, *gat_er = nullptr, *gat_m = nullptr, *gat_inv = nullptr;
+    const float *gat_al = nullptr, *gat_ar = nullptr, *gat_del = nullptr, *gat_der = nullptr;
 };
 void launch_spmm(Ctx& c, const SpmmArgs& a);
+
+// f4 / R45 GAT pieces (gat.cu)
+void launch_gat_scores(Ctx& c, const void* Y, int64_t ld, int64_t rows, int32_t d, const float* al, const float* ar,
+                       float* el, float* er);
+void launch_gat_stats(Ctx& c, const Seg* segs, int64_t n_segs, const int32_t* col, const int64_t* split,
+                      int64_t n_split, const float* el, const float* er, float* m, float* inv);
+void launch_gat_rowdots(Ctx& c, const void* g, const void* out, bool out_f32, const void* Y, int64_t ld, int32_t d,
+                        const float* el, const float* er, const float* m, const float* inv, float* cdot, float* selfds);
+void launch_gat_edge_ds(Ctx& c, int dir, const Seg* segs, int64_t n_segs, const int32_t* col, const int64_t* split,
+                        int64_t n_split, const void* g, const void* Y, int64_t ld, int32_t d, const float* el,
+                        const float* er, const float* m, const float* inv, const float* cdot, const float* selfds,
+                        float* out);
+void launch_gat_da(Ctx& c, const void* Y, int64_t ld, int32_t d, const float* w, int64_t rows, float* out);
 
 // a7 / a9: GEMMs (gemm_simt.cu; tcgen05 in gemm_tc.cu)
 // C[M x N] = [A0 | A1] (M x (K0+K1), row-major, lda0/lda1) * B (K x N row-major, ldb); epilogue ReLU or none;

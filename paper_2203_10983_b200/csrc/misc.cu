@@ -393,11 +393,18 @@ void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t
 // ---------------------------------------------------------------------------------------------
 // weights: caller layout (logical, SAGE halves [z-rows ; h-rows]) <-> padded internal layout
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ int64_t logical_row(int64_t pr, int sage, int64_t din, int64_t dpin) {
-    if (!sage) return pr < din ? pr : -1;
+// kind: 0 SAGE (rows [z-half ; h-half], 2 din), 1 GCN (din), 2 GAT ([W ; a_l ; a_r], din + 2)
+__device__ __forceinline__ int64_t logical_row(int64_t pr, int kind, int64_t din, int64_t dpin) {
+    if (kind == 1) return pr < din ? pr : -1;
     if (pr < dpin) return pr < din ? pr : -1;
     int64_t q = pr - dpin;
-    return q < din ? din + q : -1;
+    return q < (kind == 0 ? din : 2) ? din + q : -1;
+}
+__host__ __device__ __forceinline__ int64_t logical_rows(int kind, int64_t din) {
+    return kind == 0 ? 2 * din : kind == 2 ? din + 2 : din;
+}
+__device__ __forceinline__ int64_t padded_row(int64_t lr, int kind, int64_t din, int64_t dpin) {
+    return (kind != 1 && lr >= din) ? dpin + (lr - din) : lr;
 }
 
 // all layers in one launch: blockIdx.y = layer (blockIdx.y >= L: the W^T copy of layer y - L)
@@ -411,7 +418,7 @@ struct WDesc {
     const float* gpad[kMaxLayers];
     int64_t rows_p[kMaxLayers], cols_p[kMaxLayers], din[kMaxLayers], dpin[kMaxLayers], dout[kMaxLayers];
     int64_t K64[kMaxLayers], Kw[kMaxLayers];
-    int L, sage, tc;
+    int L, kind, tc;
 };
 
 template <typename T>
@@ -423,7 +430,7 @@ __global__ void k_wpack_all(const WDesc d) {
     if (y < d.L) {
         if (t >= d.rows_p[l] * cp) return;
         const int64_t pr = t / cp, pc = t % cp;
-        const int64_t lr = logical_row(pr, d.sage, d.din[l], d.dpin[l]);
+        const int64_t lr = logical_row(pr, d.kind, d.din[l], d.dpin[l]);
         const float v = (lr >= 0 && pc < d.dout[l]) ? d.W[l][lr * d.dout[l] + pc] : 0.f;
         d.Wp[l][t] = v;
         if (d.Wt[l] != (void*)d.Wp[l]) static_cast<T*>(d.Wt[l])[t] = from_f<T>(v);
@@ -434,7 +441,7 @@ __global__ void k_wpack_all(const WDesc d) {
         const int64_t half = kw / d.K64[l], j = kw % d.K64[l];
         float v = 0.f;
         if (j < d.dpin[l]) {
-            const int64_t lr = logical_row(half * d.dpin[l] + j, d.sage, d.din[l], d.dpin[l]);
+            const int64_t lr = logical_row(half * d.dpin[l] + j, d.kind, d.din[l], d.dpin[l]);
             if (lr >= 0 && n < d.dout[l]) v = d.W[l][lr * d.dout[l] + n];
         }
         static_cast<__nv_bfloat16*>(d.WT[l])[t] = __float2bfloat16_rn(v);
@@ -445,7 +452,7 @@ static WDesc make_desc(Ctx& c, float* const* W, float* const* G) {
     if (c.L > kMaxLayers) throw Error(BNS_ERR_INVALID, "too many layers");
     WDesc d{};
     d.L = c.L;
-    d.sage = c.layer == BNS_LAYER_SAGE_MEAN;
+    d.kind = c.layer == BNS_LAYER_SAGE_MEAN ? 0 : c.layer == BNS_LAYER_GCN ? 1 : 2;
     d.tc = c.use_tc ? 1 : 0;
     for (int l = 0; l < c.L; ++l) {
         d.W[l] = W[l];
@@ -518,12 +525,12 @@ void launch_wpack_tf(Ctx& c) {
 __global__ void k_sgd_all(const WDesc d, float lr, const double* __restrict__ scal, int32_t* __restrict__ nonfinite) {
     const int l = blockIdx.y;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t rows_l = (d.sage ? 2 : 1) * d.din[l], dout = d.dout[l];
+    const int64_t rows_l = logical_rows(d.kind, d.din[l]), dout = d.dout[l];
     if (t >= rows_l * dout) return;
     const bool bad = !isfinite(scal[0]);
     if (t == 0 && l == 0) *nonfinite = bad ? 1 : 0;
     const int64_t lr_ = t / dout, lc = t % dout;
-    const int64_t pr = d.sage ? (lr_ < d.din[l] ? lr_ : d.dpin[l] + (lr_ - d.din[l])) : lr_;
+    const int64_t pr = padded_row(lr_, d.kind, d.din[l], d.dpin[l]);
     const float g = d.gpad[l][pr * d.cols_p[l] + lc];
     if (d.G[l]) d.G[l][t] = g;
     if (!bad) const_cast<float*>(d.W[l])[t] -= lr * g;
@@ -532,7 +539,7 @@ __global__ void k_sgd_all(const WDesc d, float lr, const double* __restrict__ sc
 void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr) {
     const WDesc d = make_desc(c, W, G);
     int64_t mx = 0;
-    for (int l = 0; l < c.L; ++l) mx = std::max(mx, (d.sage ? 2 : 1) * d.din[l] * d.dout[l]);
+    for (int l = 0; l < c.L; ++l) mx = std::max(mx, logical_rows(d.kind, d.din[l]) * d.dout[l]);
     k_sgd_all<<<dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, c.stream>>>(d, lr, c.d_scal, c.d_nonfinite);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -682,12 +689,12 @@ __global__ void k_adam_all(const WDesc d, const AdamArgs a, const double* __rest
                            int32_t* __restrict__ nonfinite) {
     const int l = blockIdx.y;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t rows_l = (d.sage ? 2 : 1) * d.din[l], dout = d.dout[l];
+    const int64_t rows_l = logical_rows(d.kind, d.din[l]), dout = d.dout[l];
     if (t >= rows_l * dout) return;
     const bool bad = !isfinite(scal[0]);
     if (t == 0 && l == 0) *nonfinite = bad ? 1 : 0;
     const int64_t lr_ = t / dout, lc = t % dout;
-    const int64_t pr = d.sage ? (lr_ < d.din[l] ? lr_ : d.dpin[l] + (lr_ - d.din[l])) : lr_;
+    const int64_t pr = padded_row(lr_, d.kind, d.din[l], d.dpin[l]);
     const float g = d.gpad[l][pr * d.cols_p[l] + lc];
     if (d.G[l]) d.G[l][t] = g;
     if (bad) return;
@@ -708,7 +715,7 @@ void launch_adam(Ctx& c, float* const* W, float* const* G, float lr) {
     int64_t off = 0, mx = 0;
     for (int l = 0; l < c.L; ++l) {
         a.moff[l] = off;
-        const int64_t n = (d.sage ? 2 : 1) * d.din[l] * d.dout[l];
+        const int64_t n = logical_rows(d.kind, d.din[l]) * d.dout[l];
         off += n;
         mx = std::max(mx, n);
     }

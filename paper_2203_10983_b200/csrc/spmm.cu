@@ -64,6 +64,39 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
             }
             break;
         }
+        case GAT_FWD: {   // R45: pre_v = Σ_u alpha_vu Y_u + alpha_vv Y_v, ReLU on hidden layers
+            float f[VN];
+            V::to_float(*reinterpret_cast<const typename V::raw*>(static_cast<const T*>(a.self) + row * a.ld_self + vi * VN), f);
+            const float t = a.gat_el[row] + a.gat_er[row];
+            const float av = expf((t > 0.f ? t : 0.2f * t) - a.gat_m[row]) * a.gat_inv[row];
+#pragma unroll
+            for (int k = 0; k < VN; ++k) {
+                acc[k] = fmaf(av, f[k], acc[k]);
+                if (a.relu) acc[k] = fmaxf(acc[k], 0.f);
+            }
+            if (a.out_f32) {
+                float* o = static_cast<float*>(a.out) + row * a.ld_out + vi * VN;
+#pragma unroll
+                for (int k = 0; k < VN; k += 4) *reinterpret_cast<float4*>(o + k) = make_float4(acc[k], acc[k + 1], acc[k + 2], acc[k + 3]);
+                return;
+            }
+            break;
+        }
+        case GAT_BWD: {   // R45: dY_u = Σ_v alpha_vu g_v + [u inner] (alpha_uu g_u + del_u a_l) + der_u a_r
+            const float dr = a.gat_der[row];
+            if (row < a.n_in) {
+                float f[VN];
+                V::to_float(*reinterpret_cast<const typename V::raw*>(static_cast<const T*>(a.src) + row * a.ld_src + vi * VN), f);
+                const float t = a.gat_el[row] + a.gat_er[row];
+                const float au = expf((t > 0.f ? t : 0.2f * t) - a.gat_m[row]) * a.gat_inv[row];
+                const float dl = a.gat_del[row];
+#pragma unroll
+                for (int k = 0; k < VN; ++k) acc[k] = fmaf(au, f[k], acc[k]) + dl * a.gat_al[vi * VN + k];
+            }
+#pragma unroll
+            for (int k = 0; k < VN; ++k) acc[k] += dr * a.gat_ar[vi * VN + k];
+            break;
+        }
         case SAGE_BWD: {
             if (row < a.n_in) {
                 if (!a.self) break;   // R42 backward: dY has no self term
@@ -138,6 +171,14 @@ k_spmm(const SpmmArgs a) {
                 ci = a.col[eb + lane];
                 if (SC == 1) sc = (ci >= a.n_in) ? a.inv_p : 1.f;
                 if (SC == 2) sc = a.cscale[ci];
+                if (SC == 3) {   // GAT forward: alpha_vu, v = this row (R45)
+                    const float t = a.gat_el[s.row] + a.gat_er[ci];
+                    sc = expf((t > 0.f ? t : 0.2f * t) - a.gat_m[s.row]) * a.gat_inv[s.row];
+                }
+                if (SC == 4) {   // GAT backward (transposed): alpha_vu with v = the gathered row, u = this row
+                    const float t = a.gat_el[ci] + a.gat_er[s.row];
+                    sc = expf((t > 0.f ? t : 0.2f * t) - a.gat_m[ci]) * a.gat_inv[ci];
+                }
             }
             if (cnt == 32) {
                 // full chunk: no bounds checks on the edges
@@ -272,7 +313,9 @@ static void go(Ctx& c, const SpmmArgs& a, unsigned grid) {
     else if ((a.mode == SAGE_FWD || a.mode == SAGE_FWD_TF) && a.inv_p != 1.f) sc = 1;
     if (sc == 0) k_spmm<T, LPR, VPL, 0><<<grid, 256, 0, c.stream>>>(a);
     else if (sc == 1) k_spmm<T, LPR, VPL, 1><<<grid, 256, 0, c.stream>>>(a);
-    else k_spmm<T, LPR, VPL, 2><<<grid, 256, 0, c.stream>>>(a);
+    else if (sc == 2) k_spmm<T, LPR, VPL, 2><<<grid, 256, 0, c.stream>>>(a);
+    else if (sc == 3) k_spmm<T, LPR, VPL, 3><<<grid, 256, 0, c.stream>>>(a);
+    else k_spmm<T, LPR, VPL, 4><<<grid, 256, 0, c.stream>>>(a);
 }
 
 template <typename T>
@@ -334,6 +377,8 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
         a.src = static_cast<const char*>(a0.src) + c0 * ts;
         a.out = static_cast<char*>(a0.out) + c0 * (a0.out_f32 ? 4 : ts);
         if (a0.self) a.self = static_cast<const char*>(a0.self) + c0 * ts;
+        if (a0.gat_al) a.gat_al = a0.gat_al + c0;
+        if (a0.gat_ar) a.gat_ar = a0.gat_ar + c0;
         if (c.prec == BNS_BF16) dispatch<__nv_bfloat16>(c, a, grid);
         else dispatch<float>(c, a, grid);
         c.kernels += 1;

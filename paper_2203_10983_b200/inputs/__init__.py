@@ -18,7 +18,7 @@ _LIB = None
 SEED_GRAPH, SEED_FEAT, SEED_LABEL, SEED_PART, SEED_WEIGHT = 1, 2, 3, 4, 5
 BNS_SEED = 0x0123456789ABCDEF
 
-LAYER_SAGE, LAYER_GCN = 0, 1
+LAYER_SAGE, LAYER_GCN, LAYER_GAT = 0, 1, 2
 
 
 def lib():
@@ -101,7 +101,8 @@ def weights(dims, layer_kind: int, seed: int = SEED_WEIGHT) -> list[np.ndarray]:
     """Glorot-uniform fp32 weights; SAGE W^l is (2 d_{l-1}) x d_l (rows [0,d) multiply z), GCN d_{l-1} x d_l."""
     out = []
     for l in range(len(dims) - 1):
-        rows = (2 if layer_kind == LAYER_SAGE else 1) * dims[l]
+        # SAGE [z-half ; h-half] 2 d; GCN d; GAT [W ; a_l ; a_r] d + 2 (attention vectors Glorot-drawn like W)
+        rows = 2 * dims[l] if layer_kind == LAYER_SAGE else dims[l] + 2 if layer_kind == LAYER_GAT else dims[l]
         w = np.empty((rows, dims[l + 1]), np.float32)
         lib().gen_weights(rows, dims[l + 1], l, seed, _p(w))
         out.append(w)

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--partition", default="ldg2")
+    ap.add_argument("--model", default="sage", choices=["sage", "gat"], help="gat: 2-layer GAT (Table tab:gat)")
     ap.add_argument("--cache-x0", action="store_true", help="BNS_CACHE_INPUT_HALO (f1, R43): no layer-1 exchange")
     ap.add_argument("--samplers", nargs="+", default=["bns"], choices=["bns", "bes", "dropedge"],
                     help="f3 Table tab:bes analogue: edge samplers at matched dropped-edge counts (P:681)")
@@ -37,6 +38,9 @@ def main():
     from paper_2203_10983_b200 import bns
     from paper_2203_10983_b200 import inputs as I
     sh = I.SHAPES[args.config]
+    if args.model == "gat":
+        import dataclasses
+        sh = dataclasses.replace(sh, layer=I.LAYER_GAT, L=2)
     indptr, indices = I.rmat(sh.N, sh.nnz)
     part = I.partition(indptr, indices, args.m, args.partition)
     y_all = I.labels(sh.N, sh.C, sh.train_frac)
@@ -96,7 +100,7 @@ def main():
             pack_b = sum(2 * cnt["n_sent"] * dp[l] * s for l in range(1 if args.cache_x0 else 0, sh.L))
             scat_b = sum(3 * cnt["n_sent"] * dp[l] * s for l in range(1, sh.L))
             gbs = lambda b, ph: round(b / (ph * 1e-3) / 1e9, 1) if ph and ph > 0 else None
-            rec = {"config": sh.name, "m": args.m, "rank": r, "p": p, "sampler": sname, "q": q, "prec": args.prec,
+            rec = {"config": sh.name, "model": args.model, "m": args.m, "rank": r, "p": p, "sampler": sname, "q": q, "prec": args.prec,
                    "pack_gbs": gbs(pack_b, ph.get("pack")), "scatter_gbs": gbs(scat_b, ph.get("scatter")),
                    "cache_x0": bool(args.cache_x0),
                    "device_ms_per_epoch": float(np.median(ms)), "wall_ms_per_epoch": wall,

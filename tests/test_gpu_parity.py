@@ -81,7 +81,7 @@ def compare_epoch(run, orc, L, Ws, Wd, lr, prec, host=False, tag=""):
     dims = run.dims
     F = relu_flip_floor(run, orc, L, prec, tag)
     for l in range(1, L + 1):
-        if not (run.tf >> (l - 1)) & 1:     # transform-first layers do not materialise Z (R42)
+        if not (run.tf >> (l - 1)) & 1 and run.layer != bns.BNS_LAYER_GAT:   # no Z on R42 / GAT layers
             e = relerr(run.gather(bns.BNS_Q_Z, l, dims[l - 1]), orc.tensor(O.T_Z, l))
             assert e <= tol, (tag, "Z", l, e)
         e = relerr(run.gather(bns.BNS_Q_H, l, dims[l]), orc.tensor(O.T_H, l))
@@ -458,5 +458,32 @@ def test_multilabel_rejects_non_binary_targets():
         with pytest.raises(bns.BnsError) as ei:
             run.ctx[0].set_multilabel(np.full((len(indptr) - 1, 3), 2, np.uint8))
         assert ei.value.code == bns.BNS_ERR_INVALID
+    finally:
+        run.close()
+
+
+# ---------------- f4: GAT (Table tab:gat; R45) ----------------
+@pytest.mark.parametrize("prec", [bns.BNS_FP32, bns.BNS_BF16])
+@pytest.mark.parametrize("m,p,sampler", [(1, 1.0, 0), (3, 0.3, 0), (4, 0.1, 0), (3, 0.0, 0), (3, 0.4, 1), (2, 0.5, 2)])
+def test_gat_parity(prec, m, p, sampler):
+    layer = bns.BNS_LAYER_GAT
+    dims = [37, 24, 16, 5]
+    L = len(dims) - 1
+    indptr, indices, part, X, y = wl(3000, 90000, m, dims[0], dims[-1], 61 + m)   # hub rows: split segments
+    Ws = I.weights(dims, layer)
+    assert Ws[0].shape == (dims[0] + 2, dims[1])
+    Wd = [w.astype(np.float64) for w in Ws]
+    run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y)
+    orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
+    orc.set_bf16(prec == bns.BNS_BF16)
+    try:
+        for e in range(2 if prec == bns.BNS_FP32 else 1):
+            if sampler:
+                parallel(m, lambda r: run.ctx[r].sample_edges(sampler, p, SEED, e))
+                orc.sample_edges(sampler, p, SEED, e)
+            else:
+                run.sample(p, SEED, e)
+                orc.sample(p, SEED, e)
+            Ws = compare_epoch(run, orc, L, Ws, Wd, 0.5, prec, tag=f"gat epoch{e}")
     finally:
         run.close()
