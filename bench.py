@@ -162,6 +162,13 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 # algorithmic bytes / flops
 # ------------------------------------------------------------------------------------------------
+def workload_name(shape, p, world, partition):
+    """the config.workload string, identical for both arms (target nnz; the actual arc count is reported apart)"""
+    model = "GAT (1 head)" if shape.layer == 2 else "GraphSAGE-mean"
+    return (f"{shape.name}-shaped R-MAT N={shape.N} nnz={shape.nnz}, {model} {shape.L} layers hidden {shape.hidden}, "
+            f"d0={shape.d0}, C={shape.C}, p={p}, m={world} partitions ({partition})")
+
+
 def spmm_bytes(dp, L, n_in, n_halo, kept, s, tf=0):
     """Row-gather model per step.  Layer l (0-based) gathers at its input width dp[l], or at its
     output width dp[l+1] when it runs transform-first (R42, bit l of tf) -- then it also reads S (n_in x width) in
@@ -260,6 +267,9 @@ def run_reference(args):
     from paper_2203_10983_b200 import inputs as I
     shape = I.SHAPES[args.config]
     shape.p = args.p
+    if args.model == "gat":
+        import dataclasses
+        shape = dataclasses.replace(shape, layer=I.LAYER_GAT, L=2)
     scale = max(args.cpu_scale, 256.0)
     for _ in range(args.warmup):
         cpu_baseline(shape, scale * 4)
@@ -270,7 +280,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (R-MAT, Philox features/labels)",
-            "config": {"workload": f"{shape.name}-shaped R-MAT GraphSAGE {shape.L}x{shape.hidden}, p={shape.p}",
+            "config": {"workload": workload_name(shape, args.p, world, args.partition),
                        "note": "oracle timed on host cores; each step is a bounded sample scaled to the full workload"},
             "cpu_baseline": {**vals[0], "value": v}, "wall_s": wall,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -439,10 +449,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16" if prec == bns.BNS_BF16 else "f32",
             "data": "synthetic: R-MAT graph (Graph500 a,b,c=.57,.19,.19), Philox features/labels, Glorot weights",
-            "config": {"workload": f"{shape.name}-shaped R-MAT N={shape.N} nnz={int(indptr[-1])}, "
-                                   f"{'GAT (1 head)' if shape.layer == I.LAYER_GAT else 'GraphSAGE-mean'} "
-                                   f"{shape.L} layers hidden {shape.hidden}, d0={shape.d0}, C={shape.C}, p={args.p}, "
-                                   f"m={world} partitions ({args.partition})",
+            "config": {"workload": workload_name(shape, args.p, world, args.partition), "nnz_actual": int(indptr[-1]),
                        "global_batch": "full graph", "parallelism": f"partition-parallel m={world}",
                        "transform_first_layers": [l + 1 for l in range(shape.L) if (ctx.tf_layers() >> l) & 1],
                        "l2": "flushed between timed steps (2x L2 write, outside the events)",
