@@ -346,8 +346,9 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     if (c.layer == BNS_LAYER_GAT) {   // f4 / R45: Y buffer, per-layer attention scalars, dY
         for (int l = 0; l < L; ++l) tfw = std::max<int64_t>(tfw, c.dp[l + 1]);
         const int64_t R = P.n_in + c.halo_cap;
-        c.d_gat = static_cast<float*>(dalloc(c, (size_t)(2 * L * R + 2 * L * P.n_in + 3 * P.n_in + R + 16) * sizeof(float)));
+        c.d_gat = static_cast<float*>(dalloc(c, (size_t)(2 * L * R + 2 * L * P.n_in + 3 * P.n_in + 2 * R + 16) * sizeof(float)));
         c.d_gat_dy = dalloc(c, (size_t)R * c.maxd * ts);
+        c.d_gat_qp = static_cast<float*>(dalloc(c, (size_t)R * c.maxd * sizeof(float)));
     }
     if (c.tf_mask || c.layer == BNS_LAYER_GAT) c.d_tfy = dalloc(c, (size_t)(P.n_in + c.halo_cap) * tfw * ts);
     c.gflat_n = c.goff[L];
@@ -730,6 +731,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             float* selfds = cdot + n_in;
             float* del = selfds + n_in;
             float* der = del + n_in;
+            float* qr = der + gR;
             const float* al = c.Wpad[l - 1] + din * dout;
             float* g = c.d_gflat + c.goff[l - 1];
             {
@@ -745,10 +747,42 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
                 PhaseTimer t(c, BNS_PH_SPMM_BWD);
                 launch_gat_rowdots(c, c.d_dpre, last ? (const void*)c.d_logits : c.H[l], last, c.d_tfy, dout,
                                    (int32_t)dout, el, er, gm, ginv, cdot, selfds);
-                launch_gat_edge_ds(c, 0, fsegs, c.n_seg_fwd, fcol, fsplit, c.n_split_fwd, c.d_dpre, c.d_tfy, dout,
-                                   (int32_t)dout, el, er, gm, ginv, cdot, selfds, del);
-                launch_gat_edge_ds(c, 1, bsegs, c.n_seg_bwd, bcol, bsplit, c.n_split_bwd, c.d_dpre, c.d_tfy, dout,
-                                   (int32_t)dout, el, er, gm, ginv, cdot, selfds, der);
+                // del_v = g_v . Q_v - c_v q_v + self, Q_v = Σ_u w_vu Y_u (w = alpha LeakyReLU')
+                SpmmArgs aq{};
+                aq.mode = GAT_RAW;
+                aq.segs = fsegs;
+                aq.n_segs = c.n_seg_fwd;
+                aq.col = fcol;
+                aq.src = c.d_tfy;
+                aq.ld_src = dout;
+                aq.out = c.d_gat_qp;
+                aq.ld_out = dout;
+                aq.d = (int32_t)dout;
+                aq.n_in = n_in;
+                aq.inv_p = 1.f;
+                aq.sc = 5;
+                aq.gat_el = el;
+                aq.gat_er = er;
+                aq.gat_m = gm;
+                aq.gat_inv = ginv;
+                aq.partial = c.d_partial;
+                aq.split = fsplit;
+                aq.n_split = c.n_split_fwd;
+                launch_spmm(c, aq);
+                launch_gat_wsum(c, 0, fsegs, c.n_seg_fwd, fcol, fsplit, c.n_split_fwd, el, er, gm, ginv, cdot, qr);
+                launch_gat_final(c, 0, c.d_dpre, c.d_gat_qp, dout, (int32_t)dout, n_in, cdot, qr, selfds, del);
+                // der_u = Y_u . P_u - r_u + self, P_u = Σ_v w_vu g_v over the transposed segments
+                SpmmArgs ap = aq;
+                ap.segs = bsegs;
+                ap.n_segs = c.n_seg_bwd;
+                ap.col = bcol;
+                ap.src = c.d_dpre;
+                ap.sc = 6;
+                ap.split = bsplit;
+                ap.n_split = c.n_split_bwd;
+                launch_spmm(c, ap);
+                launch_gat_wsum(c, 1, bsegs, c.n_seg_bwd, bcol, bsplit, c.n_split_bwd, el, er, gm, ginv, cdot, qr);
+                launch_gat_final(c, 1, c.d_tfy, c.d_gat_qp, dout, (int32_t)dout, rows, cdot, qr, selfds, der);
                 SpmmArgs a{};
                 a.mode = GAT_BWD;
                 a.segs = bsegs;

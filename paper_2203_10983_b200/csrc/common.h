@@ -141,6 +141,7 @@ struct Ctx {
     float* d_gat = nullptr;          // f4 / R45 GAT scalars: per layer el, er (stacked rows) and softmax max / 1/Σ
                                      // (inner rows), then c, selfds, del (inner), der (stacked)
     void* d_gat_dy = nullptr;        // GAT dY, (n_in + halo_cap) x maxd storage
+    float* d_gat_qp = nullptr;       // GAT Q / P (fp32 weighted sums), (n_in + halo_cap) x maxd
     bool multilabel = false;         // f4 / R44: sigmoid BCE + F1-micro (bns_set_multilabel)
     uint8_t* d_targets = nullptr;    // n_in x C multi-hot targets
     void* d_x0cache = nullptr;       // f1 / R43: X^(0) rows of every boundary node, B_i order (BNS_CACHE_INPUT_HALO)

@@ -6,8 +6,10 @@
 //   (k_spmm SC = 3)  pre_v = Σ alpha_vu Y_u  (+ alpha_vv Y_v, ReLU in the epilogue)
 // backward, g = dPre:
 //   k_gat_rowdots    c_v = g_v . pre_v, selfds_v = alpha_vv (g_v . Y_v - c_v) LeakyReLU'(s_vv)
-//   k_gat_edge_ds    del_v = Σ_u ds_vu (forward segments) / der_u = Σ_v ds_vu (transposed segments),
-//                    ds_vu = alpha_vu (g_v . Y_u - c_v) LeakyReLU'(s_vu): coalesced row gathers, butterfly dots
+//   del_v = Σ_u ds_vu, der_u = Σ_v ds_vu with ds_vu = alpha_vu (g_v . Y_u - c_v) LeakyReLU'(s_vu), rewritten without
+//   per-edge dot products: w = alpha LeakyReLU'(s); Q_v = Σ_u w_vu Y_u and P_u = Σ_v w_vu g_v by the segment SpMM
+//   (SC 5 / 6, GAT_RAW), q_v = Σ_u w_vu and r_u = Σ_v w_vu c_v by k_gat_wsum, then k_gat_final:
+//   del_v = g_v . Q_v - c_v q_v + selfds_v, der_u = Y_u . P_u - r_u + [inner] selfds_u
 //   (k_spmm SC = 4)  dY_u = Σ_v alpha_vu g_v + [inner] (alpha_uu g_u + del_u a_l) + der_u a_r
 //   k_gat_da         da_l = Σ_v del_v Y_v, da_r = Σ_u der_u Y_u (two-stage, fixed order)
 #include "common.h"
@@ -136,106 +138,62 @@ __global__ void __launch_bounds__(256) k_gat_rowdots(const T* __restrict__ g, co
     }
 }
 
-// one warp per segment, the gathered rows read warp-coalesced like the SpMM: DIR 0 (forward segments, row v,
-// gathered Y_u) -> del partials; DIR 1 (transposed segments, row u, gathered g_v) -> der partials.  The row's own
-// vector (g_v resp. Y_u) is held in registers (VPL 16-byte vectors per lane); per edge the lanes' partial dot
-// products are summed by a butterfly, and the lane that loaded the edge's index adds its ds = alpha (dot - c_v)
-// LeakyReLU'(s).  Whole rows add the self term and store; split rows store per-segment sums for k_gat_ds_fix.
-template <typename T, int DIR, int VPL>
-__global__ void __launch_bounds__(256) k_gat_edge_ds(const Seg* __restrict__ segs, int64_t n_segs,
-                                                     const int32_t* __restrict__ col, const T* __restrict__ g,
-                                                     const T* __restrict__ Y, int64_t ld, int32_t d, int64_t n_in,
-                                                     const float* __restrict__ el, const float* __restrict__ er,
-                                                     const float* __restrict__ m, const float* __restrict__ inv,
-                                                     const float* __restrict__ cdot, const float* __restrict__ selfds,
-                                                     float* __restrict__ part, float* __restrict__ out) {
-    using V = Vec<T>;
-    using R = typename V::raw;
-    constexpr int VN = V::N;
-    constexpr int U = 4;
+// scalar edge sums over segments (self edges excluded): DIR 0 q_v = Σ_u w_vu, DIR 1 r_u = Σ_v w_vu c_v,
+// w_vu = alpha_vu LeakyReLU'(s_vu); whole rows store, split rows leave per-segment partials for k_gat_wsum_fix
+template <int DIR>
+__global__ void __launch_bounds__(256) k_gat_wsum(const Seg* __restrict__ segs, int64_t n_segs,
+                                                  const int32_t* __restrict__ col, const float* __restrict__ el,
+                                                  const float* __restrict__ er, const float* __restrict__ m,
+                                                  const float* __restrict__ inv, const float* __restrict__ cdot,
+                                                  float* __restrict__ part, float* __restrict__ out) {
     const int lane = threadIdx.x & 31;
-    const int nvec = d / VN;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t sid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sid < n_segs; sid += nw) {
         const Seg sg = segs[sid];
-        const T* own = (DIR == 0 ? g : Y) + (int64_t)sg.row * ld;
-        float ow[VPL][VN];
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-            const int v = lane + 32 * q;
-            if (v < nvec) V::to_float(reinterpret_cast<const R*>(own)[v], ow[q]);
-            else
-#pragma unroll
-                for (int k = 0; k < VN; ++k) ow[q][k] = 0.f;
-        }
-        const T* gath = DIR == 0 ? Y : g;
         float acc = 0.f;
-        for (int64_t eb = sg.e0; eb < sg.e1; eb += 32) {
-            const int cnt = (sg.e1 - eb < 32) ? (int)(sg.e1 - eb) : 32;
-            int32_t ci = 0;
-            float coef = 0.f, cv = 0.f;
-            if (lane < cnt) {
-                ci = col[eb + lane];
-                const int64_t vv = DIR == 0 ? sg.row : ci;   // the aggregating node v of the edge
-                const int64_t uu = DIR == 0 ? ci : sg.row;   // the source node u
-                const float t = el[vv] + er[uu];
-                coef = expf(lrelu(t) - m[vv]) * inv[vv] * (t > 0.f ? 1.f : 0.2f);
-                cv = cdot[vv];
-            }
-            for (int j0 = 0; j0 < cnt; j0 += U) {
-                float dots[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int j = j0 + u;
-                    const int32_t x = __shfl_sync(0xffffffffu, ci, j & 31);
-                    float s = 0.f;
-                    if (j < cnt) {
-                        const R* o = reinterpret_cast<const R*>(gath + (int64_t)x * ld);
-#pragma unroll
-                        for (int q = 0; q < VPL; ++q) {
-                            const int v = lane + 32 * q;
-                            if (v < nvec) {
-                                float f[VN];
-                                V::to_float(__ldg(o + v), f);
-#pragma unroll
-                                for (int k = 0; k < VN; ++k) s = fmaf(f[k], ow[q][k], s);
-                            }
-                        }
-                    }
-                    dots[u] = s;
-                }
-                // transposed butterfly: 6 shuffles leave lane L with the total of edge j0 + ((L >> 3) & 3)
-                const bool h16 = lane & 16, h8 = lane & 8;
-                float a0 = (h16 ? dots[2] : dots[0]) + __shfl_xor_sync(0xffffffffu, h16 ? dots[0] : dots[2], 16);
-                float a1 = (h16 ? dots[3] : dots[1]) + __shfl_xor_sync(0xffffffffu, h16 ? dots[1] : dots[3], 16);
-                float b = (h8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, h8 ? a0 : a1, 8);
-                b += __shfl_xor_sync(0xffffffffu, b, 4);
-                b += __shfl_xor_sync(0xffffffffu, b, 2);
-                b += __shfl_xor_sync(0xffffffffu, b, 1);
-                const int j = j0 + ((lane >> 3) & 3);
-                const float cj = __shfl_sync(0xffffffffu, coef, j & 31);
-                const float vj = __shfl_sync(0xffffffffu, cv, j & 31);
-                if ((lane & 7) == 0 && j < cnt) acc += cj * (b - vj);
-            }
+        for (int64_t e = sg.e0 + lane; e < sg.e1; e += 32) {
+            const int32_t x = col[e];
+            const int64_t vv = DIR == 0 ? sg.row : x;
+            const int64_t uu = DIR == 0 ? x : sg.row;
+            const float t = el[vv] + er[uu];
+            float w = expf(lrelu(t) - m[vv]) * inv[vv] * (t > 0.f ? 1.f : 0.2f);
+            if (DIR == 1) w *= cdot[vv];
+            acc += w;
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane) continue;
         if (sg.nseg > 1) part[sid] = acc;
-        else out[sg.row] = acc + (sg.row < n_in ? selfds[sg.row] : 0.f);
+        else out[sg.row] = acc;
     }
 }
 
-__global__ void k_gat_ds_fix(const Seg* __restrict__ segs, const int64_t* __restrict__ split, int64_t n_split,
-                             int64_t n_in, const float* __restrict__ selfds, const float* __restrict__ part,
-                             float* __restrict__ out) {
+__global__ void k_gat_wsum_fix(const Seg* __restrict__ segs, const int64_t* __restrict__ split, int64_t n_split,
+                               const float* __restrict__ part, float* __restrict__ out) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n_split) return;
     const int64_t sid = split[q];
     const Seg sg = segs[sid];
     float acc = 0.f;
     for (int k = 0; k < sg.nseg; ++k) acc += part[sid + k];
-    out[sg.row] = acc + (sg.row < n_in ? selfds[sg.row] : 0.f);
+    out[sg.row] = acc;
+}
+
+// DIR 0: del_v = g_v . Q_v - c_v q_v + selfds_v (inner rows);  DIR 1: der_u = Y_u . P_u - r_u + [inner] selfds_u
+template <typename T, int DIR>
+__global__ void __launch_bounds__(256) k_gat_final(const T* __restrict__ own, const float* __restrict__ qp,
+                                                   int64_t ld, int32_t d, int64_t rows, int64_t n_in,
+                                                   const float* __restrict__ cdot, const float* __restrict__ qr,
+                                                   const float* __restrict__ selfds, float* __restrict__ out) {
+    using V = Vec<T>;
+    constexpr int VN = V::N;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+        const float s = row_dot(own + r * ld, qp + r * ld, d, lane);
+        if (lane == 0)
+            out[r] = s - (DIR == 0 ? cdot[r] * qr[r] : qr[r]) + (r < n_in ? selfds[r] : 0.f);
+    }
 }
 
 // out[c] = Σ_r w_r Y_r[c]: block b sums its row range in order per column, then one pass over the blocks in order
@@ -300,33 +258,31 @@ void launch_gat_rowdots(Ctx& c, const void* g, const void* out, bool out_f32, co
     BNS_CHECK_LAUNCH();
 }
 
-void launch_gat_edge_ds(Ctx& c, int dir, const Seg* segs, int64_t n_segs, const int32_t* col, const int64_t* split,
-                        int64_t n_split, const void* g, const void* Y, int64_t ld, int32_t d, const float* el,
-                        const float* er, const float* m, const float* inv, const float* cdot, const float* selfds,
-                        float* out) {
+void launch_gat_wsum(Ctx& c, int dir, const Seg* segs, int64_t n_segs, const int32_t* col, const int64_t* split,
+                     int64_t n_split, const float* el, const float* er, const float* m, const float* inv,
+                     const float* cdot, float* out) {
     if (n_segs <= 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>((n_segs + 7) / 8, 148 * 16);
-    const int64_t n_in = c.plan.n_in;
-    const int nvec = d / (c.prec == BNS_BF16 ? 8 : 4);
-    if (nvec > 64) throw Error(BNS_ERR_INVALID, "GAT layer width too large (at most 64 16-byte vectors per row)");
-    const bool two = nvec > 32;
-#define BNS_DS(T, DIR, VPL)                                                                                       \
-    k_gat_edge_ds<T, DIR, VPL><<<grid, 256, 0, c.stream>>>(segs, n_segs, col, (const T*)g, (const T*)Y, ld, d,   \
-                                                            n_in, el, er, m, inv, cdot, selfds, c.d_partial, out)
-    if (c.prec == BNS_BF16) {
-        if (dir == 0) { if (two) BNS_DS(__nv_bfloat16, 0, 2); else BNS_DS(__nv_bfloat16, 0, 1); }
-        else { if (two) BNS_DS(__nv_bfloat16, 1, 2); else BNS_DS(__nv_bfloat16, 1, 1); }
-    } else {
-        if (dir == 0) { if (two) BNS_DS(float, 0, 2); else BNS_DS(float, 0, 1); }
-        else { if (two) BNS_DS(float, 1, 2); else BNS_DS(float, 1, 1); }
-    }
-#undef BNS_DS
+    if (dir == 0) k_gat_wsum<0><<<grid, 256, 0, c.stream>>>(segs, n_segs, col, el, er, m, inv, cdot, c.d_partial, out);
+    else k_gat_wsum<1><<<grid, 256, 0, c.stream>>>(segs, n_segs, col, el, er, m, inv, cdot, c.d_partial, out);
     c.kernels += 1;
     if (n_split > 0) {
-        k_gat_ds_fix<<<(unsigned)((n_split + 127) / 128), 128, 0, c.stream>>>(segs, split, n_split, n_in, selfds,
-                                                                              c.d_partial, out);
+        k_gat_wsum_fix<<<(unsigned)((n_split + 127) / 128), 128, 0, c.stream>>>(segs, split, n_split, c.d_partial, out);
         c.kernels += 1;
     }
+    BNS_CHECK_LAUNCH();
+}
+
+void launch_gat_final(Ctx& c, int dir, const void* own, const float* qp, int64_t ld, int32_t d, int64_t rows,
+                      const float* cdot, const float* qr, const float* selfds, float* out) {
+    if (rows <= 0) return;
+    const unsigned grid = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 16);
+    const int64_t n_in = c.plan.n_in;
+#define BNS_FIN(T, DIR) k_gat_final<T, DIR><<<grid, 256, 0, c.stream>>>((const T*)own, qp, ld, d, rows, n_in, cdot, qr, selfds, out)
+    if (c.prec == BNS_BF16) { if (dir == 0) BNS_FIN(__nv_bfloat16, 0); else BNS_FIN(__nv_bfloat16, 1); }
+    else { if (dir == 0) BNS_FIN(float, 0); else BNS_FIN(float, 1); }
+#undef BNS_FIN
+    c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 

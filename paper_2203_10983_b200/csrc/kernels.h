@@ -20,7 +20,8 @@ int64_t build_static_segments(Ctx& c, const int64_t* d_ptr, int64_t rows, int64_
 void scan_i32(Ctx& c, const int32_t* in, int64_t* out, int64_t n, int64_t* d_total);
 
 // a6 / a10: segment SpMM (spmm.cu)
-enum SpmmMode { SAGE_FWD = 0, GCN_FWD = 1, SAGE_BWD = 2, GCN_BWD = 3, SAGE_FWD_TF = 4, GAT_FWD = 5, GAT_BWD = 6 };
+enum SpmmMode { SAGE_FWD = 0, GCN_FWD = 1, SAGE_BWD = 2, GCN_BWD = 3, SAGE_FWD_TF = 4, GAT_FWD = 5, GAT_BWD = 6,
+                GAT_RAW = 7 /* the weighted sum stored as fp32, no epilogue terms */ };
 struct SpmmArgs {
     int mode;
     const Seg* segs; int64_t n_segs;
@@ -55,10 +56,15 @@ void launch_gat_stats(Ctx& c, const Seg* segs, int64_t n_segs, const int32_t* co
                       int64_t n_split, const float* el, const float* er, float* m, float* inv);
 void launch_gat_rowdots(Ctx& c, const void* g, const void* out, bool out_f32, const void* Y, int64_t ld, int32_t d,
                         const float* el, const float* er, const float* m, const float* inv, float* cdot, float* selfds);
-void launch_gat_edge_ds(Ctx& c, int dir, const Seg* segs, int64_t n_segs, const int32_t* col, const int64_t* split,
-                        int64_t n_split, const void* g, const void* Y, int64_t ld, int32_t d, const float* el,
-                        const float* er, const float* m, const float* inv, const float* cdot, const float* selfds,
-                        float* out);
+// del / der without per-edge dot products: with w_vu = alpha_vu LeakyReLU'(s_vu),
+//   del_v = g_v . Q_v - c_v q_v,  Q_v = Σ_u w_vu Y_u (segment SpMM, SC 5),   q_v = Σ_u w_vu        (k_gat_wsum 0)
+//   der_u = Y_u . P_u - r_u,      P_u = Σ_v w_vu g_v (transposed, SC 6),     r_u = Σ_v w_vu c_v    (k_gat_wsum 1)
+// plus the self edge (selfds) -- k_gat_final
+void launch_gat_wsum(Ctx& c, int dir, const Seg* segs, int64_t n_segs, const int32_t* col, const int64_t* split,
+                     int64_t n_split, const float* el, const float* er, const float* m, const float* inv,
+                     const float* cdot, float* out);
+void launch_gat_final(Ctx& c, int dir, const void* own, const float* qp, int64_t ld, int32_t d, int64_t rows,
+                      const float* cdot, const float* qr, const float* selfds, float* out);
 void launch_gat_da(Ctx& c, const void* Y, int64_t ld, int32_t d, const float* w, int64_t rows, float* out);
 
 // a7 / a9: GEMMs (gemm_simt.cu; tcgen05 in gemm_tc.cu)

@@ -82,6 +82,12 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
             }
             break;
         }
+        case GAT_RAW: {
+            float* o = static_cast<float*>(a.out) + row * a.ld_out + vi * VN;
+#pragma unroll
+            for (int k = 0; k < VN; k += 4) *reinterpret_cast<float4*>(o + k) = make_float4(acc[k], acc[k + 1], acc[k + 2], acc[k + 3]);
+            return;
+        }
         case GAT_BWD: {   // R45: dY_u = Σ_v alpha_vu g_v + [u inner] (alpha_uu g_u + del_u a_l) + der_u a_r
             const float dr = a.gat_der[row];
             if (row < a.n_in) {
@@ -175,9 +181,14 @@ k_spmm(const SpmmArgs a) {
                     const float t = a.gat_el[s.row] + a.gat_er[ci];
                     sc = expf((t > 0.f ? t : 0.2f * t) - a.gat_m[s.row]) * a.gat_inv[s.row];
                 }
-                if (SC == 4) {   // GAT backward (transposed): alpha_vu with v = the gathered row, u = this row
+                if (SC == 4 || SC == 6) {   // GAT transposed: alpha_vu with v = the gathered row, u = this row
                     const float t = a.gat_el[ci] + a.gat_er[s.row];
                     sc = expf((t > 0.f ? t : 0.2f * t) - a.gat_m[ci]) * a.gat_inv[ci];
+                    if (SC == 6) sc *= (t > 0.f ? 1.f : 0.2f);   // w_vu = alpha_vu LeakyReLU'(s_vu)
+                }
+                if (SC == 5) {   // GAT forward w_vu = alpha_vu LeakyReLU'(s_vu), v = this row
+                    const float t = a.gat_el[s.row] + a.gat_er[ci];
+                    sc = expf((t > 0.f ? t : 0.2f * t) - a.gat_m[s.row]) * a.gat_inv[s.row] * (t > 0.f ? 1.f : 0.2f);
                 }
             }
             if (cnt == 32) {
@@ -315,7 +326,9 @@ static void go(Ctx& c, const SpmmArgs& a, unsigned grid) {
     else if (sc == 1) k_spmm<T, LPR, VPL, 1><<<grid, 256, 0, c.stream>>>(a);
     else if (sc == 2) k_spmm<T, LPR, VPL, 2><<<grid, 256, 0, c.stream>>>(a);
     else if (sc == 3) k_spmm<T, LPR, VPL, 3><<<grid, 256, 0, c.stream>>>(a);
-    else k_spmm<T, LPR, VPL, 4><<<grid, 256, 0, c.stream>>>(a);
+    else if (sc == 4) k_spmm<T, LPR, VPL, 4><<<grid, 256, 0, c.stream>>>(a);
+    else if (sc == 5) k_spmm<T, LPR, VPL, 5><<<grid, 256, 0, c.stream>>>(a);
+    else k_spmm<T, LPR, VPL, 6><<<grid, 256, 0, c.stream>>>(a);
 }
 
 template <typename T>
@@ -375,7 +388,7 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
         SpmmArgs a = a0;
         a.d = (int32_t)std::min<int64_t>(tile, a0.d - c0);
         a.src = static_cast<const char*>(a0.src) + c0 * ts;
-        a.out = static_cast<char*>(a0.out) + c0 * (a0.out_f32 ? 4 : ts);
+        a.out = static_cast<char*>(a0.out) + c0 * ((a0.out_f32 || a0.mode == GAT_RAW) ? 4 : ts);
         if (a0.self) a.self = static_cast<const char*>(a0.self) + c0 * ts;
         if (a0.gat_al) a.gat_al = a0.gat_al + c0;
         if (a0.gat_ar) a.gat_ar = a0.gat_ar + c0;
