@@ -29,7 +29,7 @@ $(OBJDIR)/%.cu.o: $(PKG)/csrc/%.cu $(CHDR)
 
 $(OBJDIR)/%.cpp.o: $(PKG)/csrc/%.cpp $(CHDR)
 	@mkdir -p $(OBJDIR)
-	$(NVCC) -O2 -std=c++17 -Xcompiler -fPIC -Iinclude -I$(NCCL_DIR)/include -c -o $@ $<
+	$(NVCC) -O2 -std=c++17 -Wno-deprecated-gpu-targets -Xcompiler -fPIC,-Wall -Iinclude -I$(NCCL_DIR)/include -c -o $@ $<
 
 $(PKG)/libbns.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib

@@ -9,6 +9,7 @@
 
 #include "common.h"
 #include "kernels.h"
+#include "layers.h"
 #include "transport.h"
 
 struct bns_ctx {
@@ -128,24 +129,6 @@ std::vector<Seg> host_segments(const std::vector<int64_t>& ptr, int64_t rows, in
     }
     return s;
 }
-
-struct PhaseTimer {
-    Ctx& c;
-    int ph;
-    size_t slot;
-    PhaseTimer(Ctx& c_, int ph_) : c(c_), ph(ph_), slot(0) {
-        if (!c.timing) return;
-        slot = c.ev_used;
-        if (slot + 2 > c.ev.size()) { ph = -1; return; }
-        c.ev_used += 2;
-        c.ev_phase[slot / 2] = ph;
-        BNS_CUDA(cudaEventRecord(c.ev[slot], c.stream));
-    }
-    ~PhaseTimer() noexcept(false) {
-        if (!c.timing || ph < 0) return;
-        BNS_CUDA(cudaEventRecord(c.ev[slot + 1], c.stream));
-    }
-};
 
 void collect_times(Ctx& c) {
     if (!c.timing) return;
@@ -503,7 +486,6 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     Plan& P = c.plan;
     const int L = c.L, m = c.cfg.world;
     const size_t ts = tsize(c);
-    const bool sage = c.layer == BNS_LAYER_SAGE_MEAN;
     const int64_t n_in = P.n_in;
     // c_u = 1/p only exists on halo columns; with no halo every column scale is 1 (the kernels then skip it)
     const float inv_p = (c.n_halo > 0) ? (float)c.inv_p : 1.f;
@@ -534,25 +516,22 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         launch_wpack_all(c, W.data());
         if (c.tf_mask) launch_wpack_tf(c);
     }
-    const Seg* fsegs = c.fwd_mode == 0 ? c.d_seg_static_fwd : (c.fwd_mode == 1 ? c.d_seg_bwd : c.d_seg_fwd);
-    const int32_t* fcol = c.fwd_mode == 0 ? c.d_static_col : (c.fwd_mode == 1 ? c.d_tcol : c.d_ind_col);
-    const int64_t* fsplit = c.fwd_mode == 0 ? c.d_split_sf : (c.fwd_mode == 1 ? c.d_split_bwd : c.d_split_fwd);
-    const bool ebw = c.sampler != BNS_SAMPLER_BNS;
-    const Seg* bsegs = ebw ? c.d_eseg_bwd : c.d_seg_bwd;
-    const int32_t* bcol = ebw ? c.d_ind_tcol : c.d_tcol;
-    const int64_t* bsplit = ebw ? c.d_esplit_bwd : c.d_split_bwd;
-    // f4 / R45 GAT scalars of layer l (1-based): el, er over the stacked rows, softmax max / 1/Σ over inner rows
-    const int64_t gR = n_in + c.halo_cap;
-    auto gat_el = [&](int l) { return c.d_gat + (int64_t)(l - 1) * 2 * gR; };
-    auto gat_m = [&](int l) { return c.d_gat + (int64_t)2 * L * gR + (int64_t)(l - 1) * 2 * n_in; };
-    float* gat_tail = c.d_gat ? c.d_gat + (int64_t)2 * L * gR + (int64_t)2 * L * n_in : nullptr;   // c, selfds, del, der
+    const bool ebw = c.sampler != BNS_SAMPLER_BNS;   // f3: the sampled transposed CSR of this epoch
+    EpochView ev;
+    ev.fsegs = c.fwd_mode == 0 ? c.d_seg_static_fwd : (c.fwd_mode == 1 ? c.d_seg_bwd : c.d_seg_fwd);
+    ev.fcol = c.fwd_mode == 0 ? c.d_static_col : (c.fwd_mode == 1 ? c.d_tcol : c.d_ind_col);
+    ev.fsplit = c.fwd_mode == 0 ? c.d_split_sf : (c.fwd_mode == 1 ? c.d_split_bwd : c.d_split_fwd);
+    ev.bsegs = ebw ? c.d_eseg_bwd : c.d_seg_bwd;
+    ev.bcol = ebw ? c.d_ind_tcol : c.d_tcol;
+    ev.bsplit = ebw ? c.d_esplit_bwd : c.d_split_bwd;
+    ev.inv_p = inv_p;
     const int32_t* S_local = c.d_cand_out + c.n_halo;
     const bool dropout = c.drop > 0.0;
     if (dropout) launch_halo_gid(c);
 
     // ------------------------------ forward (Alg.1 l.8-10) ------------------------------
     for (int l = 1; l <= L; ++l) {
-        const int64_t din = c.dp[l - 1], dout = c.dp[l];
+        const int64_t din = c.dp[l - 1];
         void* Hin = c.H[l - 1];
         if (m > 1 && l == 1 && c.d_x0cache) {   // R43: layer-1 halo rows from the boundary-feature cache
             PhaseTimer t(c, BNS_PH_PACK);
@@ -572,128 +551,9 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             launch_dropout(c, Hin, c.Xd[l - 1], n_in + c.n_halo, din, l);
             Hin = c.Xd[l - 1];
         }
-        if (c.layer == BNS_LAYER_GAT) {
-            // f4 / R45: Y = Hin W on every stacked row (tcgen05), el / er, softmax statistics, then
-            // pre_v = Σ_u alpha_vu Y_u + alpha_vv Y_v with ReLU (hidden) or fp32 logits (last) in the SpMM epilogue
-            const bool last = (l == L);
-            const int64_t rows = n_in + c.n_halo;
-            float* el = gat_el(l);
-            float* er = el + gR;
-            float* gm = gat_m(l);
-            float* ginv = gm + n_in;
-            const float* al = c.Wpad[l - 1] + din * dout;
-            {
-                PhaseTimer t(c, BNS_PH_GEMM_FWD);
-                if (c.use_tc)
-                    gemm_fwd_tc(c, rows, dout, Hin, din, din, nullptr, 0, din, c.WT[l - 1], c.wkw[l - 1], c.d_tfy,
-                                dout, false, false);
-                else
-                    gemm_fwd(c, rows, dout, Hin, din, din, nullptr, 0, din, c.Wt[l - 1], dout, c.d_tfy, dout, false,
-                             false);
-            }
-            PhaseTimer t(c, BNS_PH_SPMM_FWD);
-            launch_gat_scores(c, c.d_tfy, dout, rows, (int32_t)dout, al, al + dout, el, er);
-            launch_gat_stats(c, fsegs, c.n_seg_fwd, fcol, fsplit, c.n_split_fwd, el, er, gm, ginv);
-            SpmmArgs a{};
-            a.mode = GAT_FWD;
-            a.segs = fsegs;
-            a.n_segs = c.n_seg_fwd;
-            a.col = fcol;
-            a.src = c.d_tfy;
-            a.ld_src = dout;
-            a.self = c.d_tfy;
-            a.ld_self = dout;
-            a.out = last ? (void*)c.d_logits : c.H[l];
-            a.ld_out = dout;
-            a.d = (int32_t)dout;
-            a.n_in = n_in;
-            a.inv_p = 1.f;
-            a.sc = 3;
-            a.gat_el = el;
-            a.gat_er = er;
-            a.gat_m = gm;
-            a.gat_inv = ginv;
-            a.partial = c.d_partial;
-            a.split = fsplit;
-            a.n_split = c.n_split_fwd;
-            a.relu = last ? 0 : 1;
-            a.out_f32 = last ? 1 : 0;
-            launch_spmm(c, a);
-            continue;
-        }
-        if ((c.tf_mask >> (l - 1)) & 1u) {
-            // R42 transform-first: [Y | S] = Hin [W_top | W_bot] on every stacked row, then
-            // pre_v = (1/deg_G(v)) Σ_u c_u Y_u + S_v with ReLU (hidden) or fp32 logits (last) in the SpMM epilogue
-            const bool last = (l == L);
-            const int64_t rows = n_in + c.n_halo;
-            {
-                PhaseTimer t(c, BNS_PH_GEMM_FWD);
-                if (c.use_tc)
-                    gemm_fwd_tc(c, rows, 2 * dout, Hin, din, din, nullptr, 0, din, c.WTtf[l - 1], (din + 63) / 64 * 64,
-                                c.d_tfy, 2 * dout, false, false);
-                else
-                    gemm_fwd(c, rows, 2 * dout, Hin, din, din, nullptr, 0, din, c.Wcat[l - 1], 2 * dout, c.d_tfy,
-                             2 * dout, false, false);
-            }
-            PhaseTimer t(c, BNS_PH_SPMM_FWD);
-            SpmmArgs a{};
-            a.mode = SAGE_FWD_TF;
-            a.segs = fsegs;
-            a.n_segs = c.n_seg_fwd;
-            a.col = fcol;
-            a.src = c.d_tfy;
-            a.ld_src = 2 * dout;
-            a.self = static_cast<char*>(c.d_tfy) + dout * ts;
-            a.ld_self = 2 * dout;
-            a.out = last ? (void*)c.d_logits : c.H[l];
-            a.ld_out = dout;
-            a.d = (int32_t)dout;
-            a.n_in = n_in;
-            a.inv_p = inv_p;
-            a.nscale = c.nscale;
-            a.rowscale = c.d_deg_in;
-            a.partial = c.d_partial;
-            a.split = c.fwd_mode == 0 ? c.d_split_sf : (c.fwd_mode == 1 ? c.d_split_bwd : c.d_split_fwd);
-            a.n_split = c.n_split_fwd;
-            a.relu = last ? 0 : 1;
-            a.out_f32 = last ? 1 : 0;
-            launch_spmm(c, a);
-            continue;
-        }
-        {
-            PhaseTimer t(c, BNS_PH_SPMM_FWD);
-            SpmmArgs a{};
-            a.mode = sage ? SAGE_FWD : GCN_FWD;
-            a.segs = fsegs;
-            a.n_segs = c.n_seg_fwd;
-            a.col = fcol;
-            a.src = Hin;
-            a.ld_src = din;
-            a.out = c.Z[l];
-            a.ld_out = din;
-            a.d = (int32_t)din;
-            a.n_in = n_in;
-            a.inv_p = inv_p;
-            a.nscale = c.nscale;
-            a.rowscale = sage ? c.d_deg_in : c.d_rs_in;
-            a.cscale = c.d_cscale;
-            a.partial = c.d_partial;
-            a.split = c.fwd_mode == 0 ? c.d_split_sf : (c.fwd_mode == 1 ? c.d_split_bwd : c.d_split_fwd);
-            a.n_split = c.n_split_fwd;
-            launch_spmm(c, a);
-        }
-        {
-            PhaseTimer t(c, BNS_PH_GEMM_FWD);
-            const bool last = (l == L);
-            void* out = last ? (void*)c.d_logits : c.H[l];
-            if (c.use_tc)
-                gemm_fwd_tc(c, n_in, dout, c.Z[l], din, din, sage ? Hin : nullptr, sage ? din : 0, din, c.WT[l - 1],
-                            c.wkw[l - 1], out, dout, !last, last);
-            else if (sage)
-                gemm_fwd(c, n_in, dout, c.Z[l], din, din, Hin, din, din, c.Wt[l - 1], dout, out, dout, !last, last);
-            else
-                gemm_fwd(c, n_in, dout, c.Z[l], din, din, nullptr, 0, din, c.Wt[l - 1], dout, out, dout, !last, last);
-        }
+        if (c.layer == BNS_LAYER_GAT) forward_layer_gat(c, ev, l, Hin);
+        else if ((c.tf_mask >> (l - 1)) & 1u) forward_layer_tf(c, ev, l, Hin);
+        else forward_layer_std(c, ev, l, Hin);
     }
     // ------------------------------ loss (l.11) ------------------------------
     {
@@ -718,191 +578,10 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             launch_relu_mask(c, c.d_dx, c.H[l], dout, n_in, (int32_t)dout, c.d_dpre, tfl ? c.d_deg_in : nullptr,
                              tfl ? c.d_dxcat : nullptr);
         }
-        if (c.layer == BNS_LAYER_GAT) {
-            // f4 / R45 backward (g = dPre): c_v = g_v . pre_v, del_v / der_u = Σ ds over the forward / transposed
-            // segments, dY by the weighted SpMM^T, dW = Hin^T dY, da_l = Σ del Y, da_r = Σ der Y, dX = dY W^T
-            const bool last = (l == L);
-            const int64_t rows = n_in + c.n_halo;
-            float* el = gat_el(l);
-            float* er = el + gR;
-            float* gm = gat_m(l);
-            float* ginv = gm + n_in;
-            float* cdot = gat_tail;
-            float* selfds = cdot + n_in;
-            float* del = selfds + n_in;
-            float* der = del + n_in;
-            float* qr = der + gR;
-            const float* al = c.Wpad[l - 1] + din * dout;
-            float* g = c.d_gflat + c.goff[l - 1];
-            {
-                PhaseTimer t(c, BNS_PH_GEMM_BWD);   // Y again (same GEMM, same values)
-                if (c.use_tc)
-                    gemm_fwd_tc(c, rows, dout, Hin, din, din, nullptr, 0, din, c.WT[l - 1], c.wkw[l - 1], c.d_tfy,
-                                dout, false, false);
-                else
-                    gemm_fwd(c, rows, dout, Hin, din, din, nullptr, 0, din, c.Wt[l - 1], dout, c.d_tfy, dout, false,
-                             false);
-            }
-            {
-                PhaseTimer t(c, BNS_PH_SPMM_BWD);
-                launch_gat_rowdots(c, c.d_dpre, last ? (const void*)c.d_logits : c.H[l], last, c.d_tfy, dout,
-                                   (int32_t)dout, el, er, gm, ginv, cdot, selfds);
-                // del_v = g_v . Q_v - c_v q_v + self, Q_v = Σ_u w_vu Y_u (w = alpha LeakyReLU')
-                SpmmArgs aq{};
-                aq.mode = GAT_RAW;
-                aq.segs = fsegs;
-                aq.n_segs = c.n_seg_fwd;
-                aq.col = fcol;
-                aq.src = c.d_tfy;
-                aq.ld_src = dout;
-                aq.out = c.d_gat_qp;
-                aq.ld_out = dout;
-                aq.d = (int32_t)dout;
-                aq.n_in = n_in;
-                aq.inv_p = 1.f;
-                aq.sc = 5;
-                aq.gat_el = el;
-                aq.gat_er = er;
-                aq.gat_m = gm;
-                aq.gat_inv = ginv;
-                aq.partial = c.d_partial;
-                aq.split = fsplit;
-                aq.n_split = c.n_split_fwd;
-                launch_spmm(c, aq);
-                launch_gat_wsum(c, 0, fsegs, c.n_seg_fwd, fcol, fsplit, c.n_split_fwd, el, er, gm, ginv, cdot, qr);
-                launch_gat_final(c, 0, c.d_dpre, c.d_gat_qp, dout, (int32_t)dout, n_in, cdot, qr, selfds, del);
-                // der_u = Y_u . P_u - r_u + self, P_u = Σ_v w_vu g_v over the transposed segments
-                SpmmArgs ap = aq;
-                ap.segs = bsegs;
-                ap.n_segs = c.n_seg_bwd;
-                ap.col = bcol;
-                ap.src = c.d_dpre;
-                ap.sc = 6;
-                ap.split = bsplit;
-                ap.n_split = c.n_split_bwd;
-                launch_spmm(c, ap);
-                launch_gat_wsum(c, 1, bsegs, c.n_seg_bwd, bcol, bsplit, c.n_split_bwd, el, er, gm, ginv, cdot, qr);
-                launch_gat_final(c, 1, c.d_tfy, c.d_gat_qp, dout, (int32_t)dout, rows, cdot, qr, selfds, der);
-                SpmmArgs a{};
-                a.mode = GAT_BWD;
-                a.segs = bsegs;
-                a.n_segs = c.n_seg_bwd;
-                a.col = bcol;
-                a.src = c.d_dpre;
-                a.ld_src = dout;
-                a.out = c.d_gat_dy;
-                a.ld_out = dout;
-                a.d = (int32_t)dout;
-                a.n_in = n_in;
-                a.inv_p = 1.f;
-                a.sc = 4;
-                a.gat_el = el;
-                a.gat_er = er;
-                a.gat_m = gm;
-                a.gat_inv = ginv;
-                a.gat_al = al;
-                a.gat_ar = al + dout;
-                a.gat_del = del;
-                a.gat_der = der;
-                a.partial = c.d_partial;
-                a.split = bsplit;
-                a.n_split = c.n_split_bwd;
-                launch_spmm(c, a);
-            }
-            {
-                PhaseTimer t(c, BNS_PH_GEMM_BWD);
-                auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
-                auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
-                wgrad(c, rows, din, dout, Hin, din, c.d_gat_dy, dout, g, dout);
-                launch_gat_da(c, c.d_tfy, dout, (int32_t)dout, del, n_in, g + din * dout);
-                launch_gat_da(c, c.d_tfy, dout, (int32_t)dout, der, rows, g + (din + 1) * dout);
-                if (l > 1) dxg(c, rows, din, dout, c.d_gat_dy, dout, c.Wt[l - 1], dout, c.d_dx, din, nullptr, 0);
-            }
-            if (l == 1) break;   // R29
-        } else if ((c.tf_mask >> (l - 1)) & 1u) {
-            // R42 transform-first backward: dY_u = c_u Σ_v dPre_v / deg_G(v) over every stacked row (SpMM^T at the
-            // narrow width), dW_top = Hin^T dY, dW_bot = Hin_inner^T dPre, dX = [dY | dPre] [W_top | W_bot]^T
-            const bool eb = c.sampler != BNS_SAMPLER_BNS;
-            const int64_t rows = n_in + c.n_halo;
-            {
-                PhaseTimer t(c, BNS_PH_SPMM_BWD);
-                SpmmArgs a{};
-                a.mode = SAGE_BWD;
-                a.segs = eb ? c.d_eseg_bwd : c.d_seg_bwd;
-                a.n_segs = c.n_seg_bwd;
-                a.col = eb ? c.d_ind_tcol : c.d_tcol;
-                a.src = c.d_dxcat;       // dPre_v / deg_G(v), written by k_xent / k_relu_mask
-                a.ld_src = dout;
-                a.out = c.d_tfy;
-                a.ld_out = 2 * dout;
-                a.self = nullptr;
-                a.d = (int32_t)dout;
-                a.n_in = n_in;
-                a.inv_p = inv_p;
-                a.nscale = c.nscale;
-                a.partial = c.d_partial;
-                a.split = eb ? c.d_esplit_bwd : c.d_split_bwd;
-                a.n_split = c.n_split_bwd;
-                launch_spmm(c, a);
-            }
-            {
-                PhaseTimer t(c, BNS_PH_GEMM_BWD);
-                float* g = c.d_gflat + c.goff[l - 1];
-                auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
-                auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
-                wgrad(c, rows, din, dout, Hin, din, c.d_tfy, 2 * dout, g, dout);
-                wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
-                if (l > 1) {
-                    BNS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(c.d_tfy) + dout * ts, 2 * dout * ts, c.d_dpre,
-                                               dout * ts, dout * ts, n_in, cudaMemcpyDeviceToDevice, c.stream));
-                    dxg(c, n_in, din, 2 * dout, c.d_tfy, 2 * dout, c.Wcat[l - 1], 2 * dout, c.d_dx, din, nullptr, 0);
-                    if (c.n_halo > 0)
-                        dxg(c, c.n_halo, din, dout, static_cast<char*>(c.d_tfy) + n_in * 2 * dout * ts, 2 * dout,
-                            c.Wcat[l - 1], 2 * dout, static_cast<char*>(c.d_dx) + n_in * din * ts, din, nullptr, 0);
-                }
-            }
-            if (l == 1) break;   // R29
-        } else {
-        {
-            PhaseTimer t(c, BNS_PH_GEMM_BWD);
-            float* g = c.d_gflat + c.goff[l - 1];
-            auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
-            auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
-            wgrad(c, n_in, din, dout, c.Z[l], din, c.d_dpre, dout, g, dout);
-            if (sage) wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
-            if (l > 1) {
-                if (sage)
-                    dxg(c, n_in, 2 * din, dout, c.d_dpre, dout, c.Wt[l - 1], dout, c.d_dxcat, 2 * din, c.d_deg_in, din);
-                else
-                    dxg(c, n_in, din, dout, c.d_dpre, dout, c.Wt[l - 1], dout, c.d_dxcat, din, c.d_rs_in, din);
-            }
-        }
+        if (c.layer == BNS_LAYER_GAT) backward_layer_gat(c, ev, l, Hin);
+        else if ((c.tf_mask >> (l - 1)) & 1u) backward_layer_tf(c, ev, l, Hin);
+        else backward_layer_std(c, ev, l, Hin);
         if (l == 1) break;   // R29: no gradient w.r.t. the input features
-        {
-            PhaseTimer t(c, BNS_PH_SPMM_BWD);
-            SpmmArgs a{};
-            const bool eb = c.sampler != BNS_SAMPLER_BNS;   // f3: the sampled transposed CSR of this epoch
-            a.mode = sage ? SAGE_BWD : GCN_BWD;
-            a.segs = eb ? c.d_eseg_bwd : c.d_seg_bwd;
-            a.n_segs = c.n_seg_bwd;
-            a.col = eb ? c.d_ind_tcol : c.d_tcol;
-            a.src = c.d_dxcat;
-            a.ld_src = sage ? 2 * din : din;
-            a.out = c.d_dx;
-            a.ld_out = din;
-            a.self = static_cast<char*>(c.d_dxcat) + din * ts;
-            a.ld_self = 2 * din;
-            a.d = (int32_t)din;
-            a.n_in = n_in;
-            a.inv_p = inv_p;
-            a.nscale = c.nscale;
-            a.cscale = c.d_cscale;
-            a.partial = c.d_partial;
-            a.split = eb ? c.d_esplit_bwd : c.d_split_bwd;
-            a.n_split = c.n_split_bwd;
-            launch_spmm(c, a);
-        }
-        }
         if (dropout) {   // R38: gradient w.r.t. the dropped-out input -> w.r.t. the layer input (all stacked rows)
             PhaseTimer t(c, BNS_PH_UPDATE);
             launch_dropout(c, c.d_dx, c.d_dx, n_in + c.n_halo, din, l);
