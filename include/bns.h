@@ -11,9 +11,10 @@
  *
  * Process model: one context per process and GPU, rank r == partition id i, world == m.  The three main calls are
  * COLLECTIVE: every rank calls them in the same order with identical p / seed / epoch / lr.
- * Transports: NONE (world == 1), NCCL (one process per GPU; grouped ncclSend/ncclRecv + ncclAllReduce), or LOCAL
+ * Transports: NONE (world == 1), NCCL (one process per GPU; grouped ncclSend/ncclRecv + ncclAllReduce), LOCAL
  * (several contexts of one process, each driven by its own host thread; halo rows are pulled with device copies
- * -- used to run multi-partition parity on a single GPU).
+ * -- used to run multi-partition parity on a single GPU), or IPC (one process per GPU, peer memory: SURVEY §8(f) f1,
+ * see BNS_PEER_MEMORY).
  *
  * Readings of the paper where it is silent are numbered R1..R35.  The ones that
  * shape this ABI: R1 mean denominator = full-graph degree; R3 1/p applied on the receiving side as a column scale
@@ -62,8 +63,12 @@ typedef enum {
     BNS_TRANSPORT_NONE = 0,   /* world must be 1 */
     BNS_TRANSPORT_NCCL = 1,   /* cfg.nccl_id: 128-byte ncclUniqueId, identical on all ranks (bns_get_unique_id) */
     BNS_TRANSPORT_LOCAL = 2,  /* cfg.group: in-process group from bns_group_create(world) */
-    BNS_TRANSPORT_NULL_EMULATE = 3  /* BENCHMARKING ONLY: run one rank of an m-rank job alone on one GPU; the
+    BNS_TRANSPORT_NULL_EMULATE = 3, /* BENCHMARKING ONLY: run one rank of an m-rank job alone on one GPU; the
                                        exchanges and the all-reduce are no-ops, so outputs are not the method's */
+    BNS_TRANSPORT_IPC = 4     /* SURVEY §8(f) f1, one process per GPU (several processes may share a GPU): the exchanges
+                                 and the all-reduce run over peer memory (BNS_PEER_MEMORY semantics, implied).  Buffer
+                                 handles (cudaIpcMemHandle_t) and setup-time integers move through cfg.allgather; no
+                                 NCCL communicator is created.  cfg.allgather == NULL -> BNS_ERR_INVALID. */
 } bns_transport;
 
 /* cfg.flags */
@@ -82,6 +87,21 @@ typedef enum {
  * gathered locally from it (U_i ⊆ B_i) instead of being packed and exchanged: identical values, no layer-1 message
  * (R43).  Costs |B_i| x dims[0] stored elements of HBM. */
 #define BNS_CACHE_INPUT_HALO        0x20u
+/* SURVEY §8(f) f1, with transport LOCAL (IPC implies it): the exchange steps are fused with their producer / consumer
+ * over peer memory instead of staged copies --
+ *   a4 + a5: the receiving rank gathers its halo rows H_{U_i} straight from the owners' H^(l-1)
+ *            (one kernel; no pack, no send buffer, no message);
+ *   a11 + a12: each owner adds the peers' halo-row gradients of its rows read straight from the
+ *            peers' dX, local value first then peers ascending (R25; one kernel);
+ *   a13: every rank sums all ranks' weight gradients in rank order (bitwise equal on every rank).
+ * Ordering between ranks: device-side flag barriers (system-scope release / acquire, 20 s timeout -> the epoch
+ * fails with BNS_ERR_RUNTIME instead of hanging).  Results are bitwise those of the LOCAL transport. */
+#define BNS_PEER_MEMORY             0x40u
+
+/* Host all-gather used by BNS_TRANSPORT_IPC at setup (buffer handles, counts) and by debug exchanges: copy `bytes`
+ * bytes from `send` of every rank into recv[rank * bytes]; every rank calls it with the same `bytes`.  Return 0 on
+ * success.  Called only from inside bns_setup / bns_sample_boundary on the calling thread. */
+typedef int32_t (*bns_allgather_fn)(const void* send, void* recv, int64_t bytes, void* user);
 
 typedef struct bns_ctx bns_ctx;
 typedef struct bns_group bns_group;
@@ -101,7 +121,9 @@ typedef struct {
     double max_p;             /* halo capacity: <= 0 or >= 1 -> sized for p = 1 (|B_i| rows); else
                                  ceil(max_p*|B_i| + 8 sqrt(max_p*|B_i|) + 64) rows (R34) */
     uint32_t flags;           /* BNS_PLAN_ONLY | BNS_DEBUG_EXCHANGE_INDICES | BNS_TIMING | BNS_RETAIN_GRADS |
-                                 BNS_NO_TRANSFORM_FIRST | BNS_CACHE_INPUT_HALO */
+                                 BNS_NO_TRANSFORM_FIRST | BNS_CACHE_INPUT_HALO | BNS_PEER_MEMORY */
+    bns_allgather_fn allgather;   /* transport IPC: host all-gather over the ranks (e.g. a torch gloo group); else NULL */
+    void* allgather_user;         /* passed through to allgather */
 } bns_config;
 
 /* ncclGetUniqueId into out[128] (rank 0 calls it and broadcasts the bytes, e.g. over a torch process group). */
@@ -203,7 +225,9 @@ typedef enum {
     BNS_Q_KERNEL_COUNT = 19, /* int64[1]: kernels launched by this context since setup */
     BNS_Q_INDUCED_T = 20,    /* edge samplers: int64[n_in+n_bd+1] row pointers then int32[nnz] local inner columns
                                 of the sampled TRANSPOSED aggregation (rows: inner u, then boundary index b) */
-    BNS_Q_TF_LAYERS = 21     /* int32[1]: bit l-1 set <=> layer l runs transform-first (R42) */
+    BNS_Q_TF_LAYERS = 21,    /* int32[1]: bit l-1 set <=> layer l runs transform-first (R42) */
+    BNS_Q_BOUNDARY_ROW = 22  /* int32[n_bd]: row of B_i[b] in its owner's V_j, i.e. where the peer-memory pull reads
+                                it (f1; plan, available in BNS_PLAN_ONLY) */
 } bns_query_what;
 
 enum { BNS_PH_SAMPLE = 0, BNS_PH_INDUCE, BNS_PH_PACK, BNS_PH_EXCHANGE, BNS_PH_SPMM_FWD, BNS_PH_GEMM_FWD,

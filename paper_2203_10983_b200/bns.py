@@ -19,12 +19,14 @@ LIB_PATH = os.environ.get("BNS_LIB") or os.path.join(_HERE, "libbns.so")   # BNS
 BNS_OK, BNS_ERR_INVALID, BNS_ERR_RUNTIME, BNS_ERR_STATE, BNS_ERR_OOM, BNS_ERR_NONFINITE = range(6)
 BNS_LAYER_SAGE_MEAN, BNS_LAYER_GCN, BNS_LAYER_GAT = 0, 1, 2
 BNS_FP32, BNS_BF16 = 0, 1
-BNS_TRANSPORT_NONE, BNS_TRANSPORT_NCCL, BNS_TRANSPORT_LOCAL, BNS_TRANSPORT_NULL_EMULATE = 0, 1, 2, 3
+BNS_TRANSPORT_NONE, BNS_TRANSPORT_NCCL, BNS_TRANSPORT_LOCAL, BNS_TRANSPORT_NULL_EMULATE, BNS_TRANSPORT_IPC = 0, 1, 2, 3, 4
 BNS_PLAN_ONLY, BNS_DEBUG_EXCHANGE_INDICES, BNS_TIMING, BNS_RETAIN_GRADS, BNS_NO_TRANSFORM_FIRST = 0x1, 0x2, 0x4, 0x8, 0x10
 BNS_CACHE_INPUT_HALO = 0x20
+BNS_PEER_MEMORY = 0x40   # f1: exchanges fused over peer memory (LOCAL in-process; implied by IPC)
 (BNS_Q_COUNTS, BNS_Q_INNER, BNS_Q_BOUNDARY, BNS_Q_BOUNDARY_OFF, BNS_Q_SENDCAND, BNS_Q_SENDCAND_OFF, BNS_Q_MASK,
  BNS_Q_HALO, BNS_Q_HALO_OFF, BNS_Q_SEND, BNS_Q_SEND_OFF, BNS_Q_H, BNS_Q_Z, BNS_Q_DH, BNS_Q_HALO_ROWS, BNS_Q_INDUCED,
- BNS_Q_TIMES, BNS_Q_STATIC_CSR, BNS_Q_MEMORY, BNS_Q_KERNEL_COUNT, BNS_Q_INDUCED_T, BNS_Q_TF_LAYERS) = range(22)
+ BNS_Q_TIMES, BNS_Q_STATIC_CSR, BNS_Q_MEMORY, BNS_Q_KERNEL_COUNT, BNS_Q_INDUCED_T, BNS_Q_TF_LAYERS,
+ BNS_Q_BOUNDARY_ROW) = range(23)
 BNS_SAMPLER_BNS, BNS_SAMPLER_BES, BNS_SAMPLER_DROPEDGE = 0, 1, 2
 PHASES = ["sample", "induce", "pack", "exchange", "spmm_fwd", "gemm_fwd", "loss", "gemm_bwd", "spmm_bwd",
           "exchange_bwd", "scatter", "allreduce", "update", "epoch_total", "sample_total"]
@@ -40,12 +42,34 @@ class BnsError(RuntimeError):
         self.code = code
 
 
+# bns_allgather_fn: int32 (*)(const void* send, void* recv, int64 bytes, void* user)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+
+
 class bns_config(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("transport", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("group", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("num_layers", ctypes.c_int32), ("dims", ctypes.c_void_p),
                 ("layer", ctypes.c_int32), ("precision", ctypes.c_int32), ("max_p", ctypes.c_double),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("allgather", ALLGATHER_FN), ("allgather_user", ctypes.c_void_p)]
+
+
+def torch_allgather(world: int, group=None):
+    """A bns_allgather_fn over a torch.distributed CPU (gloo) group -- host bytes only (buffer handles, counts)."""
+    import torch
+    import torch.distributed as dist
+
+    def cb(send, recv, nbytes, user):
+        try:
+            src = torch.tensor(np.frombuffer(ctypes.string_at(send, nbytes), np.uint8))
+            out = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(out, src, group=group)
+            ctypes.memmove(recv, np.concatenate([o.numpy() for o in out]).ctypes.data, nbytes * world)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
+            return 1
+
+    return ALLGATHER_FN(cb)
 
 
 _LIB = None
@@ -179,7 +203,7 @@ class Context:
 
     def __init__(self, *, rank: int, world: int, dims: Sequence[int], layer: int, precision: int, indptr, indices,
                  part_of, features, labels, device: int = 0, transport: int | None = None, nccl_id: bytes | None = None,
-                 group=None, max_p: float = 0.0, flags: int = 0, stream: int | None = None):
+                 group=None, max_p: float = 0.0, flags: int = 0, stream: int | None = None, allgather=None):
         self.indptr = np.ascontiguousarray(indptr, np.int64)
         self.indices = np.ascontiguousarray(indices, np.int32)
         self.part_of = np.ascontiguousarray(part_of, np.int32)
@@ -191,10 +215,12 @@ class Context:
         if transport is None:
             transport = BNS_TRANSPORT_NONE if world == 1 else (BNS_TRANSPORT_LOCAL if group else BNS_TRANSPORT_NCCL)
         self._id = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        self._allgather = allgather   # keep the ctypes callback alive as long as the context
         cfg = bns_config(rank=rank, world=world, device=device, transport=transport,
                          nccl_id=ctypes.addressof(self._id) if self._id else None, group=group, stream=stream,
                          num_layers=self.L, dims=self.dims.ctypes.data, layer=layer, precision=precision,
-                         max_p=max_p, flags=flags)
+                         max_p=max_p, flags=flags, allgather=allgather if allgather else ALLGATHER_FN(),
+                         allgather_user=None)
         self.h = bns_setup(cfg, self.indptr, self.indices, self.part_of, self.features, self.labels)
         # host inputs are only borrowed during setup
         self.indptr = self.indices = self.part_of = self.features = None

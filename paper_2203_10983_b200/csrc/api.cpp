@@ -85,8 +85,11 @@ void validate(const bns_config* cfg, int64_t N, const int64_t* indptr, const int
         throw Error(BNS_ERR_INVALID, "bad layer");
     if (cfg->precision != BNS_FP32 && cfg->precision != BNS_BF16) throw Error(BNS_ERR_INVALID, "bad precision");
     if (cfg->world > 1 && cfg->transport != BNS_TRANSPORT_NCCL && cfg->transport != BNS_TRANSPORT_LOCAL &&
-        cfg->transport != BNS_TRANSPORT_NULL_EMULATE && !(cfg->flags & BNS_PLAN_ONLY))
-        throw Error(BNS_ERR_INVALID, "world > 1 needs transport NCCL or LOCAL");
+        cfg->transport != BNS_TRANSPORT_NULL_EMULATE && cfg->transport != BNS_TRANSPORT_IPC &&
+        !(cfg->flags & BNS_PLAN_ONLY))
+        throw Error(BNS_ERR_INVALID, "world > 1 needs transport NCCL, LOCAL or IPC");
+    if (cfg->transport == BNS_TRANSPORT_IPC && !cfg->allgather && !(cfg->flags & BNS_PLAN_ONLY))
+        throw Error(BNS_ERR_INVALID, "transport IPC needs cfg.allgather");
     if (N < 1 || !indptr || !indices || !part_of) throw Error(BNS_ERR_INVALID, "empty graph or NULL arrays");
     if (N >= INT32_MAX) throw Error(BNS_ERR_INVALID, "num_nodes must fit int32");
     if (indptr[0] != 0) throw Error(BNS_ERR_INVALID, "indptr[0] != 0");
@@ -491,6 +494,8 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     const float inv_p = (c.n_halo > 0) ? (float)c.inv_p : 1.f;
 
     std::unique_ptr<PhaseTimer> total(new PhaseTimer(c, BNS_PH_EPOCH_TOTAL));
+    const bool peer = m > 1 && c.tr && c.tr->peer();   // f1: exchanges fused over peer memory
+    if (peer) c.tr->begin_epoch(c);
     // weights may be host or device pointers
     cudaPointerAttributes attr{};
     bool host_w = false;
@@ -537,6 +542,9 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             PhaseTimer t(c, BNS_PH_PACK);
             launch_pack_rows(c, c.d_x0cache, din, c.d_cand_out, c.n_halo, static_cast<char*>(Hin) + n_in * din * ts,
                              (int32_t)din);
+        } else if (peer) {   // f1: pack + exchange = one gather from the owners' H^(l-1)
+            PhaseTimer t(c, BNS_PH_EXCHANGE);
+            c.tr->halo_pull(c, l, static_cast<char*>(Hin) + n_in * din * ts, din);
         } else if (m > 1) {
             {
                 PhaseTimer t(c, BNS_PH_PACK);
@@ -578,6 +586,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             launch_relu_mask(c, c.d_dx, c.H[l], dout, n_in, (int32_t)dout, c.d_dpre, tfl ? c.d_deg_in : nullptr,
                              tfl ? c.d_dxcat : nullptr);
         }
+        if (peer) c.d_dx = c.tr->dx_buffer(c, l);   // f1: layer l's dX; a peer may still read layer l+1's
         if (c.layer == BNS_LAYER_GAT) backward_layer_gat(c, ev, l, Hin);
         else if ((c.tf_mask >> (l - 1)) & 1u) backward_layer_tf(c, ev, l, Hin);
         else backward_layer_std(c, ev, l, Hin);
@@ -586,7 +595,10 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
             PhaseTimer t(c, BNS_PH_UPDATE);
             launch_dropout(c, c.d_dx, c.d_dx, n_in + c.n_halo, din, l);
         }
-        if (m > 1) {
+        if (peer) {   // f1: reverse exchange + scatter-add = one gather from the peers' dX halo rows
+            PhaseTimer t(c, BNS_PH_SCATTER);
+            c.tr->grad_scatter(c, l, din);
+        } else if (m > 1) {
             {
                 PhaseTimer t(c, BNS_PH_EXCHANGE_BWD);
                 c.tr->exchange(c, static_cast<char*>(c.d_dx) + n_in * din * ts, c.recv_off.data(), c.d_gradbuf,
@@ -857,6 +869,7 @@ bns_status bns_query(bns_ctx* h, int32_t what, int32_t layer, void* dst, int64_t
             case BNS_Q_INNER: put(P.V.data(), P.V.size() * 4); break;
             case BNS_Q_BOUNDARY: put(P.B.data(), P.B.size() * 4); break;
             case BNS_Q_BOUNDARY_OFF: put(P.B_off.data(), P.B_off.size() * 8); break;
+            case BNS_Q_BOUNDARY_ROW: put(P.B_row.data(), P.B_row.size() * 4); break;
             case BNS_Q_SENDCAND: {
                 std::vector<int32_t> g(P.D_local.size());
                 for (size_t k = 0; k < g.size(); ++k) g[k] = P.V[P.D_local[k]];

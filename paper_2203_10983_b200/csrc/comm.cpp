@@ -7,6 +7,9 @@
 // stacked feature buffer (no staging on the receive side); the weight-gradient sum is one ncclAllReduce.
 // LOCAL: several contexts in one process (one host thread each); every rank PULLS the rows addressed to it with
 // device-to-device copies after a host barrier, ordered by CUDA events.  The sum is taken in rank order.
+// PEER (LOCAL + BNS_PEER_MEMORY, or IPC): the exchanges are fused into gather kernels that read the
+// other ranks' buffers directly (peer.cu), ordered by device flag barriers; buffer pointers are shared at setup
+// (in-process: raw pointers through the group; IPC: cudaIpcMemHandle_t through the caller's host all-gather).
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
@@ -31,6 +34,7 @@ struct bns_group {
     std::vector<float*> fbuf;
     std::vector<double*> dbuf;
     std::vector<int> attached;
+    std::vector<const void*> blob;   // host all-gather staging (peer-memory transport in-process)
 };
 
 namespace bns {
@@ -215,9 +219,216 @@ struct NullTransport : Transport {
     void poll(Ctx&) override {}
 };
 
+// ---------------------------------------------------------------------------------------------
+// Peer-memory transport (f1).  Shared buffers per rank, in table order (kind k, rank j) -> d_tab[k m + j]:
+//   H^(0..L-1), dX (two alternating buffers), partial weight gradients (two, by all-reduce parity), loss scalars
+//   (two), compaction segment offsets, barrier flags, send buffer (setup-time / debug generic exchange only)
+// ---------------------------------------------------------------------------------------------
+struct PeerTransport : Transport {
+    bns_group* g = nullptr;                      // in-process group (LOCAL), else null
+    bns_allgather_fn ag = nullptr;               // IPC host all-gather
+    void* ag_user = nullptr;
+    int m, me, L;
+    enum { K_DX = 0, K_G = 2, K_S = 4, K_SEG = 6, K_FLAGS = 7, K_SEND = 8, K_H = 9 };
+    int nk;
+    std::vector<void*> own;                      // my buffers in kind order
+    std::vector<void*> opened;                   // IPC mappings to close
+    void** d_tab = nullptr;                      // nk x m device table
+    int64_t* d_pnin = nullptr;                   // n_in of every rank
+    int64_t* d_delta = nullptr;                  // row offset of my rows in each peer's halo gradient
+    int32_t* d_owner_of_b = nullptr;             // owner rank of every boundary node
+    int32_t* d_row_of_b = nullptr;               // ... and its row in the owner's H
+    uint64_t* d_flags = nullptr;
+    void *dx2 = nullptr, *g2 = nullptr, *s2 = nullptr;
+    int* h_err = nullptr;                        // mapped pinned: barrier timeout flag
+    int* d_err = nullptr;
+    uint64_t bar = 0, ar_count = 0;
+    bool first = true;
+
+    PeerTransport(Ctx& c, bns_group* grp, bns_allgather_fn fn, void* user)
+        : g(grp), ag(fn), ag_user(user), m(c.cfg.world), me(c.cfg.rank), L(c.L) {
+        if (m > 32) throw Error(BNS_ERR_INVALID, "peer-memory transport: world <= 32");
+        if (g) {
+            if (g->world != m) throw Error(BNS_ERR_INVALID, "local group size != cfg.world");
+            std::lock_guard<std::mutex> lk(g->mu);
+            if (g->attached[me]) throw Error(BNS_ERR_INVALID, "local group: rank attached twice");
+            g->attached[me] = 1;
+        }
+        preload_module_functions();
+        const Plan& P = c.plan;
+        const size_t ts = c.prec == BNS_BF16 ? 2 : 4;
+        const size_t dxb = (size_t)(P.n_in + c.halo_cap) * c.maxd * ts;
+        BNS_CUDA(cudaMalloc(&dx2, dxb ? dxb : 16));
+        BNS_CUDA(cudaMalloc(&g2, c.gflat_n * sizeof(float) + 16));
+        BNS_CUDA(cudaMemset(g2, 0, c.gflat_n * sizeof(float) + 16));
+        BNS_CUDA(cudaMalloc(&s2, 4 * sizeof(double)));
+        BNS_CUDA(cudaMemset(s2, 0, 4 * sizeof(double)));
+        BNS_CUDA(cudaMalloc(&d_flags, 32 * sizeof(uint64_t)));
+        BNS_CUDA(cudaMemset(d_flags, 0, 32 * sizeof(uint64_t)));
+        BNS_CUDA(cudaMalloc(&d_delta, 32 * sizeof(int64_t)));
+        BNS_CUDA(cudaMemset(d_delta, 0, 32 * sizeof(int64_t)));
+        BNS_CUDA(cudaHostAlloc(&h_err, sizeof(int), cudaHostAllocMapped));
+        *h_err = 0;
+        BNS_CUDA(cudaHostGetDevicePointer((void**)&d_err, h_err, 0));
+        std::vector<int32_t> owner(P.n_bd + 1, 0);
+        for (int j = 0; j < m; ++j)
+            for (int64_t b = P.B_off[j]; b < P.B_off[j + 1]; ++b) owner[b] = j;
+        std::vector<int32_t> row(P.B_row);
+        row.push_back(0);
+        BNS_CUDA(cudaMalloc(&d_owner_of_b, owner.size() * 4));
+        BNS_CUDA(cudaMalloc(&d_row_of_b, row.size() * 4));
+        BNS_CUDA(cudaMemcpy(d_owner_of_b, owner.data(), owner.size() * 4, cudaMemcpyHostToDevice));
+        BNS_CUDA(cudaMemcpy(d_row_of_b, row.data(), row.size() * 4, cudaMemcpyHostToDevice));
+
+        nk = K_H + L;
+        own.assign(nk, nullptr);
+        own[K_DX] = c.d_dx;      own[K_DX + 1] = dx2;
+        own[K_G] = c.d_gflat;    own[K_G + 1] = g2;
+        own[K_S] = c.d_scal;     own[K_S + 1] = s2;
+        own[K_SEG] = c.d_seg_pos;
+        own[K_FLAGS] = d_flags;
+        own[K_SEND] = c.d_sendbuf;
+        for (int l = 0; l < L; ++l) own[K_H + l] = c.H[l];
+        std::vector<void*> tab((size_t)nk * m, nullptr);
+        if (g) {   // same process: raw pointers
+            std::vector<void*> all((size_t)nk * m);
+            allgather(c, own.data(), all.data(), nk * sizeof(void*));
+            for (int j = 0; j < m; ++j)
+                for (int k = 0; k < nk; ++k) tab[(size_t)k * m + j] = all[(size_t)j * nk + k];
+        } else {   // IPC handles
+            std::vector<cudaIpcMemHandle_t> mine(nk), all((size_t)nk * m);
+            for (int k = 0; k < nk; ++k) BNS_CUDA(cudaIpcGetMemHandle(&mine[k], own[k]));
+            allgather(c, mine.data(), all.data(), nk * sizeof(cudaIpcMemHandle_t));
+            for (int j = 0; j < m; ++j)
+                for (int k = 0; k < nk; ++k) {
+                    void* p = own[k];
+                    if (j != me) {
+                        BNS_CUDA(cudaIpcOpenMemHandle(&p, all[(size_t)j * nk + k], cudaIpcMemLazyEnablePeerAccess));
+                        opened.push_back(p);
+                    }
+                    tab[(size_t)k * m + j] = p;
+                }
+        }
+        BNS_CUDA(cudaMalloc(&d_tab, tab.size() * sizeof(void*)));
+        BNS_CUDA(cudaMemcpy(d_tab, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        std::vector<int64_t> nin(m);
+        const int64_t my_nin = P.n_in;
+        allgather(c, &my_nin, nin.data(), sizeof(int64_t));
+        BNS_CUDA(cudaMalloc(&d_pnin, m * sizeof(int64_t)));
+        BNS_CUDA(cudaMemcpy(d_pnin, nin.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice));
+        // the caller's allocations are complete on every rank before anyone's first barrier
+        int ok = 1;
+        std::vector<int> oks(m);
+        allgather(c, &ok, oks.data(), sizeof(int));
+    }
+    ~PeerTransport() override {
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
+        for (void* p : {(void*)d_tab, (void*)d_pnin, (void*)d_delta, (void*)d_owner_of_b, (void*)d_row_of_b,
+                        (void*)d_flags, dx2, g2, s2})
+            if (p) cudaFree(p);
+        if (h_err) cudaFreeHost(h_err);
+        if (g) {
+            std::lock_guard<std::mutex> lk(g->mu);
+            g->attached[me] = 0;
+        }
+    }
+    void allgather(Ctx&, const void* mine, void* all, size_t bytes) {
+        if (g) {
+            g->blob[me] = mine;
+            group_barrier(g);
+            for (int j = 0; j < m; ++j) std::memcpy(static_cast<char*>(all) + j * bytes, g->blob[j], bytes);
+            group_barrier(g);
+        } else {
+            if (ag(mine, all, (int64_t)bytes, ag_user) != 0)
+                throw Error(BNS_ERR_RUNTIME, "peer-memory transport: host all-gather callback failed");
+        }
+    }
+    void* const* row(int k) const { return d_tab + (size_t)k * m; }
+    void barrier(Ctx& c, bool fetch) {
+        launch_peer_barrier(c, reinterpret_cast<uint64_t* const*>(row(K_FLAGS)), ++bar, d_err,
+                            fetch ? reinterpret_cast<const int64_t* const*>(row(K_SEG)) : nullptr, d_pnin,
+                            fetch ? d_delta : nullptr);
+    }
+    bool peer() const override { return true; }
+    void begin_epoch(Ctx& c) override {
+        const int q = (int)(ar_count & 1);
+        c.d_gflat = static_cast<float*>(own[K_G + q]);
+        c.d_scal = static_cast<double*>(own[K_S + q]);
+        c.d_dx = own[K_DX];
+        first = true;
+    }
+    void halo_pull(Ctx& c, int l, void* dst_halo, int64_t din) override {
+        barrier(c, true);   // the owners' H^(l-1) is complete; also fetch the peers' segment offsets
+        first = false;
+        launch_halo_pull(c, dst_halo, din, row(K_H + l - 1), d_owner_of_b, d_row_of_b, (int32_t)din);
+    }
+    void* dx_buffer(Ctx&, int l) override { return own[K_DX + (l & 1)]; }
+    void grad_scatter(Ctx& c, int l, int64_t din) override {
+        barrier(c, first);   // the peers' halo gradients of layer l are complete
+        first = false;
+        launch_scatter_peer(c, c.d_dx, din, row(K_DX + (l & 1)), d_delta, (int32_t)din);
+    }
+    void exchange(Ctx& c, const void* src, const int64_t* src_off, void* dst, const int64_t* dst_off,
+                  size_t rowbytes) override {
+        if (src != c.d_sendbuf) throw Error(BNS_ERR_RUNTIME, "peer-memory transport: generic exchange needs the send buffer");
+        std::vector<int64_t> offs((size_t)(m + 1) * m);
+        allgather(c, src_off, offs.data(), (m + 1) * sizeof(int64_t));
+        std::vector<void*> send(m);
+        BNS_CUDA(cudaMemcpy(send.data(), row(K_SEND), m * sizeof(void*), cudaMemcpyDeviceToHost));
+        barrier(c, false);
+        for (int j = 0; j < m; ++j) {
+            if (j == me) continue;
+            const int64_t* oj = offs.data() + (size_t)j * (m + 1);
+            const int64_t n = oj[me + 1] - oj[me];
+            if (n != dst_off[j + 1] - dst_off[j])
+                throw Error(BNS_ERR_RUNTIME, "peer-memory transport: row count mismatch between ranks " +
+                                                 std::to_string(j) + " -> " + std::to_string(me));
+            if (n > 0)
+                BNS_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + dst_off[j] * rowbytes,
+                                         static_cast<const char*>(send[j]) + oj[me] * rowbytes, n * rowbytes,
+                                         cudaMemcpyDeviceToDevice, c.stream));
+        }
+        barrier(c, false);   // peers have finished reading my send buffer
+    }
+    void allreduce(Ctx& c, float* buf, int64_t n, double* scal, int64_t ns) override {
+        const int q = (int)(ar_count & 1);
+        if (buf != own[K_G + q] || scal != own[K_S + q])
+            throw Error(BNS_ERR_RUNTIME, "peer-memory transport: all-reduce of an unregistered buffer");
+        barrier(c, false);   // every rank's partial gradients are complete
+        float* gout = static_cast<float*>(own[K_G + (q ^ 1)]);
+        double* sout = static_cast<double*>(own[K_S + (q ^ 1)]);
+        launch_sum_ptrs(c, reinterpret_cast<const float* const*>(row(K_G + q)), m, gout, n);
+        launch_sum_ptrs_d(c, reinterpret_cast<const double* const*>(row(K_S + q)), m, sout, ns);
+        // no second barrier: a peer reads my buffer q again only after the next epoch's barriers (ping-pong)
+        c.d_gflat = gout;
+        c.d_scal = sout;
+        ++ar_count;
+    }
+    int64_t allreduce_host_i64(Ctx& c, int64_t v) override {
+        std::vector<int64_t> all(m);
+        allgather(c, &v, all.data(), sizeof(int64_t));
+        int64_t s = 0;
+        for (int64_t x : all) s += x;
+        return s;
+    }
+    void poll(Ctx&) override {
+        if (*(volatile int*)h_err)
+            throw Error(BNS_ERR_RUNTIME, "peer-memory transport: device barrier timed out (a rank did not reach the "
+                                         "collective within 20 s)");
+    }
+};
+
 }  // namespace
 
 Transport* make_transport(Ctx& c) {
+    if (c.cfg.transport == BNS_TRANSPORT_IPC) {
+        if (!c.cfg.allgather) throw Error(BNS_ERR_INVALID, "transport IPC needs cfg.allgather");
+        return new PeerTransport(c, nullptr, c.cfg.allgather, c.cfg.allgather_user);
+    }
+    if (c.cfg.transport == BNS_TRANSPORT_LOCAL && (c.cfg.flags & BNS_PEER_MEMORY) && c.cfg.world > 1) {
+        if (!c.cfg.group) throw Error(BNS_ERR_INVALID, "transport LOCAL needs cfg.group");
+        return new PeerTransport(c, c.cfg.group, nullptr, nullptr);
+    }
     switch (c.cfg.transport) {
         case BNS_TRANSPORT_NULL_EMULATE:
             return new NullTransport();
@@ -256,6 +467,7 @@ bns_status bns_group_create(int32_t world, bns_group** out) {
     g->fbuf.assign(world, nullptr);
     g->dbuf.assign(world, nullptr);
     g->attached.assign(world, 0);
+    g->blob.assign(world, nullptr);
     *out = g;
     return BNS_OK;
 }

@@ -49,6 +49,7 @@ struct Plan {
     std::vector<int64_t> br_ptr;              // boundary rows: inner neighbours of each b (local ids ascending)
     std::vector<int32_t> br_col;
     std::vector<float> deg_in, deg_bd;        // full-graph degrees deg_G
+    std::vector<int32_t> B_row;               // row of B[b] in its owner's V (f1 peer-memory pull)
 };
 
 void build_plan(Plan& P, int rank, int world, int64_t N, const int64_t* indptr, const int32_t* indices,

@@ -113,6 +113,15 @@ void launch_sum_ptrs(Ctx& c, const float* const* d_ptrs, int nptr, float* out, i
 void launch_sum_ptrs_d(Ctx& c, const double* const* d_ptrs, int nptr, double* out, int64_t n);
 void launch_fill_rowscale_bwd(Ctx& c, float* rs);
 void launch_gcn_cscale(Ctx& c);
+// f1 peer-memory exchange (peer.cu): device flag barrier over the ranks' flag slots (+ the per-peer row offsets of
+// this rank's rows in the peers' halo gradients), fused pack + forward exchange (gather from the owners' H), fused
+// reverse exchange + scatter-add (gather from the peers' dX halo rows)
+void preload_module_functions();   // load every kernel now (lazy loading would wait on a spinning barrier)
+void launch_peer_barrier(Ctx& c, uint64_t* const* d_flags, uint64_t val, int* err, const int64_t* const* d_pseg,
+                         const int64_t* d_pnin, int64_t* d_delta);
+void launch_halo_pull(Ctx& c, void* dst, int64_t ld, void* const* d_peerH, const int32_t* d_owner_of_b,
+                      const int32_t* d_row_of_b, int32_t d);
+void launch_scatter_peer(Ctx& c, void* dst, int64_t ld, void* const* d_peerdx, const int64_t* d_delta, int32_t d);
 void launch_to_storage(Ctx& c, const float* src, int64_t rows, int32_t dlog, int64_t ld_src, void* dst, int64_t ld_dst);
 
 }  // namespace bns

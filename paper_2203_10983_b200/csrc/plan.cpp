@@ -42,6 +42,14 @@ void build_plan(Plan& P, int rank, int world, int64_t N, const int64_t* indptr, 
     P.B_off[world] = (int64_t)P.B.size();
     P.n_bd = (int64_t)P.B.size();
     for (int64_t b = 0; b < P.n_bd; ++b) bidx[P.B[b]] = (int32_t)b;
+    {   // owner-local row of every boundary node: its rank among the owner's nodes in ascending gid
+        std::vector<int32_t> seen(world, 0);
+        P.B_row.assign(P.n_bd, 0);
+        for (int64_t u = 0; u < N; ++u) {
+            const int32_t r = seen[part_of[u]]++;
+            if (bidx[u] >= 0) P.B_row[bidx[u]] = r;
+        }
+    }
 
     // D_{i->j}: inner v with >= 1 neighbour in partition j != i, ascending gid
     std::vector<std::vector<int32_t>> D(world);

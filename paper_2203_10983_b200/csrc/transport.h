@@ -16,7 +16,19 @@ struct Transport {
     virtual int64_t allreduce_host_i64(Ctx& c, int64_t v) = 0;
     // Raise a pending asynchronous communicator error.
     virtual void poll(Ctx& c) = 0;
+    // f1 peer-memory transports only (peer() == true): bns_epoch then calls begin_epoch once, halo_pull instead of
+    // pack + exchange (forward layer l: the halo rows of H^(l-1) read from the owners), dx_buffer(l) as the layer-l
+    // input-gradient buffer (alternating, so a peer may still read layer l+1's halo gradients), and grad_scatter
+    // instead of reverse exchange + scatter-add (c.d_dx inner rows += the peers' halo gradients of this rank's rows).
+    // allreduce() then leaves the sum in a second buffer and repoints c.d_gflat / c.d_scal at it.
+    virtual bool peer() const { return false; }
+    virtual void begin_epoch(Ctx&) {}
+    virtual void halo_pull(Ctx&, int /*l*/, void* /*dst_halo*/, int64_t /*din*/) {}
+    virtual void* dx_buffer(Ctx& c, int /*l*/);
+    virtual void grad_scatter(Ctx&, int /*l*/, int64_t /*din*/) {}
 };
+
+inline void* Transport::dx_buffer(Ctx& c, int) { return c.d_dx; }
 
 Transport* make_transport(Ctx& c);
 

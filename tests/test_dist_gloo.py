@@ -5,7 +5,9 @@
 * the recomputed send lists S_{i,j} = {u in D_{i->j} : keep(u, j)} equal the owner-i segment of U_j (Alg.1 l.6-7,
   R27) -- the draw here is the oracle's Philox (test infrastructure), the GPU draw is checked bit-exact elsewhere;
 * per-peer row counts agree pairwise (the NCCL send/recv sizes);
-* bench.py's max-over-ranks timing reduction.
+* bench.py's max-over-ranks timing reduction;
+* f1 peer memory: the owner-row map the fused pull reads through (V_j[B_row[b]] == B[b]) and the host all-gather
+  callback that carries the CUDA IPC handles (bns.torch_allgather) called through its C function pointer.
 """
 import os
 import socket
@@ -89,6 +91,25 @@ def worker(rank, world, port, N, nnz, q):
                     dist.recv(got, j)
                     dist.send(out, j)
                 assert got[:-1].tolist() == U[Uoff[j]:Uoff[j + 1]]
+        # f1: owner rows of the boundary nodes, checked against the owners' own V lists
+        Brow = ctx.i32(bns.BNS_Q_BOUNDARY_ROW)
+        V = ctx.i32(bns.BNS_Q_INNER).tolist()
+        allV = [None] * world
+        dist.all_gather_object(allV, V)
+        for j in range(world):
+            for b in range(Boff[j], Boff[j + 1]):
+                assert allV[j][Brow[b]] == B[b]
+        # f1: the IPC host all-gather through its ctypes function pointer (what libbns calls)
+        import ctypes
+        fn = bns.torch_allgather(world)
+        nb = 67
+        send = np.arange(nb, dtype=np.uint8) + np.uint8(rank * 50)
+        recv = np.zeros(nb * world, np.uint8)
+        cfn = ctypes.cast(fn, ctypes.c_void_p).value
+        call = bns.ALLGATHER_FN(cfn)
+        assert call(send.ctypes.data, recv.ctypes.data, nb, None) == 0
+        for j in range(world):
+            assert np.array_equal(recv[j * nb:(j + 1) * nb], np.arange(nb, dtype=np.uint8) + np.uint8(j * 50))
         # max over ranks
         m = bench.max_over_ranks(float(rank + 1) * 1.5, dist, "cpu")
         assert m == 1.5 * world
