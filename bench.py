@@ -55,6 +55,9 @@ def parse():
                     help="gat: the paper's 2-layer GAT ablation (f4, Table tab:gat, PAPER.md:691-709; R45)")
     ap.add_argument("--multilabel", action="store_true",
                     help="f4: sigmoid BCE + F1-micro on seeded multi-hot targets (the Yelp task, PAPER.md:384)")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N > 1: ipc = exchanges fused over NVLink peer memory (SURVEY §8(f) f1, default); "
+                         "nccl = pack + grouped ncclSend/ncclRecv + ncclAllReduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-scale", type=float, default=64.0, help="oracle sample = workload scaled down by this")
     ap.add_argument("--no-e2e", action="store_true")
@@ -301,9 +304,19 @@ def run_ours(args):
     assert world == args.gpus or world == 1, "launch with torchrun --nproc-per-node N for --gpus N"
     if args.gpus > 1 and world == 1:
         raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    # BNS_BENCH_SHARED_GPU=1 (functional check of the N > 1 code path on a one-GPU box; NOT a measurement): every
+    # rank on cuda:0, gloo process group, transport ipc
+    shared = os.environ.get("BNS_BENCH_SHARED_GPU") == "1" and world > 1
+    if shared:
+        local = 0
+        assert args.transport == "ipc", "a shared GPU needs --transport ipc (NCCL refuses duplicate GPUs)"
+    pg_dev = "cpu" if shared else "cuda"
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     shape = I.SHAPES[args.config]
     shape.p = args.p
     if args.model == "gat":
@@ -317,13 +330,17 @@ def run_ours(args):
     X = I.features(inner, shape.d0)
     y_all = I.labels(shape.N, shape.C, shape.train_frac)
     y = np.ascontiguousarray(y_all[inner])
-    nccl_id = None
-    if world > 1:
+    nccl_id, transport, allgather = None, None, None
+    if world > 1 and args.transport == "nccl":
         obj = [bns.bns_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    elif world > 1:   # f1: peer memory; CUDA IPC handles travel over a gloo group
+        transport = bns.BNS_TRANSPORT_IPC
+        allgather = bns.torch_allgather(world, None if shared else dist.new_group(backend="gloo"))
     ctx = bns.Context(rank=rank, world=world, dims=shape.dims, layer=shape.layer, precision=prec, indptr=indptr,
                       indices=indices, part_of=part, features=X, labels=y, device=local, nccl_id=nccl_id,
+                      transport=transport, allgather=allgather,
                       max_p=0.0, flags=bns.BNS_TIMING | (bns.BNS_CACHE_INPUT_HALO if world > 1 else 0))
     if args.multilabel:
         ctx.set_multilabel(I.multilabels(shape.N, shape.C, 0.1)[inner])
@@ -386,7 +403,7 @@ def run_ours(args):
     t1_times = ctx.times()
     ph = {k: (t1_times[k] - t0_times[k]) / args.steps for k in t1_times}
     cnt = ctx.counts()
-    total_max = max_over_ranks(total_ms, dist, "cuda") if world > 1 else total_ms
+    total_max = max_over_ranks(total_ms, dist, pg_dev) if world > 1 else total_ms
     ms_per_step = total_max / args.steps
     value = 1000.0 / ms_per_step
 
@@ -409,7 +426,7 @@ def run_ours(args):
             b.synchronize()
             e_ms += a.elapsed_time(b)
         if world > 1:
-            e_ms = max_over_ranks(e_ms, dist, "cuda")
+            e_ms = max_over_ranks(e_ms, dist, pg_dev)
         wbytes = sum(w.numel() * 4 for w in Wh)
         e2e = {"value": 1000.0 * args.steps / e_ms, "unit": UNIT, "h2d_bytes_per_step": wbytes,
                "d2h_bytes_per_step": 2 * wbytes + 16,
@@ -418,7 +435,7 @@ def run_ours(args):
     # ---- per-rank partition stats (Table tab:partition style)
     stats = np.array([cnt["n_in"], cnt["n_bd"], cnt["n_halo"], cnt["nnz"], cnt["nnz_kept"]], np.float64)
     if world > 1:
-        t = torch.tensor(stats, device="cuda")
+        t = torch.tensor(stats, device=pg_dev)
         allst = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(allst, t)
         allst = [a.cpu().numpy() for a in allst]
@@ -451,6 +468,9 @@ def run_ours(args):
             "data": "synthetic: R-MAT graph (Graph500 a,b,c=.57,.19,.19), Philox features/labels, Glorot weights",
             "config": {"workload": workload_name(shape, args.p, world, args.partition), "nnz_actual": int(indptr[-1]),
                        "global_batch": "full graph", "parallelism": f"partition-parallel m={world}",
+                       "transport": None if world == 1 else (
+                           "nccl send/recv + allreduce" if args.transport == "nccl" else
+                           "peer memory over NVLink (CUDA IPC): fused pull / scatter / rank-order sum"),
                        "transform_first_layers": [l + 1 for l in range(shape.L) if (ctx.tf_layers() >> l) & 1],
                        "l2": "flushed between timed steps (2x L2 write, outside the events)",
                        "step": "%s + bns_epoch (%s update included%s)" % (
@@ -484,6 +504,9 @@ def run_ours(args):
             "step_ms": step_ms,
             "memory_bytes": ctx.memory()[0],
         }
+        if shared:
+            line["shared_gpu_functional_check"] = "all ranks on cuda:0 (BNS_BENCH_SHARED_GPU=1): not a measurement"
+
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(shape, args.cpu_scale)
         else:
@@ -492,6 +515,8 @@ def run_ours(args):
         if args.json_out:
             with open(args.json_out, "w") as f:
                 json.dump(line, f, indent=1)
+    if world > 1:
+        dist.barrier()   # no rank unmaps / frees a buffer a peer may still read
     ctx.close()
     if world > 1:
         dist.barrier()

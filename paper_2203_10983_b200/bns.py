@@ -64,7 +64,8 @@ def torch_allgather(world: int, group=None):
             src = torch.tensor(np.frombuffer(ctypes.string_at(send, nbytes), np.uint8))
             out = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
             dist.all_gather(out, src, group=group)
-            ctypes.memmove(recv, np.concatenate([o.numpy() for o in out]).ctypes.data, nbytes * world)
+            buf = np.ascontiguousarray(np.concatenate([o.numpy() for o in out]))   # keep it alive during the copy
+            ctypes.memmove(recv, buf.ctypes.data, nbytes * world)
             return 0
         except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
             return 1

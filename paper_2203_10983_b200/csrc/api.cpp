@@ -59,6 +59,21 @@ void* dalloc(Ctx& c, size_t bytes) {
     return p;
 }
 
+// a buffer peers access (f1): carved from the arena when the context runs a peer-memory transport
+void* salloc(Ctx& c, size_t bytes) {
+    if (!c.arena) return dalloc(c, bytes);
+    bytes = (std::max<size_t>(bytes, 16) + 255) & ~size_t(255);
+    if (c.arena_off + (int64_t)bytes > c.arena_size) throw Error(BNS_ERR_RUNTIME, "peer arena too small");
+    void* p = c.arena + c.arena_off;
+    c.arena_off += (int64_t)bytes;
+    return p;
+}
+
+bool peer_mode(const bns_config& cfg) {
+    return cfg.world > 1 && (cfg.transport == BNS_TRANSPORT_IPC ||
+                             (cfg.transport == BNS_TRANSPORT_LOCAL && (cfg.flags & BNS_PEER_MEMORY)));
+}
+
 template <typename T>
 T* upload(Ctx& c, const std::vector<T>& v) {
     T* d = static_cast<T*>(dalloc(c, v.size() * sizeof(T)));
@@ -164,6 +179,25 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     }
     c.nnz_i = P.row_ptr[P.n_in];
     const size_t ts = tsize(c);
+    if (peer_mode(c.cfg)) {   // f1: one exported allocation for everything the peers touch
+        const size_t rows = (size_t)(P.n_in + c.halo_cap);
+        int64_t gn = 0;
+        for (int l = 0; l < L; ++l)
+            gn += (c.layer == BNS_LAYER_SAGE_MEAN ? 2 * (int64_t)c.dp[l]
+                   : c.layer == BNS_LAYER_GAT ? (int64_t)c.dp[l] + 8 : (int64_t)c.dp[l]) * c.dp[l + 1];
+        size_t total = 2 * rows * c.maxd * ts + (size_t)P.n_send * c.maxd * ts + 2 * (size_t)gn * 4 + 4096 + 64 * 256;
+        for (int l = 0; l < L; ++l) total += rows * c.dp[l] * ts;
+        c.arena_size = (int64_t)((total + (2u << 20) - 1) & ~size_t((2u << 20) - 1));
+        c.arena = static_cast<char*>(dalloc(c, (size_t)c.arena_size));
+        c.arena_off = 0;
+        c.d_pflags = static_cast<uint64_t*>(salloc(c, 32 * sizeof(uint64_t)));
+        BNS_CUDA(cudaMemset(c.d_pflags, 0, 32 * sizeof(uint64_t)));
+        c.d_dx2 = salloc(c, rows * c.maxd * ts);
+        c.d_gflat2 = static_cast<float*>(salloc(c, (size_t)gn * sizeof(float)));
+        BNS_CUDA(cudaMemset(c.d_gflat2, 0, (size_t)gn * sizeof(float)));
+        c.d_scal2 = static_cast<double*>(salloc(c, 4 * sizeof(double)));
+        BNS_CUDA(cudaMemset(c.d_scal2, 0, 4 * sizeof(double)));
+    }
 
     // ---- static plan on device
     c.d_row_ptr = upload(c, P.row_ptr);
@@ -241,7 +275,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.d_blk = static_cast<int32_t*>(dalloc(c, (c.n_cand / 1024 + 2) * sizeof(int32_t)));
     c.d_cand_out = static_cast<int32_t*>(dalloc(c, (c.n_cand + 1) * sizeof(int32_t)));
     c.d_slot_of_b = static_cast<int32_t*>(dalloc(c, (P.n_bd + 1) * sizeof(int32_t)));
-    c.d_seg_pos = static_cast<int64_t*>(dalloc(c, (2 * m + 1 + 8) * sizeof(int64_t)));
+    c.d_seg_pos = static_cast<int64_t*>(salloc(c, (2 * m + 1 + 8) * sizeof(int64_t)));
     BNS_CUDA(cudaMallocHost(&c.h_seg_pos, (2 * m + 1 + 8) * sizeof(int64_t)));
     c.d_ind_ptr = static_cast<int64_t*>(dalloc(c, (P.n_in + 1) * sizeof(int64_t)));
     c.d_ind_col = static_cast<int32_t*>(dalloc(c, (c.nnz_i + 1) * sizeof(int32_t)));
@@ -265,14 +299,14 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     // ---- activations
     c.H.assign(L, nullptr);
     c.Z.assign(L + 1, nullptr);
-    for (int l = 0; l < L; ++l) c.H[l] = dalloc(c, (size_t)(P.n_in + c.halo_cap) * c.dp[l] * ts);
+    for (int l = 0; l < L; ++l) c.H[l] = salloc(c, (size_t)(P.n_in + c.halo_cap) * c.dp[l] * ts);
     for (int l = 1; l <= L; ++l) c.Z[l] = dalloc(c, (size_t)P.n_in * c.dp[l - 1] * ts);
     c.d_logits = static_cast<float*>(dalloc(c, (size_t)P.n_in * c.dp[L] * sizeof(float)));
     c.d_dlogits = static_cast<float*>(dalloc(c, (size_t)P.n_in * c.dp[L] * sizeof(float)));
     c.d_dpre = dalloc(c, (size_t)P.n_in * c.maxd * ts);
     c.d_dxcat = dalloc(c, (size_t)P.n_in * 2 * c.maxd * ts);
-    c.d_dx = dalloc(c, (size_t)(P.n_in + c.halo_cap) * c.maxd * ts);
-    c.d_sendbuf = dalloc(c, (size_t)P.n_send * c.maxd * ts);
+    c.d_dx = salloc(c, (size_t)(P.n_in + c.halo_cap) * c.maxd * ts);
+    c.d_sendbuf = salloc(c, (size_t)P.n_send * c.maxd * ts);
     c.d_gradbuf = dalloc(c, (size_t)P.n_send * c.maxd * ts);
     if (c.retain) {
         c.dH_keep.assign(L + 1, nullptr);
@@ -338,10 +372,10 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     }
     if (c.tf_mask || c.layer == BNS_LAYER_GAT) c.d_tfy = dalloc(c, (size_t)(P.n_in + c.halo_cap) * tfw * ts);
     c.gflat_n = c.goff[L];
-    c.d_gflat = static_cast<float*>(dalloc(c, c.gflat_n * sizeof(float)));
+    c.d_gflat = static_cast<float*>(salloc(c, c.gflat_n * sizeof(float)));
     c.splitk_cap = 32 * wmax;
     c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
-    c.d_scal = static_cast<double*>(dalloc(c, 4 * sizeof(double)));
+    c.d_scal = static_cast<double*>(salloc(c, 4 * sizeof(double)));
     c.d_lpart = static_cast<double*>(dalloc(c, 4 * 2048 * sizeof(double)));   // k_xent / k_bce block partials
     c.d_nonfinite = static_cast<int32_t*>(dalloc(c, 16));
     c.d_hostw = static_cast<float*>(dalloc(c, 2 * wlog * sizeof(float)));

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <mutex>
 
+#include <cuda.h>
 #include <nccl.h>
 
 #include "common.h"
@@ -219,6 +220,14 @@ struct NullTransport : Transport {
     void poll(Ctx&) override {}
 };
 
+void* driver_entry(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    BNS_CUDA(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw Error(BNS_ERR_RUNTIME, std::string(name) + " unavailable");
+    return p;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Peer-memory transport (f1).  Shared buffers per rank, in table order (kind k, rank j) -> d_tab[k m + j]:
 //   H^(0..L-1), dX (two alternating buffers), partial weight gradients (two, by all-reduce parity), loss scalars
@@ -256,15 +265,11 @@ struct PeerTransport : Transport {
         }
         preload_module_functions();
         const Plan& P = c.plan;
-        const size_t ts = c.prec == BNS_BF16 ? 2 : 4;
-        const size_t dxb = (size_t)(P.n_in + c.halo_cap) * c.maxd * ts;
-        BNS_CUDA(cudaMalloc(&dx2, dxb ? dxb : 16));
-        BNS_CUDA(cudaMalloc(&g2, c.gflat_n * sizeof(float) + 16));
-        BNS_CUDA(cudaMemset(g2, 0, c.gflat_n * sizeof(float) + 16));
-        BNS_CUDA(cudaMalloc(&s2, 4 * sizeof(double)));
-        BNS_CUDA(cudaMemset(s2, 0, 4 * sizeof(double)));
-        BNS_CUDA(cudaMalloc(&d_flags, 32 * sizeof(uint64_t)));
-        BNS_CUDA(cudaMemset(d_flags, 0, 32 * sizeof(uint64_t)));
+        if (!c.arena) throw Error(BNS_ERR_RUNTIME, "peer-memory transport without a peer arena");
+        dx2 = c.d_dx2;
+        g2 = c.d_gflat2;
+        s2 = c.d_scal2;
+        d_flags = c.d_pflags;
         BNS_CUDA(cudaMalloc(&d_delta, 32 * sizeof(int64_t)));
         BNS_CUDA(cudaMemset(d_delta, 0, 32 * sizeof(int64_t)));
         BNS_CUDA(cudaHostAlloc(&h_err, sizeof(int), cudaHostAllocMapped));
@@ -295,19 +300,55 @@ struct PeerTransport : Transport {
             allgather(c, own.data(), all.data(), nk * sizeof(void*));
             for (int j = 0; j < m; ++j)
                 for (int k = 0; k < nk; ++k) tab[(size_t)k * m + j] = all[(size_t)j * nk + k];
-        } else {   // IPC handles
-            std::vector<cudaIpcMemHandle_t> mine(nk), all((size_t)nk * m);
-            for (int k = 0; k < nk; ++k) BNS_CUDA(cudaIpcGetMemHandle(&mine[k], own[k]));
-            allgather(c, mine.data(), all.data(), nk * sizeof(cudaIpcMemHandle_t));
-            for (int j = 0; j < m; ++j)
-                for (int k = 0; k < nk; ++k) {
-                    void* p = own[k];
-                    if (j != me) {
-                        BNS_CUDA(cudaIpcOpenMemHandle(&p, all[(size_t)j * nk + k], cudaIpcMemLazyEnablePeerAccess));
-                        opened.push_back(p);
-                    }
-                    tab[(size_t)k * m + j] = p;
+        } else {   // IPC: each underlying allocation exported ONCE (one handle), buffers as (allocation, offset)
+            constexpr int kMaxAlloc = 32;
+            struct Exp {
+                int32_t n;
+                int32_t idx[kMaxAlloc];
+                int64_t off[kMaxAlloc];
+                cudaIpcMemHandle_t h[kMaxAlloc];
+            };
+            if (nk > kMaxAlloc) throw Error(BNS_ERR_RUNTIME, "peer-memory transport: too many shared buffers");
+            auto range = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(
+                driver_entry("cuMemGetAddressRange"));
+            Exp mine;
+            std::memset(&mine, 0, sizeof(mine));
+            std::vector<CUdeviceptr> bases;
+            for (int k = 0; k < nk; ++k) {
+                CUdeviceptr base = 0;
+                size_t sz = 0;
+                if (range(&base, &sz, (CUdeviceptr)own[k]) != CUDA_SUCCESS)
+                    throw Error(BNS_ERR_RUNTIME, "cuMemGetAddressRange failed");
+                int a = -1;
+                for (size_t q = 0; q < bases.size(); ++q)
+                    if (bases[q] == base) a = (int)q;
+                if (a < 0) {
+                    a = (int)bases.size();
+                    bases.push_back(base);
+                    BNS_CUDA(cudaIpcGetMemHandle(&mine.h[a], (void*)base));
                 }
+                mine.idx[k] = a;
+                mine.off[k] = (int64_t)((CUdeviceptr)own[k] - base);
+            }
+            mine.n = (int32_t)bases.size();
+            std::vector<Exp> all(m);
+            allgather(c, &mine, all.data(), sizeof(Exp));
+            for (int j = 0; j < m; ++j) {
+                std::vector<char*> mapped(all[j].n, nullptr);
+                if (j != me)
+                    for (int a = 0; a < all[j].n; ++a) {
+                        void* q = nullptr;
+                        const cudaError_t e = cudaIpcOpenMemHandle(&q, all[j].h[a], cudaIpcMemLazyEnablePeerAccess);
+                        if (e != cudaSuccess)
+                            throw Error(BNS_ERR_RUNTIME, std::string("cudaIpcOpenMemHandle(rank ") + std::to_string(j) +
+                                                             ", allocation " + std::to_string(a) + "): " +
+                                                             cudaGetErrorString(e));
+                        opened.push_back(q);
+                        mapped[a] = static_cast<char*>(q);
+                    }
+                for (int k = 0; k < nk; ++k)
+                    tab[(size_t)k * m + j] = j == me ? own[k] : (void*)(mapped[all[j].idx[k]] + all[j].off[k]);
+            }
         }
         BNS_CUDA(cudaMalloc(&d_tab, tab.size() * sizeof(void*)));
         BNS_CUDA(cudaMemcpy(d_tab, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice));
@@ -323,8 +364,7 @@ struct PeerTransport : Transport {
     }
     ~PeerTransport() override {
         for (void* p : opened) cudaIpcCloseMemHandle(p);
-        for (void* p : {(void*)d_tab, (void*)d_pnin, (void*)d_delta, (void*)d_owner_of_b, (void*)d_row_of_b,
-                        (void*)d_flags, dx2, g2, s2})
+        for (void* p : {(void*)d_tab, (void*)d_pnin, (void*)d_delta, (void*)d_owner_of_b, (void*)d_row_of_b})
             if (p) cudaFree(p);
         if (h_err) cudaFreeHost(h_err);
         if (g) {

@@ -91,6 +91,14 @@ struct Ctx {
     int64_t kernels = 0;
     int64_t dev_bytes = 0;
     std::vector<void*> allocs;
+    // f1 peer memory: every buffer another rank reads or writes lives in ONE allocation (the only one exported
+    // through CUDA IPC -- small cudaMallocs may be sub-allocated and cannot be exported one by one)
+    char* arena = nullptr;
+    int64_t arena_off = 0, arena_size = 0;
+    void* d_dx2 = nullptr;         // second dX buffer (alternating layers)
+    float* d_gflat2 = nullptr;     // second weight-gradient buffer (all-reduce parity)
+    double* d_scal2 = nullptr;
+    uint64_t* d_pflags = nullptr;  // device barrier flag slots [32]
     std::vector<double> times;
     std::vector<cudaEvent_t> ev;              // timing events, 2 per phase slot
     // --- per-epoch host copies of counts

@@ -102,14 +102,14 @@ def worker(rank, world, port, N, nnz, q):
         # f1: the IPC host all-gather through its ctypes function pointer (what libbns calls)
         import ctypes
         fn = bns.torch_allgather(world)
-        nb = 67
-        send = np.arange(nb, dtype=np.uint8) + np.uint8(rank * 50)
-        recv = np.zeros(nb * world, np.uint8)
         cfn = ctypes.cast(fn, ctypes.c_void_p).value
         call = bns.ALLGATHER_FN(cfn)
-        assert call(send.ctypes.data, recv.ctypes.data, nb, None) == 0
-        for j in range(world):
-            assert np.array_equal(recv[j * nb:(j + 1) * nb], np.arange(nb, dtype=np.uint8) + np.uint8(j * 50))
+        for nb in (67, 4999, 1 << 20):   # small and large (a dangling temporary only shows on large copies)
+            send = ((np.arange(nb) * 7 + rank * 50) % 251).astype(np.uint8)
+            recv = np.zeros(nb * world, np.uint8)
+            assert call(send.ctypes.data, recv.ctypes.data, nb, None) == 0
+            for j in range(world):
+                assert np.array_equal(recv[j * nb:(j + 1) * nb], ((np.arange(nb) * 7 + j * 50) % 251).astype(np.uint8))
         # max over ranks
         m = bench.max_over_ranks(float(rank + 1) * 1.5, dist, "cpu")
         assert m == 1.5 * world
