@@ -349,6 +349,22 @@ static void dispatch(Ctx& c, const SpmmArgs& a, unsigned grid) {
             default: throw Error(BNS_ERR_INVALID, "feature dim too large for the SpMM kernel");
         }
     }
+    // rows narrower than a warp: one vector per lane and the next power of two of lanes per edge (idle lanes re-load
+    // the last vector: no extra sectors).  Measured on the Reddit shape (48 bf16 = 6 vectors): 8 x 1 beats 4 x 2
+    // (-0.3 ms per pass: fewer registers, more edges in flight) and 2 x 3 (+0.3 ms).  BNS_SPMM_LANES=0: 4 x 2 style.
+    static const int pow2up = [] { const char* e = std::getenv("BNS_SPMM_LANES"); return e ? std::atoi(e) : 1; }();
+    if (pow2up) {
+        int l2 = 1;
+        while (l2 < nvec) l2 *= 2;
+        switch (l2) {
+            case 1: go<T, 1, 1>(c, a, grid); return;
+            case 2: go<T, 2, 1>(c, a, grid); return;
+            case 4: go<T, 4, 1>(c, a, grid); return;
+            case 8: go<T, 8, 1>(c, a, grid); return;
+            case 16: go<T, 16, 1>(c, a, grid); return;
+            default: break;
+        }
+    }
     int lpr = 1;
     while (lpr * 2 <= nvec) lpr *= 2;
     const int vpl = (nvec + lpr - 1) / lpr;

@@ -151,6 +151,29 @@ def test_epoch_parity(prec, layer, tf, m, p, method):
         run.close()
 
 
+@pytest.mark.parametrize("dims,prec", [([37, 64, 41], bns.BNS_BF16), ([37, 64, 24], bns.BNS_FP32),
+                                       ([37, 64, 41], bns.BNS_FP32)])
+@pytest.mark.parametrize("m,p", [(1, 1.0), (3, 0.3)])
+def test_six_vector_rows_parity(dims, prec, m, p):
+    """Transform-first last layer gathered at a width of 6 16-byte vectors (48 bf16 = Reddit's 41 classes padded;
+    24 fp32): the SpMM's 2-lanes x 3-vectors layout, forward and transposed, against the oracle."""
+    layer = bns.BNS_LAYER_SAGE_MEAN
+    L = len(dims) - 1
+    indptr, indices, part, X, y = wl(3000, 90000, m, dims[0], dims[-1], 91 + m)
+    Ws = I.weights(dims, layer)
+    Wd = [w.astype(np.float64) for w in Ws]
+    run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y)
+    orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
+    orc.set_bf16(prec == bns.BNS_BF16)
+    try:
+        for e in range(2):
+            run.sample(p, SEED, e)
+            orc.sample(p, SEED, e)
+            Ws = compare_epoch(run, orc, L, Ws, Wd, 0.5, prec, tag=f"six-vector epoch{e}")
+    finally:
+        run.close()
+
+
 def test_cora_config0():
     """BASELINE.json configs[0]: Cora-shaped, 2-layer GCN hidden 16, 2 partitions, p=0.5, fixed Philox seed."""
     sh = I.SHAPES["cora"]
