@@ -29,9 +29,16 @@ $(OBJDIR)/%.cu.o: $(PKG)/csrc/%.cu $(CHDR)
 
 $(OBJDIR)/%.cpp.o: $(PKG)/csrc/%.cpp $(CHDR)
 	@mkdir -p $(OBJDIR)
-	$(NVCC) -O2 -std=c++17 -Wno-deprecated-gpu-targets -Xcompiler -fPIC,-Wall -Iinclude -I$(NCCL_DIR)/include -c -o $@ $<
+	$(NVCC) -O2 -std=c++17 $(CXXDEF) -Wno-deprecated-gpu-targets -Xcompiler -fPIC,-Wall -Iinclude -I$(NCCL_DIR)/include -c -o $@ $<
 
 $(PKG)/libbns.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
+
+# A/B variant of the product library with another SpMM segment length (BNS_LIB=... selects it at run time)
+kseg%: 
+	$(MAKE) OBJDIR=build_kseg$* NVFLAGS="$(NVFLAGS) -DBNS_KSEG=$*" CXXDEF="-DBNS_KSEG=$*" $(PKG)/libbns_kseg$*.so LIBOUT=$(PKG)/libbns_kseg$*.so
+
+$(PKG)/libbns_kseg%.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
 
 clean:

@@ -370,10 +370,9 @@ def run_ours(args):
         del src
 
     def step(e, W, G):
-        if sampler == bns.BNS_SAMPLER_BNS:
-            ctx.sample_boundary(args.p, I.BNS_SEED, e)
-        else:
-            ctx.sample_edges(sampler, q, I.BNS_SEED, e)
+        if sampler == bns.BNS_SAMPLER_BNS:   # bns_step = bns_sample_boundary + bns_epoch in one C call
+            return ctx.step(args.p, I.BNS_SEED, e, W, args.lr, G)
+        ctx.sample_edges(sampler, q, I.BNS_SEED, e)
         return ctx.epoch(W, args.lr, G)
 
     for e in range(args.warmup):
@@ -473,9 +472,9 @@ def run_ours(args):
                            "peer memory over NVLink (CUDA IPC): fused pull / scatter / rank-order sum"),
                        "transform_first_layers": [l + 1 for l in range(shape.L) if (ctx.tf_layers() >> l) & 1],
                        "l2": "flushed between timed steps (2x L2 write, outside the events)",
-                       "step": "%s + bns_epoch (%s update included%s)" % (
-                           "bns_sample_boundary" if sampler == bns.BNS_SAMPLER_BNS else
-                           f"bns_sample_edges({args.sampler}, q={q:.4f})",
+                       "step": "%s (%s update included%s)" % (
+                           "bns_step = bns_sample_boundary + bns_epoch" if sampler == bns.BNS_SAMPLER_BNS else
+                           f"bns_sample_edges({args.sampler}, q={q:.4f}) + bns_epoch",
                            "Adam" if args.adam else "SGD",
                            (f", dropout {args.dropout}" if args.dropout > 0 else "") +
                            (", multi-label sigmoid BCE loss" if args.multilabel else ""))},

@@ -174,6 +174,12 @@ bns_status bns_sample_edges(bns_ctx* ctx, int32_t sampler, double q, uint64_t se
  * Returns after a stream sync.  Collective. */
 bns_status bns_epoch(bns_ctx* ctx, float* const* weights, float lr, float* const* grads, double* loss, double* acc);
 
+/* One training step = bns_sample_boundary(p, seed, epoch) followed by bns_epoch(weights, lr, grads, loss, acc) in
+ * one call (Alg.1 l.4-14): the same work and results, without a return to the caller between the draw and the epoch
+ * (the host only waits for the per-peer counts, then enqueues the epoch).  Errors as the two calls. */
+bns_status bns_step(bns_ctx* ctx, double p, uint64_t seed, uint64_t epoch, float* const* weights, float lr,
+                    float* const* grads, double* loss, double* acc);
+
 /* the paper's training recipe ("a GraphSAGE model with an Adam optimizer",
  * per-dataset dropout).  Defaults after bns_setup: SGD (Alg.1 l.14), no dropout.
  *   optimizer: BNS_OPT_SGD or BNS_OPT_ADAM (bias-corrected Adam; beta1, beta2, eps as usual).  The Adam moments live

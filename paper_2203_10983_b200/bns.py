@@ -32,7 +32,7 @@ PHASES = ["sample", "induce", "pack", "exchange", "spmm_fwd", "gemm_fwd", "loss"
           "exchange_bwd", "scatter", "allreduce", "update", "epoch_total", "sample_total"]
 
 EXPORTS = ["bns_get_unique_id", "bns_group_create", "bns_group_destroy", "bns_setup", "bns_sample_boundary",
-           "bns_sample_edges", "bns_set_multilabel", "bns_epoch", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
+           "bns_sample_edges", "bns_set_multilabel", "bns_epoch", "bns_step", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
 BNS_OPT_SGD, BNS_OPT_ADAM = 0, 1
 
 
@@ -93,6 +93,7 @@ def lib():
         L.bns_set_multilabel.argtypes = [vp, vp]
         L.bns_epoch.argtypes = [vp, vp, f32, vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]
         L.bns_set_training.argtypes = [vp, i32, f64, f64, f64, f64, u64]
+        L.bns_step.argtypes = [vp, f64, u64, u64, vp, f32, vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]
         L.bns_query.argtypes = [vp, i32, i32, vp, i64, ctypes.POINTER(i64)]
         L.bns_stream.restype = vp
         L.bns_stream.argtypes = [vp]
@@ -100,7 +101,7 @@ def lib():
         L.bns_last_error.argtypes = [vp]
         L.bns_destroy.argtypes = [vp]
         for f in ("bns_get_unique_id", "bns_group_create", "bns_setup", "bns_sample_boundary", "bns_sample_edges",
-                  "bns_set_multilabel", "bns_epoch",
+                  "bns_set_multilabel", "bns_epoch", "bns_step",
                   "bns_set_training", "bns_query"):
             getattr(L, f).restype = ctypes.c_int
         L.bns_group_destroy.restype = None
@@ -178,6 +179,19 @@ def bns_epoch(ctx, weights: Sequence, lr: float, grads: Sequence | None = None):
     return loss.value, acc.value
 
 
+def bns_step(ctx, p: float, seed: int, epoch: int, weights: Sequence, lr: float, grads: Sequence | None = None):
+    """bns_sample_boundary + bns_epoch in one call."""
+    L = len(weights)
+    wp = (ctypes.c_void_p * L)(*[_ptr(w) for w in weights])
+    gp = (ctypes.c_void_p * L)(*[_ptr(g) for g in grads]) if grads is not None else None
+    loss = ctypes.c_double()
+    acc = ctypes.c_double()
+    rc = lib().bns_step(ctx, float(p), int(seed) & (2**64 - 1), int(epoch) & (2**64 - 1), wp, ctypes.c_float(lr), gp,
+                        ctypes.byref(loss), ctypes.byref(acc))
+    _check(rc, ctx)
+    return loss.value, acc.value
+
+
 def bns_set_training(ctx, optimizer: int = BNS_OPT_SGD, beta1: float = 0.9, beta2: float = 0.999,
                      eps: float = 1e-8, dropout: float = 0.0, dropout_seed: int = 0):
     _check(lib().bns_set_training(ctx, optimizer, beta1, beta2, eps, dropout, int(dropout_seed) & (2**64 - 1)), ctx)
@@ -248,6 +262,12 @@ class Context:
             import torch
             torch.cuda.current_stream().synchronize()
         return bns_epoch(self.h, weights, lr, grads)
+
+    def step(self, p, seed, epoch, weights, lr, grads=None):
+        if weights and hasattr(weights[0], "is_cuda") and weights[0].is_cuda:
+            import torch
+            torch.cuda.current_stream().synchronize()
+        return bns_step(self.h, p, seed, epoch, weights, lr, grads)
 
     def set_training(self, optimizer=BNS_OPT_SGD, beta1=0.9, beta2=0.999, eps=1e-8, dropout=0.0, dropout_seed=0):
         bns_set_training(self.h, optimizer, beta1, beta2, eps, dropout, dropout_seed)

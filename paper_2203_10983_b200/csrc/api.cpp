@@ -252,6 +252,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.d_seg_fwd = static_cast<Seg*>(dalloc(c, c.seg_fwd_cap * sizeof(Seg)));
     int64_t seg_max = std::max({c.seg_fwd_cap, c.seg_bwd_cap, c.n_seg_static_fwd});
     c.d_partial = static_cast<float*>(dalloc(c, (size_t)seg_max * c.maxd * sizeof(float)));
+    c.d_spmm_work = static_cast<unsigned long long*>(dalloc(c, 64));
     // split (hub) row lists: first segment of every row with more than one segment
     auto split_list = [](const std::vector<Seg>& s) {
         std::vector<int64_t> l;
@@ -805,6 +806,13 @@ bns_status bns_epoch(bns_ctx* h, float* const* weights, float lr, float* const* 
         BNS_CUDA(cudaSetDevice(c.cfg.device));
         epoch(c, weights, lr, grads, loss, acc);
     });
+}
+
+bns_status bns_step(bns_ctx* h, double p, uint64_t seed, uint64_t ep, float* const* weights, float lr,
+                    float* const* grads, double* loss, double* acc) {
+    const bns_status st = bns_sample_boundary(h, p, seed, ep);
+    if (st != BNS_OK) return st;
+    return bns_epoch(h, weights, lr, grads, loss, acc);
 }
 
 bns_status bns_set_training(bns_ctx* h, int32_t optimizer, double beta1, double beta2, double eps, double dropout,

@@ -25,7 +25,10 @@ struct Error : std::runtime_error {
 
 #define BNS_CHECK_LAUNCH() BNS_CUDA(cudaGetLastError())
 
-constexpr int kSeg = 512;          // SpMM segment length in edges (hub rows are split into segments of this size)
+#ifndef BNS_KSEG
+#define BNS_KSEG 256   // A/B on one B200 (make kseg128 / kseg256): 512 -> 256 = m=8 rank epoch 2.23 -> 2.12 ms, m=1 24.3 -> 24.0
+#endif
+constexpr int kSeg = BNS_KSEG;     // SpMM segment length in edges (hub rows are split into segments of this size)
 constexpr int kPad = 8;            // feature dims padded to multiples of 8 (16-byte rows for fp32x4 / bf16x8)
 
 inline int64_t pad8(int64_t d) { return (d + kPad - 1) / kPad * kPad; }
@@ -142,6 +145,7 @@ struct Ctx {
     int32_t* d_static_col = nullptr; int64_t* d_static_ptr = nullptr;
     int64_t n_seg_bwd_inner = 0;
     float* d_partial = nullptr;    // hub-row partial sums
+    unsigned long long* d_spmm_work = nullptr;   // SpMM dynamic scheduling counter
     int64_t* d_split_sf = nullptr;  int64_t n_split_sf = 0;      // split rows of the static forward segments
     int64_t* d_split_bwd = nullptr; int64_t n_split_bwd_inner = 0; // [static inner part ; per-epoch halo part]
     int64_t* d_split_fwd = nullptr;                                  // per-epoch induced forward segments

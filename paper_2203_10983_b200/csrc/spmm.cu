@@ -162,7 +162,14 @@ k_spmm(const SpmmArgs a) {
     for (int v = 0; v < VPL; ++v) voff[v] = min(l + v * LPR, nvec - 1) - l;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t sid = warp; sid < a.n_segs; sid += nwarps) {
+    // static: grid-stride over the segments; dynamic (a.work): each warp claims the next segment when it is done, so
+    // a block never idles behind its longest segment (short partitions: ~1 segment per warp)
+    auto claim = [&]() -> int64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(a.work, 1ull);
+        return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+    };
+    for (int64_t sid = a.work ? claim() : warp; sid < a.n_segs; sid = a.work ? claim() : sid + nwarps) {
         const Seg s = a.segs[sid];
         uint64_t acc2[VPL][VN / 2];
 #pragma unroll
@@ -315,6 +322,36 @@ __global__ void __launch_bounds__(256) k_spmm_fixup(const SpmmArgs a) {
     }
 }
 
+// BNS_SPMM_SCHED: 0 = grid-stride over min(n_segs / 8, 148 x 32) blocks; 1 = the same over one resident wave;
+// 2 (default) = one resident wave, segments claimed dynamically (a.work)
+static int spmm_sched() {
+    static const int v = [] { const char* e = std::getenv("BNS_SPMM_SCHED"); return e ? std::atoi(e) : 2; }();
+    return v;
+}
+
+static int resident_per_gpu(const void* kern) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0) != cudaSuccess || b < 1) b = 1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return b * sms;
+}
+
+template <typename T, int LPR, int VPL, int SC>
+static void go_sc(Ctx& c, SpmmArgs a, unsigned grid) {
+    auto kern = k_spmm<T, LPR, VPL, SC>;
+    static const int wave = resident_per_gpu((const void*)kern);   // per kernel instance (thread-safe init)
+    if (spmm_sched() != 0) grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.n_segs + 7) / 8, wave));
+    if (spmm_sched() == 2) {
+        BNS_CUDA(cudaMemsetAsync(c.d_spmm_work, 0, sizeof(unsigned long long), c.stream));
+        a.work = c.d_spmm_work;
+    } else {
+        a.work = nullptr;
+    }
+    kern<<<grid, 256, 0, c.stream>>>(a);
+}
+
 template <typename T, int LPR, int VPL>
 static void go(Ctx& c, const SpmmArgs& a, unsigned grid) {
     // per-edge column scale needed?  SAGE forward only when halo columns carry 1/p != 1
@@ -322,13 +359,13 @@ static void go(Ctx& c, const SpmmArgs& a, unsigned grid) {
     if (a.sc >= 0) sc = a.sc;
     else if (a.mode == GCN_FWD) sc = 2;
     else if ((a.mode == SAGE_FWD || a.mode == SAGE_FWD_TF) && a.inv_p != 1.f) sc = 1;
-    if (sc == 0) k_spmm<T, LPR, VPL, 0><<<grid, 256, 0, c.stream>>>(a);
-    else if (sc == 1) k_spmm<T, LPR, VPL, 1><<<grid, 256, 0, c.stream>>>(a);
-    else if (sc == 2) k_spmm<T, LPR, VPL, 2><<<grid, 256, 0, c.stream>>>(a);
-    else if (sc == 3) k_spmm<T, LPR, VPL, 3><<<grid, 256, 0, c.stream>>>(a);
-    else if (sc == 4) k_spmm<T, LPR, VPL, 4><<<grid, 256, 0, c.stream>>>(a);
-    else if (sc == 5) k_spmm<T, LPR, VPL, 5><<<grid, 256, 0, c.stream>>>(a);
-    else k_spmm<T, LPR, VPL, 6><<<grid, 256, 0, c.stream>>>(a);
+    if (sc == 0) go_sc<T, LPR, VPL, 0>(c, a, grid);
+    else if (sc == 1) go_sc<T, LPR, VPL, 1>(c, a, grid);
+    else if (sc == 2) go_sc<T, LPR, VPL, 2>(c, a, grid);
+    else if (sc == 3) go_sc<T, LPR, VPL, 3>(c, a, grid);
+    else if (sc == 4) go_sc<T, LPR, VPL, 4>(c, a, grid);
+    else if (sc == 5) go_sc<T, LPR, VPL, 5>(c, a, grid);
+    else go_sc<T, LPR, VPL, 6>(c, a, grid);
 }
 
 template <typename T>

@@ -65,15 +65,15 @@ def main():
             smp = SAMP[sname]
             q = p if smp != bns.BNS_SAMPLER_DROPEDGE else 1.0 - (1.0 - p) * cross_frac
 
-            def draw(e):
+            def one(e):   # one training step (bns_step for BNS: draw + epoch in one C call, as bench.py)
                 if smp == bns.BNS_SAMPLER_BNS:
-                    ctx.sample_boundary(p, I.BNS_SEED, e)
+                    ctx.step(p, I.BNS_SEED, e, W, 0.0, G)
                 else:
                     ctx.sample_edges(smp, q, I.BNS_SEED, e)
+                    ctx.epoch(W, 0.0, G)
 
             for e in range(args.warmup):
-                draw(e)
-                ctx.epoch(W, 0.0, G)
+                one(e)
             torch.cuda.synchronize()
             t0 = ctx.times()
             k0 = ctx.kernel_count()
@@ -82,8 +82,7 @@ def main():
             for k in range(args.steps):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                draw(100 + k)
-                ctx.epoch(W, 0.0, G)
+                one(100 + k)
                 b.record(stream)
                 b.synchronize()
                 ms.append(a.elapsed_time(b))

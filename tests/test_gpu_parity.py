@@ -268,6 +268,34 @@ def test_determinism_two_runs():
     assert outs[0] == outs[1]
 
 
+@pytest.mark.parametrize("m", [1, 3])
+def test_step_equals_sample_then_epoch(m):
+    """bns_step(p, seed, epoch, W, lr, G) is bns_sample_boundary + bns_epoch in one call: bitwise the same."""
+    import torch
+    indptr, indices, part, X, y = wl(2500, 70000, m, 20, 6, 18)
+    dims = [20, 16, 6]
+    outs = []
+    for fused in (False, True):
+        run = GpuRun(indptr, indices, part, m, dims, 0, bns.BNS_BF16, X, y)
+        Ws = I.weights(dims, 0)
+        W = [[torch.tensor(w, device="cuda") for w in Ws] for _ in range(m)]
+        G = [[torch.zeros_like(w) for w in W[0]] for _ in range(m)]
+        try:
+            rec = []
+            for e in range(3):
+                if fused:
+                    out = parallel(m, lambda r: run.ctx[r].step(0.3, SEED, e, W[r], 0.2, G[r]))
+                else:
+                    run.sample(0.3, SEED, e)
+                    out = parallel(m, lambda r: run.ctx[r].epoch(W[r], 0.2, G[r]))
+                torch.cuda.synchronize()
+                rec.append((out[0], [g.cpu().numpy().tobytes() for g in G[0]], run.ctx[0].mask().tobytes()))
+            outs.append((rec, [w.cpu().numpy().tobytes() for w in W[0]]))
+        finally:
+            run.close()
+    assert outs[0] == outs[1]
+
+
 def test_binomial_counts_gpu():
     indptr, indices, part, X, y = wl(3000, 60000, 4, 4, 3, 3)
     run = GpuRun(indptr, indices, part, 4, [4, 3], 0, bns.BNS_FP32, X, y, flags=0)
