@@ -41,6 +41,13 @@ kseg%:
 $(PKG)/libbns_kseg%.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
 
+# A/B variant without the SpMM column-index prefetch
+noprefetch:
+	$(MAKE) OBJDIR=build_nopf NVFLAGS="$(NVFLAGS) -DBNS_SPMM_PREFETCH=0" $(PKG)/libbns_nopf.so
+
+$(PKG)/libbns_nopf.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
+
 clean:
 	rm -rf $(OBJDIR) oracle/liboracle.so $(PKG)/inputs/libbnsgen.so $(PKG)/libbns.so
 

@@ -138,6 +138,9 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
 #ifndef BNS_SPMM_U1
 #define BNS_SPMM_U1 8       // edges in flight per lane group for 1-vector rows
 #endif
+#ifndef BNS_SPMM_PREFETCH
+#define BNS_SPMM_PREFETCH 1
+#endif
 #ifndef BNS_SPMM_MINB1
 #define BNS_SPMM_MINB1 4    // resident 256-thread blocks per SM for 1-vector rows
 #endif
@@ -163,7 +166,8 @@ k_spmm(const SpmmArgs a) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     // static: grid-stride over the segments; dynamic (a.work): each warp claims the next segment when it is done, so
-    // a block never idles behind its longest segment (short partitions: ~1 segment per warp)
+    // a block never idles behind its longest segment (short partitions: ~1 segment per warp).  Claiming the next
+    // segment ahead (atomic issued at segment start) was measured slower at m = 8 (2.05 vs 1.99 ms): rejected.
     auto claim = [&]() -> int64_t {
         unsigned long long v = 0;
         if (lane == 0) v = atomicAdd(a.work, 1ull);
@@ -176,12 +180,25 @@ k_spmm(const SpmmArgs a) {
         for (int v = 0; v < VPL; ++v)
 #pragma unroll
             for (int k = 0; k < VN / 2; ++k) acc2[v][k] = 0ull;
+#if BNS_SPMM_PREFETCH
+        // the next chunk's 32 column indices are loaded while this chunk's rows are gathered (one dependent round
+        // trip less per 32 edges: short rows / small partitions are latency-bound)
+        int32_t ci_next = (lane < s.e1 - s.e0) ? a.col[s.e0 + lane] : 0;
+#endif
         for (int64_t eb = s.e0; eb < s.e1; eb += 32) {
             const int cnt = (s.e1 - eb < 32) ? (int)(s.e1 - eb) : 32;
             int32_t ci = 0;
             float sc = 1.f;
+#if BNS_SPMM_PREFETCH
+            const int32_t ci_cur = ci_next;
+            if (eb + 32 + lane < s.e1) ci_next = a.col[eb + 32 + lane];
+#endif
             if (lane < cnt) {
+#if BNS_SPMM_PREFETCH
+                ci = ci_cur;
+#else
                 ci = a.col[eb + lane];
+#endif
                 if (SC == 1) sc = (ci >= a.n_in) ? a.inv_p : 1.f;
                 if (SC == 2) sc = a.cscale[ci];
                 if (SC == 3) {   // GAT forward: alpha_vu, v = this row (R45)
