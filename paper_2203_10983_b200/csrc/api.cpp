@@ -276,6 +276,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.d_blk = static_cast<int32_t*>(dalloc(c, (c.n_cand / 1024 + 2) * sizeof(int32_t)));
     c.d_cand_out = static_cast<int32_t*>(dalloc(c, (c.n_cand + 1) * sizeof(int32_t)));
     c.d_slot_of_b = static_cast<int32_t*>(dalloc(c, (P.n_bd + 1) * sizeof(int32_t)));
+    c.d_bkeep = static_cast<uint32_t*>(dalloc(c, ((P.n_bd + 31) / 32 + 1) * sizeof(uint32_t)));
     c.d_seg_pos = static_cast<int64_t*>(salloc(c, (2 * m + 1 + 8) * sizeof(int64_t)));
     BNS_CUDA(cudaMallocHost(&c.h_seg_pos, (2 * m + 1 + 8) * sizeof(int64_t)));
     c.d_ind_ptr = static_cast<int64_t*>(dalloc(c, (P.n_in + 1) * sizeof(int64_t)));

@@ -127,6 +127,7 @@ struct Ctx {
     int32_t* d_blk = nullptr;      // per-block counts / offsets for compaction
     int32_t* d_cand_out = nullptr; // compacted payloads: [U_b (|U|) ; S_local (ΣS)]
     int32_t* d_slot_of_b = nullptr;
+    uint32_t* d_bkeep = nullptr;   // keep bit per boundary node (induce)
     int64_t* d_seg_pos = nullptr;  // [2m+1] compacted segment offsets
     int64_t* h_seg_pos = nullptr;  // pinned host copy
     uint32_t* d_ebits = nullptr;   // induce: keep bit per static edge

@@ -210,15 +210,29 @@ void launch_sample(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
 //   K3 order-preserving scatter of the kept (remapped) columns, K4 row pointers from the bit prefix + segment
 //   counts per row, scan, K5 segment list.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ bool edge_kept(int32_t x, const int32_t* __restrict__ slot_of_b) {
-    return x >= 0 || slot_of_b[-x - 1] >= 0;
+// keep bit of every boundary node (bit b of bkeep = keep(B_i[b], i)) packed from the draw's byte flags: the induce
+// pass then tests boundary columns against a |B_i| / 8-byte bitmask that stays in L1 (20 KB on the Reddit shape at
+// m = 8) instead of a 4-byte-per-node slot array
+__global__ void k_keep_bits(const uint8_t* __restrict__ flags, int64_t n, uint32_t* __restrict__ bkeep) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t e0 = w << 5;
+    if (e0 >= n) return;
+    uint32_t word = 0;
+    for (int j = 0; j < 32 && e0 + j < n; ++j) word |= (uint32_t)(flags[e0 + j] != 0) << j;
+    bkeep[w] = word;
+}
+
+__device__ __forceinline__ bool edge_kept_bits(int32_t x, const uint32_t* __restrict__ bkeep) {
+    if (x >= 0) return true;
+    const uint32_t b = (uint32_t)(-x - 1);
+    return (__ldg(bkeep + (b >> 5)) >> (b & 31)) & 1u;
 }
 
 // Word-per-thread versions (same bits / per-1024-edge count layout): thread t owns edges [32t, 32t + 32) and builds
 // their keep word from eight 16-byte column loads; a warp covers one 1024-edge block, so the block counts and the
 // in-block prefix are warp shuffles (no shared memory, no block barrier).
 __global__ void __launch_bounds__(256) k_induce_flags_w(const int32_t* __restrict__ col_enc, int64_t nnz,
-                                                        const int32_t* __restrict__ slot_of_b,
+                                                        const uint32_t* __restrict__ bkeep,
                                                         uint32_t* __restrict__ bits, int32_t* __restrict__ blk) {
     const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nw = (nnz + 31) >> 5;
@@ -230,13 +244,13 @@ __global__ void __launch_bounds__(256) k_induce_flags_w(const int32_t* __restric
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const int4 v = __ldg(p + q);
-                word |= (uint32_t)edge_kept(v.x, slot_of_b) << (4 * q);
-                word |= (uint32_t)edge_kept(v.y, slot_of_b) << (4 * q + 1);
-                word |= (uint32_t)edge_kept(v.z, slot_of_b) << (4 * q + 2);
-                word |= (uint32_t)edge_kept(v.w, slot_of_b) << (4 * q + 3);
+                word |= (uint32_t)edge_kept_bits(v.x, bkeep) << (4 * q);
+                word |= (uint32_t)edge_kept_bits(v.y, bkeep) << (4 * q + 1);
+                word |= (uint32_t)edge_kept_bits(v.z, bkeep) << (4 * q + 2);
+                word |= (uint32_t)edge_kept_bits(v.w, bkeep) << (4 * q + 3);
             }
         } else {
-            for (int j = 0; j < (int)(nnz - e0); ++j) word |= (uint32_t)edge_kept(col_enc[e0 + j], slot_of_b) << j;
+            for (int j = 0; j < (int)(nnz - e0); ++j) word |= (uint32_t)edge_kept_bits(col_enc[e0 + j], bkeep) << j;
         }
         bits[w] = word;
     }
@@ -262,14 +276,17 @@ __global__ void __launch_bounds__(256) k_induce_scatter_w(const int32_t* __restr
         const int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    if (word == 0) return;
-    int64_t pos = boff[w >> 5] + (x - c);
-    uint32_t m = word;
-    while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        const int32_t v = col[(w << 5) + j];
-        out_col[pos++] = v >= 0 ? v : (int32_t)n_in + slot_of_b[-v - 1];
+    // warp-cooperative over the warp's 1024-edge block: word k is processed by all lanes (lane j = edge 32k + j),
+    // so the column reads are 128-byte lines and the kept columns are written contiguously
+    const int64_t base = (w >> 5) < ((nnz + 1023) >> 10) ? boff[w >> 5] : 0;
+    const int64_t e_blk = (w - lane) << 5;
+    const int excl = x - c;
+    for (int k = 0; k < 32; ++k) {
+        const uint32_t wk = __shfl_sync(0xffffffffu, word, k);
+        const int ek = __shfl_sync(0xffffffffu, excl, k);
+        if (!((wk >> lane) & 1u)) continue;
+        const int32_t v = col[e_blk + 32 * k + lane];
+        out_col[base + ek + __popc(wk & ((1u << lane) - 1u))] = v >= 0 ? v : (int32_t)n_in + slot_of_b[-v - 1];
     }
 }
 
@@ -329,9 +346,14 @@ void launch_induce(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     const int64_t nb = (nnz + 1023) / 1024;
     if (nb > 0) {
         const unsigned wb = (unsigned)((((nnz + 31) >> 5) + 255) / 256);
-        if (c.sampler == BNS_SAMPLER_BNS)
-            k_induce_flags_w<<<wb, 256, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eblk);
-        else
+        if (c.sampler == BNS_SAMPLER_BNS) {
+            const int64_t nbw = (c.plan.n_bd + 31) / 32;
+            if (nbw > 0) {
+                k_keep_bits<<<(unsigned)((nbw + 255) / 256), 256, 0, c.stream>>>(c.d_flags, c.plan.n_bd, c.d_bkeep);
+                c.kernels += 1;
+            }
+            k_induce_flags_w<<<wb, 256, 0, c.stream>>>(c.d_col_enc, nnz, c.d_bkeep, c.d_ebits, c.d_eblk);
+        } else
             launch_induce_flags_edge(c, nb, T, seed, epoch);
         k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_eblk, c.d_eboff, nb, tot + 0);
         k_induce_scatter_w<<<wb, 256, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff, n_in,
