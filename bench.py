@@ -379,6 +379,12 @@ def run_ours(args):
         flush.fill_(float(e))
         step(e, Wt, Gt)
     barrier()
+    # N > 1: per-phase CUDA events drain the pipeline (~0.3 ms per epoch at m = 8), so the timed region runs without
+    # them and the phase split / roofline come from a second pass of the same steps; N = 1 keeps them on inside the
+    # timed region (the roofline is then measured over exactly the timed launches; cost ~1 %)
+    phase_pass = world > 1
+    if phase_pass:
+        ctx.set_timing(False)
     t0_times = ctx.times()
     k0 = ctx.kernel_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -399,6 +405,13 @@ def run_ours(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(sum(step_ms))
     launches = ctx.kernel_count() - k0
+    if phase_pass:
+        ctx.set_timing(True)
+        t0_times = ctx.times()
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            step(30_000 + k, Wt, Gt)
+        barrier()
     t1_times = ctx.times()
     ph = {k: (t1_times[k] - t0_times[k]) / args.steps for k in t1_times}
     cnt = ctx.counts()
@@ -492,6 +505,8 @@ def run_ours(args):
                               if gemm_ms > 0 else None, "unit": "TFLOP/s", "flops_per_step": gf, "gemm_ms_per_step": gemm_ms,
                               "peak": peak_dtype},
             "phases_ms": ph,
+            "phases_source": "second pass of the same steps with per-phase CUDA events (N > 1)" if phase_pass else
+                             "per-phase CUDA events on the library stream inside the timed region",
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e,

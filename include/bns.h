@@ -243,6 +243,11 @@ enum { BNS_PH_SAMPLE = 0, BNS_PH_INDUCE, BNS_PH_PACK, BNS_PH_EXCHANGE, BNS_PH_SP
 bns_status bns_query(bns_ctx* ctx, int32_t what, int32_t layer, void* host_dst, int64_t capacity_bytes,
                      int64_t* written);
 
+/* Per-phase CUDA events on (1) or off (0) for the following calls; the context must have been created with
+ * BNS_TIMING (else BNS_ERR_STATE).  Each phase event pair costs a few microseconds of pipeline drain: ~0.3 ms per
+ * epoch at m = 8 on the Reddit shape, so throughput runs at small partitions switch them off. */
+bns_status bns_set_timing(bns_ctx* ctx, int32_t on);
+
 /* The cudaStream_t the context enqueues on (as void*). */
 void* bns_stream(const bns_ctx* ctx);
 

@@ -32,7 +32,7 @@ PHASES = ["sample", "induce", "pack", "exchange", "spmm_fwd", "gemm_fwd", "loss"
           "exchange_bwd", "scatter", "allreduce", "update", "epoch_total", "sample_total"]
 
 EXPORTS = ["bns_get_unique_id", "bns_group_create", "bns_group_destroy", "bns_setup", "bns_sample_boundary",
-           "bns_sample_edges", "bns_set_multilabel", "bns_epoch", "bns_step", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
+           "bns_sample_edges", "bns_set_multilabel", "bns_epoch", "bns_step", "bns_set_timing", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
 BNS_OPT_SGD, BNS_OPT_ADAM = 0, 1
 
 
@@ -94,6 +94,7 @@ def lib():
         L.bns_epoch.argtypes = [vp, vp, f32, vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]
         L.bns_set_training.argtypes = [vp, i32, f64, f64, f64, f64, u64]
         L.bns_step.argtypes = [vp, f64, u64, u64, vp, f32, vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]
+        L.bns_set_timing.argtypes = [vp, i32]
         L.bns_query.argtypes = [vp, i32, i32, vp, i64, ctypes.POINTER(i64)]
         L.bns_stream.restype = vp
         L.bns_stream.argtypes = [vp]
@@ -101,7 +102,7 @@ def lib():
         L.bns_last_error.argtypes = [vp]
         L.bns_destroy.argtypes = [vp]
         for f in ("bns_get_unique_id", "bns_group_create", "bns_setup", "bns_sample_boundary", "bns_sample_edges",
-                  "bns_set_multilabel", "bns_epoch", "bns_step",
+                  "bns_set_multilabel", "bns_epoch", "bns_step", "bns_set_timing",
                   "bns_set_training", "bns_query"):
             getattr(L, f).restype = ctypes.c_int
         L.bns_group_destroy.restype = None
@@ -268,6 +269,9 @@ class Context:
             import torch
             torch.cuda.current_stream().synchronize()
         return bns_step(self.h, p, seed, epoch, weights, lr, grads)
+
+    def set_timing(self, on: bool):
+        _check(lib().bns_set_timing(self.h, 1 if on else 0), self.h)
 
     def set_training(self, optimizer=BNS_OPT_SGD, beta1=0.9, beta2=0.999, eps=1e-8, dropout=0.0, dropout_seed=0):
         bns_set_training(self.h, optimizer, beta1, beta2, eps, dropout, dropout_seed)

@@ -1030,6 +1030,20 @@ bns_status bns_query(bns_ctx* h, int32_t what, int32_t layer, void* dst, int64_t
     });
 }
 
+bns_status bns_set_timing(bns_ctx* h, int32_t on) {
+    if (!h) return BNS_ERR_INVALID;
+    Ctx& c = h->c;
+    if (c.failed || c.plan_only || c.ev.empty()) {
+        c.err = "bns_set_timing needs a context created with BNS_TIMING";
+        return BNS_ERR_STATE;
+    }
+    return guard(h, [&] {
+        BNS_CUDA(cudaStreamSynchronize(c.stream));
+        collect_times(c);
+        c.timing = on != 0;
+    });
+}
+
 void* bns_stream(const bns_ctx* h) { return h ? (void*)h->c.stream : nullptr; }
 
 const char* bns_last_error(const bns_ctx* h) { return h ? h->c.err.c_str() : g_err.c_str(); }

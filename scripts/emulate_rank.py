@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--partition", default="ldg2")
     ap.add_argument("--model", default="sage", choices=["sage", "gat"], help="gat: 2-layer GAT (Table tab:gat)")
     ap.add_argument("--cache-x0", action="store_true", help="BNS_CACHE_INPUT_HALO (f1, R43): no layer-1 exchange")
+    ap.add_argument("--no-timing", action="store_true", help="no per-phase CUDA events (device total only)")
     ap.add_argument("--samplers", nargs="+", default=["bns"], choices=["bns", "bes", "dropedge"],
                     help="f3 Table tab:bes analogue: edge samplers at matched dropped-edge counts (P:681)")
     args = ap.parse_args()
@@ -57,7 +58,7 @@ def main():
         ctx = bns.Context(rank=r, world=args.m, dims=sh.dims, layer=sh.layer, precision=prec, indptr=indptr,
                           indices=indices, part_of=part, features=I.features(inner, sh.d0),
                           labels=np.ascontiguousarray(y_all[inner]), transport=bns.BNS_TRANSPORT_NULL_EMULATE,
-                          flags=bns.BNS_TIMING | (bns.BNS_CACHE_INPUT_HALO if args.cache_x0 else 0))
+                          flags=(0 if args.no_timing else bns.BNS_TIMING) | (bns.BNS_CACHE_INPUT_HALO if args.cache_x0 else 0))
         W = [torch.tensor(w, device="cuda") for w in I.weights(sh.dims, sh.layer)]
         G = [torch.zeros_like(w) for w in W]
         stream = torch.cuda.ExternalStream(ctx.stream())
@@ -75,7 +76,8 @@ def main():
             for e in range(args.warmup):
                 one(e)
             torch.cuda.synchronize()
-            t0 = ctx.times()
+            if not args.no_timing:
+                ctx.set_timing(False)   # device time without per-phase events (they drain the pipeline)
             k0 = ctx.kernel_count()
             ms = []
             wall0 = time.perf_counter()
@@ -87,6 +89,13 @@ def main():
                 b.synchronize()
                 ms.append(a.elapsed_time(b))
             wall = (time.perf_counter() - wall0) / args.steps * 1e3
+            kern = (ctx.kernel_count() - k0) / args.steps
+            if not args.no_timing:   # phase split from a second pass of the same steps with the events on
+                ctx.set_timing(True)
+            t0 = ctx.times()
+            for k in range(args.steps):
+                one(200 + k)
+            torch.cuda.synchronize()
             t1 = ctx.times()
             cnt = ctx.counts()
             ph = {k: round((t1[k] - t0[k]) / args.steps, 4) for k in t1 if t1[k] - t0[k] > 0}
@@ -103,7 +112,7 @@ def main():
                    "pack_gbs": gbs(pack_b, ph.get("pack")), "scatter_gbs": gbs(scat_b, ph.get("scatter")),
                    "cache_x0": bool(args.cache_x0),
                    "device_ms_per_epoch": float(np.median(ms)), "wall_ms_per_epoch": wall,
-                   "est_nvlink_ms": comm_ms, "kernels_per_epoch": (ctx.kernel_count() - k0) / args.steps,
+                   "est_nvlink_ms": comm_ms, "kernels_per_epoch": kern,
                    "n_in": cnt["n_in"], "n_bd": cnt["n_bd"], "n_halo": cnt["n_halo"], "n_sent": cnt["n_sent"],
                    "nnz_kept": cnt["nnz_kept"], "phases_ms": ph,
                    "note": "single-GPU emulation: exchanges/all-reduce are no-ops; NOT an m-GPU measurement"}
