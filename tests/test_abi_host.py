@@ -103,7 +103,23 @@ def test_plan_only_rejects_device_calls():
     with pytest.raises(bns.BnsError) as e:
         c.epoch(w, 0.1)
     assert e.value.code == bns.BNS_ERR_STATE
+    with pytest.raises(bns.BnsError) as e:
+        c.step(0.5, 1, 0, w, 0.1)
+    assert e.value.code == bns.BNS_ERR_STATE
+    with pytest.raises(bns.BnsError) as e:
+        c.set_timing(True)
+    assert e.value.code == bns.BNS_ERR_STATE
     c.close()
+
+
+def test_ipc_transport_needs_allgather():
+    indptr, indices = I.csr_from_edges(4, [(0, 1), (1, 2), (2, 3)])
+    part = np.array([0, 0, 1, 1], np.int32)
+    with pytest.raises(bns.BnsError) as e:
+        bns.Context(rank=0, world=2, dims=[1, 2], layer=0, precision=bns.BNS_FP32, indptr=indptr, indices=indices,
+                    part_of=part, features=np.zeros((2, 1), np.float32), labels=np.zeros(2, np.int32),
+                    transport=bns.BNS_TRANSPORT_IPC)
+    assert e.value.code == bns.BNS_ERR_INVALID and "allgather" in str(e.value)
 
 
 def test_eq3_identity_through_library_plan():

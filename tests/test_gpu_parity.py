@@ -296,6 +296,36 @@ def test_step_equals_sample_then_epoch(m):
     assert outs[0] == outs[1]
 
 
+def test_set_timing_toggles_phase_events():
+    indptr, indices, part, X, y = wl(1500, 30000, 1, 20, 6, 28)
+    dims = [20, 16, 6]
+    run = GpuRun(indptr, indices, part, 1, dims, 0, bns.BNS_FP32, X, y, flags=bns.BNS_TIMING)
+    Ws = I.weights(dims, 0)
+    try:
+        c = run.ctx[0]
+        run.sample(0.5, SEED, 0)
+        run.epoch(Ws, 0.1)
+        t0 = c.times()
+        assert t0["epoch_total"] > 0
+        c.set_timing(False)
+        run.sample(0.5, SEED, 1)
+        run.epoch(Ws, 0.1)
+        assert c.times() == t0
+        c.set_timing(True)
+        run.sample(0.5, SEED, 2)
+        run.epoch(Ws, 0.1)
+        assert c.times()["epoch_total"] > t0["epoch_total"]
+    finally:
+        run.close()
+    run = GpuRun(indptr, indices, part, 1, dims, 0, bns.BNS_FP32, X, y, flags=0)
+    try:
+        with pytest.raises(bns.BnsError) as e:
+            run.ctx[0].set_timing(True)
+        assert e.value.code == bns.BNS_ERR_STATE
+    finally:
+        run.close()
+
+
 def test_binomial_counts_gpu():
     indptr, indices, part, X, y = wl(3000, 60000, 4, 4, 3, 3)
     run = GpuRun(indptr, indices, part, 4, [4, 3], 0, bns.BNS_FP32, X, y, flags=0)
