@@ -253,6 +253,8 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     int64_t seg_max = std::max({c.seg_fwd_cap, c.seg_bwd_cap, c.n_seg_static_fwd});
     c.d_partial = static_cast<float*>(dalloc(c, (size_t)seg_max * c.maxd * sizeof(float)));
     c.d_spmm_work = static_cast<unsigned long long*>(dalloc(c, 64));
+    c.d_fixcnt = static_cast<int32_t*>(dalloc(c, (size_t)(seg_max + 1) * sizeof(int32_t)));
+    BNS_CUDA(cudaMemset(c.d_fixcnt, 0, (size_t)(seg_max + 1) * sizeof(int32_t)));
     // split (hub) row lists: first segment of every row with more than one segment
     auto split_list = [](const std::vector<Seg>& s) {
         std::vector<int64_t> l;

@@ -147,6 +147,7 @@ struct Ctx {
     int64_t n_seg_bwd_inner = 0;
     float* d_partial = nullptr;    // hub-row partial sums
     unsigned long long* d_spmm_work = nullptr;   // SpMM dynamic scheduling counter
+    int32_t* d_fixcnt = nullptr;   // per-segment counters of the fused split-row fixup (zero between launches)
     int64_t* d_split_sf = nullptr;  int64_t n_split_sf = 0;      // split rows of the static forward segments
     int64_t* d_split_bwd = nullptr; int64_t n_split_bwd_inner = 0; // [static inner part ; per-epoch halo part]
     int64_t* d_split_fwd = nullptr;                                  // per-epoch induced forward segments
