@@ -48,6 +48,13 @@ noprefetch:
 $(PKG)/libbns_nopf.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
 
+# generic A/B variant: make variant VAR=name DEFS="-DBNS_X=..." -> $(PKG)/libbns_name.so (BNS_LIB selects it)
+variant:
+	$(MAKE) OBJDIR=build_$(VAR) NVFLAGS="$(NVFLAGS) $(DEFS)" CXXDEF="$(DEFS)" $(PKG)/libbns_$(VAR).so
+
+$(PKG)/libbns_$(VAR).so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
+
 clean:
 	rm -rf $(OBJDIR) oracle/liboracle.so $(PKG)/inputs/libbnsgen.so $(PKG)/libbns.so
 

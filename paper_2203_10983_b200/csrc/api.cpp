@@ -129,18 +129,19 @@ void validate(const bns_config* cfg, int64_t N, const int64_t* indptr, const int
 }
 
 // host-built segments over a static CSR whose row r spans [ptr[r], ptr[r+1]) (+ptr_base in the column array)
-std::vector<Seg> host_segments(const std::vector<int64_t>& ptr, int64_t rows, int64_t ptr_base, int64_t row_base) {
+std::vector<Seg> host_segments(const std::vector<int64_t>& ptr, int64_t rows, int64_t ptr_base, int64_t row_base,
+                              int32_t seg_long) {
     std::vector<Seg> s;
     for (int64_t r = 0; r < rows; ++r) {
         int64_t len = ptr[r + 1] - ptr[r];
-        int32_t ns = len > kSeg ? (int32_t)((len + kSeg - 1) / kSeg) : 1;
+        int32_t ns = seg_count(len, seg_long);
         int64_t first = (int64_t)s.size();
         for (int32_t k = 0; k < ns; ++k) {
             Seg g;
             g.row = (int32_t)(row_base + r);
             g.nseg = ns;
-            g.e0 = ptr_base + ptr[r] + (int64_t)k * kSeg;
-            g.e1 = std::min(ptr_base + ptr[r + 1], g.e0 + kSeg);
+            g.e0 = ptr_base + ptr[r] + (int64_t)k * seg_len(len, seg_long);
+            g.e1 = std::min(ptr_base + ptr[r + 1], g.e0 + seg_len(len, seg_long));
             g.first = first;
             s.push_back(g);
         }
@@ -178,6 +179,10 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
         c.halo_cap = P.n_bd;
     }
     c.nnz_i = P.row_ptr[P.n_in];
+    // R37: long-row segments only for jobs with >= kLongJobNnz arcs per partition (a job-wide constant: every rank
+    // of the job makes the same choice)
+    c.seg_long = c.glob_nnz / std::max(1, c.cfg.world) >= kLongJobNnz ? kSegLong : 0;
+    if (const char* e = std::getenv("BNS_SEG_LONG")) c.seg_long = std::max(0, std::atoi(e));   // tests / A/B
     const size_t ts = tsize(c);
     if (peer_mode(c.cfg)) {   // f1: one exported allocation for everything the peers touch
         const size_t rows = (size_t)(P.n_in + c.halo_cap);
@@ -234,7 +239,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.d_rs_bd = upload(c, rs_bd);
 
     // static segments: backward inner part (A_II, columns in d_tcol[0, ii_nnz)) ...
-    std::vector<Seg> sb = host_segments(P.ii_ptr, P.n_in, 0, 0);
+    std::vector<Seg> sb = host_segments(P.ii_ptr, P.n_in, 0, 0, c.seg_long);
     c.n_seg_bwd_inner = (int64_t)sb.size();
     int64_t halo_seg_cap = P.n_bd + (int64_t)P.br_col.size() / kSeg + 1;
     c.seg_bwd_cap = c.n_seg_bwd_inner + halo_seg_cap;
@@ -245,7 +250,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     for (size_t k = 0; k < scol.size(); ++k)
         scol[k] = P.col_enc[k] >= 0 ? P.col_enc[k] : (int32_t)(P.n_in + (-P.col_enc[k] - 1));
     c.d_static_col = upload(c, scol);
-    std::vector<Seg> sf = host_segments(P.row_ptr, P.n_in, 0, 0);
+    std::vector<Seg> sf = host_segments(P.row_ptr, P.n_in, 0, 0, c.seg_long);
     c.n_seg_static_fwd = (int64_t)sf.size();
     c.d_seg_static_fwd = upload(c, sf);
     c.seg_fwd_cap = P.n_in + c.nnz_i / kSeg + 1;
@@ -253,8 +258,6 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     int64_t seg_max = std::max({c.seg_fwd_cap, c.seg_bwd_cap, c.n_seg_static_fwd});
     c.d_partial = static_cast<float*>(dalloc(c, (size_t)seg_max * c.maxd * sizeof(float)));
     c.d_spmm_work = static_cast<unsigned long long*>(dalloc(c, 64));
-    c.d_fixcnt = static_cast<int32_t*>(dalloc(c, (size_t)(seg_max + 1) * sizeof(int32_t)));
-    BNS_CUDA(cudaMemset(c.d_fixcnt, 0, (size_t)(seg_max + 1) * sizeof(int32_t)));
     // split (hub) row lists: first segment of every row with more than one segment
     auto split_list = [](const std::vector<Seg>& s) {
         std::vector<int64_t> l;
@@ -744,6 +747,7 @@ bns_status bns_setup(const bns_config* cfg, int64_t num_nodes, const int64_t* in
         c.debug_idx = (cfg->flags & BNS_DEBUG_EXCHANGE_INDICES) != 0;
         c.retain = (cfg->flags & BNS_RETAIN_GRADS) != 0;
         build_plan(c.plan, cfg->rank, cfg->world, num_nodes, indptr, indices, part_of);
+        c.glob_nnz = indptr[num_nodes];
         const int64_t n_in = c.plan.n_in;
         if (n_in > 0 && (!features || !labels)) throw Error(BNS_ERR_INVALID, "features/labels NULL");
         int64_t ntr = 0;

@@ -29,6 +29,24 @@ struct Error : std::runtime_error {
 #define BNS_KSEG 256   // A/B on one B200 (make kseg128 / kseg256): 512 -> 256 = m=8 rank epoch 2.23 -> 2.12 ms, m=1 24.3 -> 24.0
 #endif
 constexpr int kSeg = BNS_KSEG;     // SpMM segment length in edges (hub rows are split into segments of this size)
+// rows longer than kLongRow are split into seg_long-edge segments instead when the job is large enough (seg_long =
+// kSegLong when the graph has >= kLongJobNnz arcs per partition, else 0 = never): fewer fp32 partials for the
+// fixup to move on big partitions, no long single-warp tails on small ones.  The split depends only on the row
+// length and that job-wide constant (R37).  Measured (one B200): Reddit m = 1 23.1 -> 22.5 ms with long segments;
+// at m = 8 they cost +13 %.
+#ifndef BNS_KSEG_LONG
+#define BNS_KSEG_LONG 1024
+#endif
+constexpr int kSegLong = BNS_KSEG_LONG;
+constexpr int64_t kLongRow = 2048;
+constexpr int64_t kLongJobNnz = 38ll * 1000 * 1000;   // ~32 x 256 edges per resident SpMM warp on 148 SMs
+__host__ __device__ inline int64_t seg_len(int64_t cnt, int32_t seg_long) {
+    return (seg_long > 0 && cnt > kLongRow) ? (int64_t)seg_long : (int64_t)kSeg;
+}
+__host__ __device__ inline int32_t seg_count(int64_t cnt, int32_t seg_long) {
+    const int64_t L = seg_len(cnt, seg_long);
+    return cnt > L ? (int32_t)((cnt + L - 1) / L) : 1;
+}
 constexpr int kPad = 8;            // feature dims padded to multiples of 8 (16-byte rows for fp32x4 / bf16x8)
 
 inline int64_t pad8(int64_t d) { return (d + kPad - 1) / kPad * kPad; }
@@ -91,6 +109,8 @@ struct Ctx {
     Transport* tr = nullptr;
     int64_t halo_cap = 0;
     int64_t nnz_i = 0;
+    int64_t glob_nnz = 0;          // arcs of the whole graph
+    int32_t seg_long = 0;          // R37 long-row segment length of this job (0: every segment kSeg edges)
     int64_t kernels = 0;
     int64_t dev_bytes = 0;
     std::vector<void*> allocs;
@@ -147,7 +167,6 @@ struct Ctx {
     int64_t n_seg_bwd_inner = 0;
     float* d_partial = nullptr;    // hub-row partial sums
     unsigned long long* d_spmm_work = nullptr;   // SpMM dynamic scheduling counter
-    int32_t* d_fixcnt = nullptr;   // per-segment counters of the fused split-row fixup (zero between launches)
     int64_t* d_split_sf = nullptr;  int64_t n_split_sf = 0;      // split rows of the static forward segments
     int64_t* d_split_bwd = nullptr; int64_t n_split_bwd_inner = 0; // [static inner part ; per-epoch halo part]
     int64_t* d_split_fwd = nullptr;                                  // per-epoch induced forward segments

@@ -43,7 +43,6 @@ struct SpmmArgs {
     int relu = 0;                         // SAGE_FWD_TF: ReLU in the epilogue
     int out_f32 = 0;                      // SAGE_FWD_TF / GAT_FWD: fp32 output (logits) instead of the storage type
     unsigned long long* work = nullptr;   // dynamic segment scheduling: next unclaimed segment (zeroed per launch)
-    int32_t* fixcnt = nullptr;            // fused split-row fixup: finished segments per split row (self-resetting)
     // f4 / R45 GAT: per-node attention scores and softmax statistics (fp32), attention vectors a_l / a_r (dout),
     // del / der (backward)
     const float *gat_el = nullptr, *gat_er = nullptr, *gat_m = nullptr, *gat_inv = nullptr;

@@ -302,14 +302,14 @@ __device__ __forceinline__ int64_t kept_before(int64_t e, const uint32_t* __rest
 
 __global__ void k_induce_rows(const int64_t* __restrict__ ptr, int64_t n_in, const uint32_t* __restrict__ bits,
                               const int64_t* __restrict__ boff, int64_t* __restrict__ out_ptr,
-                              int32_t* __restrict__ nseg) {
+                              int32_t* __restrict__ nseg, int32_t seg_long) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r > n_in) return;
     const int64_t a = kept_before(ptr[r], bits, boff);
     out_ptr[r] = a;
     if (r == n_in) return;
     const int64_t cnt = kept_before(ptr[r + 1], bits, boff) - a;
-    nseg[r] = cnt > kSeg ? (int32_t)((cnt + kSeg - 1) / kSeg) : 1;
+    nseg[r] = seg_count(cnt, seg_long);
 }
 
 // rows split into several segments are appended (first segment index) to a split list for the SpMM fixup;
@@ -319,7 +319,7 @@ __device__ __forceinline__ void push_split(int64_t* list, int64_t* count, int64_
 }
 
 __global__ void k_induce_segs(const int64_t* __restrict__ out_ptr, int64_t n_in, const int64_t* __restrict__ seg_off,
-                              Seg* __restrict__ segs, int64_t* __restrict__ split, int64_t* __restrict__ n_split) {
+                              Seg* __restrict__ segs, int64_t* __restrict__ split, int64_t* __restrict__ n_split, int32_t seg_long) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_in) return;
     const int64_t b0 = out_ptr[r], b1 = out_ptr[r + 1];
@@ -329,8 +329,8 @@ __global__ void k_induce_segs(const int64_t* __restrict__ out_ptr, int64_t n_in,
         Seg sg;
         sg.row = (int32_t)r;
         sg.nseg = (int32_t)ns;
-        sg.e0 = b0 + k * kSeg;
-        sg.e1 = min(b1, sg.e0 + kSeg);
+        sg.e0 = b0 + k * seg_len(b1 - b0, seg_long);
+        sg.e1 = min(b1, sg.e0 + seg_len(b1 - b0, seg_long));
         sg.first = s0;
         segs[s0 + k] = sg;
     }
@@ -364,20 +364,20 @@ void launch_induce(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
         BNS_CUDA(cudaMemsetAsync(tot, 0, sizeof(int64_t), c.stream));
     }
     k_induce_rows<<<(unsigned)((n_in + 1 + 255) / 256), 256, 0, c.stream>>>(c.d_row_ptr, n_in, c.d_ebits, c.d_eboff,
-                                                                          c.d_ind_ptr, c.d_row_nseg);
+                                                                          c.d_ind_ptr, c.d_row_nseg, c.seg_long);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
     scan_i32(c, c.d_row_nseg, c.d_row_soff, n_in, tot + 1);
     BNS_CUDA(cudaMemsetAsync(tot + 4, 0, sizeof(int64_t), c.stream));
     k_induce_segs<<<(unsigned)((n_in + 255) / 256), 256, 0, c.stream>>>(c.d_ind_ptr, n_in, c.d_row_soff, c.d_seg_fwd,
-                                                                       c.d_split_fwd, tot + 4);
+                                                                       c.d_split_fwd, tot + 4, c.seg_long);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 
 // backward (transposed) segments of the halo rows: halo slot s <- boundary b = U_b[s], inner neighbours of b
 __global__ void k_bwd_count(const int64_t* __restrict__ seg_pos, int m, const int32_t* __restrict__ U_b,
-                            const int64_t* __restrict__ br_ptr, int64_t cap, int32_t* __restrict__ nseg) {
+                            const int64_t* __restrict__ br_ptr, int64_t cap, int32_t* __restrict__ nseg, int32_t seg_long) {
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= cap) return;
     int64_t n_halo = seg_pos[m] - seg_pos[0];
@@ -385,7 +385,7 @@ __global__ void k_bwd_count(const int64_t* __restrict__ seg_pos, int m, const in
     if (s < n_halo) {
         int32_t b = U_b[s];
         int64_t len = br_ptr[b + 1] - br_ptr[b];
-        v = len > kSeg ? (int)((len + kSeg - 1) / kSeg) : 1;
+        v = seg_count(len, seg_long);
     }
     nseg[s] = v;
 }
@@ -393,7 +393,7 @@ __global__ void k_bwd_count(const int64_t* __restrict__ seg_pos, int m, const in
 __global__ void k_bwd_write(const int64_t* __restrict__ seg_pos, int m, const int32_t* __restrict__ U_b,
                             const int64_t* __restrict__ br_ptr, int64_t cap, const int64_t* __restrict__ soff,
                             int64_t seg_base, int64_t e_base, int64_t n_in, Seg* __restrict__ segs,
-                            int64_t* __restrict__ split, int64_t* __restrict__ n_split) {
+                            int64_t* __restrict__ split, int64_t* __restrict__ n_split, int32_t seg_long) {
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= cap) return;
     int64_t n_halo = seg_pos[m] - seg_pos[0];
@@ -406,8 +406,8 @@ __global__ void k_bwd_write(const int64_t* __restrict__ seg_pos, int m, const in
         Seg sg;
         sg.row = (int32_t)(n_in + s);
         sg.nseg = (int32_t)ns;
-        sg.e0 = e_lo + k * kSeg;
-        sg.e1 = min(e_hi, sg.e0 + kSeg);
+        sg.e0 = e_lo + k * seg_len(e_hi - e_lo, seg_long);
+        sg.e1 = min(e_hi, sg.e0 + seg_len(e_hi - e_lo, seg_long));
         sg.first = s0;
         segs[s0 + k] = sg;
     }
@@ -423,13 +423,13 @@ void launch_bwd_segments(Ctx& c) {
         return;
     }
     unsigned grid = (unsigned)((cap + 255) / 256);
-    k_bwd_count<<<grid, 256, 0, c.stream>>>(c.d_seg_pos, m, c.d_cand_out, c.d_br_ptr, cap, c.d_row_nseg);
+    k_bwd_count<<<grid, 256, 0, c.stream>>>(c.d_seg_pos, m, c.d_cand_out, c.d_br_ptr, cap, c.d_row_nseg, c.seg_long);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
     scan_i32(c, c.d_row_nseg, c.d_row_soff, cap, tot + 2);
     k_bwd_write<<<grid, 256, 0, c.stream>>>(c.d_seg_pos, m, c.d_cand_out, c.d_br_ptr, cap, c.d_row_soff,
                                             c.n_seg_bwd_inner, c.ii_nnz, c.plan.n_in, c.d_seg_bwd,
-                                            c.d_split_bwd + c.n_split_bwd_inner, tot + 3);
+                                            c.d_split_bwd + c.n_split_bwd_inner, tot + 3, c.seg_long);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -561,19 +561,19 @@ __device__ __forceinline__ int64_t trow_out(int64_t r, int64_t n_in, const int32
 __global__ void k_tinduce_rows(const int64_t* __restrict__ ptr, int64_t n_rows, int64_t n_in,
                                const int32_t* __restrict__ slot_of_b, const uint32_t* __restrict__ bits,
                                const int64_t* __restrict__ boff, int64_t* __restrict__ out_ptr,
-                               int32_t* __restrict__ nseg) {
+                               int32_t* __restrict__ nseg, int32_t seg_long) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r > n_rows) return;
     const int64_t a = kept_before(ptr[r], bits, boff);
     out_ptr[r] = a;
     if (r == n_rows) return;
     const int64_t cnt = kept_before(ptr[r + 1], bits, boff) - a;
-    nseg[r] = trow_out(r, n_in, slot_of_b) < 0 ? 0 : (cnt > kSeg ? (int32_t)((cnt + kSeg - 1) / kSeg) : 1);
+    nseg[r] = trow_out(r, n_in, slot_of_b) < 0 ? 0 : seg_count(cnt, seg_long);
 }
 
 __global__ void k_tinduce_segs(const int64_t* __restrict__ out_ptr, int64_t n_rows, int64_t n_in,
                                const int32_t* __restrict__ slot_of_b, const int64_t* __restrict__ seg_off,
-                               Seg* __restrict__ segs, int64_t* __restrict__ split, int64_t* __restrict__ n_split) {
+                               Seg* __restrict__ segs, int64_t* __restrict__ split, int64_t* __restrict__ n_split, int32_t seg_long) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rows) return;
     const int64_t s0 = seg_off[r], ns = seg_off[r + 1] - s0;
@@ -585,8 +585,8 @@ __global__ void k_tinduce_segs(const int64_t* __restrict__ out_ptr, int64_t n_ro
         Seg sg;
         sg.row = row;
         sg.nseg = (int32_t)ns;
-        sg.e0 = b0 + k * kSeg;
-        sg.e1 = min(b1, sg.e0 + kSeg);
+        sg.e0 = b0 + k * seg_len(b1 - b0, seg_long);
+        sg.e1 = min(b1, sg.e0 + seg_len(b1 - b0, seg_long));
         sg.first = s0;
         segs[s0 + k] = sg;
     }
@@ -612,14 +612,14 @@ void launch_induce_bwd_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) 
         BNS_CUDA(cudaMemsetAsync(tot + 5, 0, sizeof(int64_t), c.stream));
     }
     k_tinduce_rows<<<(unsigned)((n_rows + 1 + 255) / 256), 256, 0, c.stream>>>(
-        c.d_tptr, n_rows, n_in, c.d_slot_of_b, c.d_ebits, c.d_eboff, c.d_ind_tptr, c.d_trow_nseg);
+        c.d_tptr, n_rows, n_in, c.d_slot_of_b, c.d_ebits, c.d_eboff, c.d_ind_tptr, c.d_trow_nseg, c.seg_long);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
     scan_i32(c, c.d_trow_nseg, c.d_trow_soff, n_rows, tot + 6);
     BNS_CUDA(cudaMemsetAsync(tot + 7, 0, sizeof(int64_t), c.stream));
     if (n_rows > 0) {
         k_tinduce_segs<<<(unsigned)((n_rows + 255) / 256), 256, 0, c.stream>>>(
-            c.d_ind_tptr, n_rows, n_in, c.d_slot_of_b, c.d_trow_soff, c.d_eseg_bwd, c.d_esplit_bwd, tot + 7);
+            c.d_ind_tptr, n_rows, n_in, c.d_slot_of_b, c.d_trow_soff, c.d_eseg_bwd, c.d_esplit_bwd, tot + 7, c.seg_long);
         c.kernels += 1;
         BNS_CHECK_LAUNCH();
     }

@@ -279,39 +279,6 @@ k_spmm(const SpmmArgs a) {
                     for (int k = 0; k < VN; k += 4)
                         *reinterpret_cast<float4*>(pp + vi * VN + k) = make_float4(acc[v][k], acc[v][k + 1], acc[v][k + 2], acc[v][k + 3]);
             }
-            if (a.fixcnt) {
-                // fused split-row fixup: the warp that completes a row's last segment sums the row's partials in
-                // segment order (the same additions as k_spmm_fixup) and runs the epilogue; it resets the counter
-                const unsigned gm = LPR == 32 ? 0xffffffffu : ((1u << LPR) - 1u);
-                __threadfence();
-                __syncwarp(gm);
-                int last = 0;
-                if (l == 0) last = atomicAdd(a.fixcnt + s.first, 1) == s.nseg - 1;
-                last = __shfl_sync(gm, last, 0);
-                if (last) {
-                    __threadfence();
-#pragma unroll
-                    for (int v = 0; v < VPL; ++v) {
-                        const int vi = l + v * LPR;
-                        if (vi >= nvec) continue;
-                        float f[VN];
-#pragma unroll
-                        for (int k = 0; k < VN; ++k) f[k] = 0.f;
-                        const float* p0 = a.partial + s.first * (int64_t)a.d + vi * VN;
-                        for (int q = 0; q < s.nseg; ++q)
-#pragma unroll
-                            for (int k = 0; k < VN; k += 4) {
-                                const float4 t = __ldcg(reinterpret_cast<const float4*>(p0 + (int64_t)q * a.d + k));
-                                f[k] += t.x;
-                                f[k + 1] += t.y;
-                                f[k + 2] += t.z;
-                                f[k + 3] += t.w;
-                            }
-                        epilogue_store<T>(a, s.row, vi, f);
-                    }
-                    if (l == 0) a.fixcnt[s.first] = 0;
-                }
-            }
         } else {
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
@@ -376,14 +343,6 @@ __global__ void __launch_bounds__(256) k_spmm_fixup(const SpmmArgs a) {
 // 2 (default) = one resident wave, segments claimed dynamically (a.work)
 static int spmm_sched() {
     static const int v = [] { const char* e = std::getenv("BNS_SPMM_SCHED"); return e ? std::atoi(e) : 2; }();
-    return v;
-}
-
-// BNS_SPMM_FUSED_FIXUP=1: the warp finishing a split row's last segment sums its partials inside the SpMM instead of
-// the separate k_spmm_fixup launch (same additions, same bits).  Measured on one B200: Reddit m = 1 23.0 -> 24.0 ms
-// (one warp serially sums up to ~400 partials of a hub row: a tail), m = 8 neutral -- so off by default.
-static bool fused_fixup() {
-    static const bool v = [] { const char* e = std::getenv("BNS_SPMM_FUSED_FIXUP"); return e && e[0] == '1'; }();
     return v;
 }
 
@@ -497,7 +456,6 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
     unsigned grid = (unsigned)std::min<int64_t>((a0.n_segs + 7) / 8, 148 * 32);
     for (int64_t c0 = 0; c0 < a0.d; c0 += tile) {
         SpmmArgs a = a0;
-        a.fixcnt = fused_fixup() ? c.d_fixcnt : nullptr;
         a.d = (int32_t)std::min<int64_t>(tile, a0.d - c0);
         a.src = static_cast<const char*>(a0.src) + c0 * ts;
         a.out = static_cast<char*>(a0.out) + c0 * ((a0.out_f32 || a0.mode == GAT_RAW) ? 4 : ts);
@@ -508,7 +466,7 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
         else dispatch<float>(c, a, grid);
         c.kernels += 1;
         BNS_CHECK_LAUNCH();
-        if (a.n_split > 0 && !a.fixcnt) {   // only the split (hub) rows, listed by their first segment
+        if (a.n_split > 0) {   // only the split (hub) rows, listed by their first segment
             const unsigned fg = (unsigned)std::min<int64_t>((a.n_split + 7) / 8, 148 * 8);
             if (c.prec == BNS_BF16) k_spmm_fixup<__nv_bfloat16><<<fg, 256, 0, c.stream>>>(a);
             else k_spmm_fixup<float><<<fg, 256, 0, c.stream>>>(a);

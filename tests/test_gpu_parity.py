@@ -174,6 +174,31 @@ def test_six_vector_rows_parity(dims, prec, m, p):
         run.close()
 
 
+@pytest.mark.parametrize("prec", [bns.BNS_FP32, bns.BNS_BF16])
+@pytest.mark.parametrize("m,p", [(1, 1.0), (3, 0.5)])
+def test_long_row_segments_parity(prec, m, p, monkeypatch):
+    """R37 long-row segments (rows above 2048 kept edges split into 1024-edge segments; the default only for jobs with
+    >= 38 M arcs per partition) forced on a small dense graph: forward / transposed segment builders, the split-row
+    fixup and the static p = 1 segments against the oracle."""
+    monkeypatch.setenv("BNS_SEG_LONG", "1024")
+    dims, layer = [37, 24, 16, 5], bns.BNS_LAYER_SAGE_MEAN
+    L = len(dims) - 1
+    indptr, indices, part, X, y = wl(20000, 1500000, m, dims[0], dims[-1], 101 + m)
+    assert (np.diff(indptr) > 4096).sum() >= 2   # long rows of several 1024-edge segments
+    Ws = I.weights(dims, layer)
+    Wd = [w.astype(np.float64) for w in Ws]
+    run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y)
+    orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
+    orc.set_bf16(prec == bns.BNS_BF16)
+    try:
+        for e in range(2):
+            run.sample(p, SEED, e)
+            orc.sample(p, SEED, e)
+            Ws = compare_epoch(run, orc, L, Ws, Wd, 0.5, prec, tag=f"long-seg epoch{e}")
+    finally:
+        run.close()
+
+
 def test_cora_config0():
     """BASELINE.json configs[0]: Cora-shaped, 2-layer GCN hidden 16, 2 partitions, p=0.5, fixed Philox seed."""
     sh = I.SHAPES["cora"]
