@@ -105,3 +105,34 @@ def test_reddit_m8_sampling_bitexact_and_rows(reddit):
             assert err < 2e-2, (r, err)
     finally:
         run.close()
+
+
+@pytest.mark.parametrize("name", ["products", "yelp"])
+def test_other_shapes_m1_two_layers(name):
+    """BASELINE.json configs[2] / [3] at full size, m = 1, bf16 (bench.py's launch configuration): sampled rows of H^1
+    recomputed in float64 from X (layer 1), and of H^2 from the kernel's own H^1 rows (layer 2 -- on the Yelp shape
+    its 512-wide gather runs as two 256-column L2 tiles), against R1 / PAPER.md:100."""
+    sh = I.SHAPES[name]
+    indptr, indices = I.rmat(sh.N, sh.nnz)
+    y = I.labels(sh.N, sh.C, sh.train_frac)
+    part = np.zeros(sh.N, np.int32)
+    X = I.features(np.arange(sh.N, dtype=np.int32), sh.d0)
+    run = GpuRun(indptr, indices, part, 1, sh.dims, sh.layer, bns.BNS_BF16, X, y, flags=0)
+    try:
+        Ws = I.weights(sh.dims, sh.layer)
+        run.sample(0.1, SEED, 0)
+        loss, acc, G, _ = run.epoch(Ws, 0.0)
+        assert np.isfinite(loss)
+        rng = np.random.default_rng(1)
+        deg = np.diff(indptr)
+        rows = np.union1d(np.sort(rng.choice(sh.N, 300, replace=False)), np.argsort(-deg)[:6])
+        H1 = run.ctx[0].rows(bns.BNS_Q_H, 1, sh.dims[1])
+        H2 = run.ctx[0].rows(bns.BNS_Q_H, 2, sh.dims[2])
+        for l, (Hin, Hout) in enumerate([(X, H1), (H1, H2)]):
+            zr = z_rows(indptr, indices, lambda g: Hin[g], rows)
+            pre = np.concatenate([zr, Hin[rows].astype(np.float64)], 1) @ Ws[l].astype(np.float64)
+            h = np.maximum(pre, 0)
+            err = np.abs(Hout[rows] - h).max() / np.abs(h).max()
+            assert err < 2e-2, (name, l + 1, err)
+    finally:
+        run.close()
