@@ -12,6 +12,7 @@
 // all 4 warps drain TMEM with tcgen05.ld.32x32b and apply the epilogue (ReLU / cast / row scale).  K tails and
 // partial M / N tiles are handled by TMA's zero fill and masked stores.
 #include <cuda.h>
+#include <cstdint>
 
 #include "common.h"
 #include "dev.cuh"
@@ -39,6 +40,7 @@ struct TcArgs {
     int64_t split_stride;   // elements between split-K partial slices
     const float* rowscale;
     int64_t scale_cols;
+    int64_t msplit = INT64_MAX;   // MN-major A: output rows >= msplit come from map A1 (row m - msplit)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -155,9 +157,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                         if (kb < args.nk0) tma_load_2d(&mapA0, &full[s], sa, kb * TC_BK, (int)m0);
                         else tma_load_2d(&mapA1, &full[s], sa, (kb - args.nk0) * TC_BK, (int)m0);
                     } else {
-                        // A MN-major (A^T stored row-major as [k][m]): two boxes {64 (m), 64 (k)}
-                        tma_load_2d(&mapA0, &full[s], sa, (int)m0, kb * TC_BK);
-                        tma_load_2d(&mapA0, &full[s], sa + 8192, (int)m0 + 64, kb * TC_BK);
+                        // A MN-major (A^T stored row-major as [k][m]): two boxes {64 (m), 64 (k)}; output rows past
+                        // msplit read the second operand (two dW GEMMs sharing D in one launch)
+                        const bool second = m0 >= args.msplit;
+                        const CUtensorMap* ma = second ? &mapA1 : &mapA0;
+                        const int mm = (int)(second ? m0 - args.msplit : m0);
+                        tma_load_2d(ma, &full[s], sa, mm, kb * TC_BK);
+                        tma_load_2d(ma, &full[s], sa + 8192, mm + 64, kb * TC_BK);
                     }
                     if (!B_MN) {
                         tma_load_2d(&mapB, &full[s], sb, kb * TC_BK, (int)n0);        // box {64 (k), BN (n)}
@@ -372,6 +378,41 @@ void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int6
     CUtensorMap mb = make_map(D, N, Mn, ldd, 64);
     launch_tc<true, true>(c, ma, ma, mb, a, persistent_grid(cdiv(K, TC_BM) * cdiv(N, a.BN) * S));
     splitk_reduce(c, (int)S, K, N, Wg, ldw);
+}
+
+// [dW_0 ; dW_1] = [A0 | A1]^T D in one launch + one split-K reduce (rows [0, K) from A0, [K, 2K) from A1; the
+// GraphSAGE dW_z / dW_h pair, Wg rows contiguous).  Needs K % 128 == 0 (else two gemm_wgrad_tc calls).
+void gemm_wgrad2_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, const void* A1, int64_t lda,
+                    const void* D, int64_t ldd, float* Wg, int64_t ldw) {
+    if (K % TC_BM != 0) {
+        gemm_wgrad_tc(c, Mn, K, N, A0, lda, D, ldd, Wg, ldw);
+        gemm_wgrad_tc(c, Mn, K, N, A1, lda, D, ldd, Wg + K * ldw, ldw);
+        return;
+    }
+    if (N <= 0) return;
+    const int64_t K2 = 2 * K;
+    TcArgs a{};
+    a.M = K2;
+    a.N = N;
+    a.BN = (int)std::min<int64_t>(256, cdiv(N, 64) * 64);
+    a.nk = (int)cdiv(Mn, 64);
+    a.nk0 = a.nk;
+    a.msplit = K;
+    const int64_t tiles = cdiv(K2, TC_BM) * cdiv(N, a.BN);
+    static const int kmin = [] { const char* e = std::getenv("BNS_WGRAD_KMIN"); return e ? std::max(1, std::atoi(e)) : 16; }();
+    int64_t S = std::max<int64_t>(1, std::min<int64_t>(cdiv(148, tiles), std::max(1, a.nk / kmin)));
+    while (S > 1 && S * K2 * N > c.splitk_cap) --S;
+    a.kb_per_split = (int)cdiv(a.nk, S);
+    S = cdiv(a.nk, a.kb_per_split);
+    a.epi = EPI_F32;
+    a.out = c.d_splitk;
+    a.ldc = N;
+    a.split_stride = K2 * N;
+    CUtensorMap m0 = make_map(A0, K, Mn, lda, 64);
+    CUtensorMap m1 = make_map(A1, K, Mn, lda, 64);
+    CUtensorMap mb = make_map(D, N, Mn, ldd, 64);
+    launch_tc<true, true>(c, m0, m1, mb, a, persistent_grid(tiles * S));
+    splitk_reduce(c, (int)S, K2, N, Wg, ldw);
 }
 
 // dX: C[M x Nc] = D[M x K] · B^T with B = W [Nc][K] row-major; columns < scale_cols scaled by rowscale[row]

@@ -88,6 +88,8 @@ void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64
                  int64_t lda1, const void* WT, int64_t Kw, void* C, int64_t ldc, bool relu, bool out_f32);
 void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int64_t lda, const void* D, int64_t ldd,
                    float* Wg, int64_t ldw);
+void gemm_wgrad2_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, const void* A1, int64_t lda,
+                    const void* D, int64_t ldd, float* Wg, int64_t ldw);
 void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t ldd, const void* B, int64_t ldb,
                 void* C, int64_t ldc, const float* rowscale, int64_t scale_cols);
 

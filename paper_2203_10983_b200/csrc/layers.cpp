@@ -361,8 +361,12 @@ void backward_layer_std(Ctx& c, const EpochView& v, int l, void* Hin) {
         float* g = c.d_gflat + c.goff[l - 1];
         auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
         auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
-        wgrad(c, n_in, din, dout, c.Z[l], din, c.d_dpre, dout, g, dout);
-        if (sage) wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
+        if (sage && c.use_tc) {   // dW_z and dW_h share dPre: one launch, one split-K reduce
+            gemm_wgrad2_tc(c, n_in, din, dout, c.Z[l], Hin, din, c.d_dpre, dout, g, dout);
+        } else {
+            wgrad(c, n_in, din, dout, c.Z[l], din, c.d_dpre, dout, g, dout);
+            if (sage) wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
+        }
         if (l > 1) {
             if (sage)
                 dxg(c, n_in, 2 * din, dout, c.d_dpre, dout, c.Wt[l - 1], dout, c.d_dxcat, 2 * din, c.d_deg_in, din);

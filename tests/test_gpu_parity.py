@@ -199,6 +199,29 @@ def test_long_row_segments_parity(prec, m, p, monkeypatch):
         run.close()
 
 
+@pytest.mark.parametrize("tf", [False, True])
+@pytest.mark.parametrize("m,p", [(1, 1.0), (3, 0.4)])
+def test_merged_wgrad_parity(tf, m, p):
+    """Aggregate-first GraphSAGE layers with d_in % 128 == 0 compute dW_z and dW_h in ONE tcgen05 launch (two A
+    operands split by output row) + one split-K reduce: gradients against the oracle (bf16, 2e-2)."""
+    dims, layer, prec = [37, 128, 128, 5], bns.BNS_LAYER_SAGE_MEAN, bns.BNS_BF16
+    L = len(dims) - 1
+    indptr, indices, part, X, y = wl(3000, 90000, m, dims[0], dims[-1], 111 + m)
+    Ws = I.weights(dims, layer)
+    Wd = [w.astype(np.float64) for w in Ws]
+    flags = bns.BNS_RETAIN_GRADS | (0 if tf else bns.BNS_NO_TRANSFORM_FIRST)
+    run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y, flags=flags)
+    orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
+    orc.set_bf16(True)
+    try:
+        for e in range(2):
+            run.sample(p, SEED, e)
+            orc.sample(p, SEED, e)
+            Ws = compare_epoch(run, orc, L, Ws, Wd, 0.5, prec, tag=f"merged-wgrad epoch{e}")
+    finally:
+        run.close()
+
+
 def test_cora_config0():
     """BASELINE.json configs[0]: Cora-shaped, 2-layer GCN hidden 16, 2 partitions, p=0.5, fixed Philox seed."""
     sh = I.SHAPES["cora"]
