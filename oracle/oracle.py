@@ -157,10 +157,6 @@ class Oracle:
             a = np.ascontiguousarray(f, np.int32)
             lib().orc_set_keep(self.h, p, r, _p(a))
 
-    def wshape(self, l):
-        rows = (2 if self.layer == 0 else 1) * int(self.dims[l])
-        return rows, int(self.dims[l + 1])
-
     def epoch(self, weights, lr):
         """weights: list of float64 arrays (updated in place). Returns (loss, acc, grads)."""
         W = [np.ascontiguousarray(w, np.float64) for w in weights]

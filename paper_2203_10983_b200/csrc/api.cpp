@@ -7,6 +7,8 @@
 #include <cstring>
 #include <memory>
 
+#include <thread>
+
 #include "common.h"
 #include "kernels.h"
 #include "layers.h"
@@ -117,6 +119,28 @@ void validate(const bns_config* cfg, int64_t N, const int64_t* indptr, const int
             if (e > indptr[v] && indices[e - 1] >= u)
                 throw Error(BNS_ERR_INVALID, "columns not strictly ascending at row " + std::to_string(v));
         }
+    }
+    // symmetric (bns.h): every arc v -> u has its reverse u -> v (D_{i->j} = B_j ∩ V_i relies on it); rows are
+    // sorted by now, so each reverse is a binary search -- split over host threads (1.6 B arcs at C5)
+    {
+        const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+        std::vector<int64_t> bad(nt, -1);
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                for (int64_t v = N * t / nt; v < N * (t + 1) / nt; ++v)
+                    for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e) {
+                        const int32_t u = indices[e];
+                        if (!std::binary_search(indices + indptr[u], indices + indptr[u + 1], (int32_t)v)) {
+                            bad[t] = v;
+                            return;
+                        }
+                    }
+            });
+        for (auto& x : th) x.join();
+        for (int64_t v : bad)
+            if (v >= 0) throw Error(BNS_ERR_INVALID, "graph not symmetric: an arc of row " + std::to_string(v) +
+                                                         " has no reverse arc");
     }
     std::vector<int64_t> cnt(cfg->world, 0);
     for (int64_t v = 0; v < N; ++v) {
@@ -667,7 +691,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         PhaseTimer t(c, BNS_PH_UPDATE);
         float* const* Gp = host_w ? G.data() : (G_in ? G.data() : nullptr);
         if (c.optimizer == BNS_OPT_ADAM) {
-            ++c.adam_t;   // R39: one Adam step per bns_epoch call
+            ++c.adam_t;   // R39: one Adam step per bns_epoch call (taken back below if the step is skipped)
             launch_adam(c, W.data(), Gp, lr);
         } else {
             launch_sgd(c, W.data(), Gp, lr);
@@ -686,6 +710,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         }
     }
     BNS_CUDA(cudaStreamSynchronize(c.stream));
+    if (nonfinite && c.optimizer == BNS_OPT_ADAM) --c.adam_t;   // no update, no step: bias corrections stay in step
     if (c.tr) c.tr->poll(c);
     collect_times(c);
     const double ntr = (double)c.n_train_global;
@@ -1060,6 +1085,12 @@ void bns_destroy(bns_ctx* h) {
     if (!c.plan_only) {
         cudaSetDevice(c.cfg.device);
         if (c.stream) cudaStreamSynchronize(c.stream);
+        if (c.tr && c.stream) {
+            try {
+                c.tr->shutdown(c);
+            } catch (...) {   // no exception crosses the ABI; teardown goes on
+            }
+        }
     }
     delete c.tr;
     for (void* p : c.allocs) cudaFree(p);

@@ -36,6 +36,7 @@ struct bns_group {
     std::vector<double*> dbuf;
     std::vector<int> attached;
     std::vector<const void*> blob;   // host all-gather staging (peer-memory transport in-process)
+    std::vector<void*> deferred;     // peer arenas of detached in-process members, freed by the last one out
 };
 
 namespace bns {
@@ -53,6 +54,25 @@ void group_barrier(bns_group* g) {
     }
     if (!g->cv.wait_for(lk, std::chrono::seconds(300), [&] { return g->gen != my; }))
         throw Error(BNS_ERR_RUNTIME, "local transport: barrier timeout (a rank did not reach the collective)");
+}
+
+// In-process transports hand the other contexts' raw device pointers to kernels (k_sum_ptrs, k_halo_pull,
+// k_scatter_peer, k_peer_barrier): contexts on different devices need peer access, which is enabled here for every
+// device of the group; a group whose devices cannot reach each other is refused.
+void enable_peer_access(const Ctx& c, const std::vector<int64_t>& devs) {
+    for (int64_t d64 : devs) {
+        const int d = (int)d64;
+        if (d == c.cfg.device) continue;
+        int ok = 0;
+        BNS_CUDA(cudaDeviceCanAccessPeer(&ok, c.cfg.device, d));
+        if (!ok)
+            throw Error(BNS_ERR_INVALID, "local group: device " + std::to_string(c.cfg.device) +
+                                             " has no peer access to device " + std::to_string(d));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) throw Error(BNS_ERR_RUNTIME, std::string("cudaDeviceEnablePeerAccess: ") +
+                                                                  cudaGetErrorString(e));
+    }
 }
 
 #define BNS_NCCL(x)                                                                                         \
@@ -128,6 +148,11 @@ struct LocalTransport : Transport {
         }
         BNS_CUDA(cudaEventCreateWithFlags(&g->ev_ready[me], cudaEventDisableTiming));
         BNS_CUDA(cudaEventCreateWithFlags(&g->ev_done[me], cudaEventDisableTiming));
+        g->ival[me] = c.cfg.device;
+        group_barrier(g);
+        std::vector<int64_t> devs(g->ival.begin(), g->ival.end());
+        group_barrier(g);
+        enable_peer_access(c, devs);
     }
     ~LocalTransport() override {
         if (d_fout) cudaFree(d_fout);
@@ -275,6 +300,13 @@ struct PeerTransport : Transport {
         BNS_CUDA(cudaHostAlloc(&h_err, sizeof(int), cudaHostAllocMapped));
         *h_err = 0;
         BNS_CUDA(cudaHostGetDevicePointer((void**)&d_err, h_err, 0));
+        c.d_abort = d_err;
+        if (g) {
+            std::vector<int64_t> devs(m);
+            const int64_t dev = c.cfg.device;
+            allgather(c, &dev, devs.data(), sizeof(int64_t));
+            enable_peer_access(c, devs);
+        }
         std::vector<int32_t> owner(P.n_bd + 1, 0);
         for (int j = 0; j < m; ++j)
             for (int64_t b = P.B_off[j]; b < P.B_off[j + 1]; ++b) owner[b] = j;
@@ -370,7 +402,32 @@ struct PeerTransport : Transport {
         if (g) {
             std::lock_guard<std::mutex> lk(g->mu);
             g->attached[me] = 0;
+            bool any = false;
+            for (int a : g->attached) any = any || a;
+            if (!any) {   // every member has drained its stream: nobody reads a peer arena any more
+                for (void* p : g->deferred) cudaFree(p);
+                g->deferred.clear();
+            }
         }
+    }
+    // IPC (one process per GPU, destroyed concurrently): one more device barrier, then drain -- after it every peer
+    // has finished its last read of this rank's buffers.  In-process members are usually closed one after another
+    // from one thread, where a barrier would deadlock: the arena is handed to the group instead and freed when the
+    // last member detaches (each member syncs its own stream in bns_destroy first).
+    void shutdown(Ctx& c) override {
+        c.d_abort = nullptr;
+        if (g) {
+            std::lock_guard<std::mutex> lk(g->mu);
+            for (auto it = c.allocs.begin(); it != c.allocs.end(); ++it)
+                if (*it == (void*)c.arena) {
+                    c.allocs.erase(it);
+                    g->deferred.push_back(c.arena);
+                    break;
+                }
+            return;
+        }
+        if (!*(volatile int*)h_err) barrier(c, false);
+        cudaStreamSynchronize(c.stream);
     }
     void allgather(Ctx&, const void* mine, void* all, size_t bytes) {
         if (g) {

@@ -36,11 +36,7 @@ GatBufs gat_bufs(const Ctx& c, int l) {
 void forward_layer_gat(Ctx& c, const EpochView& v, int l, void* Hin) {
     const int L = c.L;
     const int64_t n_in = c.plan.n_in;
-    const size_t ts = tsz(c);
-    const bool sage = c.layer == BNS_LAYER_SAGE_MEAN;
     const int64_t din = c.dp[l - 1], dout = c.dp[l];
-    const float inv_p = v.inv_p;
-    (void)L; (void)ts; (void)sage; (void)inv_p;
     // f4 / R45: Y = Hin W on every stacked row (tcgen05), el / er, softmax statistics, then
     // pre_v = Σ_u alpha_vu Y_u + alpha_vv Y_v with ReLU (hidden) or fp32 logits (last) in the SpMM epilogue
     const bool last = (l == L);
@@ -96,10 +92,8 @@ void forward_layer_tf(Ctx& c, const EpochView& v, int l, void* Hin) {
     const int L = c.L;
     const int64_t n_in = c.plan.n_in;
     const size_t ts = tsz(c);
-    const bool sage = c.layer == BNS_LAYER_SAGE_MEAN;
     const int64_t din = c.dp[l - 1], dout = c.dp[l];
     const float inv_p = v.inv_p;
-    (void)L; (void)ts; (void)sage; (void)inv_p;
     // R42 transform-first: [Y | S] = Hin [W_top | W_bot] on every stacked row, then
     // pre_v = (1/deg_G(v)) Σ_u c_u Y_u + S_v with ReLU (hidden) or fp32 logits (last) in the SpMM epilogue
     const bool last = (l == L);
@@ -143,11 +137,9 @@ void forward_layer_tf(Ctx& c, const EpochView& v, int l, void* Hin) {
 void forward_layer_std(Ctx& c, const EpochView& v, int l, void* Hin) {
     const int L = c.L;
     const int64_t n_in = c.plan.n_in;
-    const size_t ts = tsz(c);
     const bool sage = c.layer == BNS_LAYER_SAGE_MEAN;
     const int64_t din = c.dp[l - 1], dout = c.dp[l];
     const float inv_p = v.inv_p;
-    (void)L; (void)ts; (void)sage; (void)inv_p;
     {
         PhaseTimer t(c, BNS_PH_SPMM_FWD);
         SpmmArgs a{};
@@ -188,11 +180,7 @@ void forward_layer_std(Ctx& c, const EpochView& v, int l, void* Hin) {
 void backward_layer_gat(Ctx& c, const EpochView& v, int l, void* Hin) {
     const int L = c.L;
     const int64_t n_in = c.plan.n_in;
-    const size_t ts = tsz(c);
-    const bool sage = c.layer == BNS_LAYER_SAGE_MEAN;
     const int64_t din = c.dp[l - 1], dout = c.dp[l];
-    const float inv_p = v.inv_p;
-    (void)L; (void)ts; (void)sage; (void)inv_p;
     // f4 / R45 backward (g = dPre): c_v = g_v . pre_v, del_v / der_u = Σ ds over the forward / transposed
     // segments, dY by the weighted SpMM^T, dW = Hin^T dY, da_l = Σ del Y, da_r = Σ der Y, dX = dY W^T
     const bool last = (l == L);
@@ -297,13 +285,10 @@ void backward_layer_gat(Ctx& c, const EpochView& v, int l, void* Hin) {
 
 // R42 backward: dY by the narrow SpMM^T, dW_top / dW_bot, dX (l > 1) into c.d_dx
 void backward_layer_tf(Ctx& c, const EpochView& v, int l, void* Hin) {
-    const int L = c.L;
     const int64_t n_in = c.plan.n_in;
     const size_t ts = tsz(c);
-    const bool sage = c.layer == BNS_LAYER_SAGE_MEAN;
     const int64_t din = c.dp[l - 1], dout = c.dp[l];
     const float inv_p = v.inv_p;
-    (void)L; (void)ts; (void)sage; (void)inv_p;
     // R42 transform-first backward: dY_u = c_u Σ_v dPre_v / deg_G(v) over every stacked row (SpMM^T at the
     // narrow width), dW_top = Hin^T dY, dW_bot = Hin_inner^T dPre, dX = [dY | dPre] [W_top | W_bot]^T
     const bool eb = c.sampler != BNS_SAMPLER_BNS;
@@ -349,13 +334,11 @@ void backward_layer_tf(Ctx& c, const EpochView& v, int l, void* Hin) {
 
 // a9 + a10: dW, [dZ' | dXself] = dPre W^T, dX = transposed aggregation (l > 1) into c.d_dx
 void backward_layer_std(Ctx& c, const EpochView& v, int l, void* Hin) {
-    const int L = c.L;
     const int64_t n_in = c.plan.n_in;
     const size_t ts = tsz(c);
     const bool sage = c.layer == BNS_LAYER_SAGE_MEAN;
     const int64_t din = c.dp[l - 1], dout = c.dp[l];
     const float inv_p = v.inv_p;
-    (void)L; (void)ts; (void)sage; (void)inv_p;
     {
         PhaseTimer t(c, BNS_PH_GEMM_BWD);
         float* g = c.d_gflat + c.goff[l - 1];

@@ -522,13 +522,15 @@ void launch_wpack_tf(Ctx& c) {
 }
 
 // a14 W <- W - lr g for every layer (g copied to the caller); skipped when the all-reduced loss is not finite
-__global__ void k_sgd_all(const WDesc d, float lr, const double* __restrict__ scal, int32_t* __restrict__ nonfinite) {
+__global__ void k_sgd_all(const WDesc d, float lr, const double* __restrict__ scal, int32_t* __restrict__ nonfinite,
+                          const volatile int* abort) {
     const int l = blockIdx.y;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t rows_l = logical_rows(d.kind, d.din[l]), dout = d.dout[l];
     if (t >= rows_l * dout) return;
     const bool bad = !isfinite(scal[0]);
     if (t == 0 && l == 0) *nonfinite = bad ? 1 : 0;
+    if (abort && *abort) return;   // a peer barrier timed out: the gradient is incomplete, leave W untouched
     const int64_t lr_ = t / dout, lc = t % dout;
     const int64_t pr = padded_row(lr_, d.kind, d.din[l], d.dpin[l]);
     const float g = d.gpad[l][pr * d.cols_p[l] + lc];
@@ -540,7 +542,8 @@ void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr) {
     const WDesc d = make_desc(c, W, G);
     int64_t mx = 0;
     for (int l = 0; l < c.L; ++l) mx = std::max(mx, logical_rows(d.kind, d.din[l]) * d.dout[l]);
-    k_sgd_all<<<dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, c.stream>>>(d, lr, c.d_scal, c.d_nonfinite);
+    k_sgd_all<<<dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, c.stream>>>(d, lr, c.d_scal, c.d_nonfinite,
+                                                                                     c.d_abort);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -686,13 +689,14 @@ struct AdamArgs {
 };
 
 __global__ void k_adam_all(const WDesc d, const AdamArgs a, const double* __restrict__ scal,
-                           int32_t* __restrict__ nonfinite) {
+                           int32_t* __restrict__ nonfinite, const volatile int* abort) {
     const int l = blockIdx.y;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t rows_l = logical_rows(d.kind, d.din[l]), dout = d.dout[l];
     if (t >= rows_l * dout) return;
     const bool bad = !isfinite(scal[0]);
     if (t == 0 && l == 0) *nonfinite = bad ? 1 : 0;
+    if (abort && *abort) return;   // a peer barrier timed out: no update, moments untouched
     const int64_t lr_ = t / dout, lc = t % dout;
     const int64_t pr = padded_row(lr_, d.kind, d.din[l], d.dpin[l]);
     const float g = d.gpad[l][pr * d.cols_p[l] + lc];
@@ -725,7 +729,8 @@ void launch_adam(Ctx& c, float* const* W, float* const* G, float lr) {
     a.eps = (float)c.eps;
     a.c1 = (float)(1.0 - std::pow(c.beta1, (double)c.adam_t));
     a.c2 = (float)(1.0 - std::pow(c.beta2, (double)c.adam_t));
-    k_adam_all<<<dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, c.stream>>>(d, a, c.d_scal, c.d_nonfinite);
+    k_adam_all<<<dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, c.stream>>>(d, a, c.d_scal, c.d_nonfinite,
+                                                                                      c.d_abort);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }

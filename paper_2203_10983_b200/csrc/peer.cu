@@ -40,6 +40,7 @@ __global__ void k_peer_barrier(uint64_t* const* __restrict__ flags, int me, int 
                                int64_t* __restrict__ delta) {
     const int j = threadIdx.x;
     if (j >= m || j == me) return;
+    if (*(volatile int*)err) return;   // an earlier barrier timed out: the epoch is already failed, do not wait again
     __threadfence_system();   // every earlier write of this stream is performed before the signal
     uint64_t* dst = flags[j] + me;
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(val) : "memory");

@@ -26,6 +26,9 @@ struct Transport {
     virtual void halo_pull(Ctx&, int /*l*/, void* /*dst_halo*/, int64_t /*din*/) {}
     virtual void* dx_buffer(Ctx& c, int /*l*/);
     virtual void grad_scatter(Ctx&, int /*l*/, int64_t /*din*/) {}
+    // bns_destroy, before the context frees anything: make sure no peer still reads this rank's shared buffers
+    // (peer transports skip the second barrier of the all-reduce, so a slower peer may be in k_sum_ptrs).
+    virtual void shutdown(Ctx&) {}
 };
 
 inline void* Transport::dx_buffer(Ctx& c, int) { return c.d_dx; }

@@ -91,6 +91,12 @@ def test_invalid_inputs():
         plan_ctx(indptr, indices, part, 2, 0, dims=(4, 3), labels=np.array([0, 3], np.int32))
     with pytest.raises(bns.BnsError):        # rank >= world
         plan_ctx(indptr, indices, part, 2, 2)
+    # asymmetric CSR (bns.h: "symmetric"): arc 3 -> 2 removed, 2 -> 3 kept -- D_{i->j} = B_j ∩ V_i would be wrong
+    ip = np.array([0, 1, 3, 5, 5], np.int64)
+    ix = np.array([1, 0, 2, 1, 3], np.int32)
+    with pytest.raises(bns.BnsError) as e:
+        plan_ctx(ip, ix, part, 2, 0)
+    assert e.value.code == bns.BNS_ERR_INVALID and "symmetric" in str(e.value)
 
 
 def test_plan_only_rejects_device_calls():

@@ -409,6 +409,33 @@ def test_nonfinite_loss_leaves_weights():
         run.close()
 
 
+def test_skipped_adam_step_is_not_counted():
+    """A non-finite loss skips the Adam update (moments untouched); the step count must not advance either, so the
+    next finite epoch applies the bias corrections of step 1 -- bitwise the same as a run without the failed epoch."""
+    import torch
+    indptr, indices, part, X, y = wl(800, 8000, 1, 8, 3, 4)
+    dims = [8, 6, 3]
+    outs = []
+    for fail_first in (False, True):
+        run = GpuRun(indptr, indices, part, 1, dims, 0, bns.BNS_FP32, X, y)
+        run.ctx[0].set_training(bns.BNS_OPT_ADAM, 0.9, 0.999, 1e-8, 0.0, 1)
+        try:
+            run.sample(1.0, SEED, 0)
+            if fail_first:
+                Wbad = [torch.tensor(w, device="cuda") for w in I.weights(dims, 0)]
+                Wbad[0][0, 0] = float("inf")
+                with pytest.raises(bns.BnsError) as e:
+                    run.ctx[0].epoch(Wbad, 0.01)
+                assert e.value.code == bns.BNS_ERR_NONFINITE
+            W = [torch.tensor(w, device="cuda") for w in I.weights(dims, 0)]
+            run.ctx[0].epoch(W, 0.01)
+            torch.cuda.synchronize()
+            outs.append([w.cpu().numpy().tobytes() for w in W])
+        finally:
+            run.close()
+    assert outs[0] == outs[1]
+
+
 def test_epoch_before_sample_is_state_error():
     indptr, indices, part, X, y = wl(300, 2000, 1, 8, 3, 4)
     run = GpuRun(indptr, indices, part, 1, [8, 3], 0, bns.BNS_FP32, X, y)

@@ -174,7 +174,11 @@ def test_barrier_timeout_is_an_error_not_a_hang():
         with pytest.raises(bns.BnsError) as ei:
             run.ctx[0].epoch(W, 0.1)
         assert ei.value.code == bns.BNS_ERR_RUNTIME and "timed out" in str(ei.value)
-        assert time.time() - t0 < 120
+        # one 20 s wait, not one per barrier: later barriers of the failed epoch return at once
+        assert time.time() - t0 < 40
+        # the update saw an incomplete gradient sum and must not have touched the caller's weights
+        for w, w0 in zip(W, Ws):
+            assert np.array_equal(w.cpu().numpy(), w0)
         with pytest.raises(bns.BnsError) as ei:
             run.ctx[0].sample_boundary(0.5, SEED, 1)
         assert ei.value.code == bns.BNS_ERR_STATE
