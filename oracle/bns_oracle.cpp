@@ -20,14 +20,14 @@
 //   reduce   g = AllReduce(g_i)             PAPER.md:291 (Alg.1 l.13); R21
 //   update   w <- w - eta g                 PAPER.md:292 (Alg.1 l.14); R9
 //
-//   bf16     R19 storage emulation (optional): stored tensors rounded to bf16, arithmetic in double -- rb()
+// Arithmetic: double throughout, in the definition's order (aggregate first, then the update).  The
+// oracle has no bf16 mode and no knowledge of the kernel's evaluation order: the GPU's bf16-storage mode (R19) and
+// its transform-first order (R42) are compared against this float64 definition directly (tests/gpu_harness.py).
 //
 // Pins (tests/test_oracle_*.py, all `-m "not gpu"`): Random123 Philox KATs; dense-adjacency float64
 // brute force with torch autograd (independent backward); central finite differences of the oracle's own
 // loss; SPEC hand examples (P4, K1,5); the survey's tiny goldens E1-E6 (tests/golden/); p=1 == unpartitioned;
-// p=0 == dense on A∘[same part]; Binomial(|B_i|, p) counts; Eq. 3 identity; for the R19 emulation:
-// rb() against torch's bfloat16 cast, bf16-exact goldens reproduce the float64 forward exactly, and gradients stay
-// within bf16 rounding of the float64 ones.
+// p=0 == dense on A∘[same part]; Binomial(|B_i|, p) counts; Eq. 3 identity.
 // Every function here is pinned; none is "parity unpinned".
 #include <cmath>
 #include <cstdint>
@@ -80,19 +80,6 @@ bool keep(uint32_t u, uint32_t i, uint64_t epoch, uint64_t seed, uint64_t T) {
 
 enum { KIND_SAGE = 0, KIND_GCN = 1, KIND_GAT = 2 };
 
-// R19 (bf16-GEMM mode): "bf16 storage of H / Z / halo / GEMM operands, fp32 accumulation,
-// fp32 master weights".  When the oracle runs in that mode it rounds every STORED tensor the definition names to
-// bf16 (round-to-nearest-even of the fp32 value) and keeps everything else in double.  rb() is that rounding.
-double rb(double x) {
-    float f = (float)x;
-    uint32_t u;
-    std::memcpy(&u, &f, 4);
-    if ((u & 0x7f800000u) == 0x7f800000u) return x;          // inf / nan unchanged
-    u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
-    std::memcpy(&f, &u, 4);
-    return (double)f;
-}
-
 struct Partition {
     // plan (static)
     std::vector<int32_t> V;                 // inner nodes, ascending gid (Alg.1 l.1)
@@ -115,7 +102,6 @@ struct Oracle {
     int L = 1;
     std::vector<int32_t> dims;              // L+1
     int kind = KIND_SAGE;
-    bool bf16 = false;                      // R19 storage emulation (see rb())
     std::vector<double> X;                  // N x dims[0]
     std::vector<int32_t> labels;            // N, -1 = not a training node
     std::vector<Partition> parts;
@@ -137,7 +123,6 @@ struct Oracle {
     uint64_t epoch_id = 0;                  // epoch of the last draw (keys the dropout masks)
     // f3: edge samplers BES / DropEdge (Table tab:bes)
     int sampler = 0;                        // 0 BNS (node), 1 BES, 2 DropEdge
-    uint32_t tf_mask = 0;                   // R42: layers (bit l-1) whose bf16 emulation follows the transform-first order
     // f4: multi-label targets (Yelp): sigmoid BCE over the train rows' C logits, F1-micro (R44)
     bool multilabel = false;
     std::vector<uint8_t> targets;           // N x C in {0, 1}
@@ -303,7 +288,7 @@ struct LocalIndex {
 //   e_vu = LeakyReLU_0.2(el_v + er_u) over u in N'(v) = {kept neighbours} ∪ {v},
 //   alpha_vu = softmax_u(e_vu),  pre_v = Σ_u alpha_vu Y_u.
 // Dropped boundary neighbours simply leave N'(v) (the softmax renormalises; no 1/p).  Weights: (din + 2) x dout
-// rows [W ; a_l ; a_r].  Y and dY are stored tensors in the bf16 emulation (R19); a_l, a_r stay fp32 / double.
+// rows [W ; a_l ; a_r].
 // ---------------------------------------------------------------------------------------------
 struct GatEdges {
     std::vector<int64_t> ptr;   // per inner row r: [ptr[r], ptr[r+1]) into col / s
@@ -311,10 +296,9 @@ struct GatEdges {
     std::vector<double> s;      // el_v + er_u
 };
 
-template <typename ST>
 void gat_setup(const Oracle& o, int i, const std::vector<int64_t>& row, const std::vector<double>& X, int din,
-               int dout, const std::vector<double>& Wq, const std::vector<double>& W, ST st, std::vector<double>& Y,
-               std::vector<double>& el, std::vector<double>& er, GatEdges& E) {
+               int dout, const std::vector<double>& W, std::vector<double>& Y, std::vector<double>& el,
+               std::vector<double>& er, GatEdges& E) {
     const Partition& P = o.parts[i];
     const size_t n_in = P.V.size(), n_h = P.U.size(), n = n_in + n_h;
     Y.assign(n * dout, 0.0);
@@ -323,8 +307,8 @@ void gat_setup(const Oracle& o, int i, const std::vector<int64_t>& row, const st
     for (size_t r = 0; r < n; ++r) {
         for (int c = 0; c < dout; ++c) {
             double y = 0.0;
-            for (int k = 0; k < din; ++k) y += X[r * din + k] * Wq[(size_t)k * dout + c];
-            Y[r * dout + c] = st(y);
+            for (int k = 0; k < din; ++k) y += X[r * din + k] * W[(size_t)k * dout + c];
+            Y[r * dout + c] = y;
         }
         for (int c = 0; c < dout; ++c) {
             el[r] += Y[r * dout + c] * W[(size_t)din * dout + c];
@@ -360,12 +344,11 @@ void gat_alpha(const GatEdges& E, size_t r, std::vector<double>& a) {
     for (int64_t e = E.ptr[r]; e < E.ptr[r + 1]; ++e) a.push_back(std::exp(leaky(E.s[e]) - mx) / den);
 }
 
-template <typename ST>
 void gat_forward(const Oracle& o, int i, const std::vector<int64_t>& row, const std::vector<double>& X, int din,
-                 int dout, const std::vector<double>& Wq, const std::vector<double>& W, ST st, std::vector<double>& pre) {
+                 int dout, const std::vector<double>& W, std::vector<double>& pre) {
     std::vector<double> Y, el, er, a;
     GatEdges E;
-    gat_setup(o, i, row, X, din, dout, Wq, W, st, Y, el, er, E);
+    gat_setup(o, i, row, X, din, dout, W, Y, el, er, E);
     const size_t n_in = o.parts[i].V.size();
     pre.assign(n_in * dout, 0.0);
     for (size_t r = 0; r < n_in; ++r) {
@@ -376,15 +359,14 @@ void gat_forward(const Oracle& o, int i, const std::vector<int64_t>& row, const 
 }
 
 // backward: c_v = g_v . pre_v; per edge dalpha = g_v . Y_u, ds = alpha (dalpha - c_v) LeakyReLU'(s);
-// dY_u += alpha g_v; del_v += ds; der_u += ds; then dY_v += del_v a_l, dY_u += der_u a_r (stored);
-// dW = X^T dY, da_l = Σ_v del_v Y_v, da_r = Σ_u der_u Y_u; dX = dY W^T (stored, then the layer's dropout)
-template <typename ST>
+// dY_u += alpha g_v; del_v += ds; der_u += ds; then dY_v += del_v a_l, dY_u += der_u a_r;
+// dW = X^T dY, da_l = Σ_v del_v Y_v, da_r = Σ_u der_u Y_u; dX = dY W^T (then the layer's dropout)
 void gat_backward(const Oracle& o, int i, const std::vector<int64_t>& row, const std::vector<double>& X, int din,
-                  int dout, const std::vector<double>& Wq, const std::vector<double>& W, ST st,
-                  const std::vector<double>& dpre, std::vector<double>& g, std::vector<double>* dX, int l) {
+                  int dout, const std::vector<double>& W, const std::vector<double>& dpre, std::vector<double>& g,
+                  std::vector<double>* dX, int l) {
     std::vector<double> Y, el, er, a;
     GatEdges E;
-    gat_setup(o, i, row, X, din, dout, Wq, W, st, Y, el, er, E);
+    gat_setup(o, i, row, X, din, dout, W, Y, el, er, E);
     const Partition& P = o.parts[i];
     const size_t n_in = P.V.size(), n = n_in + P.U.size();
     std::vector<double> dY(n * dout, 0.0), del(n, 0.0), der(n, 0.0);
@@ -411,25 +393,28 @@ void gat_backward(const Oracle& o, int i, const std::vector<int64_t>& row, const
         for (int c = 0; c < dout; ++c) {
             double x = dY[r * dout + c] + der[r] * W[(size_t)(din + 1) * dout + c];
             if (r < n_in) x += del[r] * W[(size_t)din * dout + c];
-            dY[r * dout + c] = st(x);
+            dY[r * dout + c] = x;
         }
-    for (size_t r = 0; r < n; ++r)
+    // g[k][c] accumulates over r in ascending order (loop order k-inner or c-inner gives the same sums)
+    for (size_t r = 0; r < n; ++r) {
+        for (int k = 0; k < din; ++k) {
+            const double xk = X[r * din + k];
+            for (int c = 0; c < dout; ++c) g[(size_t)k * dout + c] += xk * dY[r * dout + c];
+        }
         for (int c = 0; c < dout; ++c) {
-            const double d = dY[r * dout + c];
-            for (int k = 0; k < din; ++k) g[(size_t)k * dout + c] += X[r * din + k] * d;
             if (r < n_in) g[(size_t)din * dout + c] += del[r] * Y[r * dout + c];
             g[(size_t)(din + 1) * dout + c] += der[r] * Y[r * dout + c];
         }
+    }
     if (!dX) return;
     dX->assign(n * din, 0.0);
     for (size_t r = 0; r < n; ++r)
         for (int k = 0; k < din; ++k) {
             double x = 0.0;
-            for (int c = 0; c < dout; ++c) x += dY[r * dout + c] * Wq[(size_t)k * dout + c];
-            x = st(x);
+            for (int c = 0; c < dout; ++c) x += dY[r * dout + c] * W[(size_t)k * dout + c];
             if (o.drop > 0.0) {
                 const int32_t u = (r < n_in) ? P.V[r] : P.U[r - n_in];
-                x = st(x * drop_factor(o, u, k, l));
+                x = x * drop_factor(o, u, k, l);
             }
             (*dX)[r * din + k] = x;
         }
@@ -443,12 +428,6 @@ void gat_backward(const Oracle& o, int i, const std::vector<int64_t>& row, const
 int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* loss_out, double* acc_out) {
     if (!o.sampled) return 3;
     const int m = o.m, L = o.L;
-    auto st = [&](double x) { return o.bf16 ? rb(x) : x; };   // value as stored (R19)
-    std::vector<std::vector<double>> Wq(L);                    // GEMM operand copy of the weights (R19)
-    for (int l = 0; l < L; ++l) {
-        Wq[l] = W[l];
-        for (double& w : Wq[l]) w = st(w);
-    }
 
     o.H.assign(L + 1, std::vector<double>());
     o.Z.assign(L + 1, std::vector<double>());
@@ -497,14 +476,14 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                 for (size_t k = 0; k < buf.size(); ++k) X[(size_t)(n_in + P.U_off[j]) * din + k] = buf[k];
                 o.rows_sent_fwd[l] += (int64_t)rows;
             }
-            // R38 dropout on the layer input (inner and halo rows alike, mask keyed by global id), stored (R19)
+            // R38 dropout on the layer input (inner and halo rows alike, mask keyed by global id)
             if (o.drop > 0.0)
                 for (size_t r = 0; r < n_in + n_h; ++r) {
                     const int32_t u = (r < n_in) ? P.V[r] : P.U[r - n_in];
-                    for (int k = 0; k < din; ++k) X[r * din + k] = st(X[r * din + k] * drop_factor(o, u, k, l));
+                    for (int k = 0; k < din; ++k) X[r * din + k] = X[r * din + k] * drop_factor(o, u, k, l);
                 }
             if (o.kind == KIND_GAT) {   // f4 / R45: the attention layer on the same sampled graph
-                gat_forward(o, i, idx[i].row, X, din, dout, Wq[l - 1], W[l - 1], st, PREs[l][i]);
+                gat_forward(o, i, idx[i].row, X, din, dout, W[l - 1], PREs[l][i]);
                 Zs[l][i].assign(n_in * din, 0.0);   // GAT has no separate aggregation tensor Z
                 continue;
             }
@@ -525,7 +504,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                         if (!arc_in(o, v, u, ru, (int64_t)n_in, &c)) continue;   // dropped: contributes 0
                         for (int k = 0; k < din; ++k) z[k] += c * X[(size_t)ru * din + k];
                     }
-                    for (int k = 0; k < din; ++k) z[k] = st(z[k] / (double)dv);
+                    for (int k = 0; k < din; ++k) z[k] = z[k] / (double)dv;
                 } else {
                     // z_v = x_v / d~_v + sum_u c_u x_u / sqrt(d~_v d~_u)   (App.A P = D~^-1/2 (A+I) D~^-1/2,
                     // PAPER.md:736; S diagonal PAPER.md:771-778; R2, R16)
@@ -540,48 +519,14 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                         double a = c / std::sqrt(dtv * dtu);
                         for (int k = 0; k < din; ++k) z[k] += a * X[(size_t)ru * din + k];
                     }
-                    for (int k = 0; k < din; ++k) z[k] = st(z[k]);
                 }
             }
             // update phi: SAGE pre = W^T [z ; x]  (CONCAT(z_v, h_v); R13 no bias, R14 layout)
             //             GCN  pre = W^T z          (App.A Z = P H W)
             std::vector<double>& pre = PREs[l][i];
             pre.assign(n_in * dout, 0.0);
-            const std::vector<double>& Wl = Wq[l - 1];
-            const bool tf = o.bf16 && o.kind == KIND_SAGE && ((o.tf_mask >> (l - 1)) & 1u);
-            if (tf) {
-                // R42 (bf16 emulation only): the same layer evaluated as [Y | S] = X [W_top | W_bot] (stored), then
-                // pre_v = (1/deg_G(v)) Σ_u c_u Y_u + S_v -- equal to W^T [z ; x] by linearity, rounded where the
-                // transform-first kernel stores
-                std::vector<double> Y((n_in + n_h) * dout, 0.0);
-                for (size_t r = 0; r < n_in + n_h; ++r)
-                    for (int c = 0; c < dout; ++c) {
-                        double y = 0.0;
-                        for (int k = 0; k < din; ++k) y += X[r * din + k] * Wl[(size_t)k * dout + c];
-                        Y[r * dout + c] = st(y);
-                    }
-                for (size_t r = 0; r < n_in; ++r) {
-                    int32_t v = P.V[r];
-                    int64_t dv = deg(o, v);
-                    double* out = &pre[r * dout];
-                    if (dv > 0) {
-                        for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
-                            int32_t u = o.indices[e];
-                            int64_t ru = idx[i].row[u];
-                            double c;
-                            if (!arc_in(o, v, u, ru, (int64_t)n_in, &c)) continue;
-                            for (int k = 0; k < dout; ++k) out[k] += c * Y[(size_t)ru * dout + k];
-                        }
-                        for (int k = 0; k < dout; ++k) out[k] /= (double)dv;
-                    }
-                    for (int c = 0; c < dout; ++c) {
-                        double sv = 0.0;
-                        for (int k = 0; k < din; ++k) sv += X[r * din + k] * Wl[(size_t)(din + k) * dout + c];
-                        out[c] += st(sv);
-                    }
-                }
-            }
-            for (size_t r = 0; r < n_in && !tf; ++r) {
+            const std::vector<double>& Wl = W[l - 1];
+            for (size_t r = 0; r < n_in; ++r) {
                 double* out = &pre[r * dout];
                 for (int k = 0; k < din; ++k) {
                     double zk = Zl[r * din + k];
@@ -603,7 +548,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                 size_t g = (size_t)P.V[r];
                 for (int c = 0; c < dout; ++c) {
                     double x = PREs[l][i][r * dout + c];
-                    o.H[l][g * dout + c] = (l < L) ? st(x > 0.0 ? x : 0.0) : x;   // logits stay fp32 (R19)
+                    o.H[l][g * dout + c] = (l < L) ? (x > 0.0 ? x : 0.0) : x;
                 }
                 for (int k = 0; k < din; ++k) o.Z[l][g * din + k] = Zs[l][i][r * din + k];
             }
@@ -673,7 +618,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
     std::vector<std::vector<std::vector<double>>> gW(m, std::vector<std::vector<double>>(L));
     for (int l = L; l >= 1; --l) {
         const int din = o.dims[l - 1], dout = o.dims[l];
-        const std::vector<double>& Wl = Wq[l - 1];
+        const std::vector<double>& Wl = W[l - 1];
         std::vector<std::vector<double>> dXs(m);     // gradient w.r.t. stacked input rows (inner + halo)
         for (int i = 0; i < m; ++i) {
             const Partition& P = o.parts[i];
@@ -683,7 +628,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
             for (size_t r = 0; r < n_in; ++r)
                 for (int c = 0; c < dout; ++c) {
                     double g = o.dH[l][(size_t)P.V[r] * dout + c];
-                    dpre[r * dout + c] = (l < L) ? (PREs[l][i][r * dout + c] > 0.0 ? g : 0.0) : st(g);
+                    dpre[r * dout + c] = (l < L) ? (PREs[l][i][r * dout + c] > 0.0 ? g : 0.0) : g;
                 }
             // weight gradient of this partition
             const int wrows = (o.kind == KIND_SAGE) ? 2 * din : (o.kind == KIND_GAT) ? din + 2 : din;
@@ -691,65 +636,25 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
             g.assign((size_t)wrows * dout, 0.0);
             if (o.kind == KIND_GAT) {
                 std::vector<double>& dX = dXs[i];
-                gat_backward(o, i, idx[i].row, Xs[l][i], din, dout, Wq[l - 1], W[l - 1], st, dpre, g,
-                             l > 1 ? &dX : nullptr, l);
+                gat_backward(o, i, idx[i].row, Xs[l][i], din, dout, W[l - 1], dpre, g, l > 1 ? &dX : nullptr, l);
                 continue;
             }
-            const bool tf = o.bf16 && o.kind == KIND_SAGE && ((o.tf_mask >> (l - 1)) & 1u);
-            if (tf) {
-                // R42 emulation: dY_u = c_u Σ_{v: u in N(v)} [dPre_v / deg_G(v)] on every stacked row, the bracket
-                // and dY stored;
-                // dW_top = X^T dY, dW_bot = X_inner^T dPre; dX = dY W_top^T + [inner] dPre W_bot^T (stored)
-                std::vector<double> dY((n_in + n_h) * dout, 0.0);
-                for (size_t r = 0; r < n_in; ++r) {
-                    int32_t v = P.V[r];
-                    int64_t dv = deg(o, v);
-                    if (dv == 0) continue;
-                    for (int64_t e = o.indptr[v]; e < o.indptr[v + 1]; ++e) {
-                        int32_t u = o.indices[e];
-                        int64_t ru = idx[i].row[u];
-                        double c;
-                        if (!arc_in(o, v, u, ru, (int64_t)n_in, &c)) continue;
-                        for (int k = 0; k < dout; ++k) dY[(size_t)ru * dout + k] += c * st(dpre[r * dout + k] / (double)dv);
-                    }
+            // dW = [Z | X]^T dPre: g[k][c] accumulates over r in ascending order (the loop nest order only changes
+            // which element is visited next, not the order of any element's sum)
+            for (size_t r = 0; r < n_in; ++r) {
+                const double* d = &dpre[r * dout];
+                for (int k = 0; k < din; ++k) {
+                    const double zk = Zs[l][i][r * din + k];
+                    double* gk = &g[(size_t)k * dout];
+                    for (int c = 0; c < dout; ++c) gk[c] += zk * d[c];
                 }
-                for (double& x : dY) x = st(x);
-                for (size_t r = 0; r < n_in + n_h; ++r)
-                    for (int c = 0; c < dout; ++c) {
-                        const double d = dY[r * dout + c];
-                        for (int k = 0; k < din; ++k) g[(size_t)k * dout + c] += Xs[l][i][r * din + k] * d;
-                    }
-                for (size_t r = 0; r < n_in; ++r)
-                    for (int c = 0; c < dout; ++c) {
-                        const double d = dpre[r * dout + c];
-                        for (int k = 0; k < din; ++k) g[(size_t)(din + k) * dout + c] += Xs[l][i][r * din + k] * d;
-                    }
-                if (l == 1) continue;
-                std::vector<double>& dX = dXs[i];
-                dX.assign((n_in + n_h) * din, 0.0);
-                for (size_t r = 0; r < n_in + n_h; ++r)
+                if (o.kind == KIND_SAGE)
                     for (int k = 0; k < din; ++k) {
-                        double x = 0.0;
-                        for (int c = 0; c < dout; ++c) {
-                            x += dY[r * dout + c] * Wl[(size_t)k * dout + c];
-                            if (r < n_in) x += dpre[r * dout + c] * Wl[(size_t)(din + k) * dout + c];
-                        }
-                        x = st(x);
-                        if (o.drop > 0.0) {
-                            const int32_t u = (r < n_in) ? P.V[r] : P.U[r - n_in];
-                            x = st(x * drop_factor(o, u, k, l));
-                        }
-                        dX[r * din + k] = x;
+                        const double xk = Xs[l][i][r * din + k];
+                        double* gk = &g[(size_t)(din + k) * dout];
+                        for (int c = 0; c < dout; ++c) gk[c] += xk * d[c];
                     }
-                continue;
             }
-            for (size_t r = 0; r < n_in; ++r)
-                for (int c = 0; c < dout; ++c) {
-                    double d = dpre[r * dout + c];
-                    for (int k = 0; k < din; ++k) g[(size_t)k * dout + c] += Zs[l][i][r * din + k] * d;
-                    if (o.kind == KIND_SAGE)
-                        for (int k = 0; k < din; ++k) g[(size_t)(din + k) * dout + c] += Xs[l][i][r * din + k] * d;
-                }
             if (l == 1) continue;                   // R29: input features are not trainable
             // dZ' = (dPre W_top^T) s_v with s_v = 1/deg_G(v) (SAGE, 0 if deg 0) or 1/sqrt(d~_v) (GCN) -- the
             // row factor of the aggregation coefficient; dXself = dPre W_bot^T (SAGE self half of CONCAT)
@@ -763,8 +668,8 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                         a += dpre[r * dout + c] * Wl[(size_t)k * dout + c];
                         if (o.kind == KIND_SAGE) b += dpre[r * dout + c] * Wl[(size_t)(din + k) * dout + c];
                     }
-                    dZp[r * din + k] = st(a * sv);
-                    dXself[r * din + k] = st(b);
+                    dZp[r * din + k] = a * sv;
+                    dXself[r * din + k] = b;
                 }
             }
             // transpose of the aggregation over the kept edges of every inner v:
@@ -791,10 +696,9 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                 for (int k = 0; k < din; ++k) {
                     double x = dX[r * din + k];
                     if (o.kind == KIND_SAGE && r < n_in) x += dXself[r * din + k];
-                    x = st(x);
                     if (o.drop > 0.0) {   // R38: through the dropout of this layer's input
                         const int32_t u = (r < n_in) ? P.V[r] : P.U[r - n_in];
-                        x = st(x * drop_factor(o, u, k, l));
+                        x = x * drop_factor(o, u, k, l);
                     }
                     dX[r * din + k] = x;
                 }
@@ -817,7 +721,7 @@ int epoch(Oracle& o, std::vector<std::vector<double>>& W, double lr, double* los
                     int32_t u = P.U[s];
                     for (int k = 0; k < din; ++k) {
                         double& t = o.dH[l - 1][(size_t)u * din + k];
-                        t = st(t + dXs[i][(n_in + (size_t)s) * din + k]);
+                        t = t + dXs[i][(n_in + (size_t)s) * din + k];
                     }
                 }
             }
@@ -962,10 +866,6 @@ int32_t orc_sample_edges(void* h, int32_t sampler, double q, uint64_t seed, uint
 // R40 arc draw (v <- u) under the last orc_sample_edges' q / seed / epoch
 int32_t orc_arc_keep(void* h, int32_t v, int32_t u) { return arc_keep(*(Oracle*)h, v, u) ? 1 : 0; }
 
-// R42: layers (bit l-1) whose bf16-storage emulation follows the transform-first evaluation order (no effect in
-// double mode, where both orders are the same arithmetic)
-void orc_set_transform_first(void* h, uint32_t mask) { ((Oracle*)h)->tf_mask = mask; }
-
 // f4 / R44: multi-label targets, N x C (global ids) in {0, 1}; switches the loss to sigmoid BCE and acc to F1-micro
 void orc_set_multilabel(void* h, const uint8_t* targets) {
     Oracle& o = *(Oracle*)h;
@@ -1017,9 +917,6 @@ int64_t orc_tensor(void* h, int32_t what, int32_t layer, double* out, int64_t ca
     if (out) std::copy(t.begin(), t.begin() + std::min(n, cap), out);
     return n;
 }
-
-void orc_set_bf16(void* h, int32_t on) { ((Oracle*)h)->bf16 = on != 0; }
-double orc_round_bf16(double x) { return rb(x); }
 
 int64_t orc_rows_sent(void* h, int32_t layer) {
     Oracle& o = *(Oracle*)h;

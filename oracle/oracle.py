@@ -46,9 +46,6 @@ def lib():
         L.orc_epoch.argtypes = [vp, vp, f64, vp, vp, vp]
         L.orc_tensor.restype = i64
         L.orc_tensor.argtypes = [vp, i32, i32, vp, i64]
-        L.orc_set_bf16.argtypes = [vp, i32]
-        L.orc_round_bf16.restype = f64
-        L.orc_round_bf16.argtypes = [f64]
         L.orc_set_training.restype = i32
         L.orc_set_training.argtypes = [vp, i32, f64, f64, f64, f64, u64]
         L.orc_drop_factor.restype = f64
@@ -57,7 +54,6 @@ def lib():
         L.orc_sample_edges.argtypes = [vp, i32, f64, u64, u64]
         L.orc_arc_keep.restype = i32
         L.orc_arc_keep.argtypes = [vp, i32, i32]
-        L.orc_set_transform_first.argtypes = [vp, u32]
         L.orc_set_multilabel.argtypes = [vp, vp]
         L.orc_rows_sent.restype = i64
         L.orc_rows_sent.argtypes = [vp, i32]
@@ -79,10 +75,6 @@ def philox4x32_10(ctr, key):
 
 def draw(u, i, epoch, seed):
     return int(lib().orc_draw(u, i, epoch, seed))
-
-
-def round_bf16(x):
-    return float(lib().orc_round_bf16(float(x)))
 
 
 def threshold(p):
@@ -108,14 +100,6 @@ class Oracle:
         if getattr(self, "h", None):
             lib().orc_destroy(self.h)
             self.h = None
-
-    def set_bf16(self, on=True):
-        """R19 bf16-storage emulation: round the stored tensors (Z, H, GEMM operands, dPre, dZ', dX) to bf16."""
-        lib().orc_set_bf16(self.h, 1 if on else 0)
-
-    def set_transform_first(self, mask):
-        """R42: bf16 emulation of the transform-first order on layers in mask (bit l-1); no effect in double."""
-        lib().orc_set_transform_first(self.h, int(mask))
 
     def set_multilabel(self, targets):
         """f4 / R44: N x C multi-hot targets (global ids); loss -> sigmoid BCE, acc -> F1-micro.  None: back to CE."""

@@ -32,7 +32,8 @@ PHASES = ["sample", "induce", "pack", "exchange", "spmm_fwd", "gemm_fwd", "loss"
           "exchange_bwd", "scatter", "allreduce", "update", "epoch_total", "sample_total"]
 
 EXPORTS = ["bns_get_unique_id", "bns_group_create", "bns_group_destroy", "bns_setup", "bns_sample_boundary",
-           "bns_sample_edges", "bns_set_multilabel", "bns_epoch", "bns_step", "bns_set_timing", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy"]
+           "bns_sample_edges", "bns_set_multilabel", "bns_epoch", "bns_step", "bns_set_timing", "bns_set_training", "bns_query", "bns_stream", "bns_last_error", "bns_destroy",
+           "bns_gemm"]
 BNS_OPT_SGD, BNS_OPT_ADAM = 0, 1
 
 
@@ -96,6 +97,8 @@ def lib():
         L.bns_step.argtypes = [vp, f64, u64, u64, vp, f32, vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]
         L.bns_set_timing.argtypes = [vp, i32]
         L.bns_query.argtypes = [vp, i32, i32, vp, i64, ctypes.POINTER(i64)]
+        L.bns_gemm.argtypes = [i32, i32, i64, i64, i64, vp, vp, i64, vp, i64, vp, i64, vp, i64, i32, vp,
+                               ctypes.POINTER(i32)]
         L.bns_stream.restype = vp
         L.bns_stream.argtypes = [vp]
         L.bns_last_error.restype = ctypes.c_char_p
@@ -103,7 +106,7 @@ def lib():
         L.bns_destroy.argtypes = [vp]
         for f in ("bns_get_unique_id", "bns_group_create", "bns_setup", "bns_sample_boundary", "bns_sample_edges",
                   "bns_set_multilabel", "bns_epoch", "bns_step", "bns_set_timing",
-                  "bns_set_training", "bns_query"):
+                  "bns_set_training", "bns_query", "bns_gemm"):
             getattr(L, f).restype = ctypes.c_int
         L.bns_group_destroy.restype = None
         L.bns_destroy.restype = None
@@ -124,6 +127,19 @@ def _ptr(a) -> int:
             raise ValueError("tensor must be contiguous")
         return a.data_ptr()
     return a.ctypes.data
+
+
+BNS_GEMM_FWD, BNS_GEMM_WGRAD, BNS_GEMM_WGRAD2, BNS_GEMM_DX = range(4)
+
+
+def bns_gemm(precision, kind, M, N, K, A0, A1, lda, B, ldb, C, ldc, rowscale=None, scale_cols=0, flags=0,
+             stream=None) -> int:
+    """One GEMM of the epoch by the epoch's own kernels (bns.h bns_gemm); torch CUDA tensors in, split-K factor out."""
+    sp = ctypes.c_int32(0)
+    _check(lib().bns_gemm(precision, kind, M, N, K, _ptr(A0), _ptr(A1) if A1 is not None else None, lda, _ptr(B),
+                          ldb, _ptr(C), ldc, _ptr(rowscale) if rowscale is not None else None, scale_cols, flags,
+                          stream, ctypes.byref(sp)))
+    return sp.value
 
 
 def bns_get_unique_id() -> bytes:

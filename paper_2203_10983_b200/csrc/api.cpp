@@ -1075,6 +1075,44 @@ bns_status bns_set_timing(bns_ctx* h, int32_t on) {
     });
 }
 
+bns_status bns_gemm(int32_t precision, int32_t kind, int64_t M, int64_t N, int64_t K, const void* A0, const void* A1,
+                    int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, const float* rowscale,
+                    int64_t scale_cols, int32_t flags, void* stream, int32_t* splits) {
+    using namespace bns;
+    return guard(nullptr, [&] {
+        if (precision != BNS_BF16) throw Error(BNS_ERR_INVALID, "bns_gemm: only BNS_BF16 (tcgen05) is exposed");
+        if (M < 0 || N <= 0 || K <= 0 || !A0 || !B || !C || kind < 0 || kind > 3)
+            throw Error(BNS_ERR_INVALID, "bns_gemm: bad kind / shape / NULL operand");
+        if (kind == 2 && (K % 128 != 0 || !A1)) throw Error(BNS_ERR_INVALID, "bns_gemm: WGRAD2 needs A1 and K % 128 == 0");
+        Ctx c;
+        c.prec = BNS_BF16;
+        c.use_tc = true;
+        c.stream = static_cast<cudaStream_t>(stream);
+        c.splitk_cap = 0;
+        std::vector<void*> mine;
+        if (kind == 1 || kind == 2) {   // room for one fp32 K x N (x2) slice per split, up to 148 splits
+            c.splitk_cap = 148 * (kind == 2 ? 2 : 1) * K * N;
+            c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
+        }
+        const int64_t Kw = (K + 63) / 64 * 64;
+        try {
+            switch (kind) {
+                case 0: gemm_fwd_tc(c, M, N, A0, K, lda, A1, A1 ? K : 0, lda, B, ldb ? ldb : (A1 ? 2 * Kw : Kw), C,
+                                    ldc, flags & 1, (flags >> 1) & 1); break;
+                case 1: gemm_wgrad_tc(c, M, K, N, A0, lda, B, ldb, static_cast<float*>(C), ldc); break;
+                case 2: gemm_wgrad2_tc(c, M, K, N, A0, A1, lda, B, ldb, static_cast<float*>(C), ldc); break;
+                default: gemm_dx_tc(c, M, N, K, A0, lda, B, ldb, C, ldc, rowscale, scale_cols); break;
+            }
+            BNS_CUDA(cudaStreamSynchronize(c.stream));
+        } catch (...) {
+            for (void* p : c.allocs) cudaFree(p);
+            throw;
+        }
+        for (void* p : c.allocs) cudaFree(p);
+        if (splits) *splits = (kind == 1 || kind == 2) ? c.last_splitk : 1;
+    });
+}
+
 void* bns_stream(const bns_ctx* h) { return h ? (void*)h->c.stream : nullptr; }
 
 const char* bns_last_error(const bns_ctx* h) { return h ? h->c.err.c_str() : g_err.c_str(); }

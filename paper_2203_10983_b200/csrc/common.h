@@ -224,7 +224,8 @@ struct Ctx {
     double* d_scal = nullptr;      // [loss_sum, correct] (all-reduced)
     double* d_lpart = nullptr;     // per-block loss partials
     int32_t* d_nonfinite = nullptr;
-    const int* d_abort = nullptr;  // peer transports: mapped barrier-timeout flag (update kernels skip when set)
+    const int* d_abort = nullptr;
+    int last_splitk = 1;           // split-K factor of the last tcgen05 weight-gradient GEMM (bns_gemm reports it)  // peer transports: mapped barrier-timeout flag (update kernels skip when set)
     // --- f3: edge samplers (BES / DropEdge); allocated by the first bns_sample_edges
     int sampler = 0;               // BNS_SAMPLER_* of the last draw
     float nscale = 1.f;            // neighbour-sum scale (DropEdge: 1/q on every arc; else 1)

@@ -370,6 +370,7 @@ void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int6
     while (S > 1 && S * K * N > c.splitk_cap) --S;
     a.kb_per_split = (int)cdiv(a.nk, S);
     S = cdiv(a.nk, a.kb_per_split);
+    c.last_splitk = (int)S;
     a.epi = EPI_F32;
     a.out = c.d_splitk;
     a.ldc = N;
@@ -404,6 +405,7 @@ void gemm_wgrad2_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, co
     while (S > 1 && S * K2 * N > c.splitk_cap) --S;
     a.kb_per_split = (int)cdiv(a.nk, S);
     S = cdiv(a.nk, a.kb_per_split);
+    c.last_splitk = (int)S;
     a.epi = EPI_F32;
     a.out = c.d_splitk;
     a.ldc = N;

@@ -40,6 +40,139 @@ def relerr(a, b):
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
 
 
+# ---------------- epoch parity against the float64 oracle (fp32: 1e-5 everywhere; bf16: see below) ----------------
+# bf16 (R19 storage) is compared with the plain float64 definition -- the oracle has no bf16 mode and no knowledge of
+# the kernel's evaluation order (transform-first, R42).  A ReLU mask bit is an integer decided by floating point: a
+# hidden unit whose pre-activation lies within bf16 rounding of zero takes either branch (R36).  Such a flip leaves the
+# forward and every gradient ABOVE its layer unchanged but switches the gradient path below it, by several percent
+# normwise at the test widths (16-24 hidden units; measured with any two bf16 evaluation orders, R36).  So
+# in bf16: loss, H^l, Z^l, dLogits and the gradients above the highest flipped layer F are held to 2e-2; every flip
+# must be ambiguous (|value| <= 2^-6 of the layer maximum on both sides) and flips may touch at most FLIP_SHARE_MAX of
+# a layer's units; the gradients at and below F are reported (BF16_REPORT -> gpurun_out/bf16_margins.json) and held
+# to 2e-2 by the layer-local check instead: each layer's outputs and gradients recomputed in float64 from that
+# layer's own GPU inputs (the H^(l-1) it read, the dH^l it received and its own ReLU mask) and the oracle's sampled
+# graph -- no flip can enter there.
+FLIP_SHARE_MAX = 5e-3
+BF16_REPORT = []
+
+
+def relu_flips(run, orc, L, prec, tag):
+    """Returns (F, flips per hidden layer): F = highest hidden layer with a ReLU flip (0 if none)."""
+    F, out = 0, []
+    for l in range(1, L):
+        g = run.gather(bns.BNS_Q_H, l, run.dims[l])
+        o = orc.tensor(O.T_H, l)
+        flip = (g > 0) != (o > 0)
+        n = int(flip.sum())
+        out.append(n)
+        if n == 0:
+            continue
+        assert prec == bns.BNS_BF16, (tag, "ReLU flips in fp32", l, n)
+        scale = max(np.abs(o).max(), 1e-30)
+        assert n <= FLIP_SHARE_MAX * o.size, (tag, "too many ReLU flips", l, n, o.size)
+        assert np.abs(g[flip]).max() <= scale / 64 and np.abs(o[flip]).max() <= scale / 64, (tag, "flip not ambiguous", l)
+        F = l
+    return F, out
+
+
+def sampled_operator(orc, run, sampler, q):
+    """The epoch's sampled aggregation as one global N x N float64 matrix, from the ORACLE's induced lists (Alg.1 l.5):
+    row v (inner to rank r) holds c_u / deg_G(v) (SAGE, R1-R3) or c_u / sqrt(d~_v d~_u) + [u = v] / d~_v (GCN, App. A);
+    c_u = 1 on inner columns and 1/q on sampled boundary columns (BNS q = p, BES q; R3, R41); DropEdge: 1/q on every
+    arc (R41)."""
+    import scipy.sparse as sp
+    N = run.N
+    deg = np.diff(orc.indptr).astype(np.float64)
+    rows, cols, vals = [], [], []
+    for r in range(run.m):
+        V = orc.list(O.V_LIST, r)
+        ptr = orc.list(O.INDUCED_PTR, r)
+        col = orc.list(O.INDUCED_COL, r)
+        v = np.repeat(V, np.diff(ptr))
+        inner = orc.part_of[col] == r
+        inv = 1.0 / q if q > 0 else 0.0
+        c = np.full(len(col), inv) if sampler == bns.BNS_SAMPLER_DROPEDGE else np.where(inner, 1.0, inv)
+        if run.layer == bns.BNS_LAYER_SAGE_MEAN:
+            w = c / deg[v]
+        else:
+            w = c / np.sqrt((deg[v] + 1.0) * (deg[col] + 1.0))
+        rows.append(v)
+        cols.append(col)
+        vals.append(w)
+    if run.layer == bns.BNS_LAYER_GCN:
+        rows.append(np.arange(N))
+        cols.append(np.arange(N))
+        vals.append(1.0 / (deg + 1.0))
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(N, N))
+
+
+def bf16_round(a):
+    import torch
+    return torch.tensor(np.asarray(a, np.float32)).bfloat16().double().numpy()
+
+
+def layer_local_check(run, orc, Ws, G, L, sampler, q, tag, tol):
+    """bf16: every layer against float64 recomputed from its own GPU inputs (see above); returns the margins."""
+    A = sampled_operator(orc, run, sampler, q)
+    sage = run.layer == bns.BNS_LAYER_SAGE_MEAN
+    dims = run.dims
+    out = {}
+    for l in range(1, L + 1):
+        din = dims[l - 1]
+        Wb = bf16_round(Ws[l - 1])             # the GEMM operand of the bf16 mode (R19)
+        X = run.gather(bns.BNS_Q_H, l - 1, din)
+        AX = A @ X
+        pre = AX @ Wb[:din] + X @ Wb[din:] if sage else AX @ Wb
+        Hg = run.gather(bns.BNS_Q_H, l, dims[l])
+        out[f"H{l}"] = e = relerr(Hg, np.maximum(pre, 0) if l < L else pre)
+        assert e <= tol, (tag, "layer-local H", l, e)
+        dH = run.gather(bns.BNS_Q_DH, l, dims[l])
+        dpre = dH * (Hg > 0) if l < L else dH
+        dW = np.concatenate([AX.T @ dpre, X.T @ dpre]) if sage else AX.T @ dpre
+        out[f"dW{l}"] = e = relerr(G[l - 1], dW)
+        assert e <= tol, (tag, "layer-local dW", l, e)
+        if l > 1:
+            dX = A.T @ (dpre @ Wb[:din].T) + (dpre @ Wb[din:].T if sage else 0)
+            out[f"dH{l - 1}"] = e = relerr(run.gather(bns.BNS_Q_DH, l - 1, din), dX)
+            assert e <= tol, (tag, "layer-local dH", l - 1, e)
+    return out
+
+
+def compare_epoch(run, orc, L, Ws, Wd, lr, prec, tag="", host=False, local=True):
+    """One epoch on both sides (two independent weight trajectories: Ws fp32 on the GPU, Wd float64 in the oracle,
+    both updated in place / returned) and the parity checks described above.  Returns the GPU's new weights."""
+    tol = TOL[prec]
+    loss, acc, G, Wn = run.epoch(Ws, lr, host=host)
+    lo, ao, Go = orc.epoch(Wd, lr)
+    assert abs(loss - lo) <= LOSS_TOL * max(abs(lo), 1e-12), (tag, loss, lo)
+    ntr = max(1, int((orc.labels >= 0).sum()))
+    assert abs(acc - ao) <= (0.0 if prec == bns.BNS_FP32 else 0.02) + 2.0 / ntr, (tag, acc, ao)
+    dims = run.dims
+    F, flips = relu_flips(run, orc, L, prec, tag)
+    margins = {"loss": abs(loss - lo) / max(abs(lo), 1e-12)}
+    for l in range(1, L + 1):
+        if not (run.tf >> (l - 1)) & 1 and run.layer != bns.BNS_LAYER_GAT:   # no Z on R42 / GAT layers
+            margins[f"Z{l}"] = e = relerr(run.gather(bns.BNS_Q_Z, l, dims[l - 1]), orc.tensor(O.T_Z, l))
+            assert e <= tol, (tag, "Z", l, e)
+        margins[f"H{l}"] = e = relerr(run.gather(bns.BNS_Q_H, l, dims[l]), orc.tensor(O.T_H, l))
+        assert e <= tol, (tag, "H", l, e)
+        margins[f"dH{l}"] = e = relerr(run.gather(bns.BNS_Q_DH, l, dims[l]), orc.tensor(O.T_DH, l))
+        assert l < F or e <= tol, (tag, "dH", l, e)
+    for l in range(L):
+        margins[f"dW{l + 1}"] = e = relerr(G[l], Go[l])
+        if l + 1 > F:
+            assert e <= tol, (tag, "dW", l, e)
+            e = relerr(Wn[l], Wd[l])
+            assert e <= max(tol * 0.1, 1e-6), (tag, "W", l, e)
+    if prec == bns.BNS_BF16:
+        rec = {"tag": tag, "layer": run.layer, "m": run.m, "F": F, "flips": flips,
+               "units": [int(run.N * dims[l]) for l in range(1, L)], "vs_float64": margins}
+        if local and run.layer != bns.BNS_LAYER_GAT and run.last_draw is not None:
+            rec["layer_local"] = layer_local_check(run, orc, Ws, G, L, *run.last_draw, tag, tol)
+        BF16_REPORT.append(rec)
+    return [w.astype(np.float32) for w in Wn]
+
+
 class GpuRun:
     def __init__(self, indptr, indices, part, m, dims, layer, prec, X, y, flags=bns.BNS_RETAIN_GRADS, max_p=0.0):
         import torch
@@ -55,6 +188,7 @@ class GpuRun:
                                indices=indices, part_of=self.part, features=np.ascontiguousarray(X[inner]),
                                labels=np.ascontiguousarray(y[inner]), group=self.group, flags=flags, max_p=max_p)
 
+        self.last_draw = None    # (sampler, p or q) of the last draw, for the layer-local check
         self.ctx = parallel(m, mk)
         self.inner = [self.ctx[r].i32(bns.BNS_Q_INNER) for r in range(m)]
         self.tf = 0 if flags & bns.BNS_NO_TRANSFORM_FIRST else tf_rule(self.dims, layer)
@@ -69,6 +203,11 @@ class GpuRun:
 
     def sample(self, p, seed, epoch):
         parallel(self.m, lambda r: self.ctx[r].sample_boundary(p, seed, epoch))
+        self.last_draw = (bns.BNS_SAMPLER_BNS, p)
+
+    def sample_edges(self, sampler, q, seed, epoch):
+        parallel(self.m, lambda r: self.ctx[r].sample_edges(sampler, q, seed, epoch))
+        self.last_draw = (sampler, q)
 
     def epoch(self, Ws, lr, host=False):
         """Ws: list of float32 numpy weights (shared initial value).  Returns (loss, acc, grads, W_new) and checks

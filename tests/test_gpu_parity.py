@@ -16,7 +16,7 @@ from oracle import oracle as O
 from paper_2203_10983_b200 import bns
 from paper_2203_10983_b200 import inputs as I
 
-from gpu_harness import GpuRun, LOSS_TOL, TOL, parallel, relerr
+from gpu_harness import GpuRun, LOSS_TOL, TOL, compare_epoch, parallel, relerr, relu_flips
 
 pytestmark = pytest.mark.gpu
 SEED = I.BNS_SEED
@@ -65,62 +65,6 @@ def test_sampling_lists_bitexact(N, nnz, m, method):
         run.close()
 
 
-def compare_epoch(run, orc, L, Ws, Wd, lr, prec, host=False, tag=""):
-    tol = TOL[prec]
-    if prec == bns.BNS_BF16:
-        # bf16: every epoch starts both sides from the kernel's fp32 weights -- the fp32 / float64 trajectories
-        # differ by ~1e-4 after one lr = 0.5 step, which only multiplies ReLU flips (R36); fp32 keeps two trajectories
-        for a, b in zip(Wd, Ws):
-            a[...] = np.asarray(b, np.float64)
-    loss, acc, G, Wn = run.epoch(Ws, lr, host=host)
-    orc.set_transform_first(run.tf)          # R42: the bf16 emulation stores where the kernel stores
-    lo, ao, Go = orc.epoch(Wd, lr)
-    assert abs(loss - lo) <= LOSS_TOL * max(abs(lo), 1e-12), (tag, loss, lo)
-    ntr = max(1, int((orc.labels >= 0).sum()))
-    assert abs(acc - ao) <= (0.0 if prec == bns.BNS_FP32 else 0.02) + 2.0 / ntr, (tag, acc, ao)
-    dims = run.dims
-    F = relu_flip_floor(run, orc, L, prec, tag)
-    for l in range(1, L + 1):
-        if not (run.tf >> (l - 1)) & 1 and run.layer != bns.BNS_LAYER_GAT:   # no Z on R42 / GAT layers
-            e = relerr(run.gather(bns.BNS_Q_Z, l, dims[l - 1]), orc.tensor(O.T_Z, l))
-            assert e <= tol, (tag, "Z", l, e)
-        e = relerr(run.gather(bns.BNS_Q_H, l, dims[l]), orc.tensor(O.T_H, l))
-        assert e <= tol, (tag, "H", l, e)
-        if l >= F:
-            e = relerr(run.gather(bns.BNS_Q_DH, l, dims[l]), orc.tensor(O.T_DH, l))
-            assert e <= tol, (tag, "dH", l, e)
-    for l in range(L):
-        if l + 1 <= F:
-            continue
-        e = relerr(G[l], Go[l])
-        assert e <= tol, (tag, "dW", l, e)
-        e = relerr(Wn[l], Wd[l])
-        assert e <= max(tol * 0.1, 1e-6), (tag, "W", l, e)
-    return [w.astype(np.float32) for w in Wn]
-
-
-def relu_flip_floor(run, orc, L, prec, tag):
-    """R36: in bf16 a hidden unit whose pre-activation is within rounding of zero may take either ReLU branch.
-    Such a flip leaves the forward (the unit is ~0 either way) and every gradient above its layer unchanged, but
-    switches the gradient path below it.  Returns F = the highest hidden layer with flips (0 if none) after checking
-    that every flip is ambiguous (both values within 2^-6 of the layer's largest activation) and rare (<= 2e-4 of
-    the units, at least 4 allowed); the caller then checks dH^l for l >= F and dW^l for l > F.  fp32: no flips."""
-    F = 0
-    for l in range(1, L):
-        g = run.gather(bns.BNS_Q_H, l, run.dims[l])
-        o = orc.tensor(O.T_H, l)
-        flip = (g > 0) != (o > 0)
-        n = int(flip.sum())
-        if n == 0:
-            continue
-        assert prec == bns.BNS_BF16, (tag, "ReLU flips in fp32", l, n)
-        scale = max(np.abs(o).max(), 1e-30)
-        assert n <= max(4, 2e-4 * o.size), (tag, "too many ReLU flips", l, n)
-        assert np.abs(g[flip]).max() <= scale / 64 and np.abs(o[flip]).max() <= scale / 64, (tag, "flip not ambiguous", l)
-        F = l
-    return F
-
-
 CASES = [  # (m, p, method)
     (1, 1.0, "random"), (2, 0.5, "random"), (4, 0.1, "ldg2"), (3, 0.0, "random"), (3, 1.0, "ldg2"), (5, 0.3, "random"),
 ]
@@ -141,7 +85,6 @@ def test_epoch_parity(prec, layer, tf, m, p, method):
     flags = bns.BNS_RETAIN_GRADS | (0 if tf else bns.BNS_NO_TRANSFORM_FIRST)
     run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y, flags=flags)
     orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
-    orc.set_bf16(prec == bns.BNS_BF16)       # R19: the oracle stores what the bf16 mode stores, in bf16
     try:
         for e in range(2):
             run.sample(p, SEED, e)
@@ -164,7 +107,6 @@ def test_six_vector_rows_parity(dims, prec, m, p):
     Wd = [w.astype(np.float64) for w in Ws]
     run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y)
     orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
-    orc.set_bf16(prec == bns.BNS_BF16)
     try:
         for e in range(2):
             run.sample(p, SEED, e)
@@ -189,7 +131,6 @@ def test_long_row_segments_parity(prec, m, p, monkeypatch):
     Wd = [w.astype(np.float64) for w in Ws]
     run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y)
     orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
-    orc.set_bf16(prec == bns.BNS_BF16)
     try:
         for e in range(2):
             run.sample(p, SEED, e)
@@ -212,7 +153,6 @@ def test_merged_wgrad_parity(tf, m, p):
     flags = bns.BNS_RETAIN_GRADS | (0 if tf else bns.BNS_NO_TRANSFORM_FIRST)
     run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y, flags=flags)
     orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
-    orc.set_bf16(True)
     try:
         for e in range(2):
             run.sample(p, SEED, e)
@@ -234,7 +174,6 @@ def test_cora_config0():
     for prec in (bns.BNS_FP32, bns.BNS_BF16):
         run = GpuRun(indptr, indices, part, 2, sh.dims, sh.layer, prec, X, y)
         orc = O.Oracle(indptr, indices, part, 2, sh.dims, sh.layer, X, y)
-        orc.set_bf16(prec == bns.BNS_BF16)
         Wp, Wdp = [w.copy() for w in Ws], [w.copy() for w in Wd]
         try:
             for e in range(3):
@@ -484,7 +423,6 @@ def test_adam_dropout_parity(prec, layer, m, p, drop):
     for c in run.ctx:
         c.set_training(bns.BNS_OPT_ADAM, 0.9, 0.999, 1e-8, drop, seed)
     orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
-    orc.set_bf16(prec == bns.BNS_BF16)
     orc.set_training(optimizer=1, beta1=0.9, beta2=0.999, eps=1e-8, dropout=drop, dropout_seed=seed)
     tol = TOL[prec]
     # Adam normalises each step to ~lr, so a gradient entry within its rounding error of zero can take a step of
@@ -496,10 +434,9 @@ def test_adam_dropout_parity(prec, layer, m, p, drop):
             run.sample(p, SEED, e)
             orc.sample(p, SEED, e)
             loss, acc, G, Wn = run.epoch(Ws, lr)
-            orc.set_transform_first(run.tf)
             lo, ao, Go = orc.epoch(Wd, lr)
             assert abs(loss - lo) <= LOSS_TOL * abs(lo), (e, loss, lo)
-            F = relu_flip_floor(run, orc, L, prec, f"adam{e}")
+            F = relu_flips(run, orc, L, prec, f"adam{e}")[0]
             for l in range(1, L + 1):
                 if not (run.tf >> (l - 1)) & 1:
                     assert relerr(run.gather(bns.BNS_Q_Z, l, dims[l - 1]), orc.tensor(O.T_Z, l)) <= tol, ("Z", e, l)
@@ -585,19 +522,17 @@ def test_multilabel_parity(prec, layer, m, p):
     for r, c in enumerate(run.ctx):
         c.set_multilabel(T[run.inner[r]])
     orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
-    orc.set_bf16(prec == bns.BNS_BF16)
     orc.set_multilabel(T)
     tol = TOL[prec]
     try:
         for e in range(2 if prec == bns.BNS_FP32 else 1):
             run.sample(p, SEED, e)
             orc.sample(p, SEED, e)
-            orc.set_transform_first(run.tf)
             loss, f1, G, Wn = run.epoch(Ws, 0.5)
             lo, fo, Go = orc.epoch(Wd, 0.5)
             assert abs(loss - lo) <= LOSS_TOL * abs(lo), (e, loss, lo)
             assert abs(f1 - fo) <= (1e-3 if prec == bns.BNS_FP32 else 2e-2), (e, f1, fo)
-            F = relu_flip_floor(run, orc, L, prec, f"bce{e}")
+            F = relu_flips(run, orc, L, prec, f"bce{e}")[0]
             assert relerr(run.gather(bns.BNS_Q_DH, L, dims[L]), orc.tensor(O.T_DH, L)) <= tol
             for l in range(L):
                 if l + 1 > F:
@@ -631,11 +566,10 @@ def test_gat_parity(prec, m, p, sampler):
     Wd = [w.astype(np.float64) for w in Ws]
     run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y)
     orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
-    orc.set_bf16(prec == bns.BNS_BF16)
     try:
         for e in range(2 if prec == bns.BNS_FP32 else 1):
             if sampler:
-                parallel(m, lambda r: run.ctx[r].sample_edges(sampler, p, SEED, e))
+                run.sample_edges(sampler, p, SEED, e)
                 orc.sample_edges(sampler, p, SEED, e)
             else:
                 run.sample(p, SEED, e)

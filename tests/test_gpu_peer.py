@@ -24,7 +24,8 @@ from paper_2203_10983_b200 import bns
 from paper_2203_10983_b200 import inputs as I
 
 from gpu_harness import GpuRun, parallel
-from test_gpu_parity import compare_epoch, wl
+from gpu_harness import compare_epoch
+from test_gpu_parity import wl
 
 pytestmark = pytest.mark.gpu
 SEED = I.BNS_SEED
@@ -105,7 +106,6 @@ def test_peer_memory_oracle_parity(prec, m, p):
     run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y,
                  flags=bns.BNS_RETAIN_GRADS | bns.BNS_PEER_MEMORY)
     orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
-    orc.set_bf16(prec == bns.BNS_BF16)
     try:
         for e in range(2):
             run.sample(p, SEED, e)

@@ -201,48 +201,6 @@ def test_unbiased_aggregate():
     assert np.all(np.abs(a.mean(0) - z_exact) <= 4.5 * se + 1e-12)
 
 
-def test_bf16_rounding_matches_torch():
-    import torch
-    rng = np.random.default_rng(3)
-    xs = np.concatenate([rng.normal(size=2000) * 10.0 ** rng.integers(-30, 30, 2000), [0.0, -0.0, 1.0, 2**-133]])
-    ref = torch.tensor(xs, dtype=torch.float32).bfloat16().double().numpy()
-    got = np.array([O.round_bf16(x) for x in xs])
-    assert np.array_equal(got, ref)
-
-
-@pytest.mark.parametrize("name", ["E1", "E2", "E3", "E4"])
-def test_bf16_emulation_exact_on_representable_goldens(name):
-    # all stored forward values of E1-E4 are dyadic with <= 8 significant bits -> bf16 storage changes nothing
-    c = GOLD["cases"][name]
-    Ws = [np.array(w, np.float64) for w in GOLD[c["W"]]]
-    dims = [1] + [w.shape[1] for w in Ws]
-    o = p4_oracle(0, dims)
-    o.set_bf16(True)
-    if "draw" in c:
-        d = GOLD[c["draw"]]
-        o.set_keep(c["p"], [d["keep_rank0"], d["keep_rank1"]])
-    else:
-        o.sample(c["p"], 1, 0)
-    loss, acc, G = o.epoch([w.copy() for w in Ws], 0.0)
-    assert abs(loss - c["loss"]) < 1e-8 and acc == c["acc"]
-    np.testing.assert_allclose(o.tensor(O.T_H, len(Ws)), c["logits"], atol=0)
-    for l, g in enumerate(c["dW"]):      # gradients only differ by the bf16 rounding of dPre / dZ' / dX
-        np.testing.assert_allclose(G[l], g, rtol=2 ** -5, atol=1e-3 * np.abs(g).max())
-
-
-def test_bf16_emulation_close_to_float64():
-    ip, ix, part, X, y, Ws = random_case(61, N=60, m=3, dims=(3, 6, 4))
-    out = []
-    for bf in (False, True):
-        o = O.Oracle(ip, ix, part, 3, [3, 6, 4], 0, X, y)
-        o.set_bf16(bf)
-        o.sample(0.5, 3, 3)
-        out.append(o.epoch([w.copy() for w in Ws], 0.0))
-    assert abs(out[0][0] - out[1][0]) < 2e-2 * abs(out[0][0])
-    for a, b in zip(out[0][2], out[1][2]):
-        assert np.abs(a - b).max() <= 5e-2 * np.abs(a).max()
-
-
 # ---------------- f2: Adam and dropout (readings R38, R39) ----------------
 def test_adam_matches_torch_optim():
     import torch
@@ -324,33 +282,6 @@ def test_dropout_zero_is_identity_and_unbiased():
         acc.append(o.tensor(O.T_Z, 1))
     a = np.array(acc)
     assert np.all(np.abs(a.mean(0) - z) <= 4.5 * a.std(0) / np.sqrt(len(acc)) + 1e-12)
-
-
-# ---------------- R42: transform-first evaluation order (bf16 emulation only) ----------------
-@pytest.mark.parametrize("drop", [0.0, 0.3])
-def test_transform_first_is_noop_in_double_and_close_in_bf16(drop):
-    """In double the transform-first order is the same arithmetic (mask must not change a bit); in bf16 it only
-    moves the rounding points, so loss / grads stay within bf16 rounding of the double result, and they do move."""
-    dims = [9, 6, 5, 3]
-    ip, ix, part, X, y, Ws = random_case(73, N=60, m=3, dims=tuple(dims))
-    res = {}
-    for bf in (False, True):
-        for tf in (0, 0b111):
-            o = O.Oracle(ip, ix, part, 3, dims, 0, X, y)
-            o.set_bf16(bf)
-            o.set_transform_first(tf)
-            o.set_training(0, dropout=drop, dropout_seed=9)
-            o.sample(0.5, 3, 3)
-            loss, acc, G = o.epoch([w.copy() for w in Ws], 0.0)
-            res[(bf, tf)] = (loss, G, [o.tensor(O.T_H, l) for l in range(1, 4)],
-                             [o.tensor(O.T_DH, l) for l in range(1, 3)])
-    a, b = res[(False, 0)], res[(False, 0b111)]
-    assert a[0] == b[0] and all(np.array_equal(x, z) for x, z in zip(a[1] + a[2] + a[3], b[1] + b[2] + b[3]))
-    d, t = res[(False, 0)], res[(True, 0b111)]
-    assert abs(d[0] - t[0]) < 2e-2 * abs(d[0])
-    for x, z in zip(d[1] + d[2], t[1] + t[2]):
-        assert np.abs(x - z).max() <= 5e-2 * np.abs(x).max()
-    assert not all(np.array_equal(x, z) for x, z in zip(res[(True, 0)][1], t[1]))
 
 
 # ---------------- f4: multi-label sigmoid BCE + F1-micro (Yelp, PAPER.md:384; reading R44) ----------------
