@@ -75,16 +75,15 @@ def relu_flips(run, orc, L, prec, tag):
     return F, out
 
 
-def sampled_operator(orc, run, sampler, q):
-    """The epoch's sampled aggregation as one global N x N float64 matrix, from the ORACLE's induced lists (Alg.1 l.5):
-    row v (inner to rank r) holds c_u / deg_G(v) (SAGE, R1-R3) or c_u / sqrt(d~_v d~_u) + [u = v] / d~_v (GCN, App. A);
-    c_u = 1 on inner columns and 1/q on sampled boundary columns (BNS q = p, BES q; R3, R41); DropEdge: 1/q on every
-    arc (R41)."""
-    import scipy.sparse as sp
-    N = run.N
+def sampled_operator(orc, m, layer, sampler, q):
+    """The epoch's sampled aggregation as one global N x N float64 operator (COO triplets), from the ORACLE's induced
+    lists (Alg.1 l.5): row v (inner to rank r) holds c_u / deg_G(v) (SAGE, R1-R3) or c_u / sqrt(d~_v d~_u) +
+    [u = v] / d~_v (GCN, App. A); c_u = 1 on inner columns and 1/q on sampled boundary columns (BNS q = p, BES q; R3,
+    R41); DropEdge: 1/q on every arc (R41)."""
+    N = len(orc.indptr) - 1
     deg = np.diff(orc.indptr).astype(np.float64)
     rows, cols, vals = [], [], []
-    for r in range(run.m):
+    for r in range(m):
         V = orc.list(O.V_LIST, r)
         ptr = orc.list(O.INDUCED_PTR, r)
         col = orc.list(O.INDUCED_COL, r)
@@ -92,18 +91,18 @@ def sampled_operator(orc, run, sampler, q):
         inner = orc.part_of[col] == r
         inv = 1.0 / q if q > 0 else 0.0
         c = np.full(len(col), inv) if sampler == bns.BNS_SAMPLER_DROPEDGE else np.where(inner, 1.0, inv)
-        if run.layer == bns.BNS_LAYER_SAGE_MEAN:
+        if layer == bns.BNS_LAYER_SAGE_MEAN:
             w = c / deg[v]
         else:
             w = c / np.sqrt((deg[v] + 1.0) * (deg[col] + 1.0))
         rows.append(v)
         cols.append(col)
         vals.append(w)
-    if run.layer == bns.BNS_LAYER_GCN:
+    if layer == bns.BNS_LAYER_GCN:
         rows.append(np.arange(N))
         cols.append(np.arange(N))
         vals.append(1.0 / (deg + 1.0))
-    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(N, N))
+    return np.concatenate(rows), np.concatenate(cols), np.concatenate(vals), N
 
 
 def bf16_round(a):
@@ -111,52 +110,99 @@ def bf16_round(a):
     return torch.tensor(np.asarray(a, np.float32)).bfloat16().double().numpy()
 
 
-def layer_local_check(run, orc, Ws, G, L, sampler, q, tag, tol):
-    """bf16: every layer against float64 recomputed from its own GPU inputs (see above); returns the margins."""
-    A = sampled_operator(orc, run, sampler, q)
-    sage = run.layer == bns.BNS_LAYER_SAGE_MEAN
-    dims = run.dims
+def layer_local(op, snap, Ws, G, L, dims, layer, tol, tag, device="cpu"):
+    """bf16: every layer against float64 recomputed from its OWN GPU inputs: the H^(l-1) it read, the dH^l it received
+    and its own ReLU mask (snap), the bf16 weight operands (R19) and the oracle's sampled operator (op).  torch float64
+    (sparse CSR x dense; cuSPARSE when device = cuda).  Returns the margins; asserts <= tol."""
+    import torch
+    rows, cols, vals, N = op
+    dev = torch.device(device)
+    A = torch.sparse_coo_tensor(torch.from_numpy(np.stack([rows, cols]).astype(np.int64)), torch.from_numpy(vals),
+                                (N, N)).coalesce().to(dev)
+    At = A.t().coalesce()
+    A, At = A.to_sparse_csr(), At.to_sparse_csr()
+    sage = layer == bns.BNS_LAYER_SAGE_MEAN
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).to(dev)  # noqa: E731
+    R = lambda a, b: float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))  # noqa: E731
     out = {}
     for l in range(1, L + 1):
         din = dims[l - 1]
-        Wb = bf16_round(Ws[l - 1])             # the GEMM operand of the bf16 mode (R19)
-        X = run.gather(bns.BNS_Q_H, l - 1, din)
+        Wb = T(bf16_round(Ws[l - 1]))
+        X = T(snap[("H", l - 1)])
         AX = A @ X
         pre = AX @ Wb[:din] + X @ Wb[din:] if sage else AX @ Wb
-        Hg = run.gather(bns.BNS_Q_H, l, dims[l])
-        out[f"H{l}"] = e = relerr(Hg, np.maximum(pre, 0) if l < L else pre)
+        Hg = T(snap[("H", l)])
+        out[f"H{l}"] = e = R(Hg, pre.clamp_min(0) if l < L else pre)
         assert e <= tol, (tag, "layer-local H", l, e)
-        dH = run.gather(bns.BNS_Q_DH, l, dims[l])
+        dH = T(snap[("dH", l)])
         dpre = dH * (Hg > 0) if l < L else dH
-        dW = np.concatenate([AX.T @ dpre, X.T @ dpre]) if sage else AX.T @ dpre
-        out[f"dW{l}"] = e = relerr(G[l - 1], dW)
+        dW = torch.cat([AX.t() @ dpre, X.t() @ dpre]) if sage else AX.t() @ dpre
+        out[f"dW{l}"] = e = R(T(G[l - 1]), dW)
         assert e <= tol, (tag, "layer-local dW", l, e)
+        del AX, pre
         if l > 1:
-            dX = A.T @ (dpre @ Wb[:din].T) + (dpre @ Wb[din:].T if sage else 0)
-            out[f"dH{l - 1}"] = e = relerr(run.gather(bns.BNS_Q_DH, l - 1, din), dX)
+            dX = At @ (dpre @ Wb[:din].t())
+            if sage:
+                dX = dX + dpre @ Wb[din:].t()
+            out[f"dH{l - 1}"] = e = R(T(snap[("dH", l - 1)]), dX)
             assert e <= tol, (tag, "layer-local dH", l - 1, e)
     return out
 
 
-def compare_epoch(run, orc, L, Ws, Wd, lr, prec, tag="", host=False, local=True):
-    """One epoch on both sides (two independent weight trajectories: Ws fp32 on the GPU, Wd float64 in the oracle,
-    both updated in place / returned) and the parity checks described above.  Returns the GPU's new weights."""
+def snapshot(run, L, what=("H", "Z", "dH")):
+    """The GPU's per-layer tensors of the last epoch (inner rows by gid) as float32 -- exact for fp32 / bf16 values."""
+    snap = {}
+    for l in range(0, L + 1):
+        if "H" in what:
+            snap[("H", l)] = run.gather(bns.BNS_Q_H, l, run.dims[l]).astype(np.float32)
+        if l >= 1 and "dH" in what:
+            snap[("dH", l)] = run.gather(bns.BNS_Q_DH, l, run.dims[l]).astype(np.float32)
+        if l >= 1 and "Z" in what and not (run.tf >> (l - 1)) & 1 and run.layer != bns.BNS_LAYER_GAT:
+            snap[("Z", l)] = run.gather(bns.BNS_Q_Z, l, run.dims[l - 1]).astype(np.float32)
+    return snap
+
+
+class OracleView:
+    """The oracle's tensors of its last epoch, read lazily."""
+
+    def __init__(self, orc):
+        self.orc = orc
+
+    def get(self, kind, l):
+        return self.orc.tensor({"H": O.T_H, "Z": O.T_Z, "dH": O.T_DH}[kind], l)
+
+
+def check_epoch(gpu, orc_out, L, prec, dims, tf, layer, N, tag, labels, local_fn=None):
+    """Parity of one epoch (see the block comment above).  gpu = (loss, acc, G, W_new, snap) with snap from
+    snapshot(); orc_out = (loss, acc, G, W_new, OracleView).  local_fn(G) runs the bf16 layer-local check."""
     tol = TOL[prec]
-    loss, acc, G, Wn = run.epoch(Ws, lr, host=host)
-    lo, ao, Go = orc.epoch(Wd, lr)
+    loss, acc, G, Wn, snap = gpu
+    lo, ao, Go, Wd, ov = orc_out
     assert abs(loss - lo) <= LOSS_TOL * max(abs(lo), 1e-12), (tag, loss, lo)
-    ntr = max(1, int((orc.labels >= 0).sum()))
+    ntr = max(1, int((labels >= 0).sum()))
     assert abs(acc - ao) <= (0.0 if prec == bns.BNS_FP32 else 0.02) + 2.0 / ntr, (tag, acc, ao)
-    dims = run.dims
-    F, flips = relu_flips(run, orc, L, prec, tag)
+    # ReLU flips (R36)
+    F, flips = 0, []
+    for l in range(1, L):
+        g, o = snap[("H", l)], ov.get("H", l)
+        flip = (g > 0) != (o > 0)
+        n = int(flip.sum())
+        flips.append(n)
+        if n == 0:
+            continue
+        assert prec == bns.BNS_BF16, (tag, "ReLU flips in fp32", l, n)
+        scale = max(np.abs(o).max(), 1e-30)
+        assert n <= FLIP_SHARE_MAX * o.size, (tag, "too many ReLU flips", l, n, o.size)
+        assert np.abs(g[flip]).max() <= scale / 64 and np.abs(o[flip]).max() <= scale / 64, (tag, "flip not ambiguous", l)
+        F = l
     margins = {"loss": abs(loss - lo) / max(abs(lo), 1e-12)}
     for l in range(1, L + 1):
-        if not (run.tf >> (l - 1)) & 1 and run.layer != bns.BNS_LAYER_GAT:   # no Z on R42 / GAT layers
-            margins[f"Z{l}"] = e = relerr(run.gather(bns.BNS_Q_Z, l, dims[l - 1]), orc.tensor(O.T_Z, l))
+        if ("Z", l) in snap:
+            margins[f"Z{l}"] = e = relerr(snap[("Z", l)], ov.get("Z", l))
             assert e <= tol, (tag, "Z", l, e)
-        margins[f"H{l}"] = e = relerr(run.gather(bns.BNS_Q_H, l, dims[l]), orc.tensor(O.T_H, l))
+        margins[f"H{l}"] = e = relerr(snap[("H", l)], ov.get("H", l))
         assert e <= tol, (tag, "H", l, e)
-        margins[f"dH{l}"] = e = relerr(run.gather(bns.BNS_Q_DH, l, dims[l]), orc.tensor(O.T_DH, l))
+        margins[f"dH{l}"] = e = relerr(snap[("dH", l)], ov.get("dH", l))
         assert l < F or e <= tol, (tag, "dH", l, e)
     for l in range(L):
         margins[f"dW{l + 1}"] = e = relerr(G[l], Go[l])
@@ -164,12 +210,27 @@ def compare_epoch(run, orc, L, Ws, Wd, lr, prec, tag="", host=False, local=True)
             assert e <= tol, (tag, "dW", l, e)
             e = relerr(Wn[l], Wd[l])
             assert e <= max(tol * 0.1, 1e-6), (tag, "W", l, e)
+    rec = {"tag": tag, "prec": int(prec), "layer": layer, "F": F, "flips": flips,
+           "units": [int(N * dims[l]) for l in range(1, L)], "vs_float64": margins}
     if prec == bns.BNS_BF16:
-        rec = {"tag": tag, "layer": run.layer, "m": run.m, "F": F, "flips": flips,
-               "units": [int(run.N * dims[l]) for l in range(1, L)], "vs_float64": margins}
-        if local and run.layer != bns.BNS_LAYER_GAT and run.last_draw is not None:
-            rec["layer_local"] = layer_local_check(run, orc, Ws, G, L, *run.last_draw, tag, tol)
+        if local_fn is not None:
+            rec["layer_local"] = local_fn(G)
         BF16_REPORT.append(rec)
+    return rec
+
+
+def compare_epoch(run, orc, L, Ws, Wd, lr, prec, tag="", host=False, local=True):
+    """One epoch on both sides (two independent weight trajectories: Ws fp32 on the GPU, Wd float64 in the oracle,
+    updated in place / returned) and the parity checks of check_epoch.  Returns the GPU's new weights."""
+    loss, acc, G, Wn = run.epoch(Ws, lr, host=host)
+    lo, ao, Go = orc.epoch(Wd, lr)
+    snap = snapshot(run, L)
+    local_fn = None
+    if local and run.layer != bns.BNS_LAYER_GAT and run.last_draw is not None:
+        op = sampled_operator(orc, run.m, run.layer, *run.last_draw)
+        local_fn = lambda G_: layer_local(op, snap, Ws, G_, L, run.dims, run.layer, TOL[prec], tag)  # noqa: E731
+    check_epoch((loss, acc, G, Wn, snap), (lo, ao, Go, Wd, OracleView(orc)), L, prec, run.dims, run.tf, run.layer,
+                run.N, tag, orc.labels, local_fn)
     return [w.astype(np.float32) for w in Wn]
 
 

@@ -1,5 +1,11 @@
 """Full-size parity (BASELINE.json configs[1], Reddit-shaped: 232,965 nodes, 114.6 M arcs, 602 features, SAGE 4x256):
 
+* the north-star Target (BASELINE.json north_star, Alg. 1 PAPER.md:269-297 with the 4 x 256 model of PAPER.md:416):
+  m = 8 partitions (LOCAL transport on one GPU; two-constraint LDG and random partitions), p = 0.1, two epochs, fp32
+  and bf16, against the float64 oracle on EVERY row of every layer: loss within 1e-3, H^l / Z^l / dH^l / dW^l within
+  1e-5 (fp32) and 2e-2 (bf16, with the ReLU-flip rule and the layer-local check of tests/gpu_harness.py); plus the
+  bench configuration (m = 1, bf16) for one epoch, gradients included;
+
 * m = 1 in bench.py's launch configuration (bf16, tcgen05 GEMMs): sampled rows of Z^1 and H^1 recomputed one by one
   in float64 from raw neighbours (PAPER.md:100 / R1), and a finite loss;
 * m = 8, p = 0.1 on one GPU (LOCAL transport): keep masks, U_i and S_{i,j} bit-exact against the oracle's plan +
@@ -12,7 +18,9 @@ from oracle import oracle as O
 from paper_2203_10983_b200 import bns
 from paper_2203_10983_b200 import inputs as I
 
-from gpu_harness import GpuRun, parallel
+import threading
+
+from gpu_harness import GpuRun, OracleView, check_epoch, layer_local, parallel, sampled_operator, snapshot
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 SEED = I.BNS_SEED
@@ -136,3 +144,113 @@ def test_other_shapes_m1_two_layers(name):
             assert err < 2e-2, (name, l + 1, err)
     finally:
         run.close()
+
+
+class OracleThread(threading.Thread):
+    """One oracle (single-threaded float64, its own weight trajectory) stepping through epochs in the background;
+    after each epoch it waits until the test has compared that epoch's tensors (ctypes releases the GIL, so several
+    oracles and the GPU runs proceed at the same time on the box's cores)."""
+
+    def __init__(self, orc, W, p, epochs, lr):
+        super().__init__(daemon=True)
+        self.orc, self.W, self.p, self.epochs, self.lr = orc, W, p, epochs, lr
+        self.done = [threading.Event() for _ in range(epochs)]
+        self.go = [threading.Event() for _ in range(epochs)]
+        self.out, self.err, self.secs = [None] * epochs, None, []
+
+    def run(self):
+        import time
+        try:
+            for e in range(self.epochs):
+                t0 = time.time()
+                self.orc.sample(self.p, SEED, e)
+                lo, ao, Go = self.orc.epoch(self.W, self.lr)
+                self.secs.append(time.time() - t0)
+                self.out[e] = (lo, ao, Go, [w.copy() for w in self.W], OracleView(self.orc))
+                self.done[e].set()
+                self.go[e].wait()
+        except BaseException as ex:  # noqa: BLE001
+            self.err = ex
+            for d in self.done:
+                d.set()
+
+    def result(self, e):
+        self.done[e].wait()
+        if self.err is not None:
+            raise self.err
+        return self.out[e]
+
+
+def gpu_epochs(indptr, indices, part, m, dims, layer, prec, X, y, p, epochs, lr, light):
+    """GPU side of a configuration: per epoch (loss, acc, G, W_new, snapshot) and, in bf16, the layer-local margins
+    (the sampled operator from `light`, an oracle holding only the plan and the draw)."""
+    L = len(dims) - 1
+    run = GpuRun(indptr, indices, part, m, dims, layer, prec, X, y, flags=bns.BNS_RETAIN_GRADS,
+                 max_p=0.2 if m > 1 else 0.0)
+    W = I.weights(dims, layer)
+    out = []
+    try:
+        for e in range(epochs):
+            run.sample(p, SEED, e)
+            Ws = [w.copy() for w in W]
+            loss, acc, G, Wn = run.epoch(Ws, lr)
+            snap = snapshot(run, L)
+            local = None
+            if prec == bns.BNS_BF16:
+                light.sample(p, SEED, e)
+                op = sampled_operator(light, m, layer, bns.BNS_SAMPLER_BNS, p)
+                local = layer_local(op, snap, Ws, G, L, dims, layer, 2e-2, f"m{m} e{e} layer-local", device="cuda")
+            out.append(((loss, acc, G, Wn, snap), local))
+            W = [w.astype(np.float32) for w in Wn]
+        return out, run.tf
+    finally:
+        run.close()
+
+
+def test_north_star_full_size(reddit):
+    """BASELINE.json north_star Target: Reddit-shaped 4-layer GraphSAGE epoch at p = 0.1 on 8 partitions against the
+    oracle (SURVEY.md §8(c) "Large-config parity"), plus the m = 1 bench configuration."""
+    import json
+    import os
+    import time
+    sh, indptr, indices, y = reddit
+    dims, layer, L, lr = sh.dims, sh.layer, sh.L, 0.1
+    X = I.features(np.arange(sh.N, dtype=np.int32), sh.d0)
+    zeros = (np.zeros((sh.N, 1), np.float32), np.zeros(sh.N, np.int32))
+    configs = [("ldg2", 8, 2), ("random", 8, 2), ("single", 1, 1)]
+    threads, parts = {}, {}
+    t0 = time.time()
+    for name, m, epochs in configs:
+        part = np.zeros(sh.N, np.int32) if m == 1 else I.partition(indptr, indices, m, name)
+        parts[name] = part
+        orc = O.Oracle(indptr, indices, part, m, dims, layer, X, y)
+        threads[name] = OracleThread(orc, [w.astype(np.float64) for w in I.weights(dims, layer)], 0.1, epochs, lr)
+        threads[name].start()
+    report = {"oracle_seconds": {}, "records": []}
+    try:
+        for name, m, epochs in configs:
+            light = O.Oracle(indptr, indices, parts[name], m, [1, 1], 0, *zeros)
+            precs = (bns.BNS_BF16,) if m == 1 else (bns.BNS_FP32, bns.BNS_BF16)
+            gpu = {prec: gpu_epochs(indptr, indices, parts[name], m, dims, layer, prec, X, y, 0.1, epochs, lr, light)
+                   for prec in precs}
+            del light
+            th = threads[name]
+            for e in range(epochs):
+                orc_out = th.result(e)
+                for prec in precs:
+                    (g, local), tf = gpu[prec][0][e], gpu[prec][1]
+                    rec = check_epoch(g, orc_out, L, prec, dims, tf, layer, sh.N,
+                                      f"{name} m={m} prec={prec} epoch {e}", y,
+                                      (lambda G_, lo=local: lo) if local is not None else None)
+                    report["records"].append(rec)
+                th.go[e].set()
+            report["oracle_seconds"][name] = th.secs
+            del gpu
+    finally:
+        for th in threads.values():
+            for ev in th.go:
+                ev.set()
+    report["wall_seconds"] = time.time() - t0
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(os.path.join("gpurun_out", "north_star_fullsize.json"), "w") as f:
+        json.dump(report, f, indent=1)
