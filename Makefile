@@ -16,7 +16,7 @@ OBJDIR    := build
 all: oracle/liboracle.so $(PKG)/inputs/libbnsgen.so $(PKG)/libbns.so
 
 oracle/liboracle.so: oracle/bns_oracle.cpp
-	g++ -O2 -std=c++17 -fPIC -shared -o $@ $<
+	g++ -O3 -mavx2 -mfma -std=c++17 -fPIC -shared -o $@ $<
 
 $(PKG)/inputs/libbnsgen.so: $(PKG)/inputs/gen.cpp
 	g++ -O3 -std=c++17 -fPIC -shared -fopenmp -o $@ $<
