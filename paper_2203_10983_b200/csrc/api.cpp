@@ -306,6 +306,16 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.d_cand_out = static_cast<int32_t*>(dalloc(c, (c.n_cand + 1) * sizeof(int32_t)));
     c.d_slot_of_b = static_cast<int32_t*>(dalloc(c, (P.n_bd + 1) * sizeof(int32_t)));
     c.d_bkeep = static_cast<uint32_t*>(dalloc(c, ((P.n_bd + 31) / 32 + 1) * sizeof(uint32_t)));
+    {   // single-pass scans (induce.cu): tile states of the draw, the induce pass and the two segment chains
+        c.lb_off_induce = c.n_cand / 1024 + 1;
+        c.lb_off_segf = c.lb_off_induce + c.nnz_i / 8192 + 1;
+        c.lb_off_segb = c.lb_off_segf + P.n_in / 1024 + 1;
+        const int64_t n = c.lb_off_segb + P.n_bd / 1024 + 1;
+        c.d_lb_state = static_cast<uint64_t*>(dalloc(c, n * sizeof(uint64_t)));
+        BNS_CUDA(cudaMemset(c.d_lb_state, 0, n * sizeof(uint64_t)));
+        c.d_lb_ctr = static_cast<unsigned*>(dalloc(c, 16 * sizeof(unsigned)));
+        BNS_CUDA(cudaMemset(c.d_lb_ctr, 0, 16 * sizeof(unsigned)));
+    }
     c.d_seg_pos = static_cast<int64_t*>(salloc(c, (2 * m + 1 + 8) * sizeof(int64_t)));
     BNS_CUDA(cudaMallocHost(&c.h_seg_pos, (2 * m + 1 + 8) * sizeof(int64_t)));
     c.d_ind_ptr = static_cast<int64_t*>(dalloc(c, (P.n_in + 1) * sizeof(int64_t)));
@@ -485,15 +495,19 @@ void sample_boundary(Ctx& c, int sampler, double p, uint64_t seed, uint64_t epoc
     {
         PhaseTimer t(c, BNS_PH_SAMPLE);
         if (edges) launch_sample_edges(c, T, seed, epoch);
-        else launch_sample(c, T, seed, epoch);
+        else launch_sample_fused(c, T, seed, epoch);
     }
     const bool has_bd = c.plan.n_bd > 0;
     c.fwd_mode = edges ? 2 : (!has_bd || T >= (1ull << 32)) ? 0 : (T == 0 ? 1 : 2);
     {
         PhaseTimer t(c, BNS_PH_INDUCE);
-        if (c.fwd_mode == 2) launch_induce(c, T, seed, epoch);
-        if (edges) launch_induce_bwd_edges(c, T, seed, epoch);
-        else launch_bwd_segments(c);
+        if (edges) {
+            launch_induce_edges(c, T, seed, epoch);
+            launch_induce_bwd_edges(c, T, seed, epoch);
+        } else {
+            if (c.fwd_mode == 2) launch_induce_fused(c);
+            launch_segments_fused(c, c.fwd_mode == 2);
+        }
         if (c.layer == BNS_LAYER_GCN) launch_gcn_cscale(c);
     }
     total.reset();

@@ -148,6 +148,10 @@ struct Ctx {
     int32_t* d_cand_out = nullptr; // compacted payloads: [U_b (|U|) ; S_local (ΣS)]
     int32_t* d_slot_of_b = nullptr;
     uint32_t* d_bkeep = nullptr;   // keep bit per boundary node (induce)
+    uint64_t* d_lb_state = nullptr; // decoupled look-back tile states (induce.cu): draw | induce | segs fwd | segs bwd
+    unsigned* d_lb_ctr = nullptr;   // tile-order counters of those four chains (each reset by its last tile)
+    int64_t lb_off_induce = 0, lb_off_segf = 0, lb_off_segb = 0;
+    uint32_t lb_gen = 0;            // launch generation stamped into the tile states (nothing cleared per launch)
     int64_t* d_seg_pos = nullptr;  // [2m+1] compacted segment offsets
     int64_t* h_seg_pos = nullptr;  // pinned host copy
     uint32_t* d_ebits = nullptr;   // induce: keep bit per static edge
@@ -224,8 +228,8 @@ struct Ctx {
     double* d_scal = nullptr;      // [loss_sum, correct] (all-reduced)
     double* d_lpart = nullptr;     // per-block loss partials
     int32_t* d_nonfinite = nullptr;
-    const int* d_abort = nullptr;
-    int last_splitk = 1;           // split-K factor of the last tcgen05 weight-gradient GEMM (bns_gemm reports it)  // peer transports: mapped barrier-timeout flag (update kernels skip when set)
+    const int* d_abort = nullptr;  // peer transports: mapped barrier-timeout flag (update kernels skip when set)
+    int last_splitk = 1;           // split-K factor of the last tcgen05 weight-gradient GEMM (bns_gemm reports it)
     // --- f3: edge samplers (BES / DropEdge); allocated by the first bns_sample_edges
     int sampler = 0;               // BNS_SAMPLER_* of the last draw
     float nscale = 1.f;            // neighbour-sum scale (DropEdge: 1/q on every arc; else 1)

@@ -1,0 +1,360 @@
+// induce.cu -- a1 + a2 + a3 of the BNS draw in three single-pass kernels (decoupled look-back scans):
+//
+//   k_sample_fused   Alg.1 l.4 (R5-R7, R23): the Philox Bernoulli draw of every candidate, the
+//                    order-preserving compaction into [U_i ; S_{i,*}] (Alg.1 l.6-7, R24, R27), the boundary keep
+//                    bitmask the induce pass tests against, slot_of_b and the 2m+1 segment offsets (per-peer counts).
+//   k_induce_fused   Alg.1 l.5: the node-induced subgraph on V_i ∪ U_i -- keep bit of every static
+//                    arc (inner columns always, boundary columns by the bitmask), the kept columns scattered in global
+//                    neighbour order and remapped to halo rows n_in + slot, and the induced row pointers.
+//   k_segs_fused     SpMM work lists: forward segments of the induced rows and backward (transposed) segments of the
+//                    sampled halo rows, both chains in one launch, split (hub) rows appended for the fixup.
+//
+// Each kernel is one pass over its tiles: a tile publishes its aggregate, looks back over its predecessors' published
+// aggregates / inclusive prefixes (a warp reads 32 predecessors at a time), and then writes its outputs at their final
+// positions.  Tiles are handed out in launch order by an atomic counter (a tile only waits on tiles that already
+// started, so the look-back cannot deadlock); the tile states carry a launch generation, so nothing is cleared between
+// launches.  Results are bitwise those of the multi-pass version (count -> scan -> scatter): positions are exact
+// prefix sums.
+#include "common.h"
+#include "dev.cuh"
+#include "kernels.h"
+
+namespace bns {
+
+namespace {
+
+constexpr int kTile = 1024;          // candidates / rows / halo slots per tile (one per thread)
+constexpr int kEdgeThreads = 256;    // induce: one 32-arc word per thread -> 8192 arcs per tile
+constexpr uint64_t kValMask = (1ull << 38) - 1;
+enum { LB_NONE = 0, LB_AGG = 1, LB_PREFIX = 2 };
+
+__device__ __forceinline__ uint64_t lb_pack(uint32_t gen, int flag, int64_t v) {
+    return ((uint64_t)(gen & 0xFFFFFFu) << 40) | ((uint64_t)flag << 38) | ((uint64_t)v & kValMask);
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// tile id in launch order; the block that draws the last id resets the counter for the next launch
+__device__ __forceinline__ int64_t next_tile(unsigned* ctr, int64_t ntiles, int64_t* s_tile) {
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(ctr, 1u);
+        if ((int64_t)t == ntiles - 1) atomicExch(ctr, 0u);
+        *s_tile = t;
+    }
+    __syncthreads();
+    return *s_tile;
+}
+
+// exclusive prefix of tile t with aggregate agg (every thread passes the same agg); all threads get the result
+__device__ int64_t lookback(uint64_t* state, uint32_t gen, int64_t t, int64_t agg, int64_t* s_excl) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const uint32_t g = gen & 0xFFFFFFu;
+        int64_t excl = 0;
+        if (t > 0) {
+            if (lane == 0) st_release(state + t, lb_pack(gen, LB_AGG, agg));
+            int64_t p = t - 1;
+            for (;;) {
+                const int64_t q = p - lane;
+                const uint64_t s = q >= 0 ? ld_acquire(state + q) : lb_pack(gen, LB_PREFIX, 0);
+                const int flag = (int)((s >> 38) & 3u);
+                const bool ready = (uint32_t)(s >> 40) == g && flag != LB_NONE;
+                if (!__all_sync(0xffffffffu, ready)) continue;
+                const unsigned pm = __ballot_sync(0xffffffffu, flag == LB_PREFIX);
+                const int upto = pm ? __ffs(pm) - 1 : 31;
+                int64_t x = lane <= upto ? (int64_t)(s & kValMask) : 0;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                excl += x;
+                if (pm) break;
+                p -= 32;
+            }
+        }
+        if (lane == 0) {
+            st_release(state + t, lb_pack(gen, LB_PREFIX, excl + agg));
+            *s_excl = excl;
+        }
+    }
+    __syncthreads();
+    return *s_excl;
+}
+
+// block-wide exclusive scan of one int per thread (blockDim.x <= 1024); returns the thread's exclusive prefix, the
+// block total in *s_total
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* s_total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int s = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        s_warp[lane] = s;
+        if (lane == 31) *s_total = s;
+    }
+    __syncthreads();
+    return (w ? s_warp[w - 1] : 0) + x - v;
+}
+
+struct SampleArgs {
+    const int32_t* gid; const int32_t* key; const int32_t* payload; int64_t n, n_bd;
+    uint64_t T; uint32_t e_lo, e_hi, s_lo, s_hi;
+    const int64_t* cand_seg; int nseg;
+    uint8_t* flags; uint32_t* bkeep; int32_t* out; int32_t* slot_of_b; int64_t* seg_pos;
+    int64_t* zero; int nzero;                     // counters the later passes add to (split-list lengths)
+    uint64_t* state; unsigned* ctr; uint32_t gen; int64_t ntiles;
+};
+
+__global__ void __launch_bounds__(kTile) k_sample_fused(const SampleArgs a) {
+    __shared__ int64_t s_tile, s_excl;
+    __shared__ int s_warp[32], s_total;
+    const int64_t t = next_tile(a.ctr, a.ntiles, &s_tile);
+    const int64_t i = t * kTile + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    int keep = 0;
+    if (i < a.n) {
+        const uint32_t r = philox4((uint32_t)a.gid[i], (uint32_t)a.key[i], a.e_lo, a.e_hi, a.s_lo, a.s_hi).x;
+        keep = ((uint64_t)r < a.T) ? 1 : 0;
+        a.flags[i] = (uint8_t)keep;
+    }
+    // boundary keep bitmask (bit b of word b / 32 = keep(B_i[b], i)) for the induce pass
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    const int64_t i0 = i - lane;
+    if (lane == 0 && i0 < a.n_bd) {
+        const int64_t valid = a.n_bd - i0;
+        a.bkeep[i0 >> 5] = valid >= 32 ? bal : (bal & ((1u << valid) - 1u));
+    }
+    if (t == 0 && threadIdx.x < a.nzero) a.zero[threadIdx.x] = 0;
+    const int ex = block_excl_scan(keep, s_warp, &s_total);
+    const int64_t excl = lookback(a.state, a.gen, t, s_total, &s_excl);
+    const int64_t pos = excl + ex;
+    if (i < a.n) {
+        if (keep) a.out[pos] = a.payload[i];
+        if (i < a.n_bd) a.slot_of_b[a.payload[i]] = keep ? (int32_t)pos : -1;
+        for (int k = 0; k < a.nseg; ++k)
+            if (a.cand_seg[k] == i) a.seg_pos[k] = pos;
+    }
+    if (t == a.ntiles - 1 && threadIdx.x == 0)   // segments that start at the end (empty trailing segments)
+        for (int k = 0; k < a.nseg; ++k)
+            if (a.cand_seg[k] >= a.n) a.seg_pos[k] = excl + s_total;
+}
+
+__device__ __forceinline__ bool arc_kept(int32_t x, const uint32_t* __restrict__ bkeep) {
+    if (x >= 0) return true;
+    const uint32_t b = (uint32_t)(-x - 1);
+    return (__ldg(bkeep + (b >> 5)) >> (b & 31)) & 1u;
+}
+
+struct InduceArgs {
+    const int32_t* col_enc; int64_t nnz; const uint32_t* bkeep; const int32_t* slot_of_b; int64_t n_in;
+    const int64_t* row_ptr; int32_t* out_col; int64_t* out_ptr; int64_t* total;
+    uint64_t* state; unsigned* ctr; uint32_t gen; int64_t ntiles;
+};
+
+__global__ void __launch_bounds__(kEdgeThreads) k_induce_fused(const InduceArgs a) {
+    __shared__ int64_t s_tile, s_excl, s_rlo, s_rhi;
+    __shared__ int s_warp[32], s_total;
+    __shared__ uint32_t s_word[kEdgeThreads];
+    __shared__ int s_wex[kEdgeThreads];
+    const int64_t t = next_tile(a.ctr, a.ntiles, &s_tile);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t e0 = t * (kEdgeThreads * 32);
+    const int64_t e1 = min(a.nnz, e0 + kEdgeThreads * 32);
+    const int64_t ew = e0 + (int64_t)threadIdx.x * 32;   // this thread's 32-arc word
+    uint32_t word = 0;
+    if (ew + 32 <= a.nnz) {
+        const int4* p = reinterpret_cast<const int4*>(a.col_enc + ew);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int4 v = __ldg(p + q);
+            word |= (uint32_t)arc_kept(v.x, a.bkeep) << (4 * q);
+            word |= (uint32_t)arc_kept(v.y, a.bkeep) << (4 * q + 1);
+            word |= (uint32_t)arc_kept(v.z, a.bkeep) << (4 * q + 2);
+            word |= (uint32_t)arc_kept(v.w, a.bkeep) << (4 * q + 3);
+        }
+    } else if (ew < a.nnz) {
+        for (int j = 0; j < (int)(a.nnz - ew); ++j) word |= (uint32_t)arc_kept(a.col_enc[ew + j], a.bkeep) << j;
+    }
+    s_word[threadIdx.x] = word;
+    const int wex = block_excl_scan(__popc(word), s_warp, &s_total);
+    s_wex[threadIdx.x] = wex;
+    // rows whose first arc lies in this tile (the last tile also takes the rows starting at nnz)
+    if (threadIdx.x == 0) {
+        int64_t lo = 0, hi = a.n_in + 1;                 // first r with row_ptr[r] >= e0
+        while (lo < hi) { const int64_t md = (lo + hi) >> 1; if (a.row_ptr[md] < e0) lo = md + 1; else hi = md; }
+        s_rlo = lo;
+        if (t == a.ntiles - 1) {
+            s_rhi = a.n_in + 1;
+        } else {
+            hi = a.n_in + 1;
+            while (lo < hi) { const int64_t md = (lo + hi) >> 1; if (a.row_ptr[md] < e1) lo = md + 1; else hi = md; }
+            s_rhi = lo;
+        }
+    }
+    const int64_t excl = lookback(a.state, a.gen, t, s_total, &s_excl);   // (its barrier also publishes s_word / s_rlo)
+    // warp-cooperative order-preserving scatter of the warp's 32 words: lane j takes arc 32k + j (coalesced)
+    const int64_t ewarp = e0 + (int64_t)wid * 1024;
+    for (int k = 0; k < 32; ++k) {
+        const uint32_t wk = s_word[wid * 32 + k];
+        if (!((wk >> lane) & 1u)) continue;
+        const int32_t v = a.col_enc[ewarp + 32 * k + lane];
+        a.out_col[excl + s_wex[wid * 32 + k] + __popc(wk & ((1u << lane) - 1u))] =
+            v >= 0 ? v : (int32_t)a.n_in + a.slot_of_b[-v - 1];
+    }
+    // induced row pointers: kept arcs before the row's first static arc
+    for (int64_t r = s_rlo + threadIdx.x; r < s_rhi; r += blockDim.x) {
+        const int64_t e = a.row_ptr[r];
+        int64_t kb;
+        if (e >= e1) {
+            kb = s_total;
+        } else {
+            const int w = (int)((e - e0) >> 5), b = (int)(e & 31);
+            kb = s_wex[w] + __popc(s_word[w] & ((1u << b) - 1u));
+        }
+        a.out_ptr[r] = excl + kb;
+    }
+    if (t == a.ntiles - 1 && threadIdx.x == 0) *a.total = excl + s_total;
+}
+
+struct SegArgs {
+    // forward chain: rows of the induced CSR
+    const int64_t* ind_ptr; int64_t n_in; Seg* fsegs; int64_t* fsplit; int64_t ntiles_f;
+    // backward chain: halo slots -> their boundary rows (transposed arcs after the static A_II part)
+    const int64_t* seg_pos; int m; const int32_t* U_b; const int64_t* br_ptr; int64_t cap; int64_t seg_base;
+    int64_t e_base; Seg* bsegs; int64_t* bsplit; int64_t ntiles_b;
+    int64_t* tot;                       // [1] fwd segments, [2] bwd halo segments, [3] bwd splits, [4] fwd splits
+    int32_t seg_long;
+    uint64_t* state_f; uint64_t* state_b; unsigned* ctr_f; unsigned* ctr_b; uint32_t gen;
+};
+
+__global__ void __launch_bounds__(kTile) k_segs_fused(const SegArgs a) {
+    __shared__ int64_t s_tile, s_excl;
+    __shared__ int s_warp[32], s_total;
+    const bool fwd = blockIdx.x < a.ntiles_f;
+    const int64_t t = next_tile(fwd ? a.ctr_f : a.ctr_b, fwd ? a.ntiles_f : a.ntiles_b, &s_tile);
+    const int64_t r = t * kTile + threadIdx.x;
+    int ns = 0;
+    int64_t b0 = 0, b1 = 0;
+    int32_t row = 0;
+    if (fwd) {
+        if (r < a.n_in) {
+            b0 = a.ind_ptr[r];
+            b1 = a.ind_ptr[r + 1];
+            ns = seg_count(b1 - b0, a.seg_long);
+            row = (int32_t)r;
+        }
+    } else {
+        const int64_t n_halo = a.seg_pos[a.m] - a.seg_pos[0];
+        if (r < n_halo) {
+            const int32_t b = a.U_b[r];
+            b0 = a.e_base + a.br_ptr[b];
+            b1 = a.e_base + a.br_ptr[b + 1];
+            ns = seg_count(b1 - b0, a.seg_long);
+            row = (int32_t)(a.n_in + r);
+        }
+    }
+    const int ex = block_excl_scan(ns, s_warp, &s_total);
+    const int64_t excl = lookback(fwd ? a.state_f : a.state_b, a.gen, t, s_total, &s_excl);
+    if (ns > 0) {
+        const int64_t s0 = (fwd ? 0 : a.seg_base) + excl + ex;
+        Seg* out = fwd ? a.fsegs : a.bsegs;
+        if (ns > 1) {
+            int64_t* cnt = fwd ? a.tot + 4 : a.tot + 3;
+            (fwd ? a.fsplit : a.bsplit)[atomicAdd(reinterpret_cast<unsigned long long*>(cnt), 1ull)] = s0;
+        }
+        const int64_t L = seg_len(b1 - b0, a.seg_long);
+        for (int k = 0; k < ns; ++k) {
+            Seg sg;
+            sg.row = row;
+            sg.nseg = ns;
+            sg.e0 = b0 + k * L;
+            sg.e1 = min(b1, sg.e0 + L);
+            sg.first = s0;
+            out[s0 + k] = sg;
+        }
+    }
+    if (threadIdx.x == 0 && t == (fwd ? a.ntiles_f : a.ntiles_b) - 1) a.tot[fwd ? 1 : 2] = excl + s_total;
+}
+
+}  // namespace
+
+void launch_sample_fused(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
+    const int m = c.cfg.world;
+    int64_t* tot = c.d_seg_pos + 2 * m + 1;
+    const int64_t n = c.n_cand;
+    const int64_t nt = (n + kTile - 1) / kTile;
+    if (nt == 0) {   // nothing to draw: every offset 0, split counters cleared
+        BNS_CUDA(cudaMemsetAsync(c.d_seg_pos, 0, (2 * m + 1 + 8) * sizeof(int64_t), c.stream));
+        return;
+    }
+    SampleArgs a{};
+    a.gid = c.d_cand_gid; a.key = c.d_cand_key; a.payload = c.d_cand_payload; a.n = n; a.n_bd = c.plan.n_bd;
+    a.T = T; a.e_lo = (uint32_t)epoch; a.e_hi = (uint32_t)(epoch >> 32); a.s_lo = (uint32_t)seed;
+    a.s_hi = (uint32_t)(seed >> 32);
+    a.cand_seg = c.d_cand_seg; a.nseg = 2 * m + 1;
+    a.flags = c.d_flags; a.bkeep = c.d_bkeep; a.out = c.d_cand_out; a.slot_of_b = c.d_slot_of_b;
+    a.seg_pos = c.d_seg_pos;
+    a.zero = tot + 3; a.nzero = 2;
+    a.state = c.d_lb_state; a.ctr = c.d_lb_ctr; a.gen = ++c.lb_gen; a.ntiles = nt;
+    k_sample_fused<<<(unsigned)nt, kTile, 0, c.stream>>>(a);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+void launch_induce_fused(Ctx& c) {
+    const int m = c.cfg.world;
+    int64_t* tot = c.d_seg_pos + 2 * m + 1;
+    const int64_t nnz = c.nnz_i;
+    const int64_t nt = (nnz + kEdgeThreads * 32 - 1) / (kEdgeThreads * 32);
+    if (nt == 0) {
+        BNS_CUDA(cudaMemsetAsync(c.d_ind_ptr, 0, (c.plan.n_in + 1) * sizeof(int64_t), c.stream));
+        BNS_CUDA(cudaMemsetAsync(tot, 0, sizeof(int64_t), c.stream));
+        return;
+    }
+    InduceArgs a{};
+    a.col_enc = c.d_col_enc; a.nnz = nnz; a.bkeep = c.d_bkeep; a.slot_of_b = c.d_slot_of_b; a.n_in = c.plan.n_in;
+    a.row_ptr = c.d_row_ptr; a.out_col = c.d_ind_col; a.out_ptr = c.d_ind_ptr; a.total = tot;
+    a.state = c.d_lb_state + c.lb_off_induce; a.ctr = c.d_lb_ctr + 1; a.gen = ++c.lb_gen; a.ntiles = nt;
+    k_induce_fused<<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+void launch_segments_fused(Ctx& c, bool fwd) {
+    const int m = c.cfg.world;
+    int64_t* tot = c.d_seg_pos + 2 * m + 1;
+    SegArgs a{};
+    a.ind_ptr = c.d_ind_ptr; a.n_in = c.plan.n_in; a.fsegs = c.d_seg_fwd; a.fsplit = c.d_split_fwd;
+    a.ntiles_f = fwd ? (c.plan.n_in + kTile - 1) / kTile : 0;
+    a.seg_pos = c.d_seg_pos; a.m = m; a.U_b = c.d_cand_out; a.br_ptr = c.d_br_ptr; a.cap = c.plan.n_bd;
+    a.seg_base = c.n_seg_bwd_inner; a.e_base = c.ii_nnz; a.bsegs = c.d_seg_bwd;
+    a.bsplit = c.d_split_bwd + c.n_split_bwd_inner;
+    a.ntiles_b = (c.plan.n_bd + kTile - 1) / kTile;
+    a.tot = tot; a.seg_long = c.seg_long;
+    a.state_f = c.d_lb_state + c.lb_off_segf; a.state_b = c.d_lb_state + c.lb_off_segb;
+    a.ctr_f = c.d_lb_ctr + 2; a.ctr_b = c.d_lb_ctr + 3; a.gen = ++c.lb_gen;
+    if (a.ntiles_b == 0) BNS_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(int64_t), c.stream));
+    if (fwd && a.ntiles_f == 0) BNS_CUDA(cudaMemsetAsync(tot + 1, 0, sizeof(int64_t), c.stream));
+    const int64_t grid = a.ntiles_f + a.ntiles_b;
+    if (grid == 0) return;
+    k_segs_fused<<<(unsigned)grid, kTile, 0, c.stream>>>(a);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+}  // namespace bns

@@ -5,13 +5,15 @@
 
 namespace bns {
 
-// a1 + a2: Philox Bernoulli draw over all candidates and order-preserving compaction (sample.cu)
-void launch_sample(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch);
-// a3: induced subgraph over V_i ∪ U_i + forward segments; backward (transposed) halo segments (sample.cu)
-void launch_induce(Ctx& c, uint64_t T = 0, uint64_t seed = 0, uint64_t epoch = 0);   // T, seed, epoch: edge samplers
-void launch_bwd_segments(Ctx& c);
-// f3 edge samplers: candidate flags from the arc draws (replaces the node draw of launch_sample), and the sampled
-// transposed CSR + backward segments (replaces launch_bwd_segments)
+// a1 + a2: Philox Bernoulli draw, order-preserving compaction, boundary keep bitmask (induce.cu, one pass)
+void launch_sample_fused(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch);
+// a3: induced subgraph over V_i ∪ U_i (induce.cu, one pass); SpMM segments of the induced rows (fwd) and of the
+// sampled halo rows (transposed), one launch
+void launch_induce_fused(Ctx& c);
+void launch_segments_fused(Ctx& c, bool fwd);
+// f3 edge samplers (sample.cu): candidate flags from the arc draws, the induced forward CSR + its segments, and the
+// sampled transposed CSR + backward segments
+void launch_induce_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch);
 void launch_sample_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch);
 void launch_induce_bwd_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch);
 // static segments for a static CSR (setup)

@@ -1,5 +1,7 @@
 // sample.cu -- a1 sample, a2 compact, a3 induce (+ SpMM work segments).
 //
+// The BNS draw itself (a1-a3 for BNS) runs as three single-pass kernels in induce.cu; this file keeps the scan
+// helpers, the shared compaction scatter and the f3 edge-sampler passes.
 // a1  Alg.1 l.4: every candidate is one independent Bernoulli(p) draw (R5, R6).  The
 //     candidates of rank i are (recv side) every u in B_i keyed by i, and (send side) every u in D_{i->j} keyed by
 //     j -- i recomputes j's draw instead of receiving the broadcast U_j (Alg.1 l.6-7, R27).
@@ -14,37 +16,7 @@
 
 namespace bns {
 
-// Philox4x32-10 (Salmon et al. SC'11) -- the device copy; the oracle has its own.
-__device__ __forceinline__ uint32_t philox_x(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
-                                             uint32_t k1) {
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
-        uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-    }
-    return c0;
-}
-
 constexpr int kSampleBlock = 1024;
-
-__global__ void __launch_bounds__(kSampleBlock) k_sample_count(const int32_t* __restrict__ gid,
-                                                               const int32_t* __restrict__ key, int64_t n,
-                                                               uint64_t T, uint32_t e_lo, uint32_t e_hi,
-                                                               uint32_t s_lo, uint32_t s_hi,
-                                                               uint8_t* __restrict__ flags, int32_t* __restrict__ blk) {
-    int64_t i = (int64_t)blockIdx.x * kSampleBlock + threadIdx.x;
-    int keep = 0;
-    if (i < n) {
-        uint32_t r = philox_x((uint32_t)gid[i], (uint32_t)key[i], e_lo, e_hi, s_lo, s_hi);
-        keep = ((uint64_t)r < T) ? 1 : 0;
-        flags[i] = (uint8_t)keep;
-    }
-    int cnt = __syncthreads_count(keep);
-    if (threadIdx.x == 0) blk[blockIdx.x] = cnt;
-}
 
 // Single-block exclusive scan of n int32 (n arbitrary) -> int64 out[0..n], out[n] = total; optional extra total.
 __global__ void __launch_bounds__(1024) k_scan_top(const int32_t* __restrict__ in, int64_t* __restrict__ out,
@@ -182,84 +154,12 @@ __global__ void k_seg_tail(const int64_t* __restrict__ cand_seg, int nseg, int64
     if (k < nseg && cand_seg[k] >= n) seg_pos[k] = boff[nb];
 }
 
-void launch_sample(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
-    const int m = c.cfg.world;
-    int64_t n = c.n_cand;
-    int64_t nb = (n + kSampleBlock - 1) / kSampleBlock;
-    int64_t* boff = c.d_scan_tmp;
-    if (nb > 0) {
-        k_sample_count<<<(unsigned)nb, kSampleBlock, 0, c.stream>>>(
-            c.d_cand_gid, c.d_cand_key, n, T, (uint32_t)epoch, (uint32_t)(epoch >> 32), (uint32_t)seed,
-            (uint32_t)(seed >> 32), c.d_flags, c.d_blk);
-        k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_blk, boff, nb, nullptr);
-        k_sample_scatter<<<(unsigned)nb, kSampleBlock, 0, c.stream>>>(c.d_flags, n, c.plan.n_bd, boff,
-                                                                      c.d_cand_payload, c.d_cand_seg, 2 * m + 1,
-                                                                      c.d_cand_out, c.d_slot_of_b, c.d_seg_pos);
-        c.kernels += 3;
-    } else {
-        BNS_CUDA(cudaMemsetAsync(boff, 0, sizeof(int64_t), c.stream));
-    }
-    k_seg_tail<<<1, 128, 0, c.stream>>>(c.d_cand_seg, 2 * m + 1, n, boff, nb, c.d_seg_pos);
-    c.kernels += 1;
-    BNS_CHECK_LAUNCH();
-}
-
 // ---------------------------------------------------------------------------------------------
 // a3 induce, edge-parallel (balanced over nnz, so hub rows cost no more than their edges):
 //   K1 keep bit of every static edge (one 32-edge word per thread) + per-1024-edge counts, K2 scan of the counts,
 //   K3 order-preserving scatter of the kept (remapped) columns, K4 row pointers from the bit prefix + segment
 //   counts per row, scan, K5 segment list.
 // ---------------------------------------------------------------------------------------------
-// keep bit of every boundary node (bit b of bkeep = keep(B_i[b], i)) packed from the draw's byte flags: the induce
-// pass then tests boundary columns against a |B_i| / 8-byte bitmask that stays in L1 (20 KB on the Reddit shape at
-// m = 8) instead of a 4-byte-per-node slot array
-__global__ void k_keep_bits(const uint8_t* __restrict__ flags, int64_t n, uint32_t* __restrict__ bkeep) {
-    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t e0 = w << 5;
-    if (e0 >= n) return;
-    uint32_t word = 0;
-    for (int j = 0; j < 32 && e0 + j < n; ++j) word |= (uint32_t)(flags[e0 + j] != 0) << j;
-    bkeep[w] = word;
-}
-
-__device__ __forceinline__ bool edge_kept_bits(int32_t x, const uint32_t* __restrict__ bkeep) {
-    if (x >= 0) return true;
-    const uint32_t b = (uint32_t)(-x - 1);
-    return (__ldg(bkeep + (b >> 5)) >> (b & 31)) & 1u;
-}
-
-// Word-per-thread versions (same bits / per-1024-edge count layout): thread t owns edges [32t, 32t + 32) and builds
-// their keep word from eight 16-byte column loads; a warp covers one 1024-edge block, so the block counts and the
-// in-block prefix are warp shuffles (no shared memory, no block barrier).
-__global__ void __launch_bounds__(256) k_induce_flags_w(const int32_t* __restrict__ col_enc, int64_t nnz,
-                                                        const uint32_t* __restrict__ bkeep,
-                                                        uint32_t* __restrict__ bits, int32_t* __restrict__ blk) {
-    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nw = (nnz + 31) >> 5;
-    uint32_t word = 0;
-    if (w < nw) {
-        const int64_t e0 = w << 5;
-        if (e0 + 32 <= nnz) {
-            const int4* p = reinterpret_cast<const int4*>(col_enc + e0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int4 v = __ldg(p + q);
-                word |= (uint32_t)edge_kept_bits(v.x, bkeep) << (4 * q);
-                word |= (uint32_t)edge_kept_bits(v.y, bkeep) << (4 * q + 1);
-                word |= (uint32_t)edge_kept_bits(v.z, bkeep) << (4 * q + 2);
-                word |= (uint32_t)edge_kept_bits(v.w, bkeep) << (4 * q + 3);
-            }
-        } else {
-            for (int j = 0; j < (int)(nnz - e0); ++j) word |= (uint32_t)edge_kept_bits(col_enc[e0 + j], bkeep) << j;
-        }
-        bits[w] = word;
-    }
-    int cnt = __popc(word);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if ((threadIdx.x & 31) == 0 && (w >> 5) < ((nnz + 1023) >> 10)) blk[w >> 5] = cnt;
-}
-
 __global__ void __launch_bounds__(256) k_induce_scatter_w(const int32_t* __restrict__ col, int64_t nnz,
                                                           const int32_t* __restrict__ slot_of_b,
                                                           const uint32_t* __restrict__ bits,
@@ -289,6 +189,8 @@ __global__ void __launch_bounds__(256) k_induce_scatter_w(const int32_t* __restr
         out_col[base + ek + __popc(wk & ((1u << lane) - 1u))] = v >= 0 ? v : (int32_t)n_in + slot_of_b[-v - 1];
     }
 }
+
+void launch_induce_flags_edge(Ctx& c, int64_t nb, uint64_t T, uint64_t seed, uint64_t epoch);
 
 // number of kept edges before static edge position e
 __device__ __forceinline__ int64_t kept_before(int64_t e, const uint32_t* __restrict__ bits,
@@ -336,9 +238,9 @@ __global__ void k_induce_segs(const int64_t* __restrict__ out_ptr, int64_t n_in,
     }
 }
 
-void launch_induce_flags_edge(Ctx& c, int64_t nb, uint64_t T, uint64_t seed, uint64_t epoch);
-
-void launch_induce(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
+// a3 for the edge samplers (f3): arc keep bits from the arc draws, scan, order-preserving scatter, row pointers,
+// segment counts, scan, segment list (the BNS draw runs the single-pass kernels of induce.cu instead)
+void launch_induce_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     const int64_t n_in = c.plan.n_in;
     const int64_t nnz = c.nnz_i;
     const int m = c.cfg.world;
@@ -346,15 +248,7 @@ void launch_induce(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     const int64_t nb = (nnz + 1023) / 1024;
     if (nb > 0) {
         const unsigned wb = (unsigned)((((nnz + 31) >> 5) + 255) / 256);
-        if (c.sampler == BNS_SAMPLER_BNS) {
-            const int64_t nbw = (c.plan.n_bd + 31) / 32;
-            if (nbw > 0) {
-                k_keep_bits<<<(unsigned)((nbw + 255) / 256), 256, 0, c.stream>>>(c.d_flags, c.plan.n_bd, c.d_bkeep);
-                c.kernels += 1;
-            }
-            k_induce_flags_w<<<wb, 256, 0, c.stream>>>(c.d_col_enc, nnz, c.d_bkeep, c.d_ebits, c.d_eblk);
-        } else
-            launch_induce_flags_edge(c, nb, T, seed, epoch);
+        launch_induce_flags_edge(c, nb, T, seed, epoch);
         k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_eblk, c.d_eboff, nb, tot + 0);
         k_induce_scatter_w<<<wb, 256, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff, n_in,
                                                      c.d_ind_col);
@@ -375,65 +269,6 @@ void launch_induce(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     BNS_CHECK_LAUNCH();
 }
 
-// backward (transposed) segments of the halo rows: halo slot s <- boundary b = U_b[s], inner neighbours of b
-__global__ void k_bwd_count(const int64_t* __restrict__ seg_pos, int m, const int32_t* __restrict__ U_b,
-                            const int64_t* __restrict__ br_ptr, int64_t cap, int32_t* __restrict__ nseg, int32_t seg_long) {
-    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= cap) return;
-    int64_t n_halo = seg_pos[m] - seg_pos[0];
-    int v = 0;
-    if (s < n_halo) {
-        int32_t b = U_b[s];
-        int64_t len = br_ptr[b + 1] - br_ptr[b];
-        v = seg_count(len, seg_long);
-    }
-    nseg[s] = v;
-}
-
-__global__ void k_bwd_write(const int64_t* __restrict__ seg_pos, int m, const int32_t* __restrict__ U_b,
-                            const int64_t* __restrict__ br_ptr, int64_t cap, const int64_t* __restrict__ soff,
-                            int64_t seg_base, int64_t e_base, int64_t n_in, Seg* __restrict__ segs,
-                            int64_t* __restrict__ split, int64_t* __restrict__ n_split, int32_t seg_long) {
-    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= cap) return;
-    int64_t n_halo = seg_pos[m] - seg_pos[0];
-    if (s >= n_halo) return;
-    int32_t b = U_b[s];
-    int64_t e_lo = e_base + br_ptr[b], e_hi = e_base + br_ptr[b + 1];
-    int64_t s0 = seg_base + soff[s], ns = soff[s + 1] - soff[s];
-    if (ns > 1) push_split(split, n_split, s0);
-    for (int64_t k = 0; k < ns; ++k) {
-        Seg sg;
-        sg.row = (int32_t)(n_in + s);
-        sg.nseg = (int32_t)ns;
-        sg.e0 = e_lo + k * seg_len(e_hi - e_lo, seg_long);
-        sg.e1 = min(e_hi, sg.e0 + seg_len(e_hi - e_lo, seg_long));
-        sg.first = s0;
-        segs[s0 + k] = sg;
-    }
-}
-
-void launch_bwd_segments(Ctx& c) {
-    const int m = c.cfg.world;
-    const int64_t cap = c.plan.n_bd;
-    int64_t* tot = c.d_seg_pos + 2 * m + 1;
-    BNS_CUDA(cudaMemsetAsync(tot + 3, 0, sizeof(int64_t), c.stream));
-    if (cap == 0) {
-        BNS_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(int64_t), c.stream));
-        return;
-    }
-    unsigned grid = (unsigned)((cap + 255) / 256);
-    k_bwd_count<<<grid, 256, 0, c.stream>>>(c.d_seg_pos, m, c.d_cand_out, c.d_br_ptr, cap, c.d_row_nseg, c.seg_long);
-    c.kernels += 1;
-    BNS_CHECK_LAUNCH();
-    scan_i32(c, c.d_row_nseg, c.d_row_soff, cap, tot + 2);
-    k_bwd_write<<<grid, 256, 0, c.stream>>>(c.d_seg_pos, m, c.d_cand_out, c.d_br_ptr, cap, c.d_row_soff,
-                                            c.n_seg_bwd_inner, c.ii_nnz, c.plan.n_in, c.d_seg_bwd,
-                                            c.d_split_bwd + c.n_split_bwd_inner, tot + 3, c.seg_long);
-    c.kernels += 1;
-    BNS_CHECK_LAUNCH();
-}
-
 // ---------------------------------------------------------------------------------------------
 // f3 edge samplers: BES keeps each cross-partition arc with probability q, DropEdge every arc.
 // R40 arc draw: keep(v <- u) = Philox4x32-10(ctr = {v, u, e_lo, e_hi}, key = {s_lo ^ 0xED6E, s_hi}).x < T(q).
@@ -442,7 +277,7 @@ struct ArcKey {
     uint64_t T;
     uint32_t e_lo, e_hi, k0, k1;
     __device__ __forceinline__ bool keep(int32_t v, int32_t u) const {
-        return (uint64_t)philox_x((uint32_t)v, (uint32_t)u, e_lo, e_hi, k0, k1) < T;
+        return (uint64_t)philox4((uint32_t)v, (uint32_t)u, e_lo, e_hi, k0, k1).x < T;
     }
 };
 
@@ -452,7 +287,7 @@ inline ArcKey arc_key(uint64_t T, uint64_t seed, uint64_t epoch) {
 
 // a1 for the edge samplers: receive candidate b in B_i is communicated iff one of its arcs into V_i survives;
 // send candidate (u, peer j) iff one of u's arcs into V_j survives (j's draw recomputed, R27).  Same flags/block
-// count contract as k_sample_count, so the a2 compaction is shared.
+// count contract the compaction scatter (k_sample_scatter) expects.
 __global__ void __launch_bounds__(kSampleBlock) k_edge_cand(int64_t n_bd, int64_t n, const int32_t* __restrict__ gid,
                                                             const int32_t* __restrict__ key,
                                                             const int32_t* __restrict__ payload,

@@ -110,10 +110,11 @@ def bf16_round(a):
     return torch.tensor(np.asarray(a, np.float32)).bfloat16().double().numpy()
 
 
-def layer_local(op, snap, Ws, G, L, dims, layer, tol, tag, device="cpu"):
-    """bf16: every layer against float64 recomputed from its OWN GPU inputs: the H^(l-1) it read, the dH^l it received
-    and its own ReLU mask (snap), the bf16 weight operands (R19) and the oracle's sampled operator (op).  torch float64
-    (sparse CSR x dense; cuSPARSE when device = cuda).  Returns the margins; asserts <= tol."""
+def layer_local(op, snap, Ws, G, L, dims, layer, tol, tag, device="cpu", bf16=True):
+    """Every layer against float64 recomputed from its OWN GPU inputs: the H^(l-1) it read, the dH^l it received and
+    its own ReLU mask (snap), the weight operands (bf16-rounded in bf16 mode, R19) and the oracle's sampled operator
+    (op) -- no ReLU flip can enter.  torch float64 (sparse CSR x dense; cuSPARSE when device = cuda).  Returns the
+    margins; asserts <= tol."""
     import torch
     rows, cols, vals, N = op
     dev = torch.device(device)
@@ -127,7 +128,7 @@ def layer_local(op, snap, Ws, G, L, dims, layer, tol, tag, device="cpu"):
     out = {}
     for l in range(1, L + 1):
         din = dims[l - 1]
-        Wb = T(bf16_round(Ws[l - 1]))
+        Wb = T(bf16_round(Ws[l - 1]) if bf16 else Ws[l - 1])   # the GEMM operand (R19: bf16 in bf16 mode)
         X = T(snap[("H", l - 1)])
         AX = A @ X
         pre = AX @ Wb[:din] + X @ Wb[din:] if sage else AX @ Wb
@@ -190,10 +191,10 @@ def check_epoch(gpu, orc_out, L, prec, dims, tf, layer, N, tag, labels, local_fn
         flips.append(n)
         if n == 0:
             continue
-        assert prec == bns.BNS_BF16, (tag, "ReLU flips in fp32", l, n)
         scale = max(np.abs(o).max(), 1e-30)
-        assert n <= FLIP_SHARE_MAX * o.size, (tag, "too many ReLU flips", l, n, o.size)
-        assert np.abs(g[flip]).max() <= scale / 64 and np.abs(o[flip]).max() <= scale / 64, (tag, "flip not ambiguous", l)
+        amb = scale / 64 if prec == bns.BNS_BF16 else tol * scale   # bf16: within its rounding; fp32: within 1e-5
+        assert n <= (FLIP_SHARE_MAX if prec == bns.BNS_BF16 else 1e-6) * o.size, (tag, "too many ReLU flips", l, n)
+        assert np.abs(g[flip]).max() <= amb and np.abs(o[flip]).max() <= amb, (tag, "flip not ambiguous", l, prec)
         F = l
     margins = {"loss": abs(loss - lo) / max(abs(lo), 1e-12)}
     for l in range(1, L + 1):
@@ -212,9 +213,10 @@ def check_epoch(gpu, orc_out, L, prec, dims, tf, layer, N, tag, labels, local_fn
             assert e <= max(tol * 0.1, 1e-6), (tag, "W", l, e)
     rec = {"tag": tag, "prec": int(prec), "layer": layer, "F": F, "flips": flips,
            "units": [int(N * dims[l]) for l in range(1, L)], "vs_float64": margins}
+    if local_fn is not None:
+        rec["layer_local"] = local_fn(G)
+    assert F == 0 or "layer_local" in rec or layer == bns.BNS_LAYER_GAT, (tag, "flips need the layer-local check")
     if prec == bns.BNS_BF16:
-        if local_fn is not None:
-            rec["layer_local"] = local_fn(G)
         BF16_REPORT.append(rec)
     return rec
 
@@ -228,7 +230,8 @@ def compare_epoch(run, orc, L, Ws, Wd, lr, prec, tag="", host=False, local=True)
     local_fn = None
     if local and run.layer != bns.BNS_LAYER_GAT and run.last_draw is not None:
         op = sampled_operator(orc, run.m, run.layer, *run.last_draw)
-        local_fn = lambda G_: layer_local(op, snap, Ws, G_, L, run.dims, run.layer, TOL[prec], tag)  # noqa: E731
+        local_fn = lambda G_: layer_local(op, snap, Ws, G_, L, run.dims, run.layer, TOL[prec], tag,  # noqa: E731
+                                          bf16=prec == bns.BNS_BF16)
     check_epoch((loss, acc, G, Wn, snap), (lo, ao, Go, Wd, OracleView(orc)), L, prec, run.dims, run.tf, run.layer,
                 run.N, tag, orc.labels, local_fn)
     return [w.astype(np.float32) for w in Wn]

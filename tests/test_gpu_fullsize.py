@@ -195,11 +195,12 @@ def gpu_epochs(indptr, indices, part, m, dims, layer, prec, X, y, p, epochs, lr,
             Ws = [w.copy() for w in W]
             loss, acc, G, Wn = run.epoch(Ws, lr)
             snap = snapshot(run, L)
-            local = None
-            if prec == bns.BNS_BF16:
-                light.sample(p, SEED, e)
-                op = sampled_operator(light, m, layer, bns.BNS_SAMPLER_BNS, p)
-                local = layer_local(op, snap, Ws, G, L, dims, layer, 2e-2, f"m{m} e{e} layer-local", device="cuda")
+            light.sample(p, SEED, e)
+            op = sampled_operator(light, m, layer, bns.BNS_SAMPLER_BNS, p)
+            bf = prec == bns.BNS_BF16
+            local = layer_local(op, snap, Ws, G, L, dims, layer, 2e-2 if bf else 1e-5,
+                                f"m{m} prec{prec} e{e} layer-local", device="cuda", bf16=bf)
+            del op
             out.append(((loss, acc, G, Wn, snap), local))
             W = [w.astype(np.float32) for w in Wn]
         return out, run.tf
@@ -241,7 +242,7 @@ def test_north_star_full_size(reddit):
                     (g, local), tf = gpu[prec][0][e], gpu[prec][1]
                     rec = check_epoch(g, orc_out, L, prec, dims, tf, layer, sh.N,
                                       f"{name} m={m} prec={prec} epoch {e}", y,
-                                      (lambda G_, lo=local: lo) if local is not None else None)
+                                      lambda G_, lo=local: lo)
                     report["records"].append(rec)
                 th.go[e].set()
             report["oracle_seconds"][name] = th.secs
