@@ -2,6 +2,7 @@
 #   oracle/liboracle.so                           CPU oracle (test infrastructure only)
 #   paper_2203_10983_b200/inputs/libbnsgen.so      seeded input generators (setup)
 #   paper_2203_10983_b200/libbns.so                the product: C-ABI + sm_100a CUDA kernels + NCCL
+#   build/gather_ceiling                           measurement tool: gather ceiling of the SpMM access pattern
 PY        ?= python
 NVCC      ?= /usr/local/cuda/bin/nvcc
 SITE      := $(shell $(PY) -c "import sysconfig; print(sysconfig.get_paths()['purelib'])")
@@ -13,7 +14,12 @@ CSRC      := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cpp)
 CHDR      := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/bns.h
 OBJDIR    := build
 
-all: oracle/liboracle.so $(PKG)/inputs/libbnsgen.so $(PKG)/libbns.so
+all: oracle/liboracle.so $(PKG)/inputs/libbnsgen.so $(PKG)/libbns.so build/gather_ceiling
+
+# measurement tool (not the product): the SpMM access pattern's gather ceiling (scripts/gather_ceiling.cu)
+build/gather_ceiling: scripts/gather_ceiling.cu
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O3 -lineinfo -o $@ $<
 
 oracle/liboracle.so: oracle/bns_oracle.cpp
 	g++ -O3 -mavx2 -mfma -std=c++17 -fPIC -shared -o $@ $<

@@ -8,7 +8,10 @@
 // the loads cannot be removed.  Its GB/s over (rows, width, working set, index distribution) is the roofline the
 // SpMM's algorithmic bytes are divided by in bench.py ("ceiling"), next to the HBM copy peak.
 //
-//   gather_ceiling [iters]  ->  one JSON line per case on stdout
+//   gather_ceiling [iters]                                   synthetic cases (uniform / skewed column streams)
+//   gather_ceiling iters colfile row_bytes stride_bytes name  the column stream of a real induced CSR (int32 file),
+//                                                             e.g. the Reddit-shaped R-MAT graph in CSR order
+// -> one JSON line per case on stdout
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
@@ -28,22 +31,23 @@
 
 constexpr int U = 8;
 
-// each warp owns edges [w*chunk, (w+1)*chunk); a row of nvec 16-byte vectors (nvec a power of two <= 32) is read by
-// nvec lanes, so 32 / nvec lane groups take alternate edges (the SpMM's narrow-row layout)
-__global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ src, int nvec, const int32_t* __restrict__ col,
-                                                int64_t nnz, int64_t chunk, uint4* __restrict__ sink) {
+// each warp owns edges [w*chunk, (w+1)*chunk); a row of nvec 16-byte vectors (nvec <= 32) is read by nvec lanes, so
+// 32 / nvec lane groups take alternate edges (the SpMM's narrow-row layout)
+__global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ src, int nvec, int64_t ldv,
+                                                const int32_t* __restrict__ col, int64_t nnz, int64_t chunk,
+                                                uint4* __restrict__ sink) {
     const int lane = threadIdx.x & 31;
     const int G = 32 / nvec, grp = lane / nvec, vec = lane % nvec;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t e0 = w * chunk, e1 = min(nnz, e0 + chunk);
     uint4 acc = make_uint4(0, 0, 0, 0);
-    int64_t e = e0 + grp;
+    int64_t e = grp < G ? e0 + grp : e1;   // nvec not dividing 32: the last 32 % nvec lanes idle
     for (; e + (int64_t)(U - 1) * G < e1; e += (int64_t)U * G) {
         uint4 v[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             const int32_t c = __ldg(col + e + (int64_t)k * G);
-            const uint4* p = src + (int64_t)c * nvec + vec;
+            const uint4* p = src + (int64_t)c * ldv + vec;
             asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
                          : "l"(p));
@@ -54,7 +58,7 @@ __global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ src, i
         }
     }
     for (; e < e1; e += G) {
-        const uint4 v = __ldg(src + (int64_t)col[e] * nvec + vec);
+        const uint4 v = __ldg(src + (int64_t)col[e] * ldv + vec);
         acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
     }
     if ((acc.x | acc.y | acc.z | acc.w) == 0x9E3779B9u) sink[threadIdx.x] = acc;   // practically never taken
@@ -68,6 +72,28 @@ __global__ void k_stream(const uint4* __restrict__ src, int64_t n, uint4* __rest
         acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
     }
     if ((acc.x | acc.y | acc.z | acc.w) == 0x9E3779B9u) sink[threadIdx.x] = acc;
+}
+
+static double time_gather(const uint4* src, int nvec, int64_t ldv, const int32_t* d_col, int64_t nnz, int sms,
+                          int iters, uint4* sink) {
+    // one resident wave of 8 blocks x 8 warps per SM, equal edge chunks
+    const int64_t warps = (int64_t)sms * 8 * 8;
+    const int64_t chunk = (nnz + warps - 1) / warps;
+    const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    k_gather<<<grid, 256>>>(src, nvec, ldv, d_col, nnz, chunk, sink);
+    CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(a));
+    for (int i = 0; i < iters; ++i) k_gather<<<grid, 256>>>(src, nvec, ldv, d_col, nnz, chunk, sink);
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    CK(cudaEventDestroy(a));
+    CK(cudaEventDestroy(b));
+    return ms / 1e3 / iters;
 }
 
 int main(int argc, char** argv) {
@@ -87,6 +113,33 @@ int main(int argc, char** argv) {
     };
     uint4* sink;
     CK(cudaMalloc(&sink, 4096 * sizeof(uint4)));
+    if (argc > 5) {   // file mode: a real column stream
+        FILE* f = fopen(argv[2], "rb");
+        if (!f) { fprintf(stderr, "cannot open %s\n", argv[2]); return 1; }
+        fseek(f, 0, SEEK_END);
+        const int64_t n = ftell(f) / 4;
+        fseek(f, 0, SEEK_SET);
+        std::vector<int32_t> c(n);
+        if ((int64_t)fread(c.data(), 4, n, f) != n) { fprintf(stderr, "short read\n"); return 1; }
+        fclose(f);
+        int32_t mx = 0;
+        for (int32_t x : c) mx = std::max(mx, x);
+        const int row_bytes = atoi(argv[3]), stride = atoi(argv[4]);
+        const int64_t rows = (int64_t)mx + 1, bytes = rows * stride;
+        uint4* src;
+        CK(cudaMalloc(&src, bytes));
+        CK(cudaMemset(src, 1, bytes));
+        int32_t* dc;
+        CK(cudaMalloc(&dc, n * 4));
+        CK(cudaMemcpy(dc, c.data(), n * 4, cudaMemcpyHostToDevice));
+        const double t = time_gather(src, row_bytes / 16, stride / 16, dc, n, sms, iters, sink);
+        printf("{\"case\": \"%s\", \"rows\": %lld, \"row_bytes\": %d, \"row_stride_bytes\": %d, "
+               "\"working_set_bytes\": %lld, \"l2_bytes\": %d, \"gathered_rows\": %lld, \"gather_gbs\": %.1f, "
+               "\"gather_plus_index_gbs\": %.1f, \"ms_per_launch\": %.4f}\n",
+               argv[5], (long long)rows, row_bytes, stride, (long long)(rows * row_bytes), l2, (long long)n,
+               (double)n * row_bytes / t / 1e9, (double)n * (row_bytes + 4) / t / 1e9, t * 1e3);
+        return 0;
+    }
     int32_t* d_col;
     CK(cudaMalloc(&d_col, nnz * sizeof(int32_t)));
     std::mt19937_64 rng(12345);
@@ -107,19 +160,7 @@ int main(int argc, char** argv) {
             else col[e] = (int32_t)((r >> 1) % cs.rows);
         }
         CK(cudaMemcpy(d_col, col.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
-        // one resident wave of 8 blocks x 8 warps per SM, equal chunks
-        const int64_t warps = (int64_t)sms * 8 * 8;
-        const int64_t chunk = (nnz + warps - 1) / warps;
-        const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
-        k_gather<<<grid, 256>>>(src, nvec, d_col, nnz, chunk, sink);
-        CK(cudaDeviceSynchronize());
-        CK(cudaEventRecord(a));
-        for (int i = 0; i < iters; ++i) k_gather<<<grid, 256>>>(src, nvec, d_col, nnz, chunk, sink);
-        CK(cudaEventRecord(b));
-        CK(cudaEventSynchronize(b));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, a, b));
-        const double t = ms / 1e3 / iters;
+        const double t = time_gather(src, nvec, nvec, d_col, nnz, sms, iters, sink);
         const double gathered = (double)nnz * cs.width_b, idx = (double)nnz * 4;
         k_stream<<<sms * 8, 256>>>(src, bytes / 16, sink);
         CK(cudaDeviceSynchronize());
