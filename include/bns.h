@@ -252,15 +252,16 @@ bns_status bns_set_timing(bns_ctx* ctx, int32_t on);
  * its gradients, l.12 PAPER.md:290), run in isolation by the SAME kernels bns_epoch launches -- so the tensor-core
  * GEMMs can be checked element by element at full size against a float64 product of the same operands.  No context
  * needed; all pointers are caller-owned DEVICE memory, row-major, leading dimensions in elements.
- *   precision  BNS_BF16: tcgen05 kind::f16 (bf16 operands, fp32 accumulation in TMEM).  BNS_FP32: not available
- *              (returns BNS_ERR_INVALID) -- fp32 mode runs its own GEMM.
+ *   precision  BNS_BF16: tcgen05 kind::f16 (bf16 operands, fp32 accumulation in TMEM); BNS_FP32: 3xTF32
+ *              (tcgen05 kind::tf32 on hi / lo splits of fp32 operands, fp32 accumulation) -- every operand and
+ *              output below is then fp32.
  *   kind 0  FWD     C[M x N] = [A0 | A1] · W, A0 / A1 M x K (lda; A1 may be NULL), B = Wᵀ stored [N][Kw] with each
  *                   concat half zero-padded to a multiple of 64 columns (Kw = 64⌈K/64⌉ or 2·64⌈K/64⌉), ldb = Kw;
- *                   flags bit 0 = ReLU epilogue, bit 1 = fp32 output (else bf16).
+ *                   flags bit 0 = ReLU epilogue, bit 1 = fp32 output (else the storage type).
  *   kind 1  WGRAD   C[K x N] (fp32, ldc) = A0ᵀ · B, A0 M x K (lda), B M x N (ldb) -- M (the node count) is the
  *                   reduction, split over CTAs (split-K) and reduced in a fixed order.
  *   kind 2  WGRAD2  C[2K x N] (fp32) = [A0 | A1]ᵀ · B in one launch (the GraphSAGE dW_z / dW_h pair; K % 128 == 0).
- *   kind 3  DX      C[M x N] (bf16) = A0 · Bᵀ, A0 M x K (lda), B [N][K] (ldb); columns < scale_cols multiplied by
+ *   kind 3  DX      C[M x N] (storage type) = A0 · Bᵀ, A0 M x K (lda), B [N][K] (ldb); columns < scale_cols x
  *                   rowscale[row] (rowscale may be NULL).
  * stream: cudaStream_t (NULL = legacy default).  *splits (may be NULL) receives the split-K factor used (kinds 1-2;
  * 1 otherwise).  Returns after a stream sync; errors: BNS_ERR_INVALID (shapes / kind / precision), BNS_ERR_RUNTIME. */

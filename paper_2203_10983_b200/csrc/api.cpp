@@ -374,8 +374,9 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.WT.assign(L, nullptr);
     c.wkw.assign(L, 0);
     {
+        // tensor-core GEMMs in both modes (bf16: kind::f16; fp32: 3xTF32); BNS_NO_TC=1 selects the SIMT kernels
         const char* no_tc = std::getenv("BNS_NO_TC");
-        c.use_tc = (c.prec == BNS_BF16) && !(no_tc && no_tc[0] == '1');
+        c.use_tc = !(no_tc && no_tc[0] == '1');
     }
     int64_t wmax = 0, wlog = 0;
     for (int l = 0; l < L; ++l) {
@@ -389,7 +390,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
         c.Wpad[l] = static_cast<float*>(dalloc(c, c.wrows[l] * c.wcols[l] * sizeof(float)));
         c.Wt[l] = (c.prec == BNS_BF16) ? dalloc(c, c.wrows[l] * c.wcols[l] * 2) : (void*)c.Wpad[l];
         c.wkw[l] = (c.layer == BNS_LAYER_SAGE_MEAN ? 2 : 1) * ((int64_t)(c.dp[l] + 63) / 64 * 64);
-        if (c.use_tc) c.WT[l] = dalloc(c, c.wcols[l] * c.wkw[l] * 2);
+        if (c.use_tc) c.WT[l] = dalloc(c, c.wcols[l] * c.wkw[l] * tsize(c));
     }
     // R42: transform-first SAGE layers (narrower padded output than input), unless BNS_NO_TRANSFORM_FIRST
     c.tf_mask = 0;
@@ -402,7 +403,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
                 c.tf_mask |= 1u << l;
                 tfw = std::max<int64_t>(tfw, 2 * (int64_t)c.dp[l + 1]);
                 c.Wcat[l] = dalloc(c, (size_t)c.dp[l] * 2 * c.dp[l + 1] * ts);
-                if (c.use_tc) c.WTtf[l] = dalloc(c, (size_t)2 * c.dp[l + 1] * ((c.dp[l] + 63) / 64 * 64) * 2);
+                if (c.use_tc) c.WTtf[l] = dalloc(c, (size_t)2 * c.dp[l + 1] * ((c.dp[l] + 63) / 64 * 64) * tsize(c));
             }
     if (c.layer == BNS_LAYER_GAT) {   // f4 / R45: Y buffer, per-layer attention scalars, dY
         for (int l = 0; l < L; ++l) tfw = std::max<int64_t>(tfw, c.dp[l + 1]);
@@ -1094,12 +1095,12 @@ bns_status bns_gemm(int32_t precision, int32_t kind, int64_t M, int64_t N, int64
                     int64_t scale_cols, int32_t flags, void* stream, int32_t* splits) {
     using namespace bns;
     return guard(nullptr, [&] {
-        if (precision != BNS_BF16) throw Error(BNS_ERR_INVALID, "bns_gemm: only BNS_BF16 (tcgen05) is exposed");
+        if (precision != BNS_BF16 && precision != BNS_FP32) throw Error(BNS_ERR_INVALID, "bns_gemm: bad precision");
         if (M < 0 || N <= 0 || K <= 0 || !A0 || !B || !C || kind < 0 || kind > 3)
             throw Error(BNS_ERR_INVALID, "bns_gemm: bad kind / shape / NULL operand");
         if (kind == 2 && (K % 128 != 0 || !A1)) throw Error(BNS_ERR_INVALID, "bns_gemm: WGRAD2 needs A1 and K % 128 == 0");
         Ctx c;
-        c.prec = BNS_BF16;
+        c.prec = precision;
         c.use_tc = true;
         c.stream = static_cast<cudaStream_t>(stream);
         c.splitk_cap = 0;
@@ -1108,7 +1109,7 @@ bns_status bns_gemm(int32_t precision, int32_t kind, int64_t M, int64_t N, int64
             c.splitk_cap = 148 * (kind == 2 ? 2 : 1) * K * N;
             c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
         }
-        const int64_t Kw = (K + 63) / 64 * 64;
+        const int64_t Kw = (K + 63) / 64 * 64;   // W^T concat halves are padded to 64 in both precisions
         try {
             switch (kind) {
                 case 0: gemm_fwd_tc(c, M, N, A0, K, lda, A1, A1 ? K : 0, lda, B, ldb ? ldb : (A1 ? 2 * Kw : Kw), C,

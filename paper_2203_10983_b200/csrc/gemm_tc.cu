@@ -1,4 +1,4 @@
-// gemm_tc.cu -- a7 / a9 dense update on the 5th-generation tensor cores (tcgen05, BNS_BF16 mode).
+// gemm_tc.cu -- a7 / a9 dense update on the 5th-generation tensor cores (tcgen05).
 //
 // The update φ(z_v, h_v) = σ(W · CONCAT(z_v, h_v)) is the only true contraction on the path:
 //   fwd  Pre[n_in x d_out] = [Z | H] · W              A K-major (two tensor maps, concat along K), B = W^T K-major
@@ -6,11 +6,20 @@
 //                                                     split-K over nodes, fp32 partials reduced in fixed order
 //   dX   [dZ'|dXself]      = dPre · W^T               A K-major, B = W K-major; epilogue x 1/deg_G (or rs) on dZ'
 //
-// One CTA = one 128 x BN output tile (BN <= 256), 4 warps: warp 0 lane 0 issues TMA (SWIZZLE_128B boxes of 64
-// bf16 = 128 B) into a 4-stage mbarrier ring, warp 1 lane 0 issues tcgen05.mma.cta_group::1.kind::f16
-// (M=128, N=BN, K=16, fp32 accumulator in TMEM) and releases stages with tcgen05.commit; after the last k-block
-// all 4 warps drain TMEM with tcgen05.ld.32x32b and apply the epilogue (ReLU / cast / row scale).  K tails and
-// partial M / N tiles are handled by TMA's zero fill and masked stores.
+// Two precisions, one kernel template:
+//   BNS_BF16  kind::f16 with bf16 operands (R19), 64-element (128 B) k-blocks, 4-stage ring.
+//   BNS_FP32  3xTF32 (kind::tf32): every fp32 operand tile is split in shared memory into hi = x with the low 13
+//             mantissa bits cleared (exactly representable in tf32) and lo = x - hi (exact in fp32), and the tile
+//             product is accumulated as hi·hi + hi·lo + lo·hi in fp32 TMEM -- the dropped lo·lo term and lo's own
+//             tf32 rounding are ~2^-22 relative, so the result meets the fp32 mode's 1e-5 (plain 1xTF32 would not,
+//             SURVEY §8(c) item 19).  32-element (128 B) k-blocks, 2-stage ring of [hi | lo] tiles; four more warps
+//             do the split between the TMA landing and the MMA issue.
+// Both element types use the same byte layout (128 B SWIZZLE_128B rows, 32 B per MMA k-step).
+//
+// One CTA = one 128 x BN output tile (BN <= 256): warp 0 lane 0 issues TMA into an mbarrier ring, warp 1 lane 0
+// issues tcgen05.mma.cta_group::1 (M=128, N=BN, fp32 accumulator in TMEM) and releases stages with tcgen05.commit;
+// warps 2-5 drain TMEM with tcgen05.ld.32x32b and apply the epilogue (ReLU / cast / row scale); fp32: warps 6-9 split
+// the operands.  K tails and partial M / N tiles are handled by TMA's zero fill and masked stores.
 #include <cuda.h>
 #include <cstdint>
 
@@ -20,13 +29,21 @@
 
 namespace bns {
 
-constexpr int TC_BM = 128, TC_BK = 64, TC_STAGES = 4;
-constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;             // 16 KB
-constexpr int TC_B_BYTES = 256 * TC_BK * 2;               // 32 KB (max BN)
-constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
-constexpr int TC_SMEM = TC_STAGES * TC_STAGE_BYTES + 1024 + 256;
+constexpr int TC_BM = 128;
+constexpr int TC_ROW_BYTES = 128;                          // one SWIZZLE_128B row: 64 bf16 or 32 fp32 k-elements
+constexpr int TC_A_BYTES = TC_BM * TC_ROW_BYTES;           // 16 KB
+constexpr int TC_B_BYTES = 256 * TC_ROW_BYTES;             // 32 KB (max BN)
+constexpr int TC_HALF_BYTES = TC_A_BYTES + TC_B_BYTES;     // one [A | B] operand pair
+template <bool F32> struct TcCfg {
+    static constexpr int STAGES = F32 ? 2 : 4;
+    static constexpr int STAGE_BYTES = (F32 ? 2 : 1) * TC_HALF_BYTES;   // fp32: [A hi | B hi | A lo | B lo]
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int THREADS = F32 ? 320 : 192;
+    static constexpr int KE = F32 ? 32 : 64;               // k-elements per block (one 128 B row)
+    static constexpr int MNE = F32 ? 32 : 64;              // MN-elements per 128 B row (MN-major operands)
+};
 
-enum TcEpi { EPI_BF16 = 0, EPI_F32 = 1, EPI_BF16_ROWSCALE = 2 };
+enum TcEpi { EPI_BF16 = 0, EPI_F32 = 1, EPI_BF16_ROWSCALE = 2, EPI_F32_ROWSCALE = 3 };
 
 struct TcArgs {
     int64_t M, N;
@@ -81,26 +98,36 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t 
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
 
 // Persistent, warp-specialized: grid = min(#tiles, #SMs); tile t = (m-tile, n-tile, split) visited in
-// blockIdx-strided order.  warp 0 lane 0: TMA producer over a 4-stage smem ring; warp 1 lane 0: MMA issuer into
-// one of two TMEM accumulators (2 x 256 columns), so the epilogue of tile i overlaps the MMAs of tile i+1;
-// warps 2-5: epilogue (warp w drains TMEM lanes 32*(w%4) .. +31).
-constexpr int TC_THREADS = 192;
-
-template <bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// blockIdx-strided order.  warp 0 lane 0: TMA producer over the smem ring; warp 1 lane 0: MMA issuer into one of two
+// TMEM accumulators (2 x 256 columns), so the epilogue of tile i overlaps the MMAs of tile i+1; warps 2-5: epilogue
+// (warp w drains TMEM lanes 32*(w%4) .. +31); fp32 (3xTF32): warps 6-9 split each landed stage into hi / lo.
+template <bool A_MN, bool B_MN, bool F32>
+__global__ void __launch_bounds__(TcCfg<F32>::THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
           const __grid_constant__ CUtensorMap mapB, const TcArgs args) {
+    using Cfg = TcCfg<F32>;
+    constexpr int STAGES = Cfg::STAGES, STAGE_BYTES = Cfg::STAGE_BYTES, KE = Cfg::KE, MNE = Cfg::MNE;
+    constexpr int BOX_BYTES = KE * TC_ROW_BYTES;          // one MN-major box {MNE, KE}: 8 KB bf16, 4 KB fp32
+    constexpr int KSTEP_MN = (F32 ? 8 : 16) * TC_ROW_BYTES;   // MN-major: k-rows per MMA k-step x 128 B
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
-    uint64_t* empty = full + TC_STAGES;
-    uint64_t* tfull = empty + TC_STAGES;      // [2] accumulator ready
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* conv = full + STAGES;           // fp32: stage split into hi / lo (MMA waits on this instead of full)
+    uint64_t* empty = conv + STAGES;
+    uint64_t* tfull = empty + STAGES;         // [2] accumulator ready
     uint64_t* tempty = tfull + 2;             // [2] accumulator drained (4 epilogue warps arrive)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -120,7 +147,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
     };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&conv[s], 1); mbar_init(&empty[s], 1); }
         for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
@@ -135,7 +162,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const uint32_t b_bytes = (uint32_t)args.BN * TC_BK * 2;
+    const uint32_t b_bytes = (uint32_t)args.BN * TC_ROW_BYTES;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -148,38 +175,40 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                 decode(t, m0, n0, z, kb0, nk);
                 for (int i = 0; i < nk; ++i) {
                     mbar_wait(&empty[s], ph ^ 1u);
-                    uint8_t* sa = smem + s * TC_STAGE_BYTES;
+                    uint8_t* sa = smem + s * STAGE_BYTES;
                     uint8_t* sb = sa + TC_A_BYTES;
                     mbar_expect_tx(&full[s], TC_A_BYTES + b_bytes);
                     const int kb = kb0 + i;
                     if (!A_MN) {
-                        // A K-major: box {64 (k), 128 (m)}; concat along K: blocks [0, nk0) from A0, the rest from A1
-                        if (kb < args.nk0) tma_load_2d(&mapA0, &full[s], sa, kb * TC_BK, (int)m0);
-                        else tma_load_2d(&mapA1, &full[s], sa, (kb - args.nk0) * TC_BK, (int)m0);
+                        // A K-major: box {KE (k), 128 (m)}; concat along K: blocks [0, nk0) from A0, the rest from A1
+                        if (kb < args.nk0) tma_load_2d(&mapA0, &full[s], sa, kb * KE, (int)m0);
+                        else tma_load_2d(&mapA1, &full[s], sa, (kb - args.nk0) * KE, (int)m0);
                     } else {
-                        // A MN-major (A^T stored row-major as [k][m]): two boxes {64 (m), 64 (k)}; output rows past
-                        // msplit read the second operand (two dW GEMMs sharing D in one launch)
+                        // A MN-major (A^T stored row-major as [k][m]): 128 / MNE boxes {MNE (m), KE (k)}; output rows
+                        // past msplit read the second operand (two dW GEMMs sharing D in one launch)
                         const bool second = m0 >= args.msplit;
                         const CUtensorMap* ma = second ? &mapA1 : &mapA0;
                         const int mm = (int)(second ? m0 - args.msplit : m0);
-                        tma_load_2d(ma, &full[s], sa, mm, kb * TC_BK);
-                        tma_load_2d(ma, &full[s], sa + 8192, mm + 64, kb * TC_BK);
+#pragma unroll
+                        for (int j = 0; j < TC_BM / MNE; ++j)
+                            tma_load_2d(ma, &full[s], sa + j * BOX_BYTES, mm + MNE * j, kb * KE);
                     }
                     if (!B_MN) {
-                        tma_load_2d(&mapB, &full[s], sb, kb * TC_BK, (int)n0);        // box {64 (k), BN (n)}
+                        tma_load_2d(&mapB, &full[s], sb, kb * KE, (int)n0);           // box {KE (k), BN (n)}
                     } else {
-                        for (int j = 0; j < args.BN / 64; ++j)                         // boxes {64 (n), 64 (k)}
-                            tma_load_2d(&mapB, &full[s], sb + j * 8192, (int)n0 + 64 * j, kb * TC_BK);
+                        for (int j = 0; j < args.BN / MNE; ++j)                        // boxes {MNE (n), KE (k)}
+                            tma_load_2d(&mapB, &full[s], sb + j * BOX_BYTES, (int)n0 + MNE * j, kb * KE);
                     }
-                    if (++s == TC_STAGES) { s = 0; ph ^= 1u; }
+                    if (++s == STAGES) { s = 0; ph ^= 1u; }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             // ---------------- MMA issuer ----------------
-            // instruction descriptor: D fp32, A/B bf16, A/B major, N >> 3, M >> 4
-            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+            // instruction descriptor: D fp32, A/B bf16 (1) or tf32 (2), A/B major, N >> 3, M >> 4
+            constexpr uint32_t fmt = F32 ? 2u : 1u;
+            const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((A_MN ? 1u : 0u) << 15) |
                                    ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(args.BN >> 3) << 17) |
                                    ((uint32_t)(TC_BM >> 4) << 24);
             int s = 0;
@@ -194,22 +223,63 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t d = tmem + (uint32_t)(b * 256);
                 for (int i = 0; i < nk; ++i) {
-                    mbar_wait(&full[s], ph);
+                    mbar_wait(F32 ? &conv[s] : &full[s], ph);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t sa = smem_u32(smem + s * TC_STAGE_BYTES);
+                    const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
                     const uint32_t sb = sa + TC_A_BYTES;
 #pragma unroll
-                    for (int k = 0; k < TC_BK / 16; ++k) {
-                        // K-major SW128: +32 B per 16-element k step inside the 128 B row; SBO = 8 rows (1 KB)
-                        // MN-major SW128: +16 rows (2 KB) per k step; LBO = MN-atom stride (8 KB), SBO = 8 k-rows
-                        const uint64_t ad = A_MN ? umma_desc(sa + k * 2048, 8192, 1024) : umma_desc(sa + k * 32, 16, 1024);
-                        const uint64_t bd = B_MN ? umma_desc(sb + k * 2048, 8192, 1024) : umma_desc(sb + k * 32, 16, 1024);
-                        umma_bf16(d, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                    for (int k = 0; k < 4; ++k) {
+                        // K-major SW128: +32 B per k step (16 bf16 / 8 tf32) inside the 128 B row; SBO = 8 rows (1 KB)
+                        // MN-major SW128: +KSTEP_MN per k step; LBO = MN-atom (box) stride, SBO = 8 k-rows
+                        const uint64_t ad = A_MN ? umma_desc(sa + k * KSTEP_MN, BOX_BYTES, 1024)
+                                                 : umma_desc(sa + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? umma_desc(sb + k * KSTEP_MN, BOX_BYTES, 1024)
+                                                 : umma_desc(sb + k * 32, 16, 1024);
+                        if (!F32) {
+                            umma_bf16(d, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                        } else {
+                            // 3xTF32: hi·hi + hi·lo + lo·hi (lo tiles sit one [A | B] pair further, same layout)
+                            constexpr uint64_t lo = (uint64_t)(TC_HALF_BYTES >> 4);   // descriptor start-address units
+                            umma_tf32(d, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                            umma_tf32(d, ad, bd + lo, idesc, 1u);
+                            umma_tf32(d, ad + lo, bd, idesc, 1u);
+                        }
                     }
                     umma_commit(&empty[s]);     // stage free once these MMAs have read it
-                    if (++s == TC_STAGES) { s = 0; ph ^= 1u; }
+                    if (++s == STAGES) { s = 0; ph ^= 1u; }
                 }
                 umma_commit(&tfull[b]);         // accumulator b complete
+            }
+        }
+    } else if (F32 && warp >= 6) {
+        // ---------------- 3xTF32 operand split (warps 6..9): hi = x & ~0x1FFF (tf32-exact), lo = x - hi ----------
+        // elementwise on the raw stage bytes, so the swizzled layout carries over to the lo tiles unchanged
+        const int ct = threadIdx.x - 192;
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            int64_t m0, n0;
+            int z, kb0, nk;
+            decode(t, m0, n0, z, kb0, nk);
+            for (int i = 0; i < nk; ++i) {
+                mbar_wait(&full[s], ph);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                const int nvec = (TC_A_BYTES + (int)b_bytes) / 16;
+                for (int v = ct; v < nvec; v += 128) {
+                    uint4* p = reinterpret_cast<uint4*>(st) + v;
+                    uint4 x = *p, h, l;
+                    h.x = x.x & 0xFFFFE000u; h.y = x.y & 0xFFFFE000u; h.z = x.z & 0xFFFFE000u; h.w = x.w & 0xFFFFE000u;
+                    l.x = __float_as_uint(__uint_as_float(x.x) - __uint_as_float(h.x));
+                    l.y = __float_as_uint(__uint_as_float(x.y) - __uint_as_float(h.y));
+                    l.z = __float_as_uint(__uint_as_float(x.z) - __uint_as_float(h.z));
+                    l.w = __float_as_uint(__uint_as_float(x.w) - __uint_as_float(h.w));
+                    *p = h;
+                    *reinterpret_cast<uint4*>(st + TC_HALF_BYTES + 16 * v) = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&conv[s])) : "memory");
+                if (++s == STAGES) { s = 0; ph ^= 1u; }
             }
         }
     } else {
@@ -225,7 +295,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int64_t row = m0 + q * 32 + lane;
             const int ncols = (args.N - n0 < args.BN) ? (int)(args.N - n0) : args.BN;
-            const float rs = (args.epi == EPI_BF16_ROWSCALE && row < args.M) ? args.rowscale[row] : 1.f;
+            const bool rsc = args.epi == EPI_BF16_ROWSCALE || args.epi == EPI_F32_ROWSCALE;
+            const float rs = (rsc && row < args.M) ? args.rowscale[row] : 1.f;
             for (int c0 = 0; c0 < ncols; c0 += 16) {
                 uint32_t r[16];
                 const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 256 + c0);
@@ -240,23 +311,21 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
                 const int64_t col = n0 + c0;
-                if (args.epi == EPI_F32) {
+                if (rsc)
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        if (col + k < args.scale_cols) v[k] *= rs;
+                if (args.relu)
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) v[k] = fmaxf(v[k], 0.f);
+                if (args.epi == EPI_F32 || args.epi == EPI_F32_ROWSCALE) {
                     float* o = static_cast<float*>(args.out) + (int64_t)z * args.split_stride + row * args.ldc + col;
 #pragma unroll
                     for (int h = 0; h < 4; ++h)
-                        if (c0 + 4 * h < ncols) {
-                            float4 w = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
-                            if (args.relu) { w.x = fmaxf(w.x, 0.f); w.y = fmaxf(w.y, 0.f); w.z = fmaxf(w.z, 0.f); w.w = fmaxf(w.w, 0.f); }
-                            *reinterpret_cast<float4*>(o + 4 * h) = w;
-                        }
+                        if (c0 + 4 * h < ncols)
+                            *reinterpret_cast<float4*>(o + 4 * h) = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2],
+                                                                                v[4 * h + 3]);
                 } else {
-                    if (args.epi == EPI_BF16_ROWSCALE)
-#pragma unroll
-                        for (int k = 0; k < 16; ++k)
-                            if (col + k < args.scale_cols) v[k] *= rs;
-                    if (args.relu)
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) v[k] = fmaxf(v[k], 0.f);
                     __nv_bfloat16* o = static_cast<__nv_bfloat16*>(args.out) + row * args.ldc + col;
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
@@ -293,32 +362,47 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 2-D bf16 row-major tensor [outer][inner] with row pitch ld (elements); box {64, box_outer}, SWIZZLE_128B
-static CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+// 2-D row-major tensor [outer][inner] (bf16 or fp32) with row pitch ld (elements); box {one 128 B row of inner
+// elements, box_outer}, SWIZZLE_128B
+static CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer, bool f32) {
     CUtensorMap m;
+    const int es_bytes = f32 ? 4 : 2;
     cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-    cuuint32_t box[2] = {64u, (cuuint32_t)box_outer};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * es_bytes)};
+    cuuint32_t box[2] = {(cuuint32_t)(TC_ROW_BYTES / es_bytes), (cuuint32_t)box_outer};
     cuuint32_t es[2] = {1u, 1u};
-    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                             const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(BNS_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     return m;
+}
+
+template <bool A_MN, bool B_MN, bool F32>
+static void launch_tc_t(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const TcArgs& args,
+                        dim3 grid) {
+    using Cfg = TcCfg<F32>;
+    static bool configured = false;
+    if (!configured) {
+        BNS_CUDA(cudaFuncSetAttribute(k_gemm_tc<A_MN, B_MN, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg::SMEM));
+        configured = true;
+    }
+    k_gemm_tc<A_MN, B_MN, F32><<<grid, Cfg::THREADS, Cfg::SMEM, c.stream>>>(a0, a1, b, args);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
 }
 
 template <bool A_MN, bool B_MN>
 static void launch_tc(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const TcArgs& args,
                       dim3 grid) {
-    static bool configured = false;
-    if (!configured) {
-        BNS_CUDA(cudaFuncSetAttribute(k_gemm_tc<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
-        configured = true;
-    }
-    k_gemm_tc<A_MN, B_MN><<<grid, TC_THREADS, TC_SMEM, c.stream>>>(a0, a1, b, args);
-    c.kernels += 1;
-    BNS_CHECK_LAUNCH();
+    if (c.prec == BNS_FP32) launch_tc_t<A_MN, B_MN, true>(c, a0, a1, b, args, grid);
+    else launch_tc_t<A_MN, B_MN, false>(c, a0, a1, b, args, grid);
 }
+
+static inline bool is_f32(const Ctx& c) { return c.prec == BNS_FP32; }
+static inline int k_elems(const Ctx& c) { return is_f32(c) ? 32 : 64; }   // k-elements per block (128 B row)
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -336,19 +420,22 @@ static dim3 persistent_grid(int64_t tiles) {
 void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64_t lda0, const void* A1, int64_t K1,
                  int64_t lda1, const void* WT, int64_t Kw, void* C, int64_t ldc, bool relu, bool out_f32) {
     if (M <= 0 || N <= 0) return;
+    const bool f32 = is_f32(c);
+    const int KE = k_elems(c);
     TcArgs a{};
     a.M = M;
     a.N = N;
     a.BN = (int)std::min<int64_t>(256, cdiv(N, 16) * 16);
-    a.nk0 = (int)cdiv(K0, 64);
-    a.nk = a.nk0 + (int)cdiv(K1, 64);
-    a.epi = out_f32 ? EPI_F32 : EPI_BF16;
+    // A1's k-blocks start where W^T's second concat half starts: each half is padded to a multiple of 64
+    a.nk0 = A1 ? (int)(cdiv(K0, 64) * 64 / KE) : (int)cdiv(K0, KE);
+    a.nk = a.nk0 + (int)cdiv(K1, KE);
+    a.epi = (out_f32 || f32) ? EPI_F32 : EPI_BF16;
     a.relu = relu ? 1 : 0;
     a.out = C;
     a.ldc = ldc;
-    CUtensorMap m0 = make_map(A0, K0, M, lda0, TC_BM);
-    CUtensorMap m1 = A1 ? make_map(A1, K1, M, lda1, TC_BM) : m0;
-    CUtensorMap mb = make_map(WT, Kw, N, Kw, a.BN);
+    CUtensorMap m0 = make_map(A0, K0, M, lda0, TC_BM, f32);
+    CUtensorMap m1 = A1 ? make_map(A1, K1, M, lda1, TC_BM, f32) : m0;
+    CUtensorMap mb = make_map(WT, Kw, N, Kw, a.BN, f32);
     launch_tc<false, false>(c, m0, m1, mb, a, persistent_grid(cdiv(M, TC_BM) * cdiv(N, a.BN)));
 }
 
@@ -356,16 +443,20 @@ void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64
 void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int64_t lda, const void* D, int64_t ldd,
                    float* Wg, int64_t ldw) {
     if (K <= 0 || N <= 0) return;
+    const bool f32 = is_f32(c);
+    const int KE = k_elems(c);
     TcArgs a{};
     a.M = K;
     a.N = N;
     a.BN = (int)std::min<int64_t>(256, cdiv(N, 64) * 64);
-    a.nk = (int)cdiv(Mn, 64);
+    a.nk = (int)cdiv(Mn, KE);
     a.nk0 = a.nk;
     const int64_t tiles = cdiv(K, TC_BM) * cdiv(N, a.BN);
-    // ~one CTA per SM, but at least kmin k-blocks (64 nodes each) per split so the partial slices stay small.
-    // kmin 16 (was 32; A/B at m = 8: gemm_bwd 0.355 -> 0.344 ms): small partitions get ~2x the CTAs
-    static const int kmin = [] { const char* e = std::getenv("BNS_WGRAD_KMIN"); return e ? std::max(1, std::atoi(e)) : 16; }();
+    // ~one CTA per SM, but at least 1024 nodes (kmin k-blocks of 64 bf16 / 32 fp32 nodes) per split so the partial
+    // slices stay small.  16 x 64 (was 32 x 64; A/B at m = 8: gemm_bwd 0.355 -> 0.344 ms): small partitions get ~2x
+    // the CTAs
+    static const int kmin0 = [] { const char* e = std::getenv("BNS_WGRAD_KMIN"); return e ? std::max(1, std::atoi(e)) : 16; }();
+    const int kmin = kmin0 * 64 / KE;
     int64_t S = std::max<int64_t>(1, std::min<int64_t>(cdiv(148, tiles), std::max(1, a.nk / kmin)));
     while (S > 1 && S * K * N > c.splitk_cap) --S;
     a.kb_per_split = (int)cdiv(a.nk, S);
@@ -375,8 +466,8 @@ void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int6
     a.out = c.d_splitk;
     a.ldc = N;
     a.split_stride = K * N;
-    CUtensorMap ma = make_map(A, K, Mn, lda, 64);
-    CUtensorMap mb = make_map(D, N, Mn, ldd, 64);
+    CUtensorMap ma = make_map(A, K, Mn, lda, KE, f32);
+    CUtensorMap mb = make_map(D, N, Mn, ldd, KE, f32);
     launch_tc<true, true>(c, ma, ma, mb, a, persistent_grid(cdiv(K, TC_BM) * cdiv(N, a.BN) * S));
     splitk_reduce(c, (int)S, K, N, Wg, ldw);
 }
@@ -391,16 +482,19 @@ void gemm_wgrad2_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, co
         return;
     }
     if (N <= 0) return;
+    const bool f32 = is_f32(c);
+    const int KE = k_elems(c);
     const int64_t K2 = 2 * K;
     TcArgs a{};
     a.M = K2;
     a.N = N;
     a.BN = (int)std::min<int64_t>(256, cdiv(N, 64) * 64);
-    a.nk = (int)cdiv(Mn, 64);
+    a.nk = (int)cdiv(Mn, KE);
     a.nk0 = a.nk;
     a.msplit = K;
     const int64_t tiles = cdiv(K2, TC_BM) * cdiv(N, a.BN);
-    static const int kmin = [] { const char* e = std::getenv("BNS_WGRAD_KMIN"); return e ? std::max(1, std::atoi(e)) : 16; }();
+    static const int kmin0 = [] { const char* e = std::getenv("BNS_WGRAD_KMIN"); return e ? std::max(1, std::atoi(e)) : 16; }();
+    const int kmin = kmin0 * 64 / KE;
     int64_t S = std::max<int64_t>(1, std::min<int64_t>(cdiv(148, tiles), std::max(1, a.nk / kmin)));
     while (S > 1 && S * K2 * N > c.splitk_cap) --S;
     a.kb_per_split = (int)cdiv(a.nk, S);
@@ -410,9 +504,9 @@ void gemm_wgrad2_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, co
     a.out = c.d_splitk;
     a.ldc = N;
     a.split_stride = K2 * N;
-    CUtensorMap m0 = make_map(A0, K, Mn, lda, 64);
-    CUtensorMap m1 = make_map(A1, K, Mn, lda, 64);
-    CUtensorMap mb = make_map(D, N, Mn, ldd, 64);
+    CUtensorMap m0 = make_map(A0, K, Mn, lda, KE, f32);
+    CUtensorMap m1 = make_map(A1, K, Mn, lda, KE, f32);
+    CUtensorMap mb = make_map(D, N, Mn, ldd, KE, f32);
     launch_tc<true, true>(c, m0, m1, mb, a, persistent_grid(tiles * S));
     splitk_reduce(c, (int)S, K2, N, Wg, ldw);
 }
@@ -421,19 +515,20 @@ void gemm_wgrad2_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, co
 void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t ldd, const void* B, int64_t ldb,
                 void* C, int64_t ldc, const float* rowscale, int64_t scale_cols) {
     if (M <= 0 || Nc <= 0) return;
+    const bool f32 = is_f32(c);
     TcArgs a{};
     a.M = M;
     a.N = Nc;
     a.BN = (int)std::min<int64_t>(256, cdiv(Nc, 16) * 16);
-    a.nk = (int)cdiv(K, 64);
+    a.nk = (int)cdiv(K, k_elems(c));
     a.nk0 = a.nk;
-    a.epi = rowscale ? EPI_BF16_ROWSCALE : EPI_BF16;
+    a.epi = f32 ? (rowscale ? EPI_F32_ROWSCALE : EPI_F32) : (rowscale ? EPI_BF16_ROWSCALE : EPI_BF16);
     a.out = C;
     a.ldc = ldc;
     a.rowscale = rowscale;
     a.scale_cols = scale_cols;
-    CUtensorMap ma = make_map(D, K, M, ldd, TC_BM);
-    CUtensorMap mb = make_map(B, K, Nc, ldb, a.BN);
+    CUtensorMap ma = make_map(D, K, M, ldd, TC_BM, f32);
+    CUtensorMap mb = make_map(B, K, Nc, ldb, a.BN, f32);
     launch_tc<false, false>(c, ma, ma, mb, a, persistent_grid(cdiv(M, TC_BM) * cdiv(Nc, a.BN)));
 }
 

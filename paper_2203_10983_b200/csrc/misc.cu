@@ -444,7 +444,7 @@ __global__ void k_wpack_all(const WDesc d) {
             const int64_t lr = logical_row(half * d.dpin[l] + j, d.kind, d.din[l], d.dpin[l]);
             if (lr >= 0 && n < d.dout[l]) v = d.W[l][lr * d.dout[l] + n];
         }
-        static_cast<__nv_bfloat16*>(d.WT[l])[t] = __float2bfloat16_rn(v);
+        static_cast<T*>(d.WT[l])[t] = from_f<T>(v);   // bf16 (kind::f16) or fp32 (3xTF32) tensor-core operand
     }
 }
 
@@ -484,11 +484,11 @@ void launch_wpack_all(Ctx& c, float* const* W) {
     BNS_CHECK_LAUNCH();
 }
 
-// R42: [W_top | W_bot] (dpin x 2 dpout, storage type) and its bf16 transpose (2 dpout x K64) for a transform-first
-// layer, from the padded fp32 weights Wp (2 dpin x dpout) packed just before on the same stream
+// R42: [W_top | W_bot] (dpin x 2 dpout) and its transpose (2 dpout x K64, the tensor-core B operand), both in the
+// storage type, for a transform-first layer, from the padded fp32 weights Wp (2 dpin x dpout) packed just before
 template <typename T>
 __global__ void k_wpack_tf(const float* __restrict__ Wp, int64_t dpin, int64_t dpout, int64_t K64, T* __restrict__ Wcat,
-                           __nv_bfloat16* __restrict__ WTtf) {
+                           T* __restrict__ WTtf) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n2 = 2 * dpout;
     if (t < dpin * n2) {
@@ -500,7 +500,7 @@ __global__ void k_wpack_tf(const float* __restrict__ Wp, int64_t dpin, int64_t d
         const int64_t n = t / K64, k = t % K64;
         float v = 0.f;
         if (k < dpin) v = n < dpout ? Wp[k * dpout + n] : Wp[(dpin + k) * dpout + (n - dpout)];
-        WTtf[t] = __float2bfloat16_rn(v);
+        WTtf[t] = from_f<T>(v);
     }
 }
 
@@ -509,13 +509,14 @@ void launch_wpack_tf(Ctx& c) {
         if (!((c.tf_mask >> l) & 1u)) continue;
         const int64_t dpin = c.dp[l], dpout = c.dp[l + 1], K64 = (dpin + 63) / 64 * 64;
         const int64_t n = std::max(dpin * 2 * dpout, 2 * dpout * K64);
-        __nv_bfloat16* wt = c.use_tc ? static_cast<__nv_bfloat16*>(c.WTtf[l]) : nullptr;
         if (c.prec == BNS_BF16)
             k_wpack_tf<__nv_bfloat16><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
-                c.Wpad[l], dpin, dpout, K64, static_cast<__nv_bfloat16*>(c.Wcat[l]), wt);
+                c.Wpad[l], dpin, dpout, K64, static_cast<__nv_bfloat16*>(c.Wcat[l]),
+                static_cast<__nv_bfloat16*>(c.use_tc ? c.WTtf[l] : nullptr));
         else
             k_wpack_tf<float><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
-                c.Wpad[l], dpin, dpout, K64, static_cast<float*>(c.Wcat[l]), wt);
+                c.Wpad[l], dpin, dpout, K64, static_cast<float*>(c.Wcat[l]),
+                static_cast<float*>(c.use_tc ? c.WTtf[l] : nullptr));
         c.kernels += 1;
         BNS_CHECK_LAUNCH();
     }
