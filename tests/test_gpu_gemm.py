@@ -160,7 +160,7 @@ def f32(t):
 
 
 @pytest.mark.parametrize("K,N,concat,relu", [(608, 512, False, False), (256, 256, True, True), (256, 96, False, False),
-                                             (37, 24, True, False)])
+                                             (40, 24, True, False)])   # an 8-padded narrow layer
 def test_forward_fp32(K, N, concat, relu):
     g = torch.Generator().manual_seed(K * 11 + N)
     M = M_FULL if K >= 256 else 3001
