@@ -40,9 +40,9 @@ def parse():
     ap.add_argument("--config", default="reddit")
     ap.add_argument("--p", type=float, default=0.1)
     ap.add_argument("--prec", default="bf16", choices=["bf16", "fp32"])
-    # random: on R-MAT (no community structure) it balances kept edges best (max/mean 1.03 vs 1.17 for ldg2 at
-    # m=8, p=0.1) -- the slowest rank sets the epoch time; see DESIGN.md §4
-    ap.add_argument("--partition", default="random", choices=["ldg2", "random"])
+    # ldg2: the deterministic two-constraint (nodes, arcs) LDG stand-in for METIS;
+    # random partition is reported beside it by the emulation sweep (scripts/emulate_rank.py)
+    ap.add_argument("--partition", default="ldg2", choices=["ldg2", "random"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--adam", action="store_true", help="Adam instead of SGD (the paper's optimizer, §8(f) f2)")
     ap.add_argument("--dropout", type=float, default=0.0, help="dropout rate (paper: 0.5 on Reddit, §8(f) f2)")
@@ -59,7 +59,7 @@ def parse():
                     help="N > 1: ipc = exchanges fused over NVLink peer memory (SURVEY §8(f) f1, default); "
                          "nccl = pack + grouped ncclSend/ncclRecv + ncclAllReduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-scale", type=float, default=64.0, help="oracle sample = workload scaled down by this")
+    ap.add_argument("--cpu-scale", type=float, default=16.0, help="oracle sample = workload scaled down by this")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
@@ -212,6 +212,58 @@ def measured_peaks():
         return {}
 
 
+def host_cpu():
+    """core count and model of the host the oracle runs on"""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def gather_ceiling(shape_name, row_bytes):
+    """measured gather ceiling of the SpMM's access pattern (build/gather_ceiling on the real R-MAT column stream,
+    scripts/ceiling_rmat.py; committed as profiles/*ceiling_rmat*.jsonl): GB/s of row bytes gathered"""
+    d = os.path.join(ROOT, "profiles")
+    best = None
+    if os.path.isdir(d):
+        for f in sorted(os.listdir(d)):
+            if "ceiling_rmat" in f and f.endswith(".jsonl"):
+                best = os.path.join(d, f)
+    if not best:
+        return None
+    try:
+        for line in open(best):
+            r = json.loads(line)
+            if r["case"].startswith(shape_name) and r["row_bytes"] == row_bytes and r.get("row_stride_bytes") == row_bytes:
+                return {"gbs": r["gather_gbs"], "case": r["case"], "source": os.path.relpath(best, ROOT)}
+    except (OSError, ValueError, KeyError):
+        return None
+    return None
+
+
+def full_oracle_epoch():
+    """the oracle's full-size epoch times measured on the GPU box by tests/test_gpu_fullsize.py (north-star test,
+    committed as profiles/*north_star*.json)"""
+    d = os.path.join(ROOT, "profiles")
+    best = None
+    if os.path.isdir(d):
+        for f in sorted(os.listdir(d)):
+            if "north_star" in f and f.endswith(".json"):
+                best = os.path.join(d, f)
+    if not best:
+        return None
+    try:
+        r = json.load(open(best))
+        return {"oracle_seconds": r["oracle_seconds"], "host": r.get("host"), "source": os.path.relpath(best, ROOT)}
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def latest_traffic():
     """dram bytes per SpMM launch from the newest committed ncu --set full summary (profiles/*spmm*.json)."""
     d = os.path.join(ROOT, "profiles")
@@ -234,9 +286,18 @@ def latest_traffic():
 # CPU baseline: the oracle as it stands, single-threaded, on a scaled-down sample of the same workload
 # ------------------------------------------------------------------------------------------------
 def cpu_baseline(shape, scale, steps=1):
+    """The oracle on ONE pinned host core (sched_setaffinity = taskset -c) over a scaled-down R-MAT of the same shape
+    and model, extrapolated to the full workload by the arc ratio (labelled so); the full-size epochs the north-star
+    test measured on the box are attached beside it."""
     from oracle import oracle as O
     from paper_2203_10983_b200 import inputs as I
     sm = shape.scaled(scale)
+    try:
+        old_aff = os.sched_getaffinity(0)
+        core = max(old_aff)
+        os.sched_setaffinity(0, {core})
+    except (AttributeError, OSError):
+        old_aff, core = None, None
     indptr, indices = I.rmat(sm.N, sm.nnz)
     X = I.features(np.arange(sm.N, dtype=np.int32), sm.d0)
     y = I.labels(sm.N, sm.C, sm.train_frac)
@@ -244,18 +305,25 @@ def cpu_baseline(shape, scale, steps=1):
     orc = O.Oracle(indptr, indices, part, 1, sm.dims, sm.layer, X, y)
     W = [w.astype(np.float64) for w in I.weights(sm.dims, sm.layer)]
     ts = []
-    for e in range(steps):
-        orc.sample(shape.p, I.BNS_SEED, e)
-        t0 = time.perf_counter()
-        orc.epoch(W, 0.01)
-        ts.append(time.perf_counter() - t0)
+    try:
+        for e in range(steps):
+            orc.sample(shape.p, I.BNS_SEED, e)
+            t0 = time.perf_counter()
+            orc.epoch(W, 0.01)
+            ts.append(time.perf_counter() - t0)
+    finally:
+        if old_aff is not None:
+            os.sched_setaffinity(0, old_aff)
     t = float(np.mean(ts))
     actual_scale = shape.nnz / float(indptr[-1])
     value = 1.0 / (t * actual_scale)
-    return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": (f"oracle (single-thread float64 C++) full epoch on a {shape.name}-shaped R-MAT scaled 1/{scale:g} "
-                       f"(N={sm.N}, nnz={int(indptr[-1])}, same dims), m=1; {t:.2f} s/epoch x {actual_scale:.1f} "
-                       f"(nnz ratio; oracle work is linear in nnz at fixed dims) -> epochs/s of the full workload")}
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "pinned_core": core, "host": host_cpu(),
+            "extrapolated": True,
+            "sample": (f"oracle (single-thread float64 C++, -O3 -mavx2 -mfma) full epoch on a {shape.name}-shaped R-MAT "
+                       f"scaled 1/{scale:g} (N={sm.N}, nnz={int(indptr[-1])}, same dims), m=1, pinned to one core; "
+                       f"{t:.2f} s/epoch x {actual_scale:.1f} (arc ratio; EXTRAPOLATED -- the oracle's work is linear "
+                       f"in arcs at fixed dims) -> epochs/s of the full workload"),
+            "full_workload_measured": full_oracle_epoch()}
 
 
 # ------------------------------------------------------------------------------------------------
@@ -471,8 +539,13 @@ def run_ours(args):
         gf = gemm_flops(dp, shape.L, cnt["n_in"], shape.layer == 0)
         gemm_ms = ph["gemm_fwd"] + ph["gemm_bwd"]
         bf16_peak = peaks.get("bf16_tflops_sustained", 1391.8)
-        # fp32 mode runs the GEMMs on the CUDA cores: peak = 148 SMs x 128 FMA lanes x 2 flop x max SM clock
-        peak_dtype = bf16_peak if prec == bns.BNS_BF16 else 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        # fp32 mode: 3xTF32 on the tensor cores -- tf32 peak = the measured bf16 peak x the nominal tf32 / bf16 ratio
+        # (1.1 / 2.25 PFLOP/s dense, B200_PROFILING.md), and three tf32 MMAs per fp32-accurate product
+        peak_dtype = bf16_peak if prec == bns.BNS_BF16 else bf16_peak * (1.1 / 2.25) / 3.0
+        ceil = gather_ceiling(shape.name, max(dp[1:-1] or dp) * s)
+        traffic = latest_traffic()
+        dram_gbs = (traffic["dram_bytes_per_step"] / (spmm_ms * 1e-3) / 1e9
+                    if traffic and traffic.get("dram_bytes_per_step") and spmm_ms > 0 and prec == bns.BNS_BF16 else None)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -493,7 +566,12 @@ def run_ours(args):
                            (", multi-label sigmoid BCE loss" if args.multilabel else ""))},
             "roofline": {"bound": "hbm", "kernel": "segment SpMM (a6 fwd + a10 bwd, incl. split-row fixup)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": (achieved / hbm_peak) if achieved else None, "traffic": latest_traffic(),
+                         "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
+                         "ceiling": None if not ceil else {
+                             "gather_gbs": ceil["gbs"], "frac": (achieved / ceil["gbs"]) if achieved else None,
+                             "what": "measured gather ceiling of the same row-gather stream (no arithmetic): " +
+                                     ceil["case"], "source": ceil["source"]},
+                         "dram_gbs": dram_gbs, "dram_frac": (dram_gbs / hbm_peak) if dram_gbs else None,
                          "algorithmic_bytes_per_step": fwd_b + bwd_b, "spmm_ms_per_step": spmm_ms,
                          "spmm_share_of_step": spmm_ms / ms_per_step,
                          "gather_working_set_bytes": ws_bytes, "l2_bytes": l2,
@@ -501,7 +579,8 @@ def run_ours(args):
                                     "algorithmic GB/s above the HBM copy peak is served from L2, see traffic")
                          if ws_bytes <= l2 else "DRAM-resident gathers",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peaks else "fallback 6.65 TB/s"},
-            "roofline_gemm": {"bound": "tensor" if prec == bns.BNS_BF16 else "alu", "achieved": gf / (gemm_ms * 1e-3) / 1e12
+            "roofline_gemm": {"bound": "tensor", "kind": "tcgen05 kind::f16" if prec == bns.BNS_BF16 else
+                              "tcgen05 3xTF32 (kind::tf32, peak = tf32 / 3)", "achieved": gf / (gemm_ms * 1e-3) / 1e12
                               if gemm_ms > 0 else None, "unit": "TFLOP/s", "flops_per_step": gf, "gemm_ms_per_step": gemm_ms,
                               "peak": peak_dtype},
             "phases_ms": ph,

@@ -252,6 +252,13 @@ def test_north_star_full_size(reddit):
             for ev in th.go:
                 ev.set()
     report["wall_seconds"] = time.time() - t0
+    model = None
+    for line in open("/proc/cpuinfo"):
+        if line.startswith("model name"):
+            model = line.split(":", 1)[1].strip()
+            break
+    report["host"] = {"nproc": os.cpu_count(), "model": model,
+                      "note": "each oracle single-threaded (three run concurrently, one per configuration)"}
     os.makedirs("gpurun_out", exist_ok=True)
     with open(os.path.join("gpurun_out", "north_star_fullsize.json"), "w") as f:
         json.dump(report, f, indent=1)
