@@ -225,6 +225,8 @@ struct Ctx {
     std::vector<int64_t> goff;     // per-layer offset in gflat
     float* d_splitk = nullptr;     // split-K partials
     int64_t splitk_cap = 0;
+    float* d_tr = nullptr;         // fp32 tensor-core dW: transposed operands [A^T ; D^T] (node dimension contiguous)
+    int64_t tr_cap = 0;
     double* d_scal = nullptr;      // [loss_sum, correct] (all-reduced)
     double* d_lpart = nullptr;     // per-block loss partials
     int32_t* d_nonfinite = nullptr;

@@ -14,7 +14,11 @@
 //             tf32 rounding are ~2^-22 relative, so the result meets the fp32 mode's 1e-5 (plain 1xTF32 would not,
 //             SURVEY §8(c) item 19).  32-element (128 B) k-blocks, 2-stage ring of [hi | lo] tiles; four more warps
 //             do the split between the TMA landing and the MMA issue.
-// Both element types use the same byte layout (128 B SWIZZLE_128B rows, 32 B per MMA k-step).
+// Both element types use the same byte layout (128 B SWIZZLE_128B rows, 32 B per K-major MMA k-step).  The fp32
+// weight gradient (whose operands are MN-major: the node dimension is the reduction) runs K-major on transposed
+// copies made by k_transpose32 -- MN-major tf32 operands (SWIZZLE_128B with 32-byte atoms) gave all-zero products on
+// sm_100a in every descriptor / tensor-map combination tried (scripts/diag/), the transposes cost one extra read and
+// write of the two operands.
 //
 // One CTA = one 128 x BN output tile (BN <= 256): warp 0 lane 0 issues TMA into an mbarrier ring, warp 1 lane 0
 // issues tcgen05.mma.cta_group::1 (M=128, N=BN, fp32 accumulator in TMEM) and releases stages with tcgen05.commit;
@@ -373,7 +377,8 @@ static CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int6
     cuuint32_t es[2] = {1u, 1u};
     CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                              const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(BNS_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     return m;
@@ -439,11 +444,71 @@ void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64
     launch_tc<false, false>(c, m0, m1, mb, a, persistent_grid(cdiv(M, TC_BM) * cdiv(N, a.BN)));
 }
 
+// fp32 weight gradient: out^T operands.  dst[c][r] = src[r][c] for r < rows (the node dimension), c < cols;
+// dst row pitch ldd >= rows (padded to 4 floats for TMA); 32 x 32 tiles through shared memory
+__global__ void k_transpose32(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                              float* __restrict__ dst, int64_t ldd) {
+    __shared__ float t[32][33];
+    const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        t[i][threadIdx.x] = (r < rows && c < cols) ? src[r * lds + c] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (c < cols && r < ldd) dst[c * ldd + r] = t[threadIdx.x][i];
+    }
+}
+
+static void transpose32(Ctx& c, const void* src, int64_t rows, int64_t cols, int64_t lds, float* dst, int64_t ldd) {
+    const dim3 grid((unsigned)cdiv(ldd, 32), (unsigned)cdiv(cols, 32));
+    k_transpose32<<<grid, dim3(32, 8), 0, c.stream>>>(static_cast<const float*>(src), rows, cols, lds, dst, ldd);
+    c.kernels += 1;
+    BNS_CHECK_LAUNCH();
+}
+
+// fp32 (3xTF32) dW: [A0 | A1]^T D as a K-major GEMM of the transposed operands, split-K over nodes, fixed-order reduce
+static void wgrad_f32(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, const void* A1, int64_t lda,
+                      const void* D, int64_t ldd, float* Wg, int64_t ldw) {
+    const int64_t halves = A1 ? 2 : 1, K2 = halves * K, ldt = (Mn + 3) / 4 * 4;
+    if ((K2 + N) * ldt > c.tr_cap)
+        throw Error(BNS_ERR_RUNTIME, "fp32 weight-gradient transpose scratch too small");
+    float* At = c.d_tr;                        // [K2][ldt]
+    float* Dt = c.d_tr + K2 * ldt;             // [N][ldt]
+    transpose32(c, A0, Mn, K, lda, At, ldt);
+    if (A1) transpose32(c, A1, Mn, K, lda, At + K * ldt, ldt);
+    transpose32(c, D, Mn, N, ldd, Dt, ldt);
+    TcArgs a{};
+    a.M = K2;
+    a.N = N;
+    a.BN = (int)std::min<int64_t>(256, cdiv(N, 16) * 16);
+    a.nk = (int)cdiv(Mn, 32);
+    a.nk0 = a.nk;
+    const int64_t tiles = cdiv(K2, TC_BM) * cdiv(N, a.BN);
+    static const int kmin0 = [] { const char* e = std::getenv("BNS_WGRAD_KMIN"); return e ? std::max(1, std::atoi(e)) : 16; }();
+    const int kmin = kmin0 * 2;                // 32-node k-blocks: the same >= 1024 nodes per split as bf16
+    int64_t S = std::max<int64_t>(1, std::min<int64_t>(cdiv(148, tiles), std::max(1, a.nk / kmin)));
+    while (S > 1 && S * K2 * N > c.splitk_cap) --S;
+    a.kb_per_split = (int)cdiv(a.nk, S);
+    S = cdiv(a.nk, a.kb_per_split);
+    c.last_splitk = (int)S;
+    a.epi = EPI_F32;
+    a.out = c.d_splitk;
+    a.ldc = N;
+    a.split_stride = K2 * N;
+    CUtensorMap ma = make_map(At, ldt, K2, ldt, TC_BM, true);
+    CUtensorMap mb = make_map(Dt, ldt, N, ldt, a.BN, true);
+    launch_tc<false, false>(c, ma, ma, mb, a, persistent_grid(tiles * S));
+    splitk_reduce(c, (int)S, K2, N, Wg, ldw);
+}
+
 // dW partials: out[z][K x N] = A^T · D over k-block range z; A is [M_nodes][K] row-major, D is [M_nodes][N]
 void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int64_t lda, const void* D, int64_t ldd,
                    float* Wg, int64_t ldw) {
     if (K <= 0 || N <= 0) return;
     const bool f32 = is_f32(c);
+    if (f32) return wgrad_f32(c, Mn, K, N, A, nullptr, lda, D, ldd, Wg, ldw);
     const int KE = k_elems(c);
     TcArgs a{};
     a.M = K;
@@ -483,6 +548,7 @@ void gemm_wgrad2_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, co
     }
     if (N <= 0) return;
     const bool f32 = is_f32(c);
+    if (f32) return wgrad_f32(c, Mn, K, N, A0, A1, lda, D, ldd, Wg, ldw);
     const int KE = k_elems(c);
     const int64_t K2 = 2 * K;
     TcArgs a{};
