@@ -231,6 +231,18 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     // ---- static plan on device
     c.d_row_ptr = upload(c, P.row_ptr);
     c.d_col_enc = upload(c, P.col_enc);
+    {   // induce tiles (induce.cu, kInduceTileArcs static arcs each): first row starting in every tile
+        const int64_t nt = (c.nnz_i + kInduceTileArcs - 1) / kInduceTileArcs;
+        std::vector<int64_t> tr(nt + 1);
+        int64_t r = 0;
+        for (int64_t t = 0; t <= nt; ++t) {
+            const int64_t e0 = std::min<int64_t>(t * kInduceTileArcs, c.nnz_i + 1);
+            while (r <= P.n_in && P.row_ptr[r] < e0) ++r;
+            tr[t] = r;
+        }
+        tr[nt] = P.n_in + 1;
+        c.d_tile_row = upload(c, tr);
+    }
     c.n_cand = P.n_bd + P.n_send;
     std::vector<int32_t> gid(c.n_cand), key(c.n_cand), pay(c.n_cand);
     for (int64_t b = 0; b < P.n_bd; ++b) { gid[b] = P.B[b]; key[b] = c.cfg.rank; pay[b] = (int32_t)b; }

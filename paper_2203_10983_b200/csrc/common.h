@@ -47,6 +47,7 @@ __host__ __device__ inline int32_t seg_count(int64_t cnt, int32_t seg_long) {
     const int64_t L = seg_len(cnt, seg_long);
     return cnt > L ? (int32_t)((cnt + L - 1) / L) : 1;
 }
+constexpr int64_t kInduceTileArcs = 8192;   // induce.cu: arcs per tile (256 threads x one 32-arc word)
 constexpr int kPad = 8;            // feature dims padded to multiples of 8 (16-byte rows for fp32x4 / bf16x8)
 
 inline int64_t pad8(int64_t d) { return (d + kPad - 1) / kPad * kPad; }
@@ -148,6 +149,7 @@ struct Ctx {
     int32_t* d_cand_out = nullptr; // compacted payloads: [U_b (|U|) ; S_local (ΣS)]
     int32_t* d_slot_of_b = nullptr;
     uint32_t* d_bkeep = nullptr;   // keep bit per boundary node (induce)
+    int64_t* d_tile_row = nullptr;  // induce tile t: first inner row whose first static arc lies in it (setup)
     uint64_t* d_lb_state = nullptr; // decoupled look-back tile states (induce.cu): draw | induce | segs fwd | segs bwd
     unsigned* d_lb_ctr = nullptr;   // tile-order counters of those four chains (each reset by its last tile)
     int64_t lb_off_induce = 0, lb_off_segf = 0, lb_off_segb = 0;

@@ -16,9 +16,8 @@
 //             do the split between the TMA landing and the MMA issue.
 // Both element types use the same byte layout (128 B SWIZZLE_128B rows, 32 B per K-major MMA k-step).  The fp32
 // weight gradient (whose operands are MN-major: the node dimension is the reduction) runs K-major on transposed
-// copies made by k_transpose32 -- MN-major tf32 operands (SWIZZLE_128B with 32-byte atoms) gave all-zero products on
-// sm_100a in every descriptor / tensor-map combination tried (scripts/diag/), the transposes cost one extra read and
-// write of the two operands.
+// copies made by k_transpose32 (one extra read + write of the two operands); MN-major tf32 operands need the
+// SWIZZLE_128B variant with 32-byte atoms (TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) -- not used here.
 //
 // One CTA = one 128 x BN output tile (BN <= 256): warp 0 lane 0 issues TMA into an mbarrier ring, warp 1 lane 0
 // issues tcgen05.mma.cta_group::1 (M=128, N=BN, fp32 accumulator in TMEM) and releases stages with tcgen05.commit;

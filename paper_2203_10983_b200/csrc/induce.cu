@@ -24,7 +24,7 @@ namespace bns {
 namespace {
 
 constexpr int kTile = 1024;          // candidates / rows / halo slots per tile (one per thread)
-constexpr int kEdgeThreads = 256;    // induce: one 32-arc word per thread -> 8192 arcs per tile
+constexpr int kEdgeThreads = kInduceTileArcs / 32;   // induce: one 32-arc word per thread
 constexpr uint64_t kValMask = (1ull << 38) - 1;
 enum { LB_NONE = 0, LB_AGG = 1, LB_PREFIX = 2 };
 
@@ -162,12 +162,12 @@ __device__ __forceinline__ bool arc_kept(int32_t x, const uint32_t* __restrict__
 
 struct InduceArgs {
     const int32_t* col_enc; int64_t nnz; const uint32_t* bkeep; const int32_t* slot_of_b; int64_t n_in;
-    const int64_t* row_ptr; int32_t* out_col; int64_t* out_ptr; int64_t* total;
+    const int64_t* row_ptr; const int64_t* tile_row; int32_t* out_col; int64_t* out_ptr; int64_t* total;
     uint64_t* state; unsigned* ctr; uint32_t gen; int64_t ntiles;
 };
 
 __global__ void __launch_bounds__(kEdgeThreads) k_induce_fused(const InduceArgs a) {
-    __shared__ int64_t s_tile, s_excl, s_rlo, s_rhi;
+    __shared__ int64_t s_tile, s_excl;
     __shared__ int s_warp[32], s_total;
     __shared__ uint32_t s_word[kEdgeThreads];
     __shared__ int s_wex[kEdgeThreads];
@@ -193,20 +193,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_induce_fused(const InduceArgs 
     s_word[threadIdx.x] = word;
     const int wex = block_excl_scan(__popc(word), s_warp, &s_total);
     s_wex[threadIdx.x] = wex;
-    // rows whose first arc lies in this tile (the last tile also takes the rows starting at nnz)
-    if (threadIdx.x == 0) {
-        int64_t lo = 0, hi = a.n_in + 1;                 // first r with row_ptr[r] >= e0
-        while (lo < hi) { const int64_t md = (lo + hi) >> 1; if (a.row_ptr[md] < e0) lo = md + 1; else hi = md; }
-        s_rlo = lo;
-        if (t == a.ntiles - 1) {
-            s_rhi = a.n_in + 1;
-        } else {
-            hi = a.n_in + 1;
-            while (lo < hi) { const int64_t md = (lo + hi) >> 1; if (a.row_ptr[md] < e1) lo = md + 1; else hi = md; }
-            s_rhi = lo;
-        }
-    }
-    const int64_t excl = lookback(a.state, a.gen, t, s_total, &s_excl);   // (its barrier also publishes s_word / s_rlo)
+    const int64_t excl = lookback(a.state, a.gen, t, s_total, &s_excl);   // (its barrier also publishes s_word / s_wex)
     // warp-cooperative order-preserving scatter of the warp's 32 words: lane j takes arc 32k + j (coalesced)
     const int64_t ewarp = e0 + (int64_t)wid * 1024;
     for (int k = 0; k < 32; ++k) {
@@ -216,8 +203,10 @@ __global__ void __launch_bounds__(kEdgeThreads) k_induce_fused(const InduceArgs 
         a.out_col[excl + s_wex[wid * 32 + k] + __popc(wk & ((1u << lane) - 1u))] =
             v >= 0 ? v : (int32_t)a.n_in + a.slot_of_b[-v - 1];
     }
-    // induced row pointers: kept arcs before the row's first static arc
-    for (int64_t r = s_rlo + threadIdx.x; r < s_rhi; r += blockDim.x) {
+    // induced row pointers of the rows whose first static arc lies in this tile (setup table; the last tile also
+    // takes the rows starting at nnz): kept arcs before that arc
+    const int64_t rlo = a.tile_row[t], rhi = a.tile_row[t + 1];
+    for (int64_t r = rlo + threadIdx.x; r < rhi; r += blockDim.x) {
         const int64_t e = a.row_ptr[r];
         int64_t kb;
         if (e >= e1) {
@@ -328,7 +317,7 @@ void launch_induce_fused(Ctx& c) {
     }
     InduceArgs a{};
     a.col_enc = c.d_col_enc; a.nnz = nnz; a.bkeep = c.d_bkeep; a.slot_of_b = c.d_slot_of_b; a.n_in = c.plan.n_in;
-    a.row_ptr = c.d_row_ptr; a.out_col = c.d_ind_col; a.out_ptr = c.d_ind_ptr; a.total = tot;
+    a.row_ptr = c.d_row_ptr; a.tile_row = c.d_tile_row; a.out_col = c.d_ind_col; a.out_ptr = c.d_ind_ptr; a.total = tot;
     a.state = c.d_lb_state + c.lb_off_induce; a.ctr = c.d_lb_ctr + 1; a.gen = ++c.lb_gen; a.ntiles = nt;
     k_induce_fused<<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
     c.kernels += 1;
