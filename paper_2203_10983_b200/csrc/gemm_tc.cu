@@ -8,8 +8,8 @@
 //
 // Two precisions, one kernel template:
 //   BNS_BF16  kind::f16 with bf16 operands (R19), 64-element (128 B) k-blocks, 4-stage ring.
-//   BNS_FP32  3xTF32 (kind::tf32): every fp32 operand tile is split in shared memory into hi = x with the low 13
-//             mantissa bits cleared (exactly representable in tf32) and lo = x - hi (exact in fp32), and the tile
+//   BNS_FP32  3xTF32 (kind::tf32): every fp32 operand tile is split in shared memory into hi = x rounded to tf32
+//             (low 13 mantissa bits cleared after rounding: exactly representable) and lo = x - hi (exact), and the tile
 //             product is accumulated as hi·hi + hi·lo + lo·hi in fp32 TMEM -- the dropped lo·lo term and lo's own
 //             tf32 rounding are ~2^-22 relative, so the result meets the fp32 mode's 1e-5 (plain 1xTF32 would not,
 //             SURVEY §8(c) item 19).  32-element (128 B) k-blocks, 2-stage ring of [hi | lo] tiles; four more warps
@@ -255,7 +255,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
             }
         }
     } else if (F32 && warp >= 6) {
-        // ---------------- 3xTF32 operand split (warps 6..9): hi = x & ~0x1FFF (tf32-exact), lo = x - hi ----------
+        // ---------------- 3xTF32 operand split (warps 6..9): hi = x rounded to tf32 (11 significant bits, ties
+        // away from zero; exactly representable), lo = x - hi (exact in fp32, |lo| <= 2^-11 |x|) ----------------
         // elementwise on the raw stage bytes, so the swizzled layout carries over to the lo tiles unchanged
         const int ct = threadIdx.x - 192;
         int s = 0;
@@ -271,7 +272,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                 for (int v = ct; v < nvec; v += 128) {
                     uint4* p = reinterpret_cast<uint4*>(st) + v;
                     uint4 x = *p, h, l;
-                    h.x = x.x & 0xFFFFE000u; h.y = x.y & 0xFFFFE000u; h.z = x.z & 0xFFFFE000u; h.w = x.w & 0xFFFFE000u;
+                    h.x = (x.x + 0x1000u) & 0xFFFFE000u; h.y = (x.y + 0x1000u) & 0xFFFFE000u;
+                    h.z = (x.z + 0x1000u) & 0xFFFFE000u; h.w = (x.w + 0x1000u) & 0xFFFFE000u;
                     l.x = __float_as_uint(__uint_as_float(x.x) - __uint_as_float(h.x));
                     l.y = __float_as_uint(__uint_as_float(x.y) - __uint_as_float(h.y));
                     l.z = __float_as_uint(__uint_as_float(x.z) - __uint_as_float(h.z));

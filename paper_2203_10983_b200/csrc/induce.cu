@@ -65,7 +65,10 @@ __device__ int64_t lookback(uint64_t* state, uint32_t gen, int64_t t, int64_t ag
                 const uint64_t s = q >= 0 ? ld_acquire(state + q) : lb_pack(gen, LB_PREFIX, 0);
                 const int flag = (int)((s >> 38) & 3u);
                 const bool ready = (uint32_t)(s >> 40) == g && flag != LB_NONE;
-                if (!__all_sync(0xffffffffu, ready)) continue;
+                if (!__all_sync(0xffffffffu, ready)) {   // back off: hundreds of warps poll the same few lines
+                    __nanosleep(64);
+                    continue;
+                }
                 const unsigned pm = __ballot_sync(0xffffffffu, flag == LB_PREFIX);
                 const int upto = pm ? __ffs(pm) - 1 : 31;
                 int64_t x = lane <= upto ? (int64_t)(s & kValMask) : 0;
