@@ -252,7 +252,7 @@ bns_status bns_set_timing(bns_ctx* ctx, int32_t on);
  * its gradients, l.12 PAPER.md:290), run in isolation by the SAME kernels bns_epoch launches -- so the tensor-core
  * GEMMs can be checked element by element at full size against a float64 product of the same operands.  No context
  * needed; all pointers are caller-owned DEVICE memory, row-major, leading dimensions in elements.
- *   precision  BNS_BF16: tcgen05 kind::f16 (bf16 operands, fp32 accumulation in TMEM); BNS_FP32: 3xTF32
+ *   precision  BNS_BF16: tcgen05 kind::f16 (bf16 operands, fp32 accumulation in TMEM); BNS_FP32: split-TF32 (4 MMAs)
  *              (tcgen05 kind::tf32 on hi / lo splits of fp32 operands, fp32 accumulation) -- every operand and
  *              output below is then fp32.
  *   kind 0  FWD     C[M x N] = [A0 | A1] · W, A0 / A1 M x K (lda; A1 may be NULL), B = Wᵀ stored [N][Kw] with each

@@ -386,7 +386,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.WT.assign(L, nullptr);
     c.wkw.assign(L, 0);
     {
-        // tensor-core GEMMs in both modes (bf16: kind::f16; fp32: 3xTF32); BNS_NO_TC=1 selects the SIMT kernels
+        // tensor-core GEMMs in both modes (bf16: kind::f16; fp32: split-TF32 (4 MMAs)); BNS_NO_TC=1 selects the SIMT kernels
         const char* no_tc = std::getenv("BNS_NO_TC");
         c.use_tc = !(no_tc && no_tc[0] == '1');
     }

@@ -8,12 +8,14 @@
 //
 // Two precisions, one kernel template:
 //   BNS_BF16  kind::f16 with bf16 operands (R19), 64-element (128 B) k-blocks, 4-stage ring.
-//   BNS_FP32  3xTF32 (kind::tf32): every fp32 operand tile is split in shared memory into hi = x rounded to tf32
-//             (low 13 mantissa bits cleared after rounding: exactly representable) and lo = x - hi (exact), and the tile
-//             product is accumulated as hi·hi + hi·lo + lo·hi in fp32 TMEM -- the dropped lo·lo term and lo's own
-//             tf32 rounding are ~2^-22 relative, so the result meets the fp32 mode's 1e-5 (plain 1xTF32 would not,
-//             SURVEY §8(c) item 19).  32-element (128 B) k-blocks, 2-stage ring of [hi | lo] tiles; four more warps
-//             do the split between the TMA landing and the MMA issue.
+//   BNS_FP32  split TF32 (kind::tf32): every fp32 operand tile is split in shared memory into hi = x rounded to
+//             tf32 (exactly representable) and lo = (x - hi) rounded to tf32, and the tile product is accumulated as
+//             hi·hi + hi·lo + lo·hi + lo·lo in fp32 TMEM -- what is dropped is lo's rounding residual, <= 2^-22 |x|
+//             per operand, so each product is within ~2^-21 relative and the GEMM meets the fp32 mode's 1e-5 (plain
+//             1xTF32 would not; the 3-term form without lo·lo and with the tensor core's own
+//             tf32 conversion of lo measured 1.2e-5 on a cancellation-heavy last-layer dW).  32-element (128 B)
+//             k-blocks, 2-stage ring of [hi | lo] tiles; four more warps do the split between the TMA landing and the
+//             MMA issue.
 // Both element types use the same byte layout (128 B SWIZZLE_128B rows, 32 B per K-major MMA k-step).  The fp32
 // weight gradient (whose operands are MN-major: the node dimension is the reduction) runs K-major on transposed
 // copies made by k_transpose32 (one extra read + write of the two operands); MN-major tf32 operands need the
@@ -116,7 +118,7 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 // Persistent, warp-specialized: grid = min(#tiles, #SMs); tile t = (m-tile, n-tile, split) visited in
 // blockIdx-strided order.  warp 0 lane 0: TMA producer over the smem ring; warp 1 lane 0: MMA issuer into one of two
 // TMEM accumulators (2 x 256 columns), so the epilogue of tile i overlaps the MMAs of tile i+1; warps 2-5: epilogue
-// (warp w drains TMEM lanes 32*(w%4) .. +31); fp32 (3xTF32): warps 6-9 split each landed stage into hi / lo.
+// (warp w drains TMEM lanes 32*(w%4) .. +31); fp32 (split-TF32 (4 MMAs)): warps 6-9 split each landed stage into hi / lo.
 template <bool A_MN, bool B_MN, bool F32>
 __global__ void __launch_bounds__(TcCfg<F32>::THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
@@ -241,11 +243,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                         if (!F32) {
                             umma_bf16(d, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
                         } else {
-                            // 3xTF32: hi·hi + hi·lo + lo·hi (lo tiles sit one [A | B] pair further, same layout)
+                            // hi·hi + hi·lo + lo·hi + lo·lo (lo tiles sit one [A | B] pair further, same layout)
                             constexpr uint64_t lo = (uint64_t)(TC_HALF_BYTES >> 4);   // descriptor start-address units
                             umma_tf32(d, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
                             umma_tf32(d, ad, bd + lo, idesc, 1u);
                             umma_tf32(d, ad + lo, bd, idesc, 1u);
+                            umma_tf32(d, ad + lo, bd + lo, idesc, 1u);
                         }
                     }
                     umma_commit(&empty[s]);     // stage free once these MMAs have read it
@@ -255,8 +258,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
             }
         }
     } else if (F32 && warp >= 6) {
-        // ---------------- 3xTF32 operand split (warps 6..9): hi = x rounded to tf32 (11 significant bits, ties
-        // away from zero; exactly representable), lo = x - hi (exact in fp32, |lo| <= 2^-11 |x|) ----------------
+        // ---------------- split-TF32 operands (warps 6..9): hi = x rounded to tf32 (11 significant bits, ties away
+        // from zero; exactly representable), lo = x - hi (exact in fp32, |lo| <= 2^-11 |x|) rounded to tf32 -------
         // elementwise on the raw stage bytes, so the swizzled layout carries over to the lo tiles unchanged
         const int ct = threadIdx.x - 192;
         int s = 0;
@@ -274,10 +277,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                     uint4 x = *p, h, l;
                     h.x = (x.x + 0x1000u) & 0xFFFFE000u; h.y = (x.y + 0x1000u) & 0xFFFFE000u;
                     h.z = (x.z + 0x1000u) & 0xFFFFE000u; h.w = (x.w + 0x1000u) & 0xFFFFE000u;
-                    l.x = __float_as_uint(__uint_as_float(x.x) - __uint_as_float(h.x));
-                    l.y = __float_as_uint(__uint_as_float(x.y) - __uint_as_float(h.y));
-                    l.z = __float_as_uint(__uint_as_float(x.z) - __uint_as_float(h.z));
-                    l.w = __float_as_uint(__uint_as_float(x.w) - __uint_as_float(h.w));
+                    // lo rounded to tf32 as well, so the tensor core's own tf32 conversion changes nothing
+                    l.x = (__float_as_uint(__uint_as_float(x.x) - __uint_as_float(h.x)) + 0x1000u) & 0xFFFFE000u;
+                    l.y = (__float_as_uint(__uint_as_float(x.y) - __uint_as_float(h.y)) + 0x1000u) & 0xFFFFE000u;
+                    l.z = (__float_as_uint(__uint_as_float(x.z) - __uint_as_float(h.z)) + 0x1000u) & 0xFFFFE000u;
+                    l.w = (__float_as_uint(__uint_as_float(x.w) - __uint_as_float(h.w)) + 0x1000u) & 0xFFFFE000u;
                     *p = h;
                     *reinterpret_cast<uint4*>(st + TC_HALF_BYTES + 16 * v) = l;
                 }
@@ -469,7 +473,7 @@ static void transpose32(Ctx& c, const void* src, int64_t rows, int64_t cols, int
     BNS_CHECK_LAUNCH();
 }
 
-// fp32 (3xTF32) dW: [A0 | A1]^T D as a K-major GEMM of the transposed operands, split-K over nodes, fixed-order reduce
+// fp32 (split-TF32 (4 MMAs)) dW: [A0 | A1]^T D as a K-major GEMM of the transposed operands, split-K over nodes, fixed-order reduce
 static void wgrad_f32(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, const void* A1, int64_t lda,
                       const void* D, int64_t ldd, float* Wg, int64_t ldw) {
     const int64_t halves = A1 ? 2 : 1, K2 = halves * K, ldt = (Mn + 3) / 4 * 4;

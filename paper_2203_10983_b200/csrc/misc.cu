@@ -444,7 +444,7 @@ __global__ void k_wpack_all(const WDesc d) {
             const int64_t lr = logical_row(half * d.dpin[l] + j, d.kind, d.din[l], d.dpin[l]);
             if (lr >= 0 && n < d.dout[l]) v = d.W[l][lr * d.dout[l] + n];
         }
-        static_cast<T*>(d.WT[l])[t] = from_f<T>(v);   // bf16 (kind::f16) or fp32 (3xTF32) tensor-core operand
+        static_cast<T*>(d.WT[l])[t] = from_f<T>(v);   // bf16 (kind::f16) or fp32 (split-TF32 (4 MMAs)) tensor-core operand
     }
 }
 

@@ -1,11 +1,11 @@
-"""Kernel-level parity of the tcgen05 GEMMs (bf16 kind::f16 and the fp32 mode's 3xTF32 kind::tf32) (§8(a) a7 forward update φ = W·CONCAT(z, h), PAPER.md:100 / Alg.1 l.10
+"""Kernel-level parity of the tcgen05 GEMMs (bf16 kind::f16 and the fp32 mode's split-TF32 (4 MMAs) kind::tf32) (§8(a) a7 forward update φ = W·CONCAT(z, h), PAPER.md:100 / Alg.1 l.10
 PAPER.md:287; a9 its gradients, Alg.1 l.12 PAPER.md:290) through the C ABI entry bns_gemm, which launches the same
 kernels as bns_epoch.  Expected values: a float64 product (torch, cuBLAS DGEMM) of the SAME bf16 operands -- the
 definition, independent of the kernel.  No ReLU flips or epoch trajectories are involved, so the bar is the fp32
 accumulation error alone:
 
-* fp32 outputs (forward with fp32 epilogue, dW, and every output of the fp32 mode's 3xTF32 kernels):
-  normwise max|gpu - f64| / max|f64| <= 1e-5 -- for 3xTF32 that is the fp32 mode's own bar (one-pass TF32 is ~1e-3);
+* fp32 outputs (forward with fp32 epilogue, dW, and every output of the fp32 mode's split-TF32 (4 MMAs) kernels):
+  normwise max|gpu - f64| / max|f64| <= 1e-5 -- for split-TF32 (4 MMAs) that is the fp32 mode's own bar (one-pass TF32 is ~1e-3);
 * bf16 outputs (forward, dX): correctly rounded up to that accumulation error, i.e.
   max(|gpu - f64| - ulp_bf16(f64)/2) / max|f64| <= 1e-5.
 
@@ -154,7 +154,7 @@ def test_gemm_rejects_bad_arguments():
         assert e.value.code == bns.BNS_ERR_INVALID
 
 
-# ---------------- fp32 mode: 3xTF32 (tcgen05 kind::tf32 on hi / lo operand splits) ----------------
+# ---------------- fp32 mode: split-TF32 (4 MMAs) (tcgen05 kind::tf32 on hi / lo operand splits) ----------------
 def f32(t):
     return t.float().contiguous()
 
