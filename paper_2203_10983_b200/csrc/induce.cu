@@ -169,7 +169,7 @@ struct InduceArgs {
     uint64_t* state; unsigned* ctr; uint32_t gen; int64_t ntiles;
 };
 
-__global__ void __launch_bounds__(kEdgeThreads) k_induce_fused(const InduceArgs a) {
+__global__ void __launch_bounds__(kEdgeThreads, 3) k_induce_fused(const InduceArgs a) {
     __shared__ int64_t s_tile, s_excl;
     __shared__ int s_warp[32], s_total;
     __shared__ uint32_t s_word[kEdgeThreads];
@@ -178,33 +178,33 @@ __global__ void __launch_bounds__(kEdgeThreads) k_induce_fused(const InduceArgs 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t e0 = t * (kEdgeThreads * 32);
     const int64_t e1 = min(a.nnz, e0 + kEdgeThreads * 32);
-    const int64_t ew = e0 + (int64_t)threadIdx.x * 32;   // this thread's 32-arc word
+    // warp w owns arcs [e0 + 1024 w, +1024): 32 coalesced 128 B loads, lane l holding arc 32 j + l in v[j]; the
+    // ballot of load j is the keep word of arcs 32 j .. 32 j + 31, kept by lane j (= this thread's word)
+    const int64_t ewarp = e0 + (int64_t)wid * 1024;
+    int32_t v[32];
     uint32_t word = 0;
-    if (ew + 32 <= a.nnz) {
-        const int4* p = reinterpret_cast<const int4*>(a.col_enc + ew);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int4 v = __ldg(p + q);
-            word |= (uint32_t)arc_kept(v.x, a.bkeep) << (4 * q);
-            word |= (uint32_t)arc_kept(v.y, a.bkeep) << (4 * q + 1);
-            word |= (uint32_t)arc_kept(v.z, a.bkeep) << (4 * q + 2);
-            word |= (uint32_t)arc_kept(v.w, a.bkeep) << (4 * q + 3);
-        }
-    } else if (ew < a.nnz) {
-        for (int j = 0; j < (int)(a.nnz - ew); ++j) word |= (uint32_t)arc_kept(a.col_enc[ew + j], a.bkeep) << j;
+    for (int j = 0; j < 32; ++j) {
+        const int64_t e = ewarp + 32 * j + lane;
+        v[j] = e < a.nnz ? __ldg(a.col_enc + e) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const int64_t e = ewarp + 32 * j + lane;
+        const unsigned b = __ballot_sync(0xffffffffu, e < a.nnz && arc_kept(v[j], a.bkeep));
+        if (lane == j) word = b;
     }
     s_word[threadIdx.x] = word;
     const int wex = block_excl_scan(__popc(word), s_warp, &s_total);
     s_wex[threadIdx.x] = wex;
     const int64_t excl = lookback(a.state, a.gen, t, s_total, &s_excl);   // (its barrier also publishes s_word / s_wex)
-    // warp-cooperative order-preserving scatter of the warp's 32 words: lane j takes arc 32k + j (coalesced)
-    const int64_t ewarp = e0 + (int64_t)wid * 1024;
+    // warp-cooperative order-preserving scatter of the warp's 32 words from the registers: lane l writes arc 32 k + l
+#pragma unroll
     for (int k = 0; k < 32; ++k) {
         const uint32_t wk = s_word[wid * 32 + k];
-        if (!((wk >> lane) & 1u)) continue;
-        const int32_t v = a.col_enc[ewarp + 32 * k + lane];
-        a.out_col[excl + s_wex[wid * 32 + k] + __popc(wk & ((1u << lane) - 1u))] =
-            v >= 0 ? v : (int32_t)a.n_in + a.slot_of_b[-v - 1];
+        if ((wk >> lane) & 1u)
+            a.out_col[excl + s_wex[wid * 32 + k] + __popc(wk & ((1u << lane) - 1u))] =
+                v[k] >= 0 ? v[k] : (int32_t)a.n_in + a.slot_of_b[-v[k] - 1];
     }
     // induced row pointers of the rows whose first static arc lies in this tile (setup table; the last tile also
     // takes the rows starting at nnz): kept arcs before that arc
