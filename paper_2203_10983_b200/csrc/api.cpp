@@ -428,13 +428,19 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.gflat_n = c.goff[L];
     c.d_gflat = static_cast<float*>(salloc(c, c.gflat_n * sizeof(float)));
     c.splitk_cap = 32 * wmax;
-    c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
     if (c.use_tc && c.prec == BNS_FP32) {   // fp32 dW runs K-major on transposed operands (gemm_tc.cu)
-        int64_t kn = 0;
-        for (int l = 0; l < L; ++l) kn = std::max<int64_t>(kn, 2 * (int64_t)c.dp[l] + 2 * (int64_t)c.dp[l + 1]);
-        c.tr_cap = kn * ((P.n_in + c.halo_cap + 3) / 4 * 4);
+        int64_t kn = 0, w2 = 0;
+        for (int l = 0; l < L; ++l) {
+            kn = std::max<int64_t>(kn, 2 * (int64_t)c.dp[l] + 2 * (int64_t)c.dp[l + 1]);
+            w2 = std::max<int64_t>(w2, 2 * (int64_t)c.dp[l] * c.dp[l + 1]);
+        }
+        const int64_t rows = P.n_in + c.halo_cap;
+        c.tr_cap = kn * ((rows + 3) / 4 * 4);
         c.d_tr = static_cast<float*>(dalloc(c, c.tr_cap * sizeof(float)));
+        // one partial slice per 512 nodes (16 k-blocks of 32: the split-TF32 accumulation-chain cap)
+        c.splitk_cap = std::max<int64_t>(c.splitk_cap, ((rows + 511) / 512 + 1) * w2);
     }
+    c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
     c.d_scal = static_cast<double*>(salloc(c, 4 * sizeof(double)));
     c.d_lpart = static_cast<double*>(dalloc(c, 4 * 2048 * sizeof(double)));   // k_xent / k_bce block partials
     c.d_nonfinite = static_cast<int32_t*>(dalloc(c, 16));
@@ -1125,11 +1131,12 @@ bns_status bns_gemm(int32_t precision, int32_t kind, int64_t M, int64_t N, int64
         std::vector<void*> mine;
         if (kind == 1 || kind == 2) {   // room for one fp32 K x N (x2) slice per split, up to 148 splits
             c.splitk_cap = 148 * (kind == 2 ? 2 : 1) * K * N;
-            c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
             if (precision == BNS_FP32) {
                 c.tr_cap = ((kind == 2 ? 2 : 1) * K + N) * ((M + 3) / 4 * 4);
                 c.d_tr = static_cast<float*>(dalloc(c, c.tr_cap * sizeof(float)));
+                c.splitk_cap = std::max<int64_t>(c.splitk_cap, ((M + 511) / 512 + 1) * (kind == 2 ? 2 : 1) * K * N);
             }
+            c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
         }
         const int64_t Kw = (K + 63) / 64 * 64;   // W^T concat halves are padded to 64 in both precisions
         try {

@@ -243,12 +243,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                         if (!F32) {
                             umma_bf16(d, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
                         } else {
-                            // hi·hi + hi·lo + lo·hi + lo·lo (lo tiles sit one [A | B] pair further, same layout)
+                            // hi·hi into the hi accumulator (columns [0, 128) of the buffer), hi·lo + lo·hi + lo·lo
+                            // into the lo accumulator ([128, 256)); lo tiles sit one [A | B] pair further
                             constexpr uint64_t lo = (uint64_t)(TC_HALF_BYTES >> 4);   // descriptor start-address units
-                            umma_tf32(d, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
-                            umma_tf32(d, ad, bd + lo, idesc, 1u);
-                            umma_tf32(d, ad + lo, bd, idesc, 1u);
-                            umma_tf32(d, ad + lo, bd + lo, idesc, 1u);
+                            const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+                            umma_tf32(d, ad, bd, idesc, acc);
+                            umma_tf32(d + 128, ad, bd + lo, idesc, acc);
+                            umma_tf32(d + 128, ad + lo, bd, idesc, 1u);
+                            umma_tf32(d + 128, ad + lo, bd + lo, idesc, 1u);
                         }
                     }
                     umma_commit(&empty[s]);     // stage free once these MMAs have read it
@@ -315,10 +317,20 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row >= args.M) continue;
                 float v[16];
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+                if (F32) {   // + the lo accumulator, 128 columns further (fp32 round-to-nearest add)
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                        : "r"(taddr + 128u));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) v[k] += __uint_as_float(r[k]);
+                }
+                if (row >= args.M) continue;
                 const int64_t col = n0 + c0;
                 if (rsc)
 #pragma unroll
@@ -435,7 +447,7 @@ void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64
     TcArgs a{};
     a.M = M;
     a.N = N;
-    a.BN = (int)std::min<int64_t>(256, cdiv(N, 16) * 16);
+    a.BN = (int)std::min<int64_t>(f32 ? 128 : 256, cdiv(N, 16) * 16);   // fp32: [hi | lo] accumulators of 128 columns
     // A1's k-blocks start where W^T's second concat half starts: each half is padded to a multiple of 64
     a.nk0 = A1 ? (int)(cdiv(K0, 64) * 64 / KE) : (int)cdiv(K0, KE);
     a.nk = a.nk0 + (int)cdiv(K1, KE);
@@ -487,14 +499,16 @@ static void wgrad_f32(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, 
     TcArgs a{};
     a.M = K2;
     a.N = N;
-    a.BN = (int)std::min<int64_t>(256, cdiv(N, 16) * 16);
+    a.BN = (int)std::min<int64_t>(128, cdiv(N, 16) * 16);
     a.nk = (int)cdiv(Mn, 32);
     a.nk0 = a.nk;
     const int64_t tiles = cdiv(K2, TC_BM) * cdiv(N, a.BN);
-    static const int kmin0 = [] { const char* e = std::getenv("BNS_WGRAD_KMIN"); return e ? std::max(1, std::atoi(e)) : 16; }();
-    const int kmin = kmin0 * 2;                // 32-node k-blocks: the same >= 1024 nodes per split as bf16
-    int64_t S = std::max<int64_t>(1, std::min<int64_t>(cdiv(148, tiles), std::max(1, a.nk / kmin)));
-    while (S > 1 && S * K2 * N > c.splitk_cap) --S;
+    // the tensor core's fp32 accumulation loses accuracy with the length of the accumulation chain (measured: the
+    // error grows linearly with the k-blocks per split, 2e-5 .. 6e-5 at 100 .. 250 blocks): at most kF32Chain
+    // 32-node k-blocks per split, the fixed-order split-K reduce then adds the partials in IEEE fp32
+    constexpr int kF32Chain = 16;
+    int64_t S = std::max<int64_t>(cdiv(a.nk, kF32Chain), std::min<int64_t>(cdiv(148, tiles), std::max(1, a.nk / 32)));
+    if (S * K2 * N > c.splitk_cap) throw Error(BNS_ERR_RUNTIME, "fp32 split-K partial buffer too small");
     a.kb_per_split = (int)cdiv(a.nk, S);
     S = cdiv(a.nk, a.kb_per_split);
     c.last_splitk = (int)S;
@@ -590,7 +604,7 @@ void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t
     TcArgs a{};
     a.M = M;
     a.N = Nc;
-    a.BN = (int)std::min<int64_t>(256, cdiv(Nc, 16) * 16);
+    a.BN = (int)std::min<int64_t>(f32 ? 128 : 256, cdiv(Nc, 16) * 16);
     a.nk = (int)cdiv(K, k_elems(c));
     a.nk0 = a.nk;
     a.epi = f32 ? (rowscale ? EPI_F32_ROWSCALE : EPI_F32) : (rowscale ? EPI_BF16_ROWSCALE : EPI_BF16);
