@@ -17,6 +17,8 @@
 // depends only on the row length.
 #include <cstdlib>
 
+#include <cuda.h>
+
 #include "common.h"
 #include "dev.cuh"
 #include "kernels.h"
@@ -289,6 +291,146 @@ k_spmm(const SpmmArgs a) {
     }
 }
 
+// ------------------------------------------------------------------------------------------------------------------
+// A/B variant (BNS_SPMM_TMA=1; bf16 rows of 256 elements = 512 B, the hidden-layer gathers of the Reddit shape):
+// the gathered rows are staged through shared memory by TMA (cp.async.bulk.tensor.2d.tile::gather4 -- four rows per
+// instruction, named by their row indices) into a per-warp ring of G4_STAGES x 4 rows tracked by mbarriers; lane 0
+// issues, all 32 lanes then read their 16-byte vector of each landed row from shared memory.  Same segments, same
+// claiming, same per-lane edge order and arithmetic as k_spmm<bf16, 32, 1, SC>, so the results are bitwise equal.
+// ------------------------------------------------------------------------------------------------------------------
+constexpr int G4_STAGES = 4;
+constexpr int G4_ROW_BYTES = 512;
+constexpr int G4_WARP_BYTES = G4_STAGES * 4 * G4_ROW_BYTES;   // 8 KB per warp
+
+__device__ __forceinline__ uint32_t g4_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int SC>
+__global__ void __launch_bounds__(256, 3) k_spmm_g4(const __grid_constant__ CUtensorMap map, const SpmmArgs a) {
+    extern __shared__ __align__(128) uint8_t g4_smem_raw[];
+    __shared__ __align__(8) uint64_t bars[8][G4_STAGES];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint8_t* ring = g4_smem_raw + w * G4_WARP_BYTES;
+    uint64_t* bar = bars[w];
+    if (lane == 0) {
+        for (int st = 0; st < G4_STAGES; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(g4_smem(&bar[st])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
+    }
+    __syncwarp();
+    uint32_t cons = 0;   // groups consumed by this warp so far (stage = cons % G4_STAGES, parity = cons / G4_STAGES)
+    auto issue = [&](int64_t e, int64_t e1, uint32_t idx) {   // lane 0: rows of edges e .. e + 3 into stage idx
+        const int st = (int)(idx % G4_STAGES);
+        int32_t r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = a.col[(e + j < e1) ? e + j : e];   // pad with a row the group reads
+        const uint32_t b = g4_smem(&bar[st]), dst = g4_smem(ring + st * 4 * G4_ROW_BYTES);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(4 * G4_ROW_BYTES) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+            ::"r"(dst), "l"(&map), "r"(0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(b) : "memory");
+    };
+    auto claim = [&]() -> int64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(a.work, 1ull);
+        return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+    };
+    for (int64_t sid = claim(); sid < a.n_segs; sid = claim()) {
+        const Seg s = a.segs[sid];
+        const int64_t ng = (s.e1 - s.e0 + 3) / 4;
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+        if (lane == 0)
+            for (int64_t g = 0; g < ng && g < G4_STAGES; ++g) issue(s.e0 + 4 * g, s.e1, cons + (uint32_t)g);
+        for (int64_t g = 0; g < ng; ++g, ++cons) {
+            const int st = (int)(cons % G4_STAGES);
+            const uint32_t par = (cons / G4_STAGES) & 1u;
+            const int64_t e = s.e0 + 4 * g;
+            const int cnt = (s.e1 - e < 4) ? (int)(s.e1 - e) : 4;
+            float sc[4] = {1.f, 1.f, 1.f, 1.f};
+            if (SC == 1)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j < cnt) sc[j] = (a.col[e + j] >= a.n_in) ? a.inv_p : 1.f;
+            uint32_t done = 0;
+            const uint32_t b = g4_smem(&bar[st]);
+            while (!done)
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                             "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(b), "r"(par) : "memory");
+            const uint4* rows = reinterpret_cast<const uint4*>(ring + st * 4 * G4_ROW_BYTES);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < cnt) acc_vec2<__nv_bfloat16, SC != 0>(acc2, rows[j * 32 + lane], SC ? pk2(sc[j], sc[j]) : 0ull);
+            __syncwarp();
+            if (lane == 0 && g + G4_STAGES < ng) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads before the TMA rewrite
+                issue(s.e0 + 4 * (g + G4_STAGES), s.e1, cons + G4_STAGES);
+            }
+        }
+        float acc[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) upk2(acc2[k], acc[2 * k], acc[2 * k + 1]);
+        if (s.nseg > 1) {
+            float* pp = a.partial + sid * (int64_t)a.d + lane * 8;
+            *reinterpret_cast<float4*>(pp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            *reinterpret_cast<float4*>(pp + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        } else {
+            epilogue_store<__nv_bfloat16>(a, s.row, lane, acc);
+        }
+    }
+}
+
+static bool spmm_tma() {
+    static const bool v = [] { const char* e = std::getenv("BNS_SPMM_TMA"); return e && e[0] == '1'; }();
+    return v;
+}
+
+typedef CUresult (*G4EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// the TMA path takes bf16 rows of exactly 256 elements, per-edge scale none or 1/p on halo columns
+static bool launch_spmm_g4(Ctx& c, SpmmArgs a, int sc) {
+    if (!spmm_tma() || c.prec != BNS_BF16 || a.d != 256 || (sc != 0 && sc != 1) || a.mode == GAT_FWD ||
+        a.mode == GAT_BWD || a.mode == GAT_RAW)
+        return false;
+    static G4EncodeFn enc = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess) p = nullptr;
+        return reinterpret_cast<G4EncodeFn>(p);
+    }();
+    if (!enc) throw Error(BNS_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap map;
+    const int64_t rows = c.plan.n_in + c.halo_cap;
+    cuuint64_t dims[2] = {(cuuint64_t)a.d, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(a.ld_src * 2)};
+    cuuint32_t box[2] = {(cuuint32_t)a.d, 1u};
+    cuuint32_t es[2] = {1u, 1u};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.src), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        throw Error(BNS_ERR_RUNTIME, "gather4 tensor map encode failed");
+    const int smem = 8 * G4_WARP_BYTES;
+    auto kern = sc ? k_spmm_g4<1> : k_spmm_g4<0>;
+    static bool cfg0 = false, cfg1 = false;
+    bool& cfg = sc ? cfg1 : cfg0;
+    if (!cfg) {
+        BNS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cfg = true;
+    }
+    int per_sm = 0;
+    BNS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.n_segs + 7) / 8, (int64_t)std::max(1, per_sm) * sms));
+    BNS_CUDA(cudaMemsetAsync(c.d_spmm_work, 0, sizeof(unsigned long long), c.stream));
+    a.work = c.d_spmm_work;
+    kern<<<grid, 256, smem, c.stream>>>(map, a);
+    return true;
+}
+
 // Sum the partials of every split row in segment order, then the same epilogue.
 template <typename T>
 __global__ void __launch_bounds__(256) k_spmm_fixup(const SpmmArgs a) {
@@ -376,6 +518,7 @@ static void go(Ctx& c, const SpmmArgs& a, unsigned grid) {
     if (a.sc >= 0) sc = a.sc;
     else if (a.mode == GCN_FWD) sc = 2;
     else if ((a.mode == SAGE_FWD || a.mode == SAGE_FWD_TF) && a.inv_p != 1.f) sc = 1;
+    if (LPR == 32 && VPL == 1 && launch_spmm_g4(c, a, sc)) return;
     if (sc == 0) go_sc<T, LPR, VPL, 0>(c, a, grid);
     else if (sc == 1) go_sc<T, LPR, VPL, 1>(c, a, grid);
     else if (sc == 2) go_sc<T, LPR, VPL, 2>(c, a, grid);
