@@ -9,6 +9,10 @@ mkdir -p "$OUT"
 python bench.py --steps 20 --warmup 5 --json-out "$OUT/bench_bf16.json" > "$OUT/bench_bf16.log" 2>&1
 python bench.py --steps 10 --warmup 3 --prec fp32 --no-cpu-baseline --json-out "$OUT/bench_fp32.json" > "$OUT/bench_fp32.log" 2>&1
 python bench.py --steps 10 --warmup 3 --config products --no-cpu-baseline --json-out "$OUT/bench_products.json" > "$OUT/bench_products.log" 2>&1
+# A/B: TMA tile::gather4 staged SpMM (bf16 256-wide rows) on the L2-resident (Reddit) and DRAM-resident shapes
+BNS_SPMM_TMA=1 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --json-out "$OUT/bench_bf16_tma.json" > "$OUT/bench_bf16_tma.log" 2>&1
+BNS_SPMM_TMA=1 python bench.py --steps 10 --warmup 3 --config yelp --no-cpu-baseline --no-e2e --json-out "$OUT/bench_yelp_tma.json" > "$OUT/bench_yelp_tma.log" 2>&1
+python bench.py --steps 10 --warmup 3 --config yelp --no-cpu-baseline --no-e2e --json-out "$OUT/bench_yelp.json" > "$OUT/bench_yelp.log" 2>&1
 ./build/gather_ceiling 20 > "$OUT/gather_ceiling.jsonl" 2>&1
 python scripts/ceiling_rmat.py > "$OUT/ceiling_rmat.jsonl" 2>&1
 for part in ldg2 random; do
@@ -37,5 +41,5 @@ timeout 600 ncu --set full --clock-control none -k regex:"k_induce_fused|k_sampl
     -o "$OUT/prof_induce" python scripts/emulate_rank.py --m 8 --p 0.1 --ranks 0 --partition ldg2 --cache-x0 \
     --steps 2 --warmup 1 > /dev/null 2>&1
 python scripts/ncu_summary.py full "$OUT/prof_induce.ncu-rep" "$OUT/induce.json" > /dev/null
-rm -f "$OUT"/prof_spmm_bwd.ncu-rep "$OUT"/prof_gemm.ncu-rep "$OUT"/*.csv
+rm -f "$OUT"/*.ncu-rep "$OUT"/*.csv
 du -sh "$OUT"/*
