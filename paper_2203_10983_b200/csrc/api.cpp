@@ -622,8 +622,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     }
     {
         PhaseTimer t(c, BNS_PH_UPDATE);
-        launch_wpack_all(c, W.data());
-        if (c.tf_mask) launch_wpack_tf(c);
+        launch_wpack_all(c, W.data());   // padded W, storage copy, W^T, and the R42 packs in one launch
     }
     const bool ebw = c.sampler != BNS_SAMPLER_BNS;   // f3: the sampled transposed CSR of this epoch
     EpochView ev;

@@ -100,9 +100,20 @@ __global__ void k_splitk_reduce(const float* __restrict__ part, int S, int64_t M
     const int64_t n4 = N / 4;
     if (t >= M * n4) return;
     int64_t i = t / n4, j = (t % n4) * 4;
+    const float* p0 = part + i * ldp + j;
+    const int64_t zs = M * ldp;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int z = 0; z < S; ++z) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(part + (int64_t)z * M * ldp + i * ldp + j));
+    int z = 0;
+    // eight slices' loads in flight (the kernel is latency-bound: ~1 resident warp group per SM), added in slice order
+    for (; z + 8 <= S; z += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(p0 + (int64_t)(z + q) * zs));
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { s.x += v[q].x; s.y += v[q].y; s.z += v[q].z; s.w += v[q].w; }
+    }
+    for (; z < S; ++z) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p0 + (int64_t)z * zs));
         s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
     }
     *reinterpret_cast<float4*>(out + i * ldo + j) = s;
@@ -110,7 +121,7 @@ __global__ void k_splitk_reduce(const float* __restrict__ part, int S, int64_t M
 
 void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw) {
     const int64_t tot = K * N;
-    k_splitk_reduce<<<(unsigned)((tot / 4 + 255) / 256), 256, 0, c.stream>>>(c.d_splitk, S, K, N, N, Wg, ldw);
+    k_splitk_reduce<<<(unsigned)((tot / 4 + 127) / 128), 128, 0, c.stream>>>(c.d_splitk, S, K, N, N, Wg, ldw);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }

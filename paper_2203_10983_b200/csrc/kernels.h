@@ -109,7 +109,6 @@ void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogi
 void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre,
                       const float* rs = nullptr, void* dps = nullptr);
 void launch_wpack_all(Ctx& c, float* const* W);
-void launch_wpack_tf(Ctx& c);
 void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr);
 void launch_adam(Ctx& c, float* const* W, float* const* G, float lr);
 void launch_dropout(Ctx& c, const void* src, void* dst, int64_t rows, int64_t ld, int layer);

@@ -156,12 +156,34 @@ void launch_scatter_rows(Ctx& c, void* dst, int64_t ld, const void* src, int32_t
 constexpr int kXentBlocks = 1184;   // 148 SMs x 8: enough warps to hide the per-row latency
 
 // NPL = logits per lane held in registers (C <= 32 NPL); the row is read once
+// the last block to finish sums the per-block partials (nv interleaved values) in a fixed order -- one warp,
+// lane-strided then a fixed butterfly: deterministic, and the same values as a separate final kernel would give
+__device__ __forceinline__ void last_block_final(const double* part, int nv, double* scal, unsigned* ctr) {
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32)
+        for (int q = 0; q < nv; ++q) {
+            double a = 0.0;
+            for (int k = lane; k < (int)gridDim.x; k += 32) a += __ldcg(part + nv * k + q);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (lane == 0) scal[q] = a;
+        }
+    if (threadIdx.x == 0) *ctr = 0u;
+}
+
 template <typename T, int NPL>
 __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, int64_t ld, int64_t n, int32_t C,
                                               const int32_t* __restrict__ labels, double inv_ntr,
                                               float* __restrict__ dlog, T* __restrict__ dpre,
                                               double* __restrict__ part, const float* __restrict__ rs,
-                                              T* __restrict__ dps) {
+                                              T* __restrict__ dps, double* __restrict__ scal, unsigned* ctr) {
     __shared__ double s_loss[8];
     __shared__ double s_cor[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -230,6 +252,7 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
         part[2 * blockIdx.x] = a;
         part[2 * blockIdx.x + 1] = b;
     }
+    last_block_final(part, 2, scal, ctr);
 }
 
 // f4 / R44 multi-label: per train row and class, softplus(x) - y x (= BCE(σ(x), y)); dLogits = (σ(x) - y) / (N_train C);
@@ -239,7 +262,7 @@ __global__ void __launch_bounds__(256) k_bce(const float* __restrict__ logits, i
                                              const int32_t* __restrict__ labels, const uint8_t* __restrict__ tgt,
                                              double inv, float* __restrict__ dlog, T* __restrict__ dpre,
                                              double* __restrict__ part, const float* __restrict__ rs,
-                                             T* __restrict__ dps) {
+                                             T* __restrict__ dps, double* __restrict__ scal, unsigned* ctr) {
     __shared__ double s_v[4][8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t warp = (int64_t)blockIdx.x * 8 + w;
@@ -290,18 +313,7 @@ __global__ void __launch_bounds__(256) k_bce(const float* __restrict__ logits, i
         for (int k = 0; k < 8; ++k) a += s_v[threadIdx.x][k];
         part[4 * blockIdx.x + threadIdx.x] = a;
     }
-}
-
-// one warp: lane-strided partial sums of nv interleaved values, then a fixed butterfly (deterministic)
-__global__ void k_xent_final(const double* __restrict__ part, int nb, int nv, double* __restrict__ scal) {
-    const int lane = threadIdx.x & 31;
-    for (int q = 0; q < nv; ++q) {
-        double a = 0.0;
-        for (int k = lane; k < nb; k += 32) a += part[nv * k + q];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (lane == 0) scal[q] = a;
-    }
+    last_block_final(part, 4, scal, ctr);
 }
 
 void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
@@ -311,7 +323,7 @@ void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogi
     const int npl = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
 #define BNS_BCE(T, NPL)                                                                                              \
     k_bce<T, NPL><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, n, C, c.d_labels, c.d_targets, inv, dlogits,        \
-                                                     (T*)dpre_t, c.d_lpart, rs, (T*)dps)
+                                                     (T*)dpre_t, c.d_lpart, rs, (T*)dps, c.d_scal, c.d_lb_ctr + 8)
     if (c.prec == BNS_BF16) {
         if (npl == 1) BNS_BCE(__nv_bfloat16, 1); else if (npl == 2) BNS_BCE(__nv_bfloat16, 2);
         else if (npl == 4) BNS_BCE(__nv_bfloat16, 4); else BNS_BCE(__nv_bfloat16, 8);
@@ -320,8 +332,7 @@ void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogi
         else if (npl == 4) BNS_BCE(float, 4); else BNS_BCE(float, 8);
     }
 #undef BNS_BCE
-    k_xent_final<<<1, 32, 0, c.stream>>>(c.d_lpart, kXentBlocks, 4, c.d_scal);
-    c.kernels += 2;
+    c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 
@@ -333,7 +344,7 @@ void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlog
     if (npl == 0) throw Error(BNS_ERR_INVALID, "more than 256 classes are not supported by k_xent");
 #define BNS_XENT(T, NPL)                                                                                          \
     k_xent<T, NPL><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, n, C, c.d_labels, inv, dlogits, (T*)dpre_t,   \
-                                                      c.d_lpart, rs, (T*)dps)
+                                                      c.d_lpart, rs, (T*)dps, c.d_scal, c.d_lb_ctr + 8)
     if (c.prec == BNS_BF16) {
         if (npl == 1) BNS_XENT(__nv_bfloat16, 1); else if (npl == 2) BNS_XENT(__nv_bfloat16, 2);
         else if (npl == 4) BNS_XENT(__nv_bfloat16, 4); else BNS_XENT(__nv_bfloat16, 8);
@@ -342,8 +353,7 @@ void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlog
         else if (npl == 4) BNS_XENT(float, 4); else BNS_XENT(float, 8);
     }
 #undef BNS_XENT
-    k_xent_final<<<1, 32, 0, c.stream>>>(c.d_lpart, kXentBlocks, 2, c.d_scal);
-    c.kernels += 2;
+    c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 
@@ -418,6 +428,9 @@ struct WDesc {
     const float* gpad[kMaxLayers];
     int64_t rows_p[kMaxLayers], cols_p[kMaxLayers], din[kMaxLayers], dpin[kMaxLayers], dout[kMaxLayers];
     int64_t K64[kMaxLayers], Kw[kMaxLayers];
+    void* Wcat[kMaxLayers];   // R42 transform-first layers: [W_top | W_bot] (storage type) and its transpose
+    void* WTtf[kMaxLayers];
+    uint32_t tf_mask;
     int L, kind, tc;
 };
 
@@ -427,16 +440,34 @@ __global__ void k_wpack_all(const WDesc d) {
     const int l = y % d.L;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t cp = d.cols_p[l];
+    // padded weight element (pr, pc) straight from the caller's logical weights
+    auto wval = [&](int64_t pr, int64_t pc) -> float {
+        const int64_t lr = logical_row(pr, d.kind, d.din[l], d.dpin[l]);
+        return (lr >= 0 && pc < d.dout[l]) ? d.W[l][lr * d.dout[l] + pc] : 0.f;
+    };
     if (y < d.L) {
         if (t >= d.rows_p[l] * cp) return;
         const int64_t pr = t / cp, pc = t % cp;
-        const int64_t lr = logical_row(pr, d.kind, d.din[l], d.dpin[l]);
-        const float v = (lr >= 0 && pc < d.dout[l]) ? d.W[l][lr * d.dout[l] + pc] : 0.f;
+        const float v = wval(pr, pc);
         d.Wp[l][t] = v;
         if (d.Wt[l] != (void*)d.Wp[l]) static_cast<T*>(d.Wt[l])[t] = from_f<T>(v);
+    } else if (y >= 2 * d.L) {
+        // R42: [W_top | W_bot] (dpin x 2 dpout) and its transpose (2 dpout x K64), same launch (no extra pass)
+        if (!((d.tf_mask >> l) & 1u)) return;
+        const int64_t dpin = d.dpin[l], dpout = cp, n2 = 2 * dpout, K64 = d.K64[l];
+        if (t < dpin * n2) {
+            const int64_t k = t / n2, c = t % n2;
+            static_cast<T*>(d.Wcat[l])[t] = from_f<T>(c < dpout ? wval(k, c) : wval(dpin + k, c - dpout));
+        }
+        if (d.WTtf[l] && t < n2 * K64) {
+            const int64_t n = t / K64, k = t % K64;
+            float v = 0.f;
+            if (k < dpin) v = n < dpout ? wval(k, n) : wval(dpin + k, n - dpout);
+            static_cast<T*>(d.WTtf[l])[t] = from_f<T>(v);
+        }
     } else {
         // W^T for the tcgen05 forward: WT[n][kw], kw = half * K64 + j <-> padded row half * dpin + j
-        if (t >= cp * d.Kw[l]) return;
+        if (!d.tc || t >= cp * d.Kw[l]) return;
         const int64_t n = t / d.Kw[l], kw = t % d.Kw[l];
         const int64_t half = kw / d.K64[l], j = kw % d.K64[l];
         float v = 0.f;
@@ -468,58 +499,27 @@ static WDesc make_desc(Ctx& c, float* const* W, float* const* G) {
         d.dout[l] = c.dims[l + 1];
         d.K64[l] = (c.dp[l] + 63) / 64 * 64;
         d.Kw[l] = c.wkw[l];
+        d.Wcat[l] = ((c.tf_mask >> l) & 1u) ? c.Wcat[l] : nullptr;
+        d.WTtf[l] = ((c.tf_mask >> l) & 1u) && c.use_tc ? c.WTtf[l] : nullptr;
     }
+    d.tf_mask = c.tf_mask;
     return d;
 }
 
 void launch_wpack_all(Ctx& c, float* const* W) {
     const WDesc d = make_desc(c, W, nullptr);
     int64_t mx = 0;
-    for (int l = 0; l < c.L; ++l)
+    for (int l = 0; l < c.L; ++l) {
         mx = std::max<int64_t>(std::max<int64_t>(mx, d.rows_p[l] * d.cols_p[l]), d.tc ? d.cols_p[l] * d.Kw[l] : 0);
-    const dim3 grid((unsigned)((mx + 255) / 256), (unsigned)(c.L * (d.tc ? 2 : 1)));
+        if ((c.tf_mask >> l) & 1u)
+            mx = std::max<int64_t>(mx, std::max(d.dpin[l] * 2 * d.cols_p[l], 2 * d.cols_p[l] * d.K64[l]));
+    }
+    // y: [0, L) padded W (+ storage copy), [L, 2L) W^T for the tensor cores, [2L, 3L) transform-first packs (R42)
+    const dim3 grid((unsigned)((mx + 255) / 256), (unsigned)(c.L * (c.tf_mask ? 3 : d.tc ? 2 : 1)));
     if (c.prec == BNS_BF16) k_wpack_all<__nv_bfloat16><<<grid, 256, 0, c.stream>>>(d);
     else k_wpack_all<float><<<grid, 256, 0, c.stream>>>(d);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
-}
-
-// R42: [W_top | W_bot] (dpin x 2 dpout) and its transpose (2 dpout x K64, the tensor-core B operand), both in the
-// storage type, for a transform-first layer, from the padded fp32 weights Wp (2 dpin x dpout) packed just before
-template <typename T>
-__global__ void k_wpack_tf(const float* __restrict__ Wp, int64_t dpin, int64_t dpout, int64_t K64, T* __restrict__ Wcat,
-                           T* __restrict__ WTtf) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t n2 = 2 * dpout;
-    if (t < dpin * n2) {
-        const int64_t k = t / n2, c = t % n2;
-        const float v = c < dpout ? Wp[k * dpout + c] : Wp[(dpin + k) * dpout + (c - dpout)];
-        Wcat[t] = from_f<T>(v);
-    }
-    if (WTtf && t < n2 * K64) {
-        const int64_t n = t / K64, k = t % K64;
-        float v = 0.f;
-        if (k < dpin) v = n < dpout ? Wp[k * dpout + n] : Wp[(dpin + k) * dpout + (n - dpout)];
-        WTtf[t] = from_f<T>(v);
-    }
-}
-
-void launch_wpack_tf(Ctx& c) {
-    for (int l = 0; l < c.L; ++l) {
-        if (!((c.tf_mask >> l) & 1u)) continue;
-        const int64_t dpin = c.dp[l], dpout = c.dp[l + 1], K64 = (dpin + 63) / 64 * 64;
-        const int64_t n = std::max(dpin * 2 * dpout, 2 * dpout * K64);
-        if (c.prec == BNS_BF16)
-            k_wpack_tf<__nv_bfloat16><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
-                c.Wpad[l], dpin, dpout, K64, static_cast<__nv_bfloat16*>(c.Wcat[l]),
-                static_cast<__nv_bfloat16*>(c.use_tc ? c.WTtf[l] : nullptr));
-        else
-            k_wpack_tf<float><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
-                c.Wpad[l], dpin, dpout, K64, static_cast<float*>(c.Wcat[l]),
-                static_cast<float*>(c.use_tc ? c.WTtf[l] : nullptr));
-        c.kernels += 1;
-        BNS_CHECK_LAUNCH();
-    }
 }
 
 // a14 W <- W - lr g for every layer (g copied to the caller); skipped when the all-reduced loss is not finite
