@@ -334,7 +334,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.d_ind_col = static_cast<int32_t*>(dalloc(c, (c.nnz_i + 1) * sizeof(int32_t)));
     {
         const int64_t nb = (c.nnz_i + 1023) / 1024;
-        c.d_ebits = static_cast<uint32_t*>(dalloc(c, (nb * 32 + 32) * sizeof(uint32_t)));
+        c.d_ebits = static_cast<uint32_t*>(dalloc(c, (nb * 32 + kInduceTileArcs / 32 + 32) * sizeof(uint32_t)));
         c.d_eblk = static_cast<int32_t*>(dalloc(c, (nb + 1) * sizeof(int32_t)));
         c.d_eboff = static_cast<int64_t*>(dalloc(c, (nb + 2) * sizeof(int64_t)));
     }

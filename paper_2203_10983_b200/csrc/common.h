@@ -47,7 +47,7 @@ __host__ __device__ inline int32_t seg_count(int64_t cnt, int32_t seg_long) {
     const int64_t L = seg_len(cnt, seg_long);
     return cnt > L ? (int32_t)((cnt + L - 1) / L) : 1;
 }
-constexpr int64_t kInduceTileArcs = 8192;   // induce.cu: arcs per tile (256 threads x one 32-arc word)
+constexpr int64_t kInduceTileArcs = 32768;  // induce.cu: arcs per tile (1024 threads x one 32-arc word)
 constexpr int kPad = 8;            // feature dims padded to multiples of 8 (16-byte rows for fp32x4 / bf16x8)
 
 inline int64_t pad8(int64_t d) { return (d + kPad - 1) / kPad * kPad; }

@@ -3,13 +3,14 @@
 //   k_sample_fused   Alg.1 l.4 (R5-R7, R23): the Philox Bernoulli draw of every candidate, the
 //                    order-preserving compaction into [U_i ; S_{i,*}] (Alg.1 l.6-7, R24, R27), the boundary keep
 //                    bitmask the induce pass tests against, slot_of_b and the 2m+1 segment offsets (per-peer counts).
-//   k_induce_fused   Alg.1 l.5: the node-induced subgraph on V_i ∪ U_i -- keep bit of every static
-//                    arc (inner columns always, boundary columns by the bitmask), the kept columns scattered in global
-//                    neighbour order and remapped to halo rows n_in + slot, and the induced row pointers.
+//   k_induce_count / k_induce_scatter   Alg.1 l.5: the node-induced subgraph on V_i ∪ U_i -- keep
+//                    bit of every static arc (inner columns always, boundary columns by the bitmask), then the kept
+//                    columns scattered in global neighbour order and remapped to halo rows n_in + slot, and the
+//                    induced row pointers (two independent passes: per-tile counts, then prefix + scatter).
 //   k_segs_fused     SpMM work lists: forward segments of the induced rows and backward (transposed) segments of the
 //                    sampled halo rows, both chains in one launch, split (hub) rows appended for the fixup.
 //
-// Each kernel is one pass over its tiles: a tile publishes its aggregate, looks back over its predecessors' published
+// The draw and the segment lists are one pass over their tiles (a few hundred): a tile publishes its aggregate, looks back over its predecessors' published
 // aggregates / inclusive prefixes (a warp reads 32 predecessors at a time), and then writes its outputs at their final
 // positions.  Tiles are handed out in launch order by an atomic counter (a tile only waits on tiles that already
 // started, so the look-back cannot deadlock); the tile states carry a launch generation, so nothing is cleared between
@@ -166,45 +167,72 @@ __device__ __forceinline__ bool arc_kept(int32_t x, const uint32_t* __restrict__
 struct InduceArgs {
     const int32_t* col_enc; int64_t nnz; const uint32_t* bkeep; const int32_t* slot_of_b; int64_t n_in;
     const int64_t* row_ptr; const int64_t* tile_row; int32_t* out_col; int64_t* out_ptr; int64_t* total;
-    uint64_t* state; unsigned* ctr; uint32_t gen; int64_t ntiles;
+    uint32_t* words; int32_t* tile_cnt; int64_t ntiles;
 };
 
-__global__ void __launch_bounds__(kEdgeThreads, 3) k_induce_fused(const InduceArgs a) {
-    __shared__ int64_t s_tile, s_excl;
-    __shared__ int s_warp[32], s_total;
-    __shared__ uint32_t s_word[kEdgeThreads];
-    __shared__ int s_wex[kEdgeThreads];
-    const int64_t t = next_tile(a.ctr, a.ntiles, &s_tile);
+// pass 1: keep word of every 32-arc block (warp w of a tile owns arcs [e0 + 1024 w, +1024): 32 coalesced 128 B loads,
+// lane l holding arc 32 j + l in v[j]; the ballot of load j is the keep word of arcs 32 j .. 32 j + 31) and the kept
+// count of every tile.  No inter-tile dependency: a look-back chain over ~2,000 tiles measured 95-127 us here (the
+// inclusive prefix only travels ~32 tiles per round trip); two independent passes take a few microseconds each.
+__global__ void __launch_bounds__(kEdgeThreads) k_induce_count(const InduceArgs a) {
+    __shared__ int s_warp[32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t e0 = t * (kEdgeThreads * 32);
-    const int64_t e1 = min(a.nnz, e0 + kEdgeThreads * 32);
-    // warp w owns arcs [e0 + 1024 w, +1024): 32 coalesced 128 B loads, lane l holding arc 32 j + l in v[j]; the
-    // ballot of load j is the keep word of arcs 32 j .. 32 j + 31, kept by lane j (= this thread's word)
-    const int64_t ewarp = e0 + (int64_t)wid * 1024;
+    const int64_t ewarp = (int64_t)blockIdx.x * kInduceTileArcs + (int64_t)wid * 1024;
     int32_t v[32];
-    uint32_t word = 0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         const int64_t e = ewarp + 32 * j + lane;
         v[j] = e < a.nnz ? __ldg(a.col_enc + e) : 0;
     }
+    uint32_t word = 0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         const int64_t e = ewarp + 32 * j + lane;
         const unsigned b = __ballot_sync(0xffffffffu, e < a.nnz && arc_kept(v[j], a.bkeep));
         if (lane == j) word = b;
     }
-    s_word[threadIdx.x] = word;
-    const int wex = block_excl_scan(__popc(word), s_warp, &s_total);
-    s_wex[threadIdx.x] = wex;
-    const int64_t excl = lookback(a.state, a.gen, t, s_total, &s_excl);   // (its barrier also publishes s_word / s_wex)
-    // warp-cooperative order-preserving scatter of the warp's 32 words from the registers: lane l writes arc 32 k + l
+    a.words[(int64_t)blockIdx.x * kEdgeThreads + threadIdx.x] = word;
+    int c = __popc(word);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) s_warp[wid] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int k = 0; k < kEdgeThreads / 32; ++k) t += s_warp[k];
+        a.tile_cnt[blockIdx.x] = t;
+    }
+}
+
+// pass 2: the tile's exclusive prefix = sum of the earlier tiles' counts (one block reduction, fixed order), the
+// order-preserving scatter of the kept (remapped) columns and the induced row pointers of the rows starting in the tile
+__global__ void __launch_bounds__(kEdgeThreads) k_induce_scatter(const InduceArgs a) {
+    __shared__ int s_warp[32], s_total;
+    __shared__ int64_t s_pre[32];
+    __shared__ uint32_t s_word[kEdgeThreads];
+    __shared__ int s_wex[kEdgeThreads];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t t = blockIdx.x;
+    int64_t pre = 0;
+    for (int64_t k = threadIdx.x; k < t; k += kEdgeThreads) pre += a.tile_cnt[k];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    if (lane == 0) s_pre[wid] = pre;
+    const uint32_t word = a.words[t * kEdgeThreads + threadIdx.x];
+    s_word[threadIdx.x] = word;
+    const int wex = block_excl_scan(__popc(word), s_warp, &s_total);   // (its barriers also publish s_pre)
+    s_wex[threadIdx.x] = wex;
+    int64_t excl = 0;
+    for (int k = 0; k < kEdgeThreads / 32; ++k) excl += s_pre[k];
+    __syncthreads();
+    const int64_t e0 = t * kInduceTileArcs, e1 = min(a.nnz, e0 + kInduceTileArcs);
+    const int64_t ewarp = e0 + (int64_t)wid * 1024;
+    for (int k = 0; k < 32; ++k) {   // warp-cooperative: lane l writes arc 32 k + l of the warp's block (coalesced)
         const uint32_t wk = s_word[wid * 32 + k];
-        if ((wk >> lane) & 1u)
-            a.out_col[excl + s_wex[wid * 32 + k] + __popc(wk & ((1u << lane) - 1u))] =
-                v[k] >= 0 ? v[k] : (int32_t)a.n_in + a.slot_of_b[-v[k] - 1];
+        if (!((wk >> lane) & 1u)) continue;
+        const int32_t x = a.col_enc[ewarp + 32 * k + lane];
+        a.out_col[excl + s_wex[wid * 32 + k] + __popc(wk & ((1u << lane) - 1u))] =
+            x >= 0 ? x : (int32_t)a.n_in + a.slot_of_b[-x - 1];
     }
     // induced row pointers of the rows whose first static arc lies in this tile (setup table; the last tile also
     // takes the rows starting at nnz): kept arcs before that arc
@@ -312,7 +340,7 @@ void launch_induce_fused(Ctx& c) {
     const int m = c.cfg.world;
     int64_t* tot = c.d_seg_pos + 2 * m + 1;
     const int64_t nnz = c.nnz_i;
-    const int64_t nt = (nnz + kEdgeThreads * 32 - 1) / (kEdgeThreads * 32);
+    const int64_t nt = (nnz + kInduceTileArcs - 1) / kInduceTileArcs;
     if (nt == 0) {
         BNS_CUDA(cudaMemsetAsync(c.d_ind_ptr, 0, (c.plan.n_in + 1) * sizeof(int64_t), c.stream));
         BNS_CUDA(cudaMemsetAsync(tot, 0, sizeof(int64_t), c.stream));
@@ -321,9 +349,10 @@ void launch_induce_fused(Ctx& c) {
     InduceArgs a{};
     a.col_enc = c.d_col_enc; a.nnz = nnz; a.bkeep = c.d_bkeep; a.slot_of_b = c.d_slot_of_b; a.n_in = c.plan.n_in;
     a.row_ptr = c.d_row_ptr; a.tile_row = c.d_tile_row; a.out_col = c.d_ind_col; a.out_ptr = c.d_ind_ptr; a.total = tot;
-    a.state = c.d_lb_state + c.lb_off_induce; a.ctr = c.d_lb_ctr + 1; a.gen = ++c.lb_gen; a.ntiles = nt;
-    k_induce_fused<<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
-    c.kernels += 1;
+    a.words = c.d_ebits; a.tile_cnt = c.d_eblk; a.ntiles = nt;
+    k_induce_count<<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
+    k_induce_scatter<<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
+    c.kernels += 2;
     BNS_CHECK_LAUNCH();
 }
 
