@@ -227,12 +227,26 @@ __global__ void __launch_bounds__(kEdgeThreads) k_induce_scatter(const InduceArg
     __syncthreads();
     const int64_t e0 = t * kInduceTileArcs, e1 = min(a.nnz, e0 + kInduceTileArcs);
     const int64_t ewarp = e0 + (int64_t)wid * 1024;
-    for (int k = 0; k < 32; ++k) {   // warp-cooperative: lane l writes arc 32 k + l of the warp's block (coalesced)
-        const uint32_t wk = s_word[wid * 32 + k];
-        if (!((wk >> lane) & 1u)) continue;
-        const int32_t x = a.col_enc[ewarp + 32 * k + lane];
-        a.out_col[excl + s_wex[wid * 32 + k] + __popc(wk & ((1u << lane) - 1u))] =
-            x >= 0 ? x : (int32_t)a.n_in + a.slot_of_b[-x - 1];
+    // warp-cooperative: lane l writes arc 32 k + l of the warp's block (coalesced).  All 32 column loads, then all
+    // slot lookups, then the stores: with the stores in the same loop the loads of the next word could not be hoisted
+    // (possible aliasing) and each word cost a dependent round trip (~1 us) -- 32 of them per warp.
+    const int32_t* __restrict__ col = a.col_enc;
+    const int32_t* __restrict__ slot = a.slot_of_b;
+    int32_t* __restrict__ out = a.out_col;
+#pragma unroll 1
+    for (int h = 0; h < 32; h += 16) {   // two batches of 16 words (register budget of a 1024-thread block)
+        int32_t x[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            x[k] = ((s_word[wid * 32 + h + k] >> lane) & 1u) ? __ldg(col + ewarp + 32 * (h + k) + lane) : 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (x[k] < 0) x[k] = (int32_t)a.n_in + __ldg(slot - x[k] - 1);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t wk = s_word[wid * 32 + h + k];
+            if ((wk >> lane) & 1u) out[excl + s_wex[wid * 32 + h + k] + __popc(wk & ((1u << lane) - 1u))] = x[k];
+        }
     }
     // induced row pointers of the rows whose first static arc lies in this tile (setup table; the last tile also
     // takes the rows starting at nnz): kept arcs before that arc

@@ -181,12 +181,24 @@ __global__ void __launch_bounds__(256) k_induce_scatter_w(const int32_t* __restr
     const int64_t base = (w >> 5) < ((nnz + 1023) >> 10) ? boff[w >> 5] : 0;
     const int64_t e_blk = (w - lane) << 5;
     const int excl = x - c;
-    for (int k = 0; k < 32; ++k) {
-        const uint32_t wk = __shfl_sync(0xffffffffu, word, k);
-        const int ek = __shfl_sync(0xffffffffu, excl, k);
-        if (!((wk >> lane) & 1u)) continue;
-        const int32_t v = col[e_blk + 32 * k + lane];
-        out_col[base + ek + __popc(wk & ((1u << lane) - 1u))] = v >= 0 ? v : (int32_t)n_in + slot_of_b[-v - 1];
+    // loads of a batch of words first, then the stores (stores interleaved with the loads serialise them)
+#pragma unroll 1
+    for (int h = 0; h < 32; h += 16) {
+        int32_t v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t wk = __shfl_sync(0xffffffffu, word, h + k);
+            v[k] = ((wk >> lane) & 1u) ? __ldg(col + e_blk + 32 * (h + k) + lane) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (v[k] < 0) v[k] = (int32_t)n_in + __ldg(slot_of_b - v[k] - 1);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t wk = __shfl_sync(0xffffffffu, word, h + k);
+            const int ek = __shfl_sync(0xffffffffu, excl, h + k);
+            if ((wk >> lane) & 1u) out_col[base + ek + __popc(wk & ((1u << lane) - 1u))] = v[k];
+        }
     }
 }
 
