@@ -167,15 +167,20 @@ __device__ __forceinline__ bool arc_kept(int32_t x, const uint32_t* __restrict__
 struct InduceArgs {
     const int32_t* col_enc; int64_t nnz; const uint32_t* bkeep; const int32_t* slot_of_b; int64_t n_in;
     const int64_t* row_ptr; const int64_t* tile_row; int32_t* out_col; int64_t* out_ptr; int64_t* total;
-    uint32_t* words; int32_t* tile_cnt; int64_t ntiles;
+    uint32_t* words; int32_t* tile_cnt; int64_t ntiles; int64_t nbw;
 };
 
 // pass 1: keep word of every 32-arc block (warp w of a tile owns arcs [e0 + 1024 w, +1024): 32 coalesced 128 B loads,
 // lane l holding arc 32 j + l in v[j]; the ballot of load j is the keep word of arcs 32 j .. 32 j + 31) and the kept
 // count of every tile.  No inter-tile dependency: a look-back chain over ~2,000 tiles measured 95-127 us here (the
 // inclusive prefix only travels ~32 tiles per round trip); two independent passes take a few microseconds each.
+// SMEM: the boundary keep bitmask (|B_i| / 8 bytes) copied into shared memory first -- a warp's 32 lookups hit 32
+// random words, which L1 serves one sector per lane (the pass measured 48 us L1-bound at m = 8); shared memory
+// serves them in a few bank-conflict replays
+template <bool SMEM>
 __global__ void __launch_bounds__(kEdgeThreads) k_induce_count(const InduceArgs a) {
     __shared__ int s_warp[32];
+    extern __shared__ uint32_t s_bk[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ewarp = (int64_t)blockIdx.x * kInduceTileArcs + (int64_t)wid * 1024;
     int32_t v[32];
@@ -184,12 +189,23 @@ __global__ void __launch_bounds__(kEdgeThreads) k_induce_count(const InduceArgs 
         const int64_t e = ewarp + 32 * j + lane;
         v[j] = e < a.nnz ? __ldg(a.col_enc + e) : 0;
     }
+    if (SMEM) {
+        for (int64_t k = threadIdx.x; k < a.nbw; k += blockDim.x) s_bk[k] = __ldg(a.bkeep + k);
+        __syncthreads();
+    }
     uint32_t word = 0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         const int64_t e = ewarp + 32 * j + lane;
-        const unsigned b = __ballot_sync(0xffffffffu, e < a.nnz && arc_kept(v[j], a.bkeep));
-        if (lane == j) word = b;
+        bool kept;
+        if (SMEM) {
+            const uint32_t b = (uint32_t)(-v[j] - 1);
+            kept = v[j] >= 0 || ((s_bk[b >> 5] >> (b & 31)) & 1u);
+        } else {
+            kept = arc_kept(v[j], a.bkeep);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, e < a.nnz && kept);
+        if (lane == j) word = bal;
     }
     a.words[(int64_t)blockIdx.x * kEdgeThreads + threadIdx.x] = word;
     int c = __popc(word);
@@ -364,7 +380,19 @@ void launch_induce_fused(Ctx& c) {
     a.col_enc = c.d_col_enc; a.nnz = nnz; a.bkeep = c.d_bkeep; a.slot_of_b = c.d_slot_of_b; a.n_in = c.plan.n_in;
     a.row_ptr = c.d_row_ptr; a.tile_row = c.d_tile_row; a.out_col = c.d_ind_col; a.out_ptr = c.d_ind_ptr; a.total = tot;
     a.words = c.d_ebits; a.tile_cnt = c.d_eblk; a.ntiles = nt;
-    k_induce_count<<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
+    a.nbw = (c.plan.n_bd + 31) / 32;
+    constexpr int64_t kSmemMax = 96 << 10;   // bitmask up to 768 K boundary nodes in shared memory
+    if (a.nbw * 4 <= kSmemMax) {
+        static bool cfg = false;
+        if (!cfg) {
+            BNS_CUDA(cudaFuncSetAttribute(k_induce_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kSmemMax));
+            cfg = true;
+        }
+        k_induce_count<true><<<(unsigned)nt, kEdgeThreads, (size_t)(a.nbw * 4), c.stream>>>(a);
+    } else {
+        k_induce_count<false><<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
+    }
     k_induce_scatter<<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
