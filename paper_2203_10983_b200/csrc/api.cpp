@@ -231,12 +231,12 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     // ---- static plan on device
     c.d_row_ptr = upload(c, P.row_ptr);
     c.d_col_enc = upload(c, P.col_enc);
-    {   // induce tiles (induce.cu, kInduceTileArcs static arcs each): first row starting in every tile
-        const int64_t nt = (c.nnz_i + kInduceTileArcs - 1) / kInduceTileArcs;
+    {   // induce (induce.cu): first inner row whose first static arc lies in each 1024-arc chunk
+        const int64_t nt = (c.nnz_i + 1023) / 1024;
         std::vector<int64_t> tr(nt + 1);
         int64_t r = 0;
         for (int64_t t = 0; t <= nt; ++t) {
-            const int64_t e0 = std::min<int64_t>(t * kInduceTileArcs, c.nnz_i + 1);
+            const int64_t e0 = std::min<int64_t>(t * 1024, c.nnz_i + 1);
             while (r <= P.n_in && P.row_ptr[r] < e0) ++r;
             tr[t] = r;
         }
@@ -335,6 +335,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     {
         const int64_t nb = (c.nnz_i + 1023) / 1024;
         c.d_ebits = static_cast<uint32_t*>(dalloc(c, (nb * 32 + kInduceTileArcs / 32 + 32) * sizeof(uint32_t)));
+        c.d_ewex = static_cast<int32_t*>(dalloc(c, (nb * 32 + kInduceTileArcs / 32 + 32) * sizeof(int32_t)));
         c.d_eblk = static_cast<int32_t*>(dalloc(c, (nb + 1) * sizeof(int32_t)));
         c.d_eboff = static_cast<int64_t*>(dalloc(c, (nb + 2) * sizeof(int64_t)));
     }

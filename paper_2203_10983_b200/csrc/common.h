@@ -149,7 +149,7 @@ struct Ctx {
     int32_t* d_cand_out = nullptr; // compacted payloads: [U_b (|U|) ; S_local (ΣS)]
     int32_t* d_slot_of_b = nullptr;
     uint32_t* d_bkeep = nullptr;   // keep bit per boundary node (induce)
-    int64_t* d_tile_row = nullptr;  // induce tile t: first inner row whose first static arc lies in it (setup)
+    int64_t* d_tile_row = nullptr;  // induce: first inner row whose first static arc lies in each 1024-arc chunk
     uint64_t* d_lb_state = nullptr; // decoupled look-back tile states (induce.cu): draw | induce | segs fwd | segs bwd
     unsigned* d_lb_ctr = nullptr;   // tile-order counters of those four chains (each reset by its last tile)
     int64_t lb_off_induce = 0, lb_off_segf = 0, lb_off_segb = 0;
@@ -157,6 +157,7 @@ struct Ctx {
     int64_t* d_seg_pos = nullptr;  // [2m+1] compacted segment offsets
     int64_t* h_seg_pos = nullptr;  // pinned host copy
     uint32_t* d_ebits = nullptr;   // induce: keep bit per static edge
+    int32_t* d_ewex = nullptr;     // induce: exclusive kept-arc prefix of every 32-arc word inside its tile
     int32_t* d_eblk = nullptr;     // induce: kept edges per 1024-edge block
     int64_t* d_eboff = nullptr;    // induce: scanned block offsets
     int64_t* d_ind_ptr = nullptr;  // induced CSR (n_in+1)

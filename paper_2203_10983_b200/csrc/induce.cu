@@ -167,19 +167,20 @@ __device__ __forceinline__ bool arc_kept(int32_t x, const uint32_t* __restrict__
 struct InduceArgs {
     const int32_t* col_enc; int64_t nnz; const uint32_t* bkeep; const int32_t* slot_of_b; int64_t n_in;
     const int64_t* row_ptr; const int64_t* tile_row; int32_t* out_col; int64_t* out_ptr; int64_t* total;
-    uint32_t* words; int32_t* tile_cnt; int64_t ntiles; int64_t nbw;
+    uint32_t* words; int32_t* wex; int32_t* tile_cnt; int64_t* tile_pre; unsigned* ctr; int64_t ntiles; int64_t nbw;
 };
 
-// pass 1: keep word of every 32-arc block (warp w of a tile owns arcs [e0 + 1024 w, +1024): 32 coalesced 128 B loads,
-// lane l holding arc 32 j + l in v[j]; the ballot of load j is the keep word of arcs 32 j .. 32 j + 31) and the kept
-// count of every tile.  No inter-tile dependency: a look-back chain over ~2,000 tiles measured 95-127 us here (the
-// inclusive prefix only travels ~32 tiles per round trip); two independent passes take a few microseconds each.
-// SMEM: the boundary keep bitmask (|B_i| / 8 bytes) copied into shared memory first -- a warp's 32 lookups hit 32
-// random words, which L1 serves one sector per lane (the pass measured 48 us L1-bound at m = 8); shared memory
-// serves them in a few bank-conflict replays
+// pass 1 (one block per tile of kInduceTileArcs arcs): the keep word of every 32-arc block -- warp w owns arcs
+// [e0 + 1024 w, +1024): 32 coalesced 128 B loads, lane l holding arc 32 j + l in v[j]; the ballot of load j is the
+// keep word of arcs 32 j .. 32 j + 31 -- its exclusive prefix inside the tile, and the tile's count.  The last block
+// to finish scans the tile counts into tile prefixes.  No look-back chain (over ~2,000 tiles one measured 95-127 us:
+// the inclusive prefix travels ~32 tiles per round trip).
+// SMEM: the boundary keep bitmask (|B_i| / 8 bytes) is staged in shared memory -- a warp's 32 lookups hit 32 random
+// words, which L1 serves one sector per lane (the pass measured 48 us L1-bound at m = 8).
 template <bool SMEM>
 __global__ void __launch_bounds__(kEdgeThreads) k_induce_count(const InduceArgs a) {
-    __shared__ int s_warp[32];
+    __shared__ int s_warp[32], s_total;
+    __shared__ bool s_last;
     extern __shared__ uint32_t s_bk[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ewarp = (int64_t)blockIdx.x * kInduceTileArcs + (int64_t)wid * 1024;
@@ -207,78 +208,80 @@ __global__ void __launch_bounds__(kEdgeThreads) k_induce_count(const InduceArgs 
         const unsigned bal = __ballot_sync(0xffffffffu, e < a.nnz && kept);
         if (lane == j) word = bal;
     }
-    a.words[(int64_t)blockIdx.x * kEdgeThreads + threadIdx.x] = word;
-    int c = __popc(word);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) s_warp[wid] = c;
+    const int64_t wi = (int64_t)blockIdx.x * kEdgeThreads + threadIdx.x;
+    a.words[wi] = word;
+    a.wex[wi] = block_excl_scan(__popc(word), s_warp, &s_total);
+    if (threadIdx.x == 0) a.tile_cnt[blockIdx.x] = s_total;
+    // last block: exclusive scan of the tile counts (fixed order) -> tile prefixes and the kept total
+    __threadfence();
     __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.ctr, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    int64_t carry = 0;
+    for (int64_t base = 0; base < a.ntiles; base += blockDim.x) {
+        const int64_t k = base + threadIdx.x;
+        const int c = k < a.ntiles ? __ldcg(a.tile_cnt + k) : 0;
+        const int ex = block_excl_scan(c, s_warp, &s_total);
+        if (k < a.ntiles) a.tile_pre[k] = carry + ex;
+        carry += s_total;
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
-        int t = 0;
-        for (int k = 0; k < kEdgeThreads / 32; ++k) t += s_warp[k];
-        a.tile_cnt[blockIdx.x] = t;
+        *a.total = carry;
+        *a.ctr = 0u;
     }
 }
 
-// pass 2: the tile's exclusive prefix = sum of the earlier tiles' counts (one block reduction, fixed order), the
-// order-preserving scatter of the kept (remapped) columns and the induced row pointers of the rows starting in the tile
-__global__ void __launch_bounds__(kEdgeThreads) k_induce_scatter(const InduceArgs a) {
-    __shared__ int s_warp[32], s_total;
-    __shared__ int64_t s_pre[32];
-    __shared__ uint32_t s_word[kEdgeThreads];
-    __shared__ int s_wex[kEdgeThreads];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t t = blockIdx.x;
-    int64_t pre = 0;
-    for (int64_t k = threadIdx.x; k < t; k += kEdgeThreads) pre += a.tile_cnt[k];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
-    if (lane == 0) s_pre[wid] = pre;
-    const uint32_t word = a.words[t * kEdgeThreads + threadIdx.x];
-    s_word[threadIdx.x] = word;
-    const int wex = block_excl_scan(__popc(word), s_warp, &s_total);   // (its barriers also publish s_pre)
-    s_wex[threadIdx.x] = wex;
-    int64_t excl = 0;
-    for (int k = 0; k < kEdgeThreads / 32; ++k) excl += s_pre[k];
-    __syncthreads();
-    const int64_t e0 = t * kInduceTileArcs, e1 = min(a.nnz, e0 + kInduceTileArcs);
-    const int64_t ewarp = e0 + (int64_t)wid * 1024;
-    // warp-cooperative: lane l writes arc 32 k + l of the warp's block (coalesced).  All 32 column loads, then all
-    // slot lookups, then the stores: with the stores in the same loop the loads of the next word could not be hoisted
-    // (possible aliasing) and each word cost a dependent round trip (~1 us) -- 32 of them per warp.
+// pass 2 (one warp per 1024-arc chunk, no block barriers): lane j loads word j and its in-tile prefix, every lane
+// issues the column loads of its kept arcs of all 32 words, then the slot lookups of the kept halo columns, then the
+// order-preserving stores (remapped: halo column -> n_in + slot); then the induced row pointers of the rows whose first
+// static arc lies in this chunk (kept arcs before that arc, from the setup tile table and pass 1's words / prefixes)
+__global__ void __launch_bounds__(256) k_induce_scatter(const InduceArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nchunks = (a.nnz + 1023) >> 10;
+    if (chunk >= nchunks) return;
+    constexpr int kChunksPerTile = (int)(kInduceTileArcs / 1024);
+    const int64_t t = chunk / kChunksPerTile;
+    const int64_t ec = chunk * 1024;
+    const int64_t wbase = chunk * 32;   // word index of word 0 of this chunk
+    const uint32_t myword = a.words[wbase + lane];
+    const int64_t base = __ldg(a.tile_pre + t) + a.wex[wbase + lane];   // lane j: output position of word j
     const int32_t* __restrict__ col = a.col_enc;
     const int32_t* __restrict__ slot = a.slot_of_b;
     int32_t* __restrict__ out = a.out_col;
 #pragma unroll 1
-    for (int h = 0; h < 32; h += 16) {   // two batches of 16 words (register budget of a 1024-thread block)
+    for (int h = 0; h < 32; h += 16) {
         int32_t x[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-            x[k] = ((s_word[wid * 32 + h + k] >> lane) & 1u) ? __ldg(col + ewarp + 32 * (h + k) + lane) : 0;
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t wk = __shfl_sync(0xffffffffu, myword, h + k);
+            x[k] = ((wk >> lane) & 1u) ? __ldg(col + ec + 32 * (h + k) + lane) : 0;
+        }
 #pragma unroll
         for (int k = 0; k < 16; ++k)
             if (x[k] < 0) x[k] = (int32_t)a.n_in + __ldg(slot - x[k] - 1);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-            const uint32_t wk = s_word[wid * 32 + h + k];
-            if ((wk >> lane) & 1u) out[excl + s_wex[wid * 32 + h + k] + __popc(wk & ((1u << lane) - 1u))] = x[k];
+            const uint32_t wk = __shfl_sync(0xffffffffu, myword, h + k);
+            const int64_t bk = __shfl_sync(0xffffffffu, base, h + k);
+            if ((wk >> lane) & 1u) out[bk + __popc(wk & ((1u << lane) - 1u))] = x[k];
         }
     }
-    // induced row pointers of the rows whose first static arc lies in this tile (setup table; the last tile also
-    // takes the rows starting at nnz): kept arcs before that arc
-    const int64_t rlo = a.tile_row[t], rhi = a.tile_row[t + 1];
-    for (int64_t r = rlo + threadIdx.x; r < rhi; r += blockDim.x) {
+    // rows starting in this chunk (setup table; the last chunk also takes the rows starting at nnz)
+    const int64_t rlo = a.tile_row[chunk], rhi = a.tile_row[chunk + 1];
+    for (int64_t r = rlo + lane; r < rhi; r += 32) {
         const int64_t e = a.row_ptr[r];
-        int64_t kb;
-        if (e >= e1) {
-            kb = s_total;
-        } else {
-            const int w = (int)((e - e0) >> 5), b = (int)(e & 31);
-            kb = s_wex[w] + __popc(s_word[w] & ((1u << b) - 1u));
+        if (e >= a.nnz) {   // trailing empty rows and r = n_in
+            a.out_ptr[r] = *a.total;
+            continue;
         }
-        a.out_ptr[r] = excl + kb;
+        const int64_t w = e >> 5;
+        const int b = (int)(e & 31);
+        a.out_ptr[r] = __ldg(a.tile_pre + t) + a.wex[w] + __popc(a.words[w] & ((1u << b) - 1u));
     }
-    if (t == a.ntiles - 1 && threadIdx.x == 0) *a.total = excl + s_total;
 }
 
 struct SegArgs {
@@ -379,7 +382,8 @@ void launch_induce_fused(Ctx& c) {
     InduceArgs a{};
     a.col_enc = c.d_col_enc; a.nnz = nnz; a.bkeep = c.d_bkeep; a.slot_of_b = c.d_slot_of_b; a.n_in = c.plan.n_in;
     a.row_ptr = c.d_row_ptr; a.tile_row = c.d_tile_row; a.out_col = c.d_ind_col; a.out_ptr = c.d_ind_ptr; a.total = tot;
-    a.words = c.d_ebits; a.tile_cnt = c.d_eblk; a.ntiles = nt;
+    a.words = c.d_ebits; a.wex = c.d_ewex; a.tile_cnt = c.d_eblk; a.tile_pre = c.d_eboff; a.ctr = c.d_lb_ctr + 9;
+    a.ntiles = nt;
     a.nbw = (c.plan.n_bd + 31) / 32;
     constexpr int64_t kSmemMax = 96 << 10;   // bitmask up to 768 K boundary nodes in shared memory
     if (a.nbw * 4 <= kSmemMax) {
@@ -393,7 +397,8 @@ void launch_induce_fused(Ctx& c) {
     } else {
         k_induce_count<false><<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
     }
-    k_induce_scatter<<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
+    const int64_t nchunks = (nnz + 1023) / 1024;
+    k_induce_scatter<<<(unsigned)((nchunks + 7) / 8), 256, 0, c.stream>>>(a);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
 }
