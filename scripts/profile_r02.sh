@@ -30,7 +30,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 python scripts/ncu_summary.py launches "$OUT/emu_launches.csv" "$OUT/emu_launches.txt" > /dev/null
 for part in fwd:8 bwd:12; do
     name=${part%%:*}; skip=${part##*:}
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmm -s "$skip" -c 4 \
+    timeout 900 ncu --set full --clock-control none --import-source on -k k_spmm -s "$skip" -c 4 \
         -o "$OUT/prof_spmm_$name" python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
     python scripts/ncu_summary.py full "$OUT/prof_spmm_$name.ncu-rep" "$OUT/spmm_$name.json" k_spmm > /dev/null
 done
