@@ -52,7 +52,7 @@ def run(ranks=(0,), partition="random", steps=10, warmup=3, spot=1000, log=print
         t0 = time.time()
         ctx = bns.Context(rank=r, world=m, dims=dims, layer=sh.layer, precision=bns.BNS_BF16, indptr=indptr,
                           indices=indices, part_of=part, features=X, labels=np.ascontiguousarray(y_all[inner]),
-                          transport=bns.BNS_TRANSPORT_NULL_EMULATE, max_p=2 * p)
+                          transport=bns.BNS_TRANSPORT_NULL_EMULATE, max_p=2 * p, flags=bns.BNS_TIMING)
         t_setup = time.time() - t0
         try:
             # ---- masks and lists bit-exact (two draws)
@@ -102,6 +102,7 @@ def run(ranks=(0,), partition="random", steps=10, warmup=3, spot=1000, log=print
             for e in range(warmup):
                 ctx.step(p, I.BNS_SEED, 10 + e, W, 0.0, G)
             torch.cuda.synchronize()
+            ctx.set_timing(False)   # device time without per-phase events; the phase split from a second pass
             ms = []
             k0 = ctx.kernel_count()
             for k in range(steps):
@@ -111,6 +112,14 @@ def run(ranks=(0,), partition="random", steps=10, warmup=3, spot=1000, log=print
                 b.record(stream)
                 b.synchronize()
                 ms.append(a.elapsed_time(b))
+            kern = (ctx.kernel_count() - k0) / steps
+            ctx.set_timing(True)
+            t0p = ctx.times()
+            for k in range(steps):
+                ctx.step(p, I.BNS_SEED, 200 + k, W, 0.0, G)
+            torch.cuda.synchronize()
+            t1p = ctx.times()
+            phases = {k: round((t1p[k] - t0p[k]) / steps, 3) for k in t1p if t1p[k] - t0p[k] > 0}
             cnt = ctx.counts()
             dp = [((d + 7) // 8) * 8 for d in dims]
             xbytes = sum((cnt["n_halo"] + cnt["n_sent"]) * dp[l] * 2 for l in range(sh.L)) + \
@@ -120,7 +129,7 @@ def run(ranks=(0,), partition="random", steps=10, warmup=3, spot=1000, log=print
                    "lists_bitexact_epochs": [0, 1], "spot_rows": int(len(rows)), "spot_max_degree": int(deg[inner[rows]].max()),
                    "spot_relerr_H1": err, "loss": loss, "device_ms_per_epoch": float(np.median(ms)),
                    "projected_epochs_per_s_if_slowest": 1000.0 / float(np.median(ms)),
-                   "kernels_per_epoch": (ctx.kernel_count() - k0) / steps,
+                   "kernels_per_epoch": kern, "phases_ms": phases,
                    "n_in": cnt["n_in"], "n_bd": cnt["n_bd"], "n_halo": cnt["n_halo"], "n_sent": cnt["n_sent"],
                    "nnz_rank": cnt["nnz"], "nnz_kept": cnt["nnz_kept"], "exchange_bytes_per_epoch": int(xbytes),
                    "est_nvlink_ms": xbytes / 770e9 * 1e3, "memory_bytes": ctx.memory()[0],
