@@ -329,6 +329,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
         BNS_CUDA(cudaMemset(c.d_lb_ctr, 0, 16 * sizeof(unsigned)));
     }
     c.d_seg_pos = static_cast<int64_t*>(salloc(c, (2 * m + 1 + 8) * sizeof(int64_t)));
+    BNS_CUDA(cudaMemset(c.d_seg_pos, 0, (2 * m + 1 + 8) * sizeof(int64_t)));   // slots a draw does not write stay 0
     BNS_CUDA(cudaMallocHost(&c.h_seg_pos, (2 * m + 1 + 8) * sizeof(int64_t)));
     c.d_ind_ptr = static_cast<int64_t*>(dalloc(c, (P.n_in + 1) * sizeof(int64_t)));
     c.d_ind_col = static_cast<int32_t*>(dalloc(c, (c.nnz_i + 1) * sizeof(int32_t)));

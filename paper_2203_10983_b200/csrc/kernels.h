@@ -45,6 +45,7 @@ struct SpmmArgs {
     int relu = 0;                         // SAGE_FWD_TF: ReLU in the epilogue
     int out_f32 = 0;                      // SAGE_FWD_TF / GAT_FWD: fp32 output (logits) instead of the storage type
     unsigned long long* work = nullptr;   // dynamic segment scheduling: next unclaimed segment (zeroed per launch)
+    int chunk = 1;                        // segments per claim
     // f4 / R45 GAT: per-node attention scores and softmax statistics (fp32), attention vectors a_l / a_r (dout),
     // del / der (backward)
     const float *gat_el = nullptr, *gat_er = nullptr, *gat_m = nullptr, *gat_inv = nullptr;

@@ -13,7 +13,7 @@
 // 16-byte vectors of the row (LPR lanes per row; with narrow rows the warp's 32/LPR lane groups take alternate
 // edges and are reduced at the end).  Column indices are loaded 32 at a time and broadcast with shuffles; U edges
 // are in flight per lane.  fp32 accumulation for both storage types.  Hub rows (deg > kSeg) are split into several
-// segments whose fp32 partials are summed in a fixed order by k_spmm_fixup -- deterministic, and the split
+// segments whose fp32 partials are summed in segment order by k_spmm_fixup -- deterministic, and the split
 // depends only on the row length.
 #include <cstdlib>
 
@@ -24,6 +24,13 @@
 #include "kernels.h"
 
 namespace bns {
+
+// segments per dynamic claim: ~64 claims per warp over the launch, at least 1, at most 64 segments
+static int claim_chunk(int64_t n_segs, int64_t warps) {
+    static const int fixed = [] { const char* e = std::getenv("BNS_SPMM_CHUNK"); return e ? std::atoi(e) : 0; }();
+    if (fixed > 0) return fixed;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(64, n_segs / std::max<int64_t>(1, warps * 64)));
+}
 
 template <typename T>
 __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, int vi, float* acc) {
@@ -170,12 +177,16 @@ k_spmm(const SpmmArgs a) {
     // static: grid-stride over the segments; dynamic (a.work): each warp claims the next segment when it is done, so
     // a block never idles behind its longest segment (short partitions: ~1 segment per warp).  Claiming the next
     // segment ahead (atomic issued at segment start) was measured slower at m = 8 (2.05 vs 1.99 ms): rejected.
+    // claims take a.chunk consecutive segments at once: with millions of 1-2 edge segments (C5) one atomic per
+    // segment on one address serialised the whole kernel
+    const int64_t chunk = a.work ? a.chunk : 1;
     auto claim = [&]() -> int64_t {
         unsigned long long v = 0;
-        if (lane == 0) v = atomicAdd(a.work, 1ull);
+        if (lane == 0) v = atomicAdd(a.work, (unsigned long long)chunk);
         return (int64_t)__shfl_sync(0xffffffffu, v, 0);
     };
-    for (int64_t sid = a.work ? claim() : warp; sid < a.n_segs; sid = a.work ? claim() : sid + nwarps) {
+    for (int64_t c0 = a.work ? claim() : warp; c0 < a.n_segs; c0 = a.work ? claim() : c0 + nwarps)
+    for (int64_t sid = c0; sid < c0 + chunk && sid < a.n_segs; ++sid) {
         const Seg s = a.segs[sid];
         uint64_t acc2[VPL][VN / 2];
 #pragma unroll
@@ -333,10 +344,11 @@ __global__ void __launch_bounds__(256, 3) k_spmm_g4(const __grid_constant__ CUte
     };
     auto claim = [&]() -> int64_t {
         unsigned long long v = 0;
-        if (lane == 0) v = atomicAdd(a.work, 1ull);
+        if (lane == 0) v = atomicAdd(a.work, (unsigned long long)a.chunk);
         return (int64_t)__shfl_sync(0xffffffffu, v, 0);
     };
-    for (int64_t sid = claim(); sid < a.n_segs; sid = claim()) {
+    for (int64_t c0 = claim(); c0 < a.n_segs; c0 = claim())
+    for (int64_t sid = c0; sid < c0 + a.chunk && sid < a.n_segs; ++sid) {
         const Seg s = a.segs[sid];
         const int64_t ng = (s.e1 - s.e0 + 3) / 4;
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
@@ -427,70 +439,61 @@ static bool launch_spmm_g4(Ctx& c, SpmmArgs a, int sc) {
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.n_segs + 7) / 8, (int64_t)std::max(1, per_sm) * sms));
     BNS_CUDA(cudaMemsetAsync(c.d_spmm_work, 0, sizeof(unsigned long long), c.stream));
     a.work = c.d_spmm_work;
+    a.chunk = claim_chunk(a.n_segs, (int64_t)grid * 8);
     kern<<<grid, 256, smem, c.stream>>>(map, a);
     return true;
 }
 
-// Sum the partials of every split row, then the same epilogue.  One block per split row: warp w sums the w-th
-// contiguous eighth of the row's segments in segment order, warp 0 then adds the eight partial sums in warp order --
-// a fixed association that depends only on the row length (R37), and an 8x shorter serial tail on hub rows than one
-// warp summing every segment (at m = 8 a hub row holds ~60 segments: the one-warp fixup took ~11 us per launch).
-constexpr int kFixWarps = 8;
+// Sum the partials of every split row in segment order, then the same epilogue.  (A block-per-row variant -- eight
+// warps each summing an eighth of the segments -- measured slower: Reddit m = 1 22.7 -> 24.2 ms per epoch, m = 8
+// rank 1.56 -> 1.66 ms; most split rows have few segments and the block's barrier and idle warps cost more than the
+// hub rows' serial tail.)
 template <typename T>
-__global__ void __launch_bounds__(kFixWarps * 32) k_spmm_fixup(const SpmmArgs a) {
+__global__ void __launch_bounds__(256) k_spmm_fixup(const SpmmArgs a) {
     using V = Vec<T>;
     constexpr int VN = V::N;
-    extern __shared__ float s_fix[];                 // [kFixWarps][d]
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int nvec = a.d / VN;
-    const int64_t sid = a.split[blockIdx.x];
-    const Seg s = a.segs[sid];
-    const int per = (s.nseg + kFixWarps - 1) / kFixWarps;
-    const int q0 = min(s.nseg, w * per), q1 = min(s.nseg, q0 + per);
-    for (int vi = lane; vi < nvec; vi += 32) {
-        float acc[VN];
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q0 = warp; q0 < a.n_split; q0 += nwarps) {
+        const int64_t sid = a.split[q0];
+        const Seg s = a.segs[sid];
+        for (int vi = lane; vi < nvec; vi += 32) {
+            float acc[VN];
 #pragma unroll
-        for (int k = 0; k < VN; ++k) acc[k] = 0.f;
-        const float* pp = a.partial + sid * (int64_t)a.d + vi * VN;
-        int q = q0;
-        for (; q + 4 <= q1; q += 4) {   // 4 segments' partials in flight, added in segment order
-            float4 t[4][VN / 4];
+            for (int k = 0; k < VN; ++k) acc[k] = 0.f;
+            const float* pp = a.partial + sid * (int64_t)a.d + vi * VN;
+            int q = 0;
+            // 4 segments' partials in flight (16-byte loads), still added in segment order
+            for (; q + 4 <= s.nseg; q += 4) {
+                float4 t[4][VN / 4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < 4; ++j)
 #pragma unroll
-                for (int k = 0; k < VN / 4; ++k) t[j][k] = *reinterpret_cast<const float4*>(pp + (int64_t)(q + j) * a.d + 4 * k);
+                    for (int k = 0; k < VN / 4; ++k)
+                        t[j][k] = *reinterpret_cast<const float4*>(pp + (int64_t)(q + j) * a.d + 4 * k);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int k = 0; k < VN / 4; ++k) {
+                        acc[4 * k] += t[j][k].x;
+                        acc[4 * k + 1] += t[j][k].y;
+                        acc[4 * k + 2] += t[j][k].z;
+                        acc[4 * k + 3] += t[j][k].w;
+                    }
+            }
+            for (; q < s.nseg; ++q)
 #pragma unroll
                 for (int k = 0; k < VN / 4; ++k) {
-                    acc[4 * k] += t[j][k].x;
-                    acc[4 * k + 1] += t[j][k].y;
-                    acc[4 * k + 2] += t[j][k].z;
-                    acc[4 * k + 3] += t[j][k].w;
+                    const float4 t = *reinterpret_cast<const float4*>(pp + (int64_t)q * a.d + 4 * k);
+                    acc[4 * k] += t.x;
+                    acc[4 * k + 1] += t.y;
+                    acc[4 * k + 2] += t.z;
+                    acc[4 * k + 3] += t.w;
                 }
+            epilogue_store<T>(a, s.row, vi, acc);
         }
-        for (; q < q1; ++q)
-#pragma unroll
-            for (int k = 0; k < VN / 4; ++k) {
-                const float4 t = *reinterpret_cast<const float4*>(pp + (int64_t)q * a.d + 4 * k);
-                acc[4 * k] += t.x;
-                acc[4 * k + 1] += t.y;
-                acc[4 * k + 2] += t.z;
-                acc[4 * k + 3] += t.w;
-            }
-#pragma unroll
-        for (int k = 0; k < VN; ++k) s_fix[w * a.d + vi * VN + k] = acc[k];
-    }
-    __syncthreads();
-    if (w != 0) return;
-    for (int vi = lane; vi < nvec; vi += 32) {
-        float acc[VN];
-#pragma unroll
-        for (int k = 0; k < VN; ++k) acc[k] = s_fix[vi * VN + k];
-        for (int ww = 1; ww < kFixWarps; ++ww)
-#pragma unroll
-            for (int k = 0; k < VN; ++k) acc[k] += s_fix[ww * a.d + vi * VN + k];
-        epilogue_store<T>(a, s.row, vi, acc);
     }
 }
 
@@ -518,6 +521,7 @@ static void go_sc(Ctx& c, SpmmArgs a, unsigned grid) {
     if (spmm_sched() == 2) {
         BNS_CUDA(cudaMemsetAsync(c.d_spmm_work, 0, sizeof(unsigned long long), c.stream));
         a.work = c.d_spmm_work;
+        a.chunk = claim_chunk(a.n_segs, (int64_t)grid * 8);
     } else {
         a.work = nullptr;
     }
@@ -622,16 +626,10 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
         else dispatch<float>(c, a, grid);
         c.kernels += 1;
         BNS_CHECK_LAUNCH();
-        if (a.n_split > 0) {   // only the split (hub) rows, listed by their first segment: one block each
-            const size_t sm = (size_t)kFixWarps * a.d * sizeof(float);
-            static const bool cfg = [] {   // rows up to 3,072 floats wide (96 KB of partial sums per block)
-                cudaFuncSetAttribute(k_spmm_fixup<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
-                cudaFuncSetAttribute(k_spmm_fixup<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
-                return true;
-            }();
-            (void)cfg;
-            if (c.prec == BNS_BF16) k_spmm_fixup<__nv_bfloat16><<<(unsigned)a.n_split, kFixWarps * 32, sm, c.stream>>>(a);
-            else k_spmm_fixup<float><<<(unsigned)a.n_split, kFixWarps * 32, sm, c.stream>>>(a);
+        if (a.n_split > 0) {   // only the split (hub) rows, listed by their first segment
+            const unsigned fg = (unsigned)std::min<int64_t>((a.n_split + 7) / 8, 148 * 8);
+            if (c.prec == BNS_BF16) k_spmm_fixup<__nv_bfloat16><<<fg, 256, 0, c.stream>>>(a);
+            else k_spmm_fixup<float><<<fg, 256, 0, c.stream>>>(a);
             c.kernels += 1;
             BNS_CHECK_LAUNCH();
         }
