@@ -220,7 +220,7 @@ typedef enum {
     BNS_Q_H = 11,            /* layer l in [0,L]: H^(l) inner rows, n_in x dims[l] (l = L: logits) */
     BNS_Q_Z = 12,            /* layer l in [1,L]: aggregation output Z^(l), n_in x dims[l-1] */
     BNS_Q_DH = 13,           /* layer l in [1,L]: dL/dH^(l) after owner accumulation (l = L: dLogits);
-                                l < L needs BNS_RETAIN_GRADS */
+                                needs BNS_RETAIN_GRADS (the fp32 dLogits are only written then) */
     BNS_Q_HALO_ROWS = 14,    /* layer l in [1,L]: received halo rows of the layer-l input, |U_i| x dims[l-1] */
     BNS_Q_INDUCED = 15,      /* int64[n_in+1] row pointers then int32[nnz_kept] local columns of the induced
                                 subgraph (inner j -> j, halo slot s -> n_in + s) */

@@ -673,10 +673,10 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         PhaseTimer t(c, BNS_PH_LOSS);
         const bool tfL = (c.tf_mask >> (L - 1)) & 1u;
         if (c.multilabel)
-            launch_bce(c, c.d_logits, c.dp[L], c.dims[L], c.d_dlogits, c.d_dpre, tfL ? c.d_deg_in : nullptr,
+            launch_bce(c, c.d_logits, c.dp[L], c.dims[L], c.retain ? c.d_dlogits : nullptr, c.d_dpre, tfL ? c.d_deg_in : nullptr,
                        tfL ? c.d_dxcat : nullptr);
         else
-            launch_xent(c, c.d_logits, c.dp[L], c.dims[L], c.d_dlogits, c.d_dpre, tfL ? c.d_deg_in : nullptr,
+            launch_xent(c, c.d_logits, c.dp[L], c.dims[L], c.retain ? c.d_dlogits : nullptr, c.d_dpre, tfL ? c.d_deg_in : nullptr,
                         tfL ? c.d_dxcat : nullptr);
     }
     // ------------------------------ backward (l.12) ------------------------------
@@ -1036,11 +1036,9 @@ bns_status bns_query(bns_ctx* h, int32_t what, int32_t layer, void* dst, int64_t
             case BNS_Q_DH: {
                 need_sample();
                 if (layer < 1 || layer > L) throw Error(BNS_ERR_INVALID, "layer out of range");
+                if (!c.retain) throw Error(BNS_ERR_STATE, "BNS_Q_DH needs BNS_RETAIN_GRADS");
                 if (layer == L) rows_f32(c.d_dlogits, P.n_in, c.dp[L], c.dims[L], true);
-                else {
-                    if (!c.retain) throw Error(BNS_ERR_STATE, "BNS_Q_DH for l < L needs BNS_RETAIN_GRADS");
-                    rows_f32(c.dH_keep[layer], P.n_in, c.dp[layer], c.dims[layer], false);
-                }
+                else rows_f32(c.dH_keep[layer], P.n_in, c.dp[layer], c.dims[layer], false);
                 break;
             }
             case BNS_Q_HALO_ROWS: {

@@ -193,11 +193,11 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
     for (int64_t r = warp; r < n; r += nwarps) {
         const float* x = logits + r * ld;
         const int y = labels[r];
-        float* g = dlog + r * ld;
+        float* g = dlog ? dlog + r * ld : nullptr;   // fp32 dLogits only for BNS_Q_DH (BNS_RETAIN_GRADS)
         T* gp = dpre + r * ld;
         if (y < 0) {
             for (int c = lane; c < ld; c += 32) {
-                g[c] = 0.f;
+                if (g) g[c] = 0.f;
                 gp[c] = from_f<T>(0.f);
                 if (dps) dps[r * ld + c] = from_f<T>(0.f);
             }
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
             if (c >= ld) break;
             float v = 0.f;
             if (c < C) v = (float)(((double)expf(xv[k] - lse) - (c == y ? 1.0 : 0.0)) * inv_ntr);
-            g[c] = v;
+            if (g) g[c] = v;
             const T q = from_f<T>(v);
             gp[c] = q;
             if (dps) dps[r * ld + c] = from_f<T>(to_f(q) * rsr);   // R42: dPre / deg_G(v), from the stored dPre
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) k_bce(const float* __restrict__ logits, i
                 nfp += (pred && y == 0.f);
                 nfn += (!pred && y > 0.f);
             }
-            dlog[r * ld + c] = v;
+            if (dlog) dlog[r * ld + c] = v;
             const T q = from_f<T>(v);
             dpre[r * ld + c] = q;
             if (dps) dps[r * ld + c] = from_f<T>(to_f(q) * rsr);
