@@ -93,35 +93,53 @@ __global__ void __launch_bounds__(256) k_gemm(int64_t M, int64_t N, int64_t K, c
     }
 }
 
-// fixed-order sum of the split-K partial slices (deterministic), 4 columns per thread (N is a multiple of 8)
-__global__ void k_splitk_reduce(const float* __restrict__ part, int S, int64_t M, int64_t N, int64_t ldp,
-                                float* __restrict__ out, int64_t ldo) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// fixed-order sum of the split-K partial slices (deterministic, depends only on S): a block covers 32 float4 output
+// chunks (one per lane); warp g sums the g-th contiguous eighth of the slices in slice order -- all its loads in
+// flight at once -- and warp 0 adds the eight group sums in group order.  (One thread summing all S slices was
+// latency-bound: ~9 us per launch at m = 8 for a few MB.)
+constexpr int kRedGroups = 8;
+__global__ void __launch_bounds__(kRedGroups * 32) k_splitk_reduce(const float* __restrict__ part, int S, int64_t M,
+                                                                  int64_t N, int64_t ldp, float* __restrict__ out,
+                                                                  int64_t ldo) {
+    __shared__ float4 s_g[kRedGroups][32];
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int64_t n4 = N / 4;
-    if (t >= M * n4) return;
-    int64_t i = t / n4, j = (t % n4) * 4;
+    const int64_t t = (int64_t)blockIdx.x * 32 + lane;
+    const bool live = t < M * n4;
+    const int64_t i = live ? t / n4 : 0, j = live ? (t % n4) * 4 : 0;
     const float* p0 = part + i * ldp + j;
     const int64_t zs = M * ldp;
+    const int per = (S + kRedGroups - 1) / kRedGroups;
+    const int z0 = min(S, g * per), z1 = min(S, z0 + per);
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    int z = 0;
-    // eight slices' loads in flight (the kernel is latency-bound: ~1 resident warp group per SM), added in slice order
-    for (; z + 8 <= S; z += 8) {
-        float4 v[8];
+    if (live) {
+        int z = z0;
+        for (; z + 8 <= z1; z += 8) {
+            float4 v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(p0 + (int64_t)(z + q) * zs));
+            for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(p0 + (int64_t)(z + q) * zs));
 #pragma unroll
-        for (int q = 0; q < 8; ++q) { s.x += v[q].x; s.y += v[q].y; s.z += v[q].z; s.w += v[q].w; }
+            for (int q = 0; q < 8; ++q) { s.x += v[q].x; s.y += v[q].y; s.z += v[q].z; s.w += v[q].w; }
+        }
+        for (; z < z1; ++z) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(p0 + (int64_t)z * zs));
+            s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+        }
     }
-    for (; z < S; ++z) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(p0 + (int64_t)z * zs));
-        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    s_g[g][lane] = s;
+    __syncthreads();
+    if (g != 0 || !live) return;
+    float4 r = s_g[0][lane];
+    for (int q = 1; q < kRedGroups; ++q) {
+        const float4 v = s_g[q][lane];
+        r.x += v.x; r.y += v.y; r.z += v.z; r.w += v.w;
     }
-    *reinterpret_cast<float4*>(out + i * ldo + j) = s;
+    *reinterpret_cast<float4*>(out + i * ldo + j) = r;
 }
 
 void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw) {
-    const int64_t tot = K * N;
-    k_splitk_reduce<<<(unsigned)((tot / 4 + 127) / 128), 128, 0, c.stream>>>(c.d_splitk, S, K, N, N, Wg, ldw);
+    const int64_t n4 = K * N / 4;
+    k_splitk_reduce<<<(unsigned)((n4 + 31) / 32), kRedGroups * 32, 0, c.stream>>>(c.d_splitk, S, K, N, N, Wg, ldw);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -162,7 +180,7 @@ static void wgrad_t(Ctx& c, int64_t M, int64_t K, int64_t N, const void* A, int6
     k_gemm<T, float, 1><<<grid, 256, 0, c.stream>>>(K, N, M, (const T*)A, 0, lda, nullptr, 0, (const T*)D, ldd,
                                                     c.d_splitk, N, false, nullptr, 0, chunk);
     int64_t tot = K * N;
-    k_splitk_reduce<<<(unsigned)((tot / 4 + 255) / 256), 256, 0, c.stream>>>(c.d_splitk, (int)S, K, N, N, Wg, ldw);
+    k_splitk_reduce<<<(unsigned)((tot / 4 + 31) / 32), kRedGroups * 32, 0, c.stream>>>(c.d_splitk, (int)S, K, N, N, Wg, ldw);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
 }

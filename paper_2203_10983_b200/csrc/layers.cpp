@@ -321,13 +321,13 @@ void backward_layer_tf(Ctx& c, const EpochView& v, int l, void* Hin) {
         auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
         wgrad(c, rows, din, dout, Hin, din, c.d_tfy, 2 * dout, g, dout);
         wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
-        if (l > 1) {
+        if (l > 1) {   // dX = [dY | dPre] [W_top | W_bot]^T over every stacked row, one GEMM: halo rows have no dPre
             BNS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(c.d_tfy) + dout * ts, 2 * dout * ts, c.d_dpre,
                                        dout * ts, dout * ts, n_in, cudaMemcpyDeviceToDevice, c.stream));
-            dxg(c, n_in, din, 2 * dout, c.d_tfy, 2 * dout, c.Wcat[l - 1], 2 * dout, c.d_dx, din, nullptr, 0);
             if (c.n_halo > 0)
-                dxg(c, c.n_halo, din, dout, static_cast<char*>(c.d_tfy) + n_in * 2 * dout * ts, 2 * dout,
-                    c.Wcat[l - 1], 2 * dout, static_cast<char*>(c.d_dx) + n_in * din * ts, din, nullptr, 0);
+                BNS_CUDA(cudaMemset2DAsync(static_cast<char*>(c.d_tfy) + (n_in * 2 + 1) * dout * ts, 2 * dout * ts, 0,
+                                           dout * ts, c.n_halo, c.stream));
+            dxg(c, rows, din, 2 * dout, c.d_tfy, 2 * dout, c.Wcat[l - 1], 2 * dout, c.d_dx, din, nullptr, 0);
         }
     }
 }
