@@ -97,6 +97,12 @@ typedef enum {
  * Ordering between ranks: device-side flag barriers (system-scope release / acquire, 20 s timeout -> the epoch
  * fails with BNS_ERR_RUNTIME instead of hanging).  Results are bitwise those of the LOCAL transport. */
 #define BNS_PEER_MEMORY             0x40u
+/* R48: bns_step(p, seed, e) also enqueues the draw of (p, seed, e + 1) after the epoch's update kernels, before the
+ * closing stream sync, so the per-peer counts of the next draw reach the host with that sync.  The next
+ * bns_step(p, seed, e + 1) then starts its epoch at once: one host wait per step instead of two (the draw kernels
+ * and their results are unchanged).  A step with other arguments discards the prefetch and draws as usual.  After
+ * such a bns_step the context's current draw IS the prefetched one: bns_epoch / bns_query see draw e + 1. */
+#define BNS_PREFETCH_DRAW           0x80u
 
 /* Host all-gather used by BNS_TRANSPORT_IPC at setup (buffer handles, counts) and by debug exchanges: copy `bytes`
  * bytes from `send` of every rank into recv[rank * bytes]; every rank calls it with the same `bytes`.  Return 0 on
@@ -121,7 +127,8 @@ typedef struct {
     double max_p;             /* halo capacity: <= 0 or >= 1 -> sized for p = 1 (|B_i| rows); else
                                  ceil(max_p*|B_i| + 8 sqrt(max_p*|B_i|) + 64) rows (R34) */
     uint32_t flags;           /* BNS_PLAN_ONLY | BNS_DEBUG_EXCHANGE_INDICES | BNS_TIMING | BNS_RETAIN_GRADS |
-                                 BNS_NO_TRANSFORM_FIRST | BNS_CACHE_INPUT_HALO | BNS_PEER_MEMORY */
+                                 BNS_NO_TRANSFORM_FIRST | BNS_CACHE_INPUT_HALO | BNS_PEER_MEMORY |
+                                 BNS_PREFETCH_DRAW */
     bns_allgather_fn allgather;   /* transport IPC: host all-gather over the ranks (e.g. a torch gloo group); else NULL */
     void* allgather_user;         /* passed through to allgather */
 } bns_config;
@@ -176,7 +183,8 @@ bns_status bns_epoch(bns_ctx* ctx, float* const* weights, float lr, float* const
 
 /* One training step = bns_sample_boundary(p, seed, epoch) followed by bns_epoch(weights, lr, grads, loss, acc) in
  * one call (Alg.1 l.4-14): the same work and results, without a return to the caller between the draw and the epoch
- * (the host only waits for the per-peer counts, then enqueues the epoch).  Errors as the two calls. */
+ * (the host only waits for the per-peer counts, then enqueues the epoch; with BNS_PREFETCH_DRAW not even that when
+ * the previous step prefetched this draw, R48).  Errors as the two calls. */
 bns_status bns_step(bns_ctx* ctx, double p, uint64_t seed, uint64_t epoch, float* const* weights, float lr,
                     float* const* grads, double* loss, double* acc);
 

@@ -23,6 +23,7 @@ BNS_TRANSPORT_NONE, BNS_TRANSPORT_NCCL, BNS_TRANSPORT_LOCAL, BNS_TRANSPORT_NULL_
 BNS_PLAN_ONLY, BNS_DEBUG_EXCHANGE_INDICES, BNS_TIMING, BNS_RETAIN_GRADS, BNS_NO_TRANSFORM_FIRST = 0x1, 0x2, 0x4, 0x8, 0x10
 BNS_CACHE_INPUT_HALO = 0x20
 BNS_PEER_MEMORY = 0x40   # f1: exchanges fused over peer memory (LOCAL in-process; implied by IPC)
+BNS_PREFETCH_DRAW = 0x80   # R48: bns_step enqueues the next epoch's draw before its closing sync
 (BNS_Q_COUNTS, BNS_Q_INNER, BNS_Q_BOUNDARY, BNS_Q_BOUNDARY_OFF, BNS_Q_SENDCAND, BNS_Q_SENDCAND_OFF, BNS_Q_MASK,
  BNS_Q_HALO, BNS_Q_HALO_OFF, BNS_Q_SEND, BNS_Q_SEND_OFF, BNS_Q_H, BNS_Q_Z, BNS_Q_DH, BNS_Q_HALO_ROWS, BNS_Q_INDUCED,
  BNS_Q_TIMES, BNS_Q_STATIC_CSR, BNS_Q_MEMORY, BNS_Q_KERNEL_COUNT, BNS_Q_INDUCED_T, BNS_Q_TF_LAYERS,

@@ -504,7 +504,8 @@ void fill_x0_cache(Ctx& c) {
 // ---------------------------------------------------------------------------------------------
 // bns_sample_boundary / bns_sample_edges: a1-a3
 // ---------------------------------------------------------------------------------------------
-void sample_boundary(Ctx& c, int sampler, double p, uint64_t seed, uint64_t epoch) {
+// a1-a3 enqueued: the draw, the induced lists / segments, and the async copy of the per-peer counts to the host
+void draw_enqueue(Ctx& c, int sampler, double p, uint64_t seed, uint64_t epoch) {
     const int m = c.cfg.world;
     const uint64_t T = (uint64_t)std::floor(p * 4294967296.0);
     const bool edges = sampler != BNS_SAMPLER_BNS;
@@ -540,7 +541,14 @@ void sample_boundary(Ctx& c, int sampler, double p, uint64_t seed, uint64_t epoc
     total.reset();
     const int64_t nslot = 2 * m + 1 + 8;
     BNS_CUDA(cudaMemcpyAsync(c.h_seg_pos, c.d_seg_pos, nslot * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-    BNS_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// the host side of a draw: wait for the counts (unless an earlier sync already covered the copy), size the epoch
+void draw_finish(Ctx& c, uint64_t epoch, bool sync) {
+    const int m = c.cfg.world;
+    const bool edges = c.sampler != BNS_SAMPLER_BNS;
+    const bool has_bd = c.plan.n_bd > 0;
+    if (sync) BNS_CUDA(cudaStreamSynchronize(c.stream));
     const int64_t* sp = c.h_seg_pos;
     for (int j = 0; j <= m; ++j) c.recv_off[j] = sp[j] - sp[0];
     for (int j = 0; j <= m; ++j) c.send_off[j] = sp[m + j] - sp[m];
@@ -586,6 +594,19 @@ void sample_boundary(Ctx& c, int sampler, double p, uint64_t seed, uint64_t epoc
     collect_times(c);
     c.epoch_id = epoch;
     c.sampled = true;
+}
+
+void sample_boundary(Ctx& c, int sampler, double p, uint64_t seed, uint64_t epoch) {
+    c.pf_pending = false;   // a prefetched draw (R48) is simply overwritten
+    draw_enqueue(c, sampler, p, seed, epoch);
+    draw_finish(c, epoch, true);
+}
+
+// R48: any call that reads the current draw first adopts a prefetched one (device buffers already hold it)
+void settle(Ctx& c) {
+    if (!c.pf_pending) return;
+    c.pf_pending = false;
+    draw_finish(c, c.pf_ep, true);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -738,6 +759,11 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         }
     }
     total.reset();
+    if (c.pf_want) {   // R48: the next draw rides on this epoch's closing sync (stream order keeps it after a4-a14)
+        c.pf_want = false;
+        draw_enqueue(c, BNS_SAMPLER_BNS, c.pf_p, c.pf_seed, c.pf_ep);
+        c.pf_pending = true;
+    }
     double scal[4] = {0.0, 0.0, 0.0, 0.0};
     int32_t nonfinite = 0;
     BNS_CUDA(cudaMemcpyAsync(scal, c.d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c.stream));
@@ -870,21 +896,44 @@ bns_status bns_epoch(bns_ctx* h, float* const* weights, float lr, float* const* 
     if (!h) return BNS_ERR_INVALID;
     Ctx& c = h->c;
     if (c.failed || c.plan_only) return BNS_ERR_STATE;
-    if (!c.sampled) { c.err = "bns_epoch before bns_sample_boundary"; return BNS_ERR_STATE; }
+    if (!c.sampled && !c.pf_pending) { c.err = "bns_epoch before bns_sample_boundary"; return BNS_ERR_STATE; }
     if (!weights) { c.err = "weights is NULL"; return BNS_ERR_INVALID; }
     for (int l = 0; l < c.L; ++l)
         if (!weights[l]) { c.err = "weights[l] is NULL"; return BNS_ERR_INVALID; }
     return guard(h, [&] {
         BNS_CUDA(cudaSetDevice(c.cfg.device));
+        settle(c);
         epoch(c, weights, lr, grads, loss, acc);
     });
 }
 
 bns_status bns_step(bns_ctx* h, double p, uint64_t seed, uint64_t ep, float* const* weights, float lr,
                     float* const* grads, double* loss, double* acc) {
-    const bns_status st = bns_sample_boundary(h, p, seed, ep);
-    if (st != BNS_OK) return st;
-    return bns_epoch(h, weights, lr, grads, loss, acc);
+    if (!h) return BNS_ERR_INVALID;
+    Ctx& c = h->c;
+    const bool prefetch = (c.cfg.flags & BNS_PREFETCH_DRAW) != 0;
+    if (prefetch && c.pf_pending && c.sampler == BNS_SAMPLER_BNS && c.p == p && c.pf_seed == seed && c.pf_ep == ep &&
+        !c.failed) {
+        // the draw of this step was enqueued by the previous bns_step and its counts arrived with that step's
+        // closing sync: no wait, no re-draw
+        const bns_status st = guard(h, [&] {
+            c.pf_pending = false;
+            draw_finish(c, ep, false);
+        });
+        if (st != BNS_OK) return st;
+    } else {
+        const bns_status st = bns_sample_boundary(h, p, seed, ep);
+        if (st != BNS_OK) return st;
+    }
+    if (prefetch && ep != UINT64_MAX) {
+        c.pf_want = true;
+        c.pf_p = p;
+        c.pf_seed = seed;
+        c.pf_ep = ep + 1;
+    }
+    const bns_status st = bns_epoch(h, weights, lr, grads, loss, acc);
+    c.pf_want = false;
+    return st;
 }
 
 bns_status bns_set_training(bns_ctx* h, int32_t optimizer, double beta1, double beta2, double eps, double dropout,
@@ -947,6 +996,7 @@ bns_status bns_query(bns_ctx* h, int32_t what, int32_t layer, void* dst, int64_t
     if (!h) return BNS_ERR_INVALID;
     Ctx& c = h->c;
     return guard(h, [&] {
+        if (!c.plan_only && !c.failed) settle(c);
         const Plan& P = c.plan;
         const int m = c.cfg.world, L = c.L;
         std::vector<uint8_t> out;

@@ -106,6 +106,10 @@ struct Ctx {
     std::string err;
     bool failed = false;
     bool sampled = false;
+    // BNS_PREFETCH_DRAW (R48): bns_step enqueues the draw of (pf_p, pf_seed, pf_ep) before its closing sync
+    bool pf_want = false, pf_pending = false;
+    double pf_p = 0.0;
+    uint64_t pf_seed = 0, pf_ep = 0;
     Plan plan;
     Transport* tr = nullptr;
     int64_t halo_cap = 0;

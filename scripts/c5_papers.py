@@ -52,7 +52,7 @@ def run(ranks=(0,), partition="random", steps=10, warmup=3, spot=1000, log=print
         t0 = time.time()
         ctx = bns.Context(rank=r, world=m, dims=dims, layer=sh.layer, precision=bns.BNS_BF16, indptr=indptr,
                           indices=indices, part_of=part, features=X, labels=np.ascontiguousarray(y_all[inner]),
-                          transport=bns.BNS_TRANSPORT_NULL_EMULATE, max_p=2 * p, flags=bns.BNS_TIMING)
+                          transport=bns.BNS_TRANSPORT_NULL_EMULATE, max_p=2 * p, flags=bns.BNS_TIMING | bns.BNS_PREFETCH_DRAW)
         t_setup = time.time() - t0
         try:
             # ---- masks and lists bit-exact (two draws)

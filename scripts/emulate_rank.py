@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--model", default="sage", choices=["sage", "gat"], help="gat: 2-layer GAT (Table tab:gat)")
     ap.add_argument("--cache-x0", action="store_true", help="BNS_CACHE_INPUT_HALO (f1, R43): no layer-1 exchange")
     ap.add_argument("--no-timing", action="store_true", help="no per-phase CUDA events (device total only)")
+    ap.add_argument("--no-prefetch", action="store_true", help="no BNS_PREFETCH_DRAW (R48): draw + host wait per step")
     ap.add_argument("--samplers", nargs="+", default=["bns"], choices=["bns", "bes", "dropedge"],
                     help="f3 Table tab:bes analogue: edge samplers at matched dropped-edge counts (P:681)")
     args = ap.parse_args()
@@ -58,7 +59,8 @@ def main():
         ctx = bns.Context(rank=r, world=args.m, dims=sh.dims, layer=sh.layer, precision=prec, indptr=indptr,
                           indices=indices, part_of=part, features=I.features(inner, sh.d0),
                           labels=np.ascontiguousarray(y_all[inner]), transport=bns.BNS_TRANSPORT_NULL_EMULATE,
-                          flags=(0 if args.no_timing else bns.BNS_TIMING) | (bns.BNS_CACHE_INPUT_HALO if args.cache_x0 else 0))
+                          flags=(0 if args.no_timing else bns.BNS_TIMING) | (bns.BNS_CACHE_INPUT_HALO if args.cache_x0 else 0) |
+                          (0 if args.no_prefetch else bns.BNS_PREFETCH_DRAW))
         W = [torch.tensor(w, device="cuda") for w in I.weights(sh.dims, sh.layer)]
         G = [torch.zeros_like(w) for w in W]
         stream = torch.cuda.ExternalStream(ctx.stream())
