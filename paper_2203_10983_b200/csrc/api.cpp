@@ -1179,11 +1179,11 @@ bns_status bns_gemm(int32_t precision, int32_t kind, int64_t M, int64_t N, int64
         c.splitk_cap = 0;
         std::vector<void*> mine;
         if (kind == 1 || kind == 2) {   // room for one fp32 K x N (x2) slice per split, up to 148 splits
-            c.splitk_cap = 148 * (kind == 2 ? 2 : 1) * K * N;
+            c.splitk_cap = 148 * (kind == 2 ? 2 * K + 128 : K) * N;
             if (precision == BNS_FP32) {
                 c.tr_cap = ((kind == 2 ? 2 : 1) * K + N) * ((M + 3) / 4 * 4);
                 c.d_tr = static_cast<float*>(dalloc(c, c.tr_cap * sizeof(float)));
-                c.splitk_cap = std::max<int64_t>(c.splitk_cap, ((M + 511) / 512 + 1) * (kind == 2 ? 2 : 1) * K * N);
+                c.splitk_cap = std::max<int64_t>(c.splitk_cap, ((M + 511) / 512 + 1) * (kind == 2 ? 2 * K + 128 : K) * N);
             }
             c.d_splitk = static_cast<float*>(dalloc(c, c.splitk_cap * sizeof(float)));
         }
@@ -1193,7 +1193,7 @@ bns_status bns_gemm(int32_t precision, int32_t kind, int64_t M, int64_t N, int64
                 case 0: gemm_fwd_tc(c, M, N, A0, K, lda, A1, A1 ? K : 0, lda, B, ldb ? ldb : (A1 ? 2 * Kw : Kw), C,
                                     ldc, flags & 1, (flags >> 1) & 1); break;
                 case 1: gemm_wgrad_tc(c, M, K, N, A0, lda, B, ldb, static_cast<float*>(C), ldc); break;
-                case 2: gemm_wgrad2_tc(c, M, K, N, A0, A1, lda, B, ldb, static_cast<float*>(C), ldc); break;
+                case 2: gemm_wgrad2_tc(c, M, M, K, N, A0, A1, lda, B, ldb, B, ldb, static_cast<float*>(C), ldc); break;
                 default: gemm_dx_tc(c, M, N, K, A0, lda, B, ldb, C, ldc, rowscale, scale_cols); break;
             }
             BNS_CUDA(cudaStreamSynchronize(c.stream));

@@ -99,16 +99,16 @@ __global__ void __launch_bounds__(256) k_gemm(int64_t M, int64_t N, int64_t K, c
 // latency-bound: ~9 us per launch at m = 8 for a few MB.)
 constexpr int kRedGroups = 8;
 __global__ void __launch_bounds__(kRedGroups * 32) k_splitk_reduce(const float* __restrict__ part, int S, int64_t M,
-                                                                  int64_t N, int64_t ldp, float* __restrict__ out,
-                                                                  int64_t ldo) {
+                                                                  int64_t N, int64_t ldp, int64_t zs,
+                                                                  int64_t gap_row, int64_t gap,
+                                                                  float* __restrict__ out, int64_t ldo) {
     __shared__ float4 s_g[kRedGroups][32];
     const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int64_t n4 = N / 4;
     const int64_t t = (int64_t)blockIdx.x * 32 + lane;
     const bool live = t < M * n4;
     const int64_t i = live ? t / n4 : 0, j = live ? (t % n4) * 4 : 0;
-    const float* p0 = part + i * ldp + j;
-    const int64_t zs = M * ldp;
+    const float* p0 = part + (i < gap_row ? i : i + gap) * ldp + j;   // partial rows [gap_row, +gap) are padding
     const int per = (S + kRedGroups - 1) / kRedGroups;
     const int z0 = min(S, g * per), z1 = min(S, z0 + per);
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -137,9 +137,10 @@ __global__ void __launch_bounds__(kRedGroups * 32) k_splitk_reduce(const float* 
     *reinterpret_cast<float4*>(out + i * ldo + j) = r;
 }
 
-void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw) {
+void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw, int64_t gap_row, int64_t gap) {
     const int64_t n4 = K * N / 4;
-    k_splitk_reduce<<<(unsigned)((n4 + 31) / 32), kRedGroups * 32, 0, c.stream>>>(c.d_splitk, S, K, N, N, Wg, ldw);
+    k_splitk_reduce<<<(unsigned)((n4 + 31) / 32), kRedGroups * 32, 0, c.stream>>>(c.d_splitk, S, K, N, N, (K + gap) * N,
+                                                                                   gap_row, gap, Wg, ldw);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -180,7 +181,8 @@ static void wgrad_t(Ctx& c, int64_t M, int64_t K, int64_t N, const void* A, int6
     k_gemm<T, float, 1><<<grid, 256, 0, c.stream>>>(K, N, M, (const T*)A, 0, lda, nullptr, 0, (const T*)D, ldd,
                                                     c.d_splitk, N, false, nullptr, 0, chunk);
     int64_t tot = K * N;
-    k_splitk_reduce<<<(unsigned)((tot / 4 + 31) / 32), kRedGroups * 32, 0, c.stream>>>(c.d_splitk, (int)S, K, N, N, Wg, ldw);
+    k_splitk_reduce<<<(unsigned)((tot / 4 + 31) / 32), kRedGroups * 32, 0, c.stream>>>(c.d_splitk, (int)S, K, N, N, tot,
+                                                                                   INT64_MAX, 0, Wg, ldw);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
 }

@@ -122,7 +122,7 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 template <bool A_MN, bool B_MN, bool F32>
 __global__ void __launch_bounds__(TcCfg<F32>::THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
-          const __grid_constant__ CUtensorMap mapB, const TcArgs args) {
+          const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapB1, const TcArgs args) {
     using Cfg = TcCfg<F32>;
     constexpr int STAGES = Cfg::STAGES, STAGE_BYTES = Cfg::STAGE_BYTES, KE = Cfg::KE, MNE = Cfg::MNE;
     constexpr int BOX_BYTES = KE * TC_ROW_BYTES;          // one MN-major box {MNE, KE}: 8 KB bf16, 4 KB fp32
@@ -158,6 +158,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA1) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB1) : "memory");
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
@@ -198,11 +199,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                         for (int j = 0; j < TC_BM / MNE; ++j)
                             tma_load_2d(ma, &full[s], sa + j * BOX_BYTES, mm + MNE * j, kb * KE);
                     }
+                    // output rows past msplit also take their B operand from mapB1 (a pair of dW GEMMs with
+                    // different A and D in one launch)
+                    const CUtensorMap* mb = m0 >= args.msplit ? &mapB1 : &mapB;
                     if (!B_MN) {
-                        tma_load_2d(&mapB, &full[s], sb, kb * KE, (int)n0);           // box {KE (k), BN (n)}
+                        tma_load_2d(mb, &full[s], sb, kb * KE, (int)n0);              // box {KE (k), BN (n)}
                     } else {
                         for (int j = 0; j < args.BN / MNE; ++j)                        // boxes {MNE (n), KE (k)}
-                            tma_load_2d(&mapB, &full[s], sb + j * BOX_BYTES, (int)n0 + MNE * j, kb * KE);
+                            tma_load_2d(mb, &full[s], sb + j * BOX_BYTES, (int)n0 + MNE * j, kb * KE);
                     }
                     if (++s == STAGES) { s = 0; ph ^= 1u; }
                 }
@@ -402,8 +406,8 @@ static CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int6
 }
 
 template <bool A_MN, bool B_MN, bool F32>
-static void launch_tc_t(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const TcArgs& args,
-                        dim3 grid) {
+static void launch_tc_t(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
+                        const CUtensorMap& b1, const TcArgs& args, dim3 grid) {
     using Cfg = TcCfg<F32>;
     static bool configured = false;
     if (!configured) {
@@ -411,16 +415,16 @@ static void launch_tc_t(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, co
                                       Cfg::SMEM));
         configured = true;
     }
-    k_gemm_tc<A_MN, B_MN, F32><<<grid, Cfg::THREADS, Cfg::SMEM, c.stream>>>(a0, a1, b, args);
+    k_gemm_tc<A_MN, B_MN, F32><<<grid, Cfg::THREADS, Cfg::SMEM, c.stream>>>(a0, a1, b, b1, args);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 
 template <bool A_MN, bool B_MN>
 static void launch_tc(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const TcArgs& args,
-                      dim3 grid) {
-    if (c.prec == BNS_FP32) launch_tc_t<A_MN, B_MN, true>(c, a0, a1, b, args, grid);
-    else launch_tc_t<A_MN, B_MN, false>(c, a0, a1, b, args, grid);
+                      dim3 grid, const CUtensorMap* b1 = nullptr) {
+    if (c.prec == BNS_FP32) launch_tc_t<A_MN, B_MN, true>(c, a0, a1, b, b1 ? *b1 : b, args, grid);
+    else launch_tc_t<A_MN, B_MN, false>(c, a0, a1, b, b1 ? *b1 : b, args, grid);
 }
 
 static inline bool is_f32(const Ctx& c) { return c.prec == BNS_FP32; }
@@ -556,44 +560,58 @@ void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int6
     splitk_reduce(c, (int)S, K, N, Wg, ldw);
 }
 
-// [dW_0 ; dW_1] = [A0 | A1]^T D in one launch + one split-K reduce (rows [0, K) from A0, [K, 2K) from A1; the
-// GraphSAGE dW_z / dW_h pair, Wg rows contiguous).  Needs K % 128 == 0 (else two gemm_wgrad_tc calls).
-void gemm_wgrad2_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, const void* A1, int64_t lda,
-                    const void* D, int64_t ldd, float* Wg, int64_t ldw) {
-    if (K % TC_BM != 0) {
-        gemm_wgrad_tc(c, Mn, K, N, A0, lda, D, ldd, Wg, ldw);
-        gemm_wgrad_tc(c, Mn, K, N, A1, lda, D, ldd, Wg + K * ldw, ldw);
+// [dW_0 ; dW_1] = [A0^T D0 ; A1^T D1] in one launch + one split-K reduce: output rows [0, K) from (A0, D0) over Mn0
+// nodes, rows [K, 2K) from (A1, D1) over Mn1 nodes (Wg rows contiguous).  The second product starts at the 128-row
+// tile boundary Kp >= K; the node range is max(Mn0, Mn1) and the TMA zero-fills the rows past each operand's own
+// count.  Uses: the GraphSAGE dW_z / dW_h pair (D1 = D0, Mn1 = Mn0) and the transform-first dW_top / dW_bot pair
+// (R42: D0 = dY over every stacked row, D1 = dPre over the inner rows).
+void gemm_wgrad2_tc(Ctx& c, int64_t Mn0, int64_t Mn1, int64_t K, int64_t N, const void* A0, const void* A1,
+                    int64_t lda, const void* D0, int64_t ldd0, const void* D1, int64_t ldd1, float* Wg, int64_t ldw) {
+    if (N <= 0 || K <= 0) return;
+    const bool f32 = is_f32(c);
+    if (f32 && D1 == D0 && Mn1 == Mn0) return wgrad_f32(c, Mn0, K, N, A0, A1, lda, D0, ldd0, Wg, ldw);
+    if (f32) {
+        gemm_wgrad_tc(c, Mn0, K, N, A0, lda, D0, ldd0, Wg, ldw);
+        gemm_wgrad_tc(c, Mn1, K, N, A1, lda, D1, ldd1, Wg + K * ldw, ldw);
         return;
     }
-    if (N <= 0) return;
-    const bool f32 = is_f32(c);
-    if (f32) return wgrad_f32(c, Mn, K, N, A0, A1, lda, D, ldd, Wg, ldw);
     const int KE = k_elems(c);
-    const int64_t K2 = 2 * K;
+    const int64_t Kp = cdiv(K, TC_BM) * TC_BM, M2 = Kp + K;
+    const int64_t Mn = std::max(Mn0, Mn1);
+    if (Mn <= 0) {
+        BNS_CUDA(cudaMemset2DAsync(Wg, ldw * sizeof(float), 0, N * sizeof(float), 2 * K, c.stream));
+        return;
+    }
     TcArgs a{};
-    a.M = K2;
+    a.M = M2;
     a.N = N;
     a.BN = (int)std::min<int64_t>(256, cdiv(N, 64) * 64);
     a.nk = (int)cdiv(Mn, KE);
     a.nk0 = a.nk;
-    a.msplit = K;
-    const int64_t tiles = cdiv(K2, TC_BM) * cdiv(N, a.BN);
+    a.msplit = Kp;
+    const int64_t tiles = cdiv(M2, TC_BM) * cdiv(N, a.BN);
     static const int kmin0 = [] { const char* e = std::getenv("BNS_WGRAD_KMIN"); return e ? std::max(1, std::atoi(e)) : 16; }();
     const int kmin = kmin0 * 64 / KE;
     int64_t S = std::max<int64_t>(1, std::min<int64_t>(cdiv(148, tiles), std::max(1, a.nk / kmin)));
-    while (S > 1 && S * K2 * N > c.splitk_cap) --S;
+    while (S > 1 && S * M2 * N > c.splitk_cap) --S;
+    if (M2 * N > c.splitk_cap) {   // cannot happen with the setup sizing; keep the two-launch form as the guard
+        gemm_wgrad_tc(c, Mn0, K, N, A0, lda, D0, ldd0, Wg, ldw);
+        gemm_wgrad_tc(c, Mn1, K, N, A1, lda, D1, ldd1, Wg + K * ldw, ldw);
+        return;
+    }
     a.kb_per_split = (int)cdiv(a.nk, S);
     S = cdiv(a.nk, a.kb_per_split);
     c.last_splitk = (int)S;
     a.epi = EPI_F32;
     a.out = c.d_splitk;
     a.ldc = N;
-    a.split_stride = K2 * N;
-    CUtensorMap m0 = make_map(A0, K, Mn, lda, KE, f32);
-    CUtensorMap m1 = make_map(A1, K, Mn, lda, KE, f32);
-    CUtensorMap mb = make_map(D, N, Mn, ldd, KE, f32);
-    launch_tc<true, true>(c, m0, m1, mb, a, persistent_grid(tiles * S));
-    splitk_reduce(c, (int)S, K2, N, Wg, ldw);
+    a.split_stride = M2 * N;
+    CUtensorMap m0 = make_map(A0, K, std::max<int64_t>(Mn0, 1), lda, KE, f32);
+    CUtensorMap m1 = make_map(A1, K, std::max<int64_t>(Mn1, 1), lda, KE, f32);
+    CUtensorMap mb0 = make_map(D0, N, std::max<int64_t>(Mn0, 1), ldd0, KE, f32);
+    CUtensorMap mb1 = make_map(D1, N, std::max<int64_t>(Mn1, 1), ldd1, KE, f32);
+    launch_tc<true, true>(c, m0, m1, mb0, a, persistent_grid(tiles * S), &mb1);
+    splitk_reduce(c, (int)S, 2 * K, N, Wg, ldw, K, Kp - K);
 }
 
 // dX: C[M x Nc] = D[M x K] · B^T with B = W [Nc][K] row-major; columns < scale_cols scaled by rowscale[row]

@@ -84,15 +84,17 @@ void gemm_wgrad(Ctx& c, int64_t M, int64_t K, int64_t N, const void* A, int64_t 
 void gemm_dx(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t ldd, const void* B, int64_t ldb,
              void* C, int64_t ldc, const float* rowscale, int64_t scale_cols);
 
-void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw);
+// out[K x N] = sum over S partial slices (fixed order); partial rows [gap_row, gap_row + gap) are skipped padding
+void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw, int64_t gap_row = INT64_MAX,
+                   int64_t gap = 0);
 
 // tcgen05 bf16 versions (gemm_tc.cu); fwd takes B = W^T stored [N][Kw] with each concat half padded to 64
 void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64_t lda0, const void* A1, int64_t K1,
                  int64_t lda1, const void* WT, int64_t Kw, void* C, int64_t ldc, bool relu, bool out_f32);
 void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int64_t lda, const void* D, int64_t ldd,
                    float* Wg, int64_t ldw);
-void gemm_wgrad2_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A0, const void* A1, int64_t lda,
-                    const void* D, int64_t ldd, float* Wg, int64_t ldw);
+void gemm_wgrad2_tc(Ctx& c, int64_t Mn0, int64_t Mn1, int64_t K, int64_t N, const void* A0, const void* A1,
+                    int64_t lda, const void* D0, int64_t ldd0, const void* D1, int64_t ldd1, float* Wg, int64_t ldw);
 void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t ldd, const void* B, int64_t ldb,
                 void* C, int64_t ldc, const float* rowscale, int64_t scale_cols);
 

@@ -319,8 +319,12 @@ void backward_layer_tf(Ctx& c, const EpochView& v, int l, void* Hin) {
         float* g = c.d_gflat + c.goff[l - 1];
         auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
         auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
-        wgrad(c, rows, din, dout, Hin, din, c.d_tfy, 2 * dout, g, dout);
-        wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
+        if (c.use_tc) {   // dW_top (every stacked row) and dW_bot (inner rows) in one launch + one reduce
+            gemm_wgrad2_tc(c, rows, n_in, din, dout, Hin, Hin, din, c.d_tfy, 2 * dout, c.d_dpre, dout, g, dout);
+        } else {
+            wgrad(c, rows, din, dout, Hin, din, c.d_tfy, 2 * dout, g, dout);
+            wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
+        }
         if (l > 1) {   // dX = [dY | dPre] [W_top | W_bot]^T over every stacked row, one GEMM: halo rows have no dPre
             BNS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(c.d_tfy) + dout * ts, 2 * dout * ts, c.d_dpre,
                                        dout * ts, dout * ts, n_in, cudaMemcpyDeviceToDevice, c.stream));
@@ -345,7 +349,7 @@ void backward_layer_std(Ctx& c, const EpochView& v, int l, void* Hin) {
         auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
         auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
         if (sage && c.use_tc) {   // dW_z and dW_h share dPre: one launch, one split-K reduce
-            gemm_wgrad2_tc(c, n_in, din, dout, c.Z[l], Hin, din, c.d_dpre, dout, g, dout);
+            gemm_wgrad2_tc(c, n_in, n_in, din, dout, c.Z[l], Hin, din, c.d_dpre, dout, c.d_dpre, dout, g, dout);
         } else {
             wgrad(c, n_in, din, dout, c.Z[l], din, c.d_dpre, dout, g, dout);
             if (sage) wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
