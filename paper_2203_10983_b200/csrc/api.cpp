@@ -294,6 +294,9 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     int64_t seg_max = std::max({c.seg_fwd_cap, c.seg_bwd_cap, c.n_seg_static_fwd});
     c.d_partial = static_cast<float*>(dalloc(c, (size_t)seg_max * c.maxd * sizeof(float)));
     c.d_spmm_work = static_cast<unsigned long long*>(dalloc(c, 64));
+    c.d_spmm_arrive = static_cast<int32_t*>(dalloc(c, (size_t)seg_max * sizeof(int32_t)));
+    BNS_CUDA_HOLD(cudaMemsetAsync(c.d_spmm_work, 0, 64, c.stream));
+    BNS_CUDA_HOLD(cudaMemsetAsync(c.d_spmm_arrive, 0, (size_t)seg_max * sizeof(int32_t), c.stream));
     // split (hub) row lists: first segment of every row with more than one segment
     auto split_list = [](const std::vector<Seg>& s) {
         std::vector<int64_t> l;
@@ -540,7 +543,7 @@ void draw_enqueue(Ctx& c, int sampler, double p, uint64_t seed, uint64_t epoch) 
     }
     total.reset();
     const int64_t nslot = 2 * m + 1 + 8;
-    BNS_CUDA(cudaMemcpyAsync(c.h_seg_pos, c.d_seg_pos, nslot * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    BNS_CUDA_HOLD(cudaMemcpyAsync(c.h_seg_pos, c.d_seg_pos, nslot * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
 }
 
 // the host side of a draw: wait for the counts (unless an earlier sync already covered the copy), size the epoch
@@ -636,7 +639,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         if (host_w) {
             W[l] = c.d_hostw + off;
             G[l] = c.d_hostw + c.hostw_n + off;
-            BNS_CUDA(cudaMemcpyAsync(W[l], W_in[l], wl[l] * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+            BNS_CUDA_HOLD(cudaMemcpyAsync(W[l], W_in[l], wl[l] * sizeof(float), cudaMemcpyHostToDevice, c.stream));
         } else {
             W[l] = W_in[l];
             G[l] = G_in ? G_in[l] : nullptr;
@@ -693,12 +696,20 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     {
         PhaseTimer t(c, BNS_PH_LOSS);
         const bool tfL = (c.tf_mask >> (L - 1)) & 1u;
+        // R42 with a dX (L > 1): dPre goes straight into the dPre half of the [dY | dPre] operand, halo rows zeroed
+        void* dpre = c.d_dpre;
+        int64_t ldp = c.dp[L], nzero = 0;
+        if (tf_dpre_in_tfy(c, L)) {
+            dpre = static_cast<char*>(c.d_tfy) + c.dp[L] * ts;
+            ldp = 2 * c.dp[L];
+            nzero = c.n_halo;
+        }
         if (c.multilabel)
-            launch_bce(c, c.d_logits, c.dp[L], c.dims[L], c.retain ? c.d_dlogits : nullptr, c.d_dpre, tfL ? c.d_deg_in : nullptr,
-                       tfL ? c.d_dxcat : nullptr);
+            launch_bce(c, c.d_logits, c.dp[L], c.dims[L], c.retain ? c.d_dlogits : nullptr, dpre, tfL ? c.d_deg_in : nullptr,
+                       tfL ? c.d_dxcat : nullptr, ldp, nzero);
         else
-            launch_xent(c, c.d_logits, c.dp[L], c.dims[L], c.retain ? c.d_dlogits : nullptr, c.d_dpre, tfL ? c.d_deg_in : nullptr,
-                        tfL ? c.d_dxcat : nullptr);
+            launch_xent(c, c.d_logits, c.dp[L], c.dims[L], c.retain ? c.d_dlogits : nullptr, dpre, tfL ? c.d_deg_in : nullptr,
+                        tfL ? c.d_dxcat : nullptr, ldp, nzero);
     }
     // ------------------------------ backward (l.12) ------------------------------
     for (int l = L; l >= 1; --l) {
@@ -707,7 +718,7 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         if (l < L) {
             PhaseTimer t(c, BNS_PH_GEMM_BWD);
             if (c.retain)
-                BNS_CUDA(cudaMemcpyAsync(c.dH_keep[l], c.d_dx, n_in * dout * ts, cudaMemcpyDeviceToDevice, c.stream));
+                BNS_CUDA_HOLD(cudaMemcpyAsync(c.dH_keep[l], c.d_dx, n_in * dout * ts, cudaMemcpyDeviceToDevice, c.stream));
             const bool tfl = (c.tf_mask >> (l - 1)) & 1u;   // R42: + dPre / deg_G into d_dxcat (unused there)
             launch_relu_mask(c, c.d_dx, c.H[l], dout, n_in, (int32_t)dout, c.d_dpre, tfl ? c.d_deg_in : nullptr,
                              tfl ? c.d_dxcat : nullptr);
@@ -766,13 +777,13 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     }
     double scal[4] = {0.0, 0.0, 0.0, 0.0};
     int32_t nonfinite = 0;
-    BNS_CUDA(cudaMemcpyAsync(scal, c.d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c.stream));
-    BNS_CUDA(cudaMemcpyAsync(&nonfinite, c.d_nonfinite, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+    BNS_CUDA_HOLD(cudaMemcpyAsync(scal, c.d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c.stream));
+    BNS_CUDA_HOLD(cudaMemcpyAsync(&nonfinite, c.d_nonfinite, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
     if (host_w) {
         for (int l = 0; l < L; ++l) {
-            BNS_CUDA(cudaMemcpyAsync(W_in[l], W[l], wl[l] * sizeof(float), cudaMemcpyDeviceToHost, c.stream));
+            BNS_CUDA_HOLD(cudaMemcpyAsync(W_in[l], W[l], wl[l] * sizeof(float), cudaMemcpyDeviceToHost, c.stream));
             if (G_in && G_in[l])
-                BNS_CUDA(cudaMemcpyAsync(G_in[l], G[l], wl[l] * sizeof(float), cudaMemcpyDeviceToHost, c.stream));
+                BNS_CUDA_HOLD(cudaMemcpyAsync(G_in[l], G[l], wl[l] * sizeof(float), cudaMemcpyDeviceToHost, c.stream));
         }
     }
     BNS_CUDA(cudaStreamSynchronize(c.stream));

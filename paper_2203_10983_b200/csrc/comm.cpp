@@ -110,17 +110,20 @@ struct NcclTransport : Transport {
                                   c.stream));
         }
         BNS_NCCL(ncclGroupEnd());
+        pdl_hold();
     }
     void allreduce(Ctx& c, float* buf, int64_t n, double* scal, int64_t ns) override {
         BNS_NCCL(ncclGroupStart());
         BNS_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclFloat32, ncclSum, comm, c.stream));
         BNS_NCCL(ncclAllReduce(scal, scal, (size_t)ns, ncclFloat64, ncclSum, comm, c.stream));
         BNS_NCCL(ncclGroupEnd());
+        pdl_hold();
     }
     int64_t allreduce_host_i64(Ctx& c, int64_t v) override {
-        BNS_CUDA(cudaMemcpyAsync(d_i64, &v, sizeof(v), cudaMemcpyHostToDevice, c.stream));
+        BNS_CUDA_HOLD(cudaMemcpyAsync(d_i64, &v, sizeof(v), cudaMemcpyHostToDevice, c.stream));
         BNS_NCCL(ncclAllReduce(d_i64, d_i64, 1, ncclInt64, ncclSum, comm, c.stream));
-        BNS_CUDA(cudaMemcpyAsync(&v, d_i64, sizeof(v), cudaMemcpyDeviceToHost, c.stream));
+        pdl_hold();
+        BNS_CUDA_HOLD(cudaMemcpyAsync(&v, d_i64, sizeof(v), cudaMemcpyDeviceToHost, c.stream));
         BNS_CUDA(cudaStreamSynchronize(c.stream));
         return v;
     }
@@ -167,7 +170,7 @@ struct LocalTransport : Transport {
     }
     void wait_all(Ctx& c, std::vector<cudaEvent_t>& ev) {
         for (int j = 0; j < g->world; ++j)
-            if (j != me) BNS_CUDA(cudaStreamWaitEvent(c.stream, ev[j], 0));
+            if (j != me) BNS_CUDA_HOLD(cudaStreamWaitEvent(c.stream, ev[j], 0));
     }
     void exchange(Ctx& c, const void* src, const int64_t* src_off, void* dst, const int64_t* dst_off,
                   size_t rowbytes) override {
@@ -183,8 +186,8 @@ struct LocalTransport : Transport {
                 throw Error(BNS_ERR_RUNTIME, "local transport: row count mismatch between ranks " +
                                                  std::to_string(j) + " -> " + std::to_string(me));
             if (n == 0) continue;
-            BNS_CUDA(cudaStreamWaitEvent(c.stream, g->ev_ready[j], 0));
-            BNS_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + dst_off[j] * rowbytes,
+            BNS_CUDA_HOLD(cudaStreamWaitEvent(c.stream, g->ev_ready[j], 0));
+            BNS_CUDA_HOLD(cudaMemcpyAsync(static_cast<char*>(dst) + dst_off[j] * rowbytes,
                                      static_cast<const char*>(g->src[j]) + g->src_off[j][me] * rowbytes, n * rowbytes,
                                      cudaMemcpyDeviceToDevice, c.stream));
         }
@@ -218,12 +221,13 @@ struct LocalTransport : Transport {
         BNS_CUDA(cudaMemcpy(d_dptrs, dp.data(), m * sizeof(double*), cudaMemcpyHostToDevice));
         wait_all(c, g->ev_ready);
         launch_sum_ptrs(c, d_fptrs, m, d_fout, n);
+        pdl_hold();   // both sums read the peers' buffers
         launch_sum_ptrs_d(c, d_dptrs, m, d_dout, ns);
         BNS_CUDA(cudaEventRecord(g->ev_done[me], c.stream));
         group_barrier(g);
         wait_all(c, g->ev_done);
-        BNS_CUDA(cudaMemcpyAsync(buf, d_fout, n * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
-        BNS_CUDA(cudaMemcpyAsync(scal, d_dout, ns * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+        BNS_CUDA_HOLD(cudaMemcpyAsync(buf, d_fout, n * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+        BNS_CUDA_HOLD(cudaMemcpyAsync(scal, d_dout, ns * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
     }
     int64_t allreduce_host_i64(Ctx&, int64_t v) override {
         g->ival[me] = v;
@@ -481,7 +485,7 @@ struct PeerTransport : Transport {
                 throw Error(BNS_ERR_RUNTIME, "peer-memory transport: row count mismatch between ranks " +
                                                  std::to_string(j) + " -> " + std::to_string(me));
             if (n > 0)
-                BNS_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + dst_off[j] * rowbytes,
+                BNS_CUDA_HOLD(cudaMemcpyAsync(static_cast<char*>(dst) + dst_off[j] * rowbytes,
                                          static_cast<const char*>(send[j]) + oj[me] * rowbytes, n * rowbytes,
                                          cudaMemcpyDeviceToDevice, c.stream));
         }
@@ -495,6 +499,7 @@ struct PeerTransport : Transport {
         float* gout = static_cast<float*>(own[K_G + (q ^ 1)]);
         double* sout = static_cast<double*>(own[K_S + (q ^ 1)]);
         launch_sum_ptrs(c, reinterpret_cast<const float* const*>(row(K_G + q)), m, gout, n);
+        pdl_hold();   // both sums read the peers' buffers
         launch_sum_ptrs_d(c, reinterpret_cast<const double* const*>(row(K_S + q)), m, sout, ns);
         // no second barrier: a peer reads my buffer q again only after the next epoch's barriers (ping-pong)
         c.d_gflat = gout;

@@ -25,6 +25,18 @@ struct Error : std::runtime_error {
 
 #define BNS_CHECK_LAUNCH() BNS_CUDA(cudaGetLastError())
 
+// PDL (dev.cuh): the next kernel this host thread launches is launched with plain stream serialisation -- called
+// after every non-kernel stream operation (copies, memsets, cross-stream event waits, NCCL calls) and around the
+// peer-memory barrier, so a kernel never starts early behind work whose completion griddepcontrol.wait does not
+// cover (another stream's, another context's, the copy engines')
+void pdl_hold();
+bool pdl_take_hold();
+#define BNS_CUDA_HOLD(x)  \
+    do {                  \
+        BNS_CUDA(x);      \
+        ::bns::pdl_hold(); \
+    } while (0)
+
 #ifndef BNS_KSEG
 #define BNS_KSEG 256   // A/B on one B200 (make kseg128 / kseg256): 512 -> 256 = m=8 rank epoch 2.23 -> 2.12 ms, m=1 24.3 -> 24.0
 #endif
@@ -177,7 +189,8 @@ struct Ctx {
     int32_t* d_static_col = nullptr; int64_t* d_static_ptr = nullptr;
     int64_t n_seg_bwd_inner = 0;
     float* d_partial = nullptr;    // hub-row partial sums
-    unsigned long long* d_spmm_work = nullptr;   // SpMM dynamic scheduling counter
+    unsigned long long* d_spmm_work = nullptr;   // SpMM dynamic scheduling: [next segment, warps done] (self-resetting)
+    int32_t* d_spmm_arrive = nullptr;  // fused split-row fixup: segments of each split row finished (by first segment)
     int64_t* d_split_sf = nullptr;  int64_t n_split_sf = 0;      // split rows of the static forward segments
     int64_t* d_split_bwd = nullptr; int64_t n_split_bwd_inner = 0; // [static inner part ; per-epoch halo part]
     int64_t* d_split_fwd = nullptr;                                  // per-epoch induced forward segments

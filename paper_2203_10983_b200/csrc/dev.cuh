@@ -3,8 +3,43 @@
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace bns {
+
+// Programmatic dependent launch (PDL).  Every kernel of the library starts with pdl_grid_sync(): wait until the
+// previous grid in the stream has completed and its writes are visible (griddepcontrol.wait -- a no-op when the
+// kernel was launched without the PDL attribute), then let the next grid's CTAs be scheduled (launch_dependents).
+// Launched by pdl_launch, a kernel's CTAs therefore become resident while the previous kernel drains and start the
+// moment it completes: the launch latency and the CTA ramp of each of the ~50 kernels of an epoch overlap the tail
+// of the one before.  Because each grid waits before it touches memory and triggers only after that wait, a grid's
+// completion still implies the completion of everything enqueued before it (the usual stream order).
+__device__ __forceinline__ void pdl_grid_sync() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// BNS_PDL=0 launches every kernel with plain stream serialisation (A/B); pdl_take_hold (common.h): this launch
+// follows a non-kernel stream operation
+bool pdl_enabled();
+bool pdl_take_hold();
+
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(cudaStream_t s, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (!pdl_take_hold() && pdl_enabled()) ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);   // errors surface in BNS_CHECK_LAUNCH
+}
 
 // A 16-byte vector of the storage type: 4 x fp32 or 8 x bf16.
 template <typename T> struct Vec;

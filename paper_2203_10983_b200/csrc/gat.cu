@@ -40,6 +40,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_gat_scores(const T* __restrict__ Y, int64_t ld, int64_t rows, int32_t d,
                                                     const float* __restrict__ al, const float* __restrict__ ar,
                                                     float* __restrict__ el, float* __restrict__ er) {
+    pdl_grid_sync();
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(256) k_gat_stats(const Seg* __restrict__ segs,
                                                    const int32_t* __restrict__ col, const float* __restrict__ el,
                                                    const float* __restrict__ er, float* __restrict__ part,
                                                    float* __restrict__ m_out, float* __restrict__ inv_out) {
+    pdl_grid_sync();
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t sid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sid < n_segs; sid += nw) {
@@ -85,6 +87,7 @@ __global__ void k_gat_stats_fix(const Seg* __restrict__ segs, const int64_t* __r
                                 const float* __restrict__ el, const float* __restrict__ er,
                                 const float* __restrict__ part, float* __restrict__ m_out,
                                 float* __restrict__ inv_out) {
+    pdl_grid_sync();
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n_split) return;
     const int64_t sid = split[q];
@@ -102,6 +105,7 @@ __global__ void __launch_bounds__(256) k_gat_rowdots(const T* __restrict__ g, co
                                                      const float* __restrict__ el, const float* __restrict__ er,
                                                      const float* __restrict__ m, const float* __restrict__ inv,
                                                      float* __restrict__ cdot, float* __restrict__ selfds) {
+    pdl_grid_sync();
     using V = Vec<T>;
     constexpr int VN = V::N;
     const int lane = threadIdx.x & 31;
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(256) k_gat_wsum(const Seg* __restrict__ segs, 
                                                   const float* __restrict__ er, const float* __restrict__ m,
                                                   const float* __restrict__ inv, const float* __restrict__ cdot,
                                                   float* __restrict__ part, float* __restrict__ out) {
+    pdl_grid_sync();
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t sid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sid < n_segs; sid += nw) {
@@ -170,6 +175,7 @@ __global__ void __launch_bounds__(256) k_gat_wsum(const Seg* __restrict__ segs, 
 
 __global__ void k_gat_wsum_fix(const Seg* __restrict__ segs, const int64_t* __restrict__ split, int64_t n_split,
                                const float* __restrict__ part, float* __restrict__ out) {
+    pdl_grid_sync();
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n_split) return;
     const int64_t sid = split[q];
@@ -185,6 +191,7 @@ __global__ void __launch_bounds__(256) k_gat_final(const T* __restrict__ own, co
                                                    int64_t ld, int32_t d, int64_t rows, int64_t n_in,
                                                    const float* __restrict__ cdot, const float* __restrict__ qr,
                                                    const float* __restrict__ selfds, float* __restrict__ out) {
+    pdl_grid_sync();
     using V = Vec<T>;
     constexpr int VN = V::N;
     const int lane = threadIdx.x & 31;
@@ -201,6 +208,7 @@ constexpr int kDaBlocks = 296;
 template <typename T>
 __global__ void __launch_bounds__(256) k_gat_da1(const T* __restrict__ Y, int64_t ld, int32_t d,
                                                  const float* __restrict__ w, int64_t rows, float* __restrict__ part) {
+    pdl_grid_sync();
     const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
     const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(rows, r0 + per);
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
@@ -211,6 +219,7 @@ __global__ void __launch_bounds__(256) k_gat_da1(const T* __restrict__ Y, int64_
 }
 
 __global__ void k_gat_da2(const float* __restrict__ part, int nb, int32_t d, float* __restrict__ out) {
+    pdl_grid_sync();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= d) return;
     float s = 0.f;
@@ -224,9 +233,9 @@ void launch_gat_scores(Ctx& c, const void* Y, int64_t ld, int64_t rows, int32_t 
     if (rows <= 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 16);
     if (c.prec == BNS_BF16)
-        k_gat_scores<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)Y, ld, rows, d, al, ar, el, er);
+        pdl_launch(c.stream, k_gat_scores<__nv_bfloat16>, grid, 256, 0, (const __nv_bfloat16*)Y, ld, rows, d, al, ar, el, er);
     else
-        k_gat_scores<float><<<grid, 256, 0, c.stream>>>((const float*)Y, ld, rows, d, al, ar, el, er);
+        pdl_launch(c.stream, k_gat_scores<float>, grid, 256, 0, (const float*)Y, ld, rows, d, al, ar, el, er);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -235,10 +244,10 @@ void launch_gat_stats(Ctx& c, const Seg* segs, int64_t n_segs, const int32_t* co
                       int64_t n_split, const float* el, const float* er, float* m, float* inv) {
     if (n_segs <= 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>((n_segs + 7) / 8, 148 * 16);
-    k_gat_stats<<<grid, 256, 0, c.stream>>>(segs, n_segs, col, el, er, c.d_partial, m, inv);
+    pdl_launch(c.stream, k_gat_stats, grid, 256, 0, segs, n_segs, col, el, er, c.d_partial, m, inv);
     c.kernels += 1;
     if (n_split > 0) {
-        k_gat_stats_fix<<<(unsigned)((n_split + 127) / 128), 128, 0, c.stream>>>(segs, split, n_split, el, er,
+        pdl_launch(c.stream, k_gat_stats_fix, (unsigned)((n_split + 127) / 128), 128, 0, segs, split, n_split, el, er,
                                                                                  c.d_partial, m, inv);
         c.kernels += 1;
     }
@@ -250,7 +259,7 @@ void launch_gat_rowdots(Ctx& c, const void* g, const void* out, bool out_f32, co
     const int64_t n = c.plan.n_in;
     if (n <= 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16);
-#define BNS_RD(T, F) k_gat_rowdots<T, F><<<grid, 256, 0, c.stream>>>((const T*)g, out, (const T*)Y, ld, n, d, el, er, m, inv, cdot, selfds)
+#define BNS_RD(T, F) pdl_launch(c.stream, k_gat_rowdots<T, F>, grid, 256, 0, (const T*)g, out, (const T*)Y, ld, n, d, el, er, m, inv, cdot, selfds)
     if (c.prec == BNS_BF16) { if (out_f32) BNS_RD(__nv_bfloat16, true); else BNS_RD(__nv_bfloat16, false); }
     else { if (out_f32) BNS_RD(float, true); else BNS_RD(float, false); }
 #undef BNS_RD
@@ -263,11 +272,11 @@ void launch_gat_wsum(Ctx& c, int dir, const Seg* segs, int64_t n_segs, const int
                      const float* cdot, float* out) {
     if (n_segs <= 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>((n_segs + 7) / 8, 148 * 16);
-    if (dir == 0) k_gat_wsum<0><<<grid, 256, 0, c.stream>>>(segs, n_segs, col, el, er, m, inv, cdot, c.d_partial, out);
-    else k_gat_wsum<1><<<grid, 256, 0, c.stream>>>(segs, n_segs, col, el, er, m, inv, cdot, c.d_partial, out);
+    if (dir == 0) pdl_launch(c.stream, k_gat_wsum<0>, grid, 256, 0, segs, n_segs, col, el, er, m, inv, cdot, c.d_partial, out);
+    else pdl_launch(c.stream, k_gat_wsum<1>, grid, 256, 0, segs, n_segs, col, el, er, m, inv, cdot, c.d_partial, out);
     c.kernels += 1;
     if (n_split > 0) {
-        k_gat_wsum_fix<<<(unsigned)((n_split + 127) / 128), 128, 0, c.stream>>>(segs, split, n_split, c.d_partial, out);
+        pdl_launch(c.stream, k_gat_wsum_fix, (unsigned)((n_split + 127) / 128), 128, 0, segs, split, n_split, c.d_partial, out);
         c.kernels += 1;
     }
     BNS_CHECK_LAUNCH();
@@ -278,7 +287,7 @@ void launch_gat_final(Ctx& c, int dir, const void* own, const float* qp, int64_t
     if (rows <= 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 16);
     const int64_t n_in = c.plan.n_in;
-#define BNS_FIN(T, DIR) k_gat_final<T, DIR><<<grid, 256, 0, c.stream>>>((const T*)own, qp, ld, d, rows, n_in, cdot, qr, selfds, out)
+#define BNS_FIN(T, DIR) pdl_launch(c.stream, k_gat_final<T, DIR>, grid, 256, 0, (const T*)own, qp, ld, d, rows, n_in, cdot, qr, selfds, out)
     if (c.prec == BNS_BF16) { if (dir == 0) BNS_FIN(__nv_bfloat16, 0); else BNS_FIN(__nv_bfloat16, 1); }
     else { if (dir == 0) BNS_FIN(float, 0); else BNS_FIN(float, 1); }
 #undef BNS_FIN
@@ -289,10 +298,10 @@ void launch_gat_final(Ctx& c, int dir, const void* own, const float* qp, int64_t
 void launch_gat_da(Ctx& c, const void* Y, int64_t ld, int32_t d, const float* w, int64_t rows, float* out) {
     float* part = c.d_splitk;   // kDaBlocks x d floats (<= the split-K scratch)
     if (c.prec == BNS_BF16)
-        k_gat_da1<__nv_bfloat16><<<kDaBlocks, 256, 0, c.stream>>>((const __nv_bfloat16*)Y, ld, d, w, rows, part);
+        pdl_launch(c.stream, k_gat_da1<__nv_bfloat16>, kDaBlocks, 256, 0, (const __nv_bfloat16*)Y, ld, d, w, rows, part);
     else
-        k_gat_da1<float><<<kDaBlocks, 256, 0, c.stream>>>((const float*)Y, ld, d, w, rows, part);
-    k_gat_da2<<<(unsigned)((d + 255) / 256), 256, 0, c.stream>>>(part, kDaBlocks, d, out);
+        pdl_launch(c.stream, k_gat_da1<float>, kDaBlocks, 256, 0, (const float*)Y, ld, d, w, rows, part);
+    pdl_launch(c.stream, k_gat_da2, (unsigned)((d + 255) / 256), 256, 0, part, kDaBlocks, d, out);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
 }

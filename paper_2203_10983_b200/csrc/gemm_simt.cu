@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256) k_gemm(int64_t M, int64_t N, int64_t K, c
                                               const T* __restrict__ B, int64_t ldb, TC* __restrict__ C, int64_t ldc,
                                               bool relu, const float* __restrict__ rowscale, int64_t scale_cols,
                                               int64_t kchunk) {
+    pdl_grid_sync();
     __shared__ float As[BK][BM + 4];
     __shared__ float Bs[BK][BN + 4];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(kRedGroups * 32) k_splitk_reduce(const float* 
                                                                   int64_t N, int64_t ldp, int64_t zs,
                                                                   int64_t gap_row, int64_t gap,
                                                                   float* __restrict__ out, int64_t ldo) {
+    pdl_grid_sync();
     __shared__ float4 s_g[kRedGroups][32];
     const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int64_t n4 = N / 4;
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(kRedGroups * 32) k_splitk_reduce(const float* 
 
 void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw, int64_t gap_row, int64_t gap) {
     const int64_t n4 = K * N / 4;
-    k_splitk_reduce<<<(unsigned)((n4 + 31) / 32), kRedGroups * 32, 0, c.stream>>>(c.d_splitk, S, K, N, N, (K + gap) * N,
+    pdl_launch(c.stream, k_splitk_reduce, (unsigned)((n4 + 31) / 32), kRedGroups * 32, 0, c.d_splitk, S, K, N, N, (K + gap) * N,
                                                                                    gap_row, gap, Wg, ldw);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -151,10 +153,10 @@ static void fwd_t(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int6
     dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
     const int64_t K = K0 + K1;
     if (out_f32)
-        k_gemm<T, float, 0><<<grid, 256, 0, c.stream>>>(M, N, K, (const T*)A0, K0, lda0, (const T*)A1, lda1,
+        pdl_launch(c.stream, k_gemm<T, float, 0>, grid, 256, 0, M, N, K, (const T*)A0, K0, lda0, (const T*)A1, lda1,
                                                         (const T*)B, ldb, (float*)C, ldc, relu, nullptr, 0, 0);
     else
-        k_gemm<T, T, 0><<<grid, 256, 0, c.stream>>>(M, N, K, (const T*)A0, K0, lda0, (const T*)A1, lda1,
+        pdl_launch(c.stream, k_gemm<T, T, 0>, grid, 256, 0, M, N, K, (const T*)A0, K0, lda0, (const T*)A1, lda1,
                                                     (const T*)B, ldb, (T*)C, ldc, relu, nullptr, 0, 0);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -178,10 +180,10 @@ static void wgrad_t(Ctx& c, int64_t M, int64_t K, int64_t N, const void* A, int6
     S = (M + chunk - 1) / chunk;
     if (S < 1) S = 1;
     dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((K + BM - 1) / BM), (unsigned)S);
-    k_gemm<T, float, 1><<<grid, 256, 0, c.stream>>>(K, N, M, (const T*)A, 0, lda, nullptr, 0, (const T*)D, ldd,
+    pdl_launch(c.stream, k_gemm<T, float, 1>, grid, 256, 0, K, N, M, (const T*)A, 0, lda, nullptr, 0, (const T*)D, ldd,
                                                     c.d_splitk, N, false, nullptr, 0, chunk);
     int64_t tot = K * N;
-    k_splitk_reduce<<<(unsigned)((tot / 4 + 31) / 32), kRedGroups * 32, 0, c.stream>>>(c.d_splitk, (int)S, K, N, N, tot,
+    pdl_launch(c.stream, k_splitk_reduce, (unsigned)((tot / 4 + 31) / 32), kRedGroups * 32, 0, c.d_splitk, (int)S, K, N, N, tot,
                                                                                    INT64_MAX, 0, Wg, ldw);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
@@ -191,7 +193,7 @@ void gemm_wgrad(Ctx& c, int64_t M, int64_t K, int64_t N, const void* A, int64_t 
                 float* Wg, int64_t ldw) {
     if (K <= 0 || N <= 0) return;
     if (M <= 0) {
-        for (int64_t i = 0; i < K; ++i) BNS_CUDA(cudaMemsetAsync(Wg + i * ldw, 0, N * sizeof(float), c.stream));
+        for (int64_t i = 0; i < K; ++i) BNS_CUDA_HOLD(cudaMemsetAsync(Wg + i * ldw, 0, N * sizeof(float), c.stream));
         return;
     }
     if (c.prec == BNS_BF16) wgrad_t<__nv_bfloat16>(c, M, K, N, A, lda, D, ldd, Wg, ldw);
@@ -202,7 +204,7 @@ template <typename T>
 static void dx_t(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t ldd, const void* B, int64_t ldb,
                  void* C, int64_t ldc, const float* rowscale, int64_t scale_cols) {
     dim3 grid((unsigned)((Nc + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
-    k_gemm<T, T, 2><<<grid, 256, 0, c.stream>>>(M, Nc, K, (const T*)D, K, ldd, nullptr, 0, (const T*)B, ldb, (T*)C, ldc,
+    pdl_launch(c.stream, k_gemm<T, T, 2>, grid, 256, 0, M, Nc, K, (const T*)D, K, ldd, nullptr, 0, (const T*)B, ldb, (T*)C, ldc,
                                                 false, rowscale, scale_cols, 0);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();

@@ -167,6 +167,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // PDL: barrier init, descriptor prefetch and the TMEM allocation above overlap the previous kernel's tail; no
+    // global memory is touched before this point
+    pdl_grid_sync();
     const uint32_t tmem = *tmem_slot;
     const uint32_t b_bytes = (uint32_t)args.BN * TC_ROW_BYTES;
 
@@ -415,7 +418,7 @@ static void launch_tc_t(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, co
                                       Cfg::SMEM));
         configured = true;
     }
-    k_gemm_tc<A_MN, B_MN, F32><<<grid, Cfg::THREADS, Cfg::SMEM, c.stream>>>(a0, a1, b, b1, args);
+    pdl_launch(c.stream, k_gemm_tc<A_MN, B_MN, F32>, grid, Cfg::THREADS, Cfg::SMEM, a0, a1, b, b1, args);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -469,6 +472,7 @@ void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64
 // dst row pitch ldd >= rows (padded to 4 floats for TMA); 32 x 32 tiles through shared memory
 __global__ void k_transpose32(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
                               float* __restrict__ dst, int64_t ldd) {
+    pdl_grid_sync();
     __shared__ float t[32][33];
     const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
     for (int i = threadIdx.y; i < 32; i += 8) {
@@ -484,7 +488,7 @@ __global__ void k_transpose32(const float* __restrict__ src, int64_t rows, int64
 
 static void transpose32(Ctx& c, const void* src, int64_t rows, int64_t cols, int64_t lds, float* dst, int64_t ldd) {
     const dim3 grid((unsigned)cdiv(ldd, 32), (unsigned)cdiv(cols, 32));
-    k_transpose32<<<grid, dim3(32, 8), 0, c.stream>>>(static_cast<const float*>(src), rows, cols, lds, dst, ldd);
+    pdl_launch(c.stream, k_transpose32, grid, dim3(32, 8), 0, static_cast<const float*>(src), rows, cols, lds, dst, ldd);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -579,7 +583,7 @@ void gemm_wgrad2_tc(Ctx& c, int64_t Mn0, int64_t Mn1, int64_t K, int64_t N, cons
     const int64_t Kp = cdiv(K, TC_BM) * TC_BM, M2 = Kp + K;
     const int64_t Mn = std::max(Mn0, Mn1);
     if (Mn <= 0) {
-        BNS_CUDA(cudaMemset2DAsync(Wg, ldw * sizeof(float), 0, N * sizeof(float), 2 * K, c.stream));
+        BNS_CUDA_HOLD(cudaMemset2DAsync(Wg, ldw * sizeof(float), 0, N * sizeof(float), 2 * K, c.stream));
         return;
     }
     TcArgs a{};

@@ -125,6 +125,7 @@ struct SampleArgs {
 };
 
 __global__ void __launch_bounds__(kTile) k_sample_fused(const SampleArgs a) {
+    pdl_grid_sync();
     __shared__ int64_t s_tile, s_excl;
     __shared__ int s_warp[32], s_total;
     const int64_t t = next_tile(a.ctr, a.ntiles, &s_tile);
@@ -179,6 +180,7 @@ struct InduceArgs {
 // words, which L1 serves one sector per lane (the pass measured 48 us L1-bound at m = 8).
 template <bool SMEM>
 __global__ void __launch_bounds__(kEdgeThreads) k_induce_count(const InduceArgs a) {
+    pdl_grid_sync();
     __shared__ int s_warp[32], s_total;
     __shared__ bool s_last;
     extern __shared__ uint32_t s_bk[];
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_induce_count(const InduceArgs 
 // order-preserving stores (remapped: halo column -> n_in + slot); then the induced row pointers of the rows whose first
 // static arc lies in this chunk (kept arcs before that arc, from the setup tile table and pass 1's words / prefixes)
 __global__ void __launch_bounds__(256) k_induce_scatter(const InduceArgs a) {
+    pdl_grid_sync();
     const int lane = threadIdx.x & 31;
     const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nchunks = (a.nnz + 1023) >> 10;
@@ -296,6 +299,7 @@ struct SegArgs {
 };
 
 __global__ void __launch_bounds__(kTile) k_segs_fused(const SegArgs a) {
+    pdl_grid_sync();
     __shared__ int64_t s_tile, s_excl;
     __shared__ int s_warp[32], s_total;
     const bool fwd = blockIdx.x < a.ntiles_f;
@@ -352,7 +356,7 @@ void launch_sample_fused(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     const int64_t n = c.n_cand;
     const int64_t nt = (n + kTile - 1) / kTile;
     if (nt == 0) {   // nothing to draw: every offset 0, split counters cleared
-        BNS_CUDA(cudaMemsetAsync(c.d_seg_pos, 0, (2 * m + 1 + 8) * sizeof(int64_t), c.stream));
+        BNS_CUDA_HOLD(cudaMemsetAsync(c.d_seg_pos, 0, (2 * m + 1 + 8) * sizeof(int64_t), c.stream));
         return;
     }
     SampleArgs a{};
@@ -364,7 +368,7 @@ void launch_sample_fused(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     a.seg_pos = c.d_seg_pos;
     a.zero = tot + 3; a.nzero = 2;
     a.state = c.d_lb_state; a.ctr = c.d_lb_ctr; a.gen = ++c.lb_gen; a.ntiles = nt;
-    k_sample_fused<<<(unsigned)nt, kTile, 0, c.stream>>>(a);
+    pdl_launch(c.stream, k_sample_fused, (unsigned)nt, kTile, 0, a);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -375,8 +379,8 @@ void launch_induce_fused(Ctx& c) {
     const int64_t nnz = c.nnz_i;
     const int64_t nt = (nnz + kInduceTileArcs - 1) / kInduceTileArcs;
     if (nt == 0) {
-        BNS_CUDA(cudaMemsetAsync(c.d_ind_ptr, 0, (c.plan.n_in + 1) * sizeof(int64_t), c.stream));
-        BNS_CUDA(cudaMemsetAsync(tot, 0, sizeof(int64_t), c.stream));
+        BNS_CUDA_HOLD(cudaMemsetAsync(c.d_ind_ptr, 0, (c.plan.n_in + 1) * sizeof(int64_t), c.stream));
+        BNS_CUDA_HOLD(cudaMemsetAsync(tot, 0, sizeof(int64_t), c.stream));
         return;
     }
     InduceArgs a{};
@@ -393,12 +397,12 @@ void launch_induce_fused(Ctx& c) {
                                           (int)kSmemMax));
             cfg = true;
         }
-        k_induce_count<true><<<(unsigned)nt, kEdgeThreads, (size_t)(a.nbw * 4), c.stream>>>(a);
+        pdl_launch(c.stream, k_induce_count<true>, (unsigned)nt, kEdgeThreads, (size_t)(a.nbw * 4), a);
     } else {
-        k_induce_count<false><<<(unsigned)nt, kEdgeThreads, 0, c.stream>>>(a);
+        pdl_launch(c.stream, k_induce_count<false>, (unsigned)nt, kEdgeThreads, 0, a);
     }
     const int64_t nchunks = (nnz + 1023) / 1024;
-    k_induce_scatter<<<(unsigned)((nchunks + 7) / 8), 256, 0, c.stream>>>(a);
+    pdl_launch(c.stream, k_induce_scatter, (unsigned)((nchunks + 7) / 8), 256, 0, a);
     c.kernels += 2;
     BNS_CHECK_LAUNCH();
 }
@@ -416,11 +420,11 @@ void launch_segments_fused(Ctx& c, bool fwd) {
     a.tot = tot; a.seg_long = c.seg_long;
     a.state_f = c.d_lb_state + c.lb_off_segf; a.state_b = c.d_lb_state + c.lb_off_segb;
     a.ctr_f = c.d_lb_ctr + 2; a.ctr_b = c.d_lb_ctr + 3; a.gen = ++c.lb_gen;
-    if (a.ntiles_b == 0) BNS_CUDA(cudaMemsetAsync(tot + 2, 0, sizeof(int64_t), c.stream));
-    if (fwd && a.ntiles_f == 0) BNS_CUDA(cudaMemsetAsync(tot + 1, 0, sizeof(int64_t), c.stream));
+    if (a.ntiles_b == 0) BNS_CUDA_HOLD(cudaMemsetAsync(tot + 2, 0, sizeof(int64_t), c.stream));
+    if (fwd && a.ntiles_f == 0) BNS_CUDA_HOLD(cudaMemsetAsync(tot + 1, 0, sizeof(int64_t), c.stream));
     const int64_t grid = a.ntiles_f + a.ntiles_b;
     if (grid == 0) return;
-    k_segs_fused<<<(unsigned)grid, kTile, 0, c.stream>>>(a);
+    pdl_launch(c.stream, k_segs_fused, (unsigned)grid, kTile, 0, a);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }

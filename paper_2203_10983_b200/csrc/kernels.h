@@ -44,7 +44,9 @@ struct SpmmArgs {
     int sc = -1;                          // per-edge column scale override (-1: by mode; 2: cscale[col])
     int relu = 0;                         // SAGE_FWD_TF: ReLU in the epilogue
     int out_f32 = 0;                      // SAGE_FWD_TF / GAT_FWD: fp32 output (logits) instead of the storage type
-    unsigned long long* work = nullptr;   // dynamic segment scheduling: next unclaimed segment (zeroed per launch)
+    unsigned long long* work = nullptr;   // dynamic segment scheduling: [next unclaimed segment, warps done]; the
+                                          // last warp to finish resets both (no memset between launches)
+    int32_t* arrive = nullptr;            // non-null: split rows are summed by the warp finishing their last segment
     int chunk = 1;                        // segments per claim
     // f4 / R45 GAT: per-node attention scores and softmax statistics (fp32), attention vectors a_l / a_r (dout),
     // del / der (backward)
@@ -105,10 +107,11 @@ void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, c
 void launch_scatter_prep(Ctx& c, int64_t n_sent);
 void launch_scatter_rows(Ctx& c, void* dst, int64_t ld, const void* src, int32_t d);
 // rs / dps (optional, R42): also write dps = dPre * rs[row] (the transform-first SpMM^T source)
+// ldp: row pitch of dpre_t (-1: ld); nzero: rows after the inner rows of dpre_t set to zero (R42 halo rows)
 void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t,
-                 const float* rs = nullptr, void* dps = nullptr);
+                 const float* rs = nullptr, void* dps = nullptr, int64_t ldp = -1, int64_t nzero = 0);
 void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
-                void* dps);
+                void* dps, int64_t ldp = -1, int64_t nzero = 0);
 void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre,
                       const float* rs = nullptr, void* dps = nullptr);
 void launch_wpack_all(Ctx& c, float* const* W);

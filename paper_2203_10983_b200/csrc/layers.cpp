@@ -319,18 +319,24 @@ void backward_layer_tf(Ctx& c, const EpochView& v, int l, void* Hin) {
         float* g = c.d_gflat + c.goff[l - 1];
         auto wgrad = c.use_tc ? gemm_wgrad_tc : gemm_wgrad;
         auto dxg = c.use_tc ? gemm_dx_tc : gemm_dx;
+        // dPre: in the dPre half of d_tfy already (written there by the loss), else in d_dpre
+        const bool in_tfy = tf_dpre_in_tfy(c, l);
+        const void* dpre = in_tfy ? static_cast<const void*>(static_cast<char*>(c.d_tfy) + dout * ts) : c.d_dpre;
+        const int64_t ldp = in_tfy ? 2 * dout : dout;
         if (c.use_tc) {   // dW_top (every stacked row) and dW_bot (inner rows) in one launch + one reduce
-            gemm_wgrad2_tc(c, rows, n_in, din, dout, Hin, Hin, din, c.d_tfy, 2 * dout, c.d_dpre, dout, g, dout);
+            gemm_wgrad2_tc(c, rows, n_in, din, dout, Hin, Hin, din, c.d_tfy, 2 * dout, dpre, ldp, g, dout);
         } else {
             wgrad(c, rows, din, dout, Hin, din, c.d_tfy, 2 * dout, g, dout);
-            wgrad(c, n_in, din, dout, Hin, din, c.d_dpre, dout, g + din * dout, dout);
+            wgrad(c, n_in, din, dout, Hin, din, dpre, ldp, g + din * dout, dout);
         }
         if (l > 1) {   // dX = [dY | dPre] [W_top | W_bot]^T over every stacked row, one GEMM: halo rows have no dPre
-            BNS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(c.d_tfy) + dout * ts, 2 * dout * ts, c.d_dpre,
-                                       dout * ts, dout * ts, n_in, cudaMemcpyDeviceToDevice, c.stream));
-            if (c.n_halo > 0)
-                BNS_CUDA(cudaMemset2DAsync(static_cast<char*>(c.d_tfy) + (n_in * 2 + 1) * dout * ts, 2 * dout * ts, 0,
-                                           dout * ts, c.n_halo, c.stream));
+            if (!in_tfy) {
+                BNS_CUDA_HOLD(cudaMemcpy2DAsync(static_cast<char*>(c.d_tfy) + dout * ts, 2 * dout * ts, c.d_dpre,
+                                           dout * ts, dout * ts, n_in, cudaMemcpyDeviceToDevice, c.stream));
+                if (c.n_halo > 0)
+                    BNS_CUDA_HOLD(cudaMemset2DAsync(static_cast<char*>(c.d_tfy) + (n_in * 2 + 1) * dout * ts, 2 * dout * ts,
+                                               0, dout * ts, c.n_halo, c.stream));
+            }
             dxg(c, rows, din, 2 * dout, c.d_tfy, 2 * dout, c.Wcat[l - 1], 2 * dout, c.d_dx, din, nullptr, 0);
         }
     }

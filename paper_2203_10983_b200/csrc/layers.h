@@ -32,6 +32,12 @@ struct EpochView {
     float inv_p;
 };
 
+// R42 layer l = L with a dX (L > 1): the loss writes dPre into the dPre half of c.d_tfy (pitch 2 d_out, halo rows
+// zeroed), the [dY | dPre] operand of the one dX GEMM -- no copy between the loss and the backward
+inline bool tf_dpre_in_tfy(const Ctx& c, int l) {
+    return l == c.L && l > 1 && c.layer == BNS_LAYER_SAGE_MEAN && ((c.tf_mask >> (l - 1)) & 1u);
+}
+
 // forward of layer l (1-based) from its (dropped-out) input Hin [inner ; halo]: H[l] (hidden) or the logits
 void forward_layer_std(Ctx& c, const EpochView& v, int l, void* Hin);
 void forward_layer_tf(Ctx& c, const EpochView& v, int l, void* Hin);

@@ -6,6 +6,7 @@
 //   a14 update      W <- W - lr g (Alg.1 l.14), g copied to the caller
 //   weight pack, local all-reduce sum (rank order), GCN column scales.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.h"
 #include "dev.cuh"
@@ -13,10 +14,26 @@
 
 namespace bns {
 
+namespace {
+thread_local bool t_pdl_hold = false;
+}
+void pdl_hold() { t_pdl_hold = true; }
+bool pdl_take_hold() {
+    const bool h = t_pdl_hold;
+    t_pdl_hold = false;
+    return h;
+}
+
+bool pdl_enabled() {
+    static const bool v = [] { const char* e = std::getenv("BNS_PDL"); return !(e && e[0] == '0'); }();
+    return v;
+}
+
 // one warp per row, 16-byte vectors
 template <typename T>
 __global__ void k_pack(const T* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ idx, int64_t n,
                        T* __restrict__ dst, int32_t d) {
+    pdl_grid_sync();
     using R = typename Vec<T>::raw;
     const int nvec = d / Vec<T>::N;
     const int lane = threadIdx.x & 31;
@@ -33,9 +50,9 @@ void launch_pack_rows(Ctx& c, const void* src, int64_t ld_src, const int32_t* id
     if (n <= 0) return;
     unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16);
     if (c.prec == BNS_BF16)
-        k_pack<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)src, ld_src, idx, n, (__nv_bfloat16*)dst, d);
+        pdl_launch(c.stream, k_pack<__nv_bfloat16>, grid, 256, 0, (const __nv_bfloat16*)src, ld_src, idx, n, (__nv_bfloat16*)dst, d);
     else
-        k_pack<float><<<grid, 256, 0, c.stream>>>((const float*)src, ld_src, idx, n, (float*)dst, d);
+        pdl_launch(c.stream, k_pack<float>, grid, 256, 0, (const float*)src, ld_src, idx, n, (float*)dst, d);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -43,6 +60,7 @@ void launch_pack_rows(Ctx& c, const void* src, int64_t ld_src, const int32_t* id
 template <typename T>
 __global__ void k_scatter_add(T* __restrict__ dst, int64_t ld_dst, const int32_t* __restrict__ idx,
                               const T* __restrict__ src, int64_t n, int32_t d) {
+    pdl_grid_sync();
     using V = Vec<T>;
     using R = typename V::raw;
     constexpr int VN = V::N;
@@ -68,10 +86,10 @@ void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, c
     if (n <= 0) return;
     unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16);
     if (c.prec == BNS_BF16)
-        k_scatter_add<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((__nv_bfloat16*)dst, ld_dst, idx,
+        pdl_launch(c.stream, k_scatter_add<__nv_bfloat16>, grid, 256, 0, (__nv_bfloat16*)dst, ld_dst, idx,
                                                                  (const __nv_bfloat16*)src, n, d);
     else
-        k_scatter_add<float><<<grid, 256, 0, c.stream>>>((float*)dst, ld_dst, idx, (const float*)src, n, d);
+        pdl_launch(c.stream, k_scatter_add<float>, grid, 256, 0, (float*)dst, ld_dst, idx, (const float*)src, n, d);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -82,6 +100,7 @@ void launch_scatter_add(Ctx& c, void* dst, int64_t ld_dst, const int32_t* idx, c
 // peer in ascending order (R25, R19).
 __global__ void k_scatter_prep(const int32_t* __restrict__ S_local, int64_t n_sent, const int64_t* __restrict__ seg_pos,
                                int m, uint32_t* __restrict__ mask, int32_t* __restrict__ pos) {
+    pdl_grid_sync();
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_sent) return;
     const int64_t base = seg_pos[m];
@@ -96,6 +115,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_scatter_rows(T* __restrict__ dst, int64_t ld, const T* __restrict__ src,
                                                       int32_t d, const uint32_t* __restrict__ mask,
                                                       const int32_t* __restrict__ pos, int m, int64_t n_rows) {
+    pdl_grid_sync();
     using V = Vec<T>;
     using R = typename V::raw;
     constexpr int VN = V::N;
@@ -127,9 +147,9 @@ __global__ void __launch_bounds__(256) k_scatter_rows(T* __restrict__ dst, int64
 
 void launch_scatter_prep(Ctx& c, int64_t n_sent) {
     const int m = c.cfg.world;
-    BNS_CUDA(cudaMemsetAsync(c.d_scat_mask, 0, (c.plan.n_in + 1) * sizeof(uint32_t), c.stream));
+    BNS_CUDA_HOLD(cudaMemsetAsync(c.d_scat_mask, 0, (c.plan.n_in + 1) * sizeof(uint32_t), c.stream));
     if (n_sent <= 0) return;
-    k_scatter_prep<<<(unsigned)((n_sent + 255) / 256), 256, 0, c.stream>>>(c.d_cand_out + c.n_halo, n_sent,
+    pdl_launch(c.stream, k_scatter_prep, (unsigned)((n_sent + 255) / 256), 256, 0, c.d_cand_out + c.n_halo, n_sent,
                                                                            c.d_seg_pos, m, c.d_scat_mask,
                                                                            c.d_scat_pos);
     c.kernels += 1;
@@ -141,10 +161,10 @@ void launch_scatter_rows(Ctx& c, void* dst, int64_t ld, const void* src, int32_t
     if (n <= 0 || c.n_sent <= 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16);
     if (c.prec == BNS_BF16)
-        k_scatter_rows<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((__nv_bfloat16*)dst, ld, (const __nv_bfloat16*)src,
+        pdl_launch(c.stream, k_scatter_rows<__nv_bfloat16>, grid, 256, 0, (__nv_bfloat16*)dst, ld, (const __nv_bfloat16*)src,
                                                                   d, c.d_scat_mask, c.d_scat_pos, c.cfg.world, n);
     else
-        k_scatter_rows<float><<<grid, 256, 0, c.stream>>>((float*)dst, ld, (const float*)src, d, c.d_scat_mask,
+        pdl_launch(c.stream, k_scatter_rows<float>, grid, 256, 0, (float*)dst, ld, (const float*)src, d, c.d_scat_mask,
                                                           c.d_scat_pos, c.cfg.world, n);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -178,12 +198,22 @@ __device__ __forceinline__ void last_block_final(const double* part, int nv, dou
     if (threadIdx.x == 0) *ctr = 0u;
 }
 
+// rows [r0, r0 + nrows) of a dPre buffer (pitch ldp, ld columns) set to zero: the halo rows of the transform-first
+// [dY | dPre] operand (R42: halo rows have no dPre)
+template <typename T>
+__device__ __forceinline__ void zero_rows(T* dpre, int64_t ldp, int64_t r0, int64_t nrows, int64_t ld) {
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows * ld; i += nt)
+        dpre[(r0 + i / ld) * ldp + i % ld] = from_f<T>(0.f);
+}
+
 template <typename T, int NPL>
 __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, int64_t ld, int64_t n, int32_t C,
                                               const int32_t* __restrict__ labels, double inv_ntr,
-                                              float* __restrict__ dlog, T* __restrict__ dpre,
+                                              float* __restrict__ dlog, T* __restrict__ dpre, int64_t ldp, int64_t nzero,
                                               double* __restrict__ part, const float* __restrict__ rs,
                                               T* __restrict__ dps, double* __restrict__ scal, unsigned* ctr) {
+    pdl_grid_sync();
     __shared__ double s_loss[8];
     __shared__ double s_cor[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -194,7 +224,7 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
         const float* x = logits + r * ld;
         const int y = labels[r];
         float* g = dlog ? dlog + r * ld : nullptr;   // fp32 dLogits only for BNS_Q_DH (BNS_RETAIN_GRADS)
-        T* gp = dpre + r * ld;
+        T* gp = dpre + r * ldp;
         if (y < 0) {
             for (int c = lane; c < ld; c += 32) {
                 if (g) g[c] = 0.f;
@@ -244,6 +274,7 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
             cor += (arg == y) ? 1.0 : 0.0;
         }
     }
+    zero_rows(dpre, ldp, n, nzero, ld);
     if (lane == 0) { s_loss[w] = loss; s_cor[w] = cor; }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -260,9 +291,10 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
 template <typename T, int NPL>
 __global__ void __launch_bounds__(256) k_bce(const float* __restrict__ logits, int64_t ld, int64_t n, int32_t C,
                                              const int32_t* __restrict__ labels, const uint8_t* __restrict__ tgt,
-                                             double inv, float* __restrict__ dlog, T* __restrict__ dpre,
+                                             double inv, float* __restrict__ dlog, T* __restrict__ dpre, int64_t ldp, int64_t nzero,
                                              double* __restrict__ part, const float* __restrict__ rs,
                                              T* __restrict__ dps, double* __restrict__ scal, unsigned* ctr) {
+    pdl_grid_sync();
     __shared__ double s_v[4][8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t warp = (int64_t)blockIdx.x * 8 + w;
@@ -290,7 +322,7 @@ __global__ void __launch_bounds__(256) k_bce(const float* __restrict__ logits, i
             }
             if (dlog) dlog[r * ld + c] = v;
             const T q = from_f<T>(v);
-            dpre[r * ld + c] = q;
+            dpre[r * ldp + c] = q;
             if (dps) dps[r * ld + c] = from_f<T>(to_f(q) * rsr);
         }
         if (!train) continue;
@@ -306,6 +338,7 @@ __global__ void __launch_bounds__(256) k_bce(const float* __restrict__ logits, i
         fp += nfp;
         fn += nfn;
     }
+    zero_rows(dpre, ldp, n, nzero, ld);
     if (lane == 0) { s_v[0][w] = loss; s_v[1][w] = tp; s_v[2][w] = fp; s_v[3][w] = fn; }
     __syncthreads();
     if (threadIdx.x < 4) {
@@ -317,13 +350,14 @@ __global__ void __launch_bounds__(256) k_bce(const float* __restrict__ logits, i
 }
 
 void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
-                void* dps) {
+                void* dps, int64_t ldp, int64_t nzero) {
+    if (ldp < 0) ldp = ld;
     const double inv = c.n_train_global > 0 ? 1.0 / ((double)c.n_train_global * C) : 0.0;
     const int64_t n = c.plan.n_in;
     const int npl = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
 #define BNS_BCE(T, NPL)                                                                                              \
-    k_bce<T, NPL><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, n, C, c.d_labels, c.d_targets, inv, dlogits,        \
-                                                     (T*)dpre_t, c.d_lpart, rs, (T*)dps, c.d_scal, c.d_lb_ctr + 8)
+    pdl_launch(c.stream, k_bce<T, NPL>, kXentBlocks, 256, 0, logits, ld, n, C, c.d_labels, c.d_targets, inv, dlogits,        \
+                                                     (T*)dpre_t, ldp, nzero, c.d_lpart, rs, (T*)dps, c.d_scal, c.d_lb_ctr + 8)
     if (c.prec == BNS_BF16) {
         if (npl == 1) BNS_BCE(__nv_bfloat16, 1); else if (npl == 2) BNS_BCE(__nv_bfloat16, 2);
         else if (npl == 4) BNS_BCE(__nv_bfloat16, 4); else BNS_BCE(__nv_bfloat16, 8);
@@ -337,13 +371,14 @@ void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogi
 }
 
 void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
-                 void* dps) {
+                 void* dps, int64_t ldp, int64_t nzero) {
+    if (ldp < 0) ldp = ld;
     const double inv = c.n_train_global > 0 ? 1.0 / (double)c.n_train_global : 0.0;
     const int64_t n = c.plan.n_in;
     const int npl = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : ld <= 256 ? 8 : 0;
     if (npl == 0) throw Error(BNS_ERR_INVALID, "more than 256 classes are not supported by k_xent");
 #define BNS_XENT(T, NPL)                                                                                          \
-    k_xent<T, NPL><<<kXentBlocks, 256, 0, c.stream>>>(logits, ld, n, C, c.d_labels, inv, dlogits, (T*)dpre_t,   \
+    pdl_launch(c.stream, k_xent<T, NPL>, kXentBlocks, 256, 0, logits, ld, n, C, c.d_labels, inv, dlogits, (T*)dpre_t, ldp, nzero,   \
                                                       c.d_lpart, rs, (T*)dps, c.d_scal, c.d_lb_ctr + 8)
     if (c.prec == BNS_BF16) {
         if (npl == 1) BNS_XENT(__nv_bfloat16, 1); else if (npl == 2) BNS_XENT(__nv_bfloat16, 2);
@@ -361,6 +396,7 @@ void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlog
 template <typename T>
 __global__ void k_relu_mask(const T* __restrict__ dh, const T* __restrict__ h, int64_t ld, int64_t n,
                             T* __restrict__ dpre, const float* __restrict__ rs, T* __restrict__ dps) {
+    pdl_grid_sync();
     using R = typename Vec<T>::raw;
     constexpr int VN = Vec<T>::N;
     const int64_t nv = n / VN;
@@ -391,10 +427,10 @@ void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t
     if (n <= 0) return;
     unsigned grid = (unsigned)std::min<int64_t>((n / 4 + 255) / 256, 148 * 16);
     if (c.prec == BNS_BF16)
-        k_relu_mask<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)dh, (const __nv_bfloat16*)h, ld,
+        pdl_launch(c.stream, k_relu_mask<__nv_bfloat16>, grid, 256, 0, (const __nv_bfloat16*)dh, (const __nv_bfloat16*)h, ld,
                                                                n, (__nv_bfloat16*)dpre, rs, (__nv_bfloat16*)dps);
     else
-        k_relu_mask<float><<<grid, 256, 0, c.stream>>>((const float*)dh, (const float*)h, ld, n, (float*)dpre, rs,
+        pdl_launch(c.stream, k_relu_mask<float>, grid, 256, 0, (const float*)dh, (const float*)h, ld, n, (float*)dpre, rs,
                                                        (float*)dps);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -436,6 +472,7 @@ struct WDesc {
 
 template <typename T>
 __global__ void k_wpack_all(const WDesc d) {
+    pdl_grid_sync();
     const int y = blockIdx.y;
     const int l = y % d.L;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -516,8 +553,8 @@ void launch_wpack_all(Ctx& c, float* const* W) {
     }
     // y: [0, L) padded W (+ storage copy), [L, 2L) W^T for the tensor cores, [2L, 3L) transform-first packs (R42)
     const dim3 grid((unsigned)((mx + 255) / 256), (unsigned)(c.L * (c.tf_mask ? 3 : d.tc ? 2 : 1)));
-    if (c.prec == BNS_BF16) k_wpack_all<__nv_bfloat16><<<grid, 256, 0, c.stream>>>(d);
-    else k_wpack_all<float><<<grid, 256, 0, c.stream>>>(d);
+    if (c.prec == BNS_BF16) pdl_launch(c.stream, k_wpack_all<__nv_bfloat16>, grid, 256, 0, d);
+    else pdl_launch(c.stream, k_wpack_all<float>, grid, 256, 0, d);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -525,6 +562,7 @@ void launch_wpack_all(Ctx& c, float* const* W) {
 // a14 W <- W - lr g for every layer (g copied to the caller); skipped when the all-reduced loss is not finite
 __global__ void k_sgd_all(const WDesc d, float lr, const double* __restrict__ scal, int32_t* __restrict__ nonfinite,
                           const volatile int* abort) {
+    pdl_grid_sync();
     const int l = blockIdx.y;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t rows_l = logical_rows(d.kind, d.din[l]), dout = d.dout[l];
@@ -543,13 +581,14 @@ void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr) {
     const WDesc d = make_desc(c, W, G);
     int64_t mx = 0;
     for (int l = 0; l < c.L; ++l) mx = std::max(mx, logical_rows(d.kind, d.din[l]) * d.dout[l]);
-    k_sgd_all<<<dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, c.stream>>>(d, lr, c.d_scal, c.d_nonfinite,
+    pdl_launch(c.stream, k_sgd_all, dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, d, lr, c.d_scal, c.d_nonfinite,
                                                                                      c.d_abort);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 
 __global__ void k_sum_ptrs(const float* const* __restrict__ p, int np, float* __restrict__ out, int64_t n) {
+    pdl_grid_sync();
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     float s = 0.f;
@@ -557,6 +596,7 @@ __global__ void k_sum_ptrs(const float* const* __restrict__ p, int np, float* __
     out[t] = s;
 }
 __global__ void k_sum_ptrs_d(const double* const* __restrict__ p, int np, double* __restrict__ out, int64_t n) {
+    pdl_grid_sync();
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     double s = 0.0;
@@ -565,13 +605,13 @@ __global__ void k_sum_ptrs_d(const double* const* __restrict__ p, int np, double
 }
 void launch_sum_ptrs(Ctx& c, const float* const* d_ptrs, int nptr, float* out, int64_t n) {
     if (n <= 0) return;
-    k_sum_ptrs<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(d_ptrs, nptr, out, n);
+    pdl_launch(c.stream, k_sum_ptrs, (unsigned)((n + 255) / 256), 256, 0, d_ptrs, nptr, out, n);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 void launch_sum_ptrs_d(Ctx& c, const double* const* d_ptrs, int nptr, double* out, int64_t n) {
     if (n <= 0) return;
-    k_sum_ptrs_d<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(d_ptrs, nptr, out, n);
+    pdl_launch(c.stream, k_sum_ptrs_d, (unsigned)((n + 255) / 256), 256, 0, d_ptrs, nptr, out, n);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -580,6 +620,7 @@ void launch_sum_ptrs_d(Ctx& c, const double* const* d_ptrs, int nptr, double* ou
 __global__ void k_gcn_cscale(const float* __restrict__ rs_in, int64_t n_in, const float* __restrict__ rs_bd,
                              const int32_t* __restrict__ U_b, const int64_t* __restrict__ seg_pos, int m, float inv_p,
                              int64_t cap, float* __restrict__ cs) {
+    pdl_grid_sync();
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < n_in) { cs[t] = rs_in[t]; return; }
     int64_t s = t - n_in;
@@ -590,7 +631,7 @@ __global__ void k_gcn_cscale(const float* __restrict__ rs_in, int64_t n_in, cons
 void launch_gcn_cscale(Ctx& c) {
     const int64_t n = c.plan.n_in + c.halo_cap;
     if (n <= 0) return;
-    k_gcn_cscale<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.d_rs_in, c.plan.n_in, c.d_rs_bd, c.d_cand_out,
+    pdl_launch(c.stream, k_gcn_cscale, (unsigned)((n + 255) / 256), 256, 0, c.d_rs_in, c.plan.n_in, c.d_rs_bd, c.d_cand_out,
                                                                     c.d_seg_pos, c.cfg.world, c.inv_p, c.halo_cap,
                                                                     c.d_cscale);
     c.kernels += 1;
@@ -600,6 +641,7 @@ void launch_gcn_cscale(Ctx& c) {
 template <typename T>
 __global__ void k_to_storage(const float* __restrict__ src, int64_t rows, int32_t dlog, int64_t ld_src,
                              T* __restrict__ dst, int64_t ld_dst) {
+    pdl_grid_sync();
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= rows * ld_dst) return;
     int64_t r = t / ld_dst, k = t % ld_dst;
@@ -610,10 +652,10 @@ void launch_to_storage(Ctx& c, const float* src, int64_t rows, int32_t dlog, int
     const int64_t n = rows * ld_dst;
     if (n <= 0) return;
     if (c.prec == BNS_BF16)
-        k_to_storage<__nv_bfloat16><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(src, rows, dlog, ld_src,
+        pdl_launch(c.stream, k_to_storage<__nv_bfloat16>, (unsigned)((n + 255) / 256), 256, 0, src, rows, dlog, ld_src,
                                                                                       (__nv_bfloat16*)dst, ld_dst);
     else
-        k_to_storage<float><<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(src, rows, dlog, ld_src, (float*)dst,
+        pdl_launch(c.stream, k_to_storage<float>, (unsigned)((n + 255) / 256), 256, 0, src, rows, dlog, ld_src, (float*)dst,
                                                                               ld_dst);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -632,6 +674,7 @@ template <typename T>
 __global__ void k_dropout(const T* __restrict__ src, T* __restrict__ dst, int64_t rows, int64_t ld,
                           const int32_t* __restrict__ gid, uint32_t layer, uint32_t e_lo, uint32_t k0, uint32_t k1,
                           uint64_t thr, float scale) {
+    pdl_grid_sync();
     const int64_t nq = (ld + 3) / 4;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= rows * nq) return;
@@ -655,11 +698,11 @@ void launch_dropout(Ctx& c, const void* src, void* dst, int64_t rows, int64_t ld
     const int64_t n = rows * ((ld + 3) / 4);
     const unsigned grid = (unsigned)((n + 255) / 256);
     if (c.prec == BNS_BF16)
-        k_dropout<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, rows, ld,
+        pdl_launch(c.stream, k_dropout<__nv_bfloat16>, grid, 256, 0, (const __nv_bfloat16*)src, (__nv_bfloat16*)dst, rows, ld,
                                                              c.d_rowgid, (uint32_t)layer, (uint32_t)c.epoch_id, k0, k1,
                                                              thr, scale);
     else
-        k_dropout<float><<<grid, 256, 0, c.stream>>>((const float*)src, (float*)dst, rows, ld, c.d_rowgid,
+        pdl_launch(c.stream, k_dropout<float>, grid, 256, 0, (const float*)src, (float*)dst, rows, ld, c.d_rowgid,
                                                      (uint32_t)layer, (uint32_t)c.epoch_id, k0, k1, thr, scale);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -668,13 +711,14 @@ void launch_dropout(Ctx& c, const void* src, void* dst, int64_t rows, int64_t ld
 // global ids of the halo rows of this epoch: rowgid[n_in + s] = gid of boundary node U_b[s]
 __global__ void k_halo_gid(const int32_t* __restrict__ cand_gid, const int32_t* __restrict__ U_b, int64_t n_halo,
                            int64_t n_in, int32_t* __restrict__ rowgid) {
+    pdl_grid_sync();
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s < n_halo) rowgid[n_in + s] = cand_gid[U_b[s]];
 }
 
 void launch_halo_gid(Ctx& c) {
     if (c.n_halo <= 0) return;
-    k_halo_gid<<<(unsigned)((c.n_halo + 255) / 256), 256, 0, c.stream>>>(c.d_cand_gid, c.d_cand_out, c.n_halo,
+    pdl_launch(c.stream, k_halo_gid, (unsigned)((c.n_halo + 255) / 256), 256, 0, c.d_cand_gid, c.d_cand_out, c.n_halo,
                                                                          c.plan.n_in, c.d_rowgid);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -691,6 +735,7 @@ struct AdamArgs {
 
 __global__ void k_adam_all(const WDesc d, const AdamArgs a, const double* __restrict__ scal,
                            int32_t* __restrict__ nonfinite, const volatile int* abort) {
+    pdl_grid_sync();
     const int l = blockIdx.y;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t rows_l = logical_rows(d.kind, d.din[l]), dout = d.dout[l];
@@ -730,7 +775,7 @@ void launch_adam(Ctx& c, float* const* W, float* const* G, float lr) {
     a.eps = (float)c.eps;
     a.c1 = (float)(1.0 - std::pow(c.beta1, (double)c.adam_t));
     a.c2 = (float)(1.0 - std::pow(c.beta2, (double)c.adam_t));
-    k_adam_all<<<dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, c.stream>>>(d, a, c.d_scal, c.d_nonfinite,
+    pdl_launch(c.stream, k_adam_all, dim3((unsigned)((mx + 255) / 256), (unsigned)c.L), 256, 0, d, a, c.d_scal, c.d_nonfinite,
                                                                                       c.d_abort);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();

@@ -38,6 +38,7 @@ constexpr uint64_t kBarrierTimeoutNs = 20ull * 1000 * 1000 * 1000;
 __global__ void k_peer_barrier(uint64_t* const* __restrict__ flags, int me, int m, uint64_t val, int* err,
                                const int64_t* const* __restrict__ pseg, const int64_t* __restrict__ pnin,
                                int64_t* __restrict__ delta) {
+    pdl_grid_sync();
     const int j = threadIdx.x;
     if (j >= m || j == me) return;
     if (*(volatile int*)err) return;   // an earlier barrier timed out: the epoch is already failed, do not wait again
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(256) k_halo_pull(T* __restrict__ dst, int64_t 
                                                    int64_t n, const int32_t* __restrict__ owner_of_b,
                                                    const int32_t* __restrict__ row_of_b, T* const* __restrict__ peerH,
                                                    int32_t d) {
+    pdl_grid_sync();
     using R = typename Vec<T>::raw;
     const int nvec = d / Vec<T>::N;
     const int lane = threadIdx.x & 31;
@@ -91,6 +93,7 @@ __global__ void __launch_bounds__(256) k_scatter_peer(T* __restrict__ dst, int64
                                                       const uint32_t* __restrict__ mask, const int32_t* __restrict__ pos,
                                                       int m, int64_t n_rows, T* const* __restrict__ peerdx,
                                                       const int64_t* __restrict__ delta) {
+    pdl_grid_sync();
     using V = Vec<T>;
     using R = typename V::raw;
     constexpr int VN = V::N;
@@ -154,7 +157,12 @@ void preload_module_functions() {
 
 void launch_peer_barrier(Ctx& c, uint64_t* const* d_flags, uint64_t val, int* err, const int64_t* const* d_pseg,
                          const int64_t* d_pnin, int64_t* d_delta) {
-    k_peer_barrier<<<1, 32, 0, c.stream>>>(d_flags, c.cfg.rank, c.cfg.world, val, err, d_pseg, d_pnin, d_delta);
+    // strict stream order on both sides of the barrier: it starts after everything before it (the peers may read
+    // this rank's buffers once it signals), and the kernel after it -- a gather from the peers' memory -- starts
+    // only when it has completed
+    pdl_hold();
+    pdl_launch(c.stream, k_peer_barrier, 1, 32, 0, d_flags, c.cfg.rank, c.cfg.world, val, err, d_pseg, d_pnin, d_delta);
+    pdl_hold();
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -165,10 +173,10 @@ void launch_halo_pull(Ctx& c, void* dst, int64_t ld, void* const* d_peerH, const
     if (n <= 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16);
     if (c.prec == BNS_BF16)
-        k_halo_pull<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((__nv_bfloat16*)dst, ld, c.d_cand_out, n, d_owner_of_b,
+        pdl_launch(c.stream, k_halo_pull<__nv_bfloat16>, grid, 256, 0, (__nv_bfloat16*)dst, ld, c.d_cand_out, n, d_owner_of_b,
                                                                d_row_of_b, (__nv_bfloat16* const*)d_peerH, d);
     else
-        k_halo_pull<float><<<grid, 256, 0, c.stream>>>((float*)dst, ld, c.d_cand_out, n, d_owner_of_b, d_row_of_b,
+        pdl_launch(c.stream, k_halo_pull<float>, grid, 256, 0, (float*)dst, ld, c.d_cand_out, n, d_owner_of_b, d_row_of_b,
                                                        (float* const*)d_peerH, d);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -179,11 +187,11 @@ void launch_scatter_peer(Ctx& c, void* dst, int64_t ld, void* const* d_peerdx, c
     if (n <= 0 || c.n_sent <= 0) return;
     const unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16);
     if (c.prec == BNS_BF16)
-        k_scatter_peer<__nv_bfloat16><<<grid, 256, 0, c.stream>>>((__nv_bfloat16*)dst, ld, d, c.d_scat_mask,
+        pdl_launch(c.stream, k_scatter_peer<__nv_bfloat16>, grid, 256, 0, (__nv_bfloat16*)dst, ld, d, c.d_scat_mask,
                                                                   c.d_scat_pos, c.cfg.world, n,
                                                                   (__nv_bfloat16* const*)d_peerdx, d_delta);
     else
-        k_scatter_peer<float><<<grid, 256, 0, c.stream>>>((float*)dst, ld, d, c.d_scat_mask, c.d_scat_pos,
+        pdl_launch(c.stream, k_scatter_peer<float>, grid, 256, 0, (float*)dst, ld, d, c.d_scat_mask, c.d_scat_pos,
                                                           c.cfg.world, n, (float* const*)d_peerdx, d_delta);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();

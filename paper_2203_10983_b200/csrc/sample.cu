@@ -21,6 +21,7 @@ constexpr int kSampleBlock = 1024;
 // Single-block exclusive scan of n int32 (n arbitrary) -> int64 out[0..n], out[n] = total; optional extra total.
 __global__ void __launch_bounds__(1024) k_scan_top(const int32_t* __restrict__ in, int64_t* __restrict__ out,
                                                    int64_t n, int64_t* __restrict__ total) {
+    pdl_grid_sync();
     __shared__ int64_t warp_sums[32];
     __shared__ int64_t carry;
     if (threadIdx.x == 0) carry = 0;
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(1024) k_scan_top(const int32_t* __restrict__ i
 // Block-level exclusive scan (1024 elements per block), block sums to bsum.
 __global__ void __launch_bounds__(1024) k_scan_block(const int32_t* __restrict__ in, int64_t* __restrict__ out,
                                                      int64_t n, int32_t* __restrict__ bsum) {
+    pdl_grid_sync();
     __shared__ int32_t warp_sums[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
@@ -89,13 +91,14 @@ __global__ void __launch_bounds__(1024) k_scan_block(const int32_t* __restrict__
 }
 
 __global__ void k_scan_add(int64_t* __restrict__ out, int64_t n, const int64_t* __restrict__ boff) {
+    pdl_grid_sync();
     int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
     if (i < n) out[i] += boff[blockIdx.x];
 }
 
 void scan_i32(Ctx& c, const int32_t* in, int64_t* out, int64_t n, int64_t* d_total) {
     if (n <= 4096) {
-        k_scan_top<<<1, 1024, 0, c.stream>>>(in, out, n, d_total);
+        pdl_launch(c.stream, k_scan_top, 1, 1024, 0, in, out, n, d_total);
         c.kernels += 1;
         BNS_CHECK_LAUNCH();
         return;
@@ -103,13 +106,13 @@ void scan_i32(Ctx& c, const int32_t* in, int64_t* out, int64_t n, int64_t* d_tot
     int64_t nb = (n + 1023) / 1024;
     int32_t* bsum = reinterpret_cast<int32_t*>(c.d_scan_tmp);        // nb int32
     int64_t* boff = c.d_scan_tmp + (nb + 1) / 2 + 1;                  // nb+1 int64
-    k_scan_block<<<(unsigned)nb, 1024, 0, c.stream>>>(in, out, n, bsum);
-    k_scan_top<<<1, 1024, 0, c.stream>>>(bsum, boff, nb, nullptr);
-    k_scan_add<<<(unsigned)nb, 1024, 0, c.stream>>>(out, n, boff);
+    pdl_launch(c.stream, k_scan_block, (unsigned)nb, 1024, 0, in, out, n, bsum);
+    pdl_launch(c.stream, k_scan_top, 1, 1024, 0, bsum, boff, nb, nullptr);
+    pdl_launch(c.stream, k_scan_add, (unsigned)nb, 1024, 0, out, n, boff);
     c.kernels += 3;
     BNS_CHECK_LAUNCH();
-    BNS_CUDA(cudaMemcpyAsync(out + n, boff + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
-    if (d_total) BNS_CUDA(cudaMemcpyAsync(d_total, boff + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
+    BNS_CUDA_HOLD(cudaMemcpyAsync(out + n, boff + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
+    if (d_total) BNS_CUDA_HOLD(cudaMemcpyAsync(d_total, boff + nb, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
 }
 
 // a2: scatter kept candidates to their compacted position; recv candidates also publish slot_of_b.
@@ -120,6 +123,7 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample_scatter(const uint8_t* 
                                                                  int32_t* __restrict__ out,
                                                                  int32_t* __restrict__ slot_of_b,
                                                                  int64_t* __restrict__ seg_pos) {
+    pdl_grid_sync();
     __shared__ int32_t warp_cnt[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int64_t i = (int64_t)blockIdx.x * kSampleBlock + threadIdx.x;
@@ -150,6 +154,7 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample_scatter(const uint8_t* 
 
 __global__ void k_seg_tail(const int64_t* __restrict__ cand_seg, int nseg, int64_t n, const int64_t* __restrict__ boff,
                            int64_t nb, int64_t* __restrict__ seg_pos) {
+    pdl_grid_sync();
     int k = threadIdx.x;
     if (k < nseg && cand_seg[k] >= n) seg_pos[k] = boff[nb];
 }
@@ -165,6 +170,7 @@ __global__ void __launch_bounds__(256) k_induce_scatter_w(const int32_t* __restr
                                                           const uint32_t* __restrict__ bits,
                                                           const int64_t* __restrict__ boff, int64_t n_in,
                                                           int32_t* __restrict__ out_col) {
+    pdl_grid_sync();
     const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nw = (nnz + 31) >> 5;
     const int lane = threadIdx.x & 31;
@@ -217,6 +223,7 @@ __device__ __forceinline__ int64_t kept_before(int64_t e, const uint32_t* __rest
 __global__ void k_induce_rows(const int64_t* __restrict__ ptr, int64_t n_in, const uint32_t* __restrict__ bits,
                               const int64_t* __restrict__ boff, int64_t* __restrict__ out_ptr,
                               int32_t* __restrict__ nseg, int32_t seg_long) {
+    pdl_grid_sync();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r > n_in) return;
     const int64_t a = kept_before(ptr[r], bits, boff);
@@ -234,6 +241,7 @@ __device__ __forceinline__ void push_split(int64_t* list, int64_t* count, int64_
 
 __global__ void k_induce_segs(const int64_t* __restrict__ out_ptr, int64_t n_in, const int64_t* __restrict__ seg_off,
                               Seg* __restrict__ segs, int64_t* __restrict__ split, int64_t* __restrict__ n_split, int32_t seg_long) {
+    pdl_grid_sync();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_in) return;
     const int64_t b0 = out_ptr[r], b1 = out_ptr[r + 1];
@@ -261,21 +269,21 @@ void launch_induce_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     if (nb > 0) {
         const unsigned wb = (unsigned)((((nnz + 31) >> 5) + 255) / 256);
         launch_induce_flags_edge(c, nb, T, seed, epoch);
-        k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_eblk, c.d_eboff, nb, tot + 0);
-        k_induce_scatter_w<<<wb, 256, 0, c.stream>>>(c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff, n_in,
+        pdl_launch(c.stream, k_scan_top, 1, 1024, 0, c.d_eblk, c.d_eboff, nb, tot + 0);
+        pdl_launch(c.stream, k_induce_scatter_w, wb, 256, 0, c.d_col_enc, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff, n_in,
                                                      c.d_ind_col);
         c.kernels += 3;
     } else {
-        BNS_CUDA(cudaMemsetAsync(c.d_eboff, 0, sizeof(int64_t), c.stream));
-        BNS_CUDA(cudaMemsetAsync(tot, 0, sizeof(int64_t), c.stream));
+        BNS_CUDA_HOLD(cudaMemsetAsync(c.d_eboff, 0, sizeof(int64_t), c.stream));
+        BNS_CUDA_HOLD(cudaMemsetAsync(tot, 0, sizeof(int64_t), c.stream));
     }
-    k_induce_rows<<<(unsigned)((n_in + 1 + 255) / 256), 256, 0, c.stream>>>(c.d_row_ptr, n_in, c.d_ebits, c.d_eboff,
+    pdl_launch(c.stream, k_induce_rows, (unsigned)((n_in + 1 + 255) / 256), 256, 0, c.d_row_ptr, n_in, c.d_ebits, c.d_eboff,
                                                                           c.d_ind_ptr, c.d_row_nseg, c.seg_long);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
     scan_i32(c, c.d_row_nseg, c.d_row_soff, n_in, tot + 1);
-    BNS_CUDA(cudaMemsetAsync(tot + 4, 0, sizeof(int64_t), c.stream));
-    k_induce_segs<<<(unsigned)((n_in + 255) / 256), 256, 0, c.stream>>>(c.d_ind_ptr, n_in, c.d_row_soff, c.d_seg_fwd,
+    BNS_CUDA_HOLD(cudaMemsetAsync(tot + 4, 0, sizeof(int64_t), c.stream));
+    pdl_launch(c.stream, k_induce_segs, (unsigned)((n_in + 255) / 256), 256, 0, c.d_ind_ptr, n_in, c.d_row_soff, c.d_seg_fwd,
                                                                        c.d_split_fwd, tot + 4, c.seg_long);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
@@ -310,6 +318,7 @@ __global__ void __launch_bounds__(kSampleBlock) k_edge_cand(int64_t n_bd, int64_
                                                             const int32_t* __restrict__ col_enc,
                                                             const int64_t* __restrict__ b_off, ArcKey ak,
                                                             uint8_t* __restrict__ flags, int32_t* __restrict__ blk) {
+    pdl_grid_sync();
     const int64_t i = (int64_t)blockIdx.x * kSampleBlock + threadIdx.x;
     int keep = 0;
     if (i < n) {
@@ -336,18 +345,18 @@ void launch_sample_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     const int64_t nb = (n + kSampleBlock - 1) / kSampleBlock;
     int64_t* boff = c.d_scan_tmp;
     if (nb > 0) {
-        k_edge_cand<<<(unsigned)nb, kSampleBlock, 0, c.stream>>>(
+        pdl_launch(c.stream, k_edge_cand, (unsigned)nb, kSampleBlock, 0, 
             c.plan.n_bd, n, c.d_cand_gid, c.d_cand_key, c.d_cand_payload, c.d_vgid, c.d_br_ptr, c.d_tcol + c.ii_nnz,
             c.d_row_ptr, c.d_col_enc, c.d_cand_seg, arc_key(T, seed, epoch), c.d_flags, c.d_blk);
-        k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_blk, boff, nb, nullptr);
-        k_sample_scatter<<<(unsigned)nb, kSampleBlock, 0, c.stream>>>(c.d_flags, n, c.plan.n_bd, boff,
+        pdl_launch(c.stream, k_scan_top, 1, 1024, 0, c.d_blk, boff, nb, nullptr);
+        pdl_launch(c.stream, k_sample_scatter, (unsigned)nb, kSampleBlock, 0, c.d_flags, n, c.plan.n_bd, boff,
                                                                       c.d_cand_payload, c.d_cand_seg, 2 * m + 1,
                                                                       c.d_cand_out, c.d_slot_of_b, c.d_seg_pos);
         c.kernels += 3;
     } else {
-        BNS_CUDA(cudaMemsetAsync(boff, 0, sizeof(int64_t), c.stream));
+        BNS_CUDA_HOLD(cudaMemsetAsync(boff, 0, sizeof(int64_t), c.stream));
     }
-    k_seg_tail<<<1, 128, 0, c.stream>>>(c.d_cand_seg, 2 * m + 1, n, boff, nb, c.d_seg_pos);
+    pdl_launch(c.stream, k_seg_tail, 1, 128, 0, c.d_cand_seg, 2 * m + 1, n, boff, nb, c.d_seg_pos);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
@@ -359,6 +368,7 @@ __global__ void __launch_bounds__(1024) k_induce_flags_edge(const int32_t* __res
                                                             const int32_t* __restrict__ vgid,
                                                             const int32_t* __restrict__ bgid, int dropedge, ArcKey ak,
                                                             uint32_t* __restrict__ bits, int32_t* __restrict__ blk) {
+    pdl_grid_sync();
     const int64_t e = (int64_t)blockIdx.x * 1024 + threadIdx.x;
     int keep = 0;
     if (e < nnz) {
@@ -373,7 +383,7 @@ __global__ void __launch_bounds__(1024) k_induce_flags_edge(const int32_t* __res
 }
 
 void launch_induce_flags_edge(Ctx& c, int64_t nb, uint64_t T, uint64_t seed, uint64_t epoch) {
-    k_induce_flags_edge<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_col_enc, c.d_erow, c.nnz_i, c.d_vgid, c.d_cand_gid,
+    pdl_launch(c.stream, k_induce_flags_edge, (unsigned)nb, 1024, 0, c.d_col_enc, c.d_erow, c.nnz_i, c.d_vgid, c.d_cand_gid,
                                                              c.sampler == BNS_SAMPLER_DROPEDGE,
                                                              arc_key(T, seed, epoch), c.d_ebits, c.d_eblk);
 }
@@ -385,6 +395,7 @@ __global__ void __launch_bounds__(1024) k_tinduce_flags(const int32_t* __restric
                                                         const int32_t* __restrict__ vgid,
                                                         const int32_t* __restrict__ bgid, int dropedge, ArcKey ak,
                                                         uint32_t* __restrict__ bits, int32_t* __restrict__ blk) {
+    pdl_grid_sync();
     const int64_t e = (int64_t)blockIdx.x * 1024 + threadIdx.x;
     int keep = 0;
     if (e < nnz) {
@@ -409,6 +420,7 @@ __global__ void k_tinduce_rows(const int64_t* __restrict__ ptr, int64_t n_rows, 
                                const int32_t* __restrict__ slot_of_b, const uint32_t* __restrict__ bits,
                                const int64_t* __restrict__ boff, int64_t* __restrict__ out_ptr,
                                int32_t* __restrict__ nseg, int32_t seg_long) {
+    pdl_grid_sync();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r > n_rows) return;
     const int64_t a = kept_before(ptr[r], bits, boff);
@@ -421,6 +433,7 @@ __global__ void k_tinduce_rows(const int64_t* __restrict__ ptr, int64_t n_rows, 
 __global__ void k_tinduce_segs(const int64_t* __restrict__ out_ptr, int64_t n_rows, int64_t n_in,
                                const int32_t* __restrict__ slot_of_b, const int64_t* __restrict__ seg_off,
                                Seg* __restrict__ segs, int64_t* __restrict__ split, int64_t* __restrict__ n_split, int32_t seg_long) {
+    pdl_grid_sync();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rows) return;
     const int64_t s0 = seg_off[r], ns = seg_off[r + 1] - s0;
@@ -446,26 +459,26 @@ void launch_induce_bwd_edges(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) 
     const int64_t nnz = c.tnnz;
     const int64_t nb = (nnz + 1023) / 1024;
     if (nb > 0) {
-        k_tinduce_flags<<<(unsigned)nb, 1024, 0, c.stream>>>(c.d_tcol, c.d_terow, nnz, n_in, c.d_vgid, c.d_cand_gid,
+        pdl_launch(c.stream, k_tinduce_flags, (unsigned)nb, 1024, 0, c.d_tcol, c.d_terow, nnz, n_in, c.d_vgid, c.d_cand_gid,
                                                              c.sampler == BNS_SAMPLER_DROPEDGE,
                                                              arc_key(T, seed, epoch), c.d_ebits, c.d_eblk);
-        k_scan_top<<<1, 1024, 0, c.stream>>>(c.d_eblk, c.d_eboff, nb, tot + 5);
+        pdl_launch(c.stream, k_scan_top, 1, 1024, 0, c.d_eblk, c.d_eboff, nb, tot + 5);
         // every transposed column is an inner id (>= 0): the scatter's remap is the identity
-        k_induce_scatter_w<<<(unsigned)((((nnz + 31) >> 5) + 255) / 256), 256, 0, c.stream>>>(
+        pdl_launch(c.stream, k_induce_scatter_w, (unsigned)((((nnz + 31) >> 5) + 255) / 256), 256, 0, 
             c.d_tcol, nnz, c.d_slot_of_b, c.d_ebits, c.d_eboff, n_in, c.d_ind_tcol);
         c.kernels += 3;
     } else {
-        BNS_CUDA(cudaMemsetAsync(c.d_eboff, 0, sizeof(int64_t), c.stream));
-        BNS_CUDA(cudaMemsetAsync(tot + 5, 0, sizeof(int64_t), c.stream));
+        BNS_CUDA_HOLD(cudaMemsetAsync(c.d_eboff, 0, sizeof(int64_t), c.stream));
+        BNS_CUDA_HOLD(cudaMemsetAsync(tot + 5, 0, sizeof(int64_t), c.stream));
     }
-    k_tinduce_rows<<<(unsigned)((n_rows + 1 + 255) / 256), 256, 0, c.stream>>>(
+    pdl_launch(c.stream, k_tinduce_rows, (unsigned)((n_rows + 1 + 255) / 256), 256, 0, 
         c.d_tptr, n_rows, n_in, c.d_slot_of_b, c.d_ebits, c.d_eboff, c.d_ind_tptr, c.d_trow_nseg, c.seg_long);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
     scan_i32(c, c.d_trow_nseg, c.d_trow_soff, n_rows, tot + 6);
-    BNS_CUDA(cudaMemsetAsync(tot + 7, 0, sizeof(int64_t), c.stream));
+    BNS_CUDA_HOLD(cudaMemsetAsync(tot + 7, 0, sizeof(int64_t), c.stream));
     if (n_rows > 0) {
-        k_tinduce_segs<<<(unsigned)((n_rows + 255) / 256), 256, 0, c.stream>>>(
+        pdl_launch(c.stream, k_tinduce_segs, (unsigned)((n_rows + 255) / 256), 256, 0, 
             c.d_ind_tptr, n_rows, n_in, c.d_slot_of_b, c.d_trow_soff, c.d_eseg_bwd, c.d_esplit_bwd, tot + 7, c.seg_long);
         c.kernels += 1;
         BNS_CHECK_LAUNCH();

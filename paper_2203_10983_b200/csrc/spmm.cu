@@ -142,6 +142,78 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
     *reinterpret_cast<typename V::raw*>(static_cast<T*>(a.out) + row * a.ld_out + vi * VN) = V::from_float(acc);
 }
 
+// Sum the fp32 partials of a split row in segment order (the row's segments first .. first + nseg - 1), then the
+// epilogue; all 32 lanes, one 16-byte vector each per step.  L2 loads (__ldcg): the partials were written by other
+// SMs during this grid (fused path) or the previous one.  Shared by the fused path and k_spmm_fixup, so both give
+// the same bits.
+template <typename T>
+__device__ __forceinline__ void split_sum_store(const SpmmArgs& a, int64_t first, int32_t row, int32_t nseg, int lane) {
+    constexpr int VN = Vec<T>::N;
+    const int nvec = a.d / VN;
+    for (int vi = lane; vi < nvec; vi += 32) {
+        float acc[VN];
+#pragma unroll
+        for (int k = 0; k < VN; ++k) acc[k] = 0.f;
+        const float* pp = a.partial + first * (int64_t)a.d + vi * VN;
+        int q = 0;
+        // 4 segments' partials in flight (16-byte loads), still added in segment order
+        for (; q + 4 <= nseg; q += 4) {
+            float4 t[4][VN / 4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int k = 0; k < VN / 4; ++k)
+                    t[j][k] = __ldcg(reinterpret_cast<const float4*>(pp + (int64_t)(q + j) * a.d + 4 * k));
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int k = 0; k < VN / 4; ++k) {
+                    acc[4 * k] += t[j][k].x;
+                    acc[4 * k + 1] += t[j][k].y;
+                    acc[4 * k + 2] += t[j][k].z;
+                    acc[4 * k + 3] += t[j][k].w;
+                }
+        }
+        for (; q < nseg; ++q)
+#pragma unroll
+            for (int k = 0; k < VN / 4; ++k) {
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(pp + (int64_t)q * a.d + 4 * k));
+                acc[4 * k] += t.x;
+                acc[4 * k + 1] += t.y;
+                acc[4 * k + 2] += t.z;
+                acc[4 * k + 3] += t.w;
+            }
+        epilogue_store<T>(a, row, vi, acc);
+    }
+}
+
+// Fused split-row fixup: after writing its partial, the warp counts itself in; the warp that finishes a row's
+// last segment (in any order) sums all the row's partials in segment order and stores the row.  The counter is
+// reset by that warp, so the next launch finds it zero.
+template <typename T>
+__device__ __forceinline__ void split_arrive(const SpmmArgs& a, const Seg& s, int lane) {
+    __threadfence();   // this lane's partial is visible device-wide before the count
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(a.arrive + s.first, 1) == s.nseg - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();   // every other segment's partial is visible to this warp
+    if (lane == 0) a.arrive[s.first] = 0;
+    split_sum_store<T>(a, s.first, s.row, s.nseg, lane);
+}
+
+// Dynamic scheduling epilogue: every warp counts itself out after its last (failed) claim; the last one resets the
+// claim counter and the done counter for the next launch.
+__device__ __forceinline__ void work_done(unsigned long long* work, int lane) {
+    if (!work || lane != 0) return;
+    const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    if (atomicAdd(work + 1, 1ull) == nw - 1) {
+        atomicExch(work, 0ull);
+        atomicExch(work + 1, 0ull);
+    }
+}
+
 // SC: per-edge column scale -- 0 none (backward modes, and the forward when every column has c_u = 1),
 //     1 c_u = 1/p for halo columns (col >= n_in, SAGE forward), 2 c_u from cscale[] (GCN forward).
 #ifndef BNS_SPMM_U1
@@ -156,6 +228,7 @@ __device__ __forceinline__ void epilogue_store(const SpmmArgs& a, int64_t row, i
 template <typename T, int LPR, int VPL, int SC>
 __global__ void __launch_bounds__(256, (VPL <= 1 && SC == 0) ? BNS_SPMM_MINB1 : (VPL <= 2) ? 3 : (VPL <= 6) ? 2 : 1)
 k_spmm(const SpmmArgs a) {
+    pdl_grid_sync();
     using V = Vec<T>;
     using R = typename V::raw;
     constexpr int VN = V::N;
@@ -281,18 +354,20 @@ k_spmm(const SpmmArgs a) {
 #pragma unroll
                     for (int k = 0; k < VN; ++k) acc[v][k] += __shfl_xor_sync(0xffffffffu, acc[v][k], o);
         }
-        if (g != 0) continue;
         if (s.nseg > 1) {
-            float* pp = a.partial + sid * (int64_t)a.d;
+            if (g == 0) {
+                float* pp = a.partial + sid * (int64_t)a.d;
 #pragma unroll
-            for (int v = 0; v < VPL; ++v) {
-                const int vi = l + v * LPR;
-                if (vi < nvec)
+                for (int v = 0; v < VPL; ++v) {
+                    const int vi = l + v * LPR;
+                    if (vi < nvec)
 #pragma unroll
-                    for (int k = 0; k < VN; k += 4)
-                        *reinterpret_cast<float4*>(pp + vi * VN + k) = make_float4(acc[v][k], acc[v][k + 1], acc[v][k + 2], acc[v][k + 3]);
+                        for (int k = 0; k < VN; k += 4)
+                            *reinterpret_cast<float4*>(pp + vi * VN + k) = make_float4(acc[v][k], acc[v][k + 1], acc[v][k + 2], acc[v][k + 3]);
+                }
             }
-        } else {
+            if (a.arrive) split_arrive<T>(a, s, lane);
+        } else if (g == 0) {
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int vi = l + v * LPR;
@@ -300,6 +375,7 @@ k_spmm(const SpmmArgs a) {
             }
         }
     }
+    work_done(a.work, lane);
 }
 
 // ------------------------------------------------------------------------------------------------------------------
@@ -317,6 +393,7 @@ __device__ __forceinline__ uint32_t g4_smem(const void* p) { return (uint32_t)__
 
 template <int SC>
 __global__ void __launch_bounds__(256, 3) k_spmm_g4(const __grid_constant__ CUtensorMap map, const SpmmArgs a) {
+    pdl_grid_sync();
     extern __shared__ __align__(128) uint8_t g4_smem_raw[];
     __shared__ __align__(8) uint64_t bars[8][G4_STAGES];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -386,10 +463,12 @@ __global__ void __launch_bounds__(256, 3) k_spmm_g4(const __grid_constant__ CUte
             float* pp = a.partial + sid * (int64_t)a.d + lane * 8;
             *reinterpret_cast<float4*>(pp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
             *reinterpret_cast<float4*>(pp + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            if (a.arrive) split_arrive<__nv_bfloat16>(a, s, lane);
         } else {
             epilogue_store<__nv_bfloat16>(a, s.row, lane, acc);
         }
     }
+    work_done(a.work, lane);
 }
 
 static bool spmm_tma() {
@@ -437,10 +516,9 @@ static bool launch_spmm_g4(Ctx& c, SpmmArgs a, int sc) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.n_segs + 7) / 8, (int64_t)std::max(1, per_sm) * sms));
-    BNS_CUDA(cudaMemsetAsync(c.d_spmm_work, 0, sizeof(unsigned long long), c.stream));
     a.work = c.d_spmm_work;
     a.chunk = claim_chunk(a.n_segs, (int64_t)grid * 8);
-    kern<<<grid, 256, smem, c.stream>>>(map, a);
+    pdl_launch(c.stream, kern, grid, 256, smem, map, a);
     return true;
 }
 
@@ -450,50 +528,14 @@ static bool launch_spmm_g4(Ctx& c, SpmmArgs a, int sc) {
 // hub rows' serial tail.)
 template <typename T>
 __global__ void __launch_bounds__(256) k_spmm_fixup(const SpmmArgs a) {
-    using V = Vec<T>;
-    constexpr int VN = V::N;
+    pdl_grid_sync();
     const int lane = threadIdx.x & 31;
-    const int nvec = a.d / VN;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t q0 = warp; q0 < a.n_split; q0 += nwarps) {
         const int64_t sid = a.split[q0];
         const Seg s = a.segs[sid];
-        for (int vi = lane; vi < nvec; vi += 32) {
-            float acc[VN];
-#pragma unroll
-            for (int k = 0; k < VN; ++k) acc[k] = 0.f;
-            const float* pp = a.partial + sid * (int64_t)a.d + vi * VN;
-            int q = 0;
-            // 4 segments' partials in flight (16-byte loads), still added in segment order
-            for (; q + 4 <= s.nseg; q += 4) {
-                float4 t[4][VN / 4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int k = 0; k < VN / 4; ++k)
-                        t[j][k] = *reinterpret_cast<const float4*>(pp + (int64_t)(q + j) * a.d + 4 * k);
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int k = 0; k < VN / 4; ++k) {
-                        acc[4 * k] += t[j][k].x;
-                        acc[4 * k + 1] += t[j][k].y;
-                        acc[4 * k + 2] += t[j][k].z;
-                        acc[4 * k + 3] += t[j][k].w;
-                    }
-            }
-            for (; q < s.nseg; ++q)
-#pragma unroll
-                for (int k = 0; k < VN / 4; ++k) {
-                    const float4 t = *reinterpret_cast<const float4*>(pp + (int64_t)q * a.d + 4 * k);
-                    acc[4 * k] += t.x;
-                    acc[4 * k + 1] += t.y;
-                    acc[4 * k + 2] += t.z;
-                    acc[4 * k + 3] += t.w;
-                }
-            epilogue_store<T>(a, s.row, vi, acc);
-        }
+        split_sum_store<T>(a, sid, s.row, s.nseg, lane);
     }
 }
 
@@ -519,13 +561,12 @@ static void go_sc(Ctx& c, SpmmArgs a, unsigned grid) {
     static const int wave = resident_per_gpu((const void*)kern);   // per kernel instance (thread-safe init)
     if (spmm_sched() != 0) grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.n_segs + 7) / 8, wave));
     if (spmm_sched() == 2) {
-        BNS_CUDA(cudaMemsetAsync(c.d_spmm_work, 0, sizeof(unsigned long long), c.stream));
         a.work = c.d_spmm_work;
         a.chunk = claim_chunk(a.n_segs, (int64_t)grid * 8);
     } else {
         a.work = nullptr;
     }
-    kern<<<grid, 256, 0, c.stream>>>(a);
+    pdl_launch(c.stream, kern, grid, 256, 0, a);
 }
 
 template <typename T, int LPR, int VPL>
@@ -614,8 +655,14 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
         }
     }
     unsigned grid = (unsigned)std::min<int64_t>((a0.n_segs + 7) / 8, 148 * 32);
+    // split rows summed inside the SpMM by the warp finishing their last segment (no fixup launch) on jobs without
+    // long segments (R37: their hub rows have few 256-edge partials); large jobs keep the separate fixup pass, where
+    // one warp summing a hub row's hundreds of partials would be a serial tail.  BNS_SPMM_FUSE=0/1 forces it.
+    static const int fuse_env = [] { const char* e = std::getenv("BNS_SPMM_FUSE"); return e ? std::atoi(e) : -1; }();
+    const bool fuse = a0.n_split > 0 && (fuse_env >= 0 ? fuse_env == 1 : c.seg_long == 0);
     for (int64_t c0 = 0; c0 < a0.d; c0 += tile) {
         SpmmArgs a = a0;
+        a.arrive = fuse ? c.d_spmm_arrive : nullptr;
         a.d = (int32_t)std::min<int64_t>(tile, a0.d - c0);
         a.src = static_cast<const char*>(a0.src) + c0 * ts;
         a.out = static_cast<char*>(a0.out) + c0 * ((a0.out_f32 || a0.mode == GAT_RAW) ? 4 : ts);
@@ -626,10 +673,10 @@ void launch_spmm(Ctx& c, const SpmmArgs& a0) {
         else dispatch<float>(c, a, grid);
         c.kernels += 1;
         BNS_CHECK_LAUNCH();
-        if (a.n_split > 0) {   // only the split (hub) rows, listed by their first segment
+        if (a.n_split > 0 && !fuse) {   // only the split (hub) rows, listed by their first segment
             const unsigned fg = (unsigned)std::min<int64_t>((a.n_split + 7) / 8, 148 * 8);
-            if (c.prec == BNS_BF16) k_spmm_fixup<__nv_bfloat16><<<fg, 256, 0, c.stream>>>(a);
-            else k_spmm_fixup<float><<<fg, 256, 0, c.stream>>>(a);
+            if (c.prec == BNS_BF16) pdl_launch(c.stream, k_spmm_fixup<__nv_bfloat16>, fg, 256, 0, a);
+            else pdl_launch(c.stream, k_spmm_fixup<float>, fg, 256, 0, a);
             c.kernels += 1;
             BNS_CHECK_LAUNCH();
         }

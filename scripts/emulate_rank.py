@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--cache-x0", action="store_true", help="BNS_CACHE_INPUT_HALO (f1, R43): no layer-1 exchange")
     ap.add_argument("--no-timing", action="store_true", help="no per-phase CUDA events (device total only)")
     ap.add_argument("--no-prefetch", action="store_true", help="no BNS_PREFETCH_DRAW (R48): draw + host wait per step")
+    ap.add_argument("--ceiling", action="store_true",
+                    help="also run build/gather_ceiling on this rank's induced forward column stream (one draw)")
     ap.add_argument("--samplers", nargs="+", default=["bns"], choices=["bns", "bes", "dropedge"],
                     help="f3 Table tab:bes analogue: edge samplers at matched dropped-edge counts (P:681)")
     args = ap.parse_args()
@@ -119,6 +121,20 @@ def main():
                    "nnz_kept": cnt["nnz_kept"], "phases_ms": ph,
                    "note": "single-GPU emulation: exchanges/all-reduce are no-ops; NOT an m-GPU measurement"}
             print(json.dumps(rec), flush=True)
+            if args.ceiling and smp == bns.BNS_SAMPLER_BNS:
+                # the gather ceiling of exactly this rank's forward column stream (CSR order, no row boundaries)
+                import subprocess
+                import tempfile
+                ctx.sample_boundary(p, I.BNS_SEED, 0)
+                ptr, cols = ctx.induced(cnt["n_in"])
+                exe = os.path.join(ROOT, "build", "gather_ceiling")
+                w = dp[1] * s
+                with tempfile.TemporaryDirectory() as d:
+                    f = os.path.join(d, "col.bin")
+                    np.ascontiguousarray(cols, np.int32).tofile(f)
+                    for rb, stride, tag in [(w, w, f"{sh.name} m={args.m} rank {r} p={p} induced CSR order, {w} B rows"),
+                                            (w, 2 * w, f"{sh.name} m={args.m} rank {r} p={p} induced CSR order, {w} B rows at {2 * w} B stride")]:
+                        subprocess.run([exe, "20", f, str(rb), str(stride), tag], check=True)
         ctx.close()
 
 
