@@ -47,13 +47,6 @@ kseg%:
 $(PKG)/libbns_kseg%.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
 
-# A/B variant without the SpMM column-index prefetch
-noprefetch:
-	$(MAKE) OBJDIR=build_nopf NVFLAGS="$(NVFLAGS) -DBNS_SPMM_PREFETCH=0" $(PKG)/libbns_nopf.so
-
-$(PKG)/libbns_nopf.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
-
 # generic A/B variant: make variant VAR=name DEFS="-DBNS_X=..." -> $(PKG)/libbns_name.so (BNS_LIB selects it)
 variant:
 	$(MAKE) OBJDIR=build_$(VAR) NVFLAGS="$(NVFLAGS) $(DEFS)" CXXDEF="$(DEFS)" $(PKG)/libbns_$(VAR).so

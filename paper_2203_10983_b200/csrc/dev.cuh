@@ -127,10 +127,20 @@ template <> __device__ __forceinline__ void acc_vec2<__nv_bfloat16, true>(uint64
 #pragma unroll
     for (int k = 0; k < 4; ++k) ffma2p(a[k], pk2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xffff0000u)), s2);
 }
+// unscaled bf16: sm_100's mixed-precision add (add.rn.f32.bf16 -> FHADD.BF16) reads each bf16 half of the packed
+// word directly (.H0 / .H1), one instruction per element instead of an unpack per element plus half an FADD2 --
+// the same fp32 round-to-nearest sum of the exactly widened value, so the results are bitwise those of the unpacked
+// FADD2 form
 template <> __device__ __forceinline__ void acc_vec2<__nv_bfloat16, false>(uint64_t* a, const uint4& v, uint64_t) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) fadd2p(a[k], pk2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xffff0000u)));
+    for (int k = 0; k < 4; ++k) {
+        float lo, hi;
+        upk2(a[k], lo, hi);
+        asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tadd.rn.f32.bf16 %0, l, %0;\n\tadd.rn.f32.bf16 %1, h, %1;\n\t}"
+            : "+f"(lo), "+f"(hi) : "r"(w[k]));
+        a[k] = pk2(lo, hi);
+    }
 }
 
 // acc (VN floats) += s * v, or += v when SCALED is false
