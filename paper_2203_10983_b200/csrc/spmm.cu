@@ -16,6 +16,7 @@
 // segments whose fp32 partials are summed in segment order by k_spmm_fixup -- deterministic, and the split
 // depends only on the row length.
 #include <cstdlib>
+#include <cstring>
 
 #include <cuda.h>
 
@@ -214,6 +215,23 @@ __device__ __forceinline__ void work_done(unsigned long long* work, int lane) {
     }
 }
 
+// SC 7 (bf16 rows, 1/p exact in bf16, e.g. p = 0.1, 0.01, 0.5): acc += s * x with x and s read as bf16 by the
+// mixed-precision FMA (fma.rn.f32.bf16 -> FHFMA.BF16 on each packed half) -- the exact product rounded once, so
+// bitwise the SC 1 result (FFMA2 of the widened value by the same fp32 scale), without the unpack
+template <typename R>
+__device__ __forceinline__ void acc_vec_bf16s(uint64_t* a, const R& v, uint32_t sbits) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float lo, hi;
+        upk2(a[k], lo, hi);
+        asm("{\n\t.reg .b16 l, h, sl, sh;\n\tmov.b32 {l, h}, %2;\n\tmov.b32 {sl, sh}, %3;\n\t"
+            "fma.rn.f32.bf16 %0, l, sl, %0;\n\tfma.rn.f32.bf16 %1, h, sl, %1;\n\t}"
+            : "+f"(lo), "+f"(hi) : "r"(w[k]), "r"(sbits));
+        a[k] = pk2(lo, hi);
+    }
+}
+
 // SC: per-edge column scale -- 0 none (backward modes, and the forward when every column has c_u = 1),
 //     1 c_u = 1/p for halo columns (col >= n_in, SAGE forward), 2 c_u from cscale[] (GCN forward).
 #ifndef BNS_SPMM_U1
@@ -285,7 +303,7 @@ k_spmm(const SpmmArgs a) {
 #else
                 ci = a.col[eb + lane];
 #endif
-                if (SC == 1) sc = (ci >= a.n_in) ? a.inv_p : 1.f;
+                if (SC == 1 || SC == 7) sc = (ci >= a.n_in) ? a.inv_p : 1.f;
                 if (SC == 2) sc = a.cscale[ci];
                 if (SC == 3) {   // GAT forward: alpha_vu, v = this row (R45)
                     const float t = a.gat_el[s.row] + a.gat_er[ci];
@@ -311,7 +329,9 @@ k_spmm(const SpmmArgs a) {
                     for (int u = 0; u < U; ++u) {
                         const int j = j0 + u * G + g;
                         const uint32_t cj = (uint32_t)__shfl_sync(0xffffffffu, ci, j);
-                        if (SC) {
+                        if (SC == 7) {   // the scale's bf16 bits (exact by construction of SC 7)
+                            sj[u] = __shfl_sync(0xffffffffu, __float_as_uint(sc) >> 16, j);
+                        } else if (SC) {
                             const float t = __shfl_sync(0xffffffffu, sc, j);
                             sj[u] = pk2(t, t);
                         }
@@ -324,7 +344,8 @@ k_spmm(const SpmmArgs a) {
                     for (int u = 0; u < U; ++u)
 #pragma unroll
                         for (int v = 0; v < VPL; ++v)
-                            acc_vec2<T, SC != 0>(acc2[v], r[u][v], SC ? sj[u] : 0ull);
+                            if (SC == 7) acc_vec_bf16s(acc2[v], r[u][v], (uint32_t)sj[u]);
+                            else acc_vec2<T, SC != 0>(acc2[v], r[u][v], SC ? sj[u] : 0ull);
                 }
             } else {
                 // tail chunk (< 32 edges): one edge per lane group per step
@@ -336,7 +357,8 @@ k_spmm(const SpmmArgs a) {
                         const R* rowp = reinterpret_cast<const R*>(base + (uint64_t)cj * rvb);
 #pragma unroll
                         for (int v = 0; v < VPL; ++v)
-                            acc_vec2<T, SC != 0>(acc2[v], ldg_nc(rowp + voff[v]), pk2(t, t));
+                            if (SC == 7) acc_vec_bf16s(acc2[v], ldg_nc(rowp + voff[v]), __float_as_uint(t) >> 16);
+                            else acc_vec2<T, SC != 0>(acc2[v], ldg_nc(rowp + voff[v]), pk2(t, t));
                     }
                 }
             }
@@ -577,6 +599,14 @@ static void go(Ctx& c, const SpmmArgs& a, unsigned grid) {
     else if (a.mode == GCN_FWD) sc = 2;
     else if ((a.mode == SAGE_FWD || a.mode == SAGE_FWD_TF) && a.inv_p != 1.f) sc = 1;
     if (LPR == 32 && VPL == 1 && launch_spmm_g4(c, a, sc)) return;
+    uint32_t ib;
+    std::memcpy(&ib, &a.inv_p, 4);
+    if constexpr (sizeof(T) == 2) {
+        if (sc == 1 && (ib & 0xffffu) == 0u) {   // 1/p exact in bf16: SC 7 (the same bits as SC 1)
+            go_sc<T, LPR, VPL, 7>(c, a, grid);
+            return;
+        }
+    }
     if (sc == 0) go_sc<T, LPR, VPL, 0>(c, a, grid);
     else if (sc == 1) go_sc<T, LPR, VPL, 1>(c, a, grid);
     else if (sc == 2) go_sc<T, LPR, VPL, 2>(c, a, grid);
