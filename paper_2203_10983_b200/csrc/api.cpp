@@ -433,6 +433,17 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
     c.gflat_n = c.goff[L];
     c.d_gflat = static_cast<float*>(salloc(c, c.gflat_n * sizeof(float)));
     c.splitk_cap = 32 * wmax;
+    if (c.use_tc && c.prec == BNS_BF16 && c.layer != BNS_LAYER_GAT) {
+        // every layer's partial slices at once (deferred reduction, splitk_flush): at most ceil(148 / tiles) slices
+        // of an (M2 = 128-padded d_in + d_in) x d_out product per layer (gemm_tc.cu's split rule)
+        int64_t tot = 0;
+        for (int l = 0; l < L; ++l) {
+            const int64_t K = c.dp[l], N = c.dp[l + 1], M2 = (K + 127) / 128 * 128 + K;
+            const int64_t tiles = ((M2 + 127) / 128) * ((N + 255) / 256);
+            tot += std::max<int64_t>(1, (148 + tiles - 1) / tiles) * M2 * N;
+        }
+        c.splitk_cap = std::max(c.splitk_cap, tot);
+    }
     if (c.use_tc && c.prec == BNS_FP32) {   // fp32 dW runs K-major on transposed operands (gemm_tc.cu)
         int64_t kn = 0, w2 = 0;
         for (int l = 0; l < L; ++l) {
@@ -712,6 +723,11 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
                         tfL ? c.d_dxcat : nullptr, ldp, nzero);
     }
     // ------------------------------ backward (l.12) ------------------------------
+    // a12 (owner scatter-add of the returned halo gradients) is folded into the ReLU mask of the layer below when
+    // one launch serves every peer (d_scat_mask) and no per-layer dH copy is kept: pend holds its sources
+    ScatterIn pend{};
+    const bool fold_scatter = m > 1 && c.d_scat_mask && !c.retain;
+    c.defer_red = c.use_tc && c.prec == BNS_BF16 && c.layer != BNS_LAYER_GAT;   // one split-K reduce launch
     for (int l = L; l >= 1; --l) {
         const int64_t din = c.dp[l - 1], dout = c.dp[l];
         void* Hin = dropout ? c.Xd[l - 1] : c.H[l - 1];
@@ -721,7 +737,8 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
                 BNS_CUDA_HOLD(cudaMemcpyAsync(c.dH_keep[l], c.d_dx, n_in * dout * ts, cudaMemcpyDeviceToDevice, c.stream));
             const bool tfl = (c.tf_mask >> (l - 1)) & 1u;   // R42: + dPre / deg_G into d_dxcat (unused there)
             launch_relu_mask(c, c.d_dx, c.H[l], dout, n_in, (int32_t)dout, c.d_dpre, tfl ? c.d_deg_in : nullptr,
-                             tfl ? c.d_dxcat : nullptr);
+                             tfl ? c.d_dxcat : nullptr, pend.mask ? &pend : nullptr);
+            pend = ScatterIn{};
         }
         if (peer) c.d_dx = c.tr->dx_buffer(c, l);   // f1: layer l's dX; a peer may still read layer l+1's
         if (c.layer == BNS_LAYER_GAT) backward_layer_gat(c, ev, l, Hin);
@@ -734,7 +751,13 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
         }
         if (peer) {   // f1: reverse exchange + scatter-add = one gather from the peers' dX halo rows
             PhaseTimer t(c, BNS_PH_SCATTER);
-            c.tr->grad_scatter(c, l, din);
+            if (fold_scatter && c.n_sent > 0 && c.tr->grad_barrier(c, l, &pend.peer, &pend.delta)) {
+                pend.mask = c.d_scat_mask;
+                pend.pos = c.d_scat_pos;
+                pend.m = m;
+            } else {
+                c.tr->grad_scatter(c, l, din);
+            }
         } else if (m > 1) {
             {
                 PhaseTimer t(c, BNS_PH_EXCHANGE_BWD);
@@ -742,7 +765,14 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
                                c.send_off.data(), din * ts);
             }
             PhaseTimer t(c, BNS_PH_SCATTER);
-            if (c.d_scat_mask) {            // R25: local contribution first, then peers ascending, one launch
+            if (fold_scatter) {             // R25 in the ReLU mask of layer l - 1 (the next launch)
+                if (c.n_sent > 0) {
+                    pend.mask = c.d_scat_mask;
+                    pend.pos = c.d_scat_pos;
+                    pend.m = m;
+                    pend.src = c.d_gradbuf;
+                }
+            } else if (c.d_scat_mask) {     // R25: local contribution first, then peers ascending, one launch
                 launch_scatter_rows(c, c.d_dx, din, c.d_gradbuf, (int32_t)din);
             } else {
                 for (int j = 0; j < m; ++j) {
@@ -753,6 +783,11 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
                 }
             }
         }
+    }
+    {
+        PhaseTimer t(c, BNS_PH_GEMM_BWD);
+        splitk_flush(c);   // every layer's dW from its split-K slices, one launch
+        c.defer_red = false;
     }
     // ------------------------------ AllReduce (l.13) + update (l.14) ------------------------------
     if (m > 1) {

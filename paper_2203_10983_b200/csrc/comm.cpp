@@ -469,6 +469,13 @@ struct PeerTransport : Transport {
         first = false;
         launch_scatter_peer(c, c.d_dx, din, row(K_DX + (l & 1)), d_delta, (int32_t)din);
     }
+    bool grad_barrier(Ctx& c, int l, const void* const** peer, const int64_t** delta) override {
+        barrier(c, first);
+        first = false;
+        *peer = row(K_DX + (l & 1));
+        *delta = d_delta;
+        return true;
+    }
     void exchange(Ctx& c, const void* src, const int64_t* src_off, void* dst, const int64_t* dst_off,
                   size_t rowbytes) override {
         if (src != c.d_sendbuf) throw Error(BNS_ERR_RUNTIME, "peer-memory transport: generic exchange needs the send buffer");

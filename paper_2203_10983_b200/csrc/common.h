@@ -252,6 +252,14 @@ struct Ctx {
     int32_t* d_nonfinite = nullptr;
     const int* d_abort = nullptr;  // peer transports: mapped barrier-timeout flag (update kernels skip when set)
     int last_splitk = 1;           // split-K factor of the last tcgen05 weight-gradient GEMM (bns_gemm reports it)
+    // bf16 epochs: the split-K reductions of all layers' weight gradients run as ONE launch after the backward
+    // (splitk_flush); partial slices of the pending layers sit side by side in d_splitk
+    struct RedJob {
+        const float* part; int S; int64_t M, N, zs, gap_row, gap; float* out; int64_t ldo;
+    };
+    bool defer_red = false;
+    std::vector<RedJob> red_jobs;
+    int64_t splitk_used = 0;
     // --- f3: edge samplers (BES / DropEdge); allocated by the first bns_sample_edges
     int sampler = 0;               // BNS_SAMPLER_* of the last draw
     float nscale = 1.f;            // neighbour-sum scale (DropEdge: 1/q on every arc; else 1)

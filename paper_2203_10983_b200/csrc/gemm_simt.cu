@@ -139,7 +139,95 @@ __global__ void __launch_bounds__(kRedGroups * 32) k_splitk_reduce(const float* 
     *reinterpret_cast<float4*>(out + i * ldo + j) = r;
 }
 
+// several reductions in one launch: job q owns blocks [jb[q], jb[q + 1])
+constexpr int kRedJobs = 8;
+struct RedTable {
+    int njobs;
+    int64_t jb[kRedJobs + 1];
+    const float* part[kRedJobs];
+    int S[kRedJobs];
+    int64_t M[kRedJobs], N[kRedJobs], zs[kRedJobs], gap_row[kRedJobs], gap[kRedJobs], ldo[kRedJobs];
+    float* out[kRedJobs];
+};
+__global__ void __launch_bounds__(kRedGroups * 32) k_splitk_reduce_multi(const RedTable tb) {
+    pdl_grid_sync();
+    __shared__ float4 s_g[kRedGroups][32];
+    int q = 0;
+    while (q + 1 < tb.njobs && (int64_t)blockIdx.x >= tb.jb[q + 1]) ++q;
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int64_t N = tb.N[q], n4 = N / 4;
+    const int S = tb.S[q];
+    const int64_t t = ((int64_t)blockIdx.x - tb.jb[q]) * 32 + lane;
+    const bool live = t < tb.M[q] * n4;
+    const int64_t i = live ? t / n4 : 0, j = live ? (t % n4) * 4 : 0;
+    const float* p0 = tb.part[q] + (i < tb.gap_row[q] ? i : i + tb.gap[q]) * N + j;
+    const int64_t zs = tb.zs[q];
+    const int per = (S + kRedGroups - 1) / kRedGroups;
+    const int z0 = min(S, g * per), z1 = min(S, z0 + per);
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) {
+        int z = z0;
+        for (; z + 8 <= z1; z += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(p0 + (int64_t)(z + u) * zs));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w; }
+        }
+        for (; z < z1; ++z) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(p0 + (int64_t)z * zs));
+            s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+        }
+    }
+    s_g[g][lane] = s;
+    __syncthreads();
+    if (g != 0 || !live) return;
+    float4 r = s_g[0][lane];
+    for (int u = 1; u < kRedGroups; ++u) {
+        const float4 v = s_g[u][lane];
+        r.x += v.x; r.y += v.y; r.z += v.z; r.w += v.w;
+    }
+    *reinterpret_cast<float4*>(tb.out[q] + i * tb.ldo[q] + j) = r;
+}
+
+void splitk_flush(Ctx& c) {
+    if (c.red_jobs.empty()) {
+        c.splitk_used = 0;
+        return;
+    }
+    for (size_t q0 = 0; q0 < c.red_jobs.size(); q0 += kRedJobs) {
+        RedTable tb{};
+        tb.njobs = (int)std::min<size_t>(kRedJobs, c.red_jobs.size() - q0);
+        int64_t nb = 0;
+        for (int q = 0; q < tb.njobs; ++q) {
+            const Ctx::RedJob& jb = c.red_jobs[q0 + q];
+            tb.jb[q] = nb;
+            tb.part[q] = jb.part; tb.S[q] = jb.S; tb.M[q] = jb.M; tb.N[q] = jb.N; tb.zs[q] = jb.zs;
+            tb.gap_row[q] = jb.gap_row; tb.gap[q] = jb.gap; tb.out[q] = jb.out; tb.ldo[q] = jb.ldo;
+            nb += (jb.M * jb.N / 4 + 31) / 32;
+        }
+        tb.jb[tb.njobs] = nb;
+        pdl_launch(c.stream, k_splitk_reduce_multi, (unsigned)nb, kRedGroups * 32, 0, tb);
+        c.kernels += 1;
+        BNS_CHECK_LAUNCH();
+    }
+    c.red_jobs.clear();
+    c.splitk_used = 0;
+}
+
+float* splitk_reserve(Ctx& c, int64_t floats) {
+    if (!c.defer_red) return c.d_splitk;
+    if (c.splitk_used + floats > c.splitk_cap) splitk_flush(c);
+    return c.d_splitk + c.splitk_used;
+}
+
 void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw, int64_t gap_row, int64_t gap) {
+    if (c.defer_red) {   // the slices were written at d_splitk + splitk_used (splitk_reserve)
+        Ctx::RedJob jb{c.d_splitk + c.splitk_used, S, K, N, (K + gap) * N, gap_row, gap, Wg, ldw};
+        c.red_jobs.push_back(jb);
+        c.splitk_used += (int64_t)S * (K + gap) * N;
+        return;
+    }
     const int64_t n4 = K * N / 4;
     pdl_launch(c.stream, k_splitk_reduce, (unsigned)((n4 + 31) / 32), kRedGroups * 32, 0, c.d_splitk, S, K, N, N, (K + gap) * N,
                                                                                    gap_row, gap, Wg, ldw);

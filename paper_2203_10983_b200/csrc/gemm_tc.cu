@@ -555,7 +555,7 @@ void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int6
     S = cdiv(a.nk, a.kb_per_split);
     c.last_splitk = (int)S;
     a.epi = EPI_F32;
-    a.out = c.d_splitk;
+    a.out = splitk_reserve(c, S * K * N);
     a.ldc = N;
     a.split_stride = K * N;
     CUtensorMap ma = make_map(A, K, Mn, lda, KE, f32);
@@ -607,7 +607,7 @@ void gemm_wgrad2_tc(Ctx& c, int64_t Mn0, int64_t Mn1, int64_t K, int64_t N, cons
     S = cdiv(a.nk, a.kb_per_split);
     c.last_splitk = (int)S;
     a.epi = EPI_F32;
-    a.out = c.d_splitk;
+    a.out = splitk_reserve(c, S * M2 * N);
     a.ldc = N;
     a.split_stride = M2 * N;
     CUtensorMap m0 = make_map(A0, K, std::max<int64_t>(Mn0, 1), lda, KE, f32);

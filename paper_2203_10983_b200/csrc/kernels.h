@@ -89,6 +89,11 @@ void gemm_dx(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t ld
 // out[K x N] = sum over S partial slices (fixed order); partial rows [gap_row, gap_row + gap) are skipped padding
 void splitk_reduce(Ctx& c, int S, int64_t K, int64_t N, float* Wg, int64_t ldw, int64_t gap_row = INT64_MAX,
                    int64_t gap = 0);
+// deferred reductions (c.defer_red): the slices of a new job start at c.d_splitk + c.splitk_used; splitk_reserve
+// makes room for `floats` more (flushing the pending jobs first when they would not fit); splitk_flush reduces every
+// pending job in one launch, each in the fixed slice order of k_splitk_reduce (the same bits)
+float* splitk_reserve(Ctx& c, int64_t floats);
+void splitk_flush(Ctx& c);
 
 // tcgen05 bf16 versions (gemm_tc.cu); fwd takes B = W^T stored [N][Kw] with each concat half padded to 64
 void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64_t lda0, const void* A1, int64_t K1,
@@ -112,8 +117,19 @@ void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlog
                  const float* rs = nullptr, void* dps = nullptr, int64_t ldp = -1, int64_t nzero = 0);
 void launch_bce(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlogits, void* dpre_t, const float* rs,
                 void* dps, int64_t ldp = -1, int64_t nzero = 0);
+// a12 folded into the ReLU mask of the layer below (one launch less per layer): mask / pos from k_scatter_prep; the
+// returned rows are in the staged buffer src (row k of the returned rows) or, over peer memory, row pos + delta[j]
+// of peer j's dX (peer[j])
+struct ScatterIn {
+    const uint32_t* mask = nullptr;
+    const int32_t* pos = nullptr;
+    int m = 0;
+    const void* src = nullptr;
+    const void* const* peer = nullptr;
+    const int64_t* delta = nullptr;
+};
 void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre,
-                      const float* rs = nullptr, void* dps = nullptr);
+                      const float* rs = nullptr, void* dps = nullptr, const ScatterIn* sc = nullptr);
 void launch_wpack_all(Ctx& c, float* const* W);
 void launch_sgd(Ctx& c, float* const* W, float* const* G, float lr);
 void launch_adam(Ctx& c, float* const* W, float* const* G, float lr);

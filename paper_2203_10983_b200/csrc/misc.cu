@@ -395,11 +395,13 @@ void launch_xent(Ctx& c, const float* logits, int64_t ld, int32_t C, float* dlog
 // 16-byte vectors: dpre = dh where h > 0 else 0 (bit select on the storage words; R12 ReLU'(0) = 0)
 template <typename T>
 __global__ void k_relu_mask(const T* __restrict__ dh, const T* __restrict__ h, int64_t ld, int64_t n,
-                            T* __restrict__ dpre, const float* __restrict__ rs, T* __restrict__ dps) {
+                            T* __restrict__ dpre, const float* __restrict__ rs, T* __restrict__ dps,
+                            const ScatterIn sc) {
     pdl_grid_sync();
     using R = typename Vec<T>::raw;
     constexpr int VN = Vec<T>::N;
     const int64_t nv = n / VN;
+    const int64_t vpr = ld / VN;   // vectors per row
     const R* dv = reinterpret_cast<const R*>(dh);
     const R* hv = reinterpret_cast<const R*>(h);
     R* ov = reinterpret_cast<R*>(dpre);
@@ -408,6 +410,22 @@ __global__ void k_relu_mask(const T* __restrict__ dh, const T* __restrict__ h, i
     for (; t < nv; t += stride) {
         float a[VN], b[VN];
         Vec<T>::to_float(dv[t], a);
+        if (sc.mask) {   // a12 fused: the peers' returned rows of this owner row, peers ascending, rounded to the
+                         // storage type after every add (R25, R19) -- the values k_scatter_rows / k_scatter_peer store
+            const int64_t r = t / vpr, v = t - r * vpr;
+            uint32_t mm = sc.mask[r];
+            while (mm) {
+                const int j = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const int64_t k = sc.pos[r * sc.m + j];
+                const R* src = sc.peer ? reinterpret_cast<const R*>(static_cast<const T*>(sc.peer[j]) + (k + sc.delta[j]) * ld)
+                                       : reinterpret_cast<const R*>(static_cast<const T*>(sc.src) + k * ld);
+                Vec<T>::to_float(sc.peer ? __ldcg(src + v) : src[v], b);
+#pragma unroll
+                for (int q = 0; q < VN; ++q) a[q] += b[q];
+                Vec<T>::to_float(Vec<T>::from_float(a), a);
+            }
+        }
         Vec<T>::to_float(hv[t], b);
 #pragma unroll
         for (int k = 0; k < VN; ++k) a[k] = (b[k] > 0.f) ? a[k] : 0.f;
@@ -422,16 +440,17 @@ __global__ void k_relu_mask(const T* __restrict__ dh, const T* __restrict__ h, i
 }
 
 void launch_relu_mask(Ctx& c, const void* dh, const void* h, int64_t ld, int64_t rows, int32_t d, void* dpre,
-                      const float* rs, void* dps) {
+                      const float* rs, void* dps, const ScatterIn* sc) {
     const int64_t n = rows * ld;   // ld is a multiple of 8: whole 16-byte vectors
     if (n <= 0) return;
+    const ScatterIn s = sc ? *sc : ScatterIn{};
     unsigned grid = (unsigned)std::min<int64_t>((n / 4 + 255) / 256, 148 * 16);
     if (c.prec == BNS_BF16)
         pdl_launch(c.stream, k_relu_mask<__nv_bfloat16>, grid, 256, 0, (const __nv_bfloat16*)dh, (const __nv_bfloat16*)h, ld,
-                                                               n, (__nv_bfloat16*)dpre, rs, (__nv_bfloat16*)dps);
+                                                               n, (__nv_bfloat16*)dpre, rs, (__nv_bfloat16*)dps, s);
     else
         pdl_launch(c.stream, k_relu_mask<float>, grid, 256, 0, (const float*)dh, (const float*)h, ld, n, (float*)dpre, rs,
-                                                       (float*)dps);
+                                                       (float*)dps, s);
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }

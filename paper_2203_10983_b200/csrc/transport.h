@@ -26,6 +26,9 @@ struct Transport {
     virtual void halo_pull(Ctx&, int /*l*/, void* /*dst_halo*/, int64_t /*din*/) {}
     virtual void* dx_buffer(Ctx& c, int /*l*/);
     virtual void grad_scatter(Ctx&, int /*l*/, int64_t /*din*/) {}
+    // the barrier of grad_scatter alone, the pull folded into the next ReLU-mask kernel: the peers' layer-l dX
+    // pointer table and row deltas (false: not a peer transport)
+    virtual bool grad_barrier(Ctx&, int /*l*/, const void* const** /*peer*/, const int64_t** /*delta*/) { return false; }
     // bns_destroy, before the context frees anything: make sure no peer still reads this rank's shared buffers
     // (peer transports skip the second barrier of the all-reduce, so a slower peer may be in k_sum_ptrs).
     virtual void shutdown(Ctx&) {}
