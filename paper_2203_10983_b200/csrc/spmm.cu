@@ -243,8 +243,12 @@ __device__ __forceinline__ void acc_vec_bf16s(uint64_t* a, const R& v, uint32_t 
 #ifndef BNS_SPMM_MINB1
 #define BNS_SPMM_MINB1 4    // resident 256-thread blocks per SM for 1-vector rows
 #endif
+#ifndef BNS_SPMM_MINB7
+#define BNS_SPMM_MINB7 3    // ... with the bf16 1/p scale (SC 7)
+#endif
 template <typename T, int LPR, int VPL, int SC>
-__global__ void __launch_bounds__(256, (VPL <= 1 && SC == 0) ? BNS_SPMM_MINB1 : (VPL <= 2) ? 3 : (VPL <= 6) ? 2 : 1)
+__global__ void __launch_bounds__(256, (VPL <= 1 && SC == 0) ? BNS_SPMM_MINB1 : (VPL <= 1 && SC == 7) ? BNS_SPMM_MINB7
+                                         : (VPL <= 2) ? 3 : (VPL <= 6) ? 2 : 1)
 k_spmm(const SpmmArgs a) {
     pdl_grid_sync();
     using V = Vec<T>;

@@ -1,5 +1,5 @@
 #!/usr/bin/env bash
-# Round-2 measurement pass on one B200 (gpurun): bench lines (Reddit bf16 / fp32, products bf16 = DRAM-resident
+# Round-2 measurement pass on one B200 (bash scripts/profile_r02.sh <tag>) (gpurun): bench lines (Reddit bf16 / fp32, products bf16 = DRAM-resident
 # gathers), the gather ceilings, single-GPU emulation of the m = 8 job (every rank, ldg2 and random partitions),
 # ncu launch lists (bench and emulation) and ncu --set full captures of the SpMM / GEMM launches.
 set -u
@@ -28,16 +28,14 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python scripts/emulate_rank.py --m 8 --p 0.1 --ranks 0 --partition ldg2 --cache-x0 --no-timing --steps 2 --warmup 1 \
     > /dev/null 2>&1
 python scripts/ncu_summary.py launches "$OUT/emu_launches.csv" "$OUT/emu_launches.txt" > /dev/null
-for part in fwd:8 bwd:12; do
-    name=${part%%:*}; skip=${part##*:}
-    timeout 900 ncu --set full --clock-control none --import-source on -k k_spmm -s "$skip" -c 4 \
-        -o "$OUT/prof_spmm_$name" python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-    python scripts/ncu_summary.py full "$OUT/prof_spmm_$name.ncu-rep" "$OUT/spmm_$name.json" k_spmm > /dev/null
-done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_tc -s 16 -c 6 -o "$OUT/prof_gemm" \
+# the 8 k_spmm launches of one whole epoch (the second): their DRAM bytes are the step's SpMM traffic
+timeout 1200 ncu --set full --clock-control none -k k_spmm -s 8 -c 8 \
+    -o "$OUT/prof_spmm" python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+python scripts/ncu_summary.py full "$OUT/prof_spmm.ncu-rep" "$OUT/spmm.json" k_spmm > /dev/null
+timeout 600 ncu --set full --clock-control none -k regex:k_gemm_tc -s 16 -c 6 -o "$OUT/prof_gemm" \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 python scripts/ncu_summary.py full "$OUT/prof_gemm.ncu-rep" "$OUT/gemm.json" > /dev/null
-timeout 600 ncu --set full --clock-control none -k regex:"k_induce_fused|k_sample_fused|k_segs_fused" -s 3 -c 3 \
+timeout 600 ncu --set full --clock-control none -k regex:"k_induce_count|k_induce_scatter|k_sample_fused|k_segs_fused" -s 4 -c 4 \
     -o "$OUT/prof_induce" python scripts/emulate_rank.py --m 8 --p 0.1 --ranks 0 --partition ldg2 --cache-x0 \
     --steps 2 --warmup 1 > /dev/null 2>&1
 python scripts/ncu_summary.py full "$OUT/prof_induce.ncu-rep" "$OUT/induce.json" > /dev/null
