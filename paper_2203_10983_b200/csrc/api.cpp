@@ -184,6 +184,7 @@ void collect_times(Ctx& c) {
 }
 
 void setup_device(Ctx& c, const float* features, const int32_t* labels) {
+    BNS_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, c.cfg.device));
     Plan& P = c.plan;
     const int m = c.cfg.world;
     BNS_CUDA(cudaSetDevice(c.cfg.device));
@@ -438,7 +439,7 @@ void setup_device(Ctx& c, const float* features, const int32_t* labels) {
         // of an (M2 = 128-padded d_in + d_in) x d_out product per layer (gemm_tc.cu's split rule)
         int64_t tot = 0;
         for (int l = 0; l < L; ++l) {
-            const int64_t K = c.dp[l], N = c.dp[l + 1], M2 = (K + 127) / 128 * 128 + K;
+            const int64_t K = c.dp[l], N = c.dp[l + 1], M2 = (K + 255) / 256 * 256 + K;   // CTA-pair padding
             const int64_t tiles = ((M2 + 127) / 128) * ((N + 255) / 256);
             tot += std::max<int64_t>(1, (148 + tiles - 1) / tiles) * M2 * N;
         }

@@ -257,6 +257,7 @@ struct Ctx {
     struct RedJob {
         const float* part; int S; int64_t M, N, zs, gap_row, gap; float* out; int64_t ldo;
     };
+    int num_sms = 148;             // multiprocessors of cfg.device (persistent grids)
     bool defer_red = false;
     std::vector<RedJob> red_jobs;
     int64_t splitk_used = 0;

@@ -92,6 +92,25 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
         ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// the same box written into the smem of every CTA in ctamask (same offset), complete_tx on each CTA's mbarrier at the
+// same offset
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                               uint16_t ctamask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(ctamask)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);   // version 1, SWIZZLE_128B
@@ -114,12 +133,21 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
+// arrive on the mbarrier at this offset in every CTA of ctamask once the issued MMAs have completed
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t ctamask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"(ctamask) : "memory");
+}
 
 // Persistent, warp-specialized: grid = min(#tiles, #SMs); tile t = (m-tile, n-tile, split) visited in
 // blockIdx-strided order.  warp 0 lane 0: TMA producer over the smem ring; warp 1 lane 0: MMA issuer into one of two
 // TMEM accumulators (2 x 256 columns), so the epilogue of tile i overlaps the MMAs of tile i+1; warps 2-5: epilogue
 // (warp w drains TMEM lanes 32*(w%4) .. +31); fp32 (split-TF32 (4 MMAs)): warps 6-9 split each landed stage into hi / lo.
-template <bool A_MN, bool B_MN, bool F32>
+// MC = 2 (bf16): clusters of two CTAs own consecutive 128-row tiles of the same output columns and split-K range;
+// each CTA loads its own A tile and HALF of the shared B tile, written into both CTAs' shared memory by TMA multicast
+// (B traffic from L2 halved); a stage is refilled only when both CTAs' MMAs have released it (the MMA commit arrives
+// on the empty barrier of both CTAs).
+template <bool A_MN, bool B_MN, bool F32, int MC = 1>
 __global__ void __launch_bounds__(TcCfg<F32>::THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
           const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapB1, const TcArgs args) {
@@ -137,22 +165,26 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = MC == 2 ? cluster_ctarank() : 0u;
     const int64_t tiles_m = (args.M + TC_BM - 1) / TC_BM;
+    const int64_t tiles_mu = (tiles_m + MC - 1) / MC;   // m units: tiles (MC 1) or tile pairs (MC 2)
     const int64_t tiles_n = (args.N + args.BN - 1) / args.BN;
     const int splits = args.kb_per_split > 0 ? (args.nk + args.kb_per_split - 1) / args.kb_per_split : 1;
-    const int64_t tiles = tiles_m * tiles_n * splits;
+    const int64_t tiles = tiles_mu * tiles_n * splits;
+    const int64_t t_first = MC == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+    const int64_t t_step = MC == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
     auto decode = [&](int64_t t, int64_t& m0, int64_t& n0, int& z, int& kb0, int& nk) {
-        z = (int)(t / (tiles_m * tiles_n));
-        const int64_t r = t % (tiles_m * tiles_n);
-        m0 = (r % tiles_m) * TC_BM;
-        n0 = (r / tiles_m) * args.BN;
+        z = (int)(t / (tiles_mu * tiles_n));
+        const int64_t r = t % (tiles_mu * tiles_n);
+        m0 = ((r % tiles_mu) * MC + crank) * TC_BM;   // MC 2: the pair's second tile may lie past M (zero-filled)
+        n0 = (r / tiles_mu) * args.BN;
         kb0 = args.kb_per_split > 0 ? z * args.kb_per_split : 0;
         const int kb1 = args.kb_per_split > 0 ? min(args.nk, kb0 + args.kb_per_split) : args.nk;
         nk = kb1 - kb0;    // >= 1 by construction of the split count
     };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&conv[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&conv[s], 1); mbar_init(&empty[s], MC); }
         for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA0) : "memory");
@@ -166,6 +198,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (MC == 2) cluster_sync_all();   // the peer's barriers are initialised before any multicast reaches them
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // PDL: barrier init, descriptor prefetch and the TMEM allocation above overlap the previous kernel's tail; no
     // global memory is touched before this point
@@ -178,7 +211,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
             // ---------------- TMA producer ----------------
             int s = 0;
             uint32_t ph = 0;
-            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int64_t t = t_first; t < tiles; t += t_step) {
                 int64_t m0, n0;
                 int z, kb0, nk;
                 decode(t, m0, n0, z, kb0, nk);
@@ -205,7 +238,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                     // output rows past msplit also take their B operand from mapB1 (a pair of dW GEMMs with
                     // different A and D in one launch)
                     const CUtensorMap* mb = m0 >= args.msplit ? &mapB1 : &mapB;
-                    if (!B_MN) {
+                    if (MC == 2) {   // this CTA's half of B, multicast into both CTAs of the pair
+                        if (!B_MN) {   // box {KE (k), BN / 2 (n)}
+                            const int hb = args.BN >> 1;
+                            tma_load_2d_mc(mb, &full[s], sb + crank * hb * TC_ROW_BYTES, kb * KE, (int)n0 + (int)crank * hb,
+                                           (uint16_t)3);
+                        } else {
+                            for (int j = (int)crank; j < args.BN / MNE; j += 2)
+                                tma_load_2d_mc(mb, &full[s], sb + j * BOX_BYTES, (int)n0 + MNE * j, kb * KE, (uint16_t)3);
+                        }
+                    } else if (!B_MN) {
                         tma_load_2d(mb, &full[s], sb, kb * KE, (int)n0);              // box {KE (k), BN (n)}
                     } else {
                         for (int j = 0; j < args.BN / MNE; ++j)                        // boxes {MNE (n), KE (k)}
@@ -226,7 +268,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
-            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            for (int64_t t = t_first; t < tiles; t += t_step, ++it) {
                 int64_t m0, n0;
                 int z, kb0, nk;
                 decode(t, m0, n0, z, kb0, nk);
@@ -260,7 +302,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
                             umma_tf32(d + 128, ad + lo, bd + lo, idesc, 1u);
                         }
                     }
-                    umma_commit(&empty[s]);     // stage free once these MMAs have read it
+                    if (MC == 2) umma_commit_mc(&empty[s], (uint16_t)3);   // both CTAs' stage s: B came from both
+                    else umma_commit(&empty[s]);     // stage free once these MMAs have read it
                     if (++s == STAGES) { s = 0; ph ^= 1u; }
                 }
                 umma_commit(&tfull[b]);         // accumulator b complete
@@ -273,7 +316,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
         const int ct = threadIdx.x - 192;
         int s = 0;
         uint32_t ph = 0;
-        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int64_t t = t_first; t < tiles; t += t_step) {
             int64_t m0, n0;
             int z, kb0, nk;
             decode(t, m0, n0, z, kb0, nk);
@@ -304,7 +347,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
         // ---------------- epilogue: TMEM -> registers -> global (warps 2..5) ----------------
         const int q = warp & 3;                 // TMEM lane quarter this warp may access
         int it = 0;
-        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        for (int64_t t = t_first; t < tiles; t += t_step, ++it) {
             int64_t m0, n0;
             int z, kb0, nk;
             decode(t, m0, n0, z, kb0, nk);
@@ -367,6 +410,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUt
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (MC == 2) cluster_sync_all();   // no multicast write or commit arrival is still headed for either CTA
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
@@ -408,26 +452,61 @@ static CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int6
     return m;
 }
 
-template <bool A_MN, bool B_MN, bool F32>
+template <bool A_MN, bool B_MN, bool F32, int MC>
 static void launch_tc_t(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
                         const CUtensorMap& b1, const TcArgs& args, dim3 grid) {
     using Cfg = TcCfg<F32>;
+    auto kern = k_gemm_tc<A_MN, B_MN, F32, MC>;
     static bool configured = false;
     if (!configured) {
-        BNS_CUDA(cudaFuncSetAttribute(k_gemm_tc<A_MN, B_MN, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Cfg::SMEM));
+        BNS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
         configured = true;
     }
-    pdl_launch(c.stream, k_gemm_tc<A_MN, B_MN, F32>, grid, Cfg::THREADS, Cfg::SMEM, a0, a1, b, b1, args);
+    if (MC == 1) {
+        pdl_launch(c.stream, kern, grid, Cfg::THREADS, Cfg::SMEM, a0, a1, b, b1, args);
+    } else {   // CTA pairs: cluster dimension 2 (+ PDL as every other launch)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(Cfg::THREADS);
+        cfg.dynamicSmemBytes = Cfg::SMEM;
+        cfg.stream = c.stream;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = (!pdl_take_hold() && pdl_enabled()) ? 2 : 1;
+        BNS_CUDA(cudaLaunchKernelEx(&cfg, kern, a0, a1, b, b1, args));
+    }
     c.kernels += 1;
     BNS_CHECK_LAUNCH();
 }
 
 template <bool A_MN, bool B_MN>
 static void launch_tc(Ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const TcArgs& args,
-                      dim3 grid, const CUtensorMap* b1 = nullptr) {
-    if (c.prec == BNS_FP32) launch_tc_t<A_MN, B_MN, true>(c, a0, a1, b, b1 ? *b1 : b, args, grid);
-    else launch_tc_t<A_MN, B_MN, false>(c, a0, a1, b, b1 ? *b1 : b, args, grid);
+                      dim3 grid, const CUtensorMap* b1 = nullptr, int mc = 1) {
+    if (c.prec == BNS_FP32) launch_tc_t<A_MN, B_MN, true, 1>(c, a0, a1, b, b1 ? *b1 : b, args, grid);
+    else if (mc == 2) launch_tc_t<A_MN, B_MN, false, 2>(c, a0, a1, b, b1 ? *b1 : b, args, grid);
+    else launch_tc_t<A_MN, B_MN, false, 1>(c, a0, a1, b, b1 ? *b1 : b, args, grid);
+}
+
+// bf16 GEMMs run as CTA pairs sharing the B operand when the node dimension is large (`rows`: the output rows of the
+// forward / dX GEMMs, the reduction length of dW) and the shared operand is wide (`width`: the reduction length K of
+// the forward / dX GEMMs, the output rows of dW).  Measured (A/B in one run): Yelp m = 1 (717 K rows, K = 1024)
+// GEMMs 8.69 -> 8.40 ms; Reddit m = 1 (233 K) unchanged; products m = 1 (2.4 M rows, K <= 256) 3.28 -> 4.06 ms;
+// the m = 8 rank (32-50 K rows) 0.270 -> 0.278 ms backward.  BNS_GEMM_MC = 0: never, 2: always (M > 128).
+static int gemm_mc(const Ctx& c, int64_t M, int64_t rows, int64_t width) {
+    const char* e = std::getenv("BNS_GEMM_MC");   // read per call: tests switch it
+    const int env = e ? std::atoi(e) : 1;
+    if (env == 0 || c.prec == BNS_FP32 || M <= 128) return 1;
+    return (env == 2 || (rows >= (1ll << 18) && width >= 512)) ? 2 : 1;
+}
+// persistent grid of CTA pairs over tile pairs
+static dim3 pair_grid(const Ctx& c, int64_t pairs) {
+    return dim3((unsigned)(2 * std::max<int64_t>(1, std::min<int64_t>(pairs, c.num_sms / 2))));
 }
 
 static inline bool is_f32(const Ctx& c) { return c.prec == BNS_FP32; }
@@ -462,10 +541,14 @@ void gemm_fwd_tc(Ctx& c, int64_t M, int64_t N, const void* A0, int64_t K0, int64
     a.relu = relu ? 1 : 0;
     a.out = C;
     a.ldc = ldc;
+    const int mc = gemm_mc(c, M, M, K0 + K1);
     CUtensorMap m0 = make_map(A0, K0, M, lda0, TC_BM, f32);
     CUtensorMap m1 = A1 ? make_map(A1, K1, M, lda1, TC_BM, f32) : m0;
-    CUtensorMap mb = make_map(WT, Kw, N, Kw, a.BN, f32);
-    launch_tc<false, false>(c, m0, m1, mb, a, persistent_grid(cdiv(M, TC_BM) * cdiv(N, a.BN)));
+    CUtensorMap mb = make_map(WT, Kw, N, Kw, a.BN / mc, f32);   // MC 2: each CTA of a pair loads half of B
+    launch_tc<false, false>(c, m0, m1, mb, a,
+                            mc == 2 ? pair_grid(c, cdiv(cdiv(M, TC_BM), 2) * cdiv(N, a.BN))
+                                    : persistent_grid(cdiv(M, TC_BM) * cdiv(N, a.BN)),
+                            nullptr, mc);
 }
 
 // fp32 weight gradient: out^T operands.  dst[c][r] = src[r][c] for r < rows (the node dimension), c < cols;
@@ -560,7 +643,11 @@ void gemm_wgrad_tc(Ctx& c, int64_t Mn, int64_t K, int64_t N, const void* A, int6
     a.split_stride = K * N;
     CUtensorMap ma = make_map(A, K, Mn, lda, KE, f32);
     CUtensorMap mb = make_map(D, N, Mn, ldd, KE, f32);
-    launch_tc<true, true>(c, ma, ma, mb, a, persistent_grid(cdiv(K, TC_BM) * cdiv(N, a.BN) * S));
+    const int mc = gemm_mc(c, K, Mn, K);
+    launch_tc<true, true>(c, ma, ma, mb, a,
+                          mc == 2 ? pair_grid(c, cdiv(cdiv(K, TC_BM), 2) * cdiv(N, a.BN) * S)
+                                  : persistent_grid(cdiv(K, TC_BM) * cdiv(N, a.BN) * S),
+                          nullptr, mc);
     splitk_reduce(c, (int)S, K, N, Wg, ldw);
 }
 
@@ -580,7 +667,11 @@ void gemm_wgrad2_tc(Ctx& c, int64_t Mn0, int64_t Mn1, int64_t K, int64_t N, cons
         return;
     }
     const int KE = k_elems(c);
-    const int64_t Kp = cdiv(K, TC_BM) * TC_BM, M2 = Kp + K;
+    // the second product starts on a tile boundary -- a tile-PAIR boundary for CTA pairs, whose two tiles must read
+    // the same B operand
+    // (no pairs where the pair boundary would add a padding tile)
+    const int mc = ((K + TC_BM - 1) / TC_BM) % 2 == 0 ? gemm_mc(c, 2 * K, std::max(Mn0, Mn1), 2 * K) : 1;
+    const int64_t Kp = cdiv(K, TC_BM * mc) * TC_BM * mc, M2 = Kp + K;
     const int64_t Mn = std::max(Mn0, Mn1);
     if (Mn <= 0) {
         BNS_CUDA_HOLD(cudaMemset2DAsync(Wg, ldw * sizeof(float), 0, N * sizeof(float), 2 * K, c.stream));
@@ -614,7 +705,9 @@ void gemm_wgrad2_tc(Ctx& c, int64_t Mn0, int64_t Mn1, int64_t K, int64_t N, cons
     CUtensorMap m1 = make_map(A1, K, std::max<int64_t>(Mn1, 1), lda, KE, f32);
     CUtensorMap mb0 = make_map(D0, N, std::max<int64_t>(Mn0, 1), ldd0, KE, f32);
     CUtensorMap mb1 = make_map(D1, N, std::max<int64_t>(Mn1, 1), ldd1, KE, f32);
-    launch_tc<true, true>(c, m0, m1, mb0, a, persistent_grid(tiles * S), &mb1);
+    launch_tc<true, true>(c, m0, m1, mb0, a,
+                          mc == 2 ? pair_grid(c, cdiv(cdiv(M2, TC_BM), 2) * cdiv(N, a.BN) * S) : persistent_grid(tiles * S),
+                          &mb1, mc);
     splitk_reduce(c, (int)S, 2 * K, N, Wg, ldw, K, Kp - K);
 }
 
@@ -634,9 +727,13 @@ void gemm_dx_tc(Ctx& c, int64_t M, int64_t Nc, int64_t K, const void* D, int64_t
     a.ldc = ldc;
     a.rowscale = rowscale;
     a.scale_cols = scale_cols;
+    const int mc = gemm_mc(c, M, M, K);
     CUtensorMap ma = make_map(D, K, M, ldd, TC_BM, f32);
-    CUtensorMap mb = make_map(B, K, Nc, ldb, a.BN, f32);
-    launch_tc<false, false>(c, ma, ma, mb, a, persistent_grid(cdiv(M, TC_BM) * cdiv(Nc, a.BN)));
+    CUtensorMap mb = make_map(B, K, Nc, ldb, a.BN / mc, f32);
+    launch_tc<false, false>(c, ma, ma, mb, a,
+                            mc == 2 ? pair_grid(c, cdiv(cdiv(M, TC_BM), 2) * cdiv(Nc, a.BN))
+                                    : persistent_grid(cdiv(M, TC_BM) * cdiv(Nc, a.BN)),
+                            nullptr, mc);
 }
 
 }  // namespace bns

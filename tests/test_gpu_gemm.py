@@ -11,7 +11,8 @@ accumulation error alone:
 
 Shapes are the bench's (Reddit-shaped, m = 1: M = 232,965 stacked rows, a ragged last 128-row tile; widths 608 /
 512 / 256 / 48 padded) and the weight-gradient GEMMs run with the split-K factor the epoch uses (>= 32 slices on the
-256-wide layers).
+256-wide layers).  The bf16 GEMMs run both as single CTAs and as CTA pairs sharing the B operand by TMA multicast
+(BNS_GEMM_MC=2; by default pairs are used from 256 K rows).
 """
 import numpy as np
 import pytest
@@ -70,7 +71,9 @@ def wt_pad(W, halves):
     (256, 256, True, False, True),
     (256, 96, False, False, False),    # layer 4 transform-first, 48-wide halves
 ])
-def test_forward(K, N, concat, relu, out_f32):
+@pytest.mark.parametrize("mc", ["1", "2"])
+def test_forward(K, N, concat, relu, out_f32, mc, monkeypatch):
+    monkeypatch.setenv("BNS_GEMM_MC", mc)   # 2: CTA pairs sharing B by TMA multicast
     g = torch.Generator().manual_seed(K * 7 + N)
     M = M_FULL
     A0 = act(M, K, g)
@@ -96,7 +99,9 @@ def test_forward(K, N, concat, relu, out_f32):
     (29_121, 256, 256, 4),    # an m = 8 partition
     (1000, 64, 16, 1),        # tiny: a single split, ragged K block
 ])
-def test_wgrad(M, K, N, min_splits):
+@pytest.mark.parametrize("mc", ["1", "2"])
+def test_wgrad(M, K, N, min_splits, mc, monkeypatch):
+    monkeypatch.setenv("BNS_GEMM_MC", mc)   # 2: CTA pairs sharing B by TMA multicast
     g = torch.Generator().manual_seed(M + K + N)
     A = act(M, K, g)
     D = sgn(M, N, g, 1e-3)
@@ -109,7 +114,9 @@ def test_wgrad(M, K, N, min_splits):
 
 
 @pytest.mark.parametrize("M,K,N", [(M_FULL, 256, 256), (M_FULL, 128, 48), (5000, 128, 128)])
-def test_wgrad_merged(M, K, N):
+@pytest.mark.parametrize("mc", ["1", "2"])
+def test_wgrad_merged(M, K, N, mc, monkeypatch):
+    monkeypatch.setenv("BNS_GEMM_MC", mc)   # 2: CTA pairs sharing B by TMA multicast
     """GraphSAGE [dW_z ; dW_h] = [Z | H]^T dPre in one launch + one split-K reduce"""
     g = torch.Generator().manual_seed(3 * M + K)
     Z = sgn(M, K, g)
@@ -126,7 +133,9 @@ def test_wgrad_merged(M, K, N):
 
 @pytest.mark.parametrize("M,K,N,scale_cols", [(M_FULL, 256, 512, 256), (M_FULL, 48, 512, 0), (M_FULL, 256, 256, 256),
                                               (777, 48, 96, 48)])
-def test_dx(M, K, N, scale_cols):
+@pytest.mark.parametrize("mc", ["1", "2"])
+def test_dx(M, K, N, scale_cols, mc, monkeypatch):
+    monkeypatch.setenv("BNS_GEMM_MC", mc)   # 2: CTA pairs sharing B by TMA multicast
     """[dZ' | dX_self] = dPre W^T with the 1/deg_G row scale on the dZ' half (SAGE), or dY-side products"""
     g = torch.Generator().manual_seed(M * 5 + N)
     D = sgn(M, K, g, 1e-3)
