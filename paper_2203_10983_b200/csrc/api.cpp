@@ -572,7 +572,8 @@ void draw_finish(Ctx& c, uint64_t epoch, bool sync) {
     const int64_t* tot = sp + 2 * m + 1;
     if (c.fwd_mode == 0) { c.nnz_kept = c.nnz_i; c.n_seg_fwd = c.n_seg_static_fwd; c.n_split_fwd = c.n_split_sf; }
     else if (c.fwd_mode == 1) { c.nnz_kept = c.ii_nnz; c.n_seg_fwd = c.n_seg_bwd_inner; c.n_split_fwd = c.n_split_bwd_inner; }
-    else { c.nnz_kept = tot[0]; c.n_seg_fwd = tot[1]; c.n_split_fwd = tot[4]; }
+    else { c.nnz_kept = tot[0]; c.n_seg_fwd = tot[1] + (edges ? 0 : tot[5]); c.n_split_fwd = tot[4]; }
+    c.fwd_hub_n = (c.fwd_mode == 2 && !edges) ? tot[5] : 0;   // hub segments of the per-epoch forward list (LPT)
     if (edges) {
         c.n_seg_bwd = tot[6];
         c.n_split_bwd = tot[7];
@@ -671,6 +672,10 @@ void epoch(Ctx& c, float* const* W_in, float lr, float* const* G_in, double* los
     ev.bcol = ebw ? c.d_ind_tcol : c.d_tcol;
     ev.bsplit = ebw ? c.d_esplit_bwd : c.d_split_bwd;
     ev.inv_p = inv_p;
+    if (c.fwd_mode == 2 && c.fwd_hub_n > 0) {   // the per-epoch forward list: hub segments at its end, claimed first
+        ev.fhub_n = c.fwd_hub_n;
+        ev.fhub_base = c.seg_fwd_cap - c.fwd_hub_n;
+    }
     const int32_t* S_local = c.d_cand_out + c.n_halo;
     const bool dropout = c.drop > 0.0;
     if (dropout) launch_halo_gid(c);

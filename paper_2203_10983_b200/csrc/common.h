@@ -1,6 +1,7 @@
 // common.h -- internal declarations shared by the libbns translation units (host side).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 #include <stdexcept>
@@ -195,6 +196,7 @@ struct Ctx {
     int64_t* d_split_bwd = nullptr; int64_t n_split_bwd_inner = 0; // [static inner part ; per-epoch halo part]
     int64_t* d_split_fwd = nullptr;                                  // per-epoch induced forward segments
     int64_t n_split_fwd = 0, n_split_bwd = 0;                        // this epoch's list lengths
+    int64_t fwd_hub_n = 0;          // per-epoch forward list: hub-row segments at [seg_fwd_cap - fwd_hub_n, seg_fwd_cap)
     float* d_cscale = nullptr;     // per-column scale (GCN forward)
     float* d_gat = nullptr;          // f4 / R45 GAT scalars: per layer el, er (stacked rows) and softmax max / 1/Σ
                                      // (inner rows), then c, selfds, del (inner), der (stacked)
@@ -277,6 +279,13 @@ struct Ctx {
     int64_t n_train_global = 0;
     int64_t n_train_local = 0;
 };
+
+// the per-epoch forward segment list puts the hub rows' segments first in claim order (not for GAT, whose weight
+// kernels walk the list front to back); BNS_SPMM_LPT=0 keeps plain row order (A/B)
+inline bool fwd_lpt(const Ctx& c) {
+    const char* e = std::getenv("BNS_SPMM_LPT");
+    return c.layer != BNS_LAYER_GAT && !(e && e[0] == '0');
+}
 
 // kernel launchers (kernels.cu / gemm.cu)
 struct Launch;

@@ -293,7 +293,9 @@ struct SegArgs {
     // backward chain: halo slots -> their boundary rows (transposed arcs after the static A_II part)
     const int64_t* seg_pos; int m; const int32_t* U_b; const int64_t* br_ptr; int64_t cap; int64_t seg_base;
     int64_t e_base; Seg* bsegs; int64_t* bsplit; int64_t ntiles_b;
-    int64_t* tot;                       // [1] fwd segments, [2] bwd halo segments, [3] bwd splits, [4] fwd splits
+    int64_t* tot;                       // [1] fwd segments, [2] bwd halo segments, [3] bwd splits, [4] fwd splits,
+                                        // [5] fwd hub segments (lpt)
+    int64_t fcap; int lpt;              // lpt: forward hub rows' segments from the end of the list (fcap) down
     int32_t seg_long;
     uint64_t* state_f; uint64_t* state_b; unsigned* ctr_f; unsigned* ctr_b; uint32_t gen;
 };
@@ -325,10 +327,15 @@ __global__ void __launch_bounds__(kTile) k_segs_fused(const SegArgs a) {
             row = (int32_t)(a.n_in + r);
         }
     }
-    const int ex = block_excl_scan(ns, s_warp, &s_total);
+    // lpt (forward): a row of several segments (a hub) takes its block from the end of the list by an atomic, the
+    // single-segment rows are scanned into the front -- the SpMM claims the hub segments first (longest first)
+    const bool hub = a.lpt && fwd && ns > 1;
+    const int ex = block_excl_scan(hub ? 0 : ns, s_warp, &s_total);
     const int64_t excl = lookback(fwd ? a.state_f : a.state_b, a.gen, t, s_total, &s_excl);
     if (ns > 0) {
-        const int64_t s0 = (fwd ? 0 : a.seg_base) + excl + ex;
+        const int64_t s0 = hub ? a.fcap - (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(a.tot + 5),
+                                                             (unsigned long long)ns) - ns
+                               : (fwd ? 0 : a.seg_base) + excl + ex;
         Seg* out = fwd ? a.fsegs : a.bsegs;
         if (ns > 1) {
             int64_t* cnt = fwd ? a.tot + 4 : a.tot + 3;
@@ -366,7 +373,7 @@ void launch_sample_fused(Ctx& c, uint64_t T, uint64_t seed, uint64_t epoch) {
     a.cand_seg = c.d_cand_seg; a.nseg = 2 * m + 1;
     a.flags = c.d_flags; a.bkeep = c.d_bkeep; a.out = c.d_cand_out; a.slot_of_b = c.d_slot_of_b;
     a.seg_pos = c.d_seg_pos;
-    a.zero = tot + 3; a.nzero = 2;
+    a.zero = tot + 3; a.nzero = 3;   // split counters [3], [4] and the forward hub count [5]
     a.state = c.d_lb_state; a.ctr = c.d_lb_ctr; a.gen = ++c.lb_gen; a.ntiles = nt;
     pdl_launch(c.stream, k_sample_fused, (unsigned)nt, kTile, 0, a);
     c.kernels += 1;
@@ -418,6 +425,7 @@ void launch_segments_fused(Ctx& c, bool fwd) {
     a.bsplit = c.d_split_bwd + c.n_split_bwd_inner;
     a.ntiles_b = (c.plan.n_bd + kTile - 1) / kTile;
     a.tot = tot; a.seg_long = c.seg_long;
+    a.fcap = c.seg_fwd_cap; a.lpt = fwd_lpt(c) ? 1 : 0;
     a.state_f = c.d_lb_state + c.lb_off_segf; a.state_b = c.d_lb_state + c.lb_off_segb;
     a.ctr_f = c.d_lb_ctr + 2; a.ctr_b = c.d_lb_ctr + 3; a.gen = ++c.lb_gen;
     if (a.ntiles_b == 0) BNS_CUDA_HOLD(cudaMemsetAsync(tot + 2, 0, sizeof(int64_t), c.stream));

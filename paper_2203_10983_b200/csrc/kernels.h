@@ -47,6 +47,8 @@ struct SpmmArgs {
     unsigned long long* work = nullptr;   // dynamic segment scheduling: [next unclaimed segment, warps done]; the
                                           // last warp to finish resets both (no memset between launches)
     int32_t* arrive = nullptr;            // non-null: split rows are summed by the warp finishing their last segment
+    int64_t hub_n = 0, hub_base = 0;      // the first hub_n claims are segments hub_base.. (the hub rows' segments,
+                                          // stored at the end of the list), then segments 0..
     int chunk = 1;                        // segments per claim
     // f4 / R45 GAT: per-node attention scores and softmax statistics (fp32), attention vectors a_l / a_r (dout),
     // del / der (backward)

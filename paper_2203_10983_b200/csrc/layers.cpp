@@ -111,6 +111,8 @@ void forward_layer_tf(Ctx& c, const EpochView& v, int l, void* Hin) {
     SpmmArgs a{};
     a.mode = SAGE_FWD_TF;
     a.segs = v.fsegs;
+    a.hub_n = v.fhub_n;
+    a.hub_base = v.fhub_base;
     a.n_segs = c.n_seg_fwd;
     a.col = v.fcol;
     a.src = c.d_tfy;
@@ -145,6 +147,8 @@ void forward_layer_std(Ctx& c, const EpochView& v, int l, void* Hin) {
         SpmmArgs a{};
         a.mode = sage ? SAGE_FWD : GCN_FWD;
         a.segs = v.fsegs;
+        a.hub_n = v.fhub_n;
+        a.hub_base = v.fhub_base;
         a.n_segs = c.n_seg_fwd;
         a.col = v.fcol;
         a.src = Hin;

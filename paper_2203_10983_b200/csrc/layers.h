@@ -28,6 +28,7 @@ struct PhaseTimer {
 // ones, and the halo column scale c_u = 1/p (1 without halo)
 struct EpochView {
     const Seg* fsegs; const int32_t* fcol; const int64_t* fsplit;
+    int64_t fhub_n = 0, fhub_base = 0;   // forward list: hub segments first (SpmmArgs::hub_n)
     const Seg* bsegs; const int32_t* bcol; const int64_t* bsplit;
     float inv_p;
 };

@@ -281,7 +281,10 @@ k_spmm(const SpmmArgs a) {
         return (int64_t)__shfl_sync(0xffffffffu, v, 0);
     };
     for (int64_t c0 = a.work ? claim() : warp; c0 < a.n_segs; c0 = a.work ? claim() : c0 + nwarps)
-    for (int64_t sid = c0; sid < c0 + chunk && sid < a.n_segs; ++sid) {
+    for (int64_t vid = c0; vid < c0 + chunk && vid < a.n_segs; ++vid) {
+        // claim order: the hub rows' segments first (placed at the end of the list, longest work first), then the
+        // single-segment rows
+        const int64_t sid = vid < a.hub_n ? a.hub_base + vid : vid - a.hub_n;
         const Seg s = a.segs[sid];
         uint64_t acc2[VPL][VN / 2];
 #pragma unroll
@@ -451,7 +454,8 @@ __global__ void __launch_bounds__(256, 3) k_spmm_g4(const __grid_constant__ CUte
         return (int64_t)__shfl_sync(0xffffffffu, v, 0);
     };
     for (int64_t c0 = claim(); c0 < a.n_segs; c0 = claim())
-    for (int64_t sid = c0; sid < c0 + a.chunk && sid < a.n_segs; ++sid) {
+    for (int64_t vid = c0; vid < c0 + a.chunk && vid < a.n_segs; ++vid) {
+        const int64_t sid = vid < a.hub_n ? a.hub_base + vid : vid - a.hub_n;
         const Seg s = a.segs[sid];
         const int64_t ng = (s.e1 - s.e0 + 3) / 4;
         uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
